@@ -1,0 +1,180 @@
+/*
+ * oracle/lowprec.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU implementation of the first part of the
+ * hybrid factorization of Suzuki (arXiv 2208.01907).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  It shares no code with the CUDA path
+ * (paper_2208_01907_b200/csrc) and includes no header of it.
+ *
+ * Citations: P:n = PAPER.md line n (LaTeX source of the paper).
+ * Readings of silent/ambiguous passages are listed in DESIGN.md section 3 and
+ * referred to here as [Rn].
+ *
+ * Functions
+ *   oracle_scale          P:40 (sec. 2 opening): K = Q Kbar Q, diag(K) in {-1,0,1}.
+ *   oracle_factor_f32     P:64-67 (sec. 2.1) symmetric max-|diag| pivoting with
+ *                         rank-1 Schur update, P:72-75 (sec. 2.2) threshold
+ *                         postponing, P:82-83 enlargement, in FP32 (the lower
+ *                         precision of Alg. 1 step 1).
+ *   oracle_factor_f64     the same algorithm in FP64 (used by the planted-count
+ *                         pin of the tests and by the (double, double-double)
+ *                         pair of sec. 4.3).
+ *
+ * Arithmetic is IEEE round-to-nearest, no contraction (compiled with
+ * -ffp-contract=off); every FMA is an explicit fmaf/fma call.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* "scaled so that diagonal entries take one of -1, 0 and 1, ...        */
+/* [Q]_ii = 1/sqrt([Kbar]_ii) when [Kbar]_ii != 0, otherwise [Q]_ii = 1 ...   */
+/* Q Kbar Q = K".  Only the lower triangle (i >= j) of Kbar is read [R1].     */
+/* Kbar, K: column-major L x L with leading dimension ld (may alias).         */
+/* K is written as a full symmetric matrix.  Returns 0.                      */
+/* ------------------------------------------------------------------------- */
+int oracle_scale(int64_t L, const double *Kbar, int64_t ld, double *K, double *q)
+{
+    for (int64_t i = 0; i < L; ++i) {
+        double d = Kbar[i + i * ld];
+        q[i] = (d != 0.0) ? 1.0 / sqrt(fabs(d)) : 1.0;
+    }
+    for (int64_t j = 0; j < L; ++j) {
+        for (int64_t i = j + 1; i < L; ++i) {
+            double v = (q[i] * Kbar[i + j * ld]) * q[j];
+            K[i + j * ld] = v;
+            K[j + i * ld] = v;
+        }
+    }
+    for (int64_t i = 0; i < L; ++i) {
+        double d = Kbar[i + i * ld];
+        K[i + i * ld] = (d > 0.0) ? 1.0 : ((d < 0.0) ? -1.0 : 0.0);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Stage 1 (Alg. 1 step 1): LDL^T with symmetric pivoting and         */
+/* threshold postponing.  Written once as a macro body for the two scalar    */
+/* types so the FP64 variant is the same algorithm letter for letter.        */
+/*                                                                           */
+/* Storage: A is a full L x L column-major array of which only the lower     */
+/* triangle (row >= col) in POSITION space is used.  The paper's step         */
+/* (P:65-67): find k0 = argmax |diag| of the trailing block, swap rows and   */
+/* columns k and k0 (physically), then the rank-1 update                      */
+/*   S'_22 = K~'_22 - [K~_22]_{down 1} d^{-1} [K~_22]_{1 right}.              */
+/* The update is evaluated in the role-symmetric form [R7, R8]               */
+/*   s_i = c_i / sqrt|d|, sigma = sign d,  v_ij <- fma(-sigma*s_i, s_j, v_ij) */
+/* which is the same rank-1 update (c_i c_j / d = sigma s_i s_j) with one    */
+/* correctly rounded FMA per pivot per entry.                                */
+/*                                                                           */
+/* Outputs:                                                                  */
+/*   perm[L]   : perm[k] = original index of the k-th pivot for k < N,       */
+/*               then Lambda_2 in ascending original index [R10]             */
+/*   Dk[L]     : pivot values d_k for k < N_tau (first N are D)              */
+/*   Lfac      : L x L column-major (ld = L); column k < N holds the unit-   */
+/*               lower factor column in pivot (position) order:              */
+/*               Lfac[i + k L] = c_i / d_k for k < i < N, 1 on the diagonal,  */
+/*               0 above.  Only the leading N x N block is meaningful.       */
+/*   out[0]=N, out[1]=N_tau (pure tau-rule count, no floor, no enlargement)  */
+/* Returns 0, or -1 on bad arguments / allocation failure.                   */
+/* ------------------------------------------------------------------------- */
+#define ORACLE_FACTOR_BODY(T, FMA, SQRT, FABS)                                  \
+    if (L < 0 || !(tau > 0.0 && tau < 1.0) || n_min < 0 || n_extra < 0)       \
+        return -1;                                                            \
+    T *A = (T *)malloc((size_t)(L > 0 ? L : 1) * (size_t)(L > 0 ? L : 1) * sizeof(T)); \
+    T *s = (T *)malloc((size_t)(L > 0 ? L : 1) * sizeof(T));                  \
+    int64_t *orig = (int64_t *)malloc((size_t)(L > 0 ? L : 1) * sizeof(int64_t)); \
+    if (!A || !s || !orig) { free(A); free(s); free(orig); return -1; }       \
+    /* [R2] lower-precision start values, rounded once from the FP64 K */     \
+    for (int64_t j = 0; j < L; ++j)                                           \
+        for (int64_t i = j; i < L; ++i)                                       \
+            A[i + j * L] = (T)K[i + j * ld];                                  \
+    for (int64_t p = 0; p < L; ++p) orig[p] = p;                              \
+    int64_t Ntau = L;                                                         \
+    for (int64_t k = 0; k < L; ++k) {                                         \
+        /* [R3] P:65 max |diag|, ties -> smallest original index */           \
+        int64_t best = k;                                                     \
+        for (int64_t p = k + 1; p < L; ++p) {                                 \
+            T a = FABS(A[p + p * L]), b = FABS(A[best + best * L]);           \
+            if (a > b || (a == b && orig[p] < orig[best])) best = p;          \
+        }                                                                     \
+        T d = A[best + best * L];                                             \
+        /* [R4] P:73 |K_{i+1,i+1}/K_{ii}| < tau -> stop (ratio in FP64) */    \
+        if (k == 0 && d == (T)0) { Ntau = 0; break; }                         \
+        if (k > 0 && fabs((double)d) < tau * fabs((double)Dk[k - 1])) {      \
+            Ntau = k; break;                                                  \
+        }                                                                     \
+        /* P:66 "rows and columns ... k+1 and k0 are exchanged" */            \
+        if (best != k) {                                                      \
+            int64_t p = best; T t;                                            \
+            for (int64_t j = 0; j < k; ++j) {          /* rows of L part */   \
+                t = A[k + j * L]; A[k + j * L] = A[p + j * L]; A[p + j * L] = t; \
+            }                                                                 \
+            t = A[k + k * L]; A[k + k * L] = A[p + p * L]; A[p + p * L] = t;  \
+            for (int64_t i = k + 1; i < p; ++i) {      /* col k <-> row p */  \
+                t = A[i + k * L]; A[i + k * L] = A[p + i * L]; A[p + i * L] = t; \
+            }                                                                 \
+            for (int64_t i = p + 1; i < L; ++i) {      /* below p */          \
+                t = A[i + k * L]; A[i + k * L] = A[i + p * L]; A[i + p * L] = t; \
+            }                                                                 \
+            int64_t o = orig[k]; orig[k] = orig[p]; orig[p] = o;              \
+        }                                                                     \
+        Dk[k] = d;                                                            \
+        /* [R7] r = sqrt|d|, sigma = sign d, s_i = c_i / r (IEEE division) */ \
+        T r = SQRT(FABS(d));                                                  \
+        T sg = (d > (T)0) ? (T)1 : (T)-1;                                     \
+        for (int64_t i = k + 1; i < L; ++i) {                                 \
+            T c = A[i + k * L];                                               \
+            s[i] = c / r;                                                     \
+            A[i + k * L] = c / d;                 /* [R10] L_ik = c_i / d */  \
+        }                                                                     \
+        /* [R8] P:67 rank-1 Schur update of the trailing lower triangle */    \
+        _Pragma("omp parallel for schedule(dynamic, 16)")                     \
+        for (int64_t j = k + 1; j < L; ++j) {                                 \
+            T nsj = -sg * s[j];                                               \
+            T *col = A + j * L;                                               \
+            for (int64_t i = j; i < L; ++i)                                   \
+                col[i] = FMA(nsj, s[i], col[i]);                              \
+        }                                                                     \
+    }                                                                         \
+    /* [R5] floor, [R9] P:82 enlargement by moving the last accepted pivots */ \
+    int64_t N = Ntau;                                                         \
+    if (L - n_min < N) N = (L - n_min > 0) ? L - n_min : 0;                   \
+    if (N < L) N = (N - n_extra > 0) ? N - n_extra : 0;                       \
+    /* [R10] Pi = [pivots, Lambda_2 ascending] */                             \
+    for (int64_t p = 0; p < N; ++p) perm[p] = orig[p];                        \
+    {                                                                         \
+        char *used = (char *)calloc((size_t)(L > 0 ? L : 1), 1);              \
+        if (!used) { free(A); free(s); free(orig); return -1; }               \
+        for (int64_t p = 0; p < N; ++p) used[orig[p]] = 1;                    \
+        int64_t w = N;                                                        \
+        for (int64_t i = 0; i < L; ++i) if (!used[i]) perm[w++] = i;          \
+        free(used);                                                           \
+    }                                                                         \
+    for (int64_t j = 0; j < L; ++j)                                           \
+        for (int64_t i = 0; i < L; ++i) {                                     \
+            T v = (T)0;                                                       \
+            if (j < N && i < N) v = (i == j) ? (T)1 : ((i > j) ? A[i + j * L] : (T)0); \
+            Lfac[i + j * L] = v;                                              \
+        }                                                                     \
+    out[0] = N; out[1] = Ntau;                                                \
+    free(A); free(s); free(orig);                                             \
+    return 0;
+
+int oracle_factor_f32(int64_t L, const double *K, int64_t ld, double tau,
+                      int64_t n_min, int64_t n_extra,
+                      int64_t *perm, float *Dk, float *Lfac, int64_t *out)
+{
+    ORACLE_FACTOR_BODY(float, fmaf, sqrtf, fabsf)
+}
+
+int oracle_factor_f64(int64_t L, const double *K, int64_t ld, double tau,
+                      int64_t n_min, int64_t n_extra,
+                      int64_t *perm, double *Dk, double *Lfac, int64_t *out)
+{
+    ORACLE_FACTOR_BODY(double, fma, sqrt, fabs)
+}
