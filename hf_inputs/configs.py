@@ -226,5 +226,8 @@ def make_rhs(cfg, seed: int = 0, device="cpu") -> torch.Tensor:
     if spec.kind == "neumann":
         b = b - b.mean()
     elif spec.kind == "saddle":
-        b[2 * spec.grid * spec.grid:] = 0.0
+        nv = 2 * spec.grid * spec.grid
+        b[nv:] = 0.0
+        for c in range(2):
+            b[c:nv:2] -= b[c:nv:2].mean()
     return b.to(device)

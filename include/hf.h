@@ -1,0 +1,153 @@
+/*
+ * hf.h -- C ABI of the B200 hybrid mixed-precision factorization hot path
+ * (Suzuki, "A Hybrid Factorization Algorithm for Sparse Matrix with Mixed
+ * Precision Arithmetic", arXiv 2208.01907).  Implemented by libhf.so
+ * (paper_2208_01907_b200/csrc, hand-written CUDA for sm_100a).
+ *
+ * Citations: P:n = line n of the paper's LaTeX source.  [Rn] are
+ * the readings of silent/ambiguous passages listed in DESIGN.md section 3.
+ *
+ * Conventions (all entry points)
+ *  - Pointers are DEVICE pointers unless the name ends in _host.
+ *  - Matrices are column-major FP64 with leading dimension ld >= L.  K must be
+ *    exactly symmetric; only its lower triangle (row >= col) is read where
+ *    stated.  Index arrays are int64, 0-based, ORIGINAL indices of K.
+ *  - Every call is ordered on the context's CUDA stream.  Calls that return
+ *    *_host values synchronise that stream before returning.
+ *  - Functions return an hf_status and never abort/exit.  On error the
+ *    outputs are unspecified, handles can still be destroyed, and
+ *    hf_last_error(ctx) describes the error.
+ *  - Ownership: the caller owns K, q, b, x and every *_host buffer.  The
+ *    library owns the memory behind hf_lowfactor / hf_hybrid handles and frees
+ *    it in the *_destroy calls.  An hf_hybrid BORROWS the caller's K (used
+ *    again by hf_solve): K must stay valid and unmodified until
+ *    hf_hybrid_destroy.
+ */
+#ifndef HF_H
+#define HF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hf_ctx hf_ctx;             /* device, stream, optional NCCL comm, counters */
+typedef struct hf_lowfactor hf_lowfactor; /* Pi, Lambda_1/2, FP32 factor L, D (device)   */
+typedef struct hf_hybrid hf_hybrid;       /* X12, S22, hard factors, borrowed K          */
+
+typedef enum {
+    HF_OK = 0,
+    HF_ERR_INVALID_ARG = 1,    /* bad size/pointer, tau outside (0,1), NaN/Inf found   */
+    HF_ERR_CUDA = 2,           /* CUDA runtime error (message in hf_last_error)        */
+    HF_ERR_NCCL = 3,           /* NCCL error (multi-GPU contexts)                      */
+    HF_ERR_OOM = 4,            /* device allocation failed                             */
+    HF_ERR_NOT_CONVERGED = 5,  /* block GCR reached max_iter (info filled)             */
+    HF_ERR_BREAKDOWN = 6,      /* Gram matrix M_n not positive definite [R11]          */
+    HF_ERR_STATE = 7           /* handle in the wrong state (e.g. solve before hard)   */
+} hf_status;
+
+/* ---------------------------------------------------------------- context */
+/* device: CUDA ordinal; cuda_stream: a cudaStream_t (NULL = legacy default). */
+hf_status hf_create(int device, void *cuda_stream, hf_ctx **out);
+/* Multi-GPU context (sec. 8(e) of SURVEY.md): nccl_unique_id128 points to the
+ * 128-byte ncclUniqueId produced by hf_nccl_unique_id on rank 0 and broadcast
+ * by the caller (torch.distributed).  rank in [0, nranks). */
+hf_status hf_create_dist(int device, void *cuda_stream, const void *nccl_unique_id128,
+                         int rank, int nranks, hf_ctx **out);
+hf_status hf_nccl_unique_id(void *id128_host);
+hf_status hf_destroy(hf_ctx *ctx);
+/* Last error message of ctx (never NULL; "" when none).  ctx may be NULL for
+ * errors raised before a context existed. */
+const char *hf_last_error(const hf_ctx *ctx);
+
+/* Instrumentation: number of kernels this context launched so far, and the
+ * summed device time of one kernel class measured with CUDA events on the
+ * context stream while profiling is enabled.  class: "trailing", "chain",
+ * "dgemm", "trsm", "scale", "hard", "other". */
+hf_status hf_set_profiling(hf_ctx *ctx, int enable);
+hf_status hf_kernel_stats(hf_ctx *ctx, const char *kernel_class, double *ms_host,
+                          int64_t *launches_host);
+hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host);
+
+/* ------------------------------------------------- a1: scaling, P:40 [R1] */
+/* In place: q_i = 1/sqrt|K_ii| (1 if K_ii == 0); K_ij = (q_i K_ij) q_j for
+ * i > j from the LOWER triangle, mirrored to the upper triangle; K_ii set to
+ * exactly +1, -1 or 0 by the sign of the input diagonal.  K: L x L (ld),
+ * q: FP64[L].  Returns HF_ERR_INVALID_ARG if K holds NaN/Inf on or below the
+ * diagonal. */
+hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);
+
+/* ---------------------------- a2-a3: lower-precision factor, P:64-85 [R2-R10] */
+typedef struct {
+    double tau;       /* threshold of P:73, in (0,1)                                  */
+    int64_t n_extra;  /* P:82 enlargement: move the last n_extra pivots to Lambda_2   */
+    int64_t n_min;    /* postponement floor [R5]: |Lambda_2| >= n_min                 */
+    int32_t nb;       /* panel width (0 = automatic)                                  */
+} hf_lowprec_opts;
+
+/* FP32 LDL^T of the scaled K (lower triangle read) with symmetric max-|diag|
+ * pivoting (ties -> smallest original index), the strict ratio test
+ * |d_k| < tau |d_{k-1}| of P:73 evaluated in FP64, and the role-symmetric
+ * update v_IJ <- fmaf(-sigma s_I, s_J, v_IJ) applied once per pivot in
+ * increasing order [R8], so Pi, D and L are bit-identical to the oracle.
+ * Outputs N = |Lambda_1|, n2 = |Lambda_2| and the pure tau-rule count.
+ * A first pivot of exactly 0 is legal and postpones everything (N = 0). */
+hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
+                            const hf_lowprec_opts *opts, hf_lowfactor **out,
+                            int64_t *N_host, int64_t *n2_host, int64_t *n2_tau_only_host);
+/* perm_host[L]: Pi = [Lambda_1 in pivot order, Lambda_2 ascending] [R10];
+ * D_host[N]: FP32 pivots; Lfac: DEVICE N x N column-major (ldl >= N) unit
+ * lower factor in pivot order (U = L^T), zeros above the diagonal.  Any output
+ * pointer may be NULL to skip it. */
+hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host,
+                              float *D_host, float *Lfac, int64_t ldl);
+hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
+
+/* ------------------------ a4-a6: block GCR + Schur */
+typedef struct {
+    double tol;        /* per-column recursive ||r||_2/||b||_2 target [R13] (1e-14) */
+    int32_t max_iter;  /* iteration cap (100)                                       */
+} hf_gcr_opts;
+typedef struct {
+    int32_t iters;                 /* completed block-GCR iterations          */
+    double max_rel_res_recursive;  /* max over columns at exit (recursive r)  */
+    double max_rel_res_true;       /* max over columns of ||K12 - K11 X||/||K12|| */
+} hf_gcr_info;
+
+/* Alg. 1 steps 2-4: K11 X12 = K12 by right-preconditioned block GCR in FP64
+ * with Q^{-1} = FP32 (L D L^T)^{-1} (casts fused), then S22 = K22 - K21 X12 in
+ * FP64.  K: the SAME scaled full symmetric matrix given to hf_factor_lowprec
+ * (borrowed by the returned handle).  S22_host_or_null: n2 x n2 column-major,
+ * rows/cols in Lambda_2 ascending order.  Returns HF_ERR_NOT_CONVERGED or
+ * HF_ERR_BREAKDOWN with *out still valid and info filled. */
+hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf,
+                       const hf_gcr_opts *opts, hf_hybrid **out, double *S22_host_or_null,
+                       hf_gcr_info *info_host);
+/* X: DEVICE N x n2 (ldx >= N, rows in Pi_1 order); S22: DEVICE n2 x n2 (lds). */
+hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t ldx,
+                           double *S22, int64_t lds);
+
+/* ---------------------------- a7: hard factorization, P:192, P:84 [R15] */
+/* FP64 Bunch-Parlett (complete pivoting, alpha = (1+sqrt17)/8) LDL^T of
+ * (S22 + S22^T)/2 with 1x1/2x2 pivots; stops when max|S_ij| of the trailing
+ * block <= eps_ker * min_k |D_k|; kernel_dim = size of the block left.
+ * n2 = 0 is a no-op (kernel_dim = 0). */
+hf_status hf_factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker, int64_t *kernel_dim_host);
+/* perm2_host[n2]: pivot order as Lambda_2 positions; blocks_host[n2]: pivot
+ * sizes (1 or 2) in order, the rest 0; rank_host: n2 - kernel_dim. */
+hf_status hf_hard_export(hf_ctx *ctx, const hf_hybrid *hy, int64_t *perm2_host,
+                         int32_t *blocks_host, int64_t *rank_host);
+
+/* ------------------------------------------ a8: hybrid solve, Alg. 2 [R16] */
+/* Solves the SCALED system K x = b (b, x: device FP64[L], original order):
+ * y1 = block GCR on K11 with one column, y2 = b2 - K21 y1, x2 = S22^+ y2
+ * (kernel coordinates 0), x1 = y1 - X12 x2.  Requires hf_factor_hard. */
+hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x,
+                   hf_gcr_info *info_host);
+hf_status hf_hybrid_destroy(hf_hybrid *hy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HF_H */

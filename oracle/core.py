@@ -46,8 +46,8 @@ def lib():
             i64, dp, fp, lp = (ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64))
             L.oracle_scale.argtypes = [i64, dp, i64, dp, dp]
-            L.oracle_factor_f32.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, lp, fp, fp, lp]
-            L.oracle_factor_f64.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, lp, dp, dp, lp]
+            L.oracle_factor_f32.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, fp, fp, lp]
+            L.oracle_factor_f64.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, dp, dp, lp]
             _lib = L
     return _lib
 
@@ -107,10 +107,11 @@ class LowFactor:
 
 
 def factor_lowprec(K: np.ndarray, tau: float, n_min: int = 0, n_extra: int = 0,
-                   prec: str = "f32") -> LowFactor:
+                   prec: str = "f32", max_steps: int = 0) -> LowFactor:
     """LDL^T with symmetric max-|diag| pivoting and threshold postponing in the
     lower precision, rules [R2]-[R10].  K: scaled, exactly
-    symmetric float64 (only the lower triangle is read)."""
+    symmetric float64 (only the lower triangle is read).  max_steps > 0 stops
+    after that many pivots (bench.py's bounded CPU-baseline sample only)."""
     K = np.asfortranarray(K, dtype=np.float64)
     L = K.shape[0]
     dt = np.float32 if prec == "f32" else np.float64
@@ -120,7 +121,7 @@ def factor_lowprec(K: np.ndarray, tau: float, n_min: int = 0, n_extra: int = 0,
     Lf = np.empty((max(L, 1), max(L, 1)), dtype=dt, order="F")
     out = np.zeros(2, dtype=np.int64)
     fn = lib().oracle_factor_f32 if prec == "f32" else lib().oracle_factor_f64
-    rc = fn(L, _ptr(K, ctypes.c_double), max(L, 1), float(tau), int(n_min), int(n_extra),
+    rc = fn(L, _ptr(K, ctypes.c_double), max(L, 1), float(tau), int(n_min), int(n_extra), int(max_steps),
             _ptr(perm, ctypes.c_int64), _ptr(Dk, ct), _ptr(Lf, ct), _ptr(out, ctypes.c_int64))
     if rc != 0:
         raise ValueError("oracle_factor: invalid arguments (tau must be in (0,1))")

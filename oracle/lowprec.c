@@ -21,6 +21,9 @@
  *                         pin of the tests and by the (double, double-double)
  *                         pair of sec. 4.3).
  *
+ * max_steps > 0 stops after that many pivots (a bounded sample for bench.py's
+ * CPU baseline; results of such a run are not a factorization).
+ *
  * Arithmetic is IEEE round-to-nearest, no contraction (compiled with
  * -ffp-contract=off); every FMA is an explicit fmaf/fma call.
  */
@@ -95,7 +98,8 @@ int oracle_scale(int64_t L, const double *Kbar, int64_t ld, double *K, double *q
             A[i + j * L] = (T)K[i + j * ld];                                  \
     for (int64_t p = 0; p < L; ++p) orig[p] = p;                              \
     int64_t Ntau = L;                                                         \
-    for (int64_t k = 0; k < L; ++k) {                                         \
+    const int64_t kmax = (max_steps > 0 && max_steps < L) ? max_steps : L;   \
+    for (int64_t k = 0; k < kmax; ++k) {                                      \
         /* [R3] P:65 max |diag|, ties -> smallest original index */           \
         int64_t best = k;                                                     \
         for (int64_t p = k + 1; p < L; ++p) {                                 \
@@ -141,6 +145,7 @@ int oracle_scale(int64_t L, const double *Kbar, int64_t ld, double *K, double *q
                 col[i] = FMA(nsj, s[i], col[i]);                              \
         }                                                                     \
     }                                                                         \
+    if (kmax < L && Ntau == L) Ntau = kmax;   /* sampling run (bench only) */ \
     /* [R5] floor, [R9] P:82 enlargement by moving the last accepted pivots */ \
     int64_t N = Ntau;                                                         \
     if (L - n_min < N) N = (L - n_min > 0) ? L - n_min : 0;                   \
@@ -166,14 +171,14 @@ int oracle_scale(int64_t L, const double *Kbar, int64_t ld, double *K, double *q
     return 0;
 
 int oracle_factor_f32(int64_t L, const double *K, int64_t ld, double tau,
-                      int64_t n_min, int64_t n_extra,
+                      int64_t n_min, int64_t n_extra, int64_t max_steps,
                       int64_t *perm, float *Dk, float *Lfac, int64_t *out)
 {
     ORACLE_FACTOR_BODY(float, fmaf, sqrtf, fabsf)
 }
 
 int oracle_factor_f64(int64_t L, const double *K, int64_t ld, double tau,
-                      int64_t n_min, int64_t n_extra,
+                      int64_t n_min, int64_t n_extra, int64_t max_steps,
                       int64_t *perm, double *Dk, double *Lfac, int64_t *out)
 {
     ORACLE_FACTOR_BODY(double, fma, sqrt, fabs)

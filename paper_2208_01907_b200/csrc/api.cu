@@ -1,0 +1,269 @@
+// api.cu -- extern "C" entry points of libhf (include/hf.h).  Argument checks,
+// status/error plumbing and handle lifetime; every step of the path runs in
+// the kernels of k_*.cu.
+#include <math.h>
+
+#include <cstring>
+#include <memory>
+
+#include "hf_internal.cuh"
+
+namespace {
+
+thread_local std::string g_noctx_error;
+
+template <typename F>
+hf_status guarded(hf_ctx *ctx, F &&f) {
+    try {
+        f();
+        if (ctx) ctx->last_error.clear();
+        return HF_OK;
+    } catch (const hf::Error &e) {
+        if (ctx) ctx->last_error = e.msg;
+        else g_noctx_error = e.msg;
+        return e.st;
+    } catch (const std::bad_alloc &) {
+        if (ctx) ctx->last_error = "host allocation failed";
+        return HF_ERR_OOM;
+    } catch (const std::exception &e) {
+        if (ctx) ctx->last_error = e.what();
+        return HF_ERR_CUDA;
+    }
+}
+
+void resolve_stats(hf_ctx *ctx) {
+    for (auto &kv : ctx->pending) {
+        auto &st = ctx->stats[kv.first];
+        for (auto &pr : kv.second) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(pr.second) == cudaSuccess &&
+                cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess)
+                st.ms += ms;
+            st.launches += 1;
+            ctx->event_pool.push_back(pr.first);
+            ctx->event_pool.push_back(pr.second);
+        }
+        kv.second.clear();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+hf_status hf_create(int device, void *cuda_stream, hf_ctx **out) {
+    if (!out) return HF_ERR_INVALID_ARG;
+    *out = nullptr;
+    std::unique_ptr<hf_ctx> c(new (std::nothrow) hf_ctx());
+    if (!c) return HF_ERR_OOM;
+    hf_status s = guarded(nullptr, [&] {
+        HF_CUDA(cudaSetDevice(device));
+        cudaDeviceProp p;
+        HF_CUDA(cudaGetDeviceProperties(&p, device));
+        HF_REQUIRE(p.major >= 10, "libhf is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(p.major) + std::to_string(p.minor));
+        c->device = device;
+        c->num_sms = p.multiProcessorCount;
+        c->stream = (cudaStream_t)cuda_stream;
+    });
+    if (s != HF_OK) return s;
+    *out = c.release();
+    return HF_OK;
+}
+
+hf_status hf_destroy(hf_ctx *ctx) {
+    if (!ctx) return HF_OK;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &kv : ctx->pending)
+        for (auto &pr : kv.second) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+#ifdef HF_WITH_NCCL
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+#endif
+    delete ctx;
+    return HF_OK;
+}
+
+const char *hf_last_error(const hf_ctx *ctx) {
+    return ctx ? ctx->last_error.c_str() : g_noctx_error.c_str();
+}
+
+hf_status hf_set_profiling(hf_ctx *ctx, int enable) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    ctx->profiling = enable != 0;
+    return HF_OK;
+}
+
+hf_status hf_kernel_stats(hf_ctx *ctx, const char *cls, double *ms_host, int64_t *launches_host) {
+    if (!ctx || !cls) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        resolve_stats(ctx);
+        auto it = ctx->stats.find(cls);
+        double ms = 0.0;
+        int64_t n = 0;
+        if (it != ctx->stats.end()) {
+            ms = it->second.ms;
+            n = it->second.launches;
+        }
+        if (ms_host) *ms_host = ms;
+        if (launches_host) *launches_host = n;
+    });
+}
+
+hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host) {
+    if (!ctx || !launches_host) return HF_ERR_INVALID_ARG;
+    *launches_host = ctx->launches;
+    return HF_OK;
+}
+
+// ------------------------------------------------------------------ a1
+hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || (K && q)), "hf_scale: bad arguments");
+        if (L == 0) return;
+        hf::DBuf<int> bad;
+        bad.alloc(1, ctx->stream);
+        bad.zero(ctx->stream);
+        hf::launch_scale(ctx, L, K, ld, q, bad.p);
+        int hb = 0;
+        HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        HF_REQUIRE(!hb, "hf_scale: K holds NaN or Inf");
+    });
+}
+
+// ------------------------------------------------------------------ a2-a3
+hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
+                            const hf_lowprec_opts *opts, hf_lowfactor **out, int64_t *N_host,
+                            int64_t *n2_host, int64_t *n2_tau_only_host) {
+    if (!ctx || !out) return HF_ERR_INVALID_ARG;
+    *out = nullptr;
+    hf_lowprec_opts o{1e-2, 0, 0, 0};
+    if (opts) o = *opts;
+    std::unique_ptr<hf_lowfactor> lf(new hf_lowfactor());
+    hf_status s = guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || K), "hf_factor_lowprec: bad arguments");
+        HF_REQUIRE(o.tau > 0.0 && o.tau < 1.0, "hf_factor_lowprec: tau must lie in (0,1)");
+        HF_REQUIRE(o.n_extra >= 0 && o.n_min >= 0, "hf_factor_lowprec: n_extra/n_min < 0");
+        HF_REQUIRE(o.nb >= 0 && o.nb <= 256 && o.nb % 8 == 0, "hf_factor_lowprec: nb in {0, 8..256, multiple of 8}");
+        hf::lowprec_factor(ctx, L, K, ld, o, lf.get());
+    });
+    if (s != HF_OK) return s;
+    if (N_host) *N_host = lf->N;
+    if (n2_host) *n2_host = lf->n2;
+    if (n2_tau_only_host) *n2_tau_only_host = lf->L - lf->Ntau;
+    *out = lf.release();
+    return HF_OK;
+}
+
+hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host, float *D_host,
+                              float *Lfac, int64_t ldl) {
+    if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        if (perm_host && lf->L) std::memcpy(perm_host, lf->h_perm.data(), lf->L * sizeof(int64_t));
+        if (D_host && lf->N) std::memcpy(D_host, lf->h_D.data(), lf->N * sizeof(float));
+        if (Lfac && lf->N) {
+            HF_REQUIRE(ldl >= lf->N, "hf_lowfactor_export: ldl < N");
+            HF_CUDA(cudaMemcpy2DAsync(Lfac, ldl * sizeof(float), lf->Lfac.p, lf->N * sizeof(float),
+                                      lf->N * sizeof(float), lf->N, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    });
+}
+
+hf_status hf_lowfactor_destroy(hf_lowfactor *lf) {
+    if (lf) {
+        cudaStreamSynchronize(lf->stream);
+        delete lf;
+    }
+    return HF_OK;
+}
+
+// ------------------------------------------------------------------ a4-a6
+hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf,
+                       const hf_gcr_opts *opts, hf_hybrid **out, double *S22_host_or_null,
+                       hf_gcr_info *info_host) {
+    if (!ctx || !lf || !out) return HF_ERR_INVALID_ARG;
+    *out = nullptr;
+    hf_gcr_opts o{1e-14, 100};
+    if (opts) o = *opts;
+    hf_gcr_info info{0, 0.0, 0.0};
+    std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
+    hf_status s = guarded(ctx, [&] {
+        HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr: bad arguments");
+        HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr: tol > 0, max_iter >= 1");
+        hy->K = K;
+        hy->ld = ld;
+        hy->L = lf->L;
+        hy->N = lf->N;
+        hy->n2 = lf->n2;
+        hy->lf = lf;
+        hy->stream = ctx->stream;
+        hy->num_sms = ctx->num_sms;
+        hf::schur_gcr(ctx, hy.get(), o, &info);
+        if (S22_host_or_null && hy->n2 > 0) {
+            HF_CUDA(cudaMemcpyAsync(S22_host_or_null, hy->S22.p, hy->n2 * hy->n2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+    if (info_host) *info_host = info;
+    if (s == HF_OK || s == HF_ERR_NOT_CONVERGED || s == HF_ERR_BREAKDOWN) *out = hy.release();
+    return s;
+}
+
+hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t ldx, double *S22,
+                           int64_t lds);
+
+hf_status hf_factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker, int64_t *kernel_dim_host) {
+    if (!ctx || !hy) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(eps_ker >= 0.0, "hf_factor_hard: eps_ker < 0");
+        hf::factor_hard(ctx, hy, eps_ker);
+        if (kernel_dim_host) *kernel_dim_host = hy->kernel_dim;
+    });
+}
+
+hf_status hf_hard_export(hf_ctx *ctx, const hf_hybrid *hy, int64_t *perm2_host, int32_t *blocks_host,
+                         int64_t *rank_host) {
+    if (!ctx || !hy) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        if (!hy->hard_done) throw hf::Error{HF_ERR_STATE, "hf_hard_export: call hf_factor_hard first"};
+        const int64_t n2 = hy->n2;
+        if (rank_host) *rank_host = hy->rank;
+        if (n2 == 0) return;
+        std::vector<int32_t> p(n2), b(n2);
+        HF_CUDA(cudaMemcpyAsync(p.data(), hy->perm2.p, n2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaMemcpyAsync(b.data(), hy->blocks.p, n2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (perm2_host)
+            for (int64_t i = 0; i < n2; ++i) perm2_host[i] = p[i];
+        if (blocks_host) std::memcpy(blocks_host, b.data(), n2 * sizeof(int32_t));
+    });
+}
+
+hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, hf_gcr_info *info_host) {
+    if (!ctx || !hy || !b || !x) return HF_ERR_INVALID_ARG;
+    hf_gcr_info info{0, 0.0, 0.0};
+    hf_status s = guarded(ctx, [&] {
+        if (!hy->hard_done && hy->n2 > 0)
+            throw hf::Error{HF_ERR_STATE, "hf_solve: call hf_factor_hard first"};
+        hf_gcr_opts o{1e-14, 100};
+        hf::hybrid_solve(ctx, hy, b, x, o, &info);
+    });
+    if (info_host) *info_host = info;
+    return s;
+}
+
+hf_status hf_hybrid_destroy(hf_hybrid *hy) {
+    if (hy) {
+        cudaStreamSynchronize(hy->stream);
+        delete hy;
+    }
+    return HF_OK;
+}
+
+}  // extern "C"

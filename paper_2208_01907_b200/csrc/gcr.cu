@@ -1,0 +1,269 @@
+// gcr.cu -- host orchestration of steps a4-a8 on the context stream:
+//   Alg. 1 steps 2-5 and Alg. 2, with Algorithm 5
+//   (preconditioned block GCR) as the inner solver.
+//
+// All N x n2 blocks live in ORIGINAL row order as L x n2 arrays whose
+// Lambda_2 rows are zero: the block mat-vec K11 W is then the plain dense
+// product K W (K is the full scaled matrix, read contiguously by the DMMA
+// GEMM) with the Lambda_2 rows of the result masked to zero, and the Gram
+// products are plain column dot products.  Only the FP32 preconditioner
+// works in pivot order (gather/scatter fused into its kernels).
+//
+// Readings [R13]: M_n = Q_n^T Q_n, A_n = Q_n^T R_n, X += P_n M_n^{-1} A_n,
+// R -= Q_n M_n^{-1} A_n, G_mn = -M_m^{-1} Q_m^T Z_{n+1} for all m <= n,
+// P_{n+1} = W + sum_m P_m G_mn, Q_{n+1} = Z + sum_m Q_m G_mn; convergence when
+// every column's recursive ||r||_2 / ||b||_2 <= tol (one 8-byte D2H per
+// iteration).
+#include <algorithm>
+#include <cmath>
+
+#include "k_dgemm.cuh"
+#include "k_small.cuh"
+
+namespace hf {
+namespace {
+
+struct GcrWork {
+    DBuf<double> P, Q;       // L x cap*n
+    int64_t cap = 0;         // blocks
+    DBuf<double> Minv;       // cap * n * n
+    DBuf<double> R, H, G, Mn, An, C;
+    DBuf<double> bn2, rn2, res;
+    DBuf<double> dgw, chw, chdg;
+    DBuf<int> status;
+};
+
+void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {
+    if (need <= w.cap) return;
+    int64_t nc = std::max<int64_t>(need, std::max<int64_t>(8, 2 * w.cap));
+    DBuf<double> P2, Q2, M2;
+    P2.alloc((size_t)L * n * nc, ctx->stream);
+    Q2.alloc((size_t)L * n * nc, ctx->stream);
+    M2.alloc((size_t)n * n * nc, ctx->stream);
+    if (w.cap > 0) {
+        HF_CUDA(cudaMemcpyAsync(P2.p, w.P.p, (size_t)L * n * w.cap * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        HF_CUDA(cudaMemcpyAsync(Q2.p, w.Q.p, (size_t)L * n * w.cap * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        HF_CUDA(cudaMemcpyAsync(M2.p, w.Minv.p, (size_t)n * n * w.cap * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    w.P = std::move(P2);
+    w.Q = std::move(Q2);
+    w.Minv = std::move(M2);
+    w.cap = nc;
+}
+
+// Z = mask o (K W)   (K11 W in original row order)
+inline void matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, const double *W,
+                   int64_t n, double *Z, double beta, double alpha, GcrWork &w) {
+    dgemm(ctx, false, L, n, L, alpha, K, ld, W, L, beta, Z, L, mask, &w.dgw);
+}
+
+double read_res(hf_ctx *ctx, GcrWork &w, int *bad) {
+    double r = 0.0;
+    int st = 0;
+    HF_CUDA(cudaMemcpyAsync(&r, w.res.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    HF_CUDA(cudaMemcpyAsync(&st, w.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    *bad = st;
+    return r;
+}
+
+// Algorithm 5: solve K11 X = B (L x n, original order, Lambda_2 rows zero).
+void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, Precond &pc,
+               const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info, GcrWork &w) {
+    cudaStream_t st = ctx->stream;
+    w.R.alloc((size_t)L * n, st);
+    w.bn2.alloc(n, st);
+    w.rn2.alloc(n, st);
+    w.res.alloc(1, st);
+    w.status.alloc(1, st);
+    w.status.zero(st);
+    w.Mn.alloc((size_t)n * n, st);
+    w.An.alloc((size_t)n * n, st);
+    w.C.alloc((size_t)n * n, st);
+    double *R = w.R.p;
+
+    colnorm2(ctx, L, n, B, L, w.bn2.p);
+    precond_apply(ctx, pc, n, B, L, X, L);                       // find x_0: Q x_0 = b
+    HF_CUDA(cudaMemcpyAsync(R, B, (size_t)L * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    matvec(ctx, K, ld, L, mask, X, n, R, 1.0, -1.0, w);          // r_0 = b - A x_0
+    colnorm2(ctx, L, n, R, L, w.rn2.p);
+    maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
+    int bad = 0;
+    double res = read_res(ctx, w, &bad);
+    int iters = 0;
+    bool conv = res <= o.tol;
+    if (!conv) {
+        grow(ctx, w, L, n, 2);
+        precond_apply(ctx, pc, n, R, L, w.P.p, L);               // p_0 = w_0 = Q^{-1} r_0
+        matvec(ctx, K, ld, L, mask, w.P.p, n, w.Q.p, 0.0, 1.0, w);  // q_0 = A p_0
+        for (int it = 0; it < o.max_iter; ++it) {
+            const double *Pn = w.P.p + (size_t)it * n * L;
+            const double *Qn = w.Q.p + (size_t)it * n * L;
+            double *Minv = w.Minv.p + (size_t)it * n * n;
+            dgemm(ctx, true, n, n, L, 1.0, Qn, L, Qn, L, 0.0, w.Mn.p, n, nullptr, &w.dgw);   // M_n
+            dgemm(ctx, true, n, n, L, 1.0, Qn, L, R, L, 0.0, w.An.p, n, nullptr, &w.dgw);    // A_n
+            spd_inverse(ctx, n, w.Mn.p, n, Minv, w.chw, w.chdg, w.status.p);
+            dgemm(ctx, false, n, n, n, 1.0, Minv, n, w.An.p, n, 0.0, w.C.p, n, nullptr, &w.dgw, 1);
+            dgemm(ctx, false, L, n, n, 1.0, Pn, L, w.C.p, n, 1.0, X, L, nullptr, &w.dgw, 1);   // x += p C
+            dgemm(ctx, false, L, n, n, -1.0, Qn, L, w.C.p, n, 1.0, R, L, nullptr, &w.dgw, 1);  // r -= q C
+            colnorm2(ctx, L, n, R, L, w.rn2.p);
+            maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
+            res = read_res(ctx, w, &bad);
+            iters = it + 1;
+            if (res <= o.tol) {
+                conv = true;
+                break;
+            }
+            if (bad) {
+                info->iters = iters;
+                info->max_rel_res_recursive = res;
+                throw Error{HF_ERR_BREAKDOWN, "block GCR: Gram matrix M_n is not positive definite"};
+            }
+            if (it + 1 >= o.max_iter) break;
+            grow(ctx, w, L, n, it + 2);
+            double *Pn1 = w.P.p + (size_t)(it + 1) * n * L;
+            double *Qn1 = w.Q.p + (size_t)(it + 1) * n * L;
+            const int64_t nb = (int64_t)(it + 1) * n;
+            precond_apply(ctx, pc, n, R, L, Pn1, L);                       // w_{n+1}
+            matvec(ctx, K, ld, L, mask, Pn1, n, Qn1, 0.0, 1.0, w);         // z_{n+1} = A w_{n+1}
+            w.H.alloc((size_t)nb * n, st);
+            w.G.alloc((size_t)nb * n, st);
+            dgemm(ctx, true, nb, n, L, 1.0, w.Q.p, L, Qn1, L, 0.0, w.H.p, nb, nullptr, &w.dgw);   // Q_m^T z
+            for (int m = 0; m <= it; ++m)                                   // G_m = -M_m^{-1} Q_m^T z
+                dgemm(ctx, false, n, n, n, -1.0, w.Minv.p + (size_t)m * n * n, n, w.H.p + (size_t)m * n, nb, 0.0,
+                      w.G.p + (size_t)m * n, nb, nullptr, &w.dgw, 1);
+            dgemm(ctx, false, L, n, nb, 1.0, w.P.p, L, w.G.p, nb, 1.0, Pn1, L, nullptr, &w.dgw);  // p_{n+1}
+            dgemm(ctx, false, L, n, nb, 1.0, w.Q.p, L, w.G.p, nb, 1.0, Qn1, L, nullptr, &w.dgw);  // q_{n+1}
+        }
+    }
+    info->iters = iters;
+    info->max_rel_res_recursive = res;
+    // true residual ||B - K11 X|| / ||B|| (reported)
+    HF_CUDA(cudaMemcpyAsync(R, B, (size_t)L * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    matvec(ctx, K, ld, L, mask, X, n, R, 1.0, -1.0, w);
+    colnorm2(ctx, L, n, R, L, w.rn2.p);
+    maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
+    info->max_rel_res_true = read_res(ctx, w, &bad);
+    if (!conv) throw Error{HF_ERR_NOT_CONVERGED, "block GCR reached max_iter"};
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Alg. 1 steps 2-4
+void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info) {
+    cudaStream_t st = ctx->stream;
+    const hf_lowfactor *lf = hy->lf;
+    const int64_t L = hy->L, N = hy->N, n2 = hy->n2;
+    info->iters = 0;
+    info->max_rel_res_recursive = info->max_rel_res_true = 0.0;
+    hy->mask1.alloc(std::max<int64_t>(L, 1), st);
+    if (L > 0) mask_from_pos(ctx, L, lf->pos1.p, hy->mask1.p);
+    hy->lam2.alloc(std::max<int64_t>(n2, 1), st);
+    if (n2 > 0)
+        HF_CUDA(cudaMemcpyAsync(hy->lam2.p, lf->perm.p + N, n2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    precond_setup(ctx, hy->pc, N, L, lf->Lfac.p, lf->D.p, lf->perm.p);
+    hy->X.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
+    hy->B.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
+    hy->S22.alloc((size_t)std::max<int64_t>(n2 * n2, 1), st);
+    if (n2 == 0) return;
+    gather_K12(ctx, L, hy->K, hy->ld, hy->lam2.p, n2, hy->mask1.p, hy->B.p);   // step 2
+    gather_K22(ctx, n2, hy->K, hy->ld, hy->lam2.p, hy->S22.p);
+    if (N > 0) {
+        GcrWork w;
+        block_gcr(ctx, hy->K, hy->ld, L, hy->mask1.p, hy->pc, hy->B.p, n2, hy->X.p, o, info, w);   // step 3
+        // step 4: S22 = K22 - K21 X  (K21 X = B^T X since X is zero on Lambda_2 rows)
+        dgemm(ctx, true, n2, n2, L, -1.0, hy->B.p, L, hy->X.p, L, 1.0, hy->S22.p, n2, nullptr, &w.dgw);
+    } else {
+        HF_CUDA(cudaMemsetAsync(hy->X.p, 0, (size_t)L * n2 * sizeof(double), st));
+    }
+}
+
+// ------------------------------------------------------------------ Alg. 1 step 5
+void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker) {
+    cudaStream_t st = ctx->stream;
+    const int64_t n2 = hy->n2;
+    hy->hard_done = false;
+    if (n2 == 0) {
+        hy->rank = hy->kernel_dim = 0;
+        hy->hard_done = true;
+        return;
+    }
+    double dref = 1.0;
+    const auto &D = hy->lf->h_D;
+    if (!D.empty()) {
+        dref = INFINITY;
+        for (float d : D) dref = std::min(dref, std::fabs((double)d));
+    }
+    hy->Lh.alloc((size_t)n2 * n2, st);
+    hy->Dh.alloc((size_t)n2 * n2, st);
+    hy->perm2.alloc(n2, st);
+    hy->blocks.alloc(n2, st);
+    DBuf<double> A;
+    A.alloc((size_t)n2 * n2, st);
+    DBuf<int64_t> rk;
+    rk.alloc(1, st);
+    hard_factor(ctx, n2, hy->S22.p, eps_ker * dref, A.p, hy->Lh.p, hy->Dh.p, hy->perm2.p, hy->blocks.p, rk.p);
+    int64_t r = 0;
+    HF_CUDA(cudaMemcpyAsync(&r, rk.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HF_CUDA(cudaStreamSynchronize(st));
+    hy->rank = r;
+    hy->kernel_dim = n2 - r;
+    hy->hard_done = true;
+}
+
+// ------------------------------------------------------------------ Alg. 2
+void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
+                  hf_gcr_info *info) {
+    cudaStream_t st = ctx->stream;
+    const int64_t L = hy->L, N = hy->N, n2 = hy->n2;
+    info->iters = 0;
+    info->max_rel_res_recursive = info->max_rel_res_true = 0.0;
+    if (L == 0) return;
+    DBuf<double> bm, y1, y2, x2, z;
+    y1.alloc(L, st);
+    if (N > 0) {
+        bm.alloc(L, st);
+        mask_vec(ctx, L, hy->mask1.p, b, bm.p);
+        GcrWork w;
+        block_gcr(ctx, hy->K, hy->ld, L, hy->mask1.p, hy->pc, bm.p, 1, y1.p, o, info, w);   // step 1
+    } else {
+        HF_CUDA(cudaMemsetAsync(y1.p, 0, L * sizeof(double), st));
+    }
+    HF_CUDA(cudaMemcpyAsync(x, y1.p, L * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (n2 > 0) {
+        y2.alloc(n2, st);
+        x2.alloc(n2, st);
+        z.alloc(n2, st);
+        DBuf<double> dg;
+        gather_rows(ctx, n2, hy->lam2.p, b, y2.p);
+        dgemm(ctx, true, n2, 1, L, -1.0, hy->B.p, L, y1.p, L, 1.0, y2.p, n2, nullptr, &dg);   // step 2
+        hard_solve(ctx, n2, hy->rank, hy->Lh.p, hy->Dh.p, hy->perm2.p, hy->blocks.p, y2.p, x2.p, z.p);  // step 3
+        dgemm(ctx, false, L, 1, n2, -1.0, hy->X.p, L, x2.p, n2, 1.0, x, L, nullptr, &dg, 1);   // step 4
+        scatter_rows(ctx, n2, hy->lam2.p, x2.p, x);
+    }
+    HF_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace hf
+
+extern "C" hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t ldx, double *S22,
+                                      int64_t lds) {
+    if (!ctx || !hy) return HF_ERR_INVALID_ARG;
+    try {
+        const int64_t N = hy->N, n2 = hy->n2;
+        if (X && N > 0 && n2 > 0) {
+            if (ldx < N) throw hf::Error{HF_ERR_INVALID_ARG, "hf_hybrid_export: ldx < N"};
+            hf::gather_block_rows(ctx, N, n2, hy->lf->perm.p, hy->X.p, hy->L, X, ldx);
+        }
+        if (S22 && n2 > 0) {
+            if (lds < n2) throw hf::Error{HF_ERR_INVALID_ARG, "hf_hybrid_export: lds < n2"};
+            HF_CUDA(cudaMemcpy2DAsync(S22, lds * sizeof(double), hy->S22.p, n2 * sizeof(double), n2 * sizeof(double),
+                                      n2, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (const hf::Error &e) {
+        ctx->last_error = e.msg;
+        return e.st;
+    }
+    return HF_OK;
+}

@@ -1,0 +1,204 @@
+// hf_internal.cuh -- private definitions of libhf (B200 / sm_100a).
+// Nothing here is shared with oracle/ (test infrastructure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hf.h"
+
+#ifdef HF_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace hf {
+
+// ----------------------------------------------------------------- errors
+struct Error {
+    hf_status st;
+    std::string msg;
+};
+
+#define HF_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            throw ::hf::Error{e_ == cudaErrorMemoryAllocation ? HF_ERR_OOM : HF_ERR_CUDA, \
+                              std::string(#call) + ": " + cudaGetErrorString(e_) +     \
+                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")"}; \
+    } while (0)
+
+#define HF_CHECK_LAUNCH(ctx)                                                           \
+    do {                                                                               \
+        cudaError_t e_ = cudaGetLastError();                                           \
+        if (e_ != cudaSuccess)                                                         \
+            throw ::hf::Error{HF_ERR_CUDA, std::string("kernel launch: ") +            \
+                                               cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                                               std::to_string(__LINE__) + ")"};        \
+        (ctx)->launches++;                                                             \
+    } while (0)
+
+#define HF_REQUIRE(cond, msg)                                                          \
+    do {                                                                               \
+        if (!(cond)) throw ::hf::Error{HF_ERR_INVALID_ARG, std::string(msg)};          \
+    } while (0)
+
+// ----------------------------------------------------------------- device buffers
+template <typename T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept { *this = std::move(o); }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count, cudaStream_t stream) {
+        if (count <= n && p) return;
+        release();
+        s = stream;
+        size_t bytes = (count ? count : 1) * sizeof(T);
+        HF_CUDA(cudaMallocAsync((void **)&p, bytes, stream));
+        n = count;
+    }
+    void zero(cudaStream_t stream) {
+        if (p) HF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream));
+    }
+};
+
+// ----------------------------------------------------------------- context
+struct KStat {
+    double ms = 0.0;
+    int64_t launches = 0;
+};
+
+}  // namespace hf
+
+struct hf_ctx {
+    int device = 0;
+    cudaStream_t stream = 0;
+    int num_sms = 148;
+    int rank = 0, nranks = 1;
+#ifdef HF_WITH_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+    std::string last_error;
+    int64_t launches = 0;
+    bool profiling = false;
+    // pending (start, stop) event pairs per class; resolved lazily
+    std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::map<std::string, hf::KStat> stats;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+namespace hf {
+
+// RAII timer around launches of one kernel class (only when profiling).
+struct ClassTimer {
+    hf_ctx *ctx;
+    const char *cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ClassTimer(hf_ctx *c, const char *k) : ctx(c), cls(k) {
+        if (!ctx->profiling) return;
+        a = take(); b = take();
+        cudaEventRecord(a, ctx->stream);
+    }
+    ~ClassTimer() {
+        if (!ctx->profiling || !a) return;
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending[cls].push_back({a, b});
+    }
+    cudaEvent_t take() {
+        if (!ctx->event_pool.empty()) {
+            cudaEvent_t e = ctx->event_pool.back();
+            ctx->event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace hf
+
+// FP32 preconditioner state (k_trsm.cu)
+namespace hf {
+struct Precond {
+    int64_t N = 0, L = 0;
+    const float *Lfac = nullptr;   // N x N unit lower, pivot order
+    const float *D = nullptr;      // [N]
+    const int64_t *perm = nullptr; // [L] pivot order -> original index
+    DBuf<float> Linv;              // inverses of the 64x64 diagonal blocks
+    DBuf<float> Y;                 // N x ncol workspace (FP32)
+    DBuf<float> Xb;                // N x ncol workspace (FP32)
+    DBuf<int> flags;
+    DBuf<int> counter;
+    int epoch = 0;
+};
+}  // namespace hf
+
+// ----------------------------------------------------------------- handles
+struct hf_lowfactor {
+    int64_t L = 0, N = 0, Ntau = 0, n2 = 0;
+    std::vector<int64_t> h_perm;       // Pi (host copy)
+    std::vector<float> h_D;            // D (host copy)
+    hf::DBuf<int64_t> perm;            // Pi (device)
+    hf::DBuf<int32_t> pos1;            // original index -> pivot rank (Lambda_1) or -1
+    hf::DBuf<float> D;                 // [N]
+    hf::DBuf<float> Lfac;              // N x N unit lower, pivot order, ld = N
+    cudaStream_t stream = 0;
+};
+
+struct hf_hybrid {
+    const double *K = nullptr;         // borrowed scaled K
+    int64_t ld = 0, L = 0, N = 0, n2 = 0;
+    const hf_lowfactor *lf = nullptr;  // borrowed
+    hf::DBuf<double> X;                // L x n2, original row order, zero on Lambda_2 rows
+    hf::DBuf<double> B;                // L x n2: K12 (original row order, zero on Lambda_2 rows)
+    hf::DBuf<double> S22;              // n2 x n2, Lambda_2 ascending
+    hf::DBuf<int64_t> lam2;            // [n2] original indices (ascending)
+    hf::DBuf<uint8_t> mask1;           // [L] 1 on Lambda_1 rows
+    // stage 3
+    bool hard_done = false;
+    int64_t rank = 0, kernel_dim = 0;
+    hf::DBuf<double> Lh;               // n2 x n2 unit lower (pivoted positions)
+    hf::DBuf<double> Dh;               // n2 x n2 block diagonal
+    hf::DBuf<int32_t> perm2;           // [n2]
+    hf::DBuf<int32_t> blocks;          // [n2]
+    mutable hf::Precond pc;            // FP32 preconditioner (workspaces reused by hf_solve)
+    cudaStream_t stream = 0;
+    int num_sms = 148;
+};
+
+// ----------------------------------------------------------------- launchers
+namespace hf {
+void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);
+void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                    hf_lowfactor *lf);
+void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
+void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
+void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
+                  hf_gcr_info *info);
+}  // namespace hf

@@ -1,0 +1,608 @@
+// k_lowprec.cu -- steps a2/a3: FP32 LDL^T with symmetric max-|diag| pivoting
+// and threshold postponing (Alg. 1 step 1; sec. 2.1; sec. 2.2
+// P:72-75), rules [R2]-[R10] of DESIGN.md.
+//
+// B200 design:
+//  * Blocked LEFT-looking over panels of nb pivots with a lazily updated
+//    diagonal.  No physical row/column swaps: after every panel the active
+//    (not yet pivoted) indices are compacted STABLY, so position order equals
+//    original-index order and "ties -> smallest original index" [R3] is
+//    "ties -> smallest position".
+//  * k_chain: one cooperative persistent launch per panel, one CTA per SM.
+//    Each CTA owns a contiguous slice of rows and keeps their panel values
+//    -sigma_u s_i^u in shared memory.  Per pivot: local argmax -> one 64-bit
+//    key per CTA published to a tagged global slot -> every CTA reduces all
+//    slots (the only grid-wide exchange) -> the pivot column is assembled
+//    from the panel-start matrix plus the in-panel updates, one fmaf per
+//    earlier in-panel pivot in increasing order [R8] -> s_i = c_i / sqrt|d|,
+//    L_ik = c_i / d, lazy diagonal update.
+//  * k_trailing: symmetric rank-nb update of the trailing lower triangle,
+//    FP32 FFMA register-tiled (128x128 CTA tile, 8x8 per thread).  Every
+//    entry is ONE accumulator seeded from its value and updated with one
+//    fmaf per pivot in increasing order -- no split-K, no reassociation, no
+//    tensor cores -- which is what makes Pi, D, L bit-identical to the
+//    oracle.  The stable compaction is fused into its loads.
+//
+// Role symmetry: fmaf(-sigma s_I, s_J, v) == fmaf(-sigma s_J, s_I, v) bit for
+// bit because the product is exact inside the FMA, so the row/column roles of
+// the oracle (right-looking) and of these kernels need not match.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "hf_internal.cuh"
+
+namespace hf {
+namespace {
+
+constexpr uint32_t POS_MAX = 0x1FFFF;   // 17-bit position field -> L <= 131071
+
+// ------------------------------------------------------------------ keys
+// (|d| bits, smallest position wins ties, sign of d): the unsigned max of the
+// keys is the pivot of [R3]; 0 is neutral (no candidate).
+__device__ __forceinline__ uint64_t mkkey(float d, uint32_t pos) {
+    const uint64_t ab = __float_as_uint(fabsf(d));
+    return (ab << 32) | ((uint64_t)(POS_MAX - pos) << 15) | ((uint64_t)(d < 0.f) << 14) | 1ull;
+}
+
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ uint64_t warp_max64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ------------------------------------------------------------------ cast [R2]
+__global__ void k_cast_lower(int64_t L, const double *__restrict__ K, int64_t ldk, float *__restrict__ V,
+                             int64_t ldv) {
+    for (int64_t j = blockIdx.x; j < L; j += gridDim.x) {
+        const double *kc = K + j * ldk;
+        float *vc = V + j * ldv;
+        for (int64_t i = j + threadIdx.x; i < L; i += blockDim.x) vc[i] = __double2float_rn(kc[i]);
+    }
+}
+
+__global__ void k_iota32(int64_t n, int32_t *a) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+
+// ------------------------------------------------------------------ chain
+struct ChainArgs {
+    int64_t m;          // active size at panel start
+    int64_t K0;         // global index of the panel's first pivot
+    int nbp;            // pivots to attempt in this panel
+    int R;              // rows per CTA (smem stride)
+    double tau;
+    const float *V;     // trailing matrix (position space), lower triangle
+    int64_t ldv;
+    const int32_t *orig;  // position -> original index
+    float *S;           // S[i + t*lds] = s_i^t (positive sign), this panel
+    int64_t lds;
+    float *sigma;       // [nb] sign of d_t
+    int32_t *pivpos;    // [nb] pivot positions of this panel
+    float *Lorig;       // Lorig[orig + k*ldl] = L_{orig,k}
+    int64_t ldl;
+    float *Dk;          // [L] d_k
+    int32_t *pivorig;   // [L] original index of pivot k
+    unsigned long long *keys;  // [nbp] per-step max key (zeroed before the launch)
+    unsigned int *cnt;         // arrival counter (zeroed before the launch)
+    float *mbox;        // [2][G][nb] candidate-row mailboxes (-sigma_u s_P^u)
+    int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
+    unsigned long long *dbg;   // optional per-phase time sums (CTA 0), HF_CHAIN_DEBUG
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Per pivot k = K0 + t (all CTAs in lock step):
+//  A  local argmax over own active rows -> CTA key (warp shuffles + smem)
+//  B  warp 0 writes the candidate row's panel values to this CTA's mailbox,
+//     red.max of the key into keys[t], red.release.add on the arrival counter
+//  C  the PREVIOUS step's s / L values of own rows go to global memory now,
+//     after the release, so the release never waits on them
+//  D  one thread per CTA polls the counter (acquire) and reads keys[t]
+//  E  stop test [R4]; F  pivot-row panel values from the winner's mailbox and
+//     the panel-start column V[:, P] for own rows; G  c_i = chain of fmaf over
+//     the earlier in-panel pivots in order [R8], s = c/r, L = c/d, diagonal.
+__global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
+    extern __shared__ float smem[];
+    __shared__ unsigned long long red[32];
+    __shared__ unsigned long long bkey;
+    if (*(volatile int32_t *)&a.status[2]) return;   // uniform: set by an earlier launch
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * a.R;
+    const int64_t nown = max((int64_t)0, min((int64_t)a.R, a.m - r0));
+    const int nb = a.nbp;
+    float *sneg = smem;                       // [nbp][R]  -sigma_u s_i^u for own rows
+    float *sp = smem + (size_t)nb * a.R;      // [nbp]     s_P^u of the current pivot row
+    float *sgm = sp + nb;                     // [nbp]     sigma_u
+
+    const bool has = tid < nown;
+    const int64_t i = r0 + tid;
+    float dg = has ? a.V[i + i * a.ldv] : 0.f;      // lazy diagonal of own row
+    bool piv = !has;
+    const int32_t oi = has ? a.orig[i] : 0;
+    float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
+    // deferred stores of the previous step
+    bool pend = false;
+    float ps = 0.f, pl = 0.f;
+    int t = 0;
+    bool stopped = false;
+    const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
+    unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = dbg ? gtimer() : 0;
+#define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
+    for (; t < nb; ++t) {
+        const int64_t k = a.K0 + t;
+        // ---- A: [R3] local argmax of |diag| over own active rows
+        uint64_t key = piv ? 0ull : mkkey(dg, (uint32_t)i);
+        key = warp_max64(key);
+        if (lane == 0) red[wid] = key;
+        __syncthreads();
+        // ---- B: publish
+        if (wid == 0) {
+            uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
+            v = warp_max64(v);
+            float *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * nb;
+            if (v) {
+                const int lr = (int)((int64_t)(POS_MAX - (uint32_t)((v >> 15) & POS_MAX)) - r0);
+                for (int u = lane; u < t; u += 32) mb[u] = sneg[(size_t)u * a.R + lr];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (v) red_max_u64(&a.keys[t], v);
+                red_release_add(a.cnt, 1u);
+            }
+        }
+        // ---- C: deferred global stores of step t-1
+        if (pend) {
+            a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+            a.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            pend = false;
+        }
+        PH(0)
+        // ---- D: wait for all CTAs, read the winning key
+        if (tid == 0) {
+            const unsigned int want = (unsigned int)G * (unsigned int)(t + 1);
+            while (ld_acquire_u32(a.cnt) < want) {
+            }
+            bkey = ld_relaxed_u64(&a.keys[t]);
+        }
+        __syncthreads();
+        const uint64_t bk = bkey;
+        PH(1)
+        const float absd = __uint_as_float((uint32_t)(bk >> 32));
+        const int64_t P = (int64_t)(POS_MAX - (uint32_t)((bk >> 15) & POS_MAX));
+        const float d = ((bk >> 14) & 1) ? -absd : absd;
+        // ---- E: [R4] stop test, ratio evaluated in FP64, strict
+        const bool stop = (k == 0) ? (absd == 0.f)
+                                   : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev)));
+        if (stop) {
+            if (blockIdx.x == 0 && tid == 0) {
+                a.status[0] = (int32_t)k;
+                a.status[1] = t;
+                a.status[2] = 1;
+            }
+            stopped = true;
+            break;
+        }
+        const float sg = d > 0.f ? 1.f : -1.f;
+        // ---- F: [R6] pivot row from the winner's mailbox, stale column for own rows
+        {
+            const int owner = (int)(P / a.R);
+            const float *mb = a.mbox + ((size_t)(t & 1) * G + owner) * nb;
+            for (int u = tid; u < t; u += nthr) sp[u] = -sgm[u] * mb[u];   // s_P^u (exact sign flip)
+            if (tid == 0) sgm[t] = sg;
+        }
+        float v = 0.f;
+        if (!piv && i != P) v = (i >= P) ? a.V[i + P * a.ldv] : a.V[P + i * a.ldv];
+        __syncthreads();
+        PH(2)
+        // ---- G: column, scaled column, lazy diagonal
+        const float r = __fsqrt_rn(absd);               // [R7]
+        if (has && i == P) {
+            piv = true;
+            a.Dk[k] = d;                                // the owner records the pivot (no loads)
+            a.pivorig[k] = oi;
+            a.pivpos[t] = (int32_t)P;
+            a.sigma[t] = sg;
+        } else if (!piv) {
+            float c = v;
+            const float *sn = sneg + tid;
+            int u = 0;
+            for (; u + 8 <= t; u += 8) {                 // [R8] one fmaf per earlier pivot, in order
+                float x[8], y[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    x[q] = sn[(size_t)(u + q) * a.R];
+                    y[q] = sp[u + q];
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c = __fmaf_rn(x[q], y[q], c);
+            }
+            for (; u < t; ++u) c = __fmaf_rn(sn[(size_t)u * a.R], sp[u], c);
+            const float sv = __fdiv_rn(c, r);
+            const float ns = -sg * sv;                  // exact
+            sneg[(size_t)t * a.R + tid] = ns;
+            ps = sv;
+            pl = __fdiv_rn(c, d);                       // [R10] L = c / d
+            pend = true;
+            dg = __fmaf_rn(ns, sv, dg);                 // lazy diagonal, same fma as the update
+        }
+        dprev = d;
+        PH(3)
+    }
+    if (pend) {   // flush the last step's values
+        a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+        a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+    }
+    if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
+    if (dbg) {
+        for (int q = 0; q < 4; ++q) a.dbg[q] += ph[q];
+        a.dbg[4] += t;
+    }
+#undef PH
+}
+
+// ------------------------------------------------------------------ compaction
+// map[j'] = old position of the j'-th surviving index (stable), norig likewise.
+__global__ void k_compact(int64_t m, int nbp, const int32_t *__restrict__ pivpos,
+                          const int32_t *__restrict__ orig, int32_t *__restrict__ map,
+                          int32_t *__restrict__ norig, const int32_t *status) {
+    __shared__ int32_t srt[1024];
+    if (status[2]) return;
+    for (int q = threadIdx.x; q < nbp; q += blockDim.x) {
+        const int32_t v = pivpos[q];
+        int rk = 0;
+        for (int w = 0; w < nbp; ++w) rk += (pivpos[w] < v);
+        srt[rk] = v;
+    }
+    __syncthreads();
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nbp;   // count of pivots < p
+        while (lo < hi) {
+            int md = (lo + hi) >> 1;
+            if (srt[md] < p) lo = md + 1; else hi = md;
+        }
+        const bool isp = lo < nbp && srt[lo] == p;
+        if (!isp) {
+            map[p - lo] = (int32_t)p;
+            norig[p - lo] = orig[p];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ trailing update
+struct TrailArgs {
+    int64_t mp;            // new active size
+    int nbp;               // pivots in the panel
+    const float *Vold;
+    float *Vnew;
+    int64_t ldv;
+    const int32_t *map;    // new position -> old position
+    const float *S;        // S[old + t*lds]
+    int64_t lds;
+    const float *sigma;
+    const int32_t *status;
+};
+
+constexpr int TB = 128;    // CTA tile
+constexpr int TK = 8;      // k chunk
+
+__global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
+    if (a.status[2]) return;
+    __shared__ __align__(16) float As[2][TK][TB];
+    __shared__ __align__(16) float Bs[2][TK][TB];
+    __shared__ int32_t rmap[TB], cmap[TB];
+    __shared__ float sgm[256];
+
+    const int64_t t = blockIdx.x;
+    int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int64_t bj = t - bi * (bi + 1) / 2;
+    const int64_t row0 = bi * TB, col0 = bj * TB;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+
+    if (tid < TB) {
+        rmap[tid] = (row0 + tid < a.mp) ? a.map[row0 + tid] : -1;
+        cmap[tid] = (col0 + tid < a.mp) ? a.map[col0 + tid] : -1;
+    }
+    for (int q = tid; q < a.nbp; q += 256) sgm[q] = -a.sigma[q];
+    __syncthreads();
+
+    // accumulators seeded from the current values (compaction fused in the gather)
+    float acc[8][8];
+#define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
+#define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int32_t cm = cmap[CC(b)];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int32_t rm = rmap[RR(q)];
+            acc[q][b] = (cm >= 0 && rm >= 0 && rm >= cm) ? a.Vold[(int64_t)rm + (int64_t)cm * a.ldv] : 0.f;
+        }
+    }
+
+    // global -> register staging: each thread loads 4 A and 4 B elements per chunk
+    const int lr = tid & 127, lk = tid >> 7;   // element (row lr, k = lk + 2*q)
+    const int32_t arow = rmap[lr], bcol = cmap[lr];
+    float ra[4], rb[4];
+    auto gload = [&](int t0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kk = lk + 2 * q;
+            const int tt = t0 + kk;
+            const bool ok = tt < a.nbp;
+            ra[q] = (ok && arow >= 0) ? a.S[(int64_t)arow + (int64_t)tt * a.lds] : 0.f;
+            rb[q] = (ok && bcol >= 0) ? a.S[(int64_t)bcol + (int64_t)tt * a.lds] : 0.f;
+        }
+    };
+    auto sstore = [&](int buf, int t0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kk = lk + 2 * q;
+            const int tt = min(t0 + kk, a.nbp - 1);
+            As[buf][kk][lr] = sgm[tt] * ra[q];      // -sigma_t s_i^t (exact)
+            Bs[buf][kk][lr] = rb[q];
+        }
+    };
+
+    gload(0);
+    sstore(0, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int t0 = 0; t0 < a.nbp; t0 += TK) {
+        const bool more = t0 + TK < a.nbp;
+        if (more) gload(t0 + TK);
+        const int kmax = min(TK, a.nbp - t0);
+        if (kmax == TK) {
+#pragma unroll
+            for (int kk = 0; kk < TK; ++kk) {
+                const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][tx * 4]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + tx * 4]);
+                const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + ty * 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[q][b] = __fmaf_rn(av[q], bv[b], acc[q][b]);
+            }
+        } else {
+            for (int kk = 0; kk < kmax; ++kk) {
+                float av[8], bv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    av[q] = As[buf][kk][RR(q)];
+                    bv[q] = Bs[buf][kk][CC(q)];
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[q][b] = __fmaf_rn(av[q], bv[b], acc[q][b]);
+            }
+        }
+        if (more) {
+            sstore(buf ^ 1, t0 + TK);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+
+    // store the lower triangle of the new trailing matrix
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int64_t c = col0 + CC(b);
+        if (c >= a.mp) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t r = row0 + RR(q);
+            if (r < a.mp && r >= c) a.Vnew[r + c * a.ldv] = acc[q][b];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ factor gather
+// Lfac[a + k*N] = Lorig[pivorig[a] + k*ldl] (a > k), 1 (a == k), 0 (a < k)
+__global__ void k_gather_L(int64_t N, const int32_t *__restrict__ pivorig, const float *__restrict__ Lorig,
+                           int64_t ldl, float *__restrict__ Lfac, int64_t ldf) {
+    for (int64_t k = blockIdx.x; k < N; k += gridDim.x) {
+        const float *src = Lorig + k * ldl;
+        float *dst = Lfac + k * ldf;
+        for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
+            float v = 0.f;
+            if (r == k) v = 1.f;
+            else if (r > k) v = src[pivorig[r]];
+            dst[r] = v;
+        }
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host driver
+void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                    hf_lowfactor *lf) {
+    cudaStream_t st = ctx->stream;
+    const int nsm = ctx->num_sms;
+    lf->L = L;
+    lf->stream = st;
+    if (L == 0) {
+        lf->N = lf->Ntau = lf->n2 = 0;
+        return;
+    }
+    HF_REQUIRE(L <= (int64_t)POS_MAX - 1, "L too large for the 17-bit position key");
+
+    // panel width: the chain keeps R x nb floats per CTA in shared memory
+    int maxsmem = 0;
+    HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    cudaFuncAttributes fa;
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain));
+    maxsmem -= (int)fa.sharedSizeBytes;
+    const int64_t G0 = std::min<int64_t>(nsm, std::max<int64_t>(1, cdiv(L, 32)));
+    const int64_t R0 = cdiv(L, G0);
+    HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
+    int nb = o.nb > 0 ? o.nb : 256;
+    while (nb > 8 && (int64_t)(nb * R0 + 2 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
+    HF_REQUIRE(nb >= 8 && nb <= 1024, "panel width out of range");
+
+    DBuf<float> V[2];
+    V[0].alloc((size_t)L * L, st);
+    V[1].alloc((size_t)L * L, st);
+    DBuf<int32_t> orig[2], map;
+    orig[0].alloc(L, st);
+    orig[1].alloc(L, st);
+    map.alloc(L, st);
+    DBuf<float> S, sigma, Lorig, Dk;
+    S.alloc((size_t)L * nb, st);
+    sigma.alloc(nb, st);
+    Lorig.alloc((size_t)L * L, st);
+    Dk.alloc(L, st);
+    DBuf<int32_t> pivpos, pivorig, status;
+    pivpos.alloc(nb, st);
+    pivorig.alloc(L, st);
+    status.alloc(4, st);
+    // per-launch exchange state: keys[nb] + counter, zeroed before every chain launch
+    DBuf<unsigned long long> xchg;
+    xchg.alloc((size_t)nb + 2, st);
+    DBuf<float> mbox;
+    mbox.alloc((size_t)2 * nsm * nb, st);
+    HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
+
+    {
+        ClassTimer tm(ctx, "other");
+        k_cast_lower<<<(unsigned)std::min<int64_t>(L, 65535), 256, 0, st>>>(L, K, ld, V[0].p, L);
+        HF_CHECK_LAUNCH(ctx);
+        k_iota32<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
+        HF_CHECK_LAUNCH(ctx);
+    }
+
+    HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    DBuf<unsigned long long> dbg;
+    const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
+    if (want_dbg) {
+        dbg.alloc(8, st);
+        dbg.zero(st);
+    }
+    int cur = 0;
+    int64_t m = L, K0 = 0;
+    while (m > 0) {
+        const int nbp = (int)std::min<int64_t>(nb, m);
+        const int64_t G = std::min<int64_t>(nsm, std::max<int64_t>(1, cdiv(m, 32)));
+        const int64_t R = cdiv(m, G);
+        const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
+        const size_t shm = ((size_t)nbp * R + 2 * nbp) * sizeof(float);
+        HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
+        ChainArgs ca;
+        ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
+        ca.V = V[cur].p; ca.ldv = L; ca.orig = orig[cur].p;
+        ca.S = S.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
+        ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
+        ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
+        ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
+        {
+            ClassTimer tm(ctx, "chain");
+            void *args[] = {&ca};
+            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            HF_CHECK_LAUNCH(ctx);
+        }
+        const int64_t mp = m - nbp;
+        if (mp > 0) {
+            {
+                ClassTimer tm(ctx, "other");
+                k_compact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
+                    m, nbp, pivpos.p, orig[cur].p, map.p, orig[cur ^ 1].p, status.p);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            TrailArgs ta;
+            ta.mp = mp; ta.nbp = nbp; ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p; ta.ldv = L;
+            ta.map = map.p; ta.S = S.p; ta.lds = L; ta.sigma = sigma.p; ta.status = status.p;
+            const int64_t T = cdiv(mp, TB);
+            {
+                ClassTimer tm(ctx, "trailing");
+                k_trailing<<<(unsigned)(T * (T + 1) / 2), 256, 0, st>>>(ta);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            cur ^= 1;
+        }
+        K0 += nbp;
+        m = mp;
+    }
+    int32_t hs[4];
+    HF_CUDA(cudaMemcpyAsync(hs, status.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HF_CUDA(cudaStreamSynchronize(st));
+    const int64_t Ntau = hs[2] ? hs[0] : L;
+    if (want_dbg) {
+        unsigned long long hd[8];
+        HF_CUDA(cudaMemcpy(hd, dbg.p, sizeof(hd), cudaMemcpyDeviceToHost));
+        const double np = hd[4] ? (double)hd[4] : 1.0;
+        fprintf(stderr, "[hf chain] steps %llu  us/step: publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
+                hd[4], hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
+    }
+    // [R5] floor and [R9] enlargement: the last accepted pivots move to Lambda_2
+    int64_t N = Ntau;
+    if (L - o.n_min < N) N = std::max<int64_t>(0, L - o.n_min);
+    if (N < L) N = std::max<int64_t>(0, N - o.n_extra);
+    lf->Ntau = Ntau;
+    lf->N = N;
+    lf->n2 = L - N;
+
+    // [R10] Pi = [pivots, Lambda_2 ascending]
+    std::vector<int32_t> po(std::max<int64_t>(N, 1));
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(po.data(), pivorig.p, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    lf->h_D.assign(std::max<int64_t>(N, 1), 0.f);
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->h_D.data(), Dk.p, N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    HF_CUDA(cudaStreamSynchronize(st));
+    lf->h_D.resize(N);
+    std::vector<int32_t> rank(L, -1);
+    lf->h_perm.resize(L);
+    for (int64_t k = 0; k < N; ++k) {
+        lf->h_perm[k] = po[k];
+        rank[po[k]] = (int32_t)k;
+    }
+    int64_t w = N;
+    for (int64_t i = 0; i < L; ++i)
+        if (rank[i] < 0) lf->h_perm[w++] = i;
+
+    lf->perm.alloc(L, st);
+    lf->pos1.alloc(L, st);
+    HF_CUDA(cudaMemcpyAsync(lf->perm.p, lf->h_perm.data(), L * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    HF_CUDA(cudaMemcpyAsync(lf->pos1.p, rank.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    lf->D.alloc(std::max<int64_t>(N, 1), st);
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->D.p, Dk.p, N * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    lf->Lfac.alloc((size_t)std::max<int64_t>(N, 1) * std::max<int64_t>(N, 1), st);
+    if (N > 0) {
+        ClassTimer tm(ctx, "other");
+        k_gather_L<<<(unsigned)std::min<int64_t>(N, 65535), 256, 0, st>>>(N, pivorig.p, Lorig.p, L, lf->Lfac.p, N);
+        HF_CHECK_LAUNCH(ctx);
+    }
+    // host vectors used by the copies above must outlive them
+    HF_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace hf

@@ -1,0 +1,308 @@
+"""Thin ctypes binding of libhf.so (include/hf.h).  Argument marshalling only:
+every step of the path runs in the CUDA kernels behind the C ABI.  There is
+no CPU fallback -- if libhf.so is missing or a call fails, this raises.
+
+Matrices cross the boundary as column-major device buffers.  A contiguous
+torch tensor T of shape (n, m) is the column-major m x n matrix T^T; for the
+symmetric K that distinction vanishes.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhf.so")
+
+HF_OK, HF_ERR_INVALID_ARG, HF_ERR_CUDA, HF_ERR_NCCL, HF_ERR_OOM = 0, 1, 2, 3, 4
+HF_ERR_NOT_CONVERGED, HF_ERR_BREAKDOWN, HF_ERR_STATE = 5, 6, 7
+_NAMES = {0: "HF_OK", 1: "HF_ERR_INVALID_ARG", 2: "HF_ERR_CUDA", 3: "HF_ERR_NCCL", 4: "HF_ERR_OOM",
+          5: "HF_ERR_NOT_CONVERGED", 6: "HF_ERR_BREAKDOWN", 7: "HF_ERR_STATE"}
+
+EXPORTED = [
+    "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
+    "hf_set_profiling", "hf_kernel_stats", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
+    "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
+    "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy",
+]
+
+
+class HFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lowprec_opts(ctypes.Structure):
+    _fields_ = [("tau", ctypes.c_double), ("n_extra", ctypes.c_int64), ("n_min", ctypes.c_int64),
+                ("nb", ctypes.c_int32)]
+
+
+class gcr_opts(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32)]
+
+
+class gcr_info(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("max_rel_res_recursive", ctypes.c_double),
+                ("max_rel_res_true", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libhf.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: run `python -m paper_2208_01907_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    pi64, pdbl = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)
+    sig = {
+        "hf_create": [ctypes.c_int, vp, ctypes.POINTER(vp)],
+        "hf_create_dist": [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+        "hf_nccl_unique_id": [vp],
+        "hf_destroy": [vp],
+        "hf_set_profiling": [vp, ctypes.c_int],
+        "hf_kernel_stats": [vp, ctypes.c_char_p, pdbl, pi64],
+        "hf_launch_count": [vp, pi64],
+        "hf_scale": [vp, i64, vp, i64, vp],
+        "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
+        "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
+        "hf_lowfactor_destroy": [vp],
+        "hf_schur_gcr": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp,
+                         ctypes.POINTER(gcr_info)],
+        "hf_hybrid_export": [vp, vp, vp, i64, vp, i64],
+        "hf_factor_hard": [vp, vp, dbl, pi64],
+        "hf_hard_export": [vp, vp, vp, vp, pi64],
+        "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
+        "hf_hybrid_destroy": [vp],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.hf_last_error.argtypes = [vp]
+    L.hf_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _dev(t: torch.Tensor, dtype) -> None:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise TypeError(f"expected a contiguous CUDA {dtype} tensor")
+
+
+class Context:
+    """hf_ctx: one CUDA device + stream (+ optional NCCL communicator)."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 nccl_id: bytes | None = None, rank: int = 0, nranks: int = 1):
+        self.lib = load()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        if nccl_id is None:
+            st = self.lib.hf_create(device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        else:
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            st = self.lib.hf_create_dist(device, ctypes.c_void_p(self.stream.cuda_stream), buf, rank,
+                                         nranks, ctypes.byref(h))
+        if st != HF_OK:
+            msg = self.lib.hf_last_error(h if h.value else None).decode()
+            if h.value:
+                self.lib.hf_destroy(h)
+            raise HFError(st, msg)
+        self.h = h
+
+    def check(self, st: int, accept=()):
+        if st != HF_OK and st not in accept:
+            raise HFError(st, self.lib.hf_last_error(self.h).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.hf_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # instrumentation
+    def set_profiling(self, on: bool):
+        self.check(self.lib.hf_set_profiling(self.h, int(bool(on))))
+
+    def kernel_stats(self, cls: str):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self.check(self.lib.hf_kernel_stats(self.h, cls.encode(), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        self.check(self.lib.hf_launch_count(self.h, ctypes.byref(n)))
+        return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = load().hf_nccl_unique_id(buf)
+    if st != HF_OK:
+        raise HFError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+# ---------------------------------------------------------------------- a1
+def hf_scale(ctx: Context, K: torch.Tensor) -> torch.Tensor:
+    """In-place diagonal scaling; returns q (device FP64[L])."""
+    _dev(K, torch.float64)
+    L = K.shape[0]
+    q = torch.empty(L, dtype=torch.float64, device=K.device)
+    ctx.check(ctx.lib.hf_scale(ctx.h, L, _ptr(K), L, _ptr(q)))
+    return q
+
+
+# ---------------------------------------------------------------------- a2-a3
+class LowFactor:
+    def __init__(self, ctx: Context, h, L: int, N: int, n2: int, n2_tau: int):
+        self.ctx, self.h, self.L, self.N, self.n2, self.n2_tau_only = ctx, h, L, N, n2, n2_tau
+
+    def export(self, with_L: bool = True):
+        """(perm np.int64[L], D np.float32[N], Lfac device float32 N x N (matrix view))."""
+        perm = np.empty(self.L, dtype=np.int64)
+        D = np.empty(max(self.N, 1), dtype=np.float32)
+        Lf = None
+        if with_L and self.N > 0:
+            Lf = torch.empty(self.N, self.N, dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        self.ctx.check(self.ctx.lib.hf_lowfactor_export(self.ctx.h, self.h, _ptr(perm), _ptr(D),
+                                                        _ptr(Lf), self.N))
+        return perm, D[: self.N], (Lf.T if Lf is not None else None)
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            self.ctx.lib.hf_lowfactor_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hf_factor_lowprec(ctx: Context, K: torch.Tensor, tau: float = 1e-2, n_extra: int = 0,
+                      n_min: int = 0, nb: int = 0) -> LowFactor:
+    _dev(K, torch.float64)
+    L = K.shape[0]
+    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb))
+    h = ctypes.c_void_p()
+    N, n2, n2t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.hf_factor_lowprec(ctx.h, L, _ptr(K), L, ctypes.byref(o), ctypes.byref(h),
+                                        ctypes.byref(N), ctypes.byref(n2), ctypes.byref(n2t)))
+    return LowFactor(ctx, h, L, N.value, n2.value, n2t.value)
+
+
+# ---------------------------------------------------------------------- a4-a7
+@dataclass
+class GcrInfo:
+    iters: int
+    max_rel_res_recursive: float
+    max_rel_res_true: float
+    status: int = HF_OK
+
+
+class Hybrid:
+    def __init__(self, ctx: Context, h, lf: LowFactor, K: torch.Tensor):
+        self.ctx, self.h, self.lf, self.K = ctx, h, lf, K    # keeps K alive (borrowed)
+        self.kernel_dim = None
+
+    @property
+    def n2(self):
+        return self.lf.n2
+
+    def export(self):
+        """(X device FP64 N x n2 matrix view, S22 device FP64 n2 x n2 matrix view)."""
+        N, n2 = self.lf.N, self.lf.n2
+        dev = f"cuda:{self.ctx.device}"
+        X = torch.empty(max(n2, 1), max(N, 1), dtype=torch.float64, device=dev)
+        S = torch.empty(max(n2, 1), max(n2, 1), dtype=torch.float64, device=dev)
+        self.ctx.check(self.ctx.lib.hf_hybrid_export(self.ctx.h, self.h, _ptr(X), max(N, 1), _ptr(S),
+                                                     max(n2, 1)))
+        return X[:n2, :N].T, S[:n2, :n2].T
+
+    def hard_export(self):
+        n2 = self.lf.n2
+        p = np.zeros(max(n2, 1), dtype=np.int64)
+        b = np.zeros(max(n2, 1), dtype=np.int32)
+        r = ctypes.c_int64()
+        self.ctx.check(self.ctx.lib.hf_hard_export(self.ctx.h, self.h, _ptr(p), _ptr(b), ctypes.byref(r)))
+        return p[:n2], b[:n2], r.value
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            self.ctx.lib.hf_hybrid_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-14, max_iter: int = 100,
+                 want_S22_host: bool = False, accept_failure: bool = False):
+    """Returns (Hybrid, GcrInfo, S22 host np.ndarray or None)."""
+    _dev(K, torch.float64)
+    o = gcr_opts(float(tol), int(max_iter))
+    info = gcr_info()
+    h = ctypes.c_void_p()
+    S = np.empty((lf.n2, lf.n2), dtype=np.float64, order="F") if (want_S22_host and lf.n2) else None
+    st = ctx.lib.hf_schur_gcr(ctx.h, _ptr(K), K.shape[0], lf.h, ctypes.byref(o), ctypes.byref(h),
+                              _ptr(S), ctypes.byref(info))
+    ok = (HF_ERR_NOT_CONVERGED, HF_ERR_BREAKDOWN) if accept_failure else ()
+    ctx.check(st, ok)
+    gi = GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true, st)
+    return Hybrid(ctx, h, lf, K), gi, S
+
+
+def hf_factor_hard(ctx: Context, hy: Hybrid, eps_ker: float = 1e-10) -> int:
+    kd = ctypes.c_int64()
+    ctx.check(ctx.lib.hf_factor_hard(ctx.h, hy.h, float(eps_ker), ctypes.byref(kd)))
+    hy.kernel_dim = kd.value
+    return kd.value
+
+
+def hf_solve(ctx: Context, hy: Hybrid, b: torch.Tensor, x: torch.Tensor | None = None):
+    """Alg. 2 on the scaled system; b, x device FP64[L].  Returns (x, GcrInfo)."""
+    _dev(b, torch.float64)
+    if x is None:
+        x = torch.empty_like(b)
+    info = gcr_info()
+    ctx.check(ctx.lib.hf_solve(ctx.h, hy.h, _ptr(b), _ptr(x), ctypes.byref(info)))
+    return x, GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true)

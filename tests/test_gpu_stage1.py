@@ -1,0 +1,101 @@
+"""GPU parity of steps a1-a3 (scaling + FP32 factorization with postponing)
+against the oracle: bitwise on q, K, Pi, Lambda_2, D and L ([R1]-[R10])."""
+import numpy as np
+import pytest
+import torch
+
+import hf_inputs as hi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+def _run(ctx, Kb_t, tau, n_min=0, n_extra=0, nb=0):
+    from paper_2208_01907_b200 import hf
+    Kd = Kb_t.to("cuda").contiguous()
+    q = hf.hf_scale(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=tau, n_min=n_min, n_extra=n_extra, nb=nb)
+    perm, D, Lf = lf.export()
+    return Kd, q, lf, perm, D, Lf
+
+
+CASES = [("C0", s) for s in range(6)] + [("P64", 0), ("N16", 0), ("N32", 0), ("S12", 0), ("S24", 0),
+                                         ("P512", 0), ("P1024", 0)]
+
+
+@pytest.mark.parametrize("name,seed", CASES)
+def test_stage1_bitwise(ctx, name, seed):
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, qo = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    Kd, q, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min)
+    assert np.array_equal(q.cpu().numpy(), qo)
+    assert np.array_equal(Kd.cpu().numpy(), Ko)            # symmetric: layout-free
+    assert lf.N == Fo.N and lf.L - lf.n2_tau_only == Fo.Ntau
+    assert np.array_equal(perm, Fo.perm)
+    assert np.array_equal(D, Fo.D)
+    if Fo.N:
+        assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+
+
+@pytest.mark.parametrize("nb", [8, 16, 64, 128])
+def test_stage1_panel_width_invariance(ctx, nb):
+    """Panel width changes the blocking, never the bits (canonical order [R8])."""
+    spec = hi.CONFIGS["P512"]
+    Kb = hi.make_kbar("P512", 3)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    _, _, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min, nb=nb)
+    assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+    assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+
+
+def test_stage1_edge_cases(ctx):
+    from paper_2208_01907_b200 import hf
+    # first pivot 0 -> everything postponed
+    _, _, lf, perm, D, _ = _run(ctx, torch.tensor([[0.0, 1.0], [1.0, 0.0]], dtype=torch.float64), 1e-2)
+    assert lf.N == 0 and list(perm) == [0, 1]
+    # diag(1, 0.9, 1e-9), tau 0.05 -- factor the matrix as given (no scaling)
+    lf = hf.hf_factor_lowprec(ctx, torch.diag(torch.tensor([1.0, 0.9, 1e-9], dtype=torch.float64)).cuda(),
+                              tau=0.05)
+    perm, D, _ = lf.export()
+    assert lf.N == 2 and list(perm) == [0, 1, 2] and list(D) == [1.0, np.float32(0.9)]
+    # 1 x 1
+    _, _, lf, perm, D, Lf = _run(ctx, torch.tensor([[-3.0]], dtype=torch.float64), 1e-2)
+    assert lf.N == 1 and D[0] == -1.0
+    # enlargement and floor together
+    Kb = hi.make_kbar("P64", 1)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, 1e-2, n_min=5, n_extra=3)
+    _, _, lf, perm, D, Lf = _run(ctx, Kb, 1e-2, n_min=5, n_extra=3)
+    assert lf.N == Fo.N and np.array_equal(perm, Fo.perm) and np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+    # bad tau
+    with pytest.raises(hf.HFError):
+        hf.hf_factor_lowprec(ctx, torch.eye(3, dtype=torch.float64, device="cuda"), tau=1.5)
+    # NaN in K
+    bad = torch.eye(4, dtype=torch.float64, device="cuda")
+    bad[2, 1] = bad[1, 2] = float("nan")      # symmetric: hf_scale reads the lower triangle
+    with pytest.raises(hf.HFError):
+        hf.hf_scale(ctx, bad)
+
+
+def test_stage1_c1_full_size(ctx):
+    """Config 1 (L=4096) at full size, bitwise against the oracle."""
+    spec = hi.CONFIGS["C1"]
+    Kb = hi.make_kbar("C1", 0)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    _, _, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min)
+    assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+    assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
