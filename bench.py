@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py -- hybrid LDU factor + Schur (Alg. 1 of arXiv 2208.01907) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl hf|reference]
+
+One STEP = one pass of the whole hot path over one
+synthetic matrix already resident in HBM:
+    restore Kbar (D2D copy, the scaling is in place) -> hf_scale ->
+    hf_factor_lowprec -> hf_schur_gcr -> hf_factor_hard
+Inputs are larger than L2 (K is 2.1 GB at C2), so no L2 flush is needed.
+The metric is BASELINE.json's "hybrid LDU factor+Schur time (s), TFLOP/s":
+value = algorithmic TFLOP/s of the whole job (DESIGN.md section 7 gives the
+flop model), with seconds per factorization alongside.
+
+N > 1 (torchrun): replicas -- every rank factorises its own seeded matrix, no
+data-path collective; weak scaling, max-over-ranks time.
+
+--impl reference: the CPU oracle (oracle/, plain C + numpy) timed on the
+host cores on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FFMA_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12     # TFLOP/s, B200 FP32 non-tensor
+DMMA_PEAK_MEASURED = 37.15                              # tools/peaks.py, profiles/peaks_r01.json
+
+
+def flop_model(L, N, Ntau, n2, iters):
+    """Algorithmic flops of one hybrid factorization."""
+    m = np.arange(L, L - Ntau, -1, dtype=np.float64)          # active size before each pivot
+    f1 = float(np.sum((m - 1.0) * m))                          # rank-1 updates of the lower triangle
+    mv = 2.0 * N * N * n2                                      # K11 W
+    pc = 2.0 * N * N * n2                                      # FP32 fwd + bwd triangular solves
+    gram = sum(2.0 * N * n2 * n2 * (4 + 3 * (n + 1)) for n in range(iters))
+    f2 = (iters + 2) * mv + (iters + 1) * pc + gram
+    f3 = 2.0 * N * n2 * n2
+    f4 = n2 ** 3 / 3.0
+    return {"stage1": f1, "gcr": f2, "schur": f3, "hard": f4, "total": f1 + f2 + f3 + f4}
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.stop = index, [], threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                    "-i", str(self.index)], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                mhz.append(float(s[0]))
+                mx = float(s[1])
+                for nm, v in zip(names, s[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(mhz)) if mhz else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the roofline kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(Kb_np, spec, pivots=1024):
+    """The oracle as it stands on a bounded sample of the same workload:
+    its stage 1 for the first `pivots` pivots of the config's matrix, plus one
+    block-GCR iteration's FP64 mat-vec and FP32 preconditioner solves at the
+    config's sizes.  Returns (flops, seconds, description)."""
+    import oracle
+    L = Kb_np.shape[0]
+    t0 = time.perf_counter()
+    K, q = oracle.scale(Kb_np)
+    t1 = time.perf_counter()
+    F = oracle.factor_lowprec(K, spec.tau, n_min=spec.n_min, max_steps=pivots)
+    t2 = time.perf_counter()
+    done = F.Ntau
+    m = np.arange(L, L - done, -1, dtype=np.float64)
+    f_st1 = float(np.sum((m - 1.0) * m))
+    # one GCR iteration worth of oracle kernels on operands of the config's sizes
+    n2 = max(spec.n_min, 4)
+    N = L - n2
+    rng = np.random.default_rng(0)
+    W = rng.standard_normal((N, n2))
+    Lf = np.tril(rng.standard_normal((N, N)).astype(np.float32) * (1.0 / N), -1) + np.eye(N, dtype=np.float32)
+    Fs = oracle.LowFactor(L=N, N=N, Ntau=N, perm=np.arange(N), D=np.ones(N, np.float32),
+                          Lfac=np.asfortranarray(Lf), dtype=np.float32)
+    K11 = K[:N, :N]
+    t3 = time.perf_counter()
+    Z = K11 @ W
+    E = oracle.precond_apply(Fs, Z)
+    t4 = time.perf_counter()
+    del E
+    f_it = 2.0 * N * N * n2 * 2
+    secs = (t1 - t0) + (t2 - t1) + (t4 - t3)
+    desc = (f"oracle scale + stage 1 (first {done} pivots of {spec.name}, L={L}) + one block-GCR "
+            f"iteration's K11 W and FP32 preconditioner at N={N}, n2={n2}")
+    return f_st1 + f_it, secs, desc
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="hf", choices=["hf", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pivots-sample", type=int, default=1024)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import hf_inputs as hi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = hi.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        Kb = hi.make_kbar(spec, args.seed, device="cuda" if (torch.cuda.is_available() and spec.L > 4096) else "cpu")
+        Kb = Kb.cpu().numpy()
+        for _ in range(args.warmup):
+            oracle_sample(Kb, spec, pivots=max(16, args.pivots_sample // 16))
+        fl, sec = 0.0, 0.0
+        desc = ""
+        for _ in range(args.steps):
+            f, s_, desc = oracle_sample(Kb, spec, pivots=args.pivots_sample // 4)
+            fl += f
+            sec += s_
+        v = fl / sec / 1e12
+        line = {"metric": "hybrid_factor_schur_tflops", "value": v, "unit": "TFLOP/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "fp32+fp64", "data": "synthetic",
+                "config": {"workload": spec.name, "L": spec.L, "tau": spec.tau, "n_min": spec.n_min,
+                           "seed": args.seed, "parallelism": "none (host cores)"},
+                "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": host_cores(), "kind": "oracle",
+                                 "sample": desc},
+                "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    from paper_2208_01907_b200 import hf
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = hf.Context(local, stream)
+
+    # ---- the workload (seeded, synthetic; each rank its own seed in replica mode)
+    gen_dev = "cuda" if spec.L > 4096 else "cpu"
+    Kb = hi.make_kbar(spec, args.seed + rank, device=gen_dev).to(dev).contiguous()
+    K = torch.empty_like(Kb)
+    torch.cuda.synchronize()
+
+    def step(profile=False):
+        K.copy_(Kb)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        hf.hf_scale(ctx, K)
+        ev[1].record(stream)
+        lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)
+        ev[2].record(stream)
+        hy, info, _ = hf.hf_schur_gcr(ctx, K, lf)
+        ev[3].record(stream)
+        kd = hf.hf_factor_hard(ctx, hy)
+        ev[4].record(stream)
+        return lf, hy, info, kd, ev
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ctx.set_profiling(True)
+    for c in ("scale", "chain", "trailing", "dgemm", "trsm", "hard", "other"):
+        ctx.kernel_stats(c)            # drain the warm-up records
+    base = {c: ctx.kernel_stats(c) for c in ("scale", "chain", "trailing", "dgemm", "trsm", "hard", "other")}
+    launches0 = ctx.launch_count()
+    stage_ms = np.zeros(4)
+    results = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            lf, hy, info, kd, ev = step()
+            results.append((lf.N, lf.L - lf.n2_tau_only, lf.n2, info.iters, kd, info.max_rel_res_true))
+            for q in range(4):
+                stage_ms[q] += ev[q].elapsed_time(ev[q + 1]) if ev[q + 1].query() else 0.0
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = t_start.elapsed_time(t_end)             # ms, this rank
+    launches = ctx.launch_count() - launches0
+    ctx.set_profiling(False)
+    kstats = {c: ctx.kernel_stats(c) for c in base}
+    kms = {c: (kstats[c][0] - base[c][0]) / args.steps for c in base}
+    klaunch = {c: (kstats[c][1] - base[c][1]) / args.steps for c in base}
+
+    N, Ntau, n2, iters, kd, tres = results[-1]
+    L = spec.L
+    fm = flop_model(L, N, Ntau, n2, iters)
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    ms_step = elapsed / args.steps
+    total_flops = fm["total"] * world
+    value = total_flops / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant compute kernel (the FP32 trailing update)
+    tr_ms = kms["trailing"]
+    achieved = fm["stage1"] / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else None
+    traffic = load_traffic()
+    roof = {"kernel": "k_trailing (FP32 FFMA symmetric rank-nb update, bitwise canonical order)",
+            "bound": "alu", "achieved": achieved, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
+            "frac": (achieved / FFMA_PEAK_DERIVED) if achieved else None,
+            "peak_source": "derived 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md sec. 7); "
+                           "microbenchmark 72.6 FFMA / 74.3 FFMA2 TF/s (profiles/peaks_r01.json)",
+            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "traffic_note": traffic.get("note") if traffic else "no ncu capture committed yet",
+            "ms_per_step": tr_ms, "launches_per_step": klaunch["trailing"]}
+    dg_ms = kms["dgemm"]
+    shares = {c: round(kms[c] / ms_step, 4) for c in kms}
+
+    line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32+fp64", "data": "synthetic",
+            "config": {"workload": spec.name, "L": L, "N": N, "n2": n2, "n2_tau_only": L - Ntau,
+                       "tau": spec.tau, "n_min": spec.n_min, "seed": args.seed, "gcr_iters": iters,
+                       "kernel_dim": kd, "gcr_true_rel_res": tres,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (K fp64 %.2f GB); restore copy of Kbar inside each step" %
+                             (8 * L * L / 1e9)},
+            "seconds_per_factorization": ms_step / 1e3,
+            "stage_ms": {"scale": stage_ms[0] / args.steps, "lowprec": stage_ms[1] / args.steps,
+                         "schur_gcr": stage_ms[2] / args.steps, "hard": stage_ms[3] / args.steps},
+            "flops_per_step": fm,
+            "kernel_ms_per_step": kms, "kernel_share": shares,
+            "chain_us_per_pivot": kms["chain"] * 1e3 / max(Ntau, 1),
+            "dgemm_tflops": (fm["gcr"] + fm["schur"]) / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None,
+            "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary()}
+
+    # ---- end to end through the public API with host buffers
+    if not args.no_e2e:
+        Kh = Kb.cpu().pin_memory()
+        e2e_steps = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        d2h = 0
+        for _ in range(e2e_steps):
+            K.copy_(Kh, non_blocking=True)
+            hf.hf_scale(ctx, K)
+            lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)
+            hy, info, S22 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True)
+            kd = hf.hf_factor_hard(ctx, hy)
+            perm, D, _ = lf.export(with_L=False)
+            d2h = S22.nbytes if S22 is not None else 0
+            d2h += perm.nbytes + D.nbytes + 8
+        t1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = t0.elapsed_time(t1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        line["e2e"] = {"value": total_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": int(Kh.numel() * 8), "d2h_bytes_per_step": int(d2h),
+                       "ms_per_step": e_ms}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            f, s_, desc = oracle_sample(Kb.cpu().numpy(), spec, pivots=args.pivots_sample)
+            line["cpu_baseline"] = {"value": f / s_ / 1e12, "unit": "TFLOP/s", "cores": host_cores(),
+                                    "kind": "oracle", "sample": desc, "seconds": s_}
+        except Exception as e:   # the oracle is a reported baseline, never the product
+            line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": host_cores(), "kind": "oracle",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

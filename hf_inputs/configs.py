@@ -46,7 +46,9 @@ CONFIGS = {
     # BASELINE.json configs[0..4]
     "C0": ConfigSpec("C0", "planted", 256, n_min=4, n_hard=4, u_hard=(-10.0, -8.0)),
     "C1": ConfigSpec("C1", "neumann", 64 * 64, grid=64, n_incl=3, incl_size=8),
-    "C2": ConfigSpec("C2", "planted", 16384, n_min=64, n_hard=64, u_hard=(-12.0, -6.0)),
+    # n_min: 64 planted directions, but at L = 16384 the FP32 factor leaves more unresolved
+    # directions (Gaussian B, bulk condition ~ 4 L^2 100); DESIGN.md [R5]
+    "C2": ConfigSpec("C2", "planted", 16384, n_min=256, n_hard=64, u_hard=(-12.0, -6.0)),
     "C3": ConfigSpec("C3", "saddle", 2 * 96 * 96 + 48 * 48, grid=96, jump=1e4),
     "C4": ConfigSpec("C4", "planted", 65536, n_min=256, n_hard=256, u_hard=(-12.0, -6.0)),
     # small analogs with the same recipes (tests; the oracle finishes in seconds)
@@ -54,6 +56,7 @@ CONFIGS = {
     "P512": ConfigSpec("P512", "planted", 512, n_min=8, n_hard=8, u_hard=(-12.0, -6.0)),
     "P1024": ConfigSpec("P1024", "planted", 1024, n_min=16, n_hard=16, u_hard=(-12.0, -6.0)),
     "P2048": ConfigSpec("P2048", "planted", 2048, n_min=32, n_hard=32, u_hard=(-12.0, -6.0)),
+    "P4096": ConfigSpec("P4096", "planted", 4096, n_min=64, n_hard=64, u_hard=(-12.0, -6.0)),
     "N16": ConfigSpec("N16", "neumann", 16 * 16, grid=16, n_incl=2, incl_size=4),
     "N32": ConfigSpec("N32", "neumann", 32 * 32, grid=32, n_incl=3, incl_size=4),
     "S12": ConfigSpec("S12", "saddle", 2 * 12 * 12 + 6 * 6, grid=12, jump=1e4),

@@ -325,6 +325,7 @@ class HardFactor:
     blocks: list           # pivot block sizes in order
     mu_stop: float = 0.0   # max |S_ij| of the block left at the stop (or of the last pivot)
     thr: float = 0.0
+    mu_hist: list = field(default_factory=list)   # max |S_ij| of the trailing block at every step
 
     @property
     def kernel_dim(self) -> int:
@@ -347,6 +348,7 @@ def factor_hard(S22: np.ndarray, d_ref: float, eps_ker: float = 1e-10) -> HardFa
     thr = eps_ker * d_ref
     k = 0
     mu_stop = 0.0
+    mu_hist = []
 
     def swap(i, j):
         if i == j:
@@ -360,6 +362,7 @@ def factor_hard(S22: np.ndarray, d_ref: float, eps_ker: float = 1e-10) -> HardFa
         sub = np.abs(A[k:, k:])
         mu0 = sub.max()
         mu_stop = mu0
+        mu_hist.append(float(mu0))
         if mu0 <= thr:
             break
         dg = np.diag(sub)
@@ -403,7 +406,7 @@ def factor_hard(S22: np.ndarray, d_ref: float, eps_ker: float = 1e-10) -> HardFa
             blocks.append(2)
             k += 2
     return HardFactor(m=m, r=k, perm2=lab, Lh=Lh, Dh=Dh, blocks=blocks, mu_stop=float(mu_stop),
-                      thr=float(thr))
+                      thr=float(thr), mu_hist=mu_hist)
 
 
 def hard_solve(H: HardFactor, y: np.ndarray) -> np.ndarray:

@@ -65,6 +65,12 @@ hf_status hf_create(int device, void *cuda_stream, hf_ctx **out) {
         c->device = device;
         c->num_sms = p.multiProcessorCount;
         c->stream = (cudaStream_t)cuda_stream;
+        // keep freed workspace reserved in the stream-ordered pool: re-mapping GBs of
+        // physical memory on every factorization costs more than the factorization
+        cudaMemPool_t pool;
+        HF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        HF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     });
     if (s != HF_OK) return s;
     *out = c.release();

@@ -16,6 +16,8 @@
 // iteration).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
@@ -110,6 +112,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
             maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
             res = read_res(ctx, w, &bad);
             iters = it + 1;
+            if (getenv("HF_GCR_DEBUG")) fprintf(stderr, "[hf gcr] n2=%lld it=%d res=%.3e bad=%d\n", (long long)n, iters, res, bad);
             if (res <= o.tol) {
                 conv = true;
                 break;

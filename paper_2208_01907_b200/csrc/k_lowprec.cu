@@ -56,11 +56,14 @@ __device__ __forceinline__ uint64_t warp_max64(uint64_t v) {
 __device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
+// spin with relaxed loads, acquire once (an ld.acquire per spin iteration
+// would invalidate L1 every time)
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int *p) {
     unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -96,6 +99,7 @@ struct ChainArgs {
     int64_t ldv;
     const int32_t *orig;  // position -> original index
     float *S;           // S[i + t*lds] = s_i^t (positive sign), this panel
+    float *Sn;          // Sn[i + t*lds] = -sigma_t s_i^t
     int64_t lds;
     float *sigma;       // [nb] sign of d_t
     int32_t *pivpos;    // [nb] pivot positions of this panel
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
     // deferred stores of the previous step
     bool pend = false;
-    float ps = 0.f, pl = 0.f;
+    float ps = 0.f, pn = 0.f, pl = 0.f;
     int t = 0;
     bool stopped = false;
     const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
@@ -179,6 +183,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- C: deferred global stores of step t-1
         if (pend) {
             a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+            a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
             a.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
             pend = false;
         }
@@ -186,8 +191,9 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- D: wait for all CTAs, read the winning key
         if (tid == 0) {
             const unsigned int want = (unsigned int)G * (unsigned int)(t + 1);
-            while (ld_acquire_u32(a.cnt) < want) {
+            while (ld_relaxed_u32(a.cnt) < want) {
             }
+            fence_acquire();
             bkey = ld_relaxed_u64(&a.keys[t]);
         }
         __syncthreads();
@@ -247,6 +253,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             const float ns = -sg * sv;                  // exact
             sneg[(size_t)t * a.R + tid] = ns;
             ps = sv;
+            pn = ns;
             pl = __fdiv_rn(c, d);                       // [R10] L = c / d
             pend = true;
             dg = __fmaf_rn(ns, sv, dg);                 // lazy diagonal, same fma as the update
@@ -256,6 +263,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     }
     if (pend) {   // flush the last step's values
         a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+        a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
         a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
     }
     if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
@@ -302,21 +310,24 @@ struct TrailArgs {
     float *Vnew;
     int64_t ldv;
     const int32_t *map;    // new position -> old position
-    const float *S;        // S[old + t*lds]
+    const float *S;        // S[old + t*lds]    =  s_i^t
+    const float *Sn;       // Sn[old + t*lds]   = -sigma_t s_i^t
     int64_t lds;
-    const float *sigma;
     const int32_t *status;
 };
 
-constexpr int TB = 128;    // CTA tile
-constexpr int TK = 8;      // k chunk
+constexpr int TB = 128;    // CTA tile (rows and columns)
+constexpr int TK = 16;     // k chunk
 
+// One 128x128 tile of the new lower triangle per CTA, 256 threads, 8x8 entries
+// per thread held as 8x4 float2 accumulators and updated with FFMA2
+// (__ffma2_rn: two independent IEEE fmaf, bit-identical to the scalar form)
+// -- one fused multiply-add per entry per pivot, pivots in increasing order.
 __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
     if (a.status[2]) return;
     __shared__ __align__(16) float As[2][TK][TB];
     __shared__ __align__(16) float Bs[2][TK][TB];
     __shared__ int32_t rmap[TB], cmap[TB];
-    __shared__ float sgm[256];
 
     const int64_t t = blockIdx.x;
     int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -330,49 +341,48 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
         rmap[tid] = (row0 + tid < a.mp) ? a.map[row0 + tid] : -1;
         cmap[tid] = (col0 + tid < a.mp) ? a.map[col0 + tid] : -1;
     }
-    for (int q = tid; q < a.nbp; q += 256) sgm[q] = -a.sigma[q];
     __syncthreads();
 
-    // accumulators seeded from the current values (compaction fused in the gather)
-    float acc[8][8];
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+    // accumulators seeded from the current values (compaction fused in the gather)
+    float2 acc[8][4];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const int32_t cm = cmap[CC(b)];
+    for (int j = 0; j < 4; ++j) {
+        const int32_t cm0 = cmap[CC(2 * j)], cm1 = cmap[CC(2 * j + 1)];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int32_t rm = rmap[RR(q)];
-            acc[q][b] = (cm >= 0 && rm >= 0 && rm >= cm) ? a.Vold[(int64_t)rm + (int64_t)cm * a.ldv] : 0.f;
+            acc[q][j].x = (cm0 >= 0 && rm >= cm0) ? a.Vold[(int64_t)rm + (int64_t)cm0 * a.ldv] : 0.f;
+            acc[q][j].y = (cm1 >= 0 && rm >= cm1) ? a.Vold[(int64_t)rm + (int64_t)cm1 * a.ldv] : 0.f;
         }
     }
 
-    // global -> register staging: each thread loads 4 A and 4 B elements per chunk
+    // global -> register staging: per chunk 8 A (-sigma s) and 8 B (s) values per thread
     const int lr = tid & 127, lk = tid >> 7;   // element (row lr, k = lk + 2*q)
     const int32_t arow = rmap[lr], bcol = cmap[lr];
-    float ra[4], rb[4];
+    const float *Ap = a.Sn + (arow >= 0 ? arow : 0);
+    const float *Bp = a.S + (bcol >= 0 ? bcol : 0);
+    float ra[TK / 2], rb[TK / 2];
     auto gload = [&](int t0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int kk = lk + 2 * q;
-            const int tt = t0 + kk;
+        for (int q = 0; q < TK / 2; ++q) {
+            const int tt = t0 + lk + 2 * q;
             const bool ok = tt < a.nbp;
-            ra[q] = (ok && arow >= 0) ? a.S[(int64_t)arow + (int64_t)tt * a.lds] : 0.f;
-            rb[q] = (ok && bcol >= 0) ? a.S[(int64_t)bcol + (int64_t)tt * a.lds] : 0.f;
+            ra[q] = (ok && arow >= 0) ? Ap[(int64_t)tt * a.lds] : 0.f;
+            rb[q] = (ok && bcol >= 0) ? Bp[(int64_t)tt * a.lds] : 0.f;
         }
     };
-    auto sstore = [&](int buf, int t0) {
+    auto sstore = [&](int buf) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int kk = lk + 2 * q;
-            const int tt = min(t0 + kk, a.nbp - 1);
-            As[buf][kk][lr] = sgm[tt] * ra[q];      // -sigma_t s_i^t (exact)
-            Bs[buf][kk][lr] = rb[q];
+        for (int q = 0; q < TK / 2; ++q) {
+            As[buf][lk + 2 * q][lr] = ra[q];
+            Bs[buf][lk + 2 * q][lr] = rb[q];
         }
     };
 
     gload(0);
-    sstore(0, 0);
+    sstore(0);
     __syncthreads();
     int buf = 0;
     for (int t0 = 0; t0 < a.nbp; t0 += TK) {
@@ -387,28 +397,30 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
                 const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4]);
                 const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + ty * 4]);
                 const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) acc[q][b] = __fmaf_rn(av[q], bv[b], acc[q][b]);
+                    for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
             }
         } else {
-            for (int kk = 0; kk < kmax; ++kk) {
-                float av[8], bv[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    av[q] = As[buf][kk][RR(q)];
-                    bv[q] = Bs[buf][kk][CC(q)];
-                }
+            for (int kk = 0; kk < kmax; ++kk) {   // ragged last chunk: exactly nbp updates, no padding
+                const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][tx * 4]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + tx * 4]);
+                const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + ty * 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) acc[q][b] = __fmaf_rn(av[q], bv[b], acc[q][b]);
+                    for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
             }
         }
         if (more) {
-            sstore(buf ^ 1, t0 + TK);
+            sstore(buf ^ 1);
             __syncthreads();
             buf ^= 1;
         }
@@ -416,15 +428,20 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
 
     // store the lower triangle of the new trailing matrix
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const int64_t c = col0 + CC(b);
-        if (c >= a.mp) continue;
+    for (int j = 0; j < 4; ++j) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t r = row0 + RR(q);
-            if (r < a.mp && r >= c) a.Vnew[r + c * a.ldv] = acc[q][b];
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = col0 + CC(2 * j + h);
+            if (c >= a.mp) continue;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int64_t r = row0 + RR(q);
+                if (r < a.mp && r >= c) a.Vnew[r + c * a.ldv] = h ? acc[q][j].y : acc[q][j].x;
+            }
         }
     }
+#undef RR
+#undef CC
 }
 
 // ------------------------------------------------------------------ factor gather
@@ -478,8 +495,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     orig[0].alloc(L, st);
     orig[1].alloc(L, st);
     map.alloc(L, st);
-    DBuf<float> S, sigma, Lorig, Dk;
+    DBuf<float> S, Sn, sigma, Lorig, Dk;
     S.alloc((size_t)L * nb, st);
+    Sn.alloc((size_t)L * nb, st);
     sigma.alloc(nb, st);
     Lorig.alloc((size_t)L * L, st);
     Dk.alloc(L, st);
@@ -521,7 +539,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
         ca.V = V[cur].p; ca.ldv = L; ca.orig = orig[cur].p;
-        ca.S = S.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
+        ca.S = S.p; ca.Sn = Sn.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
@@ -541,7 +559,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             }
             TrailArgs ta;
             ta.mp = mp; ta.nbp = nbp; ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p; ta.ldv = L;
-            ta.map = map.p; ta.S = S.p; ta.lds = L; ta.sigma = sigma.p; ta.status = status.p;
+            ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L; ta.status = status.p;
             const int64_t T = cdiv(mp, TB);
             {
                 ClassTimer tm(ctx, "trailing");

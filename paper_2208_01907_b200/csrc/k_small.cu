@@ -380,11 +380,13 @@ __global__ void k_gather_block_rows(int64_t n, int64_t ncol, const int64_t *__re
 // ------------------------------------------------------------------ launchers
 void gather_K12(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const int64_t *lam2, int64_t n2,
                 const uint8_t *mask1, double *B) {
+    ClassTimer tm_(ctx, "other");
     dim3 g((unsigned)std::min<int64_t>(cdiv(L, 256), 64), (unsigned)std::min<int64_t>(n2, 65535));
     k_gather_cols<<<g, 256, 0, ctx->stream>>>(L, K, ld, lam2, n2, mask1, B);
     HF_CHECK_LAUNCH(ctx);
 }
 void gather_K22(hf_ctx *ctx, int64_t n2, const double *K, int64_t ld, const int64_t *lam2, double *K22) {
+    ClassTimer tm_(ctx, "other");
     k_gather_k22<<<(unsigned)std::min<int64_t>(cdiv(n2 * n2, 256), 4096), 256, 0, ctx->stream>>>(n2, K, ld, lam2, K22);
     HF_CHECK_LAUNCH(ctx);
 }
@@ -393,15 +395,18 @@ void mask_from_pos(hf_ctx *ctx, int64_t L, const int32_t *pos1, uint8_t *m) {
     HF_CHECK_LAUNCH(ctx);
 }
 void colnorm2(hf_ctx *ctx, int64_t M, int64_t ncol, const double *X, int64_t ldx, double *out) {
+    ClassTimer tm_(ctx, "other");
     k_colnorm2<<<(unsigned)ncol, 256, 0, ctx->stream>>>(M, X, ldx, out);
     HF_CHECK_LAUNCH(ctx);
 }
 void maxres(hf_ctx *ctx, int64_t n, const double *rn2, const double *bn2, double *out) {
+    ClassTimer tm_(ctx, "other");
     k_maxres<<<1, 256, 0, ctx->stream>>>(n, rn2, bn2, out);
     HF_CHECK_LAUNCH(ctx);
 }
 void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *Minv, DBuf<double> &wk,
                  DBuf<double> &dg, int *status) {
+    ClassTimer tm_(ctx, "other");
     wk.alloc((size_t)2 * n * n, ctx->stream);
     double *W1 = wk.p, *T = wk.p + n * n;
     k_chol_inv<<<1, 1024, 0, ctx->stream>>>(n, M, ldm, W1, T, status);
@@ -435,6 +440,7 @@ void mask_vec(hf_ctx *ctx, int64_t L, const uint8_t *m, const double *src, doubl
 }
 void gather_block_rows(hf_ctx *ctx, int64_t n, int64_t ncol, const int64_t *perm, const double *X, int64_t ldx,
                        double *out, int64_t ldo) {
+    ClassTimer tm_(ctx, "other");
     if (n <= 0 || ncol <= 0) return;
     k_gather_block_rows<<<(unsigned)std::min<int64_t>(cdiv(n * ncol, 256), 8192), 256, 0, ctx->stream>>>(
         n, ncol, perm, X, ldx, out, ldo);

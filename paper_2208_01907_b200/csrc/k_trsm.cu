@@ -25,11 +25,15 @@ constexpr int TBS = 64;
 __device__ __forceinline__ void st_release32(int *p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire32(const int *p) {
+// Poll with RELAXED loads and acquire once afterwards: an ld.acquire in a spin
+// loop emits an L1 invalidate (CCTL.IVALL) per iteration, which stalls every
+// other CTA on the SM.
+__device__ __forceinline__ int ld_relaxed32(const int *p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // inverse of each 64x64 unit-lower diagonal block (identity-padded at the edge)
 __global__ void __launch_bounds__(64) k_diag_inv(int64_t N, const float *__restrict__ Lf, int64_t ldl,
@@ -90,6 +94,22 @@ __device__ __forceinline__ void tile_fma(float (&acc)[4][4], const float (*Ls)[T
     }
 }
 
+// acc[i][j] -= sum_k Ls[k][tr*4+i] * Ys[k][tc*4+j]  (negation folded into the FFMA)
+__device__ __forceinline__ void tile_fma_neg(float (&acc)[4][4], const float (*Ls)[TBS], const float (*Ys)[TBS],
+                                             int tr, int tc) {
+#pragma unroll 8
+    for (int k = 0; k < TBS; ++k) {
+        const float4 a = *reinterpret_cast<const float4 *>(&Ls[k][tr * 4]);
+        const float4 y = *reinterpret_cast<const float4 *>(&Ys[k][tc * 4]);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(-av[i], yv[j], acc[i][j]);
+    }
+}
+
 template <bool BWD>
 __global__ void __launch_bounds__(256) k_trsm(TrsmArgs a) {
     __shared__ __align__(16) float Ls[TBS][TBS];
@@ -126,12 +146,17 @@ __global__ void __launch_bounds__(256) k_trsm(TrsmArgs a) {
                 acc[i][j] = v;
             }
         }
-        // ---- off-diagonal blocks
-        const int cbeg = BWD ? b + 1 : 0, cend = BWD ? a.nblk : b;
-        for (int cb = cbeg; cb < cend; ++cb) {
-            if (tid == 0)
-                while (ld_acquire32(&flags[cb * a.nch + cc]) != a.epoch) {
+        // ---- off-diagonal blocks, earliest-finished dependency first
+        //      (forward: 0, 1, ..., b-1; backward: nblk-1, ..., b+1)
+        const int ndep = BWD ? (a.nblk - 1 - b) : b;
+        for (int dq = 0; dq < ndep; ++dq) {
+            const int cb = BWD ? (a.nblk - 1 - dq) : dq;
+            if (tid == 0) {
+                if (ld_relaxed32(&flags[cb * a.nch + cc]) != a.epoch) {
+                    while (ld_relaxed32(&flags[cb * a.nch + cc]) != a.epoch) __nanosleep(64);
                 }
+                fence_acquire();
+            }
             __syncthreads();
             const int64_t q0 = (int64_t)cb * TBS;
             const float *src = BWD ? a.Xb : a.Y;
@@ -156,7 +181,7 @@ __global__ void __launch_bounds__(256) k_trsm(TrsmArgs a) {
                 Ys[x][y] = okb ? src[(q0 + x) + (int64_t)(c0 + y) * a.N] : 0.f;
             }
             __syncthreads();
-            tile_fma(acc, Ls, Ys, tr, tc, -1.f);
+            tile_fma_neg(acc, Ls, Ys, tr, tc);
             __syncthreads();
         }
         // ---- diagonal block: out = Linv_b (or Linv_b^T) * acc
