@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 FFMA_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12     # TFLOP/s, B200 FP32 non-tensor
 DMMA_PEAK_MEASURED = 37.15                              # tools/peaks.py, profiles/peaks_r01.json
+KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "gram", "hard", "other")
 
 
 def flop_model(L, N, Ntau, n2, iters):
@@ -233,9 +234,9 @@ def main():
     torch.cuda.synchronize()
 
     ctx.set_profiling(True)
-    for c in ("scale", "chain", "trailing", "dgemm", "trsm", "hard", "other"):
+    for c in KCLASSES:
         ctx.kernel_stats(c)            # drain the warm-up records
-    base = {c: ctx.kernel_stats(c) for c in ("scale", "chain", "trailing", "dgemm", "trsm", "hard", "other")}
+    base = {c: ctx.kernel_stats(c) for c in KCLASSES}
     launches0 = ctx.launch_count()
     stage_ms = np.zeros(4)
     results = []

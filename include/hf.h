@@ -64,11 +64,16 @@ const char *hf_last_error(const hf_ctx *ctx);
 /* Instrumentation: number of kernels this context launched so far, and the
  * summed device time of one kernel class measured with CUDA events on the
  * context stream while profiling is enabled.  class: "trailing", "chain",
- * "dgemm", "trsm", "scale", "hard", "other". */
+ * "dgemm", "trsm", "gram", "scale", "hard", "other". */
 hf_status hf_set_profiling(hf_ctx *ctx, int enable);
 hf_status hf_kernel_stats(hf_ctx *ctx, const char *kernel_class, double *ms_host,
                           int64_t *launches_host);
 hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host);
+/* Device workspaces and handle buffers come from a per-(device, stream) cache
+ * that reuses freed blocks in stream order (no memory is re-mapped by a
+ * repeated factorization); this synchronises the device and returns every
+ * cached (free) block of `device` to the driver.  Live handles are untouched. */
+hf_status hf_trim_cache(int device);
 
 /* ------------------------------------------------- a1: scaling, P:40 [R1] */
 /* In place: q_i = 1/sqrt|K_ii| (1 if K_ii == 0); K_ij = (q_i K_ij) q_j for

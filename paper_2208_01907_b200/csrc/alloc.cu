@@ -1,0 +1,121 @@
+// alloc.cu -- the library's device-memory cache.
+//
+// Every workspace and handle buffer of libhf (DBuf) comes from here.  Freed
+// blocks are kept per (device, stream) and handed out again, in stream order,
+// to later requests of (nearly) the same size, so a repeated factorization
+// maps no new memory: at C2 one step touches ~10 GB of workspaces, and
+// re-mapping that through cudaMalloc / the driver pool on every call cost more
+// than the factorization itself.  On cudaErrorMemoryAllocation the cache is
+// trimmed (device synchronised, cached blocks freed) and the request retried
+// once.  hf_trim_cache() (include/hf.h) releases everything cached.
+#include <map>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+
+#include "hf_internal.cuh"
+
+namespace hf {
+namespace {
+
+struct Live {
+    size_t bytes;
+    int dev;
+};
+
+struct Cache {
+    std::mutex mu;
+    std::map<std::pair<int, cudaStream_t>, std::multimap<size_t, void *>> free_;
+    std::unordered_map<void *, Live> live;
+    size_t cached_bytes = 0;
+};
+
+Cache &cache() {
+    static Cache *c = new Cache();   // never destroyed: frees may run at process exit
+    return *c;
+}
+
+size_t round_bytes(size_t b) {
+    if (b == 0) b = 1;
+    if (b < ((size_t)1 << 20)) return (b + 511) & ~(size_t)511;
+    return (b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+}
+
+void trim_device(int dev) {
+    Cache &c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    for (auto it = c.free_.begin(); it != c.free_.end();) {
+        if (it->first.first == dev) {
+            for (auto &kv : it->second) {
+                cudaFree(kv.second);
+                c.cached_bytes -= kv.first;
+            }
+            it = c.free_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    cudaSetDevice(cur);
+}
+
+}  // namespace
+
+void *dev_alloc(size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    HF_CUDA(cudaGetDevice(&dev));
+    const size_t want = round_bytes(bytes);
+    Cache &c = cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto f = c.free_.find({dev, s});
+        if (f != c.free_.end()) {
+            auto it = f->second.lower_bound(want);
+            // best fit, at most 25% (or 2 MB) larger than asked
+            if (it != f->second.end() && it->first <= want + std::max(want / 4, ((size_t)2 << 20))) {
+                void *p = it->second;
+                c.cached_bytes -= it->first;
+                c.live[p] = Live{it->first, dev};
+                f->second.erase(it);
+                return p;
+            }
+        }
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        trim_device(dev);
+        e = cudaMalloc(&p, want);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{e == cudaErrorMemoryAllocation ? HF_ERR_OOM : HF_ERR_CUDA,
+                    std::string("device allocation of ") + std::to_string(want) + " bytes: " + cudaGetErrorString(e)};
+    }
+    std::lock_guard<std::mutex> g(c.mu);
+    c.live[p] = Live{want, dev};
+    return p;
+}
+
+void dev_free(void *p, cudaStream_t s) {
+    if (!p) return;
+    Cache &c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.live.find(p);
+    if (it == c.live.end()) return;
+    const Live l = it->second;
+    c.live.erase(it);
+    c.free_[{l.dev, s}].insert({l.bytes, p});
+    c.cached_bytes += l.bytes;
+}
+
+}  // namespace hf
+
+extern "C" hf_status hf_trim_cache(int device) {
+    hf::trim_device(device);
+    return cudaGetLastError() == cudaSuccess ? HF_OK : HF_ERR_CUDA;
+}

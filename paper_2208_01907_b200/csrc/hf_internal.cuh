@@ -49,6 +49,10 @@ struct Error {
     } while (0)
 
 // ----------------------------------------------------------------- device buffers
+// device-memory cache (alloc.cu): stream-ordered reuse of freed blocks
+void *dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void *p, cudaStream_t s);
+
 template <typename T>
 struct DBuf {
     T *p = nullptr;
@@ -68,7 +72,7 @@ struct DBuf {
     }
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) dev_free(p, s);
         p = nullptr;
         n = 0;
     }
@@ -77,7 +81,7 @@ struct DBuf {
         release();
         s = stream;
         size_t bytes = (count ? count : 1) * sizeof(T);
-        HF_CUDA(cudaMallocAsync((void **)&p, bytes, stream));
+        p = static_cast<T *>(dev_alloc(bytes, stream));
         n = count;
     }
     void zero(cudaStream_t stream) {
@@ -150,9 +154,11 @@ struct Precond {
     const float *Lfac = nullptr;   // N x N unit lower, pivot order
     const float *D = nullptr;      // [N]
     const int64_t *perm = nullptr; // [L] pivot order -> original index
-    DBuf<float> Linv;              // inverses of the 64x64 diagonal blocks
-    DBuf<float> Y;                 // N x ncol workspace (FP32)
-    DBuf<float> Xb;                // N x ncol workspace (FP32)
+    int64_t Np = 0;                // N rounded up to the 64-row block
+    DBuf<float> Lp, Up;            // Np x Np: L padded with the identity, and L^T
+    DBuf<float> LinvF, LinvB;      // inverses of the 64x64 diagonal blocks (tile layouts)
+    DBuf<float> Y;                 // Np x ncolp workspace (FP32, row-major)
+    DBuf<float> Xb;                // Np x ncolp workspace (FP32, row-major)
     DBuf<int> flags;
     DBuf<int> counter;
     int epoch = 0;

@@ -3,10 +3,14 @@
 //   the convergence test [R13], inversion of the Gram matrices M_n (Alg. 5
 //   P:322-330, via Cholesky) and the hard factorization of S22 (Alg. 1
 //   step 5; 1x1/2x2 pivots P:84; kernel rule [R15]).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hf {
 namespace {
@@ -74,60 +78,61 @@ __global__ void k_maxres(int64_t n, const double *__restrict__ rn2, const double
 }
 
 // ------------------------------------------------------------------ SPD inverse
-// T = chol(M)^{-1} (lower), i.e. M^{-1} = T^T T.  Single CTA, global workspace
-// (n x n, ld n).  status[0] |= 1 on a non-positive pivot [R11].
-__global__ void __launch_bounds__(1024) k_chol_inv(int64_t n, const double *__restrict__ M, int64_t ldm,
-                                                   double *__restrict__ Wk, double *__restrict__ T, int *status) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t tot = n * n;
-    for (int64_t e = tid; e < tot; e += nt) {
-        const int64_t i = e % n, j = e / n;
-        Wk[e] = (i >= j) ? M[i + j * ldm] : 0.0;
-    }
-    __syncthreads();
-    __shared__ double dsh;
-    __shared__ int bad;
-    if (tid == 0) bad = 0;
-    for (int64_t j = 0; j < n; ++j) {
-        if (tid == 0) {
-            double d = Wk[j + j * n];
-            if (!(d > 0.0)) { bad = 1; d = 1.0; }
-            d = sqrt(d);
-            Wk[j + j * n] = d;
-            dsh = d;
+// Minv = M^{-1} for the SPD Gram matrix M_n of Alg. 5 by in-place
+// Gauss-Jordan elimination without pivoting (for SPD M its pivots are the
+// squared Cholesky diagonals, so "pivot <= 0" is exactly Cholesky breakdown
+// [R11] -> status[0] |= 1).  One cooperative launch: CTA c owns a contiguous
+// slice of columns; per step k every CTA reads snapshots of column k and row k
+// (written by their owners at the end of step k-1) and updates its columns;
+// one grid barrier per step.
+//   p = a_kk;  a_ij -= a_ik a_kj / p;  a_kj /= p;  a_ik = -a_ik / p;  a_kk = 1/p
+__global__ void __launch_bounds__(256) k_spd_inv(int64_t n, const double *__restrict__ M, int64_t ldm,
+                                                 double *__restrict__ A, double *__restrict__ cbuf,
+                                                 double *__restrict__ rbuf, int *status) {
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+    const int64_t per = (n + G - 1) / G;
+    const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(n, j0 + per);
+    for (int64_t j = j0; j < j1; ++j)
+        for (int64_t i = tid; i < n; i += nt) {
+            const double v = M[i + j * ldm];
+            A[i + j * n] = v;
+            if (j == 0) cbuf[i] = v;
+            if (i == 0) rbuf[j] = v;
         }
-        __syncthreads();
-        const double d = dsh;
-        for (int64_t i = j + 1 + tid; i < n; i += nt) Wk[i + j * n] /= d;
-        __syncthreads();
-        // trailing: Wk[i,k] -= Wk[i,j] Wk[k,j] for j < k <= i
-        const int64_t m = n - j - 1;
-        const int64_t np = m * (m + 1) / 2;
-        for (int64_t e = tid; e < np; e += nt) {
-            int64_t kk = (int64_t)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-            while (kk * (kk + 1) / 2 > e) --kk;
-            while ((kk + 1) * (kk + 2) / 2 <= e) ++kk;
-            const int64_t ii = e - kk * (kk + 1) / 2;   // ii <= kk  -> (row = j+1+kk, col = j+1+ii)
-            const int64_t r = j + 1 + kk, c = j + 1 + ii;
-            Wk[r + c * n] = fma(-Wk[r + j * n], Wk[c + j * n], Wk[r + c * n]);
+    int bad = 0;
+    grid.sync();
+    for (int64_t k = 0; k < n; ++k) {
+        const double *ck = cbuf + (k & 1) * n, *rk = rbuf + (k & 1) * n;
+        double *cn = cbuf + ((k + 1) & 1) * n, *rn = rbuf + ((k + 1) & 1) * n;
+        double p = ck[k];
+        if (!(p > 0.0)) {
+            bad = 1;
+            p = 1.0;
         }
-        __syncthreads();
-    }
-    // T = Wk^{-1}: column c by thread c (lower triangular inverse)
-    for (int64_t c = tid; c < n; c += nt) {
-        for (int64_t i = 0; i < n; ++i) {
-            double v;
-            if (i < c) v = 0.0;
-            else if (i == c) v = 1.0 / Wk[c + c * n];
-            else {
-                double s = 0.0;
-                for (int64_t k = c; k < i; ++k) s = fma(Wk[i + k * n], T[k + c * n], s);
-                v = -s / Wk[i + i * n];
+        const double ip = 1.0 / p;
+        for (int64_t j = j0; j < j1; ++j) {
+            double *aj = A + j * n;
+            if (j == k) {
+                for (int64_t i = tid; i < n; i += nt) {
+                    const double v = (i == k) ? ip : -ck[i] / p;
+                    aj[i] = v;
+                    if (j == k + 1) cn[i] = v;
+                    if (i == k + 1) rn[j] = v;
+                }
+            } else {
+                const double r = rk[j] / p;
+                for (int64_t i = tid; i < n; i += nt) {
+                    const double v = (i == k) ? r : fma(-ck[i], r, aj[i]);
+                    aj[i] = v;
+                    if (j == k + 1) cn[i] = v;
+                    if (i == k + 1) rn[j] = v;
+                }
             }
-            T[i + c * n] = v;
         }
+        grid.sync();
     }
-    if (tid == 0 && bad) atomicOr(status, 1);
+    if (blockIdx.x == 0 && tid == 0 && bad) atomicOr(status, 1);
 }
 
 // ------------------------------------------------------------------ hard factorization
@@ -406,12 +411,14 @@ void maxres(hf_ctx *ctx, int64_t n, const double *rn2, const double *bn2, double
 }
 void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *Minv, DBuf<double> &wk,
                  DBuf<double> &dg, int *status) {
-    ClassTimer tm_(ctx, "other");
-    wk.alloc((size_t)2 * n * n, ctx->stream);
-    double *W1 = wk.p, *T = wk.p + n * n;
-    k_chol_inv<<<1, 1024, 0, ctx->stream>>>(n, M, ldm, W1, T, status);
+    (void)dg;
+    ClassTimer tm_(ctx, "gram");
+    wk.alloc((size_t)4 * n, ctx->stream);
+    double *cb = wk.p, *rb = wk.p + 2 * n;
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(n, 4)), ctx->num_sms);
+    void *args[] = {&n, &M, &ldm, &Minv, &cb, &rb, &status};
+    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_spd_inv, dim3(G), dim3(256), args, 0, ctx->stream));
     HF_CHECK_LAUNCH(ctx);
-    dgemm(ctx, true, n, n, n, 1.0, T, n, T, n, 0.0, Minv, n, nullptr, &dg, 1);   // T^T T
 }
 void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A, double *Lh, double *Dh,
                  int32_t *lab, int32_t *blocks, int64_t *rank_dev) {

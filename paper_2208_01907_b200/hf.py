@@ -27,7 +27,7 @@ EXPORTED = [
     "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
     "hf_set_profiling", "hf_kernel_stats", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
-    "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy",
+    "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
 ]
 
 
@@ -84,6 +84,7 @@ def load() -> ctypes.CDLL:
         "hf_hard_export": [vp, vp, vp, vp, pi64],
         "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
         "hf_hybrid_destroy": [vp],
+        "hf_trim_cache": [ctypes.c_int],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -93,6 +94,13 @@ def load() -> ctypes.CDLL:
     L.hf_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
+
+
+def hf_trim_cache(device: int = 0) -> None:
+    """Return the library's cached (free) device blocks of `device` to the driver."""
+    st = load().hf_trim_cache(device)
+    if st != HF_OK:
+        raise HFError(st, "hf_trim_cache")
 
 
 def _ptr(t) -> int | None:
