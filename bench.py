@@ -52,47 +52,76 @@ def flop_model(L, N, Ntau, n2, iters):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
+    """Clock / throttle-reason sampler for the timed region.  NVML in-process
+    (the same counters nvidia-smi's clocks line reads: clocks.sm, clocks.max.sm,
+    power.draw, clocks_event_reasons.*), every 200 ms; a subprocess per sample
+    would perturb the host-driven parts of the step it is measuring.  Falls
+    back to nvidia-smi if NVML is unavailable."""
 
-    def __init__(self, index=0):
-        self.index, self.samples, self.stop = index, [], threading.Event()
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index=0, enabled=True):
+        self.index, self.samples, self.stop, self.enabled = index, [], threading.Event(), enabled
         self.th = threading.Thread(target=self._run, daemon=True)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nv = None
+        try:                     # the first queries are slow (NVML warm-up): keep them out of the timed region
+            for _ in range(3):
+                self._sample()
+        except Exception:
+            pass
+
+    def _sample(self):
+        if self.nv is not None:
+            nv, h = self.nv, self.h
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            return [nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                    nv.nvmlDeviceGetPowerUsage(h) / 1e3] + [bool(r & b_) for b_ in bits]
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        r = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-i", str(self.index)],
+                           capture_output=True, text=True, timeout=5)
+        v = [x.strip() for x in r.stdout.strip().split(",")]
+        return [float(v[0]), float(v[1]), float(v[2])] + [x.lower() == "active" for x in v[3:7]]
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         while not self.stop.is_set():
             try:
-                r = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                    "-i", str(self.index)], capture_output=True, text=True, timeout=5)
-                self.samples.append([x.strip() for x in r.stdout.strip().split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
             self.stop.wait(0.2)
 
     def __enter__(self):
-        self.th.start()
+        if self.enabled:
+            self.th.start()
         return self
 
     def __exit__(self, *a):
         self.stop.set()
-        self.th.join(timeout=10)
+        if self.enabled:
+            self.th.join(timeout=10)
 
     def summary(self):
-        mhz, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        mhz = [s[0] for s in self.samples]
+        reasons = set()
         for s in self.samples:
-            try:
-                mhz.append(float(s[0]))
-                mx = float(s[1])
-                for nm, v in zip(names, s[4:8]):
-                    if v.strip().lower() == "active":
-                        reasons.add(nm)
-            except Exception:
-                pass
-        return {"sm_mhz": float(np.median(mhz)) if mhz else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(mhz)}
+            for nm, v in zip(self.NAMES, s[3:7]):
+                if v:
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(mhz)) if mhz else None,
+                "sm_max_mhz": float(self.samples[-1][1]) if self.samples else None,
+                "power_w_max": float(max(s[2] for s in self.samples)) if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(mhz),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 def load_traffic():
@@ -153,7 +182,7 @@ def host_cores():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="hf", choices=["hf", "reference"])
@@ -227,11 +256,16 @@ def main():
         ev[3].record(stream)
         kd = hf.hf_factor_hard(ctx, hy)
         ev[4].record(stream)
-        return lf, hy, info, kd, ev
+        res = (lf.N, lf.L - lf.n2_tau_only, lf.n2, info.iters, kd, info.max_rel_res_true)
+        hy.close()               # one factorization's buffers live at a time: the library's
+        lf.close()               # memory cache then serves every step from the same blocks
+        return res, ev
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if os.environ.get("HF_ALLOC_DEBUG"):
+        print("[bench] warm-up done", file=sys.stderr, flush=True)
 
     ctx.set_profiling(True)
     for c in KCLASSES:
@@ -239,21 +273,27 @@ def main():
     base = {c: ctx.kernel_stats(c) for c in KCLASSES}
     launches0 = ctx.launch_count()
     stage_ms = np.zeros(4)
+    step_ms = []
     results = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    import gc
+    gc.collect()
+    gc.disable()              # no collector pauses inside the timed region
+    with Clocks(local, enabled=not os.environ.get("HF_BENCH_NO_CLOCKS")) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for _ in range(args.steps):
-            lf, hy, info, kd, ev = step()
-            results.append((lf.N, lf.L - lf.n2_tau_only, lf.n2, info.iters, kd, info.max_rel_res_true))
+            res, ev = step()
+            results.append(res)
             for q in range(4):
                 stage_ms[q] += ev[q].elapsed_time(ev[q + 1]) if ev[q + 1].query() else 0.0
+            step_ms.append([round(ev[q].elapsed_time(ev[q + 1]), 2) for q in range(4)])
         t_end.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         dist.barrier()
     elapsed = t_start.elapsed_time(t_end)             # ms, this rank
@@ -301,7 +341,7 @@ def main():
             "seconds_per_factorization": ms_step / 1e3,
             "stage_ms": {"scale": stage_ms[0] / args.steps, "lowprec": stage_ms[1] / args.steps,
                          "schur_gcr": stage_ms[2] / args.steps, "hard": stage_ms[3] / args.steps},
-            "flops_per_step": fm,
+            "flops_per_step": fm, "per_step_stage_ms": step_ms,
             "kernel_ms_per_step": kms, "kernel_share": shares,
             "chain_us_per_pivot": kms["chain"] * 1e3 / max(Ntau, 1),
             "dgemm_tflops": (fm["gcr"] + fm["schur"]) / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None,
@@ -327,6 +367,8 @@ def main():
             perm, D, _ = lf.export(with_L=False)
             d2h = S22.nbytes if S22 is not None else 0
             d2h += perm.nbytes + D.nbytes + 8
+            hy.close()
+            lf.close()
         t1.record(stream)
         torch.cuda.synchronize()
         e_ms = t0.elapsed_time(t1) / e2e_steps

@@ -109,6 +109,16 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
                               float *D_host, float *Lfac, int64_t ldl);
 hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
 
+/* --------------------------- a5: the preconditioner Q^{-1}, P:231-242 [R12] */
+/* W = lift( L^{-T} D^{-1} L^{-1} truncate(R) ) in FP32 for the Lambda_1 rows
+ * ("find e^ satisfying Q^ e^ = r^ in lower precision ... up-converting"),
+ * 0 on the Lambda_2 rows.  R, W: DEVICE L x ncol column-major FP64 in ORIGINAL
+ * row order (ldr, ldw >= L); only the Lambda_1 rows of R are read.  The same
+ * kernels serve every preconditioner application inside hf_schur_gcr and
+ * hf_solve (SPEC precond_solve).  Synchronises. */
+hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, const double *R,
+                           int64_t ldr, double *W, int64_t ldw);
+
 /* ------------------------ a4-a6: block GCR + Schur */
 typedef struct {
     double tol;        /* per-column recursive ||r||_2/||b||_2 target [R13] (1e-14) */

@@ -8,6 +8,8 @@
 // than the factorization itself.  On cudaErrorMemoryAllocation the cache is
 // trimmed (device synchronised, cached blocks freed) and the request retried
 // once.  hf_trim_cache() (include/hf.h) releases everything cached.
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -85,6 +87,8 @@ void *dev_alloc(size_t bytes, cudaStream_t s) {
         }
     }
     void *p = nullptr;
+    static const bool dbg = getenv("HF_ALLOC_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "[hf alloc] cudaMalloc %zu bytes (cached %zu)\n", want, c.cached_bytes);
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();

@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "hf_internal.cuh"
+#include "k_dgemm.cuh"
 
 namespace {
 
@@ -100,6 +101,14 @@ const char *hf_last_error(const hf_ctx *ctx) {
 hf_status hf_set_profiling(hf_ctx *ctx, int enable) {
     if (!ctx) return HF_ERR_INVALID_ARG;
     ctx->profiling = enable != 0;
+    // pre-create the timing events: creating thousands of them inside a timed
+    // region stalls the launch stream when the driver grows its event storage
+    if (ctx->profiling)
+        while (ctx->event_pool.size() < 16384) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) break;
+            ctx->event_pool.push_back(e);
+        }
     return HF_OK;
 }
 
@@ -186,6 +195,21 @@ hf_status hf_lowfactor_destroy(hf_lowfactor *lf) {
         delete lf;
     }
     return HF_OK;
+}
+
+// ------------------------------------------------------------------ a5 preconditioner
+hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, const double *R, int64_t ldr,
+                           double *W, int64_t ldw) {
+    if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(ncol >= 0 && ldr >= lf->L && ldw >= lf->L && (ncol == 0 || lf->L == 0 || (R && W)),
+                   "hf_precond_apply: bad arguments");
+        if (ncol == 0 || lf->L == 0) return;
+        hf::Precond pc;
+        hf::precond_setup(ctx, pc, lf->N, lf->L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        hf::precond_apply(ctx, pc, ncol, R, ldr, W, ldw);
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
 }
 
 // ------------------------------------------------------------------ a4-a6

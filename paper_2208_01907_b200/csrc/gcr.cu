@@ -164,7 +164,7 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
     hy->lam2.alloc(std::max<int64_t>(n2, 1), st);
     if (n2 > 0)
         HF_CUDA(cudaMemcpyAsync(hy->lam2.p, lf->perm.p + N, n2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    precond_setup(ctx, hy->pc, N, L, lf->Lfac.p, lf->D.p, lf->perm.p);
+    precond_setup(ctx, hy->pc, N, L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
     hy->X.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->B.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->S22.alloc((size_t)std::max<int64_t>(n2 * n2, 1), st);

@@ -97,6 +97,15 @@ struct KStat {
 
 }  // namespace hf
 
+namespace hf {
+// dataflow item table of the preconditioner solves (k_trsm.cu), per shape
+struct TrsmTable {
+    int nitems = 0, nslots = 0;
+    DBuf<int4> items;
+    DBuf<int> pbase;
+};
+}  // namespace hf
+
 struct hf_ctx {
     int device = 0;
     cudaStream_t stream = 0;
@@ -112,6 +121,7 @@ struct hf_ctx {
     std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::map<std::string, hf::KStat> stats;
     std::vector<cudaEvent_t> event_pool;
+    std::map<std::pair<int, int>, hf::TrsmTable> trsm_tables;   // (nblk, nch) -> table
 };
 
 namespace hf {
@@ -154,14 +164,24 @@ struct Precond {
     const float *Lfac = nullptr;   // N x N unit lower, pivot order
     const float *D = nullptr;      // [N]
     const int64_t *perm = nullptr; // [L] pivot order -> original index
+    const int32_t *pos1 = nullptr; // [L] original index -> pivot rank, -1 on Lambda_2
     int64_t Np = 0;                // N rounded up to the 64-row block
     DBuf<float> Lp, Up;            // Np x Np: L padded with the identity, and L^T
     DBuf<float> LinvF, LinvB;      // inverses of the 64x64 diagonal blocks (tile layouts)
+    DBuf<float> MF, MB;            // Dinv_j Op_{j,j-1}, Dinv_j Op_{j,j-2} per logical block
+    DBuf<float> P;                 // Np x ncolp: P_j of the chain recurrence (row-major)
     DBuf<float> Y;                 // Np x ncolp workspace (FP32, row-major)
     DBuf<float> Xb;                // Np x ncolp workspace (FP32, row-major)
     DBuf<int> flags;
     DBuf<int> counter;
     int epoch = 0;
+    // dataflow workspaces (k_trsm.cu), re-sized when the block/chunk counts change
+    int tab_nblk = -1, tab_nch = -1, nitems = 0, nslots = 0;
+    const int4 *items = nullptr;   // owned by the context's table cache
+    const int *pbase = nullptr;
+    DBuf<float> part;
+    DBuf<int> pflags;
+    DBuf<unsigned long long> dbg;
 };
 }  // namespace hf
 

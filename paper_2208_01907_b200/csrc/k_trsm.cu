@@ -7,13 +7,29 @@
 // solve's store ("forward/backward substitution in lower precision ...
 // BLAS level 3 TRSM").  Any summation order is allowed here [R12].
 //
-// Design (B200): persistent dataflow kernels, one per direction.
-//  * Work item = (64-row block b, 64-column RHS chunk).  Items are handed out
-//    in dependency order by an atomic counter; an item accumulates the
-//    off-diagonal products L_bq Y_q of its dependencies q in the order they
-//    finish (release flags, relaxed polling + one acquire), then applies the
-//    precomputed inverse of its 64x64 unit diagonal block and releases its own
-//    flag.  No host round trips, no launch per block.
+// Design (B200): one cooperative persistent launch per direction, blocks of
+// 64 rows, RHS chunks of 64 columns.  With Dinv_b the inverse of the unit
+// diagonal block (L_bb^{-1} forward, L_bb^{-T} backward) and Op = L / L^T,
+//     Y_b = P_b - M1_b Y_{b-1} - M2_b Y_{b-2},
+//     P_b = Dinv_b (RHS_b - sum_{q < b-2} Op_bq Y_q),   Mk_b = Dinv_b Op_{b,b-k}
+// (block indices in the direction of the solve).
+//  * CHAIN CTAs (one per chunk, alone on their SM: the helper that shares
+//    the SM exits) walk the blocks in order and keep Y_{b-1}, Y_{b-2} in a
+//    3-slot shared ring: a link of the sequential chain is two 64x64x64
+//    tile products (-M1, -M2 prefetched by cp.async during the previous
+//    link); two STORE warps copy each finished Y_b to global memory, fence
+//    and release it while the 8 compute warps already run the next link
+//    (per-slot FULL/EMPTY named barriers hand the ring slots over).
+//  * HELPER CTAs (all others) take items from a host-built table in
+//    topological order (atomic counter): PARTIAL items sum one segment of SEG
+//    dependency blocks into a partial slot; the P-item of block b adds the
+//    partial slots in fixed order, its last segment (up to b-3), and applies
+//    Dinv_b, two links ahead of the chain that consumes it.  Long sums of the
+//    last blocks are spread over many CTAs instead of serialising on one.
+//  * Release flags + relaxed polling + one acquire; the cooperative launch
+//    guarantees chain and helpers are co-resident (no deadlock by design:
+//    every table item depends only on earlier items and on chain stages
+//    earlier than its own position).
 //  * Operands are laid out so every tile load is a contiguous 16-byte
 //    cp.async (LDGSTS) into a conflict-free shared layout, double buffered so
 //    the next dependency's tiles stream in while the current one is used:
@@ -23,6 +39,9 @@
 //        a contiguous row segment.
 //  * 256 threads, 4x4 register tile per thread, FFMA.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "k_dgemm.cuh"
 
@@ -74,6 +93,14 @@ __global__ void __launch_bounds__(256) k_pad_transpose(int64_t N, int64_t Np, co
     for (int q = ty; q < 32; q += 8) Up[(j0 + tx) + (i0 + q) * Np] = t[tx][q];   // Up(j, i) = L(i, j)
 }
 
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
 // Inverse of each 64x64 unit-lower diagonal block, stored directly in the
 // shared-tile layouts of the two solves:
 //   LinvF[b][k][r] = Linv_b(r, k)   (forward:  out = Linv_b acc)
@@ -104,31 +131,47 @@ __global__ void __launch_bounds__(64) k_diag_inv(int64_t Np, const float *__rest
 
 struct TrsmArgs {
     int64_t N, Np;
-    int ncol, ncolp, nch, nblk;
+    int ncol, ncolp, nch, nblk, seg;
+    const int4 *items;   // [nitems] (logical block j, chunk, segment or -1, slot)
+    int nitems;
+    const int *pbase;    // [nblk] first partial slot of logical block j
+    float *part;         // partial sums [slot][chunk][64 x CW] (row-major)
+    float *P;            // P_j, row-major Np x ncolp (by physical row)
+    int *pflags;         // [2][nslots*nch]
+    int *aflags;         // [2][nblk*nch]   P_j ready
+    int nslots;
     const float *Lp;     // forward operand  (Np x Np, col-major)
     const float *Up;     // backward operand (Np x Np, col-major) = Lp^T
-    const float *LinvF;  // [nblk][64][64]
-    const float *LinvB;
+    const float *LinvF;  // [nblk][64][64] tile layout of Dinv (forward)
+    const float *LinvB;  // (backward)
+    const float *MF;     // [nblk][2][64][64] -M1, -M2 (forward, by logical block)
+    const float *MB;     // (backward)
     const float *D;      // [N]
     const int64_t *perm; // [L] pivot order -> original index
     const double *R;     // input, original row order (L x ncol, ldr)
     int64_t ldr;
     float *Y;            // forward result, row-major Np x ncolp
     float *Xb;           // backward result, row-major Np x ncolp
-    double *W;           // output, original row order (L x ncol, ldw)
-    int64_t ldw;
-    int *flags;          // [2][nblk*nch]
+    int *flags;          // [2][nblk*nch]   chain released Y_j
     int *counter;        // [2]
+    unsigned *smids;     // [2][nch] SM of each chain CTA (+1; 0 = not yet published)
     int epoch;
+    unsigned long long *dbg;   // optional chain phase timers (HF_TRSM_DEBUG)
 };
 
-// acc[i][j] -= sum_k As[k][tr*4+i] * Bs[k][tc*4+j]
-__device__ __forceinline__ void tile_fms(float (&acc)[4][4], const float *As, const float *Bs, int tr, int tc) {
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// acc[i][j] += sum_k As[k][tr*4+i] * Bs[k][tc*4+j]
+__device__ __forceinline__ void tile_fma(float (&acc)[4][4], const float *As, const float *Bs, int tr, int tc) {
 #pragma unroll 16
     for (int k = 0; k < TBS; ++k) {
         const float4 a = *reinterpret_cast<const float4 *>(&As[k * TBS + tr * 4]);
         const float4 y = *reinterpret_cast<const float4 *>(&Bs[k * CW + tc * 4]);
-        const float av[4] = {-a.x, -a.y, -a.z, -a.w};
+        const float av[4] = {a.x, a.y, a.z, a.w};
         const float yv[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -137,51 +180,273 @@ __device__ __forceinline__ void tile_fms(float (&acc)[4][4], const float *As, co
     }
 }
 
-template <bool BWD>
-__global__ void __launch_bounds__(256, 3) k_trsm(TrsmArgs a) {
-    extern __shared__ __align__(16) float sm[];   // [2 stages][A tile | B tile]
-    __shared__ int item_s;
-    const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
-    const int nitems = a.nblk * a.nch;
-    int *flags = a.flags + (BWD ? nitems : 0);
-    int *counter = a.counter + (BWD ? 1 : 0);
-    const float *Op = BWD ? a.Up : a.Lp;
-    const float *src = BWD ? a.Xb : a.Y;
+__device__ __forceinline__ void wait_epoch(const int *f, int epoch) {
+    if (ld_relaxed32(f) != epoch) {
+        while (ld_relaxed32(f) != epoch) __nanosleep(20);
+    }
+    fence_acquire();
+}
 
-    // copy the (A, B) tiles of dependency block q, chunk c0, into stage s
+// ------------------------------------------------------------------ setup: -M1, -M2
+// M[j][k-1] = -Dinv_j Op_{j, j-k} (logical blocks), column-major 64x64 = tile
+// layout.  Bs[k][c] = Op(r0+k, q0+c) is read from the OTHER operand (Op^T),
+// which is contiguous in c.
+template <bool BWD>
+__global__ void __launch_bounds__(256) k_mk(int nblk, int64_t Np, const float *__restrict__ Lp,
+                                            const float *__restrict__ Up, const float *__restrict__ Linv,
+                                            float *__restrict__ M) {
+    __shared__ __align__(16) float As[TILE];
+    __shared__ __align__(16) float Bs[TILE];
+    const int j = blockIdx.x, kk = blockIdx.y + 1;   // logical block, lag
+    const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
+    float *dst = M + ((size_t)j * 2 + (kk - 1)) * TILE;
+    if (j - kk < 0) {
+        for (int e = tid; e < TILE; e += 256) dst[e] = 0.f;
+        return;
+    }
+    const int b = BWD ? nblk - 1 - j : j, q = BWD ? nblk - 1 - (j - kk) : j - kk;
+    const int64_t r0 = (int64_t)b * TBS, q0 = (int64_t)q * TBS;
+    const float *Ot = BWD ? Lp : Up;   // Op^T, column-major
+    for (int e = tid; e < TILE; e += 256) {
+        const int k = e >> 6, c = e & 63;
+        As[e] = Linv[(size_t)b * TILE + e];
+        Bs[k * CW + c] = Ot[(q0 + c) + (r0 + k) * Np];
+    }
+    __syncthreads();
+    float acc[4][4] = {};
+    tile_fma(acc, As, Bs, tr, tc);   // acc = Dinv Op
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) dst[(tc * 4 + jj) * TBS + tr * 4 + i] = -acc[i][jj];
+}
+
+// W (original row order, ldw) = lift(Xb) on Lambda_1 rows, 0 on Lambda_2 rows
+__global__ void k_lift_scatter(int64_t L, int ncol, int ncolp, const int32_t *__restrict__ pos1,
+                               const float *__restrict__ Xb, double *__restrict__ W, int64_t ldw) {
+    for (int c = blockIdx.y; c < ncol; c += gridDim.y)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t r = pos1[i];
+            W[i + (int64_t)c * ldw] = r >= 0 ? (double)Xb[(int64_t)r * ncolp + c] : 0.0;
+        }
+}
+
+constexpr int NTHR = 320;                 // 8 compute warps + 2 store warps (chain); helpers use 256
+constexpr int NCOMP = 256;
+constexpr int SMEM_FLOATS = 7 * TILE;     // 112 KB: chain = Yring[3] + M[2 stages][2]; helper = 2 x (A + B)
+
+template <bool BWD>
+__global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    __shared__ int item_s;
+    const int tid = threadIdx.x, tr = tid & 15, tc = (tid >> 4) & 15;
+    int *flags = a.flags + (BWD ? a.nblk * a.nch : 0);
+    int *pflags = a.pflags + (BWD ? a.nslots * a.nch : 0);
+    int *aflags = a.aflags + (BWD ? a.nblk * a.nch : 0);
+    int *counter = a.counter + (BWD ? 1 : 0);
+    unsigned *smids = a.smids + (BWD ? a.nch : 0);
+    const float *Op = BWD ? a.Up : a.Lp;
+    float *Yout = BWD ? a.Xb : a.Y;
+    const float *Dinv = BWD ? a.LinvB : a.LinvF;
+    auto phys = [&](int j) { return BWD ? (a.nblk - 1 - j) : j; };
+
+    if ((int)blockIdx.x < a.nch) {
+        // =================================================== CHAIN (chunk cc)
+        const int cc = blockIdx.x, c0 = cc * CW;
+        if (tid == 0) atomicExch(&smids[cc], smid() + 1u);
+        float *Yr = sm;               // [3][TILE] ring: Y_j in slot j % 3
+        float *Mb = sm + 3 * TILE;    // [2 stages][-M1, -M2]
+        if (tid >= NCOMP) {
+            // ---- store warps: slot j -> global, fence, release
+            const int st = tid - NCOMP;
+            for (int j = 0; j < a.nblk; ++j) {
+                bar_sync(1 + j % 3, NTHR);                // FULL(slot j % 3)
+                const float *ys = Yr + (j % 3) * TILE;
+                const int64_t r0 = (int64_t)phys(j) * TBS;
+#pragma unroll 4
+                for (int u = 0; u < 16; ++u) {
+                    const int e = st + u * 64;            // 1024 float4 = 64 rows x 16
+                    const int r = e >> 4, c4 = (e & 15) * 4;
+                    *reinterpret_cast<float4 *>(&Yout[(r0 + r) * a.ncolp + c0 + c4]) =
+                        *reinterpret_cast<const float4 *>(&ys[r * CW + c4]);
+                }
+                bar_sync(9, NTHR - NCOMP);
+                if (st == 0) {
+                    __threadfence();
+                    st_release32(&flags[j * a.nch + cc], a.epoch);
+                }
+                bar_arrive(6 + j % 3, NTHR);              // EMPTY(slot j % 3): may be reused
+            }
+            return;
+        }
+        // ---- compute warps
+        const float *Msrc = BWD ? a.MB : a.MF;
+        auto load_m = [&](int j) {
+            float *dst = Mb + (j & 1) * 2 * TILE;
+            const float *src = Msrc + (size_t)j * 2 * TILE;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = tid + u * NCOMP;
+                cp_async16(&dst[e * 4], src + e * 4);
+            }
+            cp_commit();
+        };
+        load_m(0);
+        const bool dbg = a.dbg && cc == 0 && tid == 0;
+        unsigned long long ph[4] = {0, 0, 0, 0}, tp = dbg ? gtimer() : 0;
+#define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
+        for (int j = 0; j < a.nblk; ++j) {
+            if (j + 1 < a.nblk) load_m(j + 1);
+            const int64_t r0 = (int64_t)phys(j) * TBS;
+            if (tid == 0) wait_epoch(&aflags[j * a.nch + cc], a.epoch);
+            bar_sync(4, NCOMP);
+            PH(0)
+            float acc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 v = *reinterpret_cast<const float4 *>(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4]);
+                acc[i][0] = v.x; acc[i][1] = v.y; acc[i][2] = v.z; acc[i][3] = v.w;
+            }
+            if (j + 1 < a.nblk) cp_wait_1(); else cp_wait_all();
+            bar_sync(4, NCOMP);
+            PH(1)
+            const float *M = Mb + (j & 1) * 2 * TILE;
+            if (j >= 1) tile_fma(acc, M, Yr + ((j - 1) % 3) * TILE, tr, tc);
+            if (j >= 2) tile_fma(acc, M + TILE, Yr + ((j - 2) % 3) * TILE, tr, tc);
+            PH(2)
+            if (j >= 3) bar_sync(6 + j % 3, NTHR);       // EMPTY: store warps are done with Y_{j-3}
+            float *ys = Yr + (j % 3) * TILE;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4 *>(&ys[(tr * 4 + i) * CW + tc * 4]) =
+                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            bar_sync(4, NCOMP);                           // slot complete for the compute warps ...
+            bar_arrive(1 + j % 3, NTHR);                  // ... FULL: handed to the store warps
+            PH(3)
+        }
+        for (int j = (a.nblk > 3 ? a.nblk - 3 : 0); j < a.nblk; ++j) bar_sync(6 + j % 3, NTHR);   // drain
+        if (dbg)
+            for (int q = 0; q < 4; ++q) atomicAdd(&a.dbg[(BWD ? 4 : 0) + q], ph[q]);
+#undef PH
+        return;
+    }
+
+    // ======================================================= HELPERS (256 threads)
+    if (tid >= NCOMP) return;
+    {
+        // leave the chain CTAs' SMs to them
+        __shared__ int leave;
+        if (tid == 0) {
+            const unsigned me = smid() + 1u;
+            int l = 0;
+            for (int c = 0; c < a.nch; ++c) {
+                unsigned v;
+                while ((v = *(volatile unsigned *)&smids[c]) == 0u) __nanosleep(64);
+                l |= (v == me);
+            }
+            leave = l;
+        }
+        bar_sync(5, NCOMP);
+        if (leave) return;
+    }
+    const float *src = Yout;
     auto load_dep = [&](int s, int64_t r0, int64_t q0, int c0) {
         float *As = sm + s * 2 * TILE;
         float *Bs = As + TILE;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int e = tid + u * 256;          // 1024 16-byte chunks per tile
+            const int e = tid + u * NCOMP;        // 1024 16-byte chunks per tile
             const int k = e >> 4, r4 = (e & 15) * 4;
             cp_async16(&As[k * TBS + r4], Op + (r0 + r4) + (q0 + k) * a.Np);
             cp_async16(&Bs[k * CW + r4], src + (q0 + k) * a.ncolp + c0 + r4);
         }
     };
+    auto wait_flag = [&](const int *f) {
+        if (tid == 0) wait_epoch(f, a.epoch);
+        bar_sync(5, NCOMP);
+    };
+    // t += sum over logical dependency blocks [q_lo, q_hi) of Op_bq Y_q, double buffered
+    auto accumulate = [&](float (&t)[4][4], int64_t r0, int c0, int cc, int q_lo, int q_hi) {
+        const int ndep = q_hi - q_lo;
+        if (ndep <= 0) return;
+        wait_flag(&flags[q_lo * a.nch + cc]);
+        load_dep(0, r0, (int64_t)phys(q_lo) * TBS, c0);
+        cp_commit();
+        for (int dq = 0; dq < ndep; ++dq) {
+            if (dq + 1 < ndep) {
+                wait_flag(&flags[(q_lo + dq + 1) * a.nch + cc]);
+                load_dep((dq + 1) & 1, r0, (int64_t)phys(q_lo + dq + 1) * TBS, c0);
+                cp_commit();
+                cp_wait_1();
+            } else {
+                cp_wait_all();
+            }
+            bar_sync(5, NCOMP);
+            const float *As = sm + (dq & 1) * 2 * TILE;
+            tile_fma(t, As, As + TILE, tr, tc);
+            bar_sync(5, NCOMP);
+        }
+    };
 
     for (;;) {
         if (tid == 0) item_s = atomicAdd(counter, 1);
-        __syncthreads();
-        const int item = item_s;
-        if (item >= nitems) return;
-        const int b = BWD ? (a.nblk - 1 - item / a.nch) : (item / a.nch);
-        const int cc = item % a.nch;
+        bar_sync(5, NCOMP);
+        const int idx = item_s;
+        if (idx >= a.nitems) return;
+        const int4 it = a.items[idx];
+        const int j = it.x, cc = it.y, sg = it.z, slot = it.w;
+        const int b = phys(j);
         const int64_t r0 = (int64_t)b * TBS;
         const int c0 = cc * CW;
+        float t[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) t[i][jj] = 0.f;
+        if (sg >= 0) {
+            // ---- PARTIAL item: t = sum over segment sg of Op_bq Y_q -> slot
+            accumulate(t, r0, c0, cc, sg * a.seg, (sg + 1) * a.seg);
+            float *pp = a.part + ((size_t)slot * a.nch + cc) * (TBS * CW);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4 *>(&pp[(tr * 4 + i) * CW + tc * 4]) =
+                    make_float4(t[i][0], t[i][1], t[i][2], t[i][3]);
+            bar_sync(5, NCOMP);
+            if (tid == 0) {
+                __threadfence();
+                st_release32(&pflags[slot * a.nch + cc], a.epoch);
+            }
+            continue;
+        }
+        // ---- P-item: t = partial slots in fixed order + the last segment (up to j-3)
+        const int nq = j > 2 ? j - 2 : 0;
+        const int nseg = (nq + a.seg - 1) / a.seg;
+        for (int s2 = 0; s2 + 1 < nseg; ++s2) {
+            const int sl = a.pbase[j] + s2;
+            wait_flag(&pflags[sl * a.nch + cc]);
+            const float *pp = a.part + ((size_t)sl * a.nch + cc) * (TBS * CW);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 v = *reinterpret_cast<const float4 *>(&pp[(tr * 4 + i) * CW + tc * 4]);
+                t[i][0] += v.x;
+                t[i][1] += v.y;
+                t[i][2] += v.z;
+                t[i][3] += v.w;
+            }
+        }
+        accumulate(t, r0, c0, cc, nseg > 0 ? (nseg - 1) * a.seg : 0, nq);
+        // right-hand side minus t: forward truncates R (FP64, original order)
+        // to FP32; backward starts from z = D^{-1} y
         float acc[4][4];
-        // ---- right-hand side: forward truncates R (FP64, original order) to FP32;
-        //      backward starts from z = D^{-1} y
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + tr * 4 + i;
             if (!BWD) {
                 const int64_t pr = r < a.N ? a.perm[r] : 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = c0 + tc * 4 + j;
-                    acc[i][j] = (r < a.N && c < a.ncol) ? __double2float_rn(a.R[pr + (int64_t)c * a.ldr]) : 0.f;
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int c = c0 + tc * 4 + jj;
+                    acc[i][jj] = (r < a.N && c < a.ncol) ? __double2float_rn(a.R[pr + (int64_t)c * a.ldr]) : 0.f;
                 }
             } else {
                 const float4 y = *reinterpret_cast<const float4 *>(&a.Y[r * a.ncolp + c0 + tc * 4]);
@@ -191,79 +456,36 @@ __global__ void __launch_bounds__(256, 3) k_trsm(TrsmArgs a) {
                 acc[i][2] = __fdiv_rn(y.z, d);
                 acc[i][3] = __fdiv_rn(y.w, d);
             }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) acc[i][jj] -= t[i][jj];
         }
-        // ---- off-diagonal blocks (forward: 0 .. b-1; backward: nblk-1 .. b+1),
-        //      double buffered: tiles of dependency dq+1 stream in during dq
-        const int ndep = BWD ? (a.nblk - 1 - b) : b;
-        auto dep_block = [&](int dq) { return BWD ? (a.nblk - 1 - dq) : dq; };
-        auto wait_flag = [&](int q) {
-            if (tid == 0) {
-                const int *f = &flags[q * a.nch + cc];
-                if (ld_relaxed32(f) != a.epoch) {
-                    while (ld_relaxed32(f) != a.epoch) __nanosleep(32);
-                }
-                fence_acquire();
-            }
-            __syncthreads();
-        };
-        if (ndep > 0) {
-            wait_flag(dep_block(0));
-            load_dep(0, r0, (int64_t)dep_block(0) * TBS, c0);
-            cp_commit();
-        }
-        for (int dq = 0; dq < ndep; ++dq) {
-            if (dq + 1 < ndep) {
-                wait_flag(dep_block(dq + 1));
-                load_dep((dq + 1) & 1, r0, (int64_t)dep_block(dq + 1) * TBS, c0);
-                cp_commit();
-                cp_wait_1();
-            } else {
-                cp_wait_all();
-            }
-            __syncthreads();
-            const float *As = sm + (dq & 1) * 2 * TILE;
-            tile_fms(acc, As, As + TILE, tr, tc);
-            __syncthreads();
-        }
-        // ---- diagonal block: out = Linv_b acc (forward) or Linv_b^T acc (backward)
+        // ---- P_j = Dinv_j acc
         {
             float *As = sm, *Bs = sm + TILE;
-            const float *Li = (BWD ? a.LinvB : a.LinvF) + (size_t)b * TILE;
+            const float *Li = Dinv + (size_t)b * TILE;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int e = tid + u * 256;
+                const int e = tid + u * NCOMP;
                 cp_async16(&As[e * 4], Li + e * 4);
             }
             cp_commit();
-            // Bs[k][c] = -acc (tile_fms subtracts)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
                 *reinterpret_cast<float4 *>(&Bs[(tr * 4 + i) * CW + tc * 4]) =
-                    make_float4(-acc[i][0], -acc[i][1], -acc[i][2], -acc[i][3]);
+                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
             cp_wait_all();
-            __syncthreads();
+            bar_sync(5, NCOMP);
             float out[4][4] = {};
-            tile_fms(out, As, Bs, tr, tc);
-            // ---- store
+            tile_fma(out, As, Bs, tr, tc);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t r = r0 + tr * 4 + i;
-                float *dst = (BWD ? a.Xb : a.Y) + r * a.ncolp + c0 + tc * 4;
-                *reinterpret_cast<float4 *>(dst) = make_float4(out[i][0], out[i][1], out[i][2], out[i][3]);
-                if (BWD && r < a.N) {
-                    const int64_t pr = a.perm[r];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int c = c0 + tc * 4 + j;
-                        if (c < a.ncol) a.W[pr + (int64_t)c * a.ldw] = (double)out[i][j];   // lift + scatter
-                    }
-                }
-            }
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4 *>(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4]) =
+                    make_float4(out[i][0], out[i][1], out[i][2], out[i][3]);
         }
-        __syncthreads();
+        bar_sync(5, NCOMP);
         if (tid == 0) {
             __threadfence();
-            st_release32(&flags[b * a.nch + cc], a.epoch);
+            st_release32(&aflags[j * a.nch + cc], a.epoch);
         }
     }
 }
@@ -271,12 +493,13 @@ __global__ void __launch_bounds__(256, 3) k_trsm(TrsmArgs a) {
 }  // namespace
 
 void precond_setup(hf_ctx *ctx, Precond &p, int64_t N, int64_t L, const float *Lfac, const float *D,
-                   const int64_t *perm) {
+                   const int64_t *perm, const int32_t *pos1) {
     p.N = N;
     p.L = L;
     p.Lfac = Lfac;
     p.D = D;
     p.perm = perm;
+    p.pos1 = pos1;
     if (N == 0) return;
     cudaStream_t st = ctx->stream;
     const int64_t nblk = cdiv(N, TBS);
@@ -285,47 +508,145 @@ void precond_setup(hf_ctx *ctx, Precond &p, int64_t N, int64_t L, const float *L
     p.Up.alloc((size_t)p.Np * p.Np, st);
     p.LinvF.alloc((size_t)nblk * TILE, st);
     p.LinvB.alloc((size_t)nblk * TILE, st);
+    p.MF.alloc((size_t)nblk * 2 * TILE, st);
+    p.MB.alloc((size_t)nblk * 2 * TILE, st);
     ClassTimer tm(ctx, "trsm");
     dim3 g((unsigned)(p.Np / 32), (unsigned)(p.Np / 32));
     k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Lfac, p.Lp.p, p.Up.p);
     HF_CHECK_LAUNCH(ctx);
     k_diag_inv<<<(unsigned)nblk, TBS, 0, st>>>(p.Np, p.Lp.p, p.LinvF.p, p.LinvB.p);
     HF_CHECK_LAUNCH(ctx);
+    dim3 gm((unsigned)nblk, 2);
+    k_mk<false><<<gm, 256, 0, st>>>((int)nblk, p.Np, p.Lp.p, p.Up.p, p.LinvF.p, p.MF.p);
+    HF_CHECK_LAUNCH(ctx);
+    k_mk<true><<<gm, 256, 0, st>>>((int)nblk, p.Np, p.Lp.p, p.Up.p, p.LinvB.p, p.MB.p);
+    HF_CHECK_LAUNCH(ctx);
+}
+
+// Helper item table in topological order.  Logical blocks j (forward j = b,
+// backward j = nblk-1-b); P_j depends on chain outputs 0..j-3 and on its
+// partial slots.  Items are placed by the chain stage after which they can
+// run: P-item(j) at stage j-3; PARTIAL(j, s) (segment [s*seg, (s+1)*seg) of
+// the dependency range [0, j-2), all but its last segment) at stage
+// max((s+1)*seg - 1, j-3-LA), LA = lookahead, so bulk work is queued just
+// ahead of the chain instead of in front of it.  Within a stage: P-items
+// first.  Every item depends only on earlier items and on chain stages <=
+// its own stage, so persistent CTAs taking items in order cannot deadlock.
+static void build_items(int nblk, int nch, int seg, std::vector<int4> &items, std::vector<int> &pbase, int &nslots) {
+    const int LA = 24;
+    pbase.assign(nblk, 0);
+    nslots = 0;
+    std::vector<std::vector<int4>> stage(nblk + 2);   // stage s -> index s+1 (stage -1 first)
+    for (int j = 0; j < nblk; ++j) {
+        pbase[j] = nslots;
+        const int nq = j > 2 ? j - 2 : 0;
+        const int nseg = (nq + seg - 1) / seg;
+        nslots += std::max(0, nseg - 1);
+    }
+    for (int j = 0; j < nblk; ++j) {
+        const int st = std::max(-1, j - 3);
+        for (int c = 0; c < nch; ++c) stage[st + 1].push_back(make_int4(j, c, -1, -1));
+    }
+    for (int j = 0; j < nblk; ++j) {
+        const int nq = j > 2 ? j - 2 : 0;
+        const int nseg = (nq + seg - 1) / seg;
+        for (int s = 0; s + 1 < nseg; ++s) {
+            const int st = std::max((s + 1) * seg - 1, j - 3 - LA);
+            for (int c = 0; c < nch; ++c) stage[st + 1].push_back(make_int4(j, c, s, pbase[j] + s));
+        }
+    }
+    items.clear();
+    for (auto &v : stage)
+        for (auto &x : v) items.push_back(x);
 }
 
 void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64_t ldr, double *W, int64_t ldw) {
     cudaStream_t st = ctx->stream;
-    HF_CUDA(cudaMemset2DAsync(W, ldw * sizeof(double), 0, p.L * sizeof(double), ncol, st));
-    if (p.N == 0 || ncol == 0) return;
+    if (ncol == 0) return;
+    if (p.N == 0) {
+        HF_CUDA(cudaMemset2DAsync(W, ldw * sizeof(double), 0, p.L * sizeof(double), ncol, st));
+        return;
+    }
     const int nblk = (int)(p.Np / TBS);
     const int nch = (int)cdiv(ncol, CW);
     const int ncolp = nch * CW;
+    const int seg = std::max(8, (int)cdiv(nblk, 32));
     p.Y.alloc((size_t)p.Np * ncolp, st);
     p.Xb.alloc((size_t)p.Np * ncolp, st);
-    if (p.flags.n < (size_t)2 * nblk * nch) {
-        p.flags.alloc((size_t)2 * nblk * nch, st);
+    p.P.alloc((size_t)p.Np * ncolp, st);
+    if (p.tab_nblk != nblk || p.tab_nch != nch) {
+        auto key = std::make_pair(nblk, nch);
+        auto it = ctx->trsm_tables.find(key);
+        if (it == ctx->trsm_tables.end()) {
+            std::vector<int4> items;
+            std::vector<int> pbase;
+            TrsmTable t;
+            build_items(nblk, nch, seg, items, pbase, t.nslots);
+            t.items.alloc(items.size(), st);
+            t.pbase.alloc(pbase.size(), st);
+            HF_CUDA(cudaMemcpyAsync(t.items.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            HF_CUDA(cudaMemcpyAsync(t.pbase.p, pbase.data(), pbase.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            HF_CUDA(cudaStreamSynchronize(st));   // host vectors die here (once per shape and context)
+            t.nitems = (int)items.size();
+            it = ctx->trsm_tables.emplace(key, std::move(t)).first;
+        }
+        p.items = it->second.items.p;
+        p.pbase = it->second.pbase.p;
+        p.nitems = it->second.nitems;
+        p.nslots = it->second.nslots;
+        p.tab_nblk = nblk;
+        p.tab_nch = nch;
+        p.part.alloc((size_t)std::max(p.nslots, 1) * nch * TBS * CW, st);
+        p.pflags.alloc((size_t)2 * std::max(p.nslots, 1) * nch, st);
+        p.pflags.zero(st);
+        p.flags.alloc((size_t)4 * nblk * nch, st);   // [chain flags x2 | P flags x2]
         p.flags.zero(st);
         p.epoch = 0;
     }
-    p.counter.alloc(2, st);
-    HF_CUDA(cudaMemsetAsync(p.counter.p, 0, 2 * sizeof(int), st));
+    p.counter.alloc(2 + 2 * (size_t)nch, st);      // [2 counters | 2 x nch SM ids]
+    HF_CUDA(cudaMemsetAsync(p.counter.p, 0, (2 + 2 * (size_t)nch) * sizeof(int), st));
     p.epoch += 1;
-    TrsmArgs a{p.N, p.Np, (int)ncol, ncolp, nch, nblk, p.Lp.p, p.Up.p, p.LinvF.p, p.LinvB.p, p.D, p.perm,
-               R, ldr, p.Y.p, p.Xb.p, W, ldw, p.flags.p, p.counter.p, p.epoch};
-    const size_t shm = (size_t)4 * TILE * sizeof(float);   // 2 stages x (A + B) = 64 KB
-    static bool attr = false;
-    if (!attr) {
+    TrsmArgs a{p.N, p.Np, (int)ncol, ncolp, nch, nblk, seg, p.items, p.nitems, p.pbase, p.part.p,
+               p.P.p, p.pflags.p, p.flags.p + 2 * nblk * nch, p.nslots, p.Lp.p, p.Up.p, p.LinvF.p, p.LinvB.p,
+               p.MF.p, p.MB.p, p.D, p.perm, R, ldr, p.Y.p, p.Xb.p, p.flags.p, p.counter.p,
+               reinterpret_cast<unsigned *>(p.counter.p + 2), p.epoch, nullptr};
+    const bool want_dbg = getenv("HF_TRSM_DEBUG") != nullptr;
+    if (want_dbg) {
+        p.dbg.alloc(8, st);
+        p.dbg.zero(st);
+        a.dbg = p.dbg.p;
+    }
+    const size_t shm = (size_t)SMEM_FLOATS * sizeof(float);
+    static int per_sm = 0;
+    if (!per_sm) {
         HF_CUDA(cudaFuncSetAttribute(k_trsm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         HF_CUDA(cudaFuncSetAttribute(k_trsm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        attr = true;
+        int a0 = 0, a1 = 0;
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a0, k_trsm<false>, NTHR, shm));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_trsm<true>, NTHR, shm));
+        per_sm = std::max(1, std::min(a0, a1));
     }
-    const int nitems = nblk * nch;
-    const int grid = std::min(nitems, ctx->num_sms * 3);
+    // helpers that share an SM with a chain CTA leave, so launch more than 2 nch
+    const int grid = std::min(std::max(2 * nch + 1, nch + p.nitems + per_sm), ctx->num_sms * per_sm);
+    HF_REQUIRE(grid >= 2 * nch + 1, "preconditioner: too many RHS chunks for one launch");
     ClassTimer tm(ctx, "trsm");
-    k_trsm<false><<<grid, 256, shm, st>>>(a);
+    void *args[] = {&a};
+    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_trsm<false>, dim3(grid), dim3(NTHR), args, shm, st));
     HF_CHECK_LAUNCH(ctx);
-    k_trsm<true><<<grid, 256, shm, st>>>(a);
+    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_trsm<true>, dim3(grid), dim3(NTHR), args, shm, st));
     HF_CHECK_LAUNCH(ctx);
+    dim3 gl((unsigned)std::min<int64_t>(cdiv(p.L, 256), 1024), (unsigned)std::min<int64_t>(ncol, 1024));
+    k_lift_scatter<<<gl, 256, 0, st>>>(p.L, (int)ncol, ncolp, p.pos1, p.Xb.p, W, ldw);
+    HF_CHECK_LAUNCH(ctx);
+    if (want_dbg) {
+        unsigned long long h[8];
+        HF_CUDA(cudaMemcpyAsync(h, p.dbg.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        HF_CUDA(cudaStreamSynchronize(st));
+        for (int d = 0; d < 2; ++d)
+            fprintf(stderr, "[hf trsm %s] nblk %d nch %d grid %d items %d | us/link: wait-P %.3f  load %.3f  compute %.3f  store %.3f\n",
+                    d ? "bwd" : "fwd", nblk, nch, grid, p.nitems, h[4 * d] / 1e3 / nblk, h[4 * d + 1] / 1e3 / nblk,
+                    h[4 * d + 2] / 1e3 / nblk, h[4 * d + 3] / 1e3 / nblk);
+    }
 }
 
 }  // namespace hf

@@ -28,6 +28,7 @@ EXPORTED = [
     "hf_set_profiling", "hf_kernel_stats", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
+    "hf_precond_apply",
 ]
 
 
@@ -85,6 +86,7 @@ def load() -> ctypes.CDLL:
         "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
         "hf_hybrid_destroy": [vp],
         "hf_trim_cache": [ctypes.c_int],
+        "hf_precond_apply": [vp, vp, i64, vp, i64, vp, i64],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -281,6 +283,20 @@ class Hybrid:
             self.close()
         except Exception:
             pass
+
+
+def hf_precond_apply(ctx: Context, lf: LowFactor, R: torch.Tensor, W: torch.Tensor | None = None) -> torch.Tensor:
+    """W = Q^{-1} R (FP32 preconditioner, [R12]).  R: device FP64 L x ncol in
+    column-major layout (R.stride() == (1, L), e.g. ``t.T`` of a contiguous
+    (ncol, L) tensor), original row order.  Returns W in the same layout."""
+    if not (isinstance(R, torch.Tensor) and R.is_cuda and R.dtype == torch.float64 and R.dim() == 2
+            and R.shape[0] == lf.L and (R.shape[1] <= 1 or R.stride() == (1, lf.L))):
+        raise TypeError("R must be a column-major CUDA float64 (L, ncol) tensor")
+    ncol = R.shape[1]
+    if W is None:
+        W = torch.empty(ncol, lf.L, dtype=torch.float64, device=R.device).T
+    ctx.check(ctx.lib.hf_precond_apply(ctx.h, lf.h, ncol, _ptr(R), lf.L, _ptr(W), lf.L))
+    return W
 
 
 def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-14, max_iter: int = 100,

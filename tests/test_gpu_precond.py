@@ -1,0 +1,81 @@
+"""GPU parity of the FP32 preconditioner Q^{-1} ([R12]) through
+hf_precond_apply: the blocked dataflow TRSM pair (any summation order is
+allowed, so the bar is relative to the oracle's own FP32 error against the
+FP64 solve with the SAME FP32 factor, which is bit-identical on both sides)."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import torch
+
+import hf_inputs as hi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+def _exact(F, Rp):
+    """FP64 solve with the FP32 factor (reference for both FP32 results)."""
+    Lf = F.Lfac.astype(np.float64)
+    y = sla.solve_triangular(Lf, Rp.astype(np.float32).astype(np.float64), lower=True, unit_diagonal=True)
+    y = y / F.D.astype(np.float64)[:, None]
+    return sla.solve_triangular(Lf, y, lower=True, trans="T", unit_diagonal=True)
+
+
+# (config, seed, ncol): ragged row blocks (N % 64 != 0), chunk tails (ncol % 64 != 0),
+# several chunks, a single column (Alg. 2's solve)
+CASES = [("P512", 0, 8), ("P1024", 1, 130), ("N32", 0, 1), ("S24", 0, 64), ("C1", 0, 4), ("P2048", 0, 200)]
+
+
+@pytest.mark.parametrize("name,seed,ncol", CASES)
+def test_precond_apply_vs_oracle(ctx, name, seed, ncol):
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, _ = oracle.scale(Kb.numpy())
+    F = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    Kd = Kb.cuda()
+    hf.hf_scale(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
+    assert lf.N == F.N
+    L = Ko.shape[0]
+    rng = np.random.default_rng(seed + 7)
+    R = rng.standard_normal((L, ncol))
+    Rd = torch.from_numpy(np.ascontiguousarray(R.T)).cuda().T
+    W = hf.hf_precond_apply(ctx, lf, Rd).cpu().numpy()
+    l1, l2 = F.perm[: F.N], F.perm[F.N:]
+    assert np.all(W[l2] == 0.0)
+    Wg = W[l1]
+    Wo = oracle.precond_apply(F, R[l1])
+    Wx = _exact(F, R[l1])
+    nx = np.linalg.norm(Wx, axis=0)
+    eg = np.linalg.norm(Wg - Wx, axis=0) / nx
+    eo = np.linalg.norm(Wo - Wx, axis=0) / nx
+    # blocked solves with explicit 64x64 diagonal-block inverses (and the chain's
+    # Dinv_b L_{b,b-k} products) round differently from substitution; the bar is
+    # the oracle's own FP32 error level, over the columns (max and median)
+    assert eg.max() <= max(10 * eo.max(), 1e-6), (eg.max(), eo.max())
+    assert np.median(eg) <= max(10 * np.median(eo), 1e-6), (np.median(eg), np.median(eo))
+
+
+def test_precond_apply_exact_cases(ctx):
+    """Diagonal K: L = I, so Q^{-1} r = RN32(r) / D exactly (S:287's diag example scaled)."""
+    from paper_2208_01907_b200 import hf
+    d = torch.tensor([2.0, -4.0, 0.5, 8.0, 1.0], dtype=torch.float64)
+    Kd = torch.diag(d).cuda()
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=1e-3)
+    assert lf.N == 5
+    R = torch.tensor([[2.0, -4.0, 1.0, 8.0, 3.0], [1.0, 1.0, 1.0, 1.0, 1.0]], dtype=torch.float64).cuda().T
+    W = hf.hf_precond_apply(ctx, lf, R).cpu().numpy()
+    dn = d.numpy()
+    assert np.array_equal(W[:, 0], (np.float32([2.0, -4.0, 1.0, 8.0, 3.0]) / np.float32(dn)).astype(np.float64))
+    assert np.array_equal(W[:, 1], (np.float32(1.0) / np.float32(dn)).astype(np.float64))
