@@ -10,9 +10,9 @@
 //    "ties -> smallest position".
 //  * k_chain: one cooperative persistent launch per panel, one CTA per SM.
 //    Each CTA owns a contiguous slice of rows and keeps their panel values
-//    -sigma_u s_i^u in shared memory.  Per pivot: local argmax -> one 64-bit
-//    key per CTA published to a tagged global slot -> every CTA reduces all
-//    slots (the only grid-wide exchange) -> the pivot column is assembled
+//    -sigma_u s_i^u in shared memory.  Per pivot: local argmax -> red.max of
+//    a 64-bit key + one release-add on an arrival counter (the only
+//    grid-wide exchange) -> the pivot column is assembled
 //    from the panel-start matrix plus the in-panel updates, one fmaf per
 //    earlier in-panel pivot in increasing order [R8] -> s_i = c_i / sqrt|d|,
 //    L_ik = c_i / d, lazy diagonal update.
@@ -107,12 +107,19 @@ struct ChainArgs {
     int64_t ldl;
     float *Dk;          // [L] d_k
     int32_t *pivorig;   // [L] original index of pivot k
-    unsigned long long *keys;  // [nbp] per-step max key (zeroed before the launch)
-    unsigned int *cnt;         // arrival counter (zeroed before the launch)
-    float *mbox;        // [2][G][nb] candidate-row mailboxes (-sigma_u s_P^u)
+    unsigned long long *keys;    // [nbp] per-step max key (zeroed before the launch)
+    unsigned int *cnt;           // arrival counter (zeroed before the launch)
+    unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
     unsigned long long *dbg;   // optional per-phase time sums (CTA 0), HF_CHAIN_DEBUG
 };
+
+constexpr uint64_t TAGM = 0x3FFF;   // 14-bit step tag in the low bits of every exchanged word
+__device__ __forceinline__ uint64_t step_tag(int64_t k) { return (uint64_t)(k % 16383) + 1; }
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -122,14 +129,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Per pivot k = K0 + t (all CTAs in lock step):
 //  A  local argmax over own active rows -> CTA key (warp shuffles + smem)
-//  B  warp 0 writes the candidate row's panel values to this CTA's mailbox,
-//     red.max of the key into keys[t], red.release.add on the arrival counter
-//  C  the PREVIOUS step's s / L values of own rows go to global memory now,
-//     after the release, so the release never waits on them
-//  D  one thread per CTA polls the counter (acquire) and reads keys[t]
-//  E  stop test [R4]; F  pivot-row panel values from the winner's mailbox and
-//     the panel-start column V[:, P] for own rows; G  c_i = chain of fmaf over
-//     the earlier in-panel pivots in order [R8], s = c/r, L = c/d, diagonal.
+//  B  warp 0: red.max of the key into keys[t], then red.release.add on the
+//     arrival counter (the release orders only that red.max);
+//     warp 1: the candidate row's panel values to this CTA's mailbox as
+//     "LL" words (float bits << 32 | step tag), so no fence orders them --
+//     a reader validates every word by its tag (double buffered by step
+//     parity, so a fast CTA never overwrites a word a slow one still needs)
+//  C  the PREVIOUS step's s / L values of own rows go to global memory now
+//  D  one thread per CTA polls the counter, acquires, reads keys[t]
+//  E  stop test [R4]; F  pivot-row panel values from the winner's mailbox
+//     (tag-checked) and the panel-start column V[:, P] for own rows;
+//  G  c_i = chain of fmaf over the earlier in-panel pivots in order [R8],
+//     s = c/r, L = c/d, diagonal.
 __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     extern __shared__ float smem[];
     __shared__ unsigned long long red[32];
@@ -160,24 +171,26 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
 #define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
     for (; t < nb; ++t) {
         const int64_t k = a.K0 + t;
+        const uint64_t tag = step_tag(k);
         // ---- A: [R3] local argmax of |diag| over own active rows
         uint64_t key = piv ? 0ull : mkkey(dg, (uint32_t)i);
         key = warp_max64(key);
         if (lane == 0) red[wid] = key;
         __syncthreads();
         // ---- B: publish
-        if (wid == 0) {
+        if (wid < 2) {
             uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
             v = warp_max64(v);
-            float *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * nb;
-            if (v) {
+            if (wid == 0) {
+                if (lane == 0) {
+                    if (v) red_max_u64(&a.keys[t], v);
+                    red_release_add(a.cnt, 1u);
+                }
+            } else if (v) {
+                unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * nb;
                 const int lr = (int)((int64_t)(POS_MAX - (uint32_t)((v >> 15) & POS_MAX)) - r0);
-                for (int u = lane; u < t; u += 32) mb[u] = sneg[(size_t)u * a.R + lr];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                if (v) red_max_u64(&a.keys[t], v);
-                red_release_add(a.cnt, 1u);
+                for (int u = lane; u < t; u += 32)
+                    st_relaxed_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + lr]) << 32) | tag);
             }
         }
         // ---- C: deferred global stores of step t-1
@@ -218,8 +231,14 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- F: [R6] pivot row from the winner's mailbox, stale column for own rows
         {
             const int owner = (int)(P / a.R);
-            const float *mb = a.mbox + ((size_t)(t & 1) * G + owner) * nb;
-            for (int u = tid; u < t; u += nthr) sp[u] = -sgm[u] * mb[u];   // s_P^u (exact sign flip)
+            const unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + owner) * nb;
+            for (int u = tid; u < t; u += nthr) {
+                uint64_t w;
+                do {
+                    w = ld_relaxed_u64(&mb[u]);
+                } while ((w & TAGM) != tag);
+                sp[u] = -sgm[u] * __uint_as_float((uint32_t)(w >> 32));   // s_P^u (exact sign flip)
+            }
             if (tid == 0) sgm[t] = sg;
         }
         float v = 0.f;
@@ -505,11 +524,12 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     pivpos.alloc(nb, st);
     pivorig.alloc(L, st);
     status.alloc(4, st);
-    // per-launch exchange state: keys[nb] + counter, zeroed before every chain launch
-    DBuf<unsigned long long> xchg;
+    // per-launch exchange state: keys[nb] + counter, zeroed before every chain launch;
+    // mailbox words are tagged (self-validating), zeroed once
+    DBuf<unsigned long long> xchg, mbox;
     xchg.alloc((size_t)nb + 2, st);
-    DBuf<float> mbox;
     mbox.alloc((size_t)2 * nsm * nb, st);
+    mbox.zero(st);
     HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
 
     {
