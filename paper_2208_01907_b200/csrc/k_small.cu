@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_spd_inv(int64_t n, const double *__rest
 }
 
 // ------------------------------------------------------------------ hard factorization
-// Bunch-Parlett complete pivoting on A = (S22 + S22^T)/2 [R15].  Single CTA.
+// Bunch-Parlett complete pivoting on A = (S22 + S22^T)/2 [R15].
 // A: n x n workspace (full symmetric), Lh: n x n, Dh: n x n, lab: labels.
 struct Best {
     double v;
@@ -163,137 +163,189 @@ __device__ Best block_best(Best b, Best *sh) {
     return r;
 }
 
-__global__ void __launch_bounds__(512) k_hard_factor(int64_t n, const double *__restrict__ S, double thr,
-                                                     double *__restrict__ A, double *__restrict__ Lh,
-                                                     double *__restrict__ Dh, int32_t *__restrict__ lab,
-                                                     int32_t *__restrict__ blocks, int64_t *rank_out) {
-    __shared__ Best sh[512];
-    __shared__ double E[4];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t tot = n * n;
-    for (int64_t e = tid; e < tot; e += nt) {
-        const int64_t i = e % n, j = e / n;
-        A[e] = 0.5 * (S[i + j * n] + S[j + i * n]);
-        Lh[e] = (i == j) ? 1.0 : 0.0;
-        Dh[e] = 0.0;
-    }
-    for (int64_t i = tid; i < n; i += nt) {
-        lab[i] = (int32_t)i;
-        blocks[i] = 0;
-    }
-    __syncthreads();
+// Multi-CTA version (one cooperative launch, any n): no physical swaps --
+// indices keep their Lambda_2 position as label, an active flag marks the
+// trailing block.  CTA c owns columns j = c, c+G, ... of the FULL symmetric
+// work matrix (both triangles are updated with commutative formulas, so A
+// stays bitwise symmetric).  Per step: search (per-CTA best diagonal and
+// off-diagonal, ties by labels) -> grid barrier -> every CTA reduces the G
+// partial bests and takes the same decision -> rank-1 / rank-2 update of its
+// columns + the L column(s) -> grid barrier.  Two grid barriers per pivot.
+__global__ void __launch_bounds__(256) k_hard_factor_mc(int64_t n, const double *__restrict__ S, double thr,
+                                                        double *__restrict__ A, double *__restrict__ Lcol,
+                                                        int32_t *__restrict__ act, int32_t *__restrict__ posof,
+                                                        Best *__restrict__ gbest, double *__restrict__ Dh,
+                                                        int32_t *__restrict__ blocks, int32_t *__restrict__ pivots,
+                                                        int64_t *rank_out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ Best sh[256];
+    __shared__ Best sdg, soff;
+    const int G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+    const int c = blockIdx.x;
+    // A = (S + S^T)/2, Dh = 0, flags
+    for (int64_t j = c; j < n; j += G)
+        for (int64_t i = tid; i < n; i += nt) {
+            A[i + j * n] = 0.5 * (S[i + j * n] + S[j + i * n]);
+            Dh[i + j * n] = 0.0;
+        }
+    if (c == 0)
+        for (int64_t i = tid; i < n; i += nt) {
+            act[i] = 1;
+            posof[i] = -1;
+            blocks[i] = 0;
+        }
+    grid.sync();
     const double alpha = (1.0 + sqrt(17.0)) / 8.0;
     int64_t k = 0, nblk = 0;
     while (k < n) {
-        // mu0: max |A_ij| over the trailing block (lower part suffices: A symmetric)
-        // off: best off-diagonal (i > j) with label tie-break; dg: best diagonal
+        // ---- search over own active columns
         Best bo{-1.0, 0, 0, -1, -1}, bd{-1.0, 0, 0, -1, -1};
-        const int64_t m = n - k;
-        for (int64_t e = tid; e < m * m; e += nt) {
-            const int64_t i = k + e % m, j = k + e / m;
-            if (i < j) continue;
-            const double v = fabs(A[i + j * n]);
-            if (i == j) {
-                Best c{v, lab[i], 0, i, i};
-                if (better(c, bd)) bd = c;
-            } else {
-                const int64_t la = min(lab[i], lab[j]), lb = max(lab[i], lab[j]);
-                Best c{v, la, lb, i, j};
-                if (better(c, bo)) bo = c;
+        for (int64_t j = c; j < n; j += G) {
+            if (!act[j]) continue;
+            const double *aj = A + j * n;
+            for (int64_t i = tid; i < n; i += nt) {
+                if (!act[i]) continue;
+                const double v = fabs(aj[i]);
+                if (i == j) {
+                    Best cd{v, i, 0, i, i};
+                    if (better(cd, bd)) bd = cd;
+                } else {
+                    Best cd{v, min(i, j), max(i, j), i, j};
+                    if (better(cd, bo)) bo = cd;
+                }
             }
         }
         bd = block_best(bd, sh);
         bo = block_best(bo, sh);
-        const double mu1 = bd.v, mu0 = fmax(bd.v, bo.v);
-        if (mu0 <= thr) break;
+        if (tid == 0) {
+            gbest[2 * c] = bd;
+            gbest[2 * c + 1] = bo;
+        }
+        grid.sync();
+        // ---- every CTA: the same decision from the G partial bests
+        if (tid < 32) {
+            Best d0{-1.0, 0, 0, -1, -1}, o0{-1.0, 0, 0, -1, -1};
+            for (int g = tid; g < G; g += 32) {
+                if (better(gbest[2 * g], d0)) d0 = gbest[2 * g];
+                if (better(gbest[2 * g + 1], o0)) o0 = gbest[2 * g + 1];
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                Best x{__shfl_xor_sync(0xffffffffu, d0.v, o), __shfl_xor_sync(0xffffffffu, d0.k1, o),
+                       __shfl_xor_sync(0xffffffffu, d0.k2, o), __shfl_xor_sync(0xffffffffu, d0.i, o),
+                       __shfl_xor_sync(0xffffffffu, d0.j, o)};
+                if (better(x, d0)) d0 = x;
+                Best y{__shfl_xor_sync(0xffffffffu, o0.v, o), __shfl_xor_sync(0xffffffffu, o0.k1, o),
+                       __shfl_xor_sync(0xffffffffu, o0.k2, o), __shfl_xor_sync(0xffffffffu, o0.i, o),
+                       __shfl_xor_sync(0xffffffffu, o0.j, o)};
+                if (better(y, o0)) o0 = y;
+            }
+            if (tid == 0) {
+                sdg = d0;
+                soff = o0;
+            }
+        }
+        __syncthreads();
+        const Best d0 = sdg, o0 = soff;
+        const double mu1 = d0.v, mu0 = fmax(d0.v, o0.v);
+        if (mu0 <= thr) break;   // uniform across the grid
         if (mu1 >= alpha * mu0) {
-            // ---- 1x1 pivot at bd.i
-            const int64_t p = bd.i;
-            // swap k <-> p (rows/cols of A, rows of Lh[:, :k], labels)
-            if (p != k) {
-                for (int64_t c = tid; c < n; c += nt) {
-                    double t = A[k + c * n]; A[k + c * n] = A[p + c * n]; A[p + c * n] = t;
-                }
-                __syncthreads();
-                for (int64_t r = tid; r < n; r += nt) {
-                    double t = A[r + k * n]; A[r + k * n] = A[r + p * n]; A[r + p * n] = t;
-                }
-                for (int64_t c = tid; c < k; c += nt) {
-                    double t = Lh[k + c * n]; Lh[k + c * n] = Lh[p + c * n]; Lh[p + c * n] = t;
-                }
-                if (tid == 0) { int32_t t = lab[k]; lab[k] = lab[p]; lab[p] = t; }
-                __syncthreads();
+            // ---- 1x1 pivot at p = d0.i
+            const int64_t p = d0.i;
+            const double d = A[p + p * n];
+            const double *ap = A + p * n;
+            for (int64_t j = c; j < n; j += G) {
+                if (!act[j] || j == p) continue;
+                double *aj = A + j * n;
+                const double apj = ap[j];
+                for (int64_t i = tid; i < n; i += nt)
+                    if (act[i] && i != p) aj[i] -= (ap[i] * apj) / d;
             }
-            const double d = A[k + k * n];
-            // A[i,j] -= (c_i c_j) / d  for i, j > k  (exactly symmetric)
-            for (int64_t e = tid; e < (m - 1) * (m - 1); e += nt) {
-                const int64_t i = k + 1 + e % (m - 1), j = k + 1 + e / (m - 1);
-                A[i + j * n] -= (A[i + k * n] * A[j + k * n]) / d;
+            if (c == 0) {
+                for (int64_t i = tid; i < n; i += nt) Lcol[i + k * n] = (act[i] && i != p) ? ap[i] / d : 0.0;
+                if (tid == 0) {
+                    Dh[k + k * n] = d;
+                    blocks[nblk] = 1;
+                    pivots[k] = (int32_t)p;
+                }
             }
-            __syncthreads();
-            for (int64_t i = k + 1 + tid; i < n; i += nt) {
-                Lh[i + k * n] = A[i + k * n] / d;
-                A[i + k * n] = 0.0;
-                A[k + i * n] = 0.0;
+            grid.sync();   // column p / labels read above before the flags change
+            if (c == 0 && tid == 0) {
+                act[p] = 0;
+                posof[p] = (int32_t)k;
             }
-            if (tid == 0) { Dh[k + k * n] = d; blocks[nblk] = 1; }
             ++nblk;
             k += 1;
         } else {
-            // ---- 2x2 pivot on the best off-diagonal pair, smaller label first
-            int64_t i = bo.i, j = bo.j;
-            if (lab[i] > lab[j]) { int64_t t = i; i = j; j = t; }
-            for (int s = 0; s < 2; ++s) {
-                const int64_t dst = k + s;
-                int64_t p = (s == 0) ? i : j;
-                if (s == 1 && j == k) p = i;   // j was moved by the first swap
-                if (p != dst) {
-                    for (int64_t c = tid; c < n; c += nt) {
-                        double t = A[dst + c * n]; A[dst + c * n] = A[p + c * n]; A[p + c * n] = t;
-                    }
-                    __syncthreads();
-                    for (int64_t r = tid; r < n; r += nt) {
-                        double t = A[r + dst * n]; A[r + dst * n] = A[r + p * n]; A[r + p * n] = t;
-                    }
-                    for (int64_t c = tid; c < k; c += nt) {
-                        double t = Lh[dst + c * n]; Lh[dst + c * n] = Lh[p + c * n]; Lh[p + c * n] = t;
-                    }
-                    if (tid == 0) { int32_t t = lab[dst]; lab[dst] = lab[p]; lab[p] = t; }
-                    __syncthreads();
+            // ---- 2x2 pivot on (p, q), smaller label first
+            const int64_t p = min(o0.i, o0.j), q = max(o0.i, o0.j);
+            const double a_ = A[p + p * n], b_ = A[q + p * n], c_ = A[q + q * n];
+            const double det = a_ * c_ - b_ * b_;
+            const double E0 = c_ / det, E1 = -b_ / det, E2 = -b_ / det, E3 = a_ / det;
+            const double *ap = A + p * n, *aq = A + q * n;
+            for (int64_t j = c; j < n; j += G) {
+                if (!act[j] || j == p || j == q) continue;
+                double *aj = A + j * n;
+                const double cc0 = ap[j], cc1 = aq[j];
+                const double lc0 = cc0 * E0 + cc1 * E1, lc1 = cc0 * E2 + cc1 * E3;
+                for (int64_t i = tid; i < n; i += nt) {
+                    if (!act[i] || i == p || i == q) continue;
+                    const double cr0 = ap[i], cr1 = aq[i];
+                    const double lr0 = cr0 * E0 + cr1 * E1, lr1 = cr0 * E2 + cr1 * E3;
+                    const double t1 = lr0 * cc0 + lr1 * cc1, t2 = lc0 * cr0 + lc1 * cr1;
+                    aj[i] -= 0.5 * (t1 + t2);
                 }
             }
-            if (tid == 0) {
-                const double a = A[k + k * n], b = A[k + 1 + k * n], c = A[k + 1 + (k + 1) * n];
-                const double det = a * c - b * b;
-                E[0] = c / det; E[1] = -b / det; E[2] = -b / det; E[3] = a / det;   // inv(E), symmetric
-                Dh[k + k * n] = a; Dh[k + 1 + k * n] = b; Dh[k + (k + 1) * n] = b; Dh[k + 1 + (k + 1) * n] = c;
-                blocks[nblk] = 2;
+            if (c == 0) {
+                for (int64_t i = tid; i < n; i += nt) {
+                    const bool ok = act[i] && i != p && i != q;
+                    const double cr0 = ap[i], cr1 = aq[i];
+                    Lcol[i + k * n] = ok ? cr0 * E0 + cr1 * E1 : 0.0;
+                    Lcol[i + (k + 1) * n] = ok ? cr0 * E2 + cr1 * E3 : 0.0;
+                }
+                if (tid == 0) {
+                    Dh[k + k * n] = a_;
+                    Dh[k + 1 + k * n] = b_;
+                    Dh[k + (k + 1) * n] = b_;
+                    Dh[k + 1 + (k + 1) * n] = c_;
+                    blocks[nblk] = 2;
+                    pivots[k] = (int32_t)p;
+                    pivots[k + 1] = (int32_t)q;
+                }
             }
-            __syncthreads();
-            // Lc = C E^{-1} (C = A[k+2:, k:k+2]); A -= 0.5 (Lc C^T + C Lc^T)
-            for (int64_t e = tid; e < (m - 2) * (m - 2); e += nt) {
-                const int64_t r = k + 2 + e % (m - 2), c = k + 2 + e / (m - 2);
-                const double cr0 = A[r + k * n], cr1 = A[r + (k + 1) * n];
-                const double cc0 = A[c + k * n], cc1 = A[c + (k + 1) * n];
-                const double lr0 = cr0 * E[0] + cr1 * E[1], lr1 = cr0 * E[2] + cr1 * E[3];
-                const double lc0 = cc0 * E[0] + cc1 * E[1], lc1 = cc0 * E[2] + cc1 * E[3];
-                const double t1 = lr0 * cc0 + lr1 * cc1, t2 = lc0 * cr0 + lc1 * cr1;
-                A[r + c * n] -= 0.5 * (t1 + t2);
-            }
-            __syncthreads();
-            for (int64_t r = k + 2 + tid; r < n; r += nt) {
-                const double cr0 = A[r + k * n], cr1 = A[r + (k + 1) * n];
-                Lh[r + k * n] = cr0 * E[0] + cr1 * E[1];
-                Lh[r + (k + 1) * n] = cr0 * E[2] + cr1 * E[3];
-                A[r + k * n] = A[r + (k + 1) * n] = 0.0;
-                A[k + r * n] = A[k + 1 + r * n] = 0.0;
+            grid.sync();
+            if (c == 0 && tid == 0) {
+                act[p] = act[q] = 0;
+                posof[p] = (int32_t)k;
+                posof[q] = (int32_t)(k + 1);
             }
             ++nblk;
             k += 2;
         }
-        __syncthreads();
+        grid.sync();
     }
-    if (tid == 0) *rank_out = k;
+    if (c == 0 && tid == 0) *rank_out = k;
+}
+
+// lab[pos] = Lambda_2 position at pivoted position pos (pivots first, then the
+// kernel indices ascending); Lh (n x n, pivoted positions) unit lower with
+// Lh[pos(i), kk] = Lcol[i, kk] for kk < pos(i), kk < r.
+__global__ void k_hard_assemble(int64_t n, const int64_t *__restrict__ rank, const double *__restrict__ Lcol,
+                                const int32_t *__restrict__ posof, const int32_t *__restrict__ pivots,
+                                int32_t *__restrict__ lab, double *__restrict__ Lh) {
+    const int64_t r = *rank;
+    // kernel indices in ascending order get positions r, r+1, ... (one thread: n <= a few 1000)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int32_t w = (int32_t)r;
+        for (int64_t i = 0; i < n; ++i)
+            if (posof[i] < 0) lab[w++] = (int32_t)i;
+        for (int64_t q = 0; q < r; ++q) lab[q] = pivots[q];
+    }
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e % n, kk = e / n;   // Lh[row + kk*n] for pivoted position row
+        double v = (row == kk) ? 1.0 : 0.0;
+        if (row > kk && kk < r && row < r) v = Lcol[(int64_t)pivots[row] + kk * n];
+        Lh[e] = v;
+    }
 }
 
 // x2 = S22^+ y2 with the kernel coordinates of the pivoted vector set to 0 [R16].
@@ -423,7 +475,25 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
 void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A, double *Lh, double *Dh,
                  int32_t *lab, int32_t *blocks, int64_t *rank_dev) {
     ClassTimer tm(ctx, "hard");
-    k_hard_factor<<<1, 512, 0, ctx->stream>>>(n, S, thr, A, Lh, Dh, lab, blocks, rank_dev);
+    cudaStream_t st = ctx->stream;
+    DBuf<double> Lcol;
+    Lcol.alloc((size_t)n * n, st);
+    DBuf<int32_t> flags;
+    flags.alloc((size_t)3 * n, st);   // act | posof | pivots
+    int32_t *act = flags.p, *posof = flags.p + n, *piv = flags.p + 2 * n;
+    static int per_sm = 0;
+    if (!per_sm) {
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hard_factor_mc, 256, 0));
+        per_sm = std::max(1, per_sm);
+    }
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(n, 8)), (int64_t)ctx->num_sms * std::min(per_sm, 1));
+    DBuf<Best> gb;
+    gb.alloc((size_t)2 * G, st);
+    void *args[] = {&n, &S, &thr, &A, &Lcol.p, &act, &posof, &gb.p, &Dh, &blocks, &piv, &rank_dev};
+    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_hard_factor_mc, dim3(G), dim3(256), args, 0, st));
+    HF_CHECK_LAUNCH(ctx);
+    k_hard_assemble<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 4096), 256, 0, st>>>(n, rank_dev, Lcol.p, posof,
+                                                                                        piv, lab, Lh);
     HF_CHECK_LAUNCH(ctx);
 }
 void hard_solve(hf_ctx *ctx, int64_t n, int64_t r, const double *Lh, const double *Dh, const int32_t *lab,
