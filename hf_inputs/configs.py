@@ -49,7 +49,7 @@ CONFIGS = {
     # n_min: 64 planted directions, but at L = 16384 the FP32 factor leaves more unresolved
     # directions (Gaussian B, bulk condition ~ 4 L^2 100); DESIGN.md [R5]
     "C2": ConfigSpec("C2", "planted", 16384, n_min=256, n_hard=64, u_hard=(-12.0, -6.0)),
-    "C3": ConfigSpec("C3", "saddle", 2 * 96 * 96 + 48 * 48, grid=96, jump=1e4),
+    "C3": ConfigSpec("C3", "saddle", 2 * 96 * 96 + 2 * 48 * 48, grid=96, jump=1e4),
     "C4": ConfigSpec("C4", "planted", 65536, n_min=256, n_hard=256, u_hard=(-12.0, -6.0)),
     # small analogs with the same recipes (tests; the oracle finishes in seconds)
     "P64": ConfigSpec("P64", "planted", 64, n_min=2, n_hard=2, u_hard=(-10.0, -8.0)),
@@ -59,8 +59,8 @@ CONFIGS = {
     "P4096": ConfigSpec("P4096", "planted", 4096, n_min=64, n_hard=64, u_hard=(-12.0, -6.0)),
     "N16": ConfigSpec("N16", "neumann", 16 * 16, grid=16, n_incl=2, incl_size=4),
     "N32": ConfigSpec("N32", "neumann", 32 * 32, grid=32, n_incl=3, incl_size=4),
-    "S12": ConfigSpec("S12", "saddle", 2 * 12 * 12 + 6 * 6, grid=12, jump=1e4),
-    "S24": ConfigSpec("S24", "saddle", 2 * 24 * 24 + 12 * 12, grid=24, jump=1e4),
+    "S12": ConfigSpec("S12", "saddle", 2 * 12 * 12 + 2 * 6 * 6, grid=12, jump=1e4),
+    "S24": ConfigSpec("S24", "saddle", 2 * 24 * 24 + 2 * 12 * 12, grid=24, jump=1e4),
 }
 
 
@@ -162,12 +162,16 @@ def saddle_point(spec: ConfigSpec, seed: int, device="cpu") -> torch.Tensor:
     """[A B^T; B 0]: A = 2-dof (u_x, u_y interleaved per node, nodes row-major)
     5-point Laplacian on grid x grid nodes, h = 1/(grid-1), edge weight
     (jump or 1)/h^2 by the side of a seeded random line the edge midpoint lies
-    on; B: one row per 2x2 macro-cell with lower-left node (2I, 2J):
-    (u_x(2I+1,2J) - u_x(2I,2J) + u_y(2I,2J+1) - u_y(2I,2J)) / h.  Pure Neumann."""
+    on; B: TWO rows per 2x2 macro-cell with lower-left node (x, y) = (2I, 2J),
+    the divergence-like differences at its two diagonal corners,
+        (u_x(x+1,y)   - u_x(x,y)   + u_y(x,y+1)   - u_y(x,y))   / h
+        (u_x(x+1,y+1) - u_x(x,y+1) + u_y(x+1,y+1) - u_y(x+1,y)) / h,
+    each with 4 nonzeros +-1/h, so B has 2 (grid/2)^2 rows: 4608 x 18432 at
+    grid = 96 and L = 23040 as BASELINE.json's config 3 states.  Pure Neumann."""
     n = spec.grid
     h = 1.0 / (n - 1)
     nv = 2 * n * n
-    npc = (n // 2) ** 2
+    npc = 2 * (n // 2) ** 2
     L = nv + npc
     assert L == spec.L
     rng = np.random.Generator(np.random.Philox(config_seed(spec.name + "/line", seed)))
@@ -193,12 +197,16 @@ def saddle_point(spec: ConfigSpec, seed: int, device="cpu") -> torch.Tensor:
                         K[b, a] -= w
     for J in range(n // 2):
         for I in range(n // 2):
-            r = nv + J * (n // 2) + I
             x, y = 2 * I, 2 * J
-            for dof, val in ((2 * node(x + 1, y) + 0, 1.0 / h), (2 * node(x, y) + 0, -1.0 / h),
-                             (2 * node(x, y + 1) + 1, 1.0 / h), (2 * node(x, y) + 1, -1.0 / h)):
-                K[r, dof] += val
-                K[dof, r] += val
+            r = nv + 2 * (J * (n // 2) + I)
+            rows = (((2 * node(x + 1, y) + 0, 1.0 / h), (2 * node(x, y) + 0, -1.0 / h),
+                     (2 * node(x, y + 1) + 1, 1.0 / h), (2 * node(x, y) + 1, -1.0 / h)),
+                    ((2 * node(x + 1, y + 1) + 0, 1.0 / h), (2 * node(x, y + 1) + 0, -1.0 / h),
+                     (2 * node(x + 1, y + 1) + 1, 1.0 / h), (2 * node(x + 1, y) + 1, -1.0 / h)))
+            for q, row in enumerate(rows):
+                for dof, val in row:
+                    K[r + q, dof] += val
+                    K[dof, r + q] += val
     return torch.from_numpy(K).to(device)
 
 

@@ -43,7 +43,12 @@ def test_saddle_structure():
     assert K.shape == (spec.L, spec.L) and np.array_equal(K, K.T)
     assert np.all(K[nv:, nv:] == 0)
     Bm = K[nv:, :nv]
+    assert Bm.shape[0] == 2 * (spec.grid // 2) ** 2          # two divergence rows per 2x2 macro-cell
     assert np.all((Bm != 0).sum(1) == 4)
+    assert np.linalg.matrix_rank(Bm) == Bm.shape[0]          # no spurious pressure modes
+    # BASELINE.json config 3: L = 23040 = 18432 velocity dofs + 4608 constraint rows
+    c3 = hi.CONFIGS["C3"]
+    assert c3.L == 23040 and 2 * c3.grid ** 2 == 18432 and c3.L - 2 * c3.grid ** 2 == 4608
     # translations (u_x = 1 or u_y = 1, p = 0) are in the kernel
     for c in range(2):
         t = np.zeros(spec.L)
