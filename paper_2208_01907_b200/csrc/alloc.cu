@@ -7,7 +7,9 @@
 // re-mapping that through cudaMalloc / the driver pool on every call cost more
 // than the factorization itself.  On cudaErrorMemoryAllocation the cache is
 // trimmed (device synchronised, cached blocks freed) and the request retried
-// once.  hf_trim_cache() (include/hf.h) releases everything cached.
+// once.  At most HF_CACHE_FRACTION (default 0.4) of the device is kept
+// cached, so the caller's own allocator (torch) keeps room; hf_trim_cache()
+// (include/hf.h) releases everything cached.
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -27,6 +29,7 @@ struct Live {
 
 struct Cache {
     std::mutex mu;
+    std::map<int, size_t> cap;   // per device: max bytes kept cached (HF_CACHE_FRACTION of the device, 0.4)
     std::map<std::pair<int, cudaStream_t>, std::multimap<size_t, void *>> free_;
     std::unordered_map<void *, Live> live;
     size_t cached_bytes = 0;
@@ -108,11 +111,34 @@ void *dev_alloc(size_t bytes, cudaStream_t s) {
 void dev_free(void *p, cudaStream_t s) {
     if (!p) return;
     Cache &c = cache();
-    std::lock_guard<std::mutex> g(c.mu);
+    std::unique_lock<std::mutex> g(c.mu);
     auto it = c.live.find(p);
     if (it == c.live.end()) return;
     const Live l = it->second;
     c.live.erase(it);
+    auto ci = c.cap.find(l.dev);
+    if (ci == c.cap.end()) {
+        size_t fr = 0, tot = 0;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(l.dev);
+        cudaMemGetInfo(&fr, &tot);
+        cudaSetDevice(cur);
+        double f = 0.4;
+        if (const char *e = getenv("HF_CACHE_FRACTION")) f = atof(e);
+        ci = c.cap.emplace(l.dev, (size_t)(f * (double)tot)).first;
+    }
+    if (c.cached_bytes + l.bytes > ci->second) {
+        // over the cap: give the block back (cudaFree synchronises; only past the cap)
+        g.unlock();
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(l.dev);
+        cudaStreamSynchronize(s);
+        cudaFree(p);
+        cudaSetDevice(cur);
+        return;
+    }
     c.free_[{l.dev, s}].insert({l.bytes, p});
     c.cached_bytes += l.bytes;
 }
