@@ -1,0 +1,153 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
+times (default options, one context, the config's tau / n_min):
+
+  C2 (L = 16384): the whole oracle (stage 1 bitwise on Pi, Lambda_2, D and the
+      factor; block GCR + Schur + hard factor) against the CUDA path.
+  C3 (L = 23040): stage 1 bitwise on the first 512 pivots (the oracle's
+      bounded run), S22 against the dense FP64 Schur complement of Eq. 2
+      (LAPACK solve with K11), kernel dimension 2 (the two translations,
+      SURVEY 8(c) item 13), manufactured residual.
+  C4 (L = 65536, 34 GB in FP64): properties that hold at any size, computed on
+      the GPU in FP64 from the exported factor: the strict ratio test on every
+      accepted pivot [R4], the reconstruction bound on sampled entries,
+      the pivot rule at sampled steps [R3] (up to FP32 rounding), block-GCR
+      true residual, manufactured residual.
+
+Set HF_FULLSIZE_ORACLE=1 to also run the whole oracle at C3 (minutes)."""
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import torch
+
+import hf_inputs as hi
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+def _gpu_path(ctx, spec, Kb):
+    from paper_2208_01907_b200 import hf
+    Kd = Kb.to("cuda")
+    hf.hf_scale(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
+    hy, info, S22 = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
+    kd = hf.hf_factor_hard(ctx, hy)
+    return Kd, lf, hy, info, S22, kd
+
+
+def _rho_manufactured(ctx, hy, Kd):
+    from paper_2208_01907_b200 import hf
+    xs = hi.manufactured_x(Kd.shape[0], device="cuda")
+    b = Kd @ xs
+    x, _ = hf.hf_solve(ctx, hy, b)
+    return float((Kd @ x - b).abs().max() / b.abs().max())
+
+
+def test_c2_full_oracle(ctx):
+    spec = hi.CONFIGS["C2"]
+    Kb = hi.make_kbar("C2", 0, device="cuda").cpu()
+    Ko, _ = oracle.scale(Kb.numpy())
+    HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
+    Kd, lf, hy, info, S22, kd = _gpu_path(ctx, spec, Kb)
+    assert np.array_equal(Kd.cpu().numpy(), Ko)
+    perm, D, Lf = lf.export()
+    assert lf.N == HF.F.N and lf.L - lf.n2_tau_only == HF.F.Ntau
+    assert np.array_equal(perm, HF.F.perm)                  # Pi and Lambda_2, bitwise
+    assert np.array_equal(D, HF.F.D)
+    assert torch.equal(Lf.cpu(), torch.from_numpy(HF.F.Lfac))
+    K11, K12, K21, K22 = oracle.extract_blocks(HF.K, HF.F)
+    den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
+    assert np.linalg.norm(S22 - HF.S22) / den <= 1e-10      # [R17] e_S
+    assert info.max_rel_res_true <= 1e-12
+    thr = HF.H.thr
+    margin = min(abs(np.array(HF.H.mu_hist) - thr))
+    if margin > 10 * np.linalg.norm(S22 - HF.S22):
+        assert kd == HF.kernel_dim
+    assert _rho_manufactured(ctx, hy, Kd) <= 1e-12
+
+
+def test_c3_full(ctx):
+    spec = hi.CONFIGS["C3"]
+    Kb = hi.make_kbar("C3", 0)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Kd, lf, hy, info, S22, kd = _gpu_path(ctx, spec, Kb)
+    perm, D, Lf = lf.export()
+    if os.environ.get("HF_FULLSIZE_ORACLE"):
+        HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
+        assert np.array_equal(perm, HF.F.perm) and np.array_equal(D, HF.F.D)
+        K11, K12, K21, K22 = oracle.extract_blocks(HF.K, HF.F)
+        den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
+        assert np.linalg.norm(S22 - HF.S22) / den <= 1e-10
+        assert kd == HF.kernel_dim
+    # stage 1: the first 512 pivots, D and factor columns bitwise
+    F = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min, max_steps=512)
+    assert np.array_equal(perm[:512], F.perm[:512])
+    assert np.array_equal(D[:512], F.D[:512])
+    Lg = Lf[:, :512].cpu().numpy()
+    # oracle columns of the bounded run: rows are in ITS position order, which
+    # coincides with the final pivot order on the first 512 rows only
+    assert np.array_equal(Lg[:512], F.Lfac[:512, :512])
+    # S22 against the dense FP64 Schur complement of Eq. (2) (LAPACK solve with K11)
+    l1, l2 = perm[: lf.N], perm[lf.N:]
+    K11, K12, K22 = Ko[np.ix_(l1, l1)], Ko[np.ix_(l1, l2)], Ko[np.ix_(l2, l2)]
+    Xd = sla.solve(K11, K12, assume_a="sym", check_finite=False)
+    Sd = K22 - K12.T @ Xd
+    den = np.linalg.norm(K22) + np.linalg.norm(K12) * np.linalg.norm(Xd)
+    assert np.linalg.norm(S22 - Sd) / den <= 1e-10
+    assert info.max_rel_res_true <= 1e-12
+    assert kd == 2                       # the two rigid translations (pure Neumann reading)
+    assert _rho_manufactured(ctx, hy, Kd) <= 1e-12
+
+
+def test_c4_full_properties(ctx):
+    spec = hi.CONFIGS["C4"]
+    Kb = hi.make_kbar("C4", 0, device="cuda")
+    Kd, lf, hy, info, S22, kd = _gpu_path(ctx, spec, Kb)
+    del Kb
+    torch.cuda.empty_cache()
+    perm, D, Lf = lf.export()
+    N = lf.N
+    assert N == spec.L - spec.n_min
+    # [R4] strict ratio test held at every accepted pivot
+    Dd = np.abs(D.astype(np.float64))
+    assert np.all(Dd[1:] >= spec.tau * Dd[:-1])
+    # [R2]-[R8] reconstruction on sampled entries, in FP64 from the FP32 factor (S:291 bound)
+    p1 = torch.from_numpy(perm[:N]).cuda()
+    rng = np.random.default_rng(0)
+    a = torch.from_numpy(rng.integers(0, N, 256)).cuda()
+    b = torch.from_numpy(rng.integers(0, N, 256)).cuda()
+    La = Lf[a].double()
+    Lb = Lf[b].double()
+    Dt = torch.from_numpy(D.astype(np.float64)).cuda()
+    rec = (La * Dt * Lb).sum(1)
+    kab = Kd[p1[a], p1[b]]
+    eps32 = float(np.finfo(np.float32).eps)
+    assert float((rec - kab).abs().max()) <= 50 * N * eps32 * float(Kd.abs().max())
+    # [R3] pivot rule at sampled steps: |d_k| is the largest remaining Schur diagonal
+    # over the Lambda_1 rows (FP64 recomputation from the FP32 factor, equal up to the
+    # FP32 rounding of the lazily updated diagonal: tol = 64 sqrt(k) eps32)
+    Kdiag = Kd.diagonal()[torch.from_numpy(perm).cuda()]
+    for k in (1, 1000, N // 2, N - 1):
+        sd = torch.empty(N - k, dtype=torch.float64, device="cuda")
+        for r0 in range(k, N, 4096):
+            r1 = min(N, r0 + 4096)
+            Lk = Lf[r0:r1, :k].double()
+            sd[r0 - k:r1 - k] = Kdiag[r0:r1] - (Lk * Lk * Dt[:k]).sum(1)
+            del Lk
+        tol = 64 * np.sqrt(k) * eps32
+        assert abs(float(sd[0])) >= float(sd.abs().max()) - tol
+        assert abs(float(sd[0]) - float(D[k])) <= tol
+    assert info.max_rel_res_true <= 1e-12
+    assert _rho_manufactured(ctx, hy, Kd) <= 1e-12
