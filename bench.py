@@ -171,6 +171,19 @@ def oracle_sample(Kb_np, spec, pivots=1024):
     return f_st1 + f_it, secs, desc
 
 
+def max_over_ranks(x: float) -> float:
+    """Max of a per-rank scalar over the default process group (NCCL: device
+    tensor, gloo: host tensor); identity without a group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -190,6 +203,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pivots-sample", type=int, default=1024)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
+                    help="N>1: replicas = one matrix per rank, no data-path collective (weak scaling); "
+                         "shard = one matrix, block-GCR right-hand sides split over the ranks with the "
+                         "S22 / X12 slices broadcast over NCCL inside libhf (strong scaling of stage 2)")
     args = ap.parse_args()
 
     import torch
@@ -236,11 +253,17 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
-    ctx = hf.Context(local, stream)
+    if args.mode == "shard" and world > 1:
+        idb = [hf.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idb, src=0)
+        ctx = hf.Context(local, stream, nccl_id=idb[0], rank=rank, nranks=world)
+    else:
+        ctx = hf.Context(local, stream)
 
     # ---- the workload (seeded, synthetic; each rank its own seed in replica mode)
     gen_dev = "cuda" if spec.L > 4096 else "cpu"
-    Kb = hi.make_kbar(spec, args.seed + rank, device=gen_dev).to(dev).contiguous()
+    seed = args.seed + (rank if args.mode == "replicas" else 0)
+    Kb = hi.make_kbar(spec, seed, device=gen_dev).to(dev).contiguous()
     K = torch.empty_like(Kb)
     torch.cuda.synchronize()
 
@@ -306,12 +329,11 @@ def main():
     N, Ntau, n2, iters, kd, tres = results[-1]
     L = spec.L
     fm = flop_model(L, N, Ntau, n2, iters)
-    if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = max_over_ranks(elapsed)
     ms_step = elapsed / args.steps
-    total_flops = fm["total"] * world
+    # replicas: every rank factorises its own matrix (weak scaling); shard: one
+    # factorization per step with stage 2 split over the ranks (strong scaling)
+    total_flops = fm["total"] * (world if args.mode == "replicas" else 1)
     value = total_flops / (ms_step * 1e-3) / 1e12
 
     # ---- roofline of the dominant compute kernel (the FP32 trailing update)
@@ -331,11 +353,13 @@ def main():
 
     line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32+fp64", "data": "synthetic",
+            "scaling": "weak" if args.mode == "replicas" else "strong", "vs_baseline": None,
+            "dtype": "fp32+fp64", "data": "synthetic",
             "config": {"workload": spec.name, "L": L, "N": N, "n2": n2, "n2_tau_only": L - Ntau,
                        "tau": spec.tau, "n_min": spec.n_min, "seed": args.seed, "gcr_iters": iters,
                        "kernel_dim": kd, "gcr_true_rel_res": tres,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": ("single" if world == 1 else
+                                       ("replicas" if args.mode == "replicas" else f"stage2-rhs-shard{world}")),
                        "l2": "inputs larger than L2 (K fp64 %.2f GB); restore copy of Kbar inside each step" %
                              (8 * L * L / 1e9)},
             "seconds_per_factorization": ms_step / 1e3,
@@ -372,10 +396,7 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
         e_ms = t0.elapsed_time(t1) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = max_over_ranks(e_ms)
         line["e2e"] = {"value": total_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": int(Kh.numel() * 8), "d2h_bytes_per_step": int(d2h),
                        "ms_per_step": e_ms}

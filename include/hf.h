@@ -56,6 +56,18 @@ hf_status hf_create(int device, void *cuda_stream, hf_ctx **out);
 hf_status hf_create_dist(int device, void *cuda_stream, const void *nccl_unique_id128,
                          int rank, int nranks, hf_ctx **out);
 hf_status hf_nccl_unique_id(void *id128_host);
+/* Multi-GPU stage 2: on a context of nranks > 1, hf_schur_gcr
+ * gives rank r the contiguous column slice [c0, c1) of K12 (c0 = r n2 / G,
+ * c1 = (r+1) n2 / G), runs block GCR on it, forms S22[:, c0:c1] and broadcasts
+ * the S22 and X12 slices from their owners (one NCCL group); every rank ends
+ * with the full S22 and X12 (block-GCR statistics max-reduced).  Stage 1, the
+ * hard factorization and hf_solve are replicated (deterministic kernels:
+ * identical on every rank).  Pure host function, needs no device. */
+hf_status hf_shard_cols(int64_t n2, int nranks, int rank, int64_t *c0_host, int64_t *c1_host);
+/* Single-GPU emulation of one rank of that sharding (tests): with nranks > 0,
+ * hf_schur_gcr computes only rank's slice of S22 / X12 and leaves the other
+ * columns zero (no collective); nranks = 0 switches the emulation off. */
+hf_status hf_set_virtual_rank(hf_ctx *ctx, int rank, int nranks);
 hf_status hf_destroy(hf_ctx *ctx);
 /* Last error message of ctx (never NULL; "" when none).  ctx may be NULL for
  * errors raised before a context existed. */

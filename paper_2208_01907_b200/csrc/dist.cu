@@ -11,7 +11,46 @@
             throw ::hf::Error{HF_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
     } while (0)
 
+namespace hf {
+
+// contiguous balanced column slices: rank r owns [r n2 / G, (r+1) n2 / G)
+void shard_cols(int64_t n2, int nranks, int rank, int64_t *c0, int64_t *c1) {
+    if (nranks <= 1) {
+        *c0 = 0;
+        *c1 = n2;
+        return;
+    }
+    *c0 = (n2 * rank) / nranks;
+    *c1 = (n2 * (rank + 1)) / nranks;
+}
+
+#ifdef HF_WITH_NCCL
+void collective_begin(hf_ctx *) { HF_NCCL(ncclGroupStart()); }
+void collective_end(hf_ctx *) { HF_NCCL(ncclGroupEnd()); }
+void collective_bcast(hf_ctx *ctx, double *buf, size_t count, int root) {
+    HF_NCCL(ncclBroadcast(buf, buf, count, ncclDouble, root, ctx->comm, ctx->stream));
+}
+void collective_max(hf_ctx *ctx, double *buf, size_t count) {
+    HF_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+}
+#endif
+
+}  // namespace hf
+
 extern "C" {
+
+hf_status hf_shard_cols(int64_t n2, int nranks, int rank, int64_t *c0_host, int64_t *c1_host) {
+    if (n2 < 0 || nranks < 1 || rank < 0 || rank >= nranks || !c0_host || !c1_host) return HF_ERR_INVALID_ARG;
+    hf::shard_cols(n2, nranks, rank, c0_host, c1_host);
+    return HF_OK;
+}
+
+hf_status hf_set_virtual_rank(hf_ctx *ctx, int rank, int nranks) {
+    if (!ctx || nranks < 0 || (nranks > 0 && (rank < 0 || rank >= nranks))) return HF_ERR_INVALID_ARG;
+    ctx->vrank = nranks > 0 ? rank : 0;
+    ctx->vnranks = nranks;
+    return HF_OK;
+}
 
 hf_status hf_nccl_unique_id(void *id128_host) {
     if (!id128_host) return HF_ERR_INVALID_ARG;

@@ -22,6 +22,8 @@
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
 
+#include <string>
+
 namespace hf {
 namespace {
 
@@ -153,6 +155,16 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
 }  // namespace
 
 // ------------------------------------------------------------------ Alg. 1 steps 2-4
+// Multi-GPU (stage 2): the n2 right-hand sides (columns of K12)
+// are split into contiguous slices, one per rank (hf_shard_cols); every rank
+// runs its own block GCR on its slice and forms S22[:, slice] = K22[:, slice]
+// - K21 X[:, slice]; the slices of S22 and X are then broadcast from their
+// owners in one NCCL group (ncclBroadcast per rank: unequal slice widths, no
+// padding), and the GCR statistics are max-reduced.  Errors of one rank are
+// carried through the collectives (no rank leaves early) and raised after.
+// A "virtual" rank set with hf_set_virtual_rank computes only its slice and
+// leaves the other columns zero (single-GPU emulation of one rank, no
+// collective).
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info) {
     cudaStream_t st = ctx->stream;
     const hf_lowfactor *lf = hy->lf;
@@ -171,14 +183,63 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
     if (n2 == 0) return;
     gather_K12(ctx, L, hy->K, hy->ld, hy->lam2.p, n2, hy->mask1.p, hy->B.p);   // step 2
     gather_K22(ctx, n2, hy->K, hy->ld, hy->lam2.p, hy->S22.p);
-    if (N > 0) {
+    const bool virt = ctx->vnranks > 0;
+    const int nr = virt ? ctx->vnranks : ctx->nranks, rk = virt ? ctx->vrank : ctx->rank;
+    int64_t c0 = 0, c1 = n2;
+    shard_cols(n2, nr, rk, &c0, &c1);
+    const int64_t ns = c1 - c0;
+    if (nr > 1) HF_CUDA(cudaMemsetAsync(hy->X.p, 0, (size_t)L * n2 * sizeof(double), st));
+    int local_st = HF_OK;
+    std::string local_msg;
+    if (N > 0 && ns > 0) {
         GcrWork w;
-        block_gcr(ctx, hy->K, hy->ld, L, hy->mask1.p, hy->pc, hy->B.p, n2, hy->X.p, o, info, w);   // step 3
-        // step 4: S22 = K22 - K21 X  (K21 X = B^T X since X is zero on Lambda_2 rows)
-        dgemm(ctx, true, n2, n2, L, -1.0, hy->B.p, L, hy->X.p, L, 1.0, hy->S22.p, n2, nullptr, &w.dgw);
-    } else {
+        try {
+            block_gcr(ctx, hy->K, hy->ld, L, hy->mask1.p, hy->pc, hy->B.p + c0 * L, ns, hy->X.p + c0 * L, o, info,
+                      w);                                                                           // step 3
+        } catch (const Error &e) {
+            if (e.st != HF_ERR_NOT_CONVERGED && e.st != HF_ERR_BREAKDOWN) throw;   // CUDA errors: unrecoverable
+            local_st = e.st;
+            local_msg = e.msg;
+        }
+        // step 4: S22[:, slice] = K22[:, slice] - K21 X[:, slice]  (K21 X = B^T X: X is zero on Lambda_2 rows)
+        dgemm(ctx, true, n2, ns, L, -1.0, hy->B.p, L, hy->X.p + c0 * L, L, 1.0, hy->S22.p + c0 * n2, n2, nullptr,
+              &w.dgw);
+    } else if (N == 0) {
         HF_CUDA(cudaMemsetAsync(hy->X.p, 0, (size_t)L * n2 * sizeof(double), st));
     }
+    if (virt && nr > 1) {
+        // single-GPU emulation of rank rk: the other ranks' columns of S22 are not computed
+        if (c0 > 0) HF_CUDA(cudaMemsetAsync(hy->S22.p, 0, (size_t)c0 * n2 * sizeof(double), st));
+        if (c1 < n2) HF_CUDA(cudaMemsetAsync(hy->S22.p + c1 * n2, 0, (size_t)(n2 - c1) * n2 * sizeof(double), st));
+    }
+#ifdef HF_WITH_NCCL
+    if (!virt && ctx->comm) {   // (also with one rank: the same NCCL path, trivially)
+        DBuf<double> red;
+        red.alloc(4, st);
+        double h[4] = {(double)info->iters, info->max_rel_res_recursive, info->max_rel_res_true, (double)local_st};
+        HF_CUDA(cudaMemcpyAsync(red.p, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        collective_begin(ctx);
+        for (int r = 0; r < nr; ++r) {
+            int64_t a0, a1;
+            shard_cols(n2, nr, r, &a0, &a1);
+            if (a1 == a0) continue;
+            collective_bcast(ctx, hy->S22.p + a0 * n2, (size_t)(a1 - a0) * n2, r);
+            collective_bcast(ctx, hy->X.p + a0 * L, (size_t)(a1 - a0) * L, r);
+        }
+        collective_max(ctx, red.p, 4);
+        collective_end(ctx);
+        HF_CUDA(cudaMemcpyAsync(h, red.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        HF_CUDA(cudaStreamSynchronize(st));
+        info->iters = (int32_t)h[0];
+        info->max_rel_res_recursive = h[1];
+        info->max_rel_res_true = h[2];
+        if (local_st == HF_OK && (int)h[3] != HF_OK) {
+            local_st = (int)h[3];
+            local_msg = "block GCR failed on another rank";
+        }
+    }
+#endif
+    if (local_st != HF_OK) throw Error{(hf_status)local_st, local_msg};
 }
 
 // ------------------------------------------------------------------ Alg. 1 step 5

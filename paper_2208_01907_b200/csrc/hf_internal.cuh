@@ -111,6 +111,7 @@ struct hf_ctx {
     cudaStream_t stream = 0;
     int num_sms = 148;
     int rank = 0, nranks = 1;
+    int vrank = 0, vnranks = 0;        // single-GPU emulation of one rank (hf_set_virtual_rank)
 #ifdef HF_WITH_NCCL
     ncclComm_t comm = nullptr;
 #endif
@@ -227,4 +228,12 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
                   hf_gcr_info *info);
+// multi-GPU plumbing (dist.cu)
+void shard_cols(int64_t n2, int nranks, int rank, int64_t *c0, int64_t *c1);
+#ifdef HF_WITH_NCCL
+void collective_begin(hf_ctx *ctx);
+void collective_end(hf_ctx *ctx);
+void collective_bcast(hf_ctx *ctx, double *buf, size_t count, int root);
+void collective_max(hf_ctx *ctx, double *buf, size_t count);
+#endif
 }  // namespace hf

@@ -28,7 +28,7 @@ EXPORTED = [
     "hf_set_profiling", "hf_kernel_stats", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
-    "hf_precond_apply",
+    "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank",
 ]
 
 
@@ -87,6 +87,8 @@ def load() -> ctypes.CDLL:
         "hf_hybrid_destroy": [vp],
         "hf_trim_cache": [ctypes.c_int],
         "hf_precond_apply": [vp, vp, i64, vp, i64, vp, i64],
+        "hf_shard_cols": [i64, ctypes.c_int, ctypes.c_int, pi64, pi64],
+        "hf_set_virtual_rank": [vp, ctypes.c_int, ctypes.c_int],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -177,6 +179,19 @@ class Context:
         n = ctypes.c_int64()
         self.check(self.lib.hf_launch_count(self.h, ctypes.byref(n)))
         return n.value
+
+
+def hf_shard_cols(n2: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Column slice [c0, c1) of the n2 right-hand sides owned by `rank` (host only)."""
+    c0, c1 = ctypes.c_int64(), ctypes.c_int64()
+    st = load().hf_shard_cols(int(n2), int(nranks), int(rank), ctypes.byref(c0), ctypes.byref(c1))
+    if st != HF_OK:
+        raise HFError(st, "hf_shard_cols: bad arguments")
+    return c0.value, c1.value
+
+
+def hf_set_virtual_rank(ctx: "Context", rank: int, nranks: int) -> None:
+    ctx.check(ctx.lib.hf_set_virtual_rank(ctx.h, int(rank), int(nranks)))
 
 
 def nccl_unique_id() -> bytes:

@@ -1,0 +1,83 @@
+"""Stage-2 right-hand-side sharding on one GPU:
+  * every rank of a G-rank run emulated in turn (hf_set_virtual_rank: the
+    rank's own block GCR on its column slice of K12 and its slice of S22,
+    no collective); the slices put together must meet the same normwise bar
+    against the oracle as the single-block run (e_S <= 1e-10, [R17]) even
+    though every slice has its own Krylov space;
+  * the real NCCL path of libhf (hf_create_dist, one rank): broadcast of the
+    S22 / X12 slices and the max-reduction of the GCR statistics."""
+import numpy as np
+import pytest
+import torch
+
+import hf_inputs as hi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+def _e_S(Sg, HF):
+    K11, K12, K21, K22 = oracle.extract_blocks(HF.K, HF.F)
+    den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
+    return np.linalg.norm(Sg - HF.S22) / den
+
+
+@pytest.mark.parametrize("name,G", [("P2048", 2), ("P2048", 3), ("C0", 2), ("S24", 4)])
+def test_virtual_ranks_compose(ctx, name, G):
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, 0)
+    Ko, _ = oracle.scale(Kb.numpy())
+    HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
+    Kd = Kb.cuda()
+    hf.hf_scale(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
+    n2 = lf.n2
+    S = np.zeros((n2, n2))
+    X = np.zeros((lf.N, n2))
+    try:
+        for r in range(G):
+            hf.hf_set_virtual_rank(ctx, r, G)
+            hy, info, Sr = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
+            c0, c1 = hf.hf_shard_cols(n2, G, r)
+            assert np.all(Sr[:, :c0] == 0) and np.all(Sr[:, c1:] == 0)
+            S[:, c0:c1] = Sr[:, c0:c1]
+            Xr, _ = hy.export()
+            X[:, c0:c1] = Xr.cpu().numpy()[:, c0:c1]
+            assert info.max_rel_res_true <= 1e-12
+            hy.close()
+    finally:
+        hf.hf_set_virtual_rank(ctx, 0, 0)
+    assert _e_S(S, HF) <= 1e-10
+    assert np.linalg.norm(X - HF.X) <= 1e-8 * np.linalg.norm(HF.X)
+
+
+def test_nccl_path_one_rank():
+    from paper_2208_01907_b200 import hf
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    spec = hi.CONFIGS["P1024"]
+    Kb = hi.make_kbar("P1024", 0)
+    Ko, _ = oracle.scale(Kb.numpy())
+    HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
+    c = hf.Context(0, nccl_id=hf.nccl_unique_id(), rank=0, nranks=1)
+    try:
+        Kd = Kb.cuda()
+        hf.hf_scale(c, Kd)
+        lf = hf.hf_factor_lowprec(c, Kd, tau=spec.tau, n_min=spec.n_min)
+        hy, info, S = hf.hf_schur_gcr(c, Kd, lf, want_S22_host=True)
+        assert _e_S(S, HF) <= 1e-10 and info.max_rel_res_true <= 1e-12
+        kd = hf.hf_factor_hard(c, hy)
+        assert kd == HF.kernel_dim
+    finally:
+        c.close()
