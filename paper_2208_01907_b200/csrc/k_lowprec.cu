@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "hf_internal.cuh"
 
@@ -107,13 +108,16 @@ struct ChainArgs {
     int64_t ldl;
     float *Dk;          // [L] d_k
     int32_t *pivorig;   // [L] original index of pivot k
-    unsigned long long *keys;    // [nbp] per-step max key (zeroed before the launch)
-    unsigned int *cnt;           // arrival counter (zeroed before the launch)
+    unsigned long long *keys;    // [nbp] per-step max key (zeroed before the launch)    (xmode 0)
+    unsigned int *cnt;           // arrival counter (zeroed before the launch)          (xmode 0)
+    unsigned long long *slots;   // [2][G][SLOT_STRIDE] per-CTA key | step tag, one line each (xmode 1)
+    int xmode;                   // 0: red.max + counter; 1: spread LL slots (HF_CHAIN_XCHG)
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
     unsigned long long *dbg;   // optional per-phase time sums (CTA 0), HF_CHAIN_DEBUG
 };
 
+constexpr int SLOT_STRIDE = 32;     // 256 B between slots: no two CTAs' slots share an L2 line
 constexpr uint64_t TAGM = 0x3FFF;   // 14-bit step tag in the low bits of every exchanged word
 __device__ __forceinline__ uint64_t step_tag(int64_t k) { return (uint64_t)(k % 16383) + 1; }
 
@@ -183,8 +187,12 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             v = warp_max64(v);
             if (wid == 0) {
                 if (lane == 0) {
-                    if (v) red_max_u64(&a.keys[t], v);
-                    red_release_add(a.cnt, 1u);
+                    if (a.xmode == 1) {
+                        st_relaxed_u64(&a.slots[((size_t)(t & 1) * G + blockIdx.x) * SLOT_STRIDE], (v & ~TAGM) | tag);
+                    } else {
+                        if (v) red_max_u64(&a.keys[t], v);
+                        red_release_add(a.cnt, 1u);
+                    }
                 }
             } else if (v) {
                 unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * nb;
@@ -202,7 +210,24 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         }
         PH(0)
         // ---- D: wait for all CTAs, read the winning key
-        if (tid == 0) {
+        if (a.xmode == 1) {
+            if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
+                const unsigned long long *sl = a.slots + (size_t)(t & 1) * G * SLOT_STRIDE;
+                uint64_t mx;
+                for (;;) {
+                    bool ok = true;
+                    mx = 0;
+                    for (int g = lane; g < G; g += 32) {
+                        const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * SLOT_STRIDE]);
+                        ok &= (sv & TAGM) == tag;
+                        mx = umax64(mx, sv);
+                    }
+                    if (__all_sync(0xffffffffu, ok)) break;
+                }
+                mx = warp_max64(mx);
+                if (lane == 0) bkey = mx;
+            }
+        } else if (tid == 0) {
             const unsigned int want = (unsigned int)G * (unsigned int)(t + 1);
             while (ld_relaxed_u32(a.cnt) < want) {
             }
@@ -500,10 +525,17 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     cudaFuncAttributes fa;
     HF_CUDA(cudaFuncGetAttributes(&fa, k_chain));
     maxsmem -= (int)fa.sharedSizeBytes;
-    const int64_t G0 = std::min<int64_t>(nsm, std::max<int64_t>(1, cdiv(L, 32)));
+    // Chain geometry (measured on B200 at C2, chain + trailing ms: 148 CTAs / nb 256: 106.3,
+    // 148 / 128: 103.3, 74 / 128: 100.6, 64 / 128: 95.0, 64 / 192: 95.8, 32 / 96: 98.8):
+    // fewer CTAs make the per-pivot exchange cheaper until the rows per CTA no longer fit a
+    // 128-wide panel in shared memory, so G = max(64, L / 443) and nb = 128 by default.
+    const int nb_def = 128;
+    int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / (nb_def + 2)))));
+    if (const char *e = getenv("HF_CHAIN_CTAS")) gmax = std::max(1, std::min(nsm, atoi(e)));
+    const int64_t G0 = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(L, 32)));
     const int64_t R0 = cdiv(L, G0);
     HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
-    int nb = o.nb > 0 ? o.nb : 256;
+    int nb = o.nb > 0 ? o.nb : nb_def;
     while (nb > 8 && (int64_t)(nb * R0 + 2 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
     HF_REQUIRE(nb >= 8 && nb <= 1024, "panel width out of range");
 
@@ -526,10 +558,14 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     status.alloc(4, st);
     // per-launch exchange state: keys[nb] + counter, zeroed before every chain launch;
     // mailbox words are tagged (self-validating), zeroed once
-    DBuf<unsigned long long> xchg, mbox;
+    DBuf<unsigned long long> xchg, mbox, slots;
     xchg.alloc((size_t)nb + 2, st);
     mbox.alloc((size_t)2 * nsm * nb, st);
     mbox.zero(st);
+    slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
+    slots.zero(st);
+    int xmode = 1;
+    if (const char *e = getenv("HF_CHAIN_XCHG")) xmode = (strcmp(e, "counter") == 0) ? 0 : 1;
     HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
 
     {
@@ -551,17 +587,18 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     int64_t m = L, K0 = 0;
     while (m > 0) {
         const int nbp = (int)std::min<int64_t>(nb, m);
-        const int64_t G = std::min<int64_t>(nsm, std::max<int64_t>(1, cdiv(m, 32)));
+        const int64_t G = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(m, 32)));
         const int64_t R = cdiv(m, G);
         const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
         const size_t shm = ((size_t)nbp * R + 2 * nbp) * sizeof(float);
-        HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
+        if (xmode == 0) HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
         ca.V = V[cur].p; ca.ldv = L; ca.orig = orig[cur].p;
         ca.S = S.p; ca.Sn = Sn.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
+        ca.slots = slots.p; ca.xmode = xmode;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
         {
             ClassTimer tm(ctx, "chain");
@@ -581,9 +618,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             ta.mp = mp; ta.nbp = nbp; ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p; ta.ldv = L;
             ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L; ta.status = status.p;
             const int64_t T = cdiv(mp, TB);
+            const int64_t ntiles = T * (T + 1) / 2;
             {
                 ClassTimer tm(ctx, "trailing");
-                k_trailing<<<(unsigned)(T * (T + 1) / 2), 256, 0, st>>>(ta);
+                k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
             }
             cur ^= 1;
@@ -633,6 +671,8 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     HF_CUDA(cudaMemcpyAsync(lf->pos1.p, rank.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     lf->D.alloc(std::max<int64_t>(N, 1), st);
     if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->D.p, Dk.p, N * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    V[0].release();   // the trailing buffers are done: keep the peak at K + Lorig + Lfac
+    V[1].release();
     lf->Lfac.alloc((size_t)std::max<int64_t>(N, 1) * std::max<int64_t>(N, 1), st);
     if (N > 0) {
         ClassTimer tm(ctx, "other");
