@@ -167,9 +167,9 @@ struct Precond {
     const int64_t *perm = nullptr; // [L] pivot order -> original index
     const int32_t *pos1 = nullptr; // [L] original index -> pivot rank, -1 on Lambda_2
     int64_t Np = 0;                // N rounded up to the 64-row block
-    DBuf<float> Lp, Up;            // Np x Np: L padded with the identity, and L^T
+    DBuf<float> Lp, Up;            // Np x Np: L padded with the identity, and L^T, each block row
+                                   // scaled in place by its diagonal-block inverse (G = Dinv Op)
     DBuf<float> LinvF, LinvB;      // inverses of the 64x64 diagonal blocks (tile layouts)
-    DBuf<float> MF, MB;            // Dinv_j Op_{j,j-1}, Dinv_j Op_{j,j-2} per logical block
     DBuf<float> P;                 // Np x ncolp: P_j of the chain recurrence (row-major)
     DBuf<float> Y;                 // Np x ncolp workspace (FP32, row-major)
     DBuf<float> Xb;                // Np x ncolp workspace (FP32, row-major)

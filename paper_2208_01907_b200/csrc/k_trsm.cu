@@ -9,22 +9,25 @@
 //
 // Design (B200): one cooperative persistent launch per direction, blocks of
 // 64 rows, RHS chunks of 64 columns.  With Dinv_b the inverse of the unit
-// diagonal block (L_bb^{-1} forward, L_bb^{-T} backward) and Op = L / L^T,
-//     Y_b = P_b - M1_b Y_{b-1} - M2_b Y_{b-2},
-//     P_b = Dinv_b (RHS_b - sum_{q < b-2} Op_bq Y_q),   Mk_b = Dinv_b Op_{b,b-k}
-// (block indices in the direction of the solve).
+// diagonal block (L_bb^{-1} forward, L_bb^{-T} backward), Op = L / L^T and
+// the block-row-scaled operator G_bq = Dinv_b Op_bq (formed once, in place,
+// at setup), the solve is  Y_b = Dinv_b RHS_b - sum_{q<b} G_bq Y_q, split as
+//     Y_b = P_b - G_{b,b-1} Y_{b-1} - G_{b,b-2} Y_{b-2},
+//     P_b = Dinv_b RHS_b - sum_{q < b-2} G_bq Y_q
+// (block indices in the direction of the solve); no Dinv product is left
+// behind the last dependency of P_b.
 //  * CHAIN CTAs (one per chunk, alone on their SM: the helper that shares
 //    the SM exits) walk the blocks in order and keep Y_{b-1}, Y_{b-2} in a
 //    3-slot shared ring: a link of the sequential chain is two 64x64x64
-//    tile products (-M1, -M2 prefetched by cp.async during the previous
+//    tile products (G tiles prefetched by cp.async during the previous
 //    link); two STORE warps copy each finished Y_b to global memory, fence
 //    and release it while the 8 compute warps already run the next link
 //    (per-slot FULL/EMPTY named barriers hand the ring slots over).
 //  * HELPER CTAs (all others) take items from a host-built table in
 //    topological order (atomic counter): PARTIAL items sum one segment of SEG
-//    dependency blocks into a partial slot; the P-item of block b adds the
-//    partial slots in fixed order, its last segment (up to b-3), and applies
-//    Dinv_b, two links ahead of the chain that consumes it.  Long sums of the
+//    dependency blocks into a partial slot; the P-item of block b forms
+//    Dinv_b RHS_b first, then subtracts the partial slots in fixed order and
+//    its last segment (up to b-3), two links ahead of the chain.  Long sums of the
 //    last blocks are spread over many CTAs instead of serialising on one.
 //  * Release flags + relaxed polling + one acquire; the cooperative launch
 //    guarantees chain and helpers are co-resident (no deadlock by design:
@@ -144,8 +147,6 @@ struct TrsmArgs {
     const float *Up;     // backward operand (Np x Np, col-major) = Lp^T
     const float *LinvF;  // [nblk][64][64] tile layout of Dinv (forward)
     const float *LinvB;  // (backward)
-    const float *MF;     // [nblk][2][64][64] -M1, -M2 (forward, by logical block)
-    const float *MB;     // (backward)
     const float *D;      // [N]
     const int64_t *perm; // [L] pivot order -> original index
     const double *R;     // input, original row order (L x ncol, ldr)
@@ -165,18 +166,62 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// acc[i][j] += sum_k As[k][tr*4+i] * Bs[k][tc*4+j]
+// acc[i][j] += sum_k As[k][tr*4+i] * Bs[k][tc*4+j]; FFMA2 with a broadcast scalar
+// (half the issue slots of scalar FFMA), the pairs along j kept in float2
 __device__ __forceinline__ void tile_fma(float (&acc)[4][4], const float *As, const float *Bs, int tr, int tc) {
+    float2 c2[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        c2[i][0] = make_float2(acc[i][0], acc[i][1]);
+        c2[i][1] = make_float2(acc[i][2], acc[i][3]);
+    }
 #pragma unroll 16
     for (int k = 0; k < TBS; ++k) {
         const float4 a = *reinterpret_cast<const float4 *>(&As[k * TBS + tr * 4]);
         const float4 y = *reinterpret_cast<const float4 *>(&Bs[k * CW + tc * 4]);
         const float av[4] = {a.x, a.y, a.z, a.w};
-        const float yv[4] = {y.x, y.y, y.z, y.w};
+        const float2 y01 = make_float2(y.x, y.y), y23 = make_float2(y.z, y.w);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) {
+            c2[i][0] = __ffma2_rn(make_float2(av[i], av[i]), y01, c2[i][0]);
+            c2[i][1] = __ffma2_rn(make_float2(av[i], av[i]), y23, c2[i][1]);
+        }
+    }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av[i], yv[j], acc[i][j]);
+    for (int i = 0; i < 4; ++i) {
+        acc[i][0] = c2[i][0].x;
+        acc[i][1] = c2[i][0].y;
+        acc[i][2] = c2[i][1].x;
+        acc[i][3] = c2[i][1].y;
+    }
+}
+
+// acc -= As^T-ish product (same layouts as tile_fma)
+__device__ __forceinline__ void tile_fms(float (&acc)[4][4], const float *As, const float *Bs, int tr, int tc) {
+    float2 c2[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        c2[i][0] = make_float2(acc[i][0], acc[i][1]);
+        c2[i][1] = make_float2(acc[i][2], acc[i][3]);
+    }
+#pragma unroll 16
+    for (int k = 0; k < TBS; ++k) {
+        const float4 a = *reinterpret_cast<const float4 *>(&As[k * TBS + tr * 4]);
+        const float4 y = *reinterpret_cast<const float4 *>(&Bs[k * CW + tc * 4]);
+        const float av[4] = {-a.x, -a.y, -a.z, -a.w};
+        const float2 y01 = make_float2(y.x, y.y), y23 = make_float2(y.z, y.w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            c2[i][0] = __ffma2_rn(make_float2(av[i], av[i]), y01, c2[i][0]);
+            c2[i][1] = __ffma2_rn(make_float2(av[i], av[i]), y23, c2[i][1]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        acc[i][0] = c2[i][0].x;
+        acc[i][1] = c2[i][0].y;
+        acc[i][2] = c2[i][1].x;
+        acc[i][3] = c2[i][1].y;
     }
 }
 
@@ -187,38 +232,39 @@ __device__ __forceinline__ void wait_epoch(const int *f, int epoch) {
     fence_acquire();
 }
 
-// ------------------------------------------------------------------ setup: -M1, -M2
-// M[j][k-1] = -Dinv_j Op_{j, j-k} (logical blocks), column-major 64x64 = tile
-// layout.  Bs[k][c] = Op(r0+k, q0+c) is read from the OTHER operand (Op^T),
-// which is contiguous in c.
+// ------------------------------------------------------------------ setup: G = Dinv Op
+// In place, one 64x64 tile per CTA: Op(b-block, q-block) <- Dinv_b Op(b, q) for
+// every dependency block q of b (forward: q < b on Lp; backward: q > b on Up).
+// The tile is read coalesced (column-major) and transposed through shared
+// memory into the [k][c] operand layout.
 template <bool BWD>
-__global__ void __launch_bounds__(256) k_mk(int nblk, int64_t Np, const float *__restrict__ Lp,
-                                            const float *__restrict__ Up, const float *__restrict__ Linv,
-                                            float *__restrict__ M) {
-    __shared__ __align__(16) float As[TILE];
+__global__ void __launch_bounds__(256) k_scale_op(int nblk, int64_t Np, float *__restrict__ Op,
+                                                  const float *__restrict__ Linv) {
+    const int b = blockIdx.x, q = blockIdx.y;
+    if (BWD ? !(q > b) : !(q < b)) return;
+    __shared__ __align__(16) float buf[TBS * (TBS + 1)];   // Ts[c][k] (padded), then the Dinv tile
     __shared__ __align__(16) float Bs[TILE];
-    const int j = blockIdx.x, kk = blockIdx.y + 1;   // logical block, lag
+    float *As = buf;
     const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
-    float *dst = M + ((size_t)j * 2 + (kk - 1)) * TILE;
-    if (j - kk < 0) {
-        for (int e = tid; e < TILE; e += 256) dst[e] = 0.f;
-        return;
-    }
-    const int b = BWD ? nblk - 1 - j : j, q = BWD ? nblk - 1 - (j - kk) : j - kk;
     const int64_t r0 = (int64_t)b * TBS, q0 = (int64_t)q * TBS;
-    const float *Ot = BWD ? Lp : Up;   // Op^T, column-major
     for (int e = tid; e < TILE; e += 256) {
-        const int k = e >> 6, c = e & 63;
-        As[e] = Linv[(size_t)b * TILE + e];
-        Bs[k * CW + c] = Ot[(q0 + c) + (r0 + k) * Np];
+        const int r = e & 63, c = e >> 6;
+        buf[c * (TBS + 1) + r] = Op[(r0 + r) + (q0 + c) * Np];      // Ts[c][k] = Op(r0+k, q0+c)
     }
     __syncthreads();
+    for (int e = tid; e < TILE; e += 256) {
+        const int k = e >> 6, c = e & 63;
+        Bs[k * CW + c] = buf[c * (TBS + 1) + k];
+    }
+    __syncthreads();
+    for (int e = tid; e < TILE; e += 256) As[e] = Linv[(size_t)b * TILE + e];
+    __syncthreads();
     float acc[4][4] = {};
-    tile_fma(acc, As, Bs, tr, tc);   // acc = Dinv Op
+    tile_fma(acc, As, Bs, tr, tc);                     // Dinv_b Op_bq
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) dst[(tc * 4 + jj) * TBS + tr * 4 + i] = -acc[i][jj];
+        for (int jj = 0; jj < 4; ++jj) Op[(r0 + tr * 4 + i) + (q0 + tc * 4 + jj) * Np] = acc[i][jj];
 }
 
 // W (original row order, ldw) = lift(Xb) on Lambda_1 rows, 0 on Lambda_2 rows
@@ -255,7 +301,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
         const int cc = blockIdx.x, c0 = cc * CW;
         if (tid == 0) atomicExch(&smids[cc], smid() + 1u);
         float *Yr = sm;               // [3][TILE] ring: Y_j in slot j % 3
-        float *Mb = sm + 3 * TILE;    // [2 stages][-M1, -M2]
+        float *Mb = sm + 3 * TILE;    // [2 stages][G_{j,j-1}, G_{j,j-2}]
         if (tid >= NCOMP) {
             // ---- store warps: slot j -> global, fence, release
             const int st = tid - NCOMP;
@@ -280,14 +326,21 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             return;
         }
         // ---- compute warps
-        const float *Msrc = BWD ? a.MB : a.MF;
+        // G_{j,j-1}, G_{j,j-2} tiles of the scaled operator, layout [k][r] = G(r0+r, q0+k)
         auto load_m = [&](int j) {
             float *dst = Mb + (j & 1) * 2 * TILE;
-            const float *src = Msrc + (size_t)j * 2 * TILE;
+            const int64_t r0 = (int64_t)phys(j) * TBS;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = tid + u * NCOMP;
-                cp_async16(&dst[e * 4], src + e * 4);
+            for (int lag = 1; lag <= 2; ++lag) {
+                if (j - lag < 0) continue;
+                const int64_t q0 = (int64_t)phys(j - lag) * TBS;
+                float *d = dst + (lag - 1) * TILE;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = tid + u * NCOMP;
+                    const int k = e >> 4, r4 = (e & 15) * 4;
+                    cp_async16(&d[k * TBS + r4], Op + (r0 + r4) + (q0 + k) * a.Np);
+                }
             }
             cp_commit();
         };
@@ -311,8 +364,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             bar_sync(4, NCOMP);
             PH(1)
             const float *M = Mb + (j & 1) * 2 * TILE;
-            if (j >= 1) tile_fma(acc, M, Yr + ((j - 1) % 3) * TILE, tr, tc);
-            if (j >= 2) tile_fma(acc, M + TILE, Yr + ((j - 2) % 3) * TILE, tr, tc);
+            if (j >= 1) tile_fms(acc, M, Yr + ((j - 1) % 3) * TILE, tr, tc);
+            if (j >= 2) tile_fms(acc, M + TILE, Yr + ((j - 2) % 3) * TILE, tr, tc);
             PH(2)
             if (j >= 3) bar_sync(6 + j % 3, NTHR);       // EMPTY: store warps are done with Y_{j-3}
             float *ys = Yr + (j % 3) * TILE;
@@ -418,7 +471,48 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             }
             continue;
         }
-        // ---- P-item: t = partial slots in fixed order + the last segment (up to j-3)
+        // ---- P-item.  First Dinv_j RHS_j (no dependency): forward truncates R
+        //      (FP64, original order) to FP32, backward starts from z = D^{-1} y
+        float out[4][4] = {};
+        {
+            float rhs[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t r = r0 + tr * 4 + i;
+                if (!BWD) {
+                    const int64_t pr = r < a.N ? a.perm[r] : 0;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int c = c0 + tc * 4 + jj;
+                        rhs[i][jj] = (r < a.N && c < a.ncol) ? __double2float_rn(a.R[pr + (int64_t)c * a.ldr]) : 0.f;
+                    }
+                } else {
+                    const float4 y = *reinterpret_cast<const float4 *>(&a.Y[r * a.ncolp + c0 + tc * 4]);
+                    const float d = r < a.N ? a.D[r] : 1.f;
+                    rhs[i][0] = __fdiv_rn(y.x, d);
+                    rhs[i][1] = __fdiv_rn(y.y, d);
+                    rhs[i][2] = __fdiv_rn(y.z, d);
+                    rhs[i][3] = __fdiv_rn(y.w, d);
+                }
+            }
+            float *As = sm, *Bs = sm + TILE;
+            const float *Li = Dinv + (size_t)b * TILE;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = tid + u * NCOMP;
+                cp_async16(&As[e * 4], Li + e * 4);
+            }
+            cp_commit();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4 *>(&Bs[(tr * 4 + i) * CW + tc * 4]) =
+                    make_float4(rhs[i][0], rhs[i][1], rhs[i][2], rhs[i][3]);
+            cp_wait_all();
+            bar_sync(5, NCOMP);
+            tile_fma(out, As, Bs, tr, tc);
+            bar_sync(5, NCOMP);   // the stage-0 buffers are reused by accumulate()
+        }
+        // then t = partial slots in fixed order + the last segment (up to j-3)
         const int nq = j > 2 ? j - 2 : 0;
         const int nseg = (nq + a.seg - 1) / a.seg;
         for (int s2 = 0; s2 + 1 < nseg; ++s2) {
@@ -435,53 +529,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             }
         }
         accumulate(t, r0, c0, cc, nseg > 0 ? (nseg - 1) * a.seg : 0, nq);
-        // right-hand side minus t: forward truncates R (FP64, original order)
-        // to FP32; backward starts from z = D^{-1} y
-        float acc[4][4];
+        // P_j = Dinv_j RHS_j - t
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + tr * 4 + i;
-            if (!BWD) {
-                const int64_t pr = r < a.N ? a.perm[r] : 0;
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    const int c = c0 + tc * 4 + jj;
-                    acc[i][jj] = (r < a.N && c < a.ncol) ? __double2float_rn(a.R[pr + (int64_t)c * a.ldr]) : 0.f;
-                }
-            } else {
-                const float4 y = *reinterpret_cast<const float4 *>(&a.Y[r * a.ncolp + c0 + tc * 4]);
-                const float d = r < a.N ? a.D[r] : 1.f;
-                acc[i][0] = __fdiv_rn(y.x, d);
-                acc[i][1] = __fdiv_rn(y.y, d);
-                acc[i][2] = __fdiv_rn(y.z, d);
-                acc[i][3] = __fdiv_rn(y.w, d);
-            }
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) acc[i][jj] -= t[i][jj];
-        }
-        // ---- P_j = Dinv_j acc
-        {
-            float *As = sm, *Bs = sm + TILE;
-            const float *Li = Dinv + (size_t)b * TILE;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = tid + u * NCOMP;
-                cp_async16(&As[e * 4], Li + e * 4);
-            }
-            cp_commit();
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                *reinterpret_cast<float4 *>(&Bs[(tr * 4 + i) * CW + tc * 4]) =
-                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-            cp_wait_all();
-            bar_sync(5, NCOMP);
-            float out[4][4] = {};
-            tile_fma(out, As, Bs, tr, tc);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                *reinterpret_cast<float4 *>(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4]) =
-                    make_float4(out[i][0], out[i][1], out[i][2], out[i][3]);
-        }
+        for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<float4 *>(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4]) =
+                make_float4(out[i][0] - t[i][0], out[i][1] - t[i][1], out[i][2] - t[i][2], out[i][3] - t[i][3]);
         bar_sync(5, NCOMP);
         if (tid == 0) {
             __threadfence();
@@ -508,18 +560,17 @@ void precond_setup(hf_ctx *ctx, Precond &p, int64_t N, int64_t L, const float *L
     p.Up.alloc((size_t)p.Np * p.Np, st);
     p.LinvF.alloc((size_t)nblk * TILE, st);
     p.LinvB.alloc((size_t)nblk * TILE, st);
-    p.MF.alloc((size_t)nblk * 2 * TILE, st);
-    p.MB.alloc((size_t)nblk * 2 * TILE, st);
     ClassTimer tm(ctx, "trsm");
     dim3 g((unsigned)(p.Np / 32), (unsigned)(p.Np / 32));
     k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Lfac, p.Lp.p, p.Up.p);
     HF_CHECK_LAUNCH(ctx);
     k_diag_inv<<<(unsigned)nblk, TBS, 0, st>>>(p.Np, p.Lp.p, p.LinvF.p, p.LinvB.p);
     HF_CHECK_LAUNCH(ctx);
-    dim3 gm((unsigned)nblk, 2);
-    k_mk<false><<<gm, 256, 0, st>>>((int)nblk, p.Np, p.Lp.p, p.Up.p, p.LinvF.p, p.MF.p);
+    // G = Dinv Op in place (after the diagonal inverses, which read the diagonal blocks only)
+    dim3 gs((unsigned)nblk, (unsigned)nblk);
+    k_scale_op<false><<<gs, 256, 0, st>>>((int)nblk, p.Np, p.Lp.p, p.LinvF.p);
     HF_CHECK_LAUNCH(ctx);
-    k_mk<true><<<gm, 256, 0, st>>>((int)nblk, p.Np, p.Lp.p, p.Up.p, p.LinvB.p, p.MB.p);
+    k_scale_op<true><<<gs, 256, 0, st>>>((int)nblk, p.Np, p.Up.p, p.LinvB.p);
     HF_CHECK_LAUNCH(ctx);
 }
 
@@ -608,7 +659,7 @@ void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64
     p.epoch += 1;
     TrsmArgs a{p.N, p.Np, (int)ncol, ncolp, nch, nblk, seg, p.items, p.nitems, p.pbase, p.part.p,
                p.P.p, p.pflags.p, p.flags.p + 2 * nblk * nch, p.nslots, p.Lp.p, p.Up.p, p.LinvF.p, p.LinvB.p,
-               p.MF.p, p.MB.p, p.D, p.perm, R, ldr, p.Y.p, p.Xb.p, p.flags.p, p.counter.p,
+               p.D, p.perm, R, ldr, p.Y.p, p.Xb.p, p.flags.p, p.counter.p,
                reinterpret_cast<unsigned *>(p.counter.p + 2), p.epoch, nullptr};
     const bool want_dbg = getenv("HF_TRSM_DEBUG") != nullptr;
     if (want_dbg) {
