@@ -87,6 +87,12 @@ hf_status hf_destroy(hf_ctx *ctx) {
             cudaEventDestroy(pr.second);
         }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    for (auto e : ctx->ev)
+        if (e) cudaEventDestroy(e);
 #ifdef HF_WITH_NCCL
     if (ctx->comm) ncclCommDestroy(ctx->comm);
 #endif

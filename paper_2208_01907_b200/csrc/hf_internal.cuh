@@ -123,6 +123,8 @@ struct hf_ctx {
     std::map<std::string, hf::KStat> stats;
     std::vector<cudaEvent_t> event_pool;
     std::map<std::pair<int, int>, hf::TrsmTable> trsm_tables;   // (nblk, nch) -> table
+    cudaStream_t side = nullptr;       // second stream (stage-1 lookahead: trailing updates), lazily created
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace hf {
@@ -131,15 +133,16 @@ namespace hf {
 struct ClassTimer {
     hf_ctx *ctx;
     const char *cls;
+    cudaStream_t s;
     cudaEvent_t a = nullptr, b = nullptr;
-    ClassTimer(hf_ctx *c, const char *k) : ctx(c), cls(k) {
+    ClassTimer(hf_ctx *c, const char *k, cudaStream_t on = nullptr) : ctx(c), cls(k), s(on ? on : c->stream) {
         if (!ctx->profiling) return;
         a = take(); b = take();
-        cudaEventRecord(a, ctx->stream);
+        cudaEventRecord(a, s);
     }
     ~ClassTimer() {
         if (!ctx->profiling || !a) return;
-        cudaEventRecord(b, ctx->stream);
+        cudaEventRecord(b, s);
         ctx->pending[cls].push_back({a, b});
     }
     cudaEvent_t take() {

@@ -115,6 +115,16 @@ struct ChainArgs {
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
     unsigned long long *dbg;   // optional per-phase time sums (CTA 0), HF_CHAIN_DEBUG
+    // lookahead (the previous panel's trailing update runs concurrently): V is the
+    // matrix at the START of the previous panel, in its position space; the
+    // previous panel's updates of the pivot columns are applied here
+    const int32_t *mapprev;   // current position -> previous position (null: none)
+    const float *SNprev;      // [prev pos][nbmax] -sigma_u s_i^u of the previous panel
+    const float *sigprev;     // [nbprev] sigma of the previous panel
+    const float *DGprev;      // [prev pos] lazy diagonal at the end of the previous panel
+    int nbprev, nbmax;
+    float *SNout;             // [pos][nbmax] this panel's values (for the next panel)
+    float *DGout;             // [pos] lazy diagonal at the end of this panel
 };
 
 constexpr int SLOT_STRIDE = 32;     // 256 B between slots: no two CTAs' slots share an L2 line
@@ -155,13 +165,19 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const int64_t r0 = (int64_t)blockIdx.x * a.R;
     const int64_t nown = max((int64_t)0, min((int64_t)a.R, a.m - r0));
     const int nb = a.nbp;
+    const int nbq = a.nbprev;                 // previous panel's pivots (lookahead) or 0
     float *sneg = smem;                       // [nbp][R]  -sigma_u s_i^u for own rows
-    float *sp = smem + (size_t)nb * a.R;      // [nbp]     s_P^u of the current pivot row
-    float *sgm = sp + nb;                     // [nbp]     sigma_u
+    float *snp = sneg + (size_t)nb * a.R;     // [nbq][R]  the same for the previous panel
+    float *sp = snp + (size_t)nbq * a.R;      // [nbp]     s_P^u of the current pivot row
+    float *spp = sp + nb;                     // [nbq]     s_P^u of the previous panel
+    float *sgm = spp + nbq;                   // [nbp]     sigma_u
 
     const bool has = tid < nown;
     const int64_t i = r0 + tid;
-    float dg = has ? a.V[i + i * a.ldv] : 0.f;      // lazy diagonal of own row
+    const int64_t io = (has && a.mapprev) ? (int64_t)a.mapprev[i] : i;   // own row in V's position space
+    float dg = has ? (a.DGprev ? a.DGprev[io] : a.V[i + i * a.ldv]) : 0.f;   // lazy diagonal of own row
+    if (has)
+        for (int u = 0; u < nbq; ++u) snp[(size_t)u * a.R + tid] = a.SNprev[io * a.nbmax + u];
     bool piv = !has;
     const int32_t oi = has ? a.orig[i] : 0;
     float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
@@ -254,6 +270,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         }
         const float sg = d > 0.f ? 1.f : -1.f;
         // ---- F: [R6] pivot row from the winner's mailbox, stale column for own rows
+        const int64_t Po = a.mapprev ? (int64_t)a.mapprev[P] : P;   // pivot in V's position space
         {
             const int owner = (int)(P / a.R);
             const unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + owner) * nb;
@@ -264,10 +281,11 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
                 } while ((w & TAGM) != tag);
                 sp[u] = -sgm[u] * __uint_as_float((uint32_t)(w >> 32));   // s_P^u (exact sign flip)
             }
+            for (int u = tid; u < nbq; u += nthr) spp[u] = -a.sigprev[u] * a.SNprev[Po * a.nbmax + u];
             if (tid == 0) sgm[t] = sg;
         }
         float v = 0.f;
-        if (!piv && i != P) v = (i >= P) ? a.V[i + P * a.ldv] : a.V[P + i * a.ldv];
+        if (!piv && i != P) v = (io >= Po) ? a.V[io + Po * a.ldv] : a.V[Po + io * a.ldv];
         __syncthreads();
         PH(2)
         // ---- G: column, scaled column, lazy diagonal
@@ -280,6 +298,21 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             a.sigma[t] = sg;
         } else if (!piv) {
             float c = v;
+            {   // [R8] the previous panel's pivots first (what its trailing update applies), in order
+                const float *sq = snp + tid;
+                int u = 0;
+                for (; u + 8 <= nbq; u += 8) {
+                    float x[8], y[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        x[q] = sq[(size_t)(u + q) * a.R];
+                        y[q] = spp[u + q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) c = __fmaf_rn(x[q], y[q], c);
+                }
+                for (; u < nbq; ++u) c = __fmaf_rn(sq[(size_t)u * a.R], spp[u], c);
+            }
             const float *sn = sneg + tid;
             int u = 0;
             for (; u + 8 <= t; u += 8) {                 // [R8] one fmaf per earlier pivot, in order
@@ -311,6 +344,10 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
     }
     if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
+    if (a.SNout && has) {   // this panel's values and the lazy diagonal, for the next panel's lookahead
+        for (int u = 0; u < t; ++u) a.SNout[i * a.nbmax + u] = sneg[(size_t)u * a.R + tid];
+        a.DGout[i] = dg;
+    }
     if (dbg) {
         for (int q = 0; q < 4; ++q) a.dbg[q] += ph[q];
         a.dbg[4] += t;
@@ -530,26 +567,42 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     // fewer CTAs make the per-pivot exchange cheaper until the rows per CTA no longer fit a
     // 128-wide panel in shared memory, so G = max(64, L / 443) and nb = 128 by default.
     const int nb_def = 128;
-    int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / (nb_def + 2)))));
+    // Lookahead (HF_LOOKAHEAD=1, off by default): the chain of panel p+1 runs while panel
+    // p's trailing update runs on a second stream, applying panel p's updates to its pivot
+    // columns itself (the same fmaf, so the bits do not change).  Measured at C2: 103 ms
+    // (chain 5.5 us/pivot: the concurrent update's memory traffic slows every exchange and
+    // column read) against 99 ms serial, so the serial schedule is the default.
+    const bool look = getenv("HF_LOOKAHEAD") && atoi(getenv("HF_LOOKAHEAD")) != 0;
+    const int64_t per_row = look ? 2 * nb_def + 3 : nb_def + 2;   // floats of shared memory per row
+    int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / per_row))));
     if (const char *e = getenv("HF_CHAIN_CTAS")) gmax = std::max(1, std::min(nsm, atoi(e)));
     const int64_t G0 = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(L, 32)));
     const int64_t R0 = cdiv(L, G0);
     HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
     int nb = o.nb > 0 ? o.nb : nb_def;
-    while (nb > 8 && (int64_t)(nb * R0 + 2 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
+    // with lookahead the chain holds both panels' values of its rows in shared memory
+    const int nbf = (look ? 2 : 1);
+    while (nb > 8 && (int64_t)(nbf * nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
     HF_REQUIRE(nb >= 8 && nb <= 1024, "panel width out of range");
 
     DBuf<float> V[2];
     V[0].alloc((size_t)L * L, st);
     V[1].alloc((size_t)L * L, st);
-    DBuf<int32_t> orig[2], map;
+    DBuf<int32_t> orig[2], map[2];
     orig[0].alloc(L, st);
     orig[1].alloc(L, st);
-    map.alloc(L, st);
-    DBuf<float> S, Sn, sigma, Lorig, Dk;
-    S.alloc((size_t)L * nb, st);
-    Sn.alloc((size_t)L * nb, st);
-    sigma.alloc(nb, st);
+    map[0].alloc(L, st);
+    if (look) map[1].alloc(L, st);
+    DBuf<float> S[2], Sn[2], sigma[2], SNrow[2], DG[2], Lorig, Dk;
+    for (int b = 0; b < (look ? 2 : 1); ++b) {
+        S[b].alloc((size_t)L * nb, st);
+        Sn[b].alloc((size_t)L * nb, st);
+        sigma[b].alloc(nb, st);
+        if (look) {
+            SNrow[b].alloc((size_t)L * nb, st);
+            DG[b].alloc(L, st);
+        }
+    }
     Lorig.alloc((size_t)L * L, st);
     Dk.alloc(L, st);
     DBuf<int32_t> pivpos, pivorig, status;
@@ -575,6 +628,16 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         k_iota32<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
         HF_CHECK_LAUNCH(ctx);
     }
+    cudaStream_t st2 = st;
+    if (look) {
+        if (!ctx->side) {
+            HF_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            for (auto &e : ctx->ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        st2 = ctx->side;
+        HF_CUDA(cudaEventRecord(ctx->ev[0], st));        // the side stream starts after the setup above
+        HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[0], 0));
+    }
 
     HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     DBuf<unsigned long long> dbg;
@@ -583,23 +646,36 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         dbg.alloc(8, st);
         dbg.zero(st);
     }
-    int cur = 0;
+    // buffers of panel p: V[vb] is the matrix at the START of panel p (its position space),
+    // S/Sn/sigma/SNrow/DG[p & 1] its values, map[p & 1] its compaction (p+1 space -> p space)
+    int cur = 0, vb = 0, pidx = 0, nbprev = 0;
+    bool tr_pending = false;   // a trailing update is in flight on the side stream
     int64_t m = L, K0 = 0;
     while (m > 0) {
         const int nbp = (int)std::min<int64_t>(nb, m);
         const int64_t G = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(m, 32)));
         const int64_t R = cdiv(m, G);
         const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
-        const size_t shm = ((size_t)nbp * R + 2 * nbp) * sizeof(float);
+        const int pb = look ? (pidx & 1) : 0, qb = pb ^ 1;
+        const size_t shm = ((size_t)(nbp + (look ? nbprev : 0)) * R + 3 * nbp + (look ? nbprev : 0)) * sizeof(float);
         if (xmode == 0) HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
-        ca.V = V[cur].p; ca.ldv = L; ca.orig = orig[cur].p;
-        ca.S = S.p; ca.Sn = Sn.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
+        ca.V = V[vb].p; ca.ldv = L; ca.orig = orig[cur].p;
+        ca.S = S[pb].p; ca.Sn = Sn[pb].p; ca.lds = L; ca.sigma = sigma[pb].p; ca.pivpos = pivpos.p;
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
         ca.slots = slots.p; ca.xmode = xmode;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
+        ca.nbmax = nb;
+        if (look && pidx > 0) {
+            ca.mapprev = map[qb].p; ca.SNprev = SNrow[qb].p; ca.sigprev = sigma[qb].p; ca.DGprev = DG[qb].p;
+            ca.nbprev = nbprev;
+        } else {
+            ca.mapprev = nullptr; ca.SNprev = nullptr; ca.sigprev = nullptr; ca.DGprev = nullptr; ca.nbprev = 0;
+        }
+        ca.SNout = look ? SNrow[pb].p : nullptr;
+        ca.DGout = look ? DG[pb].p : nullptr;
         {
             ClassTimer tm(ctx, "chain");
             void *args[] = {&ca};
@@ -611,23 +687,54 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             {
                 ClassTimer tm(ctx, "other");
                 k_compact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
-                    m, nbp, pivpos.p, orig[cur].p, map.p, orig[cur ^ 1].p, status.p);
+                    m, nbp, pivpos.p, orig[cur].p, map[pb].p, orig[cur ^ 1].p, status.p);
                 HF_CHECK_LAUNCH(ctx);
             }
+            // trailing update of this panel: V at the start of panel p (V[?]) -> V at the start
+            // of panel p+1.  Serial: V[cur] -> V[cur^1].  Lookahead: the chain of panel p
+            // read V[vb] (start of panel p-1); the trailing update of panel p-1 (in flight)
+            // writes the start of panel p into the other buffer, and this one then turns it
+            // into the start of panel p+1 in V[vb], which the next chain no longer needs.
             TrailArgs ta;
-            ta.mp = mp; ta.nbp = nbp; ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p; ta.ldv = L;
-            ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L; ta.status = status.p;
+            ta.mp = mp; ta.nbp = nbp; ta.ldv = L;
+            ta.map = map[pb].p; ta.S = S[pb].p; ta.Sn = Sn[pb].p; ta.lds = L; ta.status = status.p;
             const int64_t T = cdiv(mp, TB);
             const int64_t ntiles = T * (T + 1) / 2;
-            {
+            if (!look) {
+                ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
                 ClassTimer tm(ctx, "trailing");
                 k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
+                vb ^= 1;
+            } else {
+                // the side stream: wait for this chain (S, Sn, map of panel p)
+                HF_CUDA(cudaEventRecord(ctx->ev[1], st));
+                HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[1], 0));
+                const int vsrc = (pidx == 0) ? vb : (vb ^ 1);   // start of panel p
+                ta.Vold = V[vsrc].p; ta.Vnew = V[vsrc ^ 1].p;
+                {
+                    ClassTimer tm(ctx, "trailing", st2);
+                    k_trailing<<<(unsigned)ntiles, 256, 0, st2>>>(ta);
+                    HF_CHECK_LAUNCH(ctx);
+                }
+                // the next chain reads the start of panel p (vsrc); before it runs, the trailing
+                // update of panel p-1 (which wrote vsrc) must be done -- it is, being earlier on st2;
+                // wait for everything on st2 except this launch: record after the previous one
+                if (tr_pending) HF_CUDA(cudaStreamWaitEvent(st, ctx->ev[2], 0));
+                HF_CUDA(cudaEventRecord(ctx->ev[2], st2));
+                tr_pending = true;
+                vb = vsrc;
             }
             cur ^= 1;
         }
+        nbprev = nbp;
         K0 += nbp;
         m = mp;
+        ++pidx;
+    }
+    if (look) {   // join the side stream before the trailing buffers can be released
+        HF_CUDA(cudaEventRecord(ctx->ev[3], st2));
+        HF_CUDA(cudaStreamWaitEvent(st, ctx->ev[3], 0));
     }
     int32_t hs[4];
     HF_CUDA(cudaMemcpyAsync(hs, status.p, sizeof(hs), cudaMemcpyDeviceToHost, st));

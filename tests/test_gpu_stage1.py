@@ -99,3 +99,27 @@ def test_stage1_c1_full_size(ctx):
     _, _, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min)
     assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
     assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+
+
+def test_stage1_lookahead_schedule_bitwise():
+    """The lookahead schedule (HF_LOOKAHEAD=1: panel p+1's chain concurrent with panel p's
+    trailing update, the chain applying panel p's updates to its pivot columns) gives the
+    same bits as the oracle -- the canonical order [R8] does not depend on the schedule."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, hf_inputs as hi, oracle\n"
+        "from paper_2208_01907_b200 import hf\n"
+        "spec = hi.CONFIGS['P2048']; Kb = hi.make_kbar('P2048', 1)\n"
+        "Ko, _ = oracle.scale(Kb.numpy()); Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)\n"
+        "ctx = hf.Context(0); Kd = Kb.cuda(); hf.hf_scale(ctx, Kd)\n"
+        "lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min, nb=64)\n"
+        "perm, D, Lf = lf.export()\n"
+        "assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)\n"
+        "assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)\n"
+        "print('ok')\n")
+    env = dict(os.environ, HF_LOOKAHEAD="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
