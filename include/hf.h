@@ -64,6 +64,17 @@ hf_status hf_nccl_unique_id(void *id128_host);
  * hard factorization and hf_solve are replicated (deterministic kernels:
  * identical on every rank).  Pure host function, needs no device. */
 hf_status hf_shard_cols(int64_t n2, int nranks, int rank, int64_t *c0_host, int64_t *c1_host);
+/* Multi-GPU stage 1: on a context of nranks > 1,
+ * hf_factor_lowprec splits the FP32 trailing matrix by columns: rank r holds
+ * FULL columns (all active rows) of the original indices j with
+ * (j / 128) % nranks == r and updates only those; every rank runs the pivot
+ * chain itself (same inputs, same pivots, no pivot exchange) and reads each
+ * pivot column from its owner's memory through a CUDA-IPC peer mapping over
+ * NVLink; one NCCL barrier per panel.  Results are bitwise those of one GPU.
+ * hf_set_stage1_partitions(ctx, G > 0) runs the same partitioned algorithm
+ * with all G partitions on this GPU (single-process emulation, tests); 0 = the
+ * single-GPU lower-triangle path. */
+hf_status hf_set_stage1_partitions(hf_ctx *ctx, int nparts);
 /* Single-GPU emulation of one rank of that sharding (tests): with nranks > 0,
  * hf_schur_gcr computes only rank's slice of S22 / X12 and leaves the other
  * columns zero (no collective); nranks = 0 switches the emulation off. */

@@ -171,7 +171,9 @@ hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
         HF_REQUIRE(o.tau > 0.0 && o.tau < 1.0, "hf_factor_lowprec: tau must lie in (0,1)");
         HF_REQUIRE(o.n_extra >= 0 && o.n_min >= 0, "hf_factor_lowprec: n_extra/n_min < 0");
         HF_REQUIRE(o.nb >= 0 && o.nb <= 256 && o.nb % 8 == 0, "hf_factor_lowprec: nb in {0, 8..256, multiple of 8}");
-        hf::lowprec_factor(ctx, L, K, ld, o, lf.get());
+        if (ctx->nranks > 1) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->nranks);
+        else if (ctx->s1parts > 0) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->s1parts);
+        else hf::lowprec_factor(ctx, L, K, ld, o, lf.get());
     });
     if (s != HF_OK) return s;
     if (N_host) *N_host = lf->N;

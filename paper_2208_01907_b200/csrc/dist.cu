@@ -33,6 +33,13 @@ void collective_bcast(hf_ctx *ctx, double *buf, size_t count, int root) {
 void collective_max(hf_ctx *ctx, double *buf, size_t count) {
     HF_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream));
 }
+void collective_allgather_bytes(hf_ctx *ctx, const void *send, void *recv, size_t bytes) {
+    HF_NCCL(ncclAllGather(send, recv, bytes, ncclChar, ctx->comm, ctx->stream));
+}
+// stream-ordered barrier over the ranks (a 1-int all-reduce)
+void collective_barrier(hf_ctx *ctx, int *dev_int) {
+    HF_NCCL(ncclAllReduce(dev_int, dev_int, 1, ncclInt, ncclSum, ctx->comm, ctx->stream));
+}
 #endif
 
 }  // namespace hf
@@ -49,6 +56,12 @@ hf_status hf_set_virtual_rank(hf_ctx *ctx, int rank, int nranks) {
     if (!ctx || nranks < 0 || (nranks > 0 && (rank < 0 || rank >= nranks))) return HF_ERR_INVALID_ARG;
     ctx->vrank = nranks > 0 ? rank : 0;
     ctx->vnranks = nranks;
+    return HF_OK;
+}
+
+hf_status hf_set_stage1_partitions(hf_ctx *ctx, int nparts) {
+    if (!ctx || nparts < 0 || nparts > 1024) return HF_ERR_INVALID_ARG;
+    ctx->s1parts = nparts;
     return HF_OK;
 }
 

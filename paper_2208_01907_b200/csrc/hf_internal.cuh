@@ -112,6 +112,7 @@ struct hf_ctx {
     int num_sms = 148;
     int rank = 0, nranks = 1;
     int vrank = 0, vnranks = 0;        // single-GPU emulation of one rank (hf_set_virtual_rank)
+    int s1parts = 0;                   // stage-1 column partitions emulated on this GPU (0: off)
 #ifdef HF_WITH_NCCL
     ncclComm_t comm = nullptr;
 #endif
@@ -227,6 +228,8 @@ namespace hf {
 void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);
 void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                     hf_lowfactor *lf);
+void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                          hf_lowfactor *lf, int nparts);
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
@@ -238,5 +241,7 @@ void collective_begin(hf_ctx *ctx);
 void collective_end(hf_ctx *ctx);
 void collective_bcast(hf_ctx *ctx, double *buf, size_t count, int root);
 void collective_max(hf_ctx *ctx, double *buf, size_t count);
+void collective_allgather_bytes(hf_ctx *ctx, const void *send, void *recv, size_t bytes);
+void collective_barrier(hf_ctx *ctx, int *dev_int);
 #endif
 }  // namespace hf

@@ -28,7 +28,7 @@ EXPORTED = [
     "hf_set_profiling", "hf_kernel_stats", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
-    "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank",
+    "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
 ]
 
 
@@ -89,6 +89,7 @@ def load() -> ctypes.CDLL:
         "hf_precond_apply": [vp, vp, i64, vp, i64, vp, i64],
         "hf_shard_cols": [i64, ctypes.c_int, ctypes.c_int, pi64, pi64],
         "hf_set_virtual_rank": [vp, ctypes.c_int, ctypes.c_int],
+        "hf_set_stage1_partitions": [vp, ctypes.c_int],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -192,6 +193,12 @@ def hf_shard_cols(n2: int, nranks: int, rank: int) -> tuple[int, int]:
 
 def hf_set_virtual_rank(ctx: "Context", rank: int, nranks: int) -> None:
     ctx.check(ctx.lib.hf_set_virtual_rank(ctx.h, int(rank), int(nranks)))
+
+
+def hf_set_stage1_partitions(ctx: "Context", nparts: int) -> None:
+    """Run stage 1 column-partitioned over `nparts` partitions on this GPU (emulation of the
+    multi-GPU factorization; 0 = single-GPU path)."""
+    ctx.check(ctx.lib.hf_set_stage1_partitions(ctx.h, int(nparts)))
 
 
 def nccl_unique_id() -> bytes:

@@ -81,3 +81,28 @@ def test_nccl_path_one_rank():
         assert kd == HF.kernel_dim
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("name,seed,G,nb", [("P512", 0, 1, 0), ("P512", 2, 3, 0), ("P2048", 0, 2, 0),
+                                            ("P2048", 1, 5, 64), ("N32", 0, 4, 0), ("S24", 0, 3, 128),
+                                            ("C1", 0, 8, 0)])
+def test_stage1_partitions_bitwise(ctx, name, seed, G, nb):
+    """The column-partitioned stage 1 of the multi-GPU path (every partition's FULL
+    columns, replicated pivot chain reading the pivot column from its owner), all G
+    partitions emulated on this GPU: Pi, D and L bit-identical to the oracle [R8]."""
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    Kd = Kb.cuda()
+    hf.hf_scale(ctx, Kd)
+    try:
+        hf.hf_set_stage1_partitions(ctx, G)
+        lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min, nb=nb)
+    finally:
+        hf.hf_set_stage1_partitions(ctx, 0)
+    perm, D, Lf = lf.export()
+    assert lf.N == Fo.N and lf.L - lf.n2_tau_only == Fo.Ntau
+    assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+    assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)

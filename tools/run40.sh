@@ -1,0 +1,3 @@
+python -c "from paper_2208_01907_b200 import build; build.build()" || exit 1
+timeout 900 python -m pytest tests/test_gpu_dist.py tests/test_gpu_stage1.py -x -q > gpurun_out/t40.log 2>&1; echo t=$?
+timeout 900 python tools/probe_parts.py C2 8 > gpurun_out/parts_c2.log 2>&1; echo a=$?
