@@ -75,6 +75,10 @@ hf_status hf_shard_cols(int64_t n2, int nranks, int rank, int64_t *c0_host, int6
  * with all G partitions on this GPU (single-process emulation, tests); 0 = the
  * single-GPU lower-triangle path. */
 hf_status hf_set_stage1_partitions(hf_ctx *ctx, int nparts);
+/* The columns (original indices, increasing) partition `part` of `nparts` owns
+ * in that factorization: j with (j / 128) % nparts == part.  Host only; the
+ * list is written if cols_host is not NULL (room for L entries). */
+hf_status hf_stage1_partition(int64_t L, int nparts, int part, int64_t *ncols_host, int64_t *cols_host);
 /* Single-GPU emulation of one rank of that sharding (tests): with nranks > 0,
  * hf_schur_gcr computes only rank's slice of S22 / X12 and leaves the other
  * columns zero (no collective); nranks = 0 switches the emulation off. */

@@ -59,6 +59,19 @@ hf_status hf_set_virtual_rank(hf_ctx *ctx, int rank, int nranks) {
     return HF_OK;
 }
 
+hf_status hf_stage1_partition(int64_t L, int nparts, int part, int64_t *ncols_host, int64_t *cols_host) {
+    if (L < 0 || nparts < 1 || part < 0 || part >= nparts || !ncols_host) return HF_ERR_INVALID_ARG;
+    const int64_t CB = 128;   // column block of the partitioned factorization (k_lowprec.cu)
+    int64_t n = 0;
+    for (int64_t j = 0; j < L; ++j)
+        if ((j / CB) % nparts == part) {
+            if (cols_host) cols_host[n] = j;
+            ++n;
+        }
+    *ncols_host = n;
+    return HF_OK;
+}
+
 hf_status hf_set_stage1_partitions(hf_ctx *ctx, int nparts) {
     if (!ctx || nparts < 0 || nparts > 1024) return HF_ERR_INVALID_ARG;
     ctx->s1parts = nparts;

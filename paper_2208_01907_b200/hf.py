@@ -29,6 +29,7 @@ EXPORTED = [
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
+    "hf_stage1_partition",
 ]
 
 
@@ -90,6 +91,7 @@ def load() -> ctypes.CDLL:
         "hf_shard_cols": [i64, ctypes.c_int, ctypes.c_int, pi64, pi64],
         "hf_set_virtual_rank": [vp, ctypes.c_int, ctypes.c_int],
         "hf_set_stage1_partitions": [vp, ctypes.c_int],
+        "hf_stage1_partition": [i64, ctypes.c_int, ctypes.c_int, pi64, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -199,6 +201,16 @@ def hf_set_stage1_partitions(ctx: "Context", nparts: int) -> None:
     """Run stage 1 column-partitioned over `nparts` partitions on this GPU (emulation of the
     multi-GPU factorization; 0 = single-GPU path)."""
     ctx.check(ctx.lib.hf_set_stage1_partitions(ctx.h, int(nparts)))
+
+
+def hf_stage1_partition(L: int, nparts: int, part: int) -> np.ndarray:
+    """Original column indices partition `part` owns in the multi-GPU stage 1 (host only)."""
+    n = ctypes.c_int64()
+    cols = np.empty(max(L, 1), dtype=np.int64)
+    st = load().hf_stage1_partition(int(L), int(nparts), int(part), ctypes.byref(n), cols.ctypes.data)
+    if st != HF_OK:
+        raise HFError(st, "hf_stage1_partition: bad arguments")
+    return cols[: n.value]
 
 
 def nccl_unique_id() -> bytes:

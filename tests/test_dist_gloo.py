@@ -37,6 +37,11 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(allp, mine)
             out[n2] = allp
         out["max"] = bench.max_over_ranks(float(10 * rank + 1))
+        for L in (1, 300, 16384, 23040):
+            cols = hf.hf_stage1_partition(L, world, rank)
+            allc = [None] * world
+            dist.all_gather_object(allc, cols.tolist())
+            out[("s1", L)] = allc
         seeds = [None] * world
         dist.all_gather_object(seeds, [0 + rank, 0])     # replicas: seed + rank; shard: seed
         out["seeds"] = seeds
@@ -73,6 +78,13 @@ def test_shard_plan_and_rank_max_gloo():
                 assert a[1] == b[0]                       # ... contiguously, in rank order
             w = [c1 - c0 for c0, c1 in sl]
             assert max(w) - min(w) <= 1                   # balanced
+        for L in (1, 300, 16384, 23040):
+            allc = res[r][("s1", L)]
+            flat = sorted(c for part in allc for c in part)
+            assert flat == list(range(L))                                      # every column exactly once
+            assert all(all((c // 128) % world == g for c in part) for g, part in enumerate(allc))
+            sizes = [len(part) for part in allc]
+            assert max(sizes) - min(sizes) <= 128                              # balanced to one block
     seeds = res[0]["seeds"]
     assert seeds[0][0] != seeds[1][0] and seeds[0][1] == seeds[1][1]
 
