@@ -584,7 +584,8 @@ void precond_setup(hf_ctx *ctx, Precond &p, int64_t N, int64_t L, const float *L
 // first.  Every item depends only on earlier items and on chain stages <=
 // its own stage, so persistent CTAs taking items in order cannot deadlock.
 static void build_items(int nblk, int nch, int seg, std::vector<int4> &items, std::vector<int> &pbase, int &nslots) {
-    const int LA = 24;
+    int LA = 24;   // HF_TRSM_LA: tuning
+    if (const char *e = getenv("HF_TRSM_LA")) LA = std::max(0, atoi(e));
     pbase.assign(nblk, 0);
     nslots = 0;
     std::vector<std::vector<int4>> stage(nblk + 2);   // stage s -> index s+1 (stage -1 first)
@@ -621,12 +622,13 @@ void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64
     const int nblk = (int)(p.Np / TBS);
     const int nch = (int)cdiv(ncol, CW);
     const int ncolp = nch * CW;
-    const int seg = std::max(8, (int)cdiv(nblk, 32));
+    int seg = std::max(16, (int)cdiv(nblk, 32));   // HF_TRSM_SEG: tuning (8 / 16 / 32: 7.6 / 7.2 / 7.1-7.5 ms per C2 apply)
+    if (const char *e = getenv("HF_TRSM_SEG")) seg = std::max(2, atoi(e));
     p.Y.alloc((size_t)p.Np * ncolp, st);
     p.Xb.alloc((size_t)p.Np * ncolp, st);
     p.P.alloc((size_t)p.Np * ncolp, st);
     if (p.tab_nblk != nblk || p.tab_nch != nch) {
-        auto key = std::make_pair(nblk, nch);
+        auto key = std::make_pair(nblk, nch * 1000 + seg);
         auto it = ctx->trsm_tables.find(key);
         if (it == ctx->trsm_tables.end()) {
             std::vector<int4> items;
