@@ -146,6 +146,19 @@ hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
 hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, const double *R,
                            int64_t ldr, double *W, int64_t ldw);
 
+/* ------------- NEXT-2: IR / GCR / block GCR comparison (Fig. 2) */
+/* K11 X = B with the FP32 preconditioner of lf: method 0 = Algorithm 3 (mixed-
+ * precision iterative refinement), 1 = Algorithm 4 (GCR, P:277-295,
+ * one column at a time), 2 = Algorithm 5 (block GCR).  B, X: DEVICE
+ * L x ncol column-major (ld L), original row order (Lambda_2 rows of B ignored,
+ * of X set to 0).  Stops when every column's ||r||_2/||b||_2 <= tol or after
+ * max_iter iterations (HF_ERR_NOT_CONVERGED); iters_host = iterations (max over
+ * columns for method 1), hist_host[0..hist_len) = max relative residual after
+ * iteration 0, 1, ... (-1 past the end).  Synchronises. */
+hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf, int method,
+                          int64_t ncol, const double *B, double *X, double tol, int32_t max_iter,
+                          int32_t *iters_host, double *hist_host, int32_t hist_len);
+
 /* ------------------------ a4-a6: block GCR + Schur */
 typedef struct {
     double tol;        /* per-column recursive ||r||_2/||b||_2 target [R13] (1e-14) */

@@ -23,6 +23,7 @@
 #include "k_small.cuh"
 
 #include <string>
+#include <vector>
 
 namespace hf {
 namespace {
@@ -35,6 +36,7 @@ struct GcrWork {
     DBuf<double> bn2, rn2, res;
     DBuf<double> dgw, chw, chdg;
     DBuf<int> status;
+    std::vector<double> *hist = nullptr;   // optional: max relative residual after every iteration
 };
 
 void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {
@@ -94,6 +96,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
     maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
     int bad = 0;
     double res = read_res(ctx, w, &bad);
+    if (w.hist) w.hist->push_back(res);
     int iters = 0;
     bool conv = res <= o.tol;
     if (!conv) {
@@ -113,6 +116,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
             colnorm2(ctx, L, n, R, L, w.rn2.p);
             maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
             res = read_res(ctx, w, &bad);
+            if (w.hist) w.hist->push_back(res);
             iters = it + 1;
             if (getenv("HF_GCR_DEBUG")) fprintf(stderr, "[hf gcr] n2=%lld it=%d res=%.3e bad=%d\n", (long long)n, iters, res, bad);
             if (res <= o.tol) {
@@ -153,6 +157,44 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ Alg. 3 (IR) and the comparison
+// Algorithm 3, mixed-precision iterative refinement on the same
+// kernels: x_0 = Q^{-1} b, r = b - A x, repeat e = Q^{-1} r, x += e, r = b - A x
+// (A = K11 in original row order); all columns at once, stop when every column's
+// ||r||_2 / ||b||_2 <= tol.
+void iterative_refinement(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, Precond &pc,
+                          const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info,
+                          GcrWork &w) {
+    cudaStream_t st = ctx->stream;
+    w.R.alloc((size_t)L * n, st);
+    w.bn2.alloc(n, st);
+    w.rn2.alloc(n, st);
+    w.res.alloc(1, st);
+    w.status.alloc(1, st);
+    w.status.zero(st);
+    DBuf<double> E;
+    E.alloc((size_t)L * n, st);
+    colnorm2(ctx, L, n, B, L, w.bn2.p);
+    precond_apply(ctx, pc, n, B, L, X, L);                                // steps 1-2
+    int bad = 0, iters = 0;
+    double res = 0.0;
+    for (;;) {
+        HF_CUDA(cudaMemcpyAsync(w.R.p, B, (size_t)L * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        matvec(ctx, K, ld, L, mask, X, n, w.R.p, 1.0, -1.0, w);           // r = b - A x
+        colnorm2(ctx, L, n, w.R.p, L, w.rn2.p);
+        maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
+        res = read_res(ctx, w, &bad);
+        if (w.hist) w.hist->push_back(res);
+        if (res <= o.tol || iters >= o.max_iter) break;
+        precond_apply(ctx, pc, n, w.R.p, L, E.p, L);                      // e = Q^{-1} r
+        axpy_cols(ctx, L, n, 1.0, E.p, L, X, L);                           // x += e
+        ++iters;
+    }
+    info->iters = iters;
+    info->max_rel_res_recursive = info->max_rel_res_true = res;
+    if (res > o.tol) throw Error{HF_ERR_NOT_CONVERGED, "iterative refinement reached max_iter"};
+}
 
 // ------------------------------------------------------------------ Alg. 1 steps 2-4
 // Multi-GPU (stage 2): the n2 right-hand sides (columns of K12)
@@ -325,6 +367,82 @@ extern "C" hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *
                                       n2, cudaMemcpyDeviceToDevice, ctx->stream));
         }
         HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (const hf::Error &e) {
+        ctx->last_error = e.msg;
+        return e.st;
+    }
+    return HF_OK;
+}
+
+// ------------------------------------------------------------------ Fig. 2 comparison
+// hf_krylov_solve (include/hf.h): K11 X = B by Algorithm 3 (IR), Algorithm 4 (GCR,
+// one column at a time) or Algorithm 5 (block GCR), with the FP32 preconditioner
+// of lf; the maximum relative residual after every iteration goes to hist_host.
+extern "C" hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf, int method,
+                                     int64_t ncol, const double *B, double *X, double tol, int32_t max_iter,
+                                     int32_t *iters_host, double *hist_host, int32_t hist_len) {
+    if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    try {
+        const int64_t L = lf->L;
+        if (!(method >= 0 && method <= 2) || ncol < 0 || ld < L || tol <= 0.0 || max_iter < 1 ||
+            (ncol > 0 && L > 0 && (!K || !B || !X)))
+            throw hf::Error{HF_ERR_INVALID_ARG, "hf_krylov_solve: bad arguments"};
+        if (iters_host) *iters_host = 0;
+        if (ncol == 0 || L == 0 || lf->N == 0) return HF_OK;
+        cudaStream_t st = ctx->stream;
+        hf::DBuf<uint8_t> mask;
+        mask.alloc(L, st);
+        hf::mask_from_pos(ctx, L, lf->pos1.p, mask.p);
+        hf::Precond pc;
+        hf::precond_setup(ctx, pc, lf->N, L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        hf::DBuf<double> Bm;
+        Bm.alloc((size_t)L * ncol, st);
+        for (int64_t c = 0; c < ncol; ++c) hf::mask_vec(ctx, L, mask.p, B + c * L, Bm.p + c * L);
+        hf_gcr_opts o{tol, max_iter};
+        hf_gcr_info info{0, 0.0, 0.0};
+        std::vector<double> hist;
+        int32_t iters = 0;
+        hf_status fail = HF_OK;
+        std::string fail_msg;
+        auto run = [&](auto &&f) {   // outputs are filled even when the solver does not converge
+            try {
+                f();
+            } catch (const hf::Error &e) {
+                if (e.st != HF_ERR_NOT_CONVERGED && e.st != HF_ERR_BREAKDOWN) throw;
+                fail = e.st;
+                fail_msg = e.msg;
+            }
+        };
+        if (method == 0) {
+            hf::GcrWork w;
+            w.hist = &hist;
+            run([&] { hf::iterative_refinement(ctx, K, ld, L, mask.p, pc, Bm.p, ncol, X, o, &info, w); });
+            iters = info.iters;
+        } else if (method == 2) {
+            hf::GcrWork w;
+            w.hist = &hist;
+            run([&] { hf::block_gcr(ctx, K, ld, L, mask.p, pc, Bm.p, ncol, X, o, &info, w); });
+            iters = info.iters;
+        } else {
+            // Algorithm 4 column by column; the history is the max over columns per iteration
+            std::vector<double> hmax;
+            for (int64_t c = 0; c < ncol; ++c) {
+                hf::GcrWork w;
+                std::vector<double> h1;
+                w.hist = &h1;
+                run([&] { hf::block_gcr(ctx, K, ld, L, mask.p, pc, Bm.p + c * L, 1, X + c * L, o, &info, w); });
+                iters = std::max(iters, info.iters);
+                if (hmax.size() < h1.size()) hmax.resize(h1.size(), 0.0);
+                for (size_t q = 0; q < h1.size(); ++q) hmax[q] = std::max(hmax[q], h1[q]);
+                for (size_t q = h1.size(); q < hmax.size(); ++q) hmax[q] = std::max(hmax[q], h1.empty() ? 0.0 : h1.back());
+            }
+            hist = hmax;
+        }
+        if (iters_host) *iters_host = iters;
+        if (hist_host)
+            for (int32_t q = 0; q < hist_len; ++q) hist_host[q] = q < (int32_t)hist.size() ? hist[q] : -1.0;
+        HF_CUDA(cudaStreamSynchronize(st));
+        if (fail != HF_OK) throw hf::Error{fail, fail_msg};
     } catch (const hf::Error &e) {
         ctx->last_error = e.msg;
         return e.st;

@@ -417,6 +417,15 @@ __global__ void k_gather_rows(int64_t n, const int64_t *__restrict__ idx, const 
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[idx[i]];
 }
+// Y[:, c] += alpha X[:, c]
+__global__ void k_axpy_cols(int64_t L, int64_t n, double alpha, const double *__restrict__ X, int64_t ldx,
+                            double *__restrict__ Y, int64_t ldy) {
+    const int64_t tot = L * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % L, c = e / L;
+        Y[i + c * ldy] = fma(alpha, X[i + c * ldx], Y[i + c * ldy]);
+    }
+}
 __global__ void k_mask_vec(int64_t L, const uint8_t *__restrict__ m, const double *__restrict__ src,
                            double *__restrict__ dst) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -509,6 +518,12 @@ void scatter_rows(hf_ctx *ctx, int64_t n, const int64_t *idx, const double *src,
 void gather_rows(hf_ctx *ctx, int64_t n, const int64_t *idx, const double *src, double *dst) {
     if (n <= 0) return;
     k_gather_rows<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(n, idx, src, dst);
+    HF_CHECK_LAUNCH(ctx);
+}
+void axpy_cols(hf_ctx *ctx, int64_t L, int64_t n, double alpha, const double *X, int64_t ldx, double *Y,
+               int64_t ldy) {
+    if (L <= 0 || n <= 0) return;
+    k_axpy_cols<<<(unsigned)std::min<int64_t>(cdiv(L * n, 256), 8192), 256, 0, ctx->stream>>>(L, n, alpha, X, ldx, Y, ldy);
     HF_CHECK_LAUNCH(ctx);
 }
 void mask_vec(hf_ctx *ctx, int64_t L, const uint8_t *m, const double *src, double *dst) {

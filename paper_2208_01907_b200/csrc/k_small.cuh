@@ -18,6 +18,8 @@ void hard_solve(hf_ctx *ctx, int64_t n, int64_t r, const double *Lh, const doubl
 void scatter_rows(hf_ctx *ctx, int64_t n, const int64_t *idx, const double *src, double *dst);
 void gather_rows(hf_ctx *ctx, int64_t n, const int64_t *idx, const double *src, double *dst);
 void mask_vec(hf_ctx *ctx, int64_t L, const uint8_t *m, const double *src, double *dst);
+void axpy_cols(hf_ctx *ctx, int64_t L, int64_t n, double alpha, const double *X, int64_t ldx, double *Y,
+               int64_t ldy);
 void gather_block_rows(hf_ctx *ctx, int64_t n, int64_t ncol, const int64_t *perm, const double *X, int64_t ldx,
                        double *out, int64_t ldo);
 }  // namespace hf

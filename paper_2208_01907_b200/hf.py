@@ -29,7 +29,7 @@ EXPORTED = [
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
-    "hf_stage1_partition",
+    "hf_stage1_partition", "hf_krylov_solve",
 ]
 
 
@@ -92,6 +92,7 @@ def load() -> ctypes.CDLL:
         "hf_set_virtual_rank": [vp, ctypes.c_int, ctypes.c_int],
         "hf_set_stage1_partitions": [vp, ctypes.c_int],
         "hf_stage1_partition": [i64, ctypes.c_int, ctypes.c_int, pi64, vp],
+        "hf_krylov_solve": [vp, vp, i64, vp, ctypes.c_int, i64, vp, vp, dbl, i32, ctypes.POINTER(i32), pdbl, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -331,6 +332,27 @@ def hf_precond_apply(ctx: Context, lf: LowFactor, R: torch.Tensor, W: torch.Tens
         W = torch.empty(ncol, lf.L, dtype=torch.float64, device=R.device).T
     ctx.check(ctx.lib.hf_precond_apply(ctx.h, lf.h, ncol, _ptr(R), lf.L, _ptr(W), lf.L))
     return W
+
+
+KRYLOV = {"ir": 0, "gcr": 1, "bgcr": 2}
+
+
+def hf_krylov_solve(ctx: Context, K: torch.Tensor, lf: LowFactor, B: torch.Tensor, method: str = "bgcr",
+                    tol: float = 1e-14, max_iter: int = 100, accept_failure: bool = False):
+    """K11 X = B by IR (Alg. 3), GCR (Alg. 4, per column) or block GCR (Alg. 5).
+    B: column-major CUDA float64 (L, ncol).  Returns (X, iters, history np.ndarray, status)."""
+    _dev(K, torch.float64)
+    if not (isinstance(B, torch.Tensor) and B.is_cuda and B.dtype == torch.float64 and B.dim() == 2
+            and B.shape[0] == lf.L and (B.shape[1] <= 1 or B.stride() == (1, lf.L))):
+        raise TypeError("B must be a column-major CUDA float64 (L, ncol) tensor")
+    X = torch.empty(B.shape[1], lf.L, dtype=torch.float64, device=B.device).T
+    it = ctypes.c_int32()
+    hist = np.full(max_iter + 2, -1.0)
+    st = ctx.lib.hf_krylov_solve(ctx.h, _ptr(K), K.shape[0], lf.h, KRYLOV[method], B.shape[1], _ptr(B), _ptr(X),
+                                 float(tol), int(max_iter), ctypes.byref(it),
+                                 hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(hist))
+    ctx.check(st, (HF_ERR_NOT_CONVERGED,) if accept_failure else ())
+    return X, it.value, hist[hist >= 0], st
 
 
 def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-14, max_iter: int = 100,

@@ -1,0 +1,64 @@
+"""NEXT-2: the Fig. 2 comparison on the GPU --
+Algorithm 3 (iterative refinement), Algorithm 4 (GCR, one right-hand side at a
+time) and Algorithm 5 (block GCR) with the same FP32 preconditioner and FP64
+mat-vec kernels (hf_krylov_solve), against the oracle's Alg. 3/4/5:
+  * the qualitative ordering of Fig. 2: block GCR <= GCR <= IR iterations;
+  * iteration counts within one of the oracle's (FP64 rounding of the
+    recurrences differs), solutions normwise within 1e-8 of the oracle's."""
+import numpy as np
+import pytest
+import torch
+
+import hf_inputs as hi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name,seed,ncol", [("P1024", 0, 16), ("N32", 0, 4), ("S24", 0, 8)])
+def test_fig2_ordering_and_oracle(ctx, name, seed, ncol):
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, _ = oracle.scale(Kb.numpy())
+    F = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    K11, K12, _, _ = oracle.extract_blocks(Ko, F)
+    Kd = Kb.cuda()
+    hf.hf_scale(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
+    L = Ko.shape[0]
+    rng = np.random.default_rng(seed + 3)
+    Bp = rng.standard_normal((F.N, ncol))                # pivot order (the oracle's)
+    B = np.zeros((L, ncol))
+    B[F.lam1] = Bp                                       # original row order (the library's)
+    Bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda().T
+    its, xs, conv = {}, {}, {}
+    for m in ("ir", "gcr", "bgcr"):
+        X, it, hist, st = hf.hf_krylov_solve(ctx, Kd, lf, Bd, m, max_iter=300, accept_failure=(m == "ir"))
+        conv[m] = st == hf.HF_OK
+        its[m] = it
+        xs[m] = X.cpu().numpy()[F.lam1]
+        assert len(hist) == it + 1 and (hist[-1] <= 1e-14) == conv[m]
+        assert np.all(X.cpu().numpy()[F.lam2] == 0.0)
+    assert conv["gcr"] and conv["bgcr"]
+    assert its["bgcr"] <= its["gcr"] <= its["ir"], its        # Fig. 2: IR slowest (or not converging)
+    Xb, ib = oracle.block_gcr(K11, F, Bp)
+    ig = max(oracle.gcr(K11, F, Bp[:, j])[1].iters for j in range(ncol))
+    iro = [oracle.iterative_refinement(K11, F, Bp[:, j], max_iter=300)[1] for j in range(ncol)]
+    assert abs(its["bgcr"] - ib.iters) <= 1 and abs(its["gcr"] - ig) <= 1, (its, ib.iters, ig)
+    assert conv["ir"] == all(r.converged for r in iro)
+    if conv["ir"]:
+        assert abs(its["ir"] - max(r.iters for r in iro)) <= 1
+    for m in ("ir", "gcr", "bgcr"):
+        if conv[m]:
+            assert np.linalg.norm(xs[m] - Xb) <= 1e-8 * np.linalg.norm(Xb), m
