@@ -116,6 +116,9 @@ typedef struct {
     int64_t n_extra;  /* P:82 enlargement: move the last n_extra pivots to Lambda_2   */
     int64_t n_min;    /* postponement floor [R5]: |Lambda_2| >= n_min                 */
     int32_t nb;       /* panel width (0 = automatic)                                  */
+    int32_t prec;     /* 0 or 32: FP32 factor (Alg. 1's lower precision for the       */
+                      /* (float, double) pair); 64: FP64 factor, the lower precision  */
+                      /* of the paper's (double, double-double) pair (NEXT-1)  */
 } hf_lowprec_opts;
 
 /* FP32 LDL^T of the scaled K (lower triangle read) with symmetric max-|diag|
@@ -134,6 +137,9 @@ hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
  * pointer may be NULL to skip it. */
 hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host,
                               float *D_host, float *Lfac, int64_t ldl);
+/* prec 64 factors: perm_host[L], D_host[N] (double), Lfac: DEVICE N x N double. */
+hf_status hf_lowfactor_export64(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host,
+                                double *D_host, double *Lfac, int64_t ldl);
 hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
 
 /* --------------------------- a5: the preconditioner Q^{-1}, P:231-242 [R12] */

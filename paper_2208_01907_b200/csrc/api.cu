@@ -163,15 +163,20 @@ hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
                             int64_t *n2_host, int64_t *n2_tau_only_host) {
     if (!ctx || !out) return HF_ERR_INVALID_ARG;
     *out = nullptr;
-    hf_lowprec_opts o{1e-2, 0, 0, 0};
+    hf_lowprec_opts o{1e-2, 0, 0, 0, 32};
     if (opts) o = *opts;
+    if (o.prec == 0) o.prec = 32;
     std::unique_ptr<hf_lowfactor> lf(new hf_lowfactor());
     hf_status s = guarded(ctx, [&] {
         HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || K), "hf_factor_lowprec: bad arguments");
         HF_REQUIRE(o.tau > 0.0 && o.tau < 1.0, "hf_factor_lowprec: tau must lie in (0,1)");
         HF_REQUIRE(o.n_extra >= 0 && o.n_min >= 0, "hf_factor_lowprec: n_extra/n_min < 0");
         HF_REQUIRE(o.nb >= 0 && o.nb <= 256 && o.nb % 8 == 0, "hf_factor_lowprec: nb in {0, 8..256, multiple of 8}");
-        if (ctx->nranks > 1) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->nranks);
+        HF_REQUIRE(o.prec == 32 || o.prec == 64, "hf_factor_lowprec: prec must be 32 or 64");
+        if (o.prec == 64) {
+            HF_REQUIRE(ctx->nranks == 1 && ctx->s1parts == 0, "hf_factor_lowprec: prec 64 is single-GPU");
+            hf::lowprec_factor64(ctx, L, K, ld, o, lf.get());
+        } else if (ctx->nranks > 1) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->nranks);
         else if (ctx->s1parts > 0) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->s1parts);
         else hf::lowprec_factor(ctx, L, K, ld, o, lf.get());
     });
@@ -193,6 +198,22 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
             HF_REQUIRE(ldl >= lf->N, "hf_lowfactor_export: ldl < N");
             HF_CUDA(cudaMemcpy2DAsync(Lfac, ldl * sizeof(float), lf->Lfac.p, lf->N * sizeof(float),
                                       lf->N * sizeof(float), lf->N, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    });
+}
+
+hf_status hf_lowfactor_export64(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host, double *D_host,
+                                double *Lfac, int64_t ldl) {
+    if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        if (lf->prec != 64) throw hf::Error{HF_ERR_STATE, "hf_lowfactor_export64: not a prec-64 factor"};
+        if (perm_host && lf->L) std::memcpy(perm_host, lf->h_perm.data(), lf->L * sizeof(int64_t));
+        if (D_host && lf->N) std::memcpy(D_host, lf->h_D64.data(), lf->N * sizeof(double));
+        if (Lfac && lf->N) {
+            HF_REQUIRE(ldl >= lf->N, "hf_lowfactor_export64: ldl < N");
+            HF_CUDA(cudaMemcpy2DAsync(Lfac, ldl * sizeof(double), lf->Lfac64.p, lf->N * sizeof(double),
+                                      lf->N * sizeof(double), lf->N, cudaMemcpyDeviceToDevice, ctx->stream));
+            HF_CUDA(cudaStreamSynchronize(ctx->stream));
         }
     });
 }
@@ -232,6 +253,8 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
     hf_status s = guarded(ctx, [&] {
         HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr: bad arguments");
+        if (lf->prec != 32) throw hf::Error{HF_ERR_STATE, "hf_schur_gcr: FP64 factors (prec 64) need the "
+                                                          "double-double stage 2, not built (NEXT-1)"};
         HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr: tol > 0, max_iter >= 1");
         hy->K = K;
         hy->ld = ld;

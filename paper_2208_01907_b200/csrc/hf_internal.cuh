@@ -193,6 +193,9 @@ struct Precond {
 // ----------------------------------------------------------------- handles
 struct hf_lowfactor {
     int64_t L = 0, N = 0, Ntau = 0, n2 = 0;
+    int prec = 32;                     // 32: FP32 factor (the north_star); 64: FP64 (NEXT-1)
+    std::vector<double> h_D64;         // prec 64: D (host copy, exact)
+    hf::DBuf<double> D64, Lfac64;      // prec 64: D and the N x N unit lower factor
     std::vector<int64_t> h_perm;       // Pi (host copy)
     std::vector<float> h_D;            // D (host copy)
     hf::DBuf<int64_t> perm;            // Pi (device)
@@ -230,6 +233,8 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                     hf_lowfactor *lf);
 void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                           hf_lowfactor *lf, int nparts);
+void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                      hf_lowfactor *lf);
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,

@@ -29,7 +29,7 @@ EXPORTED = [
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
-    "hf_stage1_partition", "hf_krylov_solve",
+    "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64",
 ]
 
 
@@ -41,7 +41,7 @@ class HFError(RuntimeError):
 
 class lowprec_opts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_double), ("n_extra", ctypes.c_int64), ("n_min", ctypes.c_int64),
-                ("nb", ctypes.c_int32)]
+                ("nb", ctypes.c_int32), ("prec", ctypes.c_int32)]
 
 
 class gcr_opts(ctypes.Structure):
@@ -79,6 +79,7 @@ def load() -> ctypes.CDLL:
         "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
         "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
         "hf_lowfactor_destroy": [vp],
+        "hf_lowfactor_export64": [vp, vp, vp, vp, vp, i64],
         "hf_schur_gcr": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(gcr_info)],
         "hf_hybrid_export": [vp, vp, vp, i64, vp, i64],
@@ -248,6 +249,17 @@ class LowFactor:
                                                         _ptr(Lf), self.N))
         return perm, D[: self.N], (Lf.T if Lf is not None else None)
 
+    def export64(self, with_L: bool = True):
+        """prec-64 factors: (perm np.int64[L], D np.float64[N], Lfac device float64 N x N)."""
+        perm = np.empty(self.L, dtype=np.int64)
+        D = np.empty(max(self.N, 1), dtype=np.float64)
+        Lf = None
+        if with_L and self.N > 0:
+            Lf = torch.empty(self.N, self.N, dtype=torch.float64, device=f"cuda:{self.ctx.device}")
+        self.ctx.check(self.ctx.lib.hf_lowfactor_export64(self.ctx.h, self.h, _ptr(perm), _ptr(D),
+                                                          _ptr(Lf), self.N))
+        return perm, D[: self.N], (Lf.T if Lf is not None else None)
+
     def close(self):
         if self.h is not None and self.h.value:
             self.ctx.lib.hf_lowfactor_destroy(self.h)
@@ -261,10 +273,10 @@ class LowFactor:
 
 
 def hf_factor_lowprec(ctx: Context, K: torch.Tensor, tau: float = 1e-2, n_extra: int = 0,
-                      n_min: int = 0, nb: int = 0) -> LowFactor:
+                      n_min: int = 0, nb: int = 0, prec: int = 32) -> LowFactor:
     _dev(K, torch.float64)
     L = K.shape[0]
-    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb))
+    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb), int(prec))
     h = ctypes.c_void_p()
     N, n2, n2t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     ctx.check(ctx.lib.hf_factor_lowprec(ctx.h, L, _ptr(K), L, ctypes.byref(o), ctypes.byref(h),

@@ -1,0 +1,4 @@
+python -c "from paper_2208_01907_b200 import build; build.build()" || exit 1
+HF_TRAILING=narrow timeout 600 python -m pytest tests/test_gpu_stage1.py -x -q > gpurun_out/t50.log 2>&1; echo t=$?
+HF_TRAILING=narrow timeout 600 python tools/probe_stage1.py C2 > gpurun_out/p50n.log 2>&1; echo p=$?
+timeout 600 python tools/probe_stage1.py C2 > gpurun_out/p50.log 2>&1; echo p=$?
