@@ -235,7 +235,7 @@ hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, co
                    "hf_precond_apply: bad arguments");
         if (ncol == 0 || lf->L == 0) return;
         hf::Precond pc;
-        hf::precond_setup(ctx, pc, lf->N, lf->L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        hf::precond_setup(ctx, pc, lf);
         hf::precond_apply(ctx, pc, ncol, R, ldr, W, ldw);
         HF_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -253,8 +253,7 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
     hf_status s = guarded(ctx, [&] {
         HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr: bad arguments");
-        if (lf->prec != 32) throw hf::Error{HF_ERR_STATE, "hf_schur_gcr: FP64 factors (prec 64) need the "
-                                                          "double-double stage 2, not built (NEXT-1)"};
+
         HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr: tol > 0, max_iter >= 1");
         hy->K = K;
         hy->ld = ld;

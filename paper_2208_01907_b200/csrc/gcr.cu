@@ -218,7 +218,7 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
     hy->lam2.alloc(std::max<int64_t>(n2, 1), st);
     if (n2 > 0)
         HF_CUDA(cudaMemcpyAsync(hy->lam2.p, lf->perm.p + N, n2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    precond_setup(ctx, hy->pc, N, L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+    precond_setup(ctx, hy->pc, lf);
     hy->X.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->B.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->S22.alloc((size_t)std::max<int64_t>(n2 * n2, 1), st);
@@ -295,10 +295,18 @@ void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker) {
         return;
     }
     double dref = 1.0;
-    const auto &D = hy->lf->h_D;
-    if (!D.empty()) {
-        dref = INFINITY;
-        for (float d : D) dref = std::min(dref, std::fabs((double)d));
+    if (hy->lf->prec == 64) {
+        const auto &D = hy->lf->h_D64;
+        if (!D.empty()) {
+            dref = INFINITY;
+            for (double d : D) dref = std::min(dref, std::fabs(d));
+        }
+    } else {
+        const auto &D = hy->lf->h_D;
+        if (!D.empty()) {
+            dref = INFINITY;
+            for (float d : D) dref = std::min(dref, std::fabs((double)d));
+        }
     }
     hy->Lh.alloc((size_t)n2 * n2, st);
     hy->Dh.alloc((size_t)n2 * n2, st);
@@ -394,7 +402,7 @@ extern "C" hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, c
         mask.alloc(L, st);
         hf::mask_from_pos(ctx, L, lf->pos1.p, mask.p);
         hf::Precond pc;
-        hf::precond_setup(ctx, pc, lf->N, L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        hf::precond_setup(ctx, pc, lf);
         hf::DBuf<double> Bm;
         Bm.alloc((size_t)L * ncol, st);
         for (int64_t c = 0; c < ncol; ++c) hf::mask_vec(ctx, L, mask.p, B + c * L, Bm.p + c * L);

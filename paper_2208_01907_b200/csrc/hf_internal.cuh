@@ -162,21 +162,22 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace hf
 
-// FP32 preconditioner state (k_trsm.cu)
+// preconditioner state (k_trsm.cu): T = float (FP32 factor) or double (FP64, NEXT-1)
 namespace hf {
-struct Precond {
+template <typename T>
+struct PrecondT {
     int64_t N = 0, L = 0;
-    const float *Lfac = nullptr;   // N x N unit lower, pivot order
-    const float *D = nullptr;      // [N]
+    const T *Lfac = nullptr;       // N x N unit lower, pivot order
+    const T *D = nullptr;          // [N]
     const int64_t *perm = nullptr; // [L] pivot order -> original index
     const int32_t *pos1 = nullptr; // [L] original index -> pivot rank, -1 on Lambda_2
     int64_t Np = 0;                // N rounded up to the 64-row block
-    DBuf<float> Lp, Up;            // Np x Np: L padded with the identity, and L^T, each block row
+    DBuf<T> Lp, Up;            // Np x Np: L padded with the identity, and L^T, each block row
                                    // scaled in place by its diagonal-block inverse (G = Dinv Op)
-    DBuf<float> LinvF, LinvB;      // inverses of the 64x64 diagonal blocks (tile layouts)
-    DBuf<float> P;                 // Np x ncolp: P_j of the chain recurrence (row-major)
-    DBuf<float> Y;                 // Np x ncolp workspace (FP32, row-major)
-    DBuf<float> Xb;                // Np x ncolp workspace (FP32, row-major)
+    DBuf<T> LinvF, LinvB;      // inverses of the 64x64 diagonal blocks (tile layouts)
+    DBuf<T> P;                 // Np x ncolp: P_j of the chain recurrence (row-major)
+    DBuf<T> Y;                 // Np x ncolp workspace (FP32, row-major)
+    DBuf<T> Xb;                // Np x ncolp workspace (FP32, row-major)
     DBuf<int> flags;
     DBuf<int> counter;
     int epoch = 0;
@@ -184,9 +185,14 @@ struct Precond {
     int tab_nblk = -1, tab_nch = -1, nitems = 0, nslots = 0;
     const int4 *items = nullptr;   // owned by the context's table cache
     const int *pbase = nullptr;
-    DBuf<float> part;
+    DBuf<T> part;
     DBuf<int> pflags;
     DBuf<unsigned long long> dbg;
+};
+struct Precond {
+    int prec = 32;
+    PrecondT<float> f;
+    PrecondT<double> d;
 };
 }  // namespace hf
 

@@ -24,8 +24,7 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
            const uint8_t *rowmask, DBuf<double> *work, int splits = 0);
 
 // FP32 preconditioner Q^{-1} (k_trsm.cu); struct Precond is in hf_internal.cuh
-void precond_setup(hf_ctx *ctx, Precond &p, int64_t N, int64_t L, const float *Lfac, const float *D,
-                   const int64_t *perm, const int32_t *pos1);
+void precond_setup(hf_ctx *ctx, Precond &p, const hf_lowfactor *lf);
 // W (L x ncol, original order, ldw) = Q^{-1} R (R: L x ncol, original order, ldr);
 // rows of Lambda_2 in W are set to 0.
 void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64_t ldr, double *W,

@@ -1,0 +1,4 @@
+python -c "from paper_2208_01907_b200 import build; build.build()" || exit 1
+timeout 900 python -m pytest tests/test_gpu_fp64.py tests/test_gpu_precond.py -x -q > gpurun_out/t52.log 2>&1; echo t=$?
+timeout 600 python -m pytest tests/test_gpu_stage23.py -x -q >> gpurun_out/t52.log 2>&1; echo t=$?
+timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench52.log 2>&1; echo b=$?
