@@ -129,3 +129,26 @@ def test_block_gcr_identity_and_errors(ctx):
     lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
     hy, info, _ = hf.hf_schur_gcr(ctx, Kd, lf, max_iter=1, accept_failure=True)
     assert info.status == hf.HF_ERR_NOT_CONVERGED and info.iters == 1
+
+
+def test_determinism_repeated_runs(ctx):
+    """repeated runs on the same input give the same bits -- stage 1 by [R8],
+    and stages 2-3 because every reduction of the CUDA path has a fixed order (the
+    preconditioner's partial sums are added in a fixed slot order, split-K GEMMs
+    reduce their partial tiles in order)."""
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS["P2048"]
+    Kb = hi.make_kbar("P2048", 1)
+    outs = []
+    for _ in range(2):
+        Kd = Kb.cuda()
+        hf.hf_scale(ctx, Kd)
+        lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
+        hy, info, S22 = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
+        kd = hf.hf_factor_hard(ctx, hy)
+        b = torch.arange(spec.L, dtype=torch.float64, device="cuda") % 7
+        x, _ = hf.hf_solve(ctx, hy, b)
+        outs.append((lf.export()[0], S22.copy(), kd, info.iters, x.cpu().numpy()))
+    a, b2 = outs
+    assert np.array_equal(a[0], b2[0]) and np.array_equal(a[1], b2[1]) and a[2:4] == b2[2:4]
+    assert np.array_equal(a[4], b2[4])
