@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
@@ -326,6 +327,188 @@ __global__ void __launch_bounds__(256) k_hard_factor_mc(int64_t n, const double 
     if (c == 0 && tid == 0) *rank_out = k;
 }
 
+// Fused variant (default): ONE grid barrier per pivot.  The update of pivot
+// step k and the search for step k+1 are one pass over each CTA's columns
+// (the search reads the freshly updated values and skips the step-k pivots);
+// the per-CTA bests are double buffered by step parity, so a CTA that has
+// decided and moved on never overwrites bests another CTA is still reading.
+__device__ __forceinline__ void warp_best(Best &b) {
+    for (int o = 16; o > 0; o >>= 1) {
+        Best x{__shfl_xor_sync(0xffffffffu, b.v, o), __shfl_xor_sync(0xffffffffu, b.k1, o),
+               __shfl_xor_sync(0xffffffffu, b.k2, o), __shfl_xor_sync(0xffffffffu, b.i, o),
+               __shfl_xor_sync(0xffffffffu, b.j, o)};
+        if (better(x, b)) b = x;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *__restrict__ S, double thr,
+                                                       double *__restrict__ A, double *__restrict__ Lcol,
+                                                       int32_t *__restrict__ act, int32_t *__restrict__ posof,
+                                                       Best *__restrict__ gbest, double *__restrict__ Dh,
+                                                       int32_t *__restrict__ blocks, int32_t *__restrict__ pivots,
+                                                       int64_t *rank_out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ Best sh[256];
+    __shared__ Best sdg, soff;
+    const int G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+    const int c = blockIdx.x;
+    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+    // A = (S + S^T)/2 and the first search, fused
+    Best bo{-1.0, 0, 0, -1, -1}, bd{-1.0, 0, 0, -1, -1};
+    for (int64_t j = c; j < n; j += G)
+        for (int64_t i = tid; i < n; i += nt) {
+            const double v = 0.5 * (S[i + j * n] + S[j + i * n]);
+            A[i + j * n] = v;
+            Dh[i + j * n] = 0.0;
+            if (i == j) {
+                Best cd{fabs(v), i, 0, i, i};
+                if (better(cd, bd)) bd = cd;
+            } else {
+                Best cd{fabs(v), min(i, j), max(i, j), i, j};
+                if (better(cd, bo)) bo = cd;
+            }
+        }
+    if (c == 0)
+        for (int64_t i = tid; i < n; i += nt) {
+            act[i] = 1;
+            posof[i] = -1;
+            blocks[i] = 0;
+        }
+    int par = 0;
+    bd = block_best(bd, sh);
+    bo = block_best(bo, sh);
+    if (tid == 0) {
+        gbest[(size_t)par * 2 * G + 2 * c] = bd;
+        gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
+    }
+    grid.sync();
+    int64_t k = 0, nblk = 0;
+    while (k < n) {
+        // ---- the same decision in every CTA from the G partial bests of this step
+        if (tid < 32) {
+            Best d0{-1.0, 0, 0, -1, -1}, o0{-1.0, 0, 0, -1, -1};
+            const Best *gb = gbest + (size_t)par * 2 * G;
+            for (int g = tid; g < G; g += 32) {
+                if (better(gb[2 * g], d0)) d0 = gb[2 * g];
+                if (better(gb[2 * g + 1], o0)) o0 = gb[2 * g + 1];
+            }
+            warp_best(d0);
+            warp_best(o0);
+            if (tid == 0) {
+                sdg = d0;
+                soff = o0;
+            }
+        }
+        __syncthreads();
+        const Best d0 = sdg, o0 = soff;
+        const double mu1 = d0.v, mu0 = fmax(d0.v, o0.v);
+        if (mu0 <= thr) break;   // uniform
+        par ^= 1;
+        bo = Best{-1.0, 0, 0, -1, -1};
+        bd = Best{-1.0, 0, 0, -1, -1};
+        if (mu1 >= alpha * mu0) {
+            // ---- 1x1 pivot at p: update + next search in one pass
+            const int64_t p = d0.i;
+            const double d = A[p + p * n];
+            const double *ap = A + p * n;
+            for (int64_t j = c; j < n; j += G) {
+                if (!act[j] || j == p) continue;
+                double *aj = A + j * n;
+                const double apj = ap[j];
+                for (int64_t i = tid; i < n; i += nt) {
+                    if (!act[i] || i == p) continue;
+                    const double v = aj[i] - (ap[i] * apj) / d;
+                    aj[i] = v;
+                    if (i == j) {
+                        Best cd{fabs(v), i, 0, i, i};
+                        if (better(cd, bd)) bd = cd;
+                    } else {
+                        Best cd{fabs(v), min(i, j), max(i, j), i, j};
+                        if (better(cd, bo)) bo = cd;
+                    }
+                }
+            }
+            if (c == 0) {
+                for (int64_t i = tid; i < n; i += nt) Lcol[i + k * n] = (act[i] && i != p) ? ap[i] / d : 0.0;
+                if (tid == 0) {
+                    Dh[k + k * n] = d;
+                    blocks[nblk] = 1;
+                    pivots[k] = (int32_t)p;
+                    posof[p] = (int32_t)k;
+                }
+            }
+            bd = block_best(bd, sh);
+            bo = block_best(bo, sh);
+            if (tid == 0) {
+                gbest[(size_t)par * 2 * G + 2 * c] = bd;
+                gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
+            }
+            grid.sync();   // everyone has used act[] and column p of this step
+            if (c == 0 && tid == 0) act[p] = 0;
+            ++nblk;
+            k += 1;
+        } else {
+            // ---- 2x2 pivot on (p, q), smaller label first
+            const int64_t p = min(o0.i, o0.j), q = max(o0.i, o0.j);
+            const double a_ = A[p + p * n], b_ = A[q + p * n], c_ = A[q + q * n];
+            const double det = a_ * c_ - b_ * b_;
+            const double E0 = c_ / det, E1 = -b_ / det, E2 = -b_ / det, E3 = a_ / det;
+            const double *ap = A + p * n, *aq = A + q * n;
+            for (int64_t j = c; j < n; j += G) {
+                if (!act[j] || j == p || j == q) continue;
+                double *aj = A + j * n;
+                const double cc0 = ap[j], cc1 = aq[j];
+                const double lc0 = cc0 * E0 + cc1 * E1, lc1 = cc0 * E2 + cc1 * E3;
+                for (int64_t i = tid; i < n; i += nt) {
+                    if (!act[i] || i == p || i == q) continue;
+                    const double cr0 = ap[i], cr1 = aq[i];
+                    const double lr0 = cr0 * E0 + cr1 * E1, lr1 = cr0 * E2 + cr1 * E3;
+                    const double t1 = lr0 * cc0 + lr1 * cc1, t2 = lc0 * cr0 + lc1 * cr1;
+                    const double v = aj[i] - 0.5 * (t1 + t2);
+                    aj[i] = v;
+                    if (i == j) {
+                        Best cd{fabs(v), i, 0, i, i};
+                        if (better(cd, bd)) bd = cd;
+                    } else {
+                        Best cd{fabs(v), min(i, j), max(i, j), i, j};
+                        if (better(cd, bo)) bo = cd;
+                    }
+                }
+            }
+            if (c == 0) {
+                for (int64_t i = tid; i < n; i += nt) {
+                    const bool ok = act[i] && i != p && i != q;
+                    const double cr0 = ap[i], cr1 = aq[i];
+                    Lcol[i + k * n] = ok ? cr0 * E0 + cr1 * E1 : 0.0;
+                    Lcol[i + (k + 1) * n] = ok ? cr0 * E2 + cr1 * E3 : 0.0;
+                }
+                if (tid == 0) {
+                    Dh[k + k * n] = a_;
+                    Dh[k + 1 + k * n] = b_;
+                    Dh[k + (k + 1) * n] = b_;
+                    Dh[k + 1 + (k + 1) * n] = c_;
+                    blocks[nblk] = 2;
+                    pivots[k] = (int32_t)p;
+                    pivots[k + 1] = (int32_t)q;
+                    posof[p] = (int32_t)k;
+                    posof[q] = (int32_t)(k + 1);
+                }
+            }
+            bd = block_best(bd, sh);
+            bo = block_best(bo, sh);
+            if (tid == 0) {
+                gbest[(size_t)par * 2 * G + 2 * c] = bd;
+                gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
+            }
+            grid.sync();
+            if (c == 0 && tid == 0) act[p] = act[q] = 0;
+            ++nblk;
+            k += 2;
+        }
+    }
+    if (c == 0 && tid == 0) *rank_out = k;
+}
+
 // lab[pos] = Lambda_2 position at pivoted position pos (pivots first, then the
 // kernel indices ascending); Lh (n x n, pivoted positions) unit lower with
 // Lh[pos(i), kk] = Lcol[i, kk] for kk < pos(i), kk < r.
@@ -497,9 +680,11 @@ void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A,
     }
     int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(n, 8)), (int64_t)ctx->num_sms * std::min(per_sm, 1));
     DBuf<Best> gb;
-    gb.alloc((size_t)2 * G, st);
+    gb.alloc((size_t)4 * G, st);   // [2 step parities][2 G]
     void *args[] = {&n, &S, &thr, &A, &Lcol.p, &act, &posof, &gb.p, &Dh, &blocks, &piv, &rank_dev};
-    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_hard_factor_mc, dim3(G), dim3(256), args, 0, st));
+    static const bool unfused = getenv("HF_HARD_UNFUSED") != nullptr;   // the 3-barrier reference variant
+    HF_CUDA(cudaLaunchCooperativeKernel(unfused ? (void *)k_hard_factor_mc : (void *)k_hard_factor_f, dim3(G),
+                                        dim3(256), args, 0, st));
     HF_CHECK_LAUNCH(ctx);
     k_hard_assemble<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 4096), 256, 0, st>>>(n, rank_dev, Lcol.p, posof,
                                                                                         piv, lab, Lh);
