@@ -167,7 +167,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //     s = c/r, L = c/d, diagonal.
 template <bool PARTS>
 __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
     __shared__ unsigned long long bkey;
     __shared__ uint32_t pcol;   // (partition << 20 | local column) of the pivot (parts mode)
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const int nbq = a.nbprev;                 // previous panel's pivots (lookahead) or 0
     float *sneg = smem;                       // [nbp][R]  -sigma_u s_i^u for own rows
     float *snp = sneg + (size_t)nb * a.R;     // [nbq][R]  the same for the previous panel
-    float *sp = snp + (size_t)nbq * a.R;      // [nbp]     s_P^u of the current pivot row
+    float *sp = smem + (((size_t)(nb + nbq) * a.R + 3) & ~(size_t)3);   // [nbp] s_P^u of the current pivot row (16-B aligned)
     float *spp = sp + nb;                     // [nbq]     s_P^u of the previous panel
     float *sgm = spp + nbq;                   // [nbp]     sigma_u
 
@@ -340,6 +340,14 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         const float sg = d > 0.f ? 1.f : -1.f;
         // ---- F: [R6] pivot row from the winner's mailbox, stale column for own rows
         const int64_t Po = a.mapprev ? (int64_t)a.mapprev[P] : P;   // pivot in V's position space
+        // the column load is issued first so its latency overlaps the mailbox poll below
+        float v = 0.f;
+        if (PARTS) {
+            const uint32_t w = pcol;   // read after the barrier that published bkey
+            if (!piv && i != P) v = a.parts[w >> 20][i + (int64_t)(w & 0xFFFFF) * a.ldp];
+        } else if (!piv && i != P) {
+            v = (io >= Po) ? a.V[io + Po * a.ldv] : a.V[Po + io * a.ldv];
+        }
         {
             const int owner = (int)(P / a.R);
             const unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + owner) * (nb + 1);
@@ -352,13 +360,6 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             }
             for (int u = tid; u < nbq; u += nthr) spp[u] = -a.sigprev[u] * a.SNprev[Po * a.nbmax + u];
             if (tid == 0) sgm[t] = sg;
-        }
-        float v = 0.f;
-        if (PARTS) {
-            const uint32_t w = pcol;   // read after the barrier that published bkey
-            if (!piv && i != P) v = a.parts[w >> 20][i + (int64_t)(w & 0xFFFFF) * a.ldp];
-        } else if (!piv && i != P) {
-            v = (io >= Po) ? a.V[io + Po * a.ldv] : a.V[Po + io * a.ldv];
         }
         __syncthreads();
         PH(2)
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             }
             const float *sn = sneg + tid;
             int u = 0;
-            for (; u + 8 <= t; u += 8) {                 // [R8] one fmaf per earlier pivot, in order
+            for (; u + 8 <= t; u += 8) {             // [R8] one fmaf per earlier pivot, in order
                 float x[8], y[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -491,42 +492,54 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
     const int64_t bj = t - bi * (bi + 1) / 2;
     const int64_t row0 = bi * TB, col0 = bj * TB;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
 
-    if (tid < TB) {
-        rmap[tid] = (row0 + tid < a.mp) ? a.map[row0 + tid] : -1;
-        cmap[tid] = (col0 + tid < a.mp) ? a.map[col0 + tid] : -1;
-    }
+    if (tid < TB) rmap[tid] = (tid < mpr) ? a.map[row0 + tid] : -1;
+    else cmap[tid - TB] = (tid - TB < mpc) ? a.map[col0 + tid - TB] : -1;
     __syncthreads();
 
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
-    // accumulators seeded from the current values (compaction fused in the gather)
+    // accumulators seeded from the current values (compaction fused in the gather):
+    // one 64-bit column pointer per column, 32-bit row offsets
     float2 acc[8][4];
+    {
+        int32_t rm[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int32_t cm0 = cmap[CC(2 * j)], cm1 = cmap[CC(2 * j + 1)];
+        for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int32_t rm = rmap[RR(q)];
-            acc[q][j].x = (cm0 >= 0 && rm >= cm0) ? a.Vold[(int64_t)rm + (int64_t)cm0 * a.ldv] : 0.f;
-            acc[q][j].y = (cm1 >= 0 && rm >= cm1) ? a.Vold[(int64_t)rm + (int64_t)cm1 * a.ldv] : 0.f;
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int32_t cm = cmap[CC(2 * j + h)];
+                const float *colp = a.Vold + (int64_t)(cm >= 0 ? cm : 0) * a.ldv;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float v = (cm >= 0 && rm[q] >= cm) ? __ldg(colp + rm[q]) : 0.f;
+                    if (h) acc[q][j].y = v;
+                    else acc[q][j].x = v;
+                }
+            }
         }
     }
 
     // global -> register staging: per chunk 8 A (-sigma s) and 8 B (s) values per thread
     const int lr = tid & 127, lk = tid >> 7;   // element (row lr, k = lk + 2*q)
     const int32_t arow = rmap[lr], bcol = cmap[lr];
-    const float *Ap = a.Sn + (arow >= 0 ? arow : 0);
-    const float *Bp = a.S + (bcol >= 0 ? bcol : 0);
+    const float *Ap = a.Sn + (arow >= 0 ? arow : 0) + (int64_t)lk * a.lds;
+    const float *Bp = a.S + (bcol >= 0 ? bcol : 0) + (int64_t)lk * a.lds;
+    const int64_t lds2 = 2 * a.lds, ldsk = (int64_t)TK * a.lds;
+    const bool aok = arow >= 0, bok = bcol >= 0;
     float ra[TK / 2], rb[TK / 2];
     auto gload = [&](int t0) {
 #pragma unroll
         for (int q = 0; q < TK / 2; ++q) {
-            const int tt = t0 + lk + 2 * q;
-            const bool ok = tt < a.nbp;
-            ra[q] = (ok && arow >= 0) ? Ap[(int64_t)tt * a.lds] : 0.f;
-            rb[q] = (ok && bcol >= 0) ? Bp[(int64_t)tt * a.lds] : 0.f;
+            const bool ok = t0 + lk + 2 * q < a.nbp;
+            ra[q] = (ok && aok) ? __ldg(Ap + q * lds2) : 0.f;
+            rb[q] = (ok && bok) ? __ldg(Bp + q * lds2) : 0.f;
         }
+        Ap += ldsk;
+        Bp += ldsk;
     };
     auto sstore = [&](int buf) {
 #pragma unroll
@@ -581,17 +594,28 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
         }
     }
 
-    // store the lower triangle of the new trailing matrix
+    // store the lower triangle of the new trailing matrix: 16-byte stores on full
+    // off-diagonal tiles (rows tx*4..+3 are contiguous), masked scalar stores elsewhere
+    const bool full = (row0 > col0) && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t c = col0 + CC(2 * j + h);
-            if (c >= a.mp) continue;
+            const int cl = CC(2 * j + h);
+            float *colp = a.Vnew + (col0 + cl) * a.ldv + row0;
+            if (full) {
+                *reinterpret_cast<float4 *>(colp + tx * 4) =
+                    h ? make_float4(acc[0][j].y, acc[1][j].y, acc[2][j].y, acc[3][j].y)
+                      : make_float4(acc[0][j].x, acc[1][j].x, acc[2][j].x, acc[3][j].x);
+                *reinterpret_cast<float4 *>(colp + 64 + tx * 4) =
+                    h ? make_float4(acc[4][j].y, acc[5][j].y, acc[6][j].y, acc[7][j].y)
+                      : make_float4(acc[4][j].x, acc[5][j].x, acc[6][j].x, acc[7][j].x);
+            } else if (cl < mpc) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int64_t r = row0 + RR(q);
-                if (r < a.mp && r >= c) a.Vnew[r + c * a.ldv] = h ? acc[q][j].y : acc[q][j].x;
+                for (int q = 0; q < 8; ++q) {
+                    const int rl = RR(q);
+                    if (rl < mpr && row0 + rl >= col0 + cl) colp[rl] = h ? acc[q][j].y : acc[q][j].x;
+                }
             }
         }
     }
@@ -976,7 +1000,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         const int64_t R = cdiv(m, G);
         const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
         const int pb = look ? (pidx & 1) : 0, qb = pb ^ 1;
-        const size_t shm = ((size_t)(nbp + (look ? nbprev : 0)) * R + 3 * nbp + (look ? nbprev : 0)) * sizeof(float);
+        const size_t shm = ((size_t)(nbp + (look ? nbprev : 0)) * R + 3 * nbp + (look ? nbprev : 0) + 4) * sizeof(float);
         if (xmode == 0) HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
@@ -1023,7 +1047,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             if (!look) {
                 ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
                 ClassTimer tm(ctx, "trailing");
-                k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
+k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
                 vb ^= 1;
             } else {
@@ -1203,7 +1227,7 @@ void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, c
         const int64_t G = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(m, 32)));
         const int64_t R = cdiv(m, G);
         const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
-        const size_t shm = ((size_t)nbp * R + 3 * nbp) * sizeof(float);
+        const size_t shm = ((size_t)nbp * R + 3 * nbp + 4) * sizeof(float);
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
         ca.V = nullptr; ca.ldv = L; ca.orig = orig[cur].p;
