@@ -101,8 +101,8 @@ namespace hf {
 // dataflow item table of the preconditioner solves (k_trsm.cu), per shape
 struct TrsmTable {
     int nitems = 0, nslots = 0;
-    DBuf<int4> items;
-    DBuf<int> pbase;
+    DBuf<int4> items;     // PARTIAL items
+    DBuf<int4> pinfo;     // per block: (first slot, #slots, tail q_lo, tail q_hi)
 };
 }  // namespace hf
 
@@ -184,7 +184,7 @@ struct PrecondT {
     // dataflow workspaces (k_trsm.cu), re-sized when the block/chunk counts change
     int tab_nblk = -1, tab_nch = -1, nitems = 0, nslots = 0;
     const int4 *items = nullptr;   // owned by the context's table cache
-    const int *pbase = nullptr;
+    const int4 *pinfo = nullptr;
     DBuf<T> part;
     DBuf<int> pflags;
     DBuf<unsigned long long> dbg;

@@ -23,12 +23,18 @@
 //    link); two STORE warps copy each finished Y_b to global memory, fence
 //    and release it while the 8 compute warps already run the next link
 //    (per-slot FULL/EMPTY named barriers hand the ring slots over).
+//  * ROLES BY SM: the first CTA to reach an SM takes the next role ticket
+//    (chain chunks, then P-workers); a CTA landing on a role's SM leaves, so
+//    every latency-critical CTA has its SM alone.
+//  * P-WORKERS (two per chunk, blocks j alternating) form P_j = base_j - (near
+//    partial slots) - (tail: G_{j,j-3} Y_{j-3}), the short sums that remain
+//    once Y_{j-3} is out.
 //  * HELPER CTAs (all others) take items from a host-built table in
-//    topological order (atomic counter): PARTIAL items sum one segment of SEG
-//    dependency blocks into a partial slot; the P-item of block b forms
-//    Dinv_b RHS_b first, then subtracts the partial slots in fixed order and
-//    its last segment (up to b-3), two links ahead of the chain.  Long sums of the
-//    last blocks are spread over many CTAs instead of serialising on one.
+//    topological order (atomic counter): PARTIAL items sum one segment of
+//    dependency blocks into a slot (segments grow geometrically away from the
+//    diagonal: 1, 2, 4, ..., SEG blocks); EARLY items form base_j = Dinv_j RHS_j
+//    - (bulk slots) well ahead of the chain.  Dependency flags are checked
+//    eight at a time and three stages of tile loads are in flight.
 //  * Release flags + relaxed polling + one acquire; the cooperative launch
 //    guarantees chain and helpers are co-resident (no deadlock by design:
 //    every table item depends only on earlier items and on chain stages
@@ -74,6 +80,7 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }

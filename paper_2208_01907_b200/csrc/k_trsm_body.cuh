@@ -58,9 +58,10 @@ __global__ void __launch_bounds__(64) k_diag_inv(int64_t Np, const T *__restrict
 struct TrsmArgs {
     int64_t N, Np;
     int ncol, ncolp, nch, nblk, seg;
-    const int4 *items;   // [nitems] (logical block j, chunk, segment or -1, slot)
+    const int4 *items;   // [nitems] (logical block j, chunk, q_lo | q_hi << 16, slot >= 0: PARTIAL | < 0: EARLY)
+    const int4 *pinfo;   // [nblk] block j: (first slot, #bulk slots, #near slots, tail q_lo); base slot last
+    int npw;             // P-worker CTAs per chunk (block j -> worker j % npw)
     int nitems;
-    const int *pbase;    // [nblk] first partial slot of logical block j
     T *part;         // partial sums [slot][chunk][64 x CW] (row-major)
     T *P;            // P_j, row-major Np x ncolp (by physical row)
     int *pflags;         // [2][nslots*nch]
@@ -78,7 +79,7 @@ struct TrsmArgs {
     T *Xb;           // backward result, row-major Np x ncolp
     int *flags;          // [2][nblk*nch]   chain released Y_j
     int *counter;        // [2]
-    unsigned *smids;     // [2][nch] SM of each chain CTA (+1; 0 = not yet published)
+    unsigned *smids;     // [2 dir][owner | role + 2][TRSM_MAXSM] role assignment by SM
     int epoch;
     unsigned long long *dbg;   // optional chain phase timers (HF_TRSM_DEBUG)
 };
@@ -87,7 +88,8 @@ struct TrsmArgs {
 // acc[i][j] (+|-)= sum_k As[k][tr*4+i] * Bs[k][tc*4+j]; FP32: FFMA2 with a broadcast
 // scalar (half the issue slots of scalar FFMA), the pairs along j kept in float2
 template <bool NEG>
-__device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc) {
+__device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc, int k0 = 0,
+                                          int k1 = TBS) {
     if constexpr (sizeof(T) == 4) {
         float2 c2[4][2];
 #pragma unroll
@@ -96,7 +98,7 @@ __device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *
             c2[i][1] = make_float2(acc[i][2], acc[i][3]);
         }
 #pragma unroll 16
-        for (int k = 0; k < TBS; ++k) {
+        for (int k = k0; k < k1; ++k) {
             const V4<T> a = ld4(&As[k * TBS + tr * 4]);
             const V4<T> y = ld4(&Bs[k * CW + tc * 4]);
             const T av[4] = {NEG ? -a.x : a.x, NEG ? -a.y : a.y, NEG ? -a.z : a.z, NEG ? -a.w : a.w};
@@ -116,7 +118,7 @@ __device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *
         }
     } else {
 #pragma unroll 8
-        for (int k = 0; k < TBS; ++k) {
+        for (int k = k0; k < k1; ++k) {
             const V4<T> a = ld4(&As[k * TBS + tr * 4]);
             const V4<T> y = ld4(&Bs[k * CW + tc * 4]);
             const T av[4] = {NEG ? -a.x : a.x, NEG ? -a.y : a.y, NEG ? -a.z : a.z, NEG ? -a.w : a.w};
@@ -128,11 +130,13 @@ __device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *
         }
     }
 }
-__device__ __forceinline__ void tile_fma(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc) {
-    tile_prod<false>(acc, As, Bs, tr, tc);
+__device__ __forceinline__ void tile_fma(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc, int k0 = 0,
+                                         int k1 = TBS) {
+    tile_prod<false>(acc, As, Bs, tr, tc, k0, k1);
 }
-__device__ __forceinline__ void tile_fms(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc) {
-    tile_prod<true>(acc, As, Bs, tr, tc);
+__device__ __forceinline__ void tile_fms(T (&acc)[4][4], const T *As, const T *Bs, int tr, int tc, int k0 = 0,
+                                         int k1 = TBS) {
+    tile_prod<true>(acc, As, Bs, tr, tc, k0, k1);
 }
 
 // ------------------------------------------------------------------ setup: G = Dinv Op
@@ -183,7 +187,8 @@ __global__ void k_lift_scatter(int64_t L, int ncol, int ncolp, const int32_t *__
 
 constexpr int NTHR = 320;                 // 8 compute warps + 2 store warps (chain); helpers use 256
 constexpr int NCOMP = 256;
-constexpr int SMEM_ELEMS = 7 * TILE;     // 112 KB: chain = Yring[3] + M[2 stages][2]; helper = 2 x (A + B)
+constexpr int TRSM_MAXSM = 256;           // SM id table size of the role assignment
+constexpr int SMEM_ELEMS = 7 * TILE;     // 112 KB: chain = Yring[3] + M[2 stages][2]; helper = 3 x (A + B)
 
 template <bool BWD>
 __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
@@ -194,16 +199,38 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
     int *pflags = a.pflags + (BWD ? a.nslots * a.nch : 0);
     int *aflags = a.aflags + (BWD ? a.nblk * a.nch : 0);
     int *counter = a.counter + (BWD ? 1 : 0);
-    unsigned *smids = a.smids + (BWD ? a.nch : 0);
+    // role by SM: the first CTA to arrive on an SM claims it and takes the next role
+    // ticket (chain chunks, then P-workers); a CTA that finds its SM owned by a role
+    // leaves, so chain CTAs and P-workers each have an SM to themselves
+    unsigned *smrole = a.smids + (BWD ? 2 * TRSM_MAXSM : 0);   // [owner | role + 2] per SM
+    int *role_ctr = a.counter + 2 + (BWD ? 1 : 0);
+    const int nroles = a.nch * (1 + a.npw);
+    __shared__ int role_s;
+    if (tid == 0) {
+        const unsigned me = smid() % TRSM_MAXSM;
+        int role = -1;   // -1: helper, -2: leave
+        if (atomicCAS(&smrole[me], 0u, 1u) == 0u) {
+            const int r = atomicAdd(role_ctr, 1);
+            role = r < nroles ? r : -1;
+            atomicExch(&smrole[TRSM_MAXSM + me], (unsigned)(role + 2));
+        } else {
+            unsigned v;
+            while ((v = *(volatile unsigned *)&smrole[TRSM_MAXSM + me]) == 0u) __nanosleep(32);
+            role = v >= 2u ? -2 : -1;
+        }
+        role_s = role;
+    }
+    __syncthreads();
+    const int role = role_s;
+    if (role == -2) return;
     const T *Op = BWD ? a.Up : a.Lp;
     T *Yout = BWD ? a.Xb : a.Y;
     const T *Dinv = BWD ? a.LinvB : a.LinvF;
     auto phys = [&](int j) { return BWD ? (a.nblk - 1 - j) : j; };
 
-    if ((int)blockIdx.x < a.nch) {
+    if (role >= 0 && role < a.nch) {
         // =================================================== CHAIN (chunk cc)
-        const int cc = blockIdx.x, c0 = cc * CW;
-        if (tid == 0) atomicExch(&smids[cc], smid() + 1u);
+        const int cc = role, c0 = cc * CW;
         T *Yr = sm;               // [3][TILE] ring: Y_j in slot j % 3
         T *Mb = sm + 3 * TILE;    // [2 stages][G_{j,j-1}, G_{j,j-2}]
         if (tid >= NCOMP) {
@@ -286,24 +313,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
         return;
     }
 
-    // ======================================================= HELPERS (256 threads)
+    // ============================================ P-WORKERS and HELPERS (NCOMP threads)
     if (tid >= NCOMP) return;
-    {
-        // leave the chain CTAs' SMs to them
-        __shared__ int leave;
-        if (tid == 0) {
-            const unsigned me = smid() + 1u;
-            int l = 0;
-            for (int c = 0; c < a.nch; ++c) {
-                unsigned v;
-                while ((v = *(volatile unsigned *)&smids[c]) == 0u) __nanosleep(64);
-                l |= (v == me);
-            }
-            leave = l;
-        }
-        bar_sync(5, NCOMP);
-        if (leave) return;
-    }
+    const bool worker = role >= a.nch;
     const T *src = Yout;
     auto load_dep = [&](int s, int64_t r0, int64_t q0, int c0) {
         T *As = sm + s * 2 * TILE;
@@ -316,127 +328,218 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             cp_async16(&Bs[k * CW + r4], src + (q0 + k) * a.ncolp + c0 + r4);
         }
     };
-    auto wait_flag = [&](const int *f) {
-        if (tid == 0) wait_epoch(f, a.epoch);
-        bar_sync(5, NCOMP);
-    };
-    // t += sum over logical dependency blocks [q_lo, q_hi) of Op_bq Y_q, double buffered
+    // t += sum over logical dependency blocks [q_lo, q_hi) of Op_bq Y_q, three stages of
+    // cp.async in flight.  Released flags are checked eight at a time (independent loads,
+    // one round trip), so old dependencies cost no poll each.
+    __shared__ int rdy_s;
     auto accumulate = [&](T (&t)[4][4], int64_t r0, int c0, int cc, int q_lo, int q_hi) {
         const int ndep = q_hi - q_lo;
         if (ndep <= 0) return;
-        wait_flag(&flags[q_lo * a.nch + cc]);
+        int ready = 0;   // blocks [q_lo, q_lo + ready) known released (uniform)
+        auto ensure = [&](int dq) {
+            if (dq < ready) return;
+            if (tid == 0) {
+                const int *f = flags + (size_t)(q_lo + dq) * a.nch + cc;
+                const int nchk = min(8, ndep - dq);
+                int v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = u < nchk ? ld_relaxed32(f + (size_t)u * a.nch) : 0;
+                int n = 0;
+                while (n < nchk && v[n] == a.epoch) ++n;
+                if (n == 0) {
+                    while (ld_relaxed32(f) != a.epoch) __nanosleep(20);
+                    n = 1;
+                }
+                fence_acquire();
+                rdy_s = dq + n;
+            }
+            bar_sync(5, NCOMP);
+            ready = rdy_s;
+        };
+        ensure(0);
         load_dep(0, r0, (int64_t)phys(q_lo) * TBS, c0);
         cp_commit();
+        if (ndep > 1) {
+            ensure(1);
+            load_dep(1, r0, (int64_t)phys(q_lo + 1) * TBS, c0);
+            cp_commit();
+        }
         for (int dq = 0; dq < ndep; ++dq) {
-            if (dq + 1 < ndep) {
-                wait_flag(&flags[(q_lo + dq + 1) * a.nch + cc]);
-                load_dep((dq + 1) & 1, r0, (int64_t)phys(q_lo + dq + 1) * TBS, c0);
+            if (dq + 2 < ndep) {
+                ensure(dq + 2);
+                load_dep((dq + 2) % 3, r0, (int64_t)phys(q_lo + dq + 2) * TBS, c0);
                 cp_commit();
+                cp_wait_2();
+            } else if (dq + 1 < ndep) {
                 cp_wait_1();
             } else {
                 cp_wait_all();
             }
             bar_sync(5, NCOMP);
-            const T *As = sm + (dq & 1) * 2 * TILE;
+            const T *As = sm + (dq % 3) * 2 * TILE;
             tile_fma(t, As, As + TILE, tr, tc);
             bar_sync(5, NCOMP);
         }
     };
+    // out = Dinv_j RHS_j (no dependency): forward truncates R (FP64, original order)
+    // to FP32, backward starts from z = D^{-1} y
+    auto dinv_rhs = [&](T (&out)[4][4], int b, int64_t r0, int c0) {
+        T rhs[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + tr * 4 + i;
+            if (!BWD) {
+                const int64_t pr = r < a.N ? a.perm[r] : 0;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int c = c0 + tc * 4 + jj;
+                    rhs[i][jj] = (r < a.N && c < a.ncol) ? cvt_down(a.R[pr + (int64_t)c * a.ldr], T()) : T(0);
+                }
+            } else {
+                const V4<T> y = ld4(&a.Y[r * a.ncolp + c0 + tc * 4]);
+                const T d = r < a.N ? a.D[r] : T(1);
+                rhs[i][0] = div_rn(y.x, d);
+                rhs[i][1] = div_rn(y.y, d);
+                rhs[i][2] = div_rn(y.z, d);
+                rhs[i][3] = div_rn(y.w, d);
+            }
+        }
+        T *As = sm, *Bs = sm + TILE;
+        const T *Li = Dinv + (size_t)b * TILE;
+#pragma unroll
+        for (int u = 0; u < TILE / EPC / NCOMP; ++u) {
+            const int e = (tid + u * NCOMP) * EPC;
+            cp_async16(&As[e], Li + e);
+        }
+        cp_commit();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            st4(&Bs[(tr * 4 + i) * CW + tc * 4], rhs[i][0], rhs[i][1], rhs[i][2], rhs[i][3]);
+        cp_wait_all();
+        bar_sync(5, NCOMP);
+        tile_fma(out, As, Bs, tr, tc);
+        bar_sync(5, NCOMP);   // the stage-0 buffers are reused by accumulate()
+    };
+    // acc += slots [s_lo, s_hi) of chunk cc in increasing order, in batches: tid 0 waits
+    // for the next slot and takes every consecutive slot already released with it, then
+    // all threads stream the batch (two slots' loads in flight)
+    auto sum_slots = [&](T (&acc)[4][4], int cc, int s_lo, int s_hi) {
+        for (int s2 = s_lo; s2 < s_hi;) {
+            if (tid == 0) {
+                const int *pf = pflags + cc;
+                if (ld_relaxed32(pf + (size_t)s2 * a.nch) != a.epoch)
+                    while (ld_relaxed32(pf + (size_t)s2 * a.nch) != a.epoch) __nanosleep(20);
+                int e = s2 + 1;
+                while (e < s_hi && ld_relaxed32(pf + (size_t)e * a.nch) == a.epoch) ++e;
+                fence_acquire();
+                item_s = e;
+            }
+            bar_sync(5, NCOMP);
+            const int e = item_s;
+            bar_sync(5, NCOMP);   // item_s is rewritten by the next batch / item fetch
+            const T *pp = a.part + ((size_t)s2 * a.nch + cc) * (TBS * CW) + (tr * 4) * CW + tc * 4;
+            const size_t sstride = (size_t)a.nch * TBS * CW;
+            V4<T> cur[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cur[i] = ld4(pp + i * CW);
+            for (int q = s2; q < e; ++q) {
+                V4<T> nxt[4];
+                if (q + 1 < e) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) nxt[i] = ld4(pp + (size_t)(q + 1 - s2) * sstride + i * CW);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[i][0] += cur[i].x;
+                    acc[i][1] += cur[i].y;
+                    acc[i][2] += cur[i].z;
+                    acc[i][3] += cur[i].w;
+                }
+                if (q + 1 < e) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+                }
+            }
+            s2 = e;
+        }
+    };
+    auto store_slot = [&](const T (&v)[4][4], int cc, int sl) {
+        T *pp = a.part + ((size_t)sl * a.nch + cc) * (TBS * CW);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st4(&pp[(tr * 4 + i) * CW + tc * 4], v[i][0], v[i][1], v[i][2], v[i][3]);
+        bar_sync(5, NCOMP);
+        if (tid == 0) {
+            __threadfence();
+            st_release32(&pflags[sl * a.nch + cc], a.epoch);
+        }
+    };
 
+    if (worker) {
+        // ------------------------------------------------ P-WORKER (chunk cc, blocks j = w mod npw)
+        // P_j = base_j - (near slots, in order) - tail [tail_lo, j-2), alone on its SM so the
+        // few short sums between Y_{j-3} and P_j run at full speed (base_j = Dinv_j RHS_j -
+        // bulk slots comes from an EARLY item of the helpers).
+        const int wi = role - a.nch, cc = wi / a.npw, w = wi % a.npw;
+        const int c0 = cc * CW;
+        const bool wdbg = a.dbg && tid == 0 && cc == 0;
+        unsigned long long wph[4] = {0, 0, 0, 0}, wtp = wdbg ? gtimer() : 0;
+#define WPH(q) if (wdbg) { unsigned long long n_ = gtimer(); wph[q] += n_ - wtp; wtp = n_; }
+        for (int j = w; j < a.nblk; j += a.npw) {
+            const int4 pi = a.pinfo[j];   // (first slot, #bulk, #near, tail_lo)
+            const int64_t r0 = (int64_t)phys(j) * TBS;
+            const int sbase = pi.x + pi.y + pi.z;
+            T base[4][4] = {}, t[4][4] = {};
+            WPH(3)
+            sum_slots(base, cc, sbase, sbase + 1);
+            WPH(0)
+            sum_slots(t, cc, pi.x + pi.y, sbase);
+            WPH(1)
+            accumulate(t, r0, c0, cc, pi.w, j > 2 ? j - 2 : 0);
+            WPH(2)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                st4(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4], base[i][0] - t[i][0], base[i][1] - t[i][1],
+                    base[i][2] - t[i][2], base[i][3] - t[i][3]);
+            bar_sync(5, NCOMP);
+            if (tid == 0) {
+                __threadfence();
+                st_release32(&aflags[j * a.nch + cc], a.epoch);
+            }
+        }
+        if (wdbg)
+            for (int q = 0; q < 4; ++q) atomicAdd(&a.dbg[8 + (BWD ? 4 : 0) + q], wph[q]);
+#undef WPH
+        return;
+    }
+
+    // ------------------------------------------- HELPERS: PARTIAL and EARLY items in table order
     for (;;) {
         if (tid == 0) item_s = atomicAdd(counter, 1);
         bar_sync(5, NCOMP);
         const int idx = item_s;
+        bar_sync(5, NCOMP);   // item_s is reused by sum_slots
         if (idx >= a.nitems) return;
         const int4 it = a.items[idx];
-        const int j = it.x, cc = it.y, sg = it.z, slot = it.w;
+        const int j = it.x, cc = it.y, slot = it.w;
         const int b = phys(j);
         const int64_t r0 = (int64_t)b * TBS;
         const int c0 = cc * CW;
-        T t[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) t[i][jj] = T(0);
-        if (sg >= 0) {
-            // ---- PARTIAL item: t = sum over segment sg of Op_bq Y_q -> slot
-            accumulate(t, r0, c0, cc, sg * a.seg, (sg + 1) * a.seg);
-            T *pp = a.part + ((size_t)slot * a.nch + cc) * (TBS * CW);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                st4(&pp[(tr * 4 + i) * CW + tc * 4], t[i][0], t[i][1], t[i][2], t[i][3]);
-            bar_sync(5, NCOMP);
-            if (tid == 0) {
-                __threadfence();
-                st_release32(&pflags[slot * a.nch + cc], a.epoch);
-            }
-            continue;
-        }
-        // ---- P-item.  First Dinv_j RHS_j (no dependency): forward truncates R
-        //      (FP64, original order) to FP32, backward starts from z = D^{-1} y
-        T out[4][4] = {};
-        {
-            T rhs[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t r = r0 + tr * 4 + i;
-                if (!BWD) {
-                    const int64_t pr = r < a.N ? a.perm[r] : 0;
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const int c = c0 + tc * 4 + jj;
-                        rhs[i][jj] = (r < a.N && c < a.ncol) ? cvt_down(a.R[pr + (int64_t)c * a.ldr], T()) : T(0);
-                    }
-                } else {
-                    const V4<T> y = ld4(&a.Y[r * a.ncolp + c0 + tc * 4]);
-                    const T d = r < a.N ? a.D[r] : T(1);
-                    rhs[i][0] = div_rn(y.x, d);
-                    rhs[i][1] = div_rn(y.y, d);
-                    rhs[i][2] = div_rn(y.z, d);
-                    rhs[i][3] = div_rn(y.w, d);
-                }
-            }
-            T *As = sm, *Bs = sm + TILE;
-            const T *Li = Dinv + (size_t)b * TILE;
-#pragma unroll
-            for (int u = 0; u < TILE / EPC / NCOMP; ++u) {
-                const int e = (tid + u * NCOMP) * EPC;
-                cp_async16(&As[e], Li + e);
-            }
-            cp_commit();
+        T t[4][4] = {};
+        if (slot >= 0) {
+            // PARTIAL: t = sum over the segment [q_lo, q_hi) of Op_bq Y_q -> slot
+            accumulate(t, r0, c0, cc, it.z & 0xFFFF, it.z >> 16);
+            store_slot(t, cc, slot);
+        } else {
+            // EARLY: base_j = Dinv_j RHS_j - (bulk slots, in order) -> the base slot
+            const int4 pi = a.pinfo[j];
+            T out[4][4] = {};
+            dinv_rhs(out, b, r0, c0);
+            sum_slots(t, cc, pi.x, pi.x + pi.y);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                st4(&Bs[(tr * 4 + i) * CW + tc * 4], rhs[i][0], rhs[i][1], rhs[i][2], rhs[i][3]);
-            cp_wait_all();
-            bar_sync(5, NCOMP);
-            tile_fma(out, As, Bs, tr, tc);
-            bar_sync(5, NCOMP);   // the stage-0 buffers are reused by accumulate()
-        }
-        // then t = partial slots in fixed order + the last segment (up to j-3)
-        const int nq = j > 2 ? j - 2 : 0;
-        const int nseg = (nq + a.seg - 1) / a.seg;
-        for (int s2 = 0; s2 + 1 < nseg; ++s2) {
-            const int sl = a.pbase[j] + s2;
-            wait_flag(&pflags[sl * a.nch + cc]);
-            const T *pp = a.part + ((size_t)sl * a.nch + cc) * (TBS * CW);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const V4<T> v = ld4(&pp[(tr * 4 + i) * CW + tc * 4]);
-                t[i][0] += v.x;
-                t[i][1] += v.y;
-                t[i][2] += v.z;
-                t[i][3] += v.w;
-            }
-        }
-        accumulate(t, r0, c0, cc, nseg > 0 ? (nseg - 1) * a.seg : 0, nq);
-        // P_j = Dinv_j RHS_j - t
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            st4(&a.P[(r0 + tr * 4 + i) * a.ncolp + c0 + tc * 4], out[i][0] - t[i][0], out[i][1] - t[i][1], out[i][2] - t[i][2], out[i][3] - t[i][3]);
-        bar_sync(5, NCOMP);
-        if (tid == 0) {
-            __threadfence();
-            st_release32(&aflags[j * a.nch + cc], a.epoch);
+                for (int jj = 0; jj < 4; ++jj) out[i][jj] -= t[i][jj];
+            store_slot(out, cc, pi.x + pi.y + pi.z);
         }
     }
 }
@@ -481,38 +584,60 @@ void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T 
     HF_CHECK_LAUNCH(ctx);
 }
 
-// Helper item table in topological order.  Logical blocks j (forward j = b,
-// backward j = nblk-1-b); P_j depends on chain outputs 0..j-3 and on its
-// partial slots.  Items are placed by the chain stage after which they can
-// run: P-item(j) at stage j-3; PARTIAL(j, s) (segment [s*seg, (s+1)*seg) of
-// the dependency range [0, j-2), all but its last segment) at stage
-// max((s+1)*seg - 1, j-3-LA), LA = lookahead, so bulk work is queued just
-// ahead of the chain instead of in front of it.  Within a stage: P-items
-// first.  Every item depends only on earlier items and on chain stages <=
-// its own stage, so persistent CTAs taking items in order cannot deadlock.
-static void build_items(int nblk, int nch, int seg, std::vector<int4> &items, std::vector<int> &pbase, int &nslots) {
+// Work decomposition of P_j = Dinv_j RHS_j - sum_{q < j-2} G_jq Y_q (logical
+// blocks j: forward j = b, backward j = nblk-1-b).  The dependency range is cut
+// into segments whose sizes grow GEOMETRICALLY away from the diagonal: a TAIL
+// that the P-worker sums itself once Y_{j-3} is out, NEAR partial segments of
+// 1, 2, 4, ... < SEG blocks and BULK partial segments of SEG blocks back to
+// q = 0.  A segment ending at q_hi can run once Y_{q_hi-1} is out; the sizes
+// keep every near segment's work below the chain time left until P_j is
+// needed.  The helpers' table holds, in topological order, PARTIAL items
+// (placed at chain stage max(q_hi - 1, j - 3 - LA), LA = lookahead, so bulk
+// work is queued just ahead of the chain instead of in front of it) and one
+// EARLY item per block and chunk, base_j = Dinv_j RHS_j - (bulk slots), placed
+// ELAG stages after its last bulk segment's gate (at most j - 3).  The
+// P-worker of (j, chunk) computes P_j = base_j - (near slots) - tail.  Every
+// table item depends only on earlier items and on chain stages <= its own,
+// and a P-worker only on items and chain stages before its block, so the
+// persistent CTAs cannot deadlock.  Slot layout of block j: [bulk..., near...,
+// base]; slots are summed in increasing q order (deterministic).
+static void build_items(int nblk, int nch, int seg, std::vector<int4> &items, std::vector<int4> &pinfo, int &nslots) {
     int LA = 24;   // HF_TRSM_LA: tuning
     if (const char *e = getenv("HF_TRSM_LA")) LA = std::max(0, atoi(e));
-    pbase.assign(nblk, 0);
+    int TAIL = 1;  // HF_TRSM_TAIL: tuning (1 / 2 / 4: 7.06 / 7.17 / 7.72 ms per C2 apply)
+    if (const char *e = getenv("HF_TRSM_TAIL")) TAIL = std::max(1, atoi(e));
+    int ELAG = 8;  // HF_TRSM_ELAG: stages between the last bulk segment's gate and its EARLY item
+    const bool GEO = !(getenv("HF_TRSM_GEO") && atoi(getenv("HF_TRSM_GEO")) == 0);   // geometric near segments
+    if (const char *e = getenv("HF_TRSM_ELAG")) ELAG = std::max(0, atoi(e));
+    pinfo.assign(nblk, make_int4(0, 0, 0, 0));
     nslots = 0;
     std::vector<std::vector<int4>> stage(nblk + 2);   // stage s -> index s+1 (stage -1 first)
-    for (int j = 0; j < nblk; ++j) {
-        pbase[j] = nslots;
-        const int nq = j > 2 ? j - 2 : 0;
-        const int nseg = (nq + seg - 1) / seg;
-        nslots += std::max(0, nseg - 1);
-    }
-    for (int j = 0; j < nblk; ++j) {
-        const int st = std::max(-1, j - 3);
-        for (int c = 0; c < nch; ++c) stage[st + 1].push_back(make_int4(j, c, -1, -1));
-    }
+    std::vector<std::pair<int, int>> segs;
     for (int j = 0; j < nblk; ++j) {
         const int nq = j > 2 ? j - 2 : 0;
-        const int nseg = (nq + seg - 1) / seg;
-        for (int s = 0; s + 1 < nseg; ++s) {
-            const int st = std::max((s + 1) * seg - 1, j - 3 - LA);
-            for (int c = 0; c < nch; ++c) stage[st + 1].push_back(make_int4(j, c, s, pbase[j] + s));
+        segs.clear();
+        const int tail_lo = std::max(0, nq - TAIL);
+        int hi = tail_lo, sz = GEO ? 1 : seg, nnear = 0;
+        while (hi > 0) {
+            const int lo = std::max(0, hi - sz);
+            segs.push_back({lo, hi});
+            if (sz < seg) ++nnear;
+            hi = lo;
+            sz = std::min(seg, 2 * sz);
         }
+        std::reverse(segs.begin(), segs.end());      // increasing q: bulk first, then near
+        const int nbulk = (int)segs.size() - nnear;
+        pinfo[j] = make_int4(nslots, nbulk, nnear, tail_lo);
+        int st_e = -1;
+        for (int s2 = 0; s2 < (int)segs.size(); ++s2) {
+            const int lo = segs[s2].first, h2 = segs[s2].second;
+            const int sst = std::max(h2 - 1, j - 3 - LA);
+            if (s2 < nbulk) st_e = std::max(st_e, std::max(sst, h2 - 1 + ELAG));
+            for (int c = 0; c < nch; ++c) stage[sst + 1].push_back(make_int4(j, c, lo | (h2 << 16), nslots + s2));
+        }
+        st_e = std::max(-1, std::min(st_e, j - 3));   // before the P-worker needs it, after its bulk partials
+        for (int c = 0; c < nch; ++c) stage[st_e + 1].push_back(make_int4(j, c, 0, -1 - nbulk));
+        nslots += (int)segs.size() + 1;     // + the base slot
     }
     items.clear();
     for (auto &v : stage)
@@ -538,20 +663,20 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         auto key = std::make_pair(nblk, nch * 1000 + seg);
         auto it = ctx->trsm_tables.find(key);
         if (it == ctx->trsm_tables.end()) {
-            std::vector<int4> items;
-            std::vector<int> pbase;
+            std::vector<int4> items, pinfo;
             TrsmTable t;
-            build_items(nblk, nch, seg, items, pbase, t.nslots);
-            t.items.alloc(items.size(), st);
-            t.pbase.alloc(pbase.size(), st);
-            HF_CUDA(cudaMemcpyAsync(t.items.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
-            HF_CUDA(cudaMemcpyAsync(t.pbase.p, pbase.data(), pbase.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            build_items(nblk, nch, seg, items, pinfo, t.nslots);
+            t.items.alloc(std::max<size_t>(items.size(), 1), st);
+            t.pinfo.alloc(pinfo.size(), st);
+            if (!items.empty())
+                HF_CUDA(cudaMemcpyAsync(t.items.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            HF_CUDA(cudaMemcpyAsync(t.pinfo.p, pinfo.data(), pinfo.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
             HF_CUDA(cudaStreamSynchronize(st));   // host vectors die here (once per shape and context)
             t.nitems = (int)items.size();
             it = ctx->trsm_tables.emplace(key, std::move(t)).first;
         }
         p.items = it->second.items.p;
-        p.pbase = it->second.pbase.p;
+        p.pinfo = it->second.pinfo.p;
         p.nitems = it->second.nitems;
         p.nslots = it->second.nslots;
         p.tab_nblk = nblk;
@@ -563,16 +688,24 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         p.flags.zero(st);
         p.epoch = 0;
     }
-    p.counter.alloc(2 + 2 * (size_t)nch, st);      // [2 counters | 2 x nch SM ids]
-    HF_CUDA(cudaMemsetAsync(p.counter.p, 0, (2 + 2 * (size_t)nch) * sizeof(int), st));
+    int npw = 2;   // HF_TRSM_PW: P-worker CTAs per chunk
+    if (const char *e = getenv("HF_TRSM_PW")) npw = std::max(1, atoi(e));
+    const int nroles = nch * (1 + npw);
+    // [2 item counters | 2 role tickets | 2 directions x (owner[MAXSM] | role[MAXSM])]
+    const size_t ncnt = 4 + 4 * (size_t)TRSM_MAXSM;
+    p.counter.alloc(ncnt, st);
+    HF_CUDA(cudaMemsetAsync(p.counter.p, 0, ncnt * sizeof(int), st));
     p.epoch += 1;
-    TrsmArgs a{p.N, p.Np, (int)ncol, ncolp, nch, nblk, seg, p.items, p.nitems, p.pbase, p.part.p,
-               p.P.p, p.pflags.p, p.flags.p + 2 * nblk * nch, p.nslots, p.Lp.p, p.Up.p, p.LinvF.p, p.LinvB.p,
-               p.D, p.perm, R, ldr, p.Y.p, p.Xb.p, p.flags.p, p.counter.p,
-               reinterpret_cast<unsigned *>(p.counter.p + 2), p.epoch, nullptr};
+    TrsmArgs a;
+    a.N = p.N; a.Np = p.Np; a.ncol = (int)ncol; a.ncolp = ncolp; a.nch = nch; a.nblk = nblk; a.seg = seg;
+    a.items = p.items; a.pinfo = p.pinfo; a.npw = npw; a.nitems = p.nitems; a.part = p.part.p; a.P = p.P.p;
+    a.pflags = p.pflags.p; a.aflags = p.flags.p + 2 * nblk * nch; a.nslots = p.nslots; a.Lp = p.Lp.p; a.Up = p.Up.p;
+    a.LinvF = p.LinvF.p; a.LinvB = p.LinvB.p; a.D = p.D; a.perm = p.perm; a.R = R; a.ldr = ldr; a.Y = p.Y.p;
+    a.Xb = p.Xb.p; a.flags = p.flags.p; a.counter = p.counter.p;
+    a.smids = reinterpret_cast<unsigned *>(p.counter.p + 4); a.epoch = p.epoch; a.dbg = nullptr;
     const bool want_dbg = getenv("HF_TRSM_DEBUG") != nullptr;
     if (want_dbg) {
-        p.dbg.alloc(8, st);
+        p.dbg.alloc(16, st);
         p.dbg.zero(st);
         a.dbg = p.dbg.p;
     }
@@ -586,9 +719,10 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, k_trsm<true>, NTHR, shm));
         per_sm = std::max(1, std::min(a0, a1));
     }
-    // helpers that share an SM with a chain CTA leave, so launch more than 2 nch
-    const int grid = std::min(std::max(2 * nch + 1, nch + p.nitems + per_sm), ctx->num_sms * per_sm);
-    HF_REQUIRE(grid >= 2 * nch + 1, "preconditioner: too many RHS chunks for one launch");
+    // roles by SM (chain CTAs, P-workers), then helpers; CTAs sharing an SM with a
+    // role leave, so launch enough that helpers remain
+    const int grid = std::min(std::max(nroles * per_sm + 1, nroles + p.nitems + per_sm), ctx->num_sms * per_sm);
+    HF_REQUIRE(grid >= nroles * per_sm + 1, "preconditioner: too many RHS chunks for one launch");
     ClassTimer tm(ctx, "trsm");
     void *args[] = {&a};
     HF_CUDA(cudaLaunchCooperativeKernel((void *)k_trsm<false>, dim3(grid), dim3(NTHR), args, shm, st));
@@ -599,13 +733,17 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
     k_lift_scatter<<<gl, 256, 0, st>>>(p.L, (int)ncol, ncolp, p.pos1, p.Xb.p, W, ldw);
     HF_CHECK_LAUNCH(ctx);
     if (want_dbg) {
-        unsigned long long h[8];
+        unsigned long long h[16];
         HF_CUDA(cudaMemcpyAsync(h, p.dbg.p, sizeof(h), cudaMemcpyDeviceToHost, st));
         HF_CUDA(cudaStreamSynchronize(st));
-        for (int d = 0; d < 2; ++d)
+        for (int d = 0; d < 2; ++d) {
             fprintf(stderr, "[hf trsm %s] nblk %d nch %d grid %d items %d | us/link: wait-P %.3f  load %.3f  compute %.3f  store %.3f\n",
                     d ? "bwd" : "fwd", nblk, nch, grid, p.nitems, h[4 * d] / 1e3 / nblk, h[4 * d + 1] / 1e3 / nblk,
                     h[4 * d + 2] / 1e3 / nblk, h[4 * d + 3] / 1e3 / nblk);
+            fprintf(stderr, "[hf trsm %s] P-workers (chunk 0), us per block: base %.3f  near slots %.3f  tail %.3f  store+next %.3f\n",
+                    d ? "bwd" : "fwd", h[8 + 4 * d] / 1e3 / nblk, h[9 + 4 * d] / 1e3 / nblk, h[10 + 4 * d] / 1e3 / nblk,
+                    h[11 + 4 * d] / 1e3 / nblk);
+        }
     }
 }
 

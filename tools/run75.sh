@@ -1,0 +1,2 @@
+HF_TRSM_PERSM=1 HF_TRSM_TAIL=1 HF_TRSM_TRACE=1 timeout 300 python tools/prof_trsm.py C2 256 2 2>&1 | tail -7
+for v in "HF_TRSM_PERSM=1" "HF_TRSM_PERSM=2"; do echo "$v $(env $v HF_TRSM_TAIL=1 timeout 300 python tools/prof_trsm.py C2 256 3 2>&1 | tail -1)"; done
