@@ -97,16 +97,35 @@ __device__ __forceinline__ void tile_prod(T (&acc)[4][4], const T *As, const T *
             c2[i][0] = make_float2(acc[i][0], acc[i][1]);
             c2[i][1] = make_float2(acc[i][2], acc[i][3]);
         }
-#pragma unroll 16
-        for (int k = k0; k < k1; ++k) {
-            const V4<T> a = ld4(&As[k * TBS + tr * 4]);
-            const V4<T> y = ld4(&Bs[k * CW + tc * 4]);
-            const T av[4] = {NEG ? -a.x : a.x, NEG ? -a.y : a.y, NEG ? -a.z : a.z, NEG ? -a.w : a.w};
-            const float2 y01 = make_float2(y.x, y.y), y23 = make_float2(y.z, y.w);
+        // software pipelined: the fragments of the next 4 k are loaded while the current 4
+        // are used (the chain CTA runs this with only 2 warps per SM sub-partition)
+        V4<T> fa[2][4], fy[2][4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                c2[i][0] = __ffma2_rn(make_float2(av[i], av[i]), y01, c2[i][0]);
-                c2[i][1] = __ffma2_rn(make_float2(av[i], av[i]), y23, c2[i][1]);
+        for (int u = 0; u < 4; ++u) {
+            fa[0][u] = ld4(&As[(k0 + u) * TBS + tr * 4]);
+            fy[0][u] = ld4(&Bs[(k0 + u) * CW + tc * 4]);
+        }
+#pragma unroll
+        for (int kb = 0; kb < TBS; kb += 4) {
+            const int cur = (kb >> 2) & 1;
+            if (k0 + kb >= k1) break;
+            if (k0 + kb + 4 < k1) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    fa[cur ^ 1][u] = ld4(&As[(k0 + kb + 4 + u) * TBS + tr * 4]);
+                    fy[cur ^ 1][u] = ld4(&Bs[(k0 + kb + 4 + u) * CW + tc * 4]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const V4<T> a = fa[cur][u], y = fy[cur][u];
+                const T av[4] = {NEG ? -a.x : a.x, NEG ? -a.y : a.y, NEG ? -a.z : a.z, NEG ? -a.w : a.w};
+                const float2 y01 = make_float2(y.x, y.y), y23 = make_float2(y.z, y.w);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    c2[i][0] = __ffma2_rn(make_float2(av[i], av[i]), y01, c2[i][0]);
+                    c2[i][1] = __ffma2_rn(make_float2(av[i], av[i]), y23, c2[i][1]);
+                }
             }
         }
 #pragma unroll
