@@ -340,7 +340,7 @@ def main():
     tr_ms = kms["trailing"]
     achieved = fm["stage1"] / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else None
     traffic = load_traffic()
-    roof = {"kernel": "k_trailing (FP32 FFMA symmetric rank-nb update, bitwise canonical order)",
+    roof = {"kernel": "k_trailing_c (FP32 FFMA2 symmetric rank-nb update, bitwise canonical order)",
             "bound": "alu", "achieved": achieved, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
             "frac": (achieved / FFMA_PEAK_DERIVED) if achieved else None,
             "peak_source": "derived 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md sec. 7); "

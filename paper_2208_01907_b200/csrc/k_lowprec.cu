@@ -470,6 +470,9 @@ struct TrailArgs {
     const float *Sn;       // Sn[old + t*lds]   = -sigma_t s_i^t
     int64_t lds;
     const int32_t *status;
+    const float *Sc;       // Sc[t*ldc + new]  = s^t of the row at NEW position (compacted panel)
+    const float *Snc;      // Snc[t*ldc + new] = -sigma_t s^t
+    int64_t ldc;           // multiple of 4; >= the padded tile extent
 };
 
 constexpr int TB = 128;    // CTA tile (rows and columns)
@@ -596,6 +599,160 @@ __global__ void __launch_bounds__(256, 2) k_trailing(TrailArgs a) {
 
     // store the lower triangle of the new trailing matrix: 16-byte stores on full
     // off-diagonal tiles (rows tx*4..+3 are contiguous), masked scalar stores elsewhere
+    const bool full = (row0 > col0) && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int cl = CC(2 * j + h);
+            float *colp = a.Vnew + (col0 + cl) * a.ldv + row0;
+            if (full) {
+                *reinterpret_cast<float4 *>(colp + tx * 4) =
+                    h ? make_float4(acc[0][j].y, acc[1][j].y, acc[2][j].y, acc[3][j].y)
+                      : make_float4(acc[0][j].x, acc[1][j].x, acc[2][j].x, acc[3][j].x);
+                *reinterpret_cast<float4 *>(colp + 64 + tx * 4) =
+                    h ? make_float4(acc[4][j].y, acc[5][j].y, acc[6][j].y, acc[7][j].y)
+                      : make_float4(acc[4][j].x, acc[5][j].x, acc[6][j].x, acc[7][j].x);
+            } else if (cl < mpc) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int rl = RR(q);
+                    if (rl < mpr && row0 + rl >= col0 + cl) colp[rl] = h ? acc[q][j].y : acc[q][j].x;
+                }
+            }
+        }
+    }
+#undef RR
+#undef CC
+}
+
+// The panel in the NEW position space: Sc[t*ldc + new] = S[map[new] + t*lds] (and Sn),
+// so the trailing kernel streams contiguous 128-row slices of it with 16-byte cp.async.
+__global__ void k_gather_panel(int64_t mp, int nbp, const int32_t *__restrict__ map, const float *__restrict__ S,
+                               const float *__restrict__ Sn, int64_t lds, float *__restrict__ Sc,
+                               float *__restrict__ Snc, int64_t ldc, const int32_t *status) {
+    if (status[2]) return;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= mp) return;
+    const int64_t o = map[p];
+    const int t0 = blockIdx.y * 16, t1 = min(nbp, t0 + 16);
+#pragma unroll 4
+    for (int t = t0; t < t1; ++t) {
+        Sc[(int64_t)t * ldc + p] = S[o + (int64_t)t * lds];
+        Snc[(int64_t)t * ldc + p] = Sn[o + (int64_t)t * lds];
+    }
+}
+
+__device__ __forceinline__ void cp_async16_g(void *sdst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+// k_trailing with the panel operands streamed from the compacted panel by 16-byte
+// cp.async, three stages in flight (no register staging, no per-element address
+// arithmetic); the same single fmaf chain per entry in pivot order.
+constexpr int TNS = 3;   // cp.async stages
+constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float);
+__global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
+    if (a.status[2]) return;
+    extern __shared__ __align__(16) float dsm_t[];   // [TNS][TK][TB] x 2 (48 KB: dynamic)
+    float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t);
+    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t + TNS * TK * TB);
+    __shared__ int32_t rmap[TB], cmap[TB];
+
+    const int64_t t = blockIdx.x;
+    int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int64_t bj = t - bi * (bi + 1) / 2;
+    const int64_t row0 = bi * TB, col0 = bj * TB;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
+    const int nchunk = (a.nbp + TK - 1) / TK;
+
+    // chunk c -> stage c % TNS: TK pivots x 128 positions of each operand, 2 x 16 B per thread each
+    auto issue = [&](int c) {
+        if (c < nchunk) {
+            const int st = c % TNS;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int e = tid + u * 256;            // 512 16-byte pieces = 16 rows x 32
+                const int k = e >> 5, r4 = (e & 31) * 4;
+                const int64_t off = (int64_t)(c * TK + k) * a.ldc;
+                cp_async16_g(&As[st][k][r4], a.Snc + off + row0 + r4);
+                cp_async16_g(&Bs[st][k][r4], a.Sc + off + col0 + r4);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    issue(1);
+
+    if (tid < TB) rmap[tid] = (tid < mpr) ? a.map[row0 + tid] : -1;
+    else cmap[tid - TB] = (tid - TB < mpc) ? a.map[col0 + tid - TB] : -1;
+    __syncthreads();
+
+#define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
+#define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+    float2 acc[8][4];
+    {
+        int32_t rm[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int32_t cm = cmap[CC(2 * j + h)];
+                const float *colp = a.Vold + (int64_t)(cm >= 0 ? cm : 0) * a.ldv;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float v = (cm >= 0 && rm[q] >= cm) ? __ldg(colp + rm[q]) : 0.f;
+                    if (h) acc[q][j].y = v;
+                    else acc[q][j].x = v;
+                }
+            }
+        }
+    }
+
+    for (int c = 0; c < nchunk; ++c) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();                    // chunk c landed for all threads; stage (c+2)%3 is free
+        issue(c + 2);
+        const int st = c % TNS;
+        const int kmax = min(TK, a.nbp - c * TK);
+        if (kmax == TK) {
+#pragma unroll
+            for (int kk = 0; kk < TK; ++kk) {
+                const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+            }
+        } else {
+            for (int kk = 0; kk < kmax; ++kk) {   // ragged last chunk: exactly nbp updates
+                const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+            }
+        }
+    }
+
     const bool full = (row0 > col0) && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -935,11 +1092,16 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     orig[1].alloc(L, st);
     map[0].alloc(L, st);
     if (look) map[1].alloc(L, st);
-    DBuf<float> S[2], Sn[2], sigma[2], SNrow[2], DG[2], Lorig, Dk;
+    DBuf<float> S[2], Sn[2], sigma[2], SNrow[2], DG[2], Lorig, Dk, Sc, Snc;
+    const int64_t ldc = cdiv(L, TB) * TB;   // compacted panel: padded to whole 128-row tiles
     for (int b = 0; b < (look ? 2 : 1); ++b) {
         S[b].alloc((size_t)L * nb, st);
         Sn[b].alloc((size_t)L * nb, st);
         sigma[b].alloc(nb, st);
+        if (b == 0 && !look) {   // the compacted panel of the streaming trailing kernel
+            Sc.alloc((size_t)ldc * cdiv(nb, TK) * TK, st);
+            Snc.alloc((size_t)ldc * cdiv(nb, TK) * TK, st);
+        }
         if (look) {
             SNrow[b].alloc((size_t)L * nb, st);
             DG[b].alloc(L, st);
@@ -983,6 +1145,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
 
     HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     DBuf<unsigned long long> dbg;
     const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
     if (want_dbg) {
@@ -1042,12 +1205,20 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             TrailArgs ta;
             ta.mp = mp; ta.nbp = nbp; ta.ldv = L;
             ta.map = map[pb].p; ta.S = S[pb].p; ta.Sn = Sn[pb].p; ta.lds = L; ta.status = status.p;
+            ta.Sc = Sc.p; ta.Snc = Snc.p; ta.ldc = ldc;
             const int64_t T = cdiv(mp, TB);
             const int64_t ntiles = T * (T + 1) / 2;
             if (!look) {
                 ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
+                if (Sc.p) {
+                    ClassTimer tg(ctx, "other");
+                    k_gather_panel<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st>>>(
+                        mp, nbp, map[pb].p, S[pb].p, Sn[pb].p, L, Sc.p, Snc.p, ldc, status.p);
+                    HF_CHECK_LAUNCH(ctx);
+                }
                 ClassTimer tm(ctx, "trailing");
-k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
+                if (Sc.p) k_trailing_c<<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
+                else k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
                 vb ^= 1;
             } else {

@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_stage1.py tests/test_gpu_dist.py tests/test_gpu_stage23.py tests/test_gpu_fp64.py tests/test_gpu_krylov.py -x -q > gpurun_out/t88.log 2>&1; echo t=$?
+timeout 600 python bench.py > gpurun_out/bench88.log 2>&1; echo b=$?
