@@ -189,6 +189,28 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
 hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t ldx,
                            double *S22, int64_t lds);
 
+/* ------------------- NEXT-1: the (double, double-double) pair */
+/* Alg. 1 steps 2-4 with the higher precision raised to double-double (Table 1's
+ * (double, quadruple) row): block GCR (Alg. 5) with every N x n2
+ * block as (hi, lo) double pairs, K11 W formed with error-free products and
+ * double-double sums, Gram inverses and updates in double-double, and
+ * S22 = K22 - K21 X12 in double-double.  lf must be the FP64 factorization
+ * (hf_factor_lowprec with prec = 64): its FP64 L D L^T is the lower-precision
+ * preconditioner, applied to the residual rounded to double.  opts: tol is
+ * the per-column recursive ||r||/||b|| target (default 1e-28).  S22hi/lo_host:
+ * n2 x n2 column-major (S22 = hi + lo exactly).  The returned hybrid is a
+ * double-double one: hf_factor_hard factors S22 in double-double (same rule
+ * as below), hf_hard_export works, hf_solve returns HF_ERR_STATE.  One rank
+ * only (HF_ERR_INVALID_ARG on a distributed or virtual-rank context). */
+hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf,
+                          const hf_gcr_opts *opts, hf_hybrid **out, double *S22hi_host_or_null,
+                          double *S22lo_host_or_null, hf_gcr_info *info_host);
+/* X (L x n2, ORIGINAL row order, zero on Lambda_2 rows) and S22 of a
+ * double-double hybrid as hi / lo parts; DEVICE pointers (any may be NULL);
+ * HF_ERR_STATE on a double hybrid. */
+hf_status hf_hybrid_export_dd(hf_ctx *ctx, const hf_hybrid *hy, double *Xhi, double *Xlo, int64_t ldx,
+                              double *S22hi, double *S22lo, int64_t lds);
+
 /* ---------------------------- a7: hard factorization, P:192, P:84 [R15] */
 /* FP64 Bunch-Parlett (complete pivoting, alpha = (1+sqrt17)/8) LDL^T of
  * (S22 + S22^T)/2 with 1x1/2x2 pivots; stops when max|S_ij| of the trailing

@@ -278,11 +278,64 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
 hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t ldx, double *S22,
                            int64_t lds);
 
+hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf,
+                          const hf_gcr_opts *opts, hf_hybrid **out, double *S22hi_host_or_null,
+                          double *S22lo_host_or_null, hf_gcr_info *info_host) {
+    if (!ctx || !lf || !out) return HF_ERR_INVALID_ARG;
+    *out = nullptr;
+    hf_gcr_opts o{1e-28, 100};
+    if (opts) o = *opts;
+    hf_gcr_info info{0, 0.0, 0.0};
+    std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
+    hf_status s = guarded(ctx, [&] {
+        HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr_dd: bad arguments");
+        HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr_dd: tol > 0, max_iter >= 1");
+        HF_REQUIRE(lf->prec == 64, "hf_schur_gcr_dd: the factor must be FP64 (hf_factor_lowprec with prec 64)");
+        HF_REQUIRE(ctx->nranks <= 1 && ctx->vnranks == 0, "hf_schur_gcr_dd: single-rank only");
+        hy->K = K;
+        hy->ld = ld;
+        hy->L = lf->L;
+        hy->N = lf->N;
+        hy->n2 = lf->n2;
+        hy->lf = lf;
+        hy->stream = ctx->stream;
+        hy->num_sms = ctx->num_sms;
+        hf::schur_gcr_dd(ctx, hy.get(), o, &info);
+        const size_t bytes = (size_t)hy->n2 * hy->n2 * sizeof(double);
+        if (S22hi_host_or_null && hy->n2 > 0)
+            HF_CUDA(cudaMemcpyAsync(S22hi_host_or_null, hy->S22.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (S22lo_host_or_null && hy->n2 > 0)
+            HF_CUDA(cudaMemcpyAsync(S22lo_host_or_null, hy->S22lo.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+    if (info_host) *info_host = info;
+    if (s == HF_OK || s == HF_ERR_NOT_CONVERGED || s == HF_ERR_BREAKDOWN) *out = hy.release();
+    return s;
+}
+
+hf_status hf_hybrid_export_dd(hf_ctx *ctx, const hf_hybrid *hy, double *Xhi, double *Xlo, int64_t ldx,
+                              double *S22hi, double *S22lo, int64_t lds) {
+    if (!ctx || !hy) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        if (!hy->dd) throw hf::Error{HF_ERR_STATE, "hf_hybrid_export_dd: not a double-double hybrid"};
+        const int64_t L = hy->L, n2 = hy->n2;
+        HF_REQUIRE(ldx >= L && lds >= n2, "hf_hybrid_export_dd: leading dimensions");
+        if (n2 == 0) return;
+        cudaStream_t st = ctx->stream;
+        if (Xhi) HF_CUDA(cudaMemcpy2DAsync(Xhi, ldx * 8, hy->X.p, L * 8, L * 8, n2, cudaMemcpyDeviceToDevice, st));
+        if (Xlo) HF_CUDA(cudaMemcpy2DAsync(Xlo, ldx * 8, hy->Xlo.p, L * 8, L * 8, n2, cudaMemcpyDeviceToDevice, st));
+        if (S22hi) HF_CUDA(cudaMemcpy2DAsync(S22hi, lds * 8, hy->S22.p, n2 * 8, n2 * 8, n2, cudaMemcpyDeviceToDevice, st));
+        if (S22lo) HF_CUDA(cudaMemcpy2DAsync(S22lo, lds * 8, hy->S22lo.p, n2 * 8, n2 * 8, n2, cudaMemcpyDeviceToDevice, st));
+        HF_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 hf_status hf_factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker, int64_t *kernel_dim_host) {
     if (!ctx || !hy) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {
         HF_REQUIRE(eps_ker >= 0.0, "hf_factor_hard: eps_ker < 0");
-        hf::factor_hard(ctx, hy, eps_ker);
+        if (hy->dd) hf::factor_hard_dd(ctx, hy, eps_ker);
+        else hf::factor_hard(ctx, hy, eps_ker);
         if (kernel_dim_host) *kernel_dim_host = hy->kernel_dim;
     });
 }
@@ -311,6 +364,7 @@ hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x,
     hf_status s = guarded(ctx, [&] {
         if (!hy->hard_done && hy->n2 > 0)
             throw hf::Error{HF_ERR_STATE, "hf_solve: call hf_factor_hard first"};
+        if (hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve: not available for a double-double hybrid"};
         hf_gcr_opts o{1e-14, 100};
         hf::hybrid_solve(ctx, hy, b, x, o, &info);
     });

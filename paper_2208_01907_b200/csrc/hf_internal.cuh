@@ -218,6 +218,8 @@ struct hf_hybrid {
     hf::DBuf<double> X;                // L x n2, original row order, zero on Lambda_2 rows
     hf::DBuf<double> B;                // L x n2: K12 (original row order, zero on Lambda_2 rows)
     hf::DBuf<double> S22;              // n2 x n2, Lambda_2 ascending
+    bool dd = false;                   // NEXT-1: X and S22 in double-double (hi in X / S22, lo below)
+    hf::DBuf<double> Xlo, S22lo;
     hf::DBuf<int64_t> lam2;            // [n2] original indices (ascending)
     hf::DBuf<uint8_t> mask1;           // [L] 1 on Lambda_1 rows
     // stage 3
@@ -243,6 +245,8 @@ void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const
                       hf_lowfactor *lf);
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
+void schur_gcr_dd(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);   // gcr_dd.cu
+void factor_hard_dd(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
                   hf_gcr_info *info);
 // multi-GPU plumbing (dist.cu)

@@ -1098,7 +1098,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         S[b].alloc((size_t)L * nb, st);
         Sn[b].alloc((size_t)L * nb, st);
         sigma[b].alloc(nb, st);
-        if (b == 0 && !look) {   // the compacted panel of the streaming trailing kernel
+        if (b == 0) {   // the compacted panel of the streaming trailing kernel (gathered on its stream)
             Sc.alloc((size_t)ldc * cdiv(nb, TK) * TK, st);
             Snc.alloc((size_t)ldc * cdiv(nb, TK) * TK, st);
         }
@@ -1228,8 +1228,14 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 const int vsrc = (pidx == 0) ? vb : (vb ^ 1);   // start of panel p
                 ta.Vold = V[vsrc].p; ta.Vnew = V[vsrc ^ 1].p;
                 {
+                    ClassTimer tg(ctx, "other", st2);
+                    k_gather_panel<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st2>>>(
+                        mp, nbp, map[pb].p, S[pb].p, Sn[pb].p, L, Sc.p, Snc.p, ldc, status.p);
+                    HF_CHECK_LAUNCH(ctx);
+                }
+                {
                     ClassTimer tm(ctx, "trailing", st2);
-                    k_trailing<<<(unsigned)ntiles, 256, 0, st2>>>(ta);
+                    k_trailing_c<<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st2>>>(ta);
                     HF_CHECK_LAUNCH(ctx);
                 }
                 // the next chain reads the start of panel p (vsrc); before it runs, the trailing

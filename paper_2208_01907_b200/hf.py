@@ -29,7 +29,8 @@ EXPORTED = [
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
-    "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64",
+    "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64", "hf_schur_gcr_dd",
+    "hf_hybrid_export_dd",
 ]
 
 
@@ -83,6 +84,9 @@ def load() -> ctypes.CDLL:
         "hf_schur_gcr": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(gcr_info)],
         "hf_hybrid_export": [vp, vp, vp, i64, vp, i64],
+        "hf_schur_gcr_dd": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp, vp,
+                            ctypes.POINTER(gcr_info)],
+        "hf_hybrid_export_dd": [vp, vp, vp, vp, i64, vp, vp, i64],
         "hf_factor_hard": [vp, vp, dbl, pi64],
         "hf_hard_export": [vp, vp, vp, vp, pi64],
         "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
@@ -312,6 +316,16 @@ class Hybrid:
                                                      max(n2, 1)))
         return X[:n2, :N].T, S[:n2, :n2].T
 
+    def export_dd(self):
+        """Double-double hybrid: (Xhi, Xlo: device L x n2, original row order; S22hi, S22lo: device n2 x n2)."""
+        L, n2 = self.lf.L, self.lf.n2
+        dev = f"cuda:{self.ctx.device}"
+        out = [torch.empty(max(n2, 1), max(L, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        out += [torch.empty(max(n2, 1), max(n2, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.ctx.check(self.ctx.lib.hf_hybrid_export_dd(self.ctx.h, self.h, _ptr(out[0]), _ptr(out[1]), max(L, 1),
+                                                        _ptr(out[2]), _ptr(out[3]), max(n2, 1)))
+        return out[0][:n2, :L].T, out[1][:n2, :L].T, out[2][:n2, :n2].T, out[3][:n2, :n2].T
+
     def hard_export(self):
         n2 = self.lf.n2
         p = np.zeros(max(n2, 1), dtype=np.int64)
@@ -381,6 +395,25 @@ def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-1
     ctx.check(st, ok)
     gi = GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true, st)
     return Hybrid(ctx, h, lf, K), gi, S
+
+
+def hf_schur_gcr_dd(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-28, max_iter: int = 100,
+                    want_S22_host: bool = False, accept_failure: bool = False):
+    """NEXT-1: block GCR + Schur complement in double-double with the FP64 factor lf
+    (prec = 64) as preconditioner.  Returns (Hybrid, GcrInfo, (S22hi, S22lo) host or None)."""
+    _dev(K, torch.float64)
+    o = gcr_opts(float(tol), int(max_iter))
+    info = gcr_info()
+    h = ctypes.c_void_p()
+    want = want_S22_host and lf.n2
+    Sh = np.empty((lf.n2, lf.n2), dtype=np.float64, order="F") if want else None
+    Sl = np.empty((lf.n2, lf.n2), dtype=np.float64, order="F") if want else None
+    st = ctx.lib.hf_schur_gcr_dd(ctx.h, _ptr(K), K.shape[0], lf.h, ctypes.byref(o), ctypes.byref(h),
+                                 _ptr(Sh), _ptr(Sl), ctypes.byref(info))
+    ok = (HF_ERR_NOT_CONVERGED, HF_ERR_BREAKDOWN) if accept_failure else ()
+    ctx.check(st, ok)
+    gi = GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true, st)
+    return Hybrid(ctx, h, lf, K), gi, ((Sh, Sl) if want else None)
 
 
 def hf_factor_hard(ctx: Context, hy: Hybrid, eps_ker: float = 1e-10) -> int:

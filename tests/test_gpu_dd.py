@@ -1,0 +1,104 @@
+"""NEXT-1, the (double, double-double) pair: FP64 canonical stage 1
+(prec 64) + block GCR, Schur complement and hard factorization in double-double
+(hf_schur_gcr_dd), against the EXACT rational Schur complement of Eq. (2)
+ and its exact rank (oracle/exact.py).
+
+Bars: normwise e_S = ||S22_dd - S||_max / (||K22|| + ||K21|| ||X||)_max <= 1e-26
+(double-double unit roundoff 2^-104 ~ 5e-32, times the growth of the GCR's
+stopping tolerance 1e-28 through X); the FP64 path on the same inputs is
+reported beside it and must be >= 1e6 times less accurate unless it is itself
+below 1e-26; kernel_dim == n2 - rank(S) exactly."""
+import numpy as np
+import pytest
+import torch
+
+import hf_inputs as hi
+from hf_inputs.configs import ConfigSpec
+from oracle import exact
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "P48": ConfigSpec("P48", "planted", 48, n_min=3, n_hard=3, u_hard=(-10.0, -8.0)),
+    "P64": ConfigSpec("P64", "planted", 64, n_min=4, n_hard=4, u_hard=(-12.0, -6.0)),
+    "S4": ConfigSpec("S4", "saddle", 2 * 4 * 4 + 2 * 2 * 2, grid=4, jump=1e4),
+    "S6": ConfigSpec("S6", "saddle", 2 * 6 * 6 + 2 * 3 * 3, grid=6, jump=1e4),
+    "N8": ConfigSpec("N8", "neumann", 8 * 8, grid=8, n_incl=1, incl_size=2),
+}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_01907_b200 import hf
+    c = hf.Context(0)
+    yield c
+    c.close()
+
+
+def _run(ctx, spec, seed):
+    from paper_2208_01907_b200 import hf
+    K = hi.make_kbar(spec, seed).to("cuda")
+    hf.hf_scale(ctx, K)
+    lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min, prec=64)
+    hy, info, S = hf.hf_schur_gcr_dd(ctx, K, lf, want_S22_host=True)
+    return K, lf, hy, info, S
+
+
+@pytest.mark.parametrize("name,seed", [("P48", 0), ("P48", 1), ("P64", 0), ("S4", 0), ("S6", 0), ("N8", 0)])
+def test_dd_schur_vs_exact(ctx, name, seed):
+    from paper_2208_01907_b200 import hf
+    spec = CASES[name]
+    K, lf, hy, info, S = _run(ctx, spec, seed)
+    perm, _, _ = lf.export64()
+    N, n2 = lf.N, lf.n2
+    assert n2 >= 1
+    lam1, lam2 = [int(i) for i in perm[:N]], [int(i) for i in perm[N:]]
+    Kh = K.cpu().numpy()
+    Sx = exact.schur(Kh, lam1, lam2)
+    Shi, Slo = S
+    # normwise error against the exact S22 ([R17] form)
+    K22 = Kh[np.ix_(lam2, lam2)]
+    K21 = Kh[np.ix_(lam2, lam1)]
+    Xhi, Xlo, _, _ = hy.export_dd()
+    X = Xhi.cpu().numpy()[lam1]
+    den = np.abs(K22).max() + np.abs(K21).sum(1).max() * np.abs(X).max()
+    num = exact.rel_err(Sx, Shi, Slo) * max(abs(float(v)) for r in Sx for v in r)
+    e_dd = num / den
+    assert e_dd <= 1e-26, e_dd
+    assert info.max_rel_res_true <= 1e-26
+    # the FP64 path on the same inputs (the (double, double) hybrid)
+    hy64, _, S64 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True)
+    e_64 = exact.rel_err(Sx, S64, np.zeros_like(S64)) * max(abs(float(v)) for r in Sx for v in r) / den
+    assert e_dd <= 1e-26 and (e_64 <= 1e-26 or e_64 >= 1e6 * e_dd), (e_dd, e_64)
+    # hard factorization in double-double: kernel dimension = exact rank deficiency
+    kd = hf.hf_factor_hard(ctx, hy, eps_ker=1e-20)
+    assert kd == n2 - exact.rank(Sx)
+    hy64.close()
+    hy.close()
+    lf.close()
+
+
+def test_dd_requires_fp64_factor(ctx):
+    from paper_2208_01907_b200 import hf
+    spec = CASES["P48"]
+    K = hi.make_kbar(spec, 0).to("cuda")
+    hf.hf_scale(ctx, K)
+    lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)   # FP32 factor
+    with pytest.raises(hf.HFError) as e:
+        hf.hf_schur_gcr_dd(ctx, K, lf)
+    assert e.value.status == hf.HF_ERR_INVALID_ARG
+    lf.close()
+
+
+def test_dd_solve_is_refused(ctx):
+    from paper_2208_01907_b200 import hf
+    K, lf, hy, info, S = _run(ctx, CASES["P48"], 0)
+    hf.hf_factor_hard(ctx, hy, eps_ker=1e-20)
+    b = torch.ones(lf.L, dtype=torch.float64, device="cuda")
+    with pytest.raises(hf.HFError) as e:
+        hf.hf_solve(ctx, hy, b)
+    assert e.value.status == hf.HF_ERR_STATE
+    hy.close()
+    lf.close()
