@@ -40,6 +40,7 @@ class ConfigSpec:
     jump: float = 1.0         # saddle: coefficient jump across the line
     k_in: float = 1e6         # neumann: coefficient inside inclusions
     k_link: float = 1e-8      # neumann: coefficient of the edges joining them to the bulk
+    delta: float = 0.0        # stokes_ns: stabilisation weight of the pressure block
 
 
 CONFIGS = {
@@ -63,6 +64,11 @@ CONFIGS = {
     "N32": ConfigSpec("N32", "neumann", 32 * 32, grid=32, n_incl=3, incl_size=4),
     "S12": ConfigSpec("S12", "saddle", 2 * 12 * 12 + 2 * 6 * 6, grid=12, jump=1e4),
     "S24": ConfigSpec("S24", "saddle", 2 * 24 * 24 + 2 * 12 * 12, grid=24, jump=1e4),
+    # NEXT-3: nonsymmetric [A B^T; -B delta D] (stokes-like) and [A B^T; -B 0] (dd-hole-like)
+    "T8": ConfigSpec("T8", "stokes_ns", 2 * 8 * 8 + 2 * 4 * 4, grid=8, jump=1e4, delta=1e-2),
+    "H8": ConfigSpec("H8", "stokes_ns", 2 * 8 * 8 + 2 * 4 * 4, grid=8, jump=1e4, delta=0.0),
+    "T24": ConfigSpec("T24", "stokes_ns", 2 * 24 * 24 + 2 * 12 * 12, grid=24, jump=1e4, delta=1e-2),
+    "T96": ConfigSpec("T96", "stokes_ns", 2 * 96 * 96 + 2 * 48 * 48, grid=96, jump=1e4, delta=1e-2),
 }
 
 
@@ -212,6 +218,48 @@ def saddle_point(spec: ConfigSpec, seed: int, device="cpu") -> torch.Tensor:
     return torch.from_numpy(K).to(device)
 
 
+def stokes_ns(spec: ConfigSpec, seed: int, device="cpu") -> torch.Tensor:
+    """NONSYMMETRIC [A B^T; -B delta D] (the paper's stokes / dd-hole block
+    structure; delta = 0 gives [A B^T; -B 0]):
+    A and B exactly as saddle_point on the same grid and seeded line, the
+    lower-left block negated, D the graph Laplacian of the pressure unknowns
+    (the two unknowns of a macro-cell and the 4-neighbour macro-cells joined
+    with weight 1).  Returned as a row-major tensor holding the MATRIX Kbar
+    (entry [i, j]); column-major code needs Kbar.T.contiguous() (see colmajor)."""
+    n = spec.grid
+    base = saddle_point(ConfigSpec(spec.name, "saddle", spec.L, grid=n, jump=spec.jump), seed, "cpu").numpy()
+    nv = 2 * n * n
+    K = base.copy()
+    K[nv:, :nv] *= -1.0
+    if spec.delta != 0.0:
+        m = n // 2
+        D = np.zeros((2 * m * m, 2 * m * m))
+
+        def link(a, b):
+            D[a, a] += 1.0
+            D[b, b] += 1.0
+            D[a, b] -= 1.0
+            D[b, a] -= 1.0
+
+        for J in range(m):
+            for I in range(m):
+                c = 2 * (J * m + I)
+                link(c, c + 1)
+                if I + 1 < m:
+                    link(c, c + 2)
+                    link(c + 1, c + 3)
+                if J + 1 < m:
+                    link(c, c + 2 * m)
+                    link(c + 1, c + 2 * m + 1)
+        K[nv:, nv:] += spec.delta * D
+    return torch.from_numpy(K).to(device)
+
+
+def colmajor(K: torch.Tensor) -> torch.Tensor:
+    """The same matrix laid out column-major (what libhf reads) in a contiguous tensor."""
+    return K.T.contiguous()
+
+
 def make_kbar(cfg, seed: int = 0, device="cpu") -> torch.Tensor:
     spec = _spec(cfg)
     if spec.kind == "planted":
@@ -220,6 +268,8 @@ def make_kbar(cfg, seed: int = 0, device="cpu") -> torch.Tensor:
         return neumann_inclusions(spec, seed, device)
     if spec.kind == "saddle":
         return saddle_point(spec, seed, device)
+    if spec.kind == "stokes_ns":
+        return stokes_ns(spec, seed, device)
     raise ValueError(spec.kind)
 
 

@@ -132,7 +132,8 @@ def factor_lowprec(K: np.ndarray, tau: float, n_min: int = 0, n_extra: int = 0,
 
 def precond_apply(F: LowFactor, R: np.ndarray) -> np.ndarray:
     """Q^{-1} R of P:242: truncate R to the lower precision, forward unit-lower
-    solve, divide by D, backward L^T solve, lift back to FP64 [R12].
+    solve, divide by D, backward L^T solve (U for a nonsymmetric LDU factor),
+    lift back to FP64 [R12].
     R: N x m in pivot order (float64)."""
     R = np.atleast_2d(np.asarray(R, dtype=np.float64).reshape(F.N, -1))
     if F.N == 0:
@@ -142,7 +143,8 @@ def precond_apply(F: LowFactor, R: np.ndarray) -> np.ndarray:
     y = sla.solve_triangular(F.Lfac, r, lower=True, unit_diagonal=True,
                              check_finite=False)                      # forward
     y = (y / F.D[:, None].astype(dt)).astype(dt)                      # D^{-1}
-    e = sla.solve_triangular(F.Lfac, y, lower=True, trans="T", unit_diagonal=True,
+    Ub = getattr(F, "Ufac", None)          # nonsymmetric LDU (oracle/nonsym.py): U = Ufac^T
+    e = sla.solve_triangular(F.Lfac if Ub is None else Ub, y, lower=True, trans="T", unit_diagonal=True,
                              check_finite=False)                      # backward
     return np.asarray(e, dtype=dt).astype(np.float64)                 # lift
 

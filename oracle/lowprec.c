@@ -183,3 +183,114 @@ int oracle_factor_f64(int64_t L, const double *K, int64_t ld, double tau,
 {
     ORACLE_FACTOR_BODY(double, fma, sqrt, fabs)
 }
+
+/* ========================================================================= */
+/* NEXT-3: the NONSYMMETRIC matrices of sec. 4.2-4.3     */
+/* ([A B^T; -B delta D], [A B^T; -B 0]) with the same   */
+/* symmetric pivoting and postponing.                               */
+/* ========================================================================= */
+
+/* P:40 scaling for a general matrix: K_ij = (q_i Kbar_ij) q_j for i != j,    */
+/* every entry read (no symmetry assumed), diag(K) in {-1, 0, 1}.             */
+int oracle_scale_full(int64_t L, const double *Kbar, int64_t ld, double *K, double *q)
+{
+    for (int64_t i = 0; i < L; ++i) {
+        double d = Kbar[i + i * ld];
+        q[i] = (d != 0.0) ? 1.0 / sqrt(fabs(d)) : 1.0;
+    }
+    for (int64_t j = 0; j < L; ++j)
+        for (int64_t i = 0; i < L; ++i) {
+            if (i == j) continue;
+            K[i + j * ld] = (q[i] * Kbar[i + j * ld]) * q[j];
+        }
+    for (int64_t i = 0; i < L; ++i) {
+        double d = Kbar[i + i * ld];
+        K[i + i * ld] = (d > 0.0) ? 1.0 : ((d < 0.0) ? -1.0 : 0.0);
+    }
+    return 0;
+}
+
+/* FP32 LDU with symmetric pivoting and threshold postponing ("S'_22 */
+/* = K~'_22 - [K~_22]_{down 1} d^{-1} [K~_22]_{1 right}"), right-looking on   */
+/* the full matrix with physical row and column swaps.  Canonical arithmetic */
+/* [R19] (fixed roles, one FMA per entry per pivot, pivots in order):        */
+/*   d = v_PP, l_i = c_i / d (c_i = v_iP, IEEE division), r_j = v_Pj,         */
+/*   v_ij <- fmaf(-l_i, r_j, v_ij)  for every active (i, j), diagonal too.    */
+/* Pivot rule [R3], stop test [R4], floor [R5], enlargement [R9], Pi [R10]    */
+/* exactly as oracle_factor_f32.  Factors (pivot order, ld = L):              */
+/*   Lfac[i + k L] = l_i (unit lower), Ufac[i + k L] = r_i / d_k: column k    */
+/*   holds ROW k of the unit upper U (so U = Ufac^T), Dk[k] = d_k.            */
+int oracle_ldu_f32(int64_t L, const double *K, int64_t ld, double tau, int64_t n_min, int64_t n_extra,
+                   int64_t *perm, float *Dk, float *Lfac, float *Ufac, int64_t *out)
+{
+    if (L < 0 || !(tau > 0.0 && tau < 1.0) || n_min < 0 || n_extra < 0) return -1;
+    const size_t LL = (size_t)(L > 0 ? L : 1) * (size_t)(L > 0 ? L : 1);
+    float *A = (float *)malloc(LL * sizeof(float));
+    float *l = (float *)malloc((size_t)(L > 0 ? L : 1) * sizeof(float));
+    float *r = (float *)malloc((size_t)(L > 0 ? L : 1) * sizeof(float));
+    int64_t *orig = (int64_t *)malloc((size_t)(L > 0 ? L : 1) * sizeof(int64_t));
+    if (!A || !l || !r || !orig) { free(A); free(l); free(r); free(orig); return -1; }
+    for (int64_t j = 0; j < L; ++j)
+        for (int64_t i = 0; i < L; ++i) A[i + j * L] = (float)K[i + j * ld];   /* [R2] */
+    for (int64_t p = 0; p < L; ++p) orig[p] = p;
+    int64_t Ntau = L;
+    for (int64_t k = 0; k < L; ++k) {
+        int64_t best = k;                                                     /* [R3] */
+        for (int64_t p = k + 1; p < L; ++p) {
+            float a = fabsf(A[p + p * L]), b = fabsf(A[best + best * L]);
+            if (a > b || (a == b && orig[p] < orig[best])) best = p;
+        }
+        float d = A[best + best * L];
+        if (k == 0 && d == 0.0f) { Ntau = 0; break; }                        /* [R4] */
+        if (k > 0 && fabs((double)d) < tau * fabs((double)Dk[k - 1])) { Ntau = k; break; }
+        if (best != k) {                      /* swap rows k, best and columns k, best */
+            for (int64_t j = 0; j < L; ++j) {
+                float t = A[k + j * L]; A[k + j * L] = A[best + j * L]; A[best + j * L] = t;
+            }
+            for (int64_t i = 0; i < L; ++i) {
+                float t = A[i + k * L]; A[i + k * L] = A[i + best * L]; A[i + best * L] = t;
+            }
+            int64_t o = orig[k]; orig[k] = orig[best]; orig[best] = o;
+        }
+        Dk[k] = d;
+        for (int64_t i = k + 1; i < L; ++i) {
+            l[i] = A[i + k * L] / d;          /* column: c_i / d */
+            r[i] = A[k + i * L];              /* row value r_i = v_{P i} */
+        }
+        for (int64_t i = k + 1; i < L; ++i) {
+            A[i + k * L] = l[i];              /* L_ik stored in place (below the pivot) */
+            A[k + i * L] = r[i] / d;          /* U_ki stored in place (right of the pivot) */
+        }
+        _Pragma("omp parallel for schedule(static)")
+        for (int64_t j = k + 1; j < L; ++j) {
+            const float rj = r[j];
+            float *col = A + j * L;
+            for (int64_t i = k + 1; i < L; ++i) col[i] = fmaf(-l[i], rj, col[i]);
+        }
+    }
+    int64_t N = Ntau;
+    if (L - n_min < N) N = (L - n_min > 0) ? L - n_min : 0;
+    if (N < L) N = (N - n_extra > 0) ? N - n_extra : 0;
+    for (int64_t p = 0; p < N; ++p) perm[p] = orig[p];
+    {
+        char *used = (char *)calloc((size_t)(L > 0 ? L : 1), 1);
+        if (!used) { free(A); free(l); free(r); free(orig); return -1; }
+        for (int64_t p = 0; p < N; ++p) used[orig[p]] = 1;
+        int64_t w = N;
+        for (int64_t i = 0; i < L; ++i) if (!used[i]) perm[w++] = i;
+        free(used);
+    }
+    for (int64_t j = 0; j < L; ++j)
+        for (int64_t i = 0; i < L; ++i) {
+            float vl = 0.0f, vu = 0.0f;
+            if (j < N && i < N) {
+                vl = (i == j) ? 1.0f : ((i > j) ? A[i + j * L] : 0.0f);
+                vu = (i == j) ? 1.0f : ((i > j) ? A[j + i * L] : 0.0f);
+            }
+            Lfac[i + j * L] = vl;
+            Ufac[i + j * L] = vu;
+        }
+    out[0] = N; out[1] = Ntau;
+    free(A); free(l); free(r); free(orig);
+    return 0;
+}

@@ -103,3 +103,49 @@ def left_looking_ldlt(K: np.ndarray, tau: float):
         Lcols.append(lc)
         done.add(best)
     return piv, D, Lcols
+
+
+def left_looking_ldu(K: np.ndarray, tau: float):
+    """NEXT-3 pin: the nonsymmetric FP32 rule [R19] by left-looking exact
+    replay (no swaps, original indices): v_IJ^(k) = start value with one
+    exact-rounded fmaf(-l_I^t, r_J^t, .) per earlier pivot t; l_I = RN32(c_I/d),
+    r_J = v_{P J}.  Returns (pivots, D, Lcols, Urows) for the tau-rule alone,
+    Lcols[k] = {I: l_I^k}, Urows[k] = {J: RN32(r_J^k / d_k)}."""
+    L = K.shape[0]
+    v0 = {(i, j): f32(float(np.float32(K[i, j]))) for i in range(L) for j in range(L)}
+    piv, D, Ls, Rs, Lcols, Urows = [], [], [], [], [], []
+    done = set()
+
+    def entry(i, j, k):
+        v = v0[(i, j)]
+        for t in range(k):
+            v = fmaf_exact(-Ls[t][i], Rs[t][j], v)
+        return v
+
+    for k in range(L):
+        cands = [i for i in range(L) if i not in done]
+        best, bd = None, None
+        for i in cands:
+            d = entry(i, i, k)
+            if best is None or abs(d) > abs(bd):
+                best, bd = i, d
+        d = bd
+        if k == 0 and d == 0.0:
+            break
+        if k > 0 and abs(float(d)) < tau * abs(float(D[-1])):
+            break
+        lc, rr, ur = {}, {}, {}
+        for i in cands:
+            if i == best:
+                continue
+            lc[i] = f32(entry(i, best, k) / d)
+            rr[i] = entry(best, i, k)
+            ur[i] = f32(rr[i] / d)
+        piv.append(best)
+        D.append(d)
+        Ls.append(lc)
+        Rs.append(rr)
+        Lcols.append(lc)
+        Urows.append(ur)
+        done.add(best)
+    return piv, D, Lcols, Urows
