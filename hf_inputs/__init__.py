@@ -11,8 +11,10 @@ Recipes (DESIGN.md section 4 states them in full):
   C2 planted  L=16384, 64 hard u~U[-12,-6]
   C3 saddle   [A B^T; B 0], A: 2-dof Laplacian 96x96, 1e4 jump across a seeded line
   C4 planted  L=65536, 256 hard u~U[-12,-6]
+  NEXT-3 (nonsymmetric): stokes_ns [A B^T; -B delta D] (T8, T24, T96) and
+          delta = 0 ([A B^T; -B 0], H8); colmajor() gives the column-major bytes
 """
 from .configs import (  # noqa: F401
     CONFIGS, ConfigSpec, make_kbar, make_rhs, manufactured_x, planted, neumann_inclusions,
-    saddle_point, config_seed,
+    saddle_point, config_seed, stokes_ns, colmajor,
 )

@@ -109,6 +109,9 @@ hf_status hf_trim_cache(int device);
  * q: FP64[L].  Returns HF_ERR_INVALID_ARG if K holds NaN/Inf on or below the
  * diagonal. */
 hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);
+/* NEXT-3: the same scaling for a GENERAL matrix (every entry read and written:
+ * K_ij = (q_i Kbar_ij) q_j, K_ii = sign Kbar_ii).  Same errors as hf_scale. */
+hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);
 
 /* ---------------------------- a2-a3: lower-precision factor, P:64-85 [R2-R10] */
 typedef struct {
@@ -119,6 +122,10 @@ typedef struct {
     int32_t prec;     /* 0 or 32: FP32 factor (Alg. 1's lower precision for the       */
                       /* (float, double) pair); 64: FP64 factor, the lower precision  */
                       /* of the paper's (double, double-double) pair (NEXT-1)  */
+    int32_t nonsym;   /* NEXT-3: 1 = K is a GENERAL matrix (every entry read):       */
+                      /* FP32 LDU with the same pivoting / postponing, rule [R19]     */
+                      /* (d = v_PP, l_I = c_I / d, r_J = v_PJ, v_IJ <- fmaf(-l_I,     */
+                      /* r_J, v_IJ)); prec 32, one GPU.  0 = symmetric LDL^T.        */
 } hf_lowprec_opts;
 
 /* FP32 LDL^T of the scaled K (lower triangle read) with symmetric max-|diag|
@@ -141,6 +148,10 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
 hf_status hf_lowfactor_export64(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host,
                                 double *D_host, double *Lfac, int64_t ldl);
 hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
+/* NEXT-3: the unit upper factor U of a nonsymmetric LDU as Ufac = U^T (N x N,
+ * DEVICE, ldu >= N, pivot order): Ufac[i + k ldu] = U_ki.  HF_ERR_STATE on a
+ * symmetric factor. */
+hf_status hf_lowfactor_export_u(hf_ctx *ctx, const hf_lowfactor *lf, float *Ufac, int64_t ldu);
 
 /* --------------------------- a5: the preconditioner Q^{-1}, P:231-242 [R12] */
 /* W = lift( L^{-T} D^{-1} L^{-1} truncate(R) ) in FP32 for the Lambda_1 rows

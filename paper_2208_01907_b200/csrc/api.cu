@@ -157,13 +157,29 @@ hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
     });
 }
 
+hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || (K && q)), "hf_scale_full: bad arguments");
+        if (L == 0) return;
+        hf::DBuf<int> bad;
+        bad.alloc(1, ctx->stream);
+        bad.zero(ctx->stream);
+        hf::launch_scale_full(ctx, L, K, ld, q, bad.p);
+        int hb = 0;
+        HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        HF_REQUIRE(!hb, "hf_scale_full: K holds NaN or Inf");
+    });
+}
+
 // ------------------------------------------------------------------ a2-a3
 hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
                             const hf_lowprec_opts *opts, hf_lowfactor **out, int64_t *N_host,
                             int64_t *n2_host, int64_t *n2_tau_only_host) {
     if (!ctx || !out) return HF_ERR_INVALID_ARG;
     *out = nullptr;
-    hf_lowprec_opts o{1e-2, 0, 0, 0, 32};
+    hf_lowprec_opts o{1e-2, 0, 0, 0, 32, 0};
     if (opts) o = *opts;
     if (o.prec == 0) o.prec = 32;
     std::unique_ptr<hf_lowfactor> lf(new hf_lowfactor());
@@ -173,7 +189,11 @@ hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
         HF_REQUIRE(o.n_extra >= 0 && o.n_min >= 0, "hf_factor_lowprec: n_extra/n_min < 0");
         HF_REQUIRE(o.nb >= 0 && o.nb <= 256 && o.nb % 8 == 0, "hf_factor_lowprec: nb in {0, 8..256, multiple of 8}");
         HF_REQUIRE(o.prec == 32 || o.prec == 64, "hf_factor_lowprec: prec must be 32 or 64");
-        if (o.prec == 64) {
+        if (o.nonsym) {
+            HF_REQUIRE(o.prec == 32, "hf_factor_lowprec: the nonsymmetric LDU is FP32 only");
+            HF_REQUIRE(ctx->nranks == 1 && ctx->s1parts == 0, "hf_factor_lowprec: the nonsymmetric LDU is single-GPU");
+            hf::lowprec_factor_ns(ctx, L, K, ld, o, lf.get());
+        } else if (o.prec == 64) {
             HF_REQUIRE(ctx->nranks == 1 && ctx->s1parts == 0, "hf_factor_lowprec: prec 64 is single-GPU");
             hf::lowprec_factor64(ctx, L, K, ld, o, lf.get());
         } else if (ctx->nranks > 1) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->nranks);
@@ -198,6 +218,19 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
             HF_REQUIRE(ldl >= lf->N, "hf_lowfactor_export: ldl < N");
             HF_CUDA(cudaMemcpy2DAsync(Lfac, ldl * sizeof(float), lf->Lfac.p, lf->N * sizeof(float),
                                       lf->N * sizeof(float), lf->N, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    });
+}
+
+hf_status hf_lowfactor_export_u(hf_ctx *ctx, const hf_lowfactor *lf, float *Ufac, int64_t ldu) {
+    if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        if (!lf->nonsym) throw hf::Error{HF_ERR_STATE, "hf_lowfactor_export_u: not a nonsymmetric (LDU) factor"};
+        if (Ufac && lf->N) {
+            HF_REQUIRE(ldu >= lf->N, "hf_lowfactor_export_u: ldu < N");
+            HF_CUDA(cudaMemcpy2DAsync(Ufac, ldu * sizeof(float), lf->Ufac.p, lf->N * sizeof(float),
+                                      lf->N * sizeof(float), lf->N, cudaMemcpyDeviceToDevice, ctx->stream));
+            HF_CUDA(cudaStreamSynchronize(ctx->stream));
         }
     });
 }

@@ -208,6 +208,8 @@ struct hf_lowfactor {
     hf::DBuf<int32_t> pos1;            // original index -> pivot rank (Lambda_1) or -1
     hf::DBuf<float> D;                 // [N]
     hf::DBuf<float> Lfac;              // N x N unit lower, pivot order, ld = N
+    bool nonsym = false;               // NEXT-3: LDU of a general matrix; U = Ufac^T
+    hf::DBuf<float> Ufac;              // N x N: column k = row k of the unit upper U
     cudaStream_t stream = 0;
 };
 
@@ -237,12 +239,15 @@ struct hf_hybrid {
 // ----------------------------------------------------------------- launchers
 namespace hf {
 void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);
+void launch_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);   // NEXT-3
 void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                     hf_lowfactor *lf);
 void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                           hf_lowfactor *lf, int nparts);
 void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                       hf_lowfactor *lf);
+void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                       hf_lowfactor *lf);   // NEXT-3
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void schur_gcr_dd(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);   // gcr_dd.cu

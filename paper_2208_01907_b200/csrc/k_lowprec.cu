@@ -653,6 +653,9 @@ __device__ __forceinline__ void cp_async16_g(void *sdst, const void *gsrc) {
 // arithmetic); the same single fmaf chain per entry in pivot order.
 constexpr int TNS = 3;   // cp.async stages
 constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float);
+// NS (NEXT-3, nonsymmetric LDU): the FULL square trailing matrix (T x T tiles),
+// A operand -l_I, B operand r_J, v_IJ <- fmaf(-l_I, r_J, v_IJ) [R19].
+template <bool NS>
 __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     if (a.status[2]) return;
     extern __shared__ __align__(16) float dsm_t[];   // [TNS][TK][TB] x 2 (48 KB: dynamic)
@@ -661,10 +664,17 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     __shared__ int32_t rmap[TB], cmap[TB];
 
     const int64_t t = blockIdx.x;
-    int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while (bi * (bi + 1) / 2 > t) --bi;
-    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-    const int64_t bj = t - bi * (bi + 1) / 2;
+    int64_t bi, bj;
+    if (NS) {
+        const int64_t T = (a.mp + TB - 1) / TB;
+        bi = t % T;
+        bj = t / T;
+    } else {
+        bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+        while (bi * (bi + 1) / 2 > t) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+        bj = t - bi * (bi + 1) / 2;
+    }
     const int64_t row0 = bi * TB, col0 = bj * TB;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
@@ -707,7 +717,8 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
                 const float *colp = a.Vold + (int64_t)(cm >= 0 ? cm : 0) * a.ldv;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const float v = (cm >= 0 && rm[q] >= cm) ? __ldg(colp + rm[q]) : 0.f;
+                    const bool ok = NS ? (cm >= 0 && rm[q] >= 0) : (cm >= 0 && rm[q] >= cm);
+                    const float v = ok ? __ldg(colp + rm[q]) : 0.f;
                     if (h) acc[q][j].y = v;
                     else acc[q][j].x = v;
                 }
@@ -753,7 +764,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
         }
     }
 
-    const bool full = (row0 > col0) && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
+    const bool full = (NS || row0 > col0) && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -771,7 +782,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const int rl = RR(q);
-                    if (rl < mpr && row0 + rl >= col0 + cl) colp[rl] = h ? acc[q][j].y : acc[q][j].x;
+                    if (rl < mpr && (NS || row0 + rl >= col0 + cl)) colp[rl] = h ? acc[q][j].y : acc[q][j].x;
                 }
             }
         }
@@ -1145,7 +1156,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
 
     HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
-    HF_CUDA(cudaFuncSetAttribute(k_trailing_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     DBuf<unsigned long long> dbg;
     const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
     if (want_dbg) {
@@ -1217,7 +1228,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                     HF_CHECK_LAUNCH(ctx);
                 }
                 ClassTimer tm(ctx, "trailing");
-                if (Sc.p) k_trailing_c<<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
+                if (Sc.p) k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
                 else k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
                 vb ^= 1;
@@ -1235,7 +1246,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 }
                 {
                     ClassTimer tm(ctx, "trailing", st2);
-                    k_trailing_c<<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st2>>>(ta);
+                    k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st2>>>(ta);
                     HF_CHECK_LAUNCH(ctx);
                 }
                 // the next chain reads the start of panel p (vsrc); before it runs, the trailing
@@ -1467,6 +1478,308 @@ void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, c
 #endif
     for (auto &b : VP) b.release();
     lowprec_finish(ctx, L, o, lf, status, pivorig, Dk, Lorig, nullptr);
+}
+
+// ========================================================================= NEXT-3
+// Nonsymmetric LDU with symmetric pivoting and threshold postponing (the
+// paper's stokes / dd-hole matrices; Eq. 1 P:46 is
+// written for a general K), canonical FP32 arithmetic [R19]:
+//   d = v_PP, l_I = c_I / d (IEEE), r_J = v_PJ, v_IJ <- fmaf(-l_I, r_J, v_IJ),
+// one fmaf per entry per pivot in pivot order -- bit-identical to the
+// right-looking oracle (oracle_ldu_f32) by the same argument as [R8] with the
+// roles fixed (the product -l_I r_J is exact inside the FMA).
+namespace {
+
+__global__ void k_cast_full(int64_t L, const double *__restrict__ K, int64_t ldk, float *__restrict__ V, int64_t ldv) {
+    for (int64_t j = blockIdx.x; j < L; j += gridDim.x)
+        for (int64_t i = threadIdx.x; i < L; i += blockDim.x) V[i + j * ldv] = __double2float_rn(K[i + j * ldk]);
+}
+
+struct ChainNSArgs {
+    int64_t m, K0;
+    int nbp, R;
+    double tau;
+    const float *V;               // full trailing matrix at the panel start (position space)
+    int64_t ldv;
+    const int32_t *orig;
+    float *S;                     // S[i + t*lds]  = r_i^t  (trailing B operand)
+    float *Sn;                    // Sn[i + t*lds] = -l_i^t (trailing A operand)
+    int64_t lds;
+    int32_t *pivpos;
+    float *Lorig, *Uorig;         // [orig + k*ldl]: l = c / d, r / d
+    int64_t ldl;
+    float *Dk;
+    int32_t *pivorig;
+    unsigned long long *slots;    // [2][G][SLOT_STRIDE] key | tag
+    unsigned long long *mbox;     // [2][G][2 (nb+1)] candidate row: (-l, r) words, float bits << 32 | tag
+    int32_t *status;
+};
+
+// Per pivot (CTA = a slice of rows; each row i also stands for COLUMN i):
+//  A local argmax of the lazy diagonal -> this CTA's slot; the candidate's panel
+//    values (-l_P^u, r_P^u), u < t, to the mailbox (tagged words)
+//  D every slot of this step -> the pivot key (smallest position on ties)
+//  E stop test [R4]
+//  F pivot row's (-l_P^u, r_P^u) from the winner's mailbox; column V[:, P] and
+//    row V[P, :] entries of own indices from the panel-start matrix
+//  G c_i = V_iP + sum_u fmaf(-l_i^u, r_P^u), r_i = V_Pi + sum_u fmaf(-l_P^u, r_i^u)
+//    (u ascending), l_i = c_i / d, lazy diagonal fmaf(-l_i, r_i, v_ii)
+__global__ void __launch_bounds__(1024, 1) k_chain_ns(ChainNSArgs a) {
+    extern __shared__ float smem[];
+    __shared__ unsigned long long red[32];
+    __shared__ unsigned long long bkey;
+    if (*(volatile int32_t *)&a.status[2]) return;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * a.R;
+    const int64_t nown = max((int64_t)0, min((int64_t)a.R, a.m - r0));
+    const int nb = a.nbp;
+    float *nl = smem;                          // [nb][R] -l_i^u of own indices
+    float *rr = nl + (size_t)nb * a.R;         // [nb][R]  r_i^u of own indices
+    float *spl = rr + (size_t)nb * a.R;        // [nb] -l_P^u of the pivot
+    float *spr = spl + nb;                     // [nb]  r_P^u of the pivot
+    const bool has = tid < nown;
+    const int64_t i = r0 + tid;
+    const int32_t oi = has ? a.orig[i] : 0;
+    float dg = has ? a.V[i + i * a.ldv] : 0.f;
+    bool piv = !has;
+    float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
+    bool pend = false;
+    float ps = 0.f, pn = 0.f, pl = 0.f, pu = 0.f;
+    int t = 0;
+    bool stopped = false;
+    for (; t < nb; ++t) {
+        const int64_t k = a.K0 + t;
+        const uint64_t tag = step_tag(k);
+        uint64_t key = piv ? 0ull : mkkey(dg, (uint32_t)i);
+        key = warp_max64(key);
+        if (lane == 0) red[wid] = key;
+        __syncthreads();
+        if (wid < 2) {
+            uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
+            v = warp_max64(v);
+            if (wid == 0) {
+                if (lane == 0) {
+                    unsigned long long *slot = &a.slots[((size_t)(t & 1) * G + blockIdx.x) * SLOT_STRIDE];
+                    st_relaxed_u64(slot, (v & ~TAGM) | tag);
+                }
+            } else if (v) {
+                unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * 2 * (nb + 1);
+                const int lr = (int)((int64_t)(POS_MAX - (uint32_t)((v >> 15) & POS_MAX)) - r0);
+                for (int u = lane; u < t; u += 32) {
+                    st_relaxed_u64(&mb[2 * u], ((unsigned long long)__float_as_uint(nl[(size_t)u * a.R + lr]) << 32) | tag);
+                    st_relaxed_u64(&mb[2 * u + 1], ((unsigned long long)__float_as_uint(rr[(size_t)u * a.R + lr]) << 32) | tag);
+                }
+            }
+        }
+        if (pend) {   // deferred global stores of step t-1
+            a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+            a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
+            a.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            a.Uorig[(int64_t)oi + (k - 1) * a.ldl] = pu;
+            pend = false;
+        }
+        if (wid == 0) {
+            const unsigned long long *sl = a.slots + (size_t)(t & 1) * G * SLOT_STRIDE;
+            uint64_t mx;
+            for (;;) {
+                bool ok = true;
+                mx = 0;
+                for (int g = lane; g < G; g += 32) {
+                    const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * SLOT_STRIDE]);
+                    ok &= (sv & TAGM) == tag;
+                    mx = umax64(mx, sv);
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+            }
+            mx = warp_max64(mx);
+            if (lane == 0) bkey = mx;
+        }
+        __syncthreads();
+        const uint64_t bk = bkey;
+        const float absd = __uint_as_float((uint32_t)(bk >> 32));
+        const int64_t P = (int64_t)(POS_MAX - (uint32_t)((bk >> 15) & POS_MAX));
+        const float d = ((bk >> 14) & 1) ? -absd : absd;
+        const bool stop = (k == 0) ? (absd == 0.f) : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev)));
+        if (stop) {
+            if (blockIdx.x == 0 && tid == 0) {
+                a.status[0] = (int32_t)k;
+                a.status[1] = t;
+                a.status[2] = 1;
+            }
+            stopped = true;
+            break;
+        }
+        float vc = 0.f, vr = 0.f;   // panel-start column / row entries of own index
+        if (!piv && i != P) {
+            vc = a.V[i + P * a.ldv];
+            vr = a.V[P + i * a.ldv];
+        }
+        {
+            const int owner = (int)(P / a.R);
+            const unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + owner) * 2 * (nb + 1);
+            for (int u = tid; u < 2 * t; u += nthr) {
+                uint64_t w;
+                do {
+                    w = ld_relaxed_u64(&mb[u]);
+                } while ((w & TAGM) != tag);
+                const float x = __uint_as_float((uint32_t)(w >> 32));
+                if (u & 1) spr[u >> 1] = x;
+                else spl[u >> 1] = x;
+            }
+        }
+        __syncthreads();
+        if (has && i == P) {
+            piv = true;
+            a.Dk[k] = d;
+            a.pivorig[k] = oi;
+            a.pivpos[t] = (int32_t)P;
+        } else if (!piv) {
+            float c = vc, r = vr;
+            const float *xl = nl + tid, *xr = rr + tid;
+            for (int u = 0; u < t; ++u) {                      // [R19] one fmaf per earlier pivot, in order
+                c = __fmaf_rn(xl[(size_t)u * a.R], spr[u], c);
+                r = __fmaf_rn(spl[u], xr[(size_t)u * a.R], r);
+            }
+            const float l = __fdiv_rn(c, d);
+            nl[(size_t)t * a.R + tid] = -l;
+            rr[(size_t)t * a.R + tid] = r;
+            ps = r;
+            pn = -l;
+            pl = l;
+            pu = __fdiv_rn(r, d);
+            pend = true;
+            dg = __fmaf_rn(-l, r, dg);                         // lazy diagonal, the trailing update's fma
+        }
+        dprev = d;
+    }
+    if (pend) {
+        a.S[i + (int64_t)(t - 1) * a.lds] = ps;
+        a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
+        a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+        a.Uorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pu;
+    }
+    if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
+}
+
+}  // namespace
+
+void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                       hf_lowfactor *lf) {
+    cudaStream_t st = ctx->stream;
+    lf->L = L;
+    lf->nonsym = true;
+    if (L == 0) {
+        lf->N = lf->Ntau = lf->n2 = 0;
+        return;
+    }
+    HF_REQUIRE(L <= (int64_t)POS_MAX - 1, "L too large for the 17-bit position key");
+    const int nsm = ctx->num_sms;
+    int maxsmem = 0;
+    HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    cudaFuncAttributes fa;
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_ns));
+    maxsmem -= (int)fa.sharedSizeBytes;
+    const int nb_def = 64;   // two panel values per own index
+    int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / (2 * nb_def + 2)))));
+    const int64_t G0 = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(L, 32)));
+    const int64_t R0 = cdiv(L, G0);
+    HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
+    int nb = o.nb > 0 ? o.nb : nb_def;
+    while (nb > 8 && (int64_t)(2 * nb * R0 + 2 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
+    nb = std::max(TK, (nb / TK) * TK);
+    HF_REQUIRE((int64_t)(2 * nb * R0 + 2 * nb) * 4 <= (int64_t)maxsmem, "panel does not fit in shared memory");
+
+    DBuf<float> V[2], S, Sn, Sc, Snc, Lorig, Uorig, Dk;
+    V[0].alloc((size_t)L * L, st);
+    V[1].alloc((size_t)L * L, st);
+    DBuf<int32_t> orig[2], map, pivpos, pivorig, status;
+    orig[0].alloc(L, st);
+    orig[1].alloc(L, st);
+    map.alloc(L, st);
+    S.alloc((size_t)L * nb, st);
+    Sn.alloc((size_t)L * nb, st);
+    const int64_t ldc = cdiv(L, TB) * TB;
+    Sc.alloc((size_t)ldc * nb, st);
+    Snc.alloc((size_t)ldc * nb, st);
+    Lorig.alloc((size_t)L * L, st);
+    Uorig.alloc((size_t)L * L, st);
+    Dk.alloc(L, st);
+    pivpos.alloc(nb, st);
+    pivorig.alloc(L, st);
+    status.alloc(4, st);
+    DBuf<unsigned long long> mbox, slots;
+    mbox.alloc((size_t)2 * nsm * 2 * (nb + 1), st);
+    mbox.zero(st);
+    slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
+    slots.zero(st);
+    HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
+    {
+        ClassTimer tm(ctx, "other");
+        k_cast_full<<<(unsigned)std::min<int64_t>(L, 65535), 256, 0, st>>>(L, K, ld, V[0].p, L);
+        HF_CHECK_LAUNCH(ctx);
+        k_iota32<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
+        HF_CHECK_LAUNCH(ctx);
+    }
+    HF_CUDA(cudaFuncSetAttribute(k_chain_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    int cur = 0;
+    int64_t m = L, K0 = 0;
+    while (m > 0) {
+        const int nbp = (int)std::min<int64_t>(nb, m);
+        const int64_t G = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(m, 32)));
+        const int64_t R = cdiv(m, G);
+        const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
+        const size_t shm = ((size_t)2 * nbp * R + 2 * nbp) * sizeof(float);
+        ChainNSArgs ca;
+        ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
+        ca.V = V[cur].p; ca.ldv = L; ca.orig = orig[cur].p;
+        ca.S = S.p; ca.Sn = Sn.p; ca.lds = L; ca.pivpos = pivpos.p;
+        ca.Lorig = Lorig.p; ca.Uorig = Uorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
+        ca.slots = slots.p; ca.mbox = mbox.p; ca.status = status.p;
+        {
+            ClassTimer tm(ctx, "chain");
+            void *args[] = {&ca};
+            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain_ns, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            HF_CHECK_LAUNCH(ctx);
+        }
+        const int64_t mp = m - nbp;
+        if (mp > 0) {
+            {
+                ClassTimer tm(ctx, "other");
+                k_compact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
+                    m, nbp, pivpos.p, orig[cur].p, map.p, orig[cur ^ 1].p, status.p);
+                HF_CHECK_LAUNCH(ctx);
+                k_gather_panel<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st>>>(
+                    mp, nbp, map.p, S.p, Sn.p, L, Sc.p, Snc.p, ldc, status.p);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            TrailArgs ta;
+            ta.mp = mp; ta.nbp = nbp; ta.ldv = L; ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L;
+            ta.status = status.p; ta.Sc = Sc.p; ta.Snc = Snc.p; ta.ldc = ldc;
+            ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
+            const int64_t T = cdiv(mp, TB);
+            {
+                ClassTimer tm(ctx, "trailing");
+                k_trailing_c<true><<<(unsigned)(T * T), 256, TRAIL_C_SMEM, st>>>(ta);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            cur ^= 1;
+        }
+        K0 += nbp;
+        m = mp;
+    }
+    V[0].release();
+    V[1].release();
+    lowprec_finish(ctx, L, o, lf, status, pivorig, Dk, Lorig, nullptr);
+    const int64_t N = lf->N;
+    lf->Ufac.alloc((size_t)std::max<int64_t>(N, 1) * std::max<int64_t>(N, 1), st);
+    if (N > 0) {
+        ClassTimer tm(ctx, "other");
+        k_gather_L<<<(unsigned)std::min<int64_t>(N, 65535), 256, 0, st>>>(N, pivorig.p, Uorig.p, L, lf->Ufac.p, N);
+        HF_CHECK_LAUNCH(ctx);
+    }
+    HF_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace hf

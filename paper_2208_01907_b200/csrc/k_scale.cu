@@ -3,6 +3,8 @@
 // HBM-bound: reads the lower triangle once (4 L^2 B) and writes the full
 // symmetric FP64 matrix (8 L^2 B).  32x32 tiles of the lower triangle are
 // staged in shared memory so the mirrored (transposed) write is coalesced.
+#include <algorithm>
+
 #include "hf_internal.cuh"
 
 namespace hf {
@@ -60,7 +62,30 @@ __global__ void __launch_bounds__(256) k_scale_tiles(int64_t L, double *__restri
     }
 }
 
+// NEXT-3: every entry of a general matrix, K_ij = (q_i Kbar_ij) q_j, diagonal sign.
+__global__ void k_scale_full(int64_t L, double *__restrict__ K, int64_t ld, const double *__restrict__ q, int *bad) {
+    for (int64_t j = blockIdx.x; j < L; j += gridDim.x) {
+        const double qj = q[j];
+        int badl = 0;
+        for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+            const double kb = K[i + j * ld];
+            if (!isfinite(kb)) badl = 1;
+            K[i + j * ld] = (i == j) ? ((kb > 0.0) ? 1.0 : ((kb < 0.0) ? -1.0 : 0.0))
+                                     : __dmul_rn(__dmul_rn(q[i], kb), qj);
+        }
+        if (badl) atomicOr(bad, 1);
+    }
+}
+
 }  // namespace
+
+void launch_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag) {
+    ClassTimer tm(ctx, "scale");
+    k_scale_q<<<(unsigned)cdiv(L, 256), 256, 0, ctx->stream>>>(L, K, ld, q, bad_flag);
+    HF_CHECK_LAUNCH(ctx);
+    k_scale_full<<<(unsigned)std::min<int64_t>(L, 65535), 256, 0, ctx->stream>>>(L, K, ld, q, bad_flag);
+    HF_CHECK_LAUNCH(ctx);
+}
 
 void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag) {
     ClassTimer tm(ctx, "scale");

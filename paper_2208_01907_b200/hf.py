@@ -30,7 +30,7 @@ EXPORTED = [
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
     "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64", "hf_schur_gcr_dd",
-    "hf_hybrid_export_dd",
+    "hf_hybrid_export_dd", "hf_lowfactor_export_u", "hf_scale_full",
 ]
 
 
@@ -42,7 +42,7 @@ class HFError(RuntimeError):
 
 class lowprec_opts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_double), ("n_extra", ctypes.c_int64), ("n_min", ctypes.c_int64),
-                ("nb", ctypes.c_int32), ("prec", ctypes.c_int32)]
+                ("nb", ctypes.c_int32), ("prec", ctypes.c_int32), ("nonsym", ctypes.c_int32)]
 
 
 class gcr_opts(ctypes.Structure):
@@ -77,10 +77,12 @@ def load() -> ctypes.CDLL:
         "hf_kernel_stats": [vp, ctypes.c_char_p, pdbl, pi64],
         "hf_launch_count": [vp, pi64],
         "hf_scale": [vp, i64, vp, i64, vp],
+        "hf_scale_full": [vp, i64, vp, i64, vp],
         "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
         "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
         "hf_lowfactor_destroy": [vp],
         "hf_lowfactor_export64": [vp, vp, vp, vp, vp, i64],
+        "hf_lowfactor_export_u": [vp, vp, vp, i64],
         "hf_schur_gcr": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(gcr_info)],
         "hf_hybrid_export": [vp, vp, vp, i64, vp, i64],
@@ -237,6 +239,15 @@ def hf_scale(ctx: Context, K: torch.Tensor) -> torch.Tensor:
     return q
 
 
+def hf_scale_full(ctx: Context, K: torch.Tensor) -> torch.Tensor:
+    """NEXT-3: in-place scaling of a general matrix (memory = column-major K); returns q."""
+    _dev(K, torch.float64)
+    L = K.shape[0]
+    q = torch.empty(L, dtype=torch.float64, device=K.device)
+    ctx.check(ctx.lib.hf_scale_full(ctx.h, L, _ptr(K), L, _ptr(q)))
+    return q
+
+
 # ---------------------------------------------------------------------- a2-a3
 class LowFactor:
     def __init__(self, ctx: Context, h, L: int, N: int, n2: int, n2_tau: int):
@@ -252,6 +263,12 @@ class LowFactor:
         self.ctx.check(self.ctx.lib.hf_lowfactor_export(self.ctx.h, self.h, _ptr(perm), _ptr(D),
                                                         _ptr(Lf), self.N))
         return perm, D[: self.N], (Lf.T if Lf is not None else None)
+
+    def export_u(self):
+        """Nonsymmetric factor: Ufac (device float32 N x N, pivot order) with U = Ufac^T."""
+        U = torch.empty(max(self.N, 1), max(self.N, 1), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        self.ctx.check(self.ctx.lib.hf_lowfactor_export_u(self.ctx.h, self.h, _ptr(U), max(self.N, 1)))
+        return U[: self.N, : self.N].T
 
     def export64(self, with_L: bool = True):
         """prec-64 factors: (perm np.int64[L], D np.float64[N], Lfac device float64 N x N)."""
@@ -277,10 +294,12 @@ class LowFactor:
 
 
 def hf_factor_lowprec(ctx: Context, K: torch.Tensor, tau: float = 1e-2, n_extra: int = 0,
-                      n_min: int = 0, nb: int = 0, prec: int = 32) -> LowFactor:
+                      n_min: int = 0, nb: int = 0, prec: int = 32, nonsym: bool = False) -> LowFactor:
+    """nonsym=True (NEXT-3): K is a general matrix whose COLUMN-major bytes are the
+    tensor's memory (pass hf_inputs.colmajor(Kbar-like tensor))."""
     _dev(K, torch.float64)
     L = K.shape[0]
-    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb), int(prec))
+    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb), int(prec), int(bool(nonsym)))
     h = ctypes.c_void_p()
     N, n2, n2t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     ctx.check(ctx.lib.hf_factor_lowprec(ctx.h, L, _ptr(K), L, ctypes.byref(o), ctypes.byref(h),
