@@ -225,6 +225,12 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
     if (n2 == 0) return;
     gather_K12(ctx, L, hy->K, hy->ld, hy->lam2.p, n2, hy->mask1.p, hy->B.p);   // step 2
     gather_K22(ctx, n2, hy->K, hy->ld, hy->lam2.p, hy->S22.p);
+    hy->nonsym = lf->nonsym;
+    if (hy->nonsym) {   // NEXT-3: the actual K21 (K21 != K12^T)
+        hy->B2.alloc((size_t)L * n2, st);
+        gather_K21T(ctx, L, hy->K, hy->ld, hy->lam2.p, n2, hy->mask1.p, hy->B2.p);
+    }
+    const double *K21T = hy->nonsym ? hy->B2.p : hy->B.p;
     const bool virt = ctx->vnranks > 0;
     const int nr = virt ? ctx->vnranks : ctx->nranks, rk = virt ? ctx->vrank : ctx->rank;
     int64_t c0 = 0, c1 = n2;
@@ -244,7 +250,7 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
             local_msg = e.msg;
         }
         // step 4: S22[:, slice] = K22[:, slice] - K21 X[:, slice]  (K21 X = B^T X: X is zero on Lambda_2 rows)
-        dgemm(ctx, true, n2, ns, L, -1.0, hy->B.p, L, hy->X.p + c0 * L, L, 1.0, hy->S22.p + c0 * n2, n2, nullptr,
+        dgemm(ctx, true, n2, ns, L, -1.0, K21T, L, hy->X.p + c0 * L, L, 1.0, hy->S22.p + c0 * n2, n2, nullptr,
               &w.dgw);
     } else if (N == 0) {
         HF_CUDA(cudaMemsetAsync(hy->X.p, 0, (size_t)L * n2 * sizeof(double), st));
@@ -308,6 +314,23 @@ void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker) {
             for (float d : D) dref = std::min(dref, std::fabs((double)d));
         }
     }
+    if (hy->nonsym) {   // NEXT-3: LU with complete pivoting (the 1x1 / 2x2 symmetric pivots do not apply)
+        hy->LUh.alloc((size_t)n2 * n2, st);
+        hy->perm2.alloc(n2, st);
+        hy->pcol2.alloc(n2, st);
+        hy->blocks.alloc(n2, st);
+        HF_CUDA(cudaMemsetAsync(hy->blocks.p, 0, n2 * sizeof(int32_t), st));
+        DBuf<int64_t> rk;
+        rk.alloc(1, st);
+        hard_lu(ctx, n2, hy->S22.p, eps_ker * dref, hy->LUh.p, hy->perm2.p, hy->pcol2.p, rk.p);
+        int64_t r = 0;
+        HF_CUDA(cudaMemcpyAsync(&r, rk.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        HF_CUDA(cudaStreamSynchronize(st));
+        hy->rank = r;
+        hy->kernel_dim = n2 - r;
+        hy->hard_done = true;
+        return;
+    }
     hy->Lh.alloc((size_t)n2 * n2, st);
     hy->Dh.alloc((size_t)n2 * n2, st);
     hy->perm2.alloc(n2, st);
@@ -350,8 +373,12 @@ void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, 
         z.alloc(n2, st);
         DBuf<double> dg;
         gather_rows(ctx, n2, hy->lam2.p, b, y2.p);
-        dgemm(ctx, true, n2, 1, L, -1.0, hy->B.p, L, y1.p, L, 1.0, y2.p, n2, nullptr, &dg);   // step 2
-        hard_solve(ctx, n2, hy->rank, hy->Lh.p, hy->Dh.p, hy->perm2.p, hy->blocks.p, y2.p, x2.p, z.p);  // step 3
+        dgemm(ctx, true, n2, 1, L, -1.0, hy->nonsym ? hy->B2.p : hy->B.p, L, y1.p, L, 1.0, y2.p, n2, nullptr,
+              &dg);                                                                                   // step 2
+        if (hy->nonsym)
+            hard_lu_solve(ctx, n2, hy->rank, hy->LUh.p, hy->perm2.p, hy->pcol2.p, y2.p, x2.p, z.p);   // step 3
+        else
+            hard_solve(ctx, n2, hy->rank, hy->Lh.p, hy->Dh.p, hy->perm2.p, hy->blocks.p, y2.p, x2.p, z.p);
         dgemm(ctx, false, L, 1, n2, -1.0, hy->X.p, L, x2.p, n2, 1.0, x, L, nullptr, &dg, 1);   // step 4
         scatter_rows(ctx, n2, hy->lam2.p, x2.p, x);
     }

@@ -221,6 +221,10 @@ struct hf_hybrid {
     hf::DBuf<double> B;                // L x n2: K12 (original row order, zero on Lambda_2 rows)
     hf::DBuf<double> S22;              // n2 x n2, Lambda_2 ascending
     bool dd = false;                   // NEXT-1: X and S22 in double-double (hi in X / S22, lo below)
+    bool nonsym = false;               // NEXT-3: general K: B2 = K21^T, S22 by LU with complete pivoting
+    hf::DBuf<double> B2;               // L x n2: K21^T (original row order, zero on Lambda_2 rows)
+    hf::DBuf<double> LUh;              // n2 x n2: [L \ U] of P S22 Q
+    hf::DBuf<int32_t> pcol2;           // [n2] column pivot labels (perm2 holds the row labels)
     hf::DBuf<double> Xlo, S22lo;
     hf::DBuf<int64_t> lam2;            // [n2] original indices (ascending)
     hf::DBuf<uint8_t> mask1;           // [L] 1 on Lambda_1 rows

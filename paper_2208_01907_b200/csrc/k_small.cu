@@ -27,6 +27,121 @@ __global__ void k_gather_cols(int64_t L, const double *__restrict__ K, int64_t l
     }
 }
 
+// NEXT-3: B2[i + j*L] = K[lam2[j] + i*ld] on Lambda_1 rows (K21^T in original row order)
+__global__ void k_gather_rows_t(int64_t L, const double *__restrict__ K, int64_t ld, const int64_t *__restrict__ lam2,
+                                int64_t n2, const uint8_t *__restrict__ mask1, double *__restrict__ B) {
+    for (int64_t j = blockIdx.y; j < n2; j += gridDim.y) {
+        const int64_t r = lam2[j];
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += (int64_t)gridDim.x * blockDim.x)
+            B[i + j * L] = mask1[i] ? K[r + i * ld] : 0.0;
+    }
+}
+
+// NEXT-3: LU with complete pivoting of the nonsymmetric S22 in FP64, one CTA, in
+// place: pivot = largest |entry| of the trailing block, ties -> smallest column
+// label, then smallest row label (the oracle's rule); rows and columns are swapped
+// physically; stop when the pivot is <= thr; A ends as [L \ U] with P S Q = L U.
+__global__ void __launch_bounds__(1024) k_hard_lu(int n, const double *__restrict__ S, double thr, double *A,
+                                                  int32_t *prow, int32_t *pcol, int64_t *rank_out) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    for (int64_t e = tid; e < (int64_t)n * n; e += nt) A[e] = S[e];
+    for (int i = tid; i < n; i += nt) {
+        prow[i] = i;
+        pcol[i] = i;
+    }
+    __shared__ double rv[32];
+    __shared__ int ri[32], rj[32], bi_s, bj_s;
+    __shared__ double bv_s;
+    __syncthreads();
+    auto better = [&](double v, int i, int j, double bv, int bi, int bj) {
+        // larger |value|; ties: smaller column label, then smaller row label
+        if (v != bv) return v > bv;
+        if (j < 0 || bj < 0) return bj < 0 && j >= 0;
+        const int cj = pcol[j], cb = pcol[bj];
+        if (cj != cb) return cj < cb;
+        return prow[i] < prow[bi];
+    };
+    int k = 0;
+    for (; k < n; ++k) {
+        double bv = -1.0;
+        int bi = -1, bj = -1;
+        for (int64_t e = tid; e < (int64_t)(n - k) * (n - k); e += nt) {
+            const int i = k + (int)(e % (n - k)), j = k + (int)(e / (n - k));
+            const double v = fabs(A[i + (int64_t)j * n]);
+            if (better(v, i, j, bv, bi, bj)) { bv = v; bi = i; bj = j; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (better(ov, oi, oj, bv, bi, bj)) { bv = ov; bi = oi; bj = oj; }
+        }
+        if (lane == 0) { rv[wid] = bv; ri[wid] = bi; rj[wid] = bj; }
+        __syncthreads();
+        if (tid == 0) {
+            double v = -1.0;
+            int i2 = -1, j2 = -1;
+            for (int w = 0; w < nw; ++w)
+                if (better(rv[w], ri[w], rj[w], v, i2, j2)) { v = rv[w]; i2 = ri[w]; j2 = rj[w]; }
+            bv_s = v; bi_s = i2; bj_s = j2;
+        }
+        __syncthreads();
+        if (bv_s <= thr) break;   // uniform
+        const int pi = bi_s, pj = bj_s;
+        // swap rows k, pi (all columns) and columns k, pj (all rows)
+        if (pi != k)
+            for (int j = tid; j < n; j += nt) {
+                const double t = A[k + (int64_t)j * n];
+                A[k + (int64_t)j * n] = A[pi + (int64_t)j * n];
+                A[pi + (int64_t)j * n] = t;
+            }
+        __syncthreads();
+        if (pj != k)
+            for (int i = tid; i < n; i += nt) {
+                const double t = A[i + (int64_t)k * n];
+                A[i + (int64_t)k * n] = A[i + (int64_t)pj * n];
+                A[i + (int64_t)pj * n] = t;
+            }
+        if (tid == 0) {
+            const int a = prow[k]; prow[k] = prow[pi]; prow[pi] = a;
+            const int b = pcol[k]; pcol[k] = pcol[pj]; pcol[pj] = b;
+        }
+        __syncthreads();
+        const double d = A[k + (int64_t)k * n];
+        for (int i = k + 1 + tid; i < n; i += nt) A[i + (int64_t)k * n] = A[i + (int64_t)k * n] / d;   // L column
+        __syncthreads();
+        for (int64_t e = tid; e < (int64_t)(n - k - 1) * (n - k - 1); e += nt) {
+            const int i = k + 1 + (int)(e % (n - k - 1)), j = k + 1 + (int)(e / (n - k - 1));
+            A[i + (int64_t)j * n] = fma(-A[i + (int64_t)k * n], A[k + (int64_t)j * n], A[i + (int64_t)j * n]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *rank_out = k;
+}
+
+// x = S^+ y on the factored part: z = y[prow], L z' = z (r x r), U v = z', x[pcol[:r]] = v, 0 elsewhere
+__global__ void k_hard_lu_solve(int n, int64_t r, const double *__restrict__ A, const int32_t *__restrict__ prow,
+                                const int32_t *__restrict__ pcol, const double *__restrict__ y, double *x, double *z) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < n; i += nt) {
+        z[i] = y[prow[i]];
+        x[i] = 0.0;
+    }
+    __syncthreads();
+    for (int64_t k = 0; k < r; ++k) {          // forward, unit lower
+        const double zk = z[k];
+        for (int64_t i = k + 1 + tid; i < r; i += nt) z[i] -= A[i + k * n] * zk;
+        __syncthreads();
+    }
+    for (int64_t k = r - 1; k >= 0; --k) {     // backward, upper
+        if (tid == 0) z[k] = z[k] / A[k + k * n];
+        __syncthreads();
+        const double zk = z[k];
+        for (int64_t i = tid; i < k; i += nt) z[i] -= A[i + k * n] * zk;
+        __syncthreads();
+    }
+    for (int64_t i = tid; i < r; i += nt) x[pcol[i]] = z[i];
+}
+
 // K22[a + b*n2] = K[lam2[a] + lam2[b]*ld]
 __global__ void k_gather_k22(int64_t n2, const double *__restrict__ K, int64_t ld, const int64_t *__restrict__ lam2,
                              double *__restrict__ K22) {
@@ -632,6 +747,24 @@ void gather_K12(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const int64
     ClassTimer tm_(ctx, "other");
     dim3 g((unsigned)std::min<int64_t>(cdiv(L, 256), 64), (unsigned)std::min<int64_t>(n2, 65535));
     k_gather_cols<<<g, 256, 0, ctx->stream>>>(L, K, ld, lam2, n2, mask1, B);
+    HF_CHECK_LAUNCH(ctx);
+}
+void gather_K21T(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const int64_t *lam2, int64_t n2,
+                 const uint8_t *mask1, double *B) {
+    ClassTimer tm_(ctx, "other");
+    dim3 g((unsigned)std::min<int64_t>(cdiv(L, 256), 64), (unsigned)std::min<int64_t>(n2, 65535));
+    k_gather_rows_t<<<g, 256, 0, ctx->stream>>>(L, K, ld, lam2, n2, mask1, B);
+    HF_CHECK_LAUNCH(ctx);
+}
+void hard_lu(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A, int32_t *prow, int32_t *pcol,
+             int64_t *rank_dev) {
+    ClassTimer tm(ctx, "hard");
+    k_hard_lu<<<1, 1024, 0, ctx->stream>>>((int)n, S, thr, A, prow, pcol, rank_dev);
+    HF_CHECK_LAUNCH(ctx);
+}
+void hard_lu_solve(hf_ctx *ctx, int64_t n, int64_t r, const double *A, const int32_t *prow, const int32_t *pcol,
+                   const double *y, double *x, double *z) {
+    k_hard_lu_solve<<<1, 256, 0, ctx->stream>>>((int)n, r, A, prow, pcol, y, x, z);
     HF_CHECK_LAUNCH(ctx);
 }
 void gather_K22(hf_ctx *ctx, int64_t n2, const double *K, int64_t ld, const int64_t *lam2, double *K22) {

@@ -6,6 +6,13 @@ namespace hf {
 void gather_K12(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const int64_t *lam2, int64_t n2,
                 const uint8_t *mask1, double *B);
 void gather_K22(hf_ctx *ctx, int64_t n2, const double *K, int64_t ld, const int64_t *lam2, double *K22);
+// NEXT-3 (nonsymmetric): K21^T gather, LU with complete pivoting of S22 and its solve
+void gather_K21T(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const int64_t *lam2, int64_t n2,
+                 const uint8_t *mask1, double *B);
+void hard_lu(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A, int32_t *prow, int32_t *pcol,
+             int64_t *rank_dev);
+void hard_lu_solve(hf_ctx *ctx, int64_t n, int64_t r, const double *A, const int32_t *prow, const int32_t *pcol,
+                   const double *y, double *x, double *z);
 void mask_from_pos(hf_ctx *ctx, int64_t L, const int32_t *pos1, uint8_t *m);
 void colnorm2(hf_ctx *ctx, int64_t M, int64_t ncol, const double *X, int64_t ldx, double *out);
 void maxres(hf_ctx *ctx, int64_t n, const double *rn2, const double *bn2, double *out);

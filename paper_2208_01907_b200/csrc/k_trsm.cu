@@ -153,7 +153,8 @@ void precond_setup(hf_ctx *ctx, Precond &p, const hf_lowfactor *lf) {
     if (lf->prec == 64)
         p64::precond_setup_t(ctx, p.d, lf->N, lf->L, lf->Lfac64.p, lf->D64.p, lf->perm.p, lf->pos1.p);
     else
-        p32::precond_setup_t(ctx, p.f, lf->N, lf->L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        p32::precond_setup_t(ctx, p.f, lf->N, lf->L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p,
+                             lf->nonsym ? lf->Ufac.p : nullptr);
 }
 
 void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64_t ldr, double *W, int64_t ldw) {

@@ -564,8 +564,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
 }
 
 // ------------------------------------------------------------------ host side
+// Ufac != null (NEXT-3, nonsymmetric LDU): the backward operator is U = Ufac^T
+// instead of L^T, and its diagonal-block inverses come from Ufac.
 void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T *Lfac, const T *D,
-                   const int64_t *perm, const int32_t *pos1) {
+                   const int64_t *perm, const int32_t *pos1, const T *Ufac = nullptr) {
     p.N = N;
     p.L = L;
     p.Lfac = Lfac;
@@ -582,8 +584,19 @@ void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T 
     p.LinvB.alloc((size_t)nblk * TILE, st);
     ClassTimer tm(ctx, "trsm");
     dim3 g((unsigned)(p.Np / 32), (unsigned)(p.Np / 32));
-    k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Lfac, p.Lp.p, p.Up.p);
-    HF_CHECK_LAUNCH(ctx);
+    DBuf<T> Ulp, Ltr, scr;   // nonsymmetric only: Ufac padded, a discarded transpose / inverse
+    if (!Ufac) {
+        k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Lfac, p.Lp.p, p.Up.p);
+        HF_CHECK_LAUNCH(ctx);
+    } else {
+        Ulp.alloc((size_t)p.Np * p.Np, st);
+        Ltr.alloc((size_t)p.Np * p.Np, st);
+        k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Lfac, p.Lp.p, Ltr.p);
+        HF_CHECK_LAUNCH(ctx);
+        k_pad_transpose<<<g, 256, 0, st>>>(N, p.Np, Ufac, Ulp.p, p.Up.p);   // Up = Ufac^T = U
+        HF_CHECK_LAUNCH(ctx);
+        Ltr.release();
+    }
     const size_t sm_inv = (size_t)2 * TBS * (TBS + 1) * sizeof(T);
     const size_t sm_sc = ((size_t)TBS * (TBS + 1) + 4 + TILE) * sizeof(T);
     static bool attr_setup = false;
@@ -593,8 +606,16 @@ void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T 
         HF_CUDA(cudaFuncSetAttribute(k_scale_op<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
         attr_setup = true;
     }
-    k_diag_inv<<<(unsigned)nblk, TBS, sm_inv, st>>>(p.Np, p.Lp.p, p.LinvF.p, p.LinvB.p);
-    HF_CHECK_LAUNCH(ctx);
+    if (!Ufac) {
+        k_diag_inv<<<(unsigned)nblk, TBS, sm_inv, st>>>(p.Np, p.Lp.p, p.LinvF.p, p.LinvB.p);
+        HF_CHECK_LAUNCH(ctx);
+    } else {
+        scr.alloc((size_t)nblk * TILE, st);
+        k_diag_inv<<<(unsigned)nblk, TBS, sm_inv, st>>>(p.Np, p.Lp.p, p.LinvF.p, scr.p);
+        HF_CHECK_LAUNCH(ctx);
+        k_diag_inv<<<(unsigned)nblk, TBS, sm_inv, st>>>(p.Np, Ulp.p, scr.p, p.LinvB.p);   // (U_bb)^{-1}
+        HF_CHECK_LAUNCH(ctx);
+    }
     // G = Dinv Op in place (after the diagonal inverses, which read the diagonal blocks only)
     dim3 gs((unsigned)nblk, (unsigned)nblk);
     k_scale_op<false><<<gs, 256, sm_sc, st>>>((int)nblk, p.Np, p.Lp.p, p.LinvF.p);

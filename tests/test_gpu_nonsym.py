@@ -9,6 +9,7 @@ import torch
 
 import hf_inputs as hi
 from hf_inputs.configs import ConfigSpec
+from oracle import core as oracle_core
 from oracle import nonsym
 
 pytestmark = pytest.mark.gpu
@@ -60,4 +61,66 @@ def test_stage1_nonsym_bitwise(ctx, name, L, seed, nb):
     assert np.array_equal(D, F.D)
     assert np.array_equal(Lf.cpu().numpy(), F.Lfac)
     assert np.array_equal(Uf.cpu().numpy(), F.Ufac)
+    lf.close()
+
+
+@pytest.mark.parametrize("name,L,seed", [("T8", None, 0), ("H8", None, 0), ("T24", None, 0), ("H8", None, 2),
+                                         ("rand", 300, 1)])
+def test_hybrid_nonsym_vs_oracle(ctx, name, L, seed):
+    """Alg. 1 steps 2-5 and Alg. 2 on the nonsymmetric path: S22 normwise ([R17] form),
+    X12, kernel dimension, manufactured solution, against oracle/nonsym.py."""
+    from paper_2208_01907_b200 import hf
+    Kbar = _kbar(name, L, seed)
+    Ko, _ = nonsym.scale_full(Kbar)
+    HF = nonsym.hybrid_factor(Ko, 1e-2, n_min=2)
+    Kd = hi.colmajor(torch.from_numpy(Kbar)).cuda()
+    hf.hf_scale_full(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=1e-2, n_min=2, nonsym=True)
+    hy, info, S22 = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
+    F = HF.F
+    l1, l2 = F.lam1, F.lam2
+    K21, K22 = Ko[np.ix_(l2, l1)], Ko[np.ix_(l2, l2)]
+    den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
+    assert np.linalg.norm(S22 - HF.S22) / den <= 1e-10
+    X, _ = hy.export()
+    assert np.abs(X.cpu().numpy() - HF.X).max() <= 1e-8 * max(1.0, np.abs(HF.X).max())
+    assert info.max_rel_res_true <= 1e-12
+    kd = hf.hf_factor_hard(ctx, hy, eps_ker=1e-10)
+    margin = min(abs(np.array(HF.H.mu_hist) - HF.H.thr)) if HF.H is not None else 1.0
+    if margin > 10 * np.linalg.norm(S22 - HF.S22):
+        assert kd == HF.kernel_dim
+    xs = hi.manufactured_x(lf.L).numpy()
+    b = Ko @ xs
+    x, _ = hf.hf_solve(ctx, hy, torch.from_numpy(b).cuda())
+    xg = x.cpu().numpy()
+    assert np.abs(Ko @ xg - b).max() <= 1e-12 * np.abs(b).max()
+    xo, _ = nonsym.hybrid_solve(HF, b)
+    assert np.abs(Ko @ xo - b).max() <= 1e-12 * np.abs(b).max()
+    hy.close()
+    lf.close()
+
+
+def test_precond_nonsym_vs_oracle(ctx):
+    """Q^{-1} = U^{-1} D^{-1} L^{-1} in FP32 against the oracle's FP32 solves."""
+    from paper_2208_01907_b200 import hf
+    Kbar = _kbar("rand", 700, 2)
+    Ko, _ = nonsym.scale_full(Kbar)
+    F = nonsym.factor_ldu(Ko, 1e-2, n_min=2)
+    Kd = hi.colmajor(torch.from_numpy(Kbar)).cuda()
+    hf.hf_scale_full(ctx, Kd)
+    lf = hf.hf_factor_lowprec(ctx, Kd, tau=1e-2, n_min=2, nonsym=True)
+    rng = np.random.default_rng(0)
+    R = rng.standard_normal((lf.L, 5))
+    R[F.lam2] = 0.0
+    W = hf.hf_precond_apply(ctx, lf, torch.from_numpy(R.T.copy()).cuda().T)
+    Wg = W.cpu().numpy()
+    Wo = np.zeros_like(R)
+    Wo[F.lam1] = oracle_core.precond_apply(F, R[F.lam1])
+    # both are FP32 solves of the same FP32 factors: agree to the FP32 error level of the solve
+    eps32 = float(np.finfo(np.float32).eps)
+    K11 = Ko[np.ix_(F.lam1, F.lam1)]
+    exact = np.linalg.solve(K11, R[F.lam1])
+    e_o = np.abs(Wo[F.lam1] - exact).max()
+    e_g = np.abs(Wg[F.lam1] - exact).max()
+    assert e_g <= max(10 * e_o, 100 * eps32 * np.abs(exact).max())
     lf.close()
