@@ -211,7 +211,8 @@ hf_status hf_hybrid_export(hf_ctx *ctx, const hf_hybrid *hy, double *X, int64_t 
  * the per-column recursive ||r||/||b|| target (default 1e-28).  S22hi/lo_host:
  * n2 x n2 column-major (S22 = hi + lo exactly).  The returned hybrid is a
  * double-double one: hf_factor_hard factors S22 in double-double (same rule
- * as below), hf_hard_export works, hf_solve returns HF_ERR_STATE.  One rank
+ * as below), hf_hard_export works, hf_solve_dd solves (hf_solve returns
+ * HF_ERR_STATE).  One rank
  * only (HF_ERR_INVALID_ARG on a distributed or virtual-rank context). */
 hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfactor *lf,
                           const hf_gcr_opts *opts, hf_hybrid **out, double *S22hi_host_or_null,
@@ -221,6 +222,12 @@ hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
  * HF_ERR_STATE on a double hybrid. */
 hf_status hf_hybrid_export_dd(hf_ctx *ctx, const hf_hybrid *hy, double *Xhi, double *Xlo, int64_t ldx,
                               double *S22hi, double *S22lo, int64_t lds);
+/* Alg. 2 in double-double on a double-double hybrid after
+ * hf_factor_hard: b DEVICE FP64[L] (scaled system, original order), x = xhi + xlo
+ * DEVICE FP64[L] each; block GCR tolerance 1e-28; kernel coordinates 0 [R16].
+ * HF_ERR_STATE on a double hybrid or before hf_factor_hard. */
+hf_status hf_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *xhi, double *xlo,
+                      hf_gcr_info *info_host);
 
 /* ---------------------------- a7: hard factorization, P:192, P:84 [R15] */
 /* FP64 Bunch-Parlett (complete pivoting, alpha = (1+sqrt17)/8) LDL^T of

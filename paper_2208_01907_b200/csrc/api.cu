@@ -346,6 +346,20 @@ hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
     return s;
 }
 
+hf_status hf_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *xhi, double *xlo,
+                      hf_gcr_info *info_host) {
+    if (!ctx || !hy || !b || !xhi || !xlo) return HF_ERR_INVALID_ARG;
+    hf_gcr_info info{0, 0.0, 0.0};
+    hf_status s = guarded(ctx, [&] {
+        if (!hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: not a double-double hybrid"};
+        if (!hy->hard_done && hy->n2 > 0) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: call hf_factor_hard first"};
+        hf_gcr_opts o{1e-28, 100};
+        hf::hybrid_solve_dd(ctx, hy, b, xhi, xlo, o, &info);
+    });
+    if (info_host) *info_host = info;
+    return s;
+}
+
 hf_status hf_hybrid_export_dd(hf_ctx *ctx, const hf_hybrid *hy, double *Xhi, double *Xlo, int64_t ldx,
                               double *S22hi, double *S22lo, int64_t lds) {
     if (!ctx || !hy) return HF_ERR_INVALID_ARG;
@@ -397,7 +411,7 @@ hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x,
     hf_status s = guarded(ctx, [&] {
         if (!hy->hard_done && hy->n2 > 0)
             throw hf::Error{HF_ERR_STATE, "hf_solve: call hf_factor_hard first"};
-        if (hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve: not available for a double-double hybrid"};
+        if (hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve: a double-double hybrid is solved by hf_solve_dd"};
         hf_gcr_opts o{1e-14, 100};
         hf::hybrid_solve(ctx, hy, b, x, o, &info);
     });

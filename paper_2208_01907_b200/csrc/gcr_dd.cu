@@ -320,14 +320,16 @@ __global__ void k_dd_copy(int64_t n, const double *sh, const double *sl, double 
 // ties to the smallest (label) pair -- the FP64 kernel's rule.  Outputs the rank
 // and the pivot sequence (labels, block sizes).
 __global__ void __launch_bounds__(1024) k_dd_hard(int n, const double *Sh, const double *Sl, double thr, double *Ah,
-                                                  double *Al, int32_t *act, int32_t *pivots, int32_t *blocks,
-                                                  int64_t *rank_out) {
+                                                  double *Al, double *Lch, double *Lcl, int32_t *act, int32_t *pivots,
+                                                  int32_t *blocks, int64_t *rank_out) {
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int64_t e = tid; e < (int64_t)n * n; e += nt) {
         const int64_t i = e % n, j = e / n;
         const dd v = dd_mul({0.5, 0.0}, dd_add({Sh[i + j * n], Sl[i + j * n]}, {Sh[j + i * n], Sl[j + i * n]}));
         Ah[e] = v.hi;
         Al[e] = v.lo;
+        Lch[e] = 0.0;
+        Lcl[e] = 0.0;
     }
     for (int i = tid; i < n; i += nt) {
         act[i] = 1;
@@ -393,6 +395,12 @@ __global__ void __launch_bounds__(1024) k_dd_hard(int n, const double *Sh, const
                 Ah[e] = v.hi;
                 Al[e] = v.lo;
             }
+            for (int i = tid; i < n; i += nt)   // L column (label space): l_ip = A_ip / d
+                if (act[i] && i != p) {
+                    const dd l = dd_div({Ah[i + (int64_t)p * n], Al[i + (int64_t)p * n]}, d);
+                    Lch[i + (int64_t)p * n] = l.hi;
+                    Lcl[i + (int64_t)p * n] = l.lo;
+                }
             __syncthreads();
             if (tid == 0) {
                 act[p] = 0;
@@ -418,6 +426,16 @@ __global__ void __launch_bounds__(1024) k_dd_hard(int n, const double *Sh, const
                 Ah[e] = v.hi;
                 Al[e] = v.lo;
             }
+            for (int i = tid; i < n; i += nt)   // the two L columns: [l0 l1] = [A_ip A_iq] E^{-1}
+                if (act[i] && i != p && i != q) {
+                    const dd aip{Ah[i + (int64_t)p * n], Al[i + (int64_t)p * n]}, aiq{Ah[i + (int64_t)q * n], Al[i + (int64_t)q * n]};
+                    const dd l0 = dd_div(dd_sub(dd_mul(aip, c_), dd_mul(aiq, b_)), det);
+                    const dd l1 = dd_div(dd_sub(dd_mul(aiq, a_), dd_mul(aip, b_)), det);
+                    Lch[i + (int64_t)p * n] = l0.hi;
+                    Lcl[i + (int64_t)p * n] = l0.lo;
+                    Lch[i + (int64_t)q * n] = l1.hi;
+                    Lcl[i + (int64_t)q * n] = l1.lo;
+                }
             __syncthreads();
             if (tid == 0) {
                 act[p] = act[q] = 0;
@@ -431,6 +449,101 @@ __global__ void __launch_bounds__(1024) k_dd_hard(int n, const double *Sh, const
         __syncthreads();
     }
     if (tid == 0) *rank_out = k;
+}
+
+// x = S22^+ y in double-double with the factors of k_dd_hard (label space: D blocks at
+// A[p, p] / A[q, p] / A[q, q], L columns in Lc), kernel coordinates 0 [R16]; one CTA.
+__global__ void __launch_bounds__(256) k_dd_hard_solve(int n, int64_t r, const double *Ah, const double *Al,
+                                                       const double *Lch, const double *Lcl, const int32_t *pivots,
+                                                       const int32_t *blocks, const double *yh, const double *yl,
+                                                       double *xh, double *xl, int32_t *act) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ double rh[256], rl[256];
+    for (int i = tid; i < n; i += nt) {
+        xh[i] = yh[i];
+        xl[i] = yl ? yl[i] : 0.0;
+        act[i] = 1;
+    }
+    __syncthreads();
+    // forward: z_i -= l_ip z_p (pivot blocks in order)
+    for (int64_t k = 0, b = 0; k < r; ++b) {
+        const int bs = blocks[b];
+        const int p = pivots[k], q = bs == 2 ? pivots[k + 1] : -1;
+        const dd zp{xh[p], xl[p]}, zq = q >= 0 ? dd{xh[q], xl[q]} : dd{0.0, 0.0};
+        __syncthreads();
+        for (int i = tid; i < n; i += nt) {
+            if (!act[i] || i == p || i == q) continue;
+            dd v = dd_mul({Lch[i + (int64_t)p * n], Lcl[i + (int64_t)p * n]}, zp);
+            if (q >= 0) v = dd_add(v, dd_mul({Lch[i + (int64_t)q * n], Lcl[i + (int64_t)q * n]}, zq));
+            const dd z = dd_sub({xh[i], xl[i]}, v);
+            xh[i] = z.hi;
+            xl[i] = z.lo;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            act[p] = 0;
+            if (q >= 0) act[q] = 0;
+        }
+        __syncthreads();
+        k += bs;
+    }
+    // block diagonal, then kernel coordinates 0
+    if (tid == 0) {
+        for (int64_t k = 0, b = 0; k < r; ++b) {
+            const int bs = blocks[b];
+            const int p = pivots[k];
+            if (bs == 1) {
+                const dd z = dd_div({xh[p], xl[p]}, {Ah[p + (int64_t)p * n], Al[p + (int64_t)p * n]});
+                xh[p] = z.hi;
+                xl[p] = z.lo;
+            } else {
+                const int q = pivots[k + 1];
+                const dd a_{Ah[p + (int64_t)p * n], Al[p + (int64_t)p * n]}, b_{Ah[q + (int64_t)p * n], Al[q + (int64_t)p * n]},
+                    c_{Ah[q + (int64_t)q * n], Al[q + (int64_t)q * n]};
+                const dd det = dd_sub(dd_mul(a_, c_), dd_mul(b_, b_));
+                const dd z0{xh[p], xl[p]}, z1{xh[q], xl[q]};
+                const dd w0 = dd_div(dd_sub(dd_mul(c_, z0), dd_mul(b_, z1)), det);
+                const dd w1 = dd_div(dd_sub(dd_mul(a_, z1), dd_mul(b_, z0)), det);
+                xh[p] = w0.hi; xl[p] = w0.lo;
+                xh[q] = w1.hi; xl[q] = w1.lo;
+            }
+            k += bs;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += nt)
+        if (act[i]) {   // never pivoted: kernel coordinate
+            xh[i] = 0.0;
+            xl[i] = 0.0;
+        }
+    __syncthreads();
+    // backward: z_p -= sum_i l_ip z_i over the rows eliminated after p (blocks in reverse)
+    int64_t nb = 0;
+    for (int64_t k = 0; k < r; ++nb) k += blocks[nb];
+    for (int64_t b = nb - 1, k = r; b >= 0; --b) {
+        const int bs = blocks[b];
+        k -= bs;
+        for (int c = 0; c < bs; ++c) {
+            const int p = pivots[k + c];
+            // rows after the block: every i whose L entry in column p is set (zero elsewhere)
+            dd s{0.0, 0.0};
+            for (int i = tid; i < n; i += nt) {
+                const dd l{Lch[i + (int64_t)p * n], Lcl[i + (int64_t)p * n]};
+                if (l.hi != 0.0 || l.lo != 0.0) s = dd_add(s, dd_mul(l, {xh[i], xl[i]}));
+            }
+            rh[tid] = s.hi;
+            rl[tid] = s.lo;
+            __syncthreads();
+            if (tid == 0) {
+                dd t{0.0, 0.0};
+                for (int w = 0; w < nt; ++w) t = dd_add(t, {rh[w], rl[w]});
+                const dd z = dd_sub({xh[p], xl[p]}, t);
+                xh[p] = z.hi;
+                xl[p] = z.lo;
+            }
+            __syncthreads();
+        }
+    }
 }
 
 // ------------------------------------------------------------------ Alg. 5 in dd
@@ -639,17 +752,20 @@ void factor_hard_dd(hf_ctx *ctx, hf_hybrid *hy, double eps_ker) {
     }
     hy->perm2.alloc(n2, st);
     hy->blocks.alloc(n2, st);
-    DBuf<double> Ah, Al;
-    Ah.alloc((size_t)n2 * n2, st);
-    Al.alloc((size_t)n2 * n2, st);
+    HF_CUDA(cudaMemsetAsync(hy->blocks.p, 0, n2 * sizeof(int32_t), st));
+    const size_t nn = (size_t)n2 * n2;
+    hy->Dh.alloc(nn, st);      // the eliminated matrix (D blocks at the pivot entries), hi
+    hy->Dhlo.alloc(nn, st);
+    hy->Lh.alloc(nn, st);      // L columns in label space, hi
+    hy->Lhlo.alloc(nn, st);
     DBuf<int32_t> act;
     act.alloc(n2, st);
     DBuf<int64_t> rk;
     rk.alloc(1, st);
     {
         ClassTimer tm(ctx, "hard");
-        k_dd_hard<<<1, 1024, 0, st>>>((int)n2, hy->S22.p, hy->S22lo.p, eps_ker * dref, Ah.p, Al.p, act.p, hy->perm2.p,
-                                       hy->blocks.p, rk.p);
+        k_dd_hard<<<1, 1024, 0, st>>>((int)n2, hy->S22.p, hy->S22lo.p, eps_ker * dref, hy->Dh.p, hy->Dhlo.p, hy->Lh.p,
+                                       hy->Lhlo.p, act.p, hy->perm2.p, hy->blocks.p, rk.p);
         HF_CHECK_LAUNCH(ctx);
     }
     int64_t r = 0;
@@ -658,6 +774,47 @@ void factor_hard_dd(hf_ctx *ctx, hf_hybrid *hy, double eps_ker) {
     hy->rank = r;
     hy->kernel_dim = n2 - r;
     hy->hard_done = true;
+}
+
+// ------------------------------------------------------------------ Alg. 2 in dd
+// The scaled system K x = b (b double, original order) solved in double-double:
+// y1 = K11^{-1} b1 (dd block GCR, one column), y2 = b2 - K21 y1, x2 = S22^+ y2 (dd
+// Bunch-Parlett factors, kernel coordinates 0 [R16]), x1 = y1 - X12 x2; x = hi + lo.
+void hybrid_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *xh, double *xl,
+                     const hf_gcr_opts &o, hf_gcr_info *info) {
+    cudaStream_t st = ctx->stream;
+    const int64_t L = hy->L, N = hy->N, n2 = hy->n2;
+    info->iters = 0;
+    info->max_rel_res_recursive = info->max_rel_res_true = 0.0;
+    if (L == 0) return;
+    DBuf<double> bm, y2h, y2l, x2h, x2l;
+    GcrDD g;
+    if (N > 0) {
+        bm.alloc(L, st);
+        mask_vec(ctx, L, hy->mask1.p, b, bm.p);
+        block_gcr_dd(ctx, hy->K, hy->ld, L, hy->mask1.p, hy->pc, bm.p, 1, xh, xl, o, info, g);   // step 1
+    } else {
+        HF_CUDA(cudaMemsetAsync(xh, 0, L * sizeof(double), st));
+        HF_CUDA(cudaMemsetAsync(xl, 0, L * sizeof(double), st));
+    }
+    if (n2 > 0) {
+        y2h.alloc(n2, st);
+        y2l.alloc(n2, st);
+        x2h.alloc(n2, st);
+        x2l.alloc(n2, st);
+        gather_rows(ctx, n2, hy->lam2.p, b, y2h.p);
+        HF_CUDA(cudaMemsetAsync(y2l.p, 0, n2 * sizeof(double), st));
+        ddgemm(ctx, true, n2, 1, L, -1.0, hy->B.p, nullptr, L, xh, xl, L, true, y2h.p, y2l.p, n2, nullptr, g.w);  // step 2
+        DBuf<int32_t> act;
+        act.alloc(n2, st);
+        k_dd_hard_solve<<<1, 256, 0, st>>>((int)n2, hy->rank, hy->Dh.p, hy->Dhlo.p, hy->Lh.p, hy->Lhlo.p,
+                                           hy->perm2.p, hy->blocks.p, y2h.p, y2l.p, x2h.p, x2l.p, act.p);   // step 3
+        HF_CHECK_LAUNCH(ctx);
+        ddgemm(ctx, false, L, 1, n2, -1.0, hy->X.p, hy->Xlo.p, L, x2h.p, x2l.p, n2, true, xh, xl, L, nullptr, g.w);   // step 4
+        scatter_rows(ctx, n2, hy->lam2.p, x2h.p, xh);
+        scatter_rows(ctx, n2, hy->lam2.p, x2l.p, xl);
+    }
+    HF_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace hf

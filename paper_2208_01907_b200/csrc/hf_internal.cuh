@@ -225,7 +225,7 @@ struct hf_hybrid {
     hf::DBuf<double> B2;               // L x n2: K21^T (original row order, zero on Lambda_2 rows)
     hf::DBuf<double> LUh;              // n2 x n2: [L \ U] of P S22 Q
     hf::DBuf<int32_t> pcol2;           // [n2] column pivot labels (perm2 holds the row labels)
-    hf::DBuf<double> Xlo, S22lo;
+    hf::DBuf<double> Xlo, S22lo, Lhlo, Dhlo;   // dd: lo parts (Lh / Dh hold the hi parts)
     hf::DBuf<int64_t> lam2;            // [n2] original indices (ascending)
     hf::DBuf<uint8_t> mask1;           // [L] 1 on Lambda_1 rows
     // stage 3
@@ -256,6 +256,8 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void schur_gcr_dd(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);   // gcr_dd.cu
 void factor_hard_dd(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
+void hybrid_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *xh, double *xl,
+                     const hf_gcr_opts &o, hf_gcr_info *info);
 void hybrid_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, const hf_gcr_opts &o,
                   hf_gcr_info *info);
 // multi-GPU plumbing (dist.cu)

@@ -30,7 +30,7 @@ EXPORTED = [
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
     "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64", "hf_schur_gcr_dd",
-    "hf_hybrid_export_dd", "hf_lowfactor_export_u", "hf_scale_full",
+    "hf_hybrid_export_dd", "hf_lowfactor_export_u", "hf_scale_full", "hf_solve_dd",
 ]
 
 
@@ -89,6 +89,7 @@ def load() -> ctypes.CDLL:
         "hf_schur_gcr_dd": [vp, vp, i64, vp, ctypes.POINTER(gcr_opts), ctypes.POINTER(vp), vp, vp,
                             ctypes.POINTER(gcr_info)],
         "hf_hybrid_export_dd": [vp, vp, vp, vp, i64, vp, vp, i64],
+        "hf_solve_dd": [vp, vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
         "hf_factor_hard": [vp, vp, dbl, pi64],
         "hf_hard_export": [vp, vp, vp, vp, pi64],
         "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
@@ -450,3 +451,13 @@ def hf_solve(ctx: Context, hy: Hybrid, b: torch.Tensor, x: torch.Tensor | None =
     info = gcr_info()
     ctx.check(ctx.lib.hf_solve(ctx.h, hy.h, _ptr(b), _ptr(x), ctypes.byref(info)))
     return x, GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true)
+
+
+def hf_solve_dd(ctx: Context, hy: Hybrid, b: torch.Tensor):
+    """NEXT-1: Alg. 2 in double-double on a double-double hybrid.  Returns (xhi, xlo, GcrInfo)."""
+    _dev(b, torch.float64)
+    xh = torch.empty_like(b)
+    xl = torch.empty_like(b)
+    info = gcr_info()
+    ctx.check(ctx.lib.hf_solve_dd(ctx.h, hy.h, _ptr(b), _ptr(xh), _ptr(xl), ctypes.byref(info)))
+    return xh, xl, GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true)

@@ -92,7 +92,7 @@ def test_dd_requires_fp64_factor(ctx):
     lf.close()
 
 
-def test_dd_solve_is_refused(ctx):
+def test_dd_solve_is_refused_by_the_double_entry(ctx):
     from paper_2208_01907_b200 import hf
     K, lf, hy, info, S = _run(ctx, CASES["P48"], 0)
     hf.hf_factor_hard(ctx, hy, eps_ker=1e-20)
@@ -100,5 +100,43 @@ def test_dd_solve_is_refused(ctx):
     with pytest.raises(hf.HFError) as e:
         hf.hf_solve(ctx, hy, b)
     assert e.value.status == hf.HF_ERR_STATE
+    hy.close()
+    lf.close()
+
+
+@pytest.mark.parametrize("name,seed", [("P48", 0), ("P64", 0), ("S4", 0), ("N8", 0)])
+def test_dd_solve_exact_residual(ctx, name, seed):
+    """Alg. 2 in double-double: the residual b - K x evaluated EXACTLY (Fractions), b = K x*
+    with x*_i = i mod 11.  Bar: max |b - K x| / max |b| <= 1e-26 (the block-GCR
+    tolerance 1e-28 times the size of b); the FP64 path's exact residual is reported beside
+    it and must be >= 1e6 times larger unless itself below the bar.  (The FORWARD error is
+    kappa(K) times this -- up to 1e13 on the planted cases -- so it is not the bar.)"""
+    from fractions import Fraction
+    from paper_2208_01907_b200 import hf
+    spec = CASES[name]
+    K, lf, hy, info, S = _run(ctx, spec, seed)
+    hf.hf_factor_hard(ctx, hy, eps_ker=1e-20)
+    Kh = K.cpu().numpy()
+    L = Kh.shape[0]
+    xs = hi.manufactured_x(L).numpy()
+    b = Kh @ xs
+    F = exact.to_fractions(Kh)
+    bf = [Fraction(float(v)) for v in b]
+
+    def exact_res(x):
+        return float(max(abs(bf[i] - sum((F[i][j] * x[j] for j in range(L)), Fraction(0))) for i in range(L))
+                     / max(abs(v) for v in bf))
+
+    xh, xl, sinfo = hf.hf_solve_dd(ctx, hy, torch.from_numpy(b).cuda())
+    xh, xl = xh.cpu().numpy(), xl.cpu().numpy()
+    res_dd = exact_res([Fraction(float(xh[i])) + Fraction(float(xl[i])) for i in range(L)])
+    assert res_dd <= 1e-26, res_dd
+    hy64, _, _ = hf.hf_schur_gcr(ctx, K, lf)
+    hf.hf_factor_hard(ctx, hy64, eps_ker=1e-10)
+    x64, _ = hf.hf_solve(ctx, hy64, torch.from_numpy(b).cuda())
+    x64 = x64.cpu().numpy()
+    res_64 = exact_res([Fraction(float(x64[i])) for i in range(L)])
+    assert res_64 <= 1e-26 or res_64 >= 1e6 * res_dd, (res_dd, res_64)
+    hy64.close()
     hy.close()
     lf.close()
