@@ -294,3 +294,104 @@ int oracle_ldu_f32(int64_t L, const double *K, int64_t ld, double tau, int64_t n
     free(A); free(l); free(r); free(orig);
     return 0;
 }
+
+/* ========================================================================= */
+/* NEXT-4: multi-block threshold postponing (sec. 2.2,  */
+/* P:69-85).  The indices are split into blocks in elimination-tree order    */
+/* (blk[original index] = block number 0..nblk-1, e.g. the post-order of a   */
+/* nested-dissection tree).  "During the LDU-factorization of the sub- */
+/* matrix with index Lambda_j, if |K_{i+1,i+1}/K_ii| < tau, then the lower   */
+/* block of the matrix is not factorized": the pivots of block j are  */
+/* chosen among ITS remaining indices only (max |diag|, ties -> smallest     */
+/* original index [R3]), the ratio test compares successive pivots of the    */
+/* same block, a block's first pivot is only tested against 0; the rest of a */
+/* stopped block is postponed to Lambda_0.  "At the end of all threshold     */
+/* factorization following the elimination tree, we will again apply the     */
+/* LDU-factorization to the last Schur complement with indices Lambda_0"     */
+/* (P:80): a final pass over every remaining index with the same rules; its  */
+/* tau-stop ends the factorization (Ntau).  Floor [R5] and the enlargement   */
+/* by n_extra entries ("usually n = 4") as in oracle_factor_f32.       */
+/* Arithmetic exactly [R2]-[R10] (this function IS oracle_factor_f32 when    */
+/* nblk = 0).  Outputs as oracle_factor_f32.                                 */
+/* ========================================================================= */
+int oracle_factor_blocks_f32(int64_t L, const double *K, int64_t ld, double tau, int64_t n_min, int64_t n_extra,
+                             const int32_t *blk, int32_t nblk, int64_t *perm, float *Dk, float *Lfac, int64_t *out)
+{
+    if (L < 0 || !(tau > 0.0 && tau < 1.0) || n_min < 0 || n_extra < 0 || nblk < 0) return -1;
+    const size_t LL = (size_t)(L > 0 ? L : 1) * (size_t)(L > 0 ? L : 1);
+    float *A = (float *)malloc(LL * sizeof(float));
+    float *s = (float *)malloc((size_t)(L > 0 ? L : 1) * sizeof(float));
+    int64_t *orig = (int64_t *)malloc((size_t)(L > 0 ? L : 1) * sizeof(int64_t));
+    if (!A || !s || !orig) { free(A); free(s); free(orig); return -1; }
+    for (int64_t j = 0; j < L; ++j)
+        for (int64_t i = j; i < L; ++i) A[i + j * L] = (float)K[i + j * ld];
+    for (int64_t p = 0; p < L; ++p) orig[p] = p;
+    int64_t Ntau = L;
+    int32_t cur = 0;          /* current block; cur == nblk: the final pass over Lambda_0 */
+    int first = 1;            /* next pivot is the first of its block / pass */
+    int64_t k = 0;
+    while (k < L) {
+        int64_t best = -1;
+        for (int64_t p = k; p < L; ++p) {
+            if (cur < nblk && blk[orig[p]] != cur) continue;
+            if (best < 0) { best = p; continue; }
+            float a = fabsf(A[p + p * L]), b = fabsf(A[best + best * L]);
+            if (a > b || (a == b && orig[p] < orig[best])) best = p;
+        }
+        int fail = (best < 0);
+        float d = 0.0f;
+        if (!fail) {
+            d = A[best + best * L];
+            fail = first ? (d == 0.0f) : (fabs((double)d) < tau * fabs((double)Dk[k - 1]));
+        }
+        if (fail) {
+            if (cur < nblk) { ++cur; first = 1; continue; }   /* the rest of the block -> Lambda_0 */
+            Ntau = k;                                         /* the final pass stops */
+            break;
+        }
+        if (best != k) {   /* swap in the lower-triangle storage, exactly as oracle_factor_f32 */
+            int64_t p = best; float t;
+            for (int64_t j = 0; j < k; ++j) { t = A[k + j * L]; A[k + j * L] = A[p + j * L]; A[p + j * L] = t; }
+            t = A[k + k * L]; A[k + k * L] = A[p + p * L]; A[p + p * L] = t;
+            for (int64_t i = k + 1; i < p; ++i) { t = A[i + k * L]; A[i + k * L] = A[p + i * L]; A[p + i * L] = t; }
+            for (int64_t i = p + 1; i < L; ++i) { t = A[i + k * L]; A[i + k * L] = A[i + p * L]; A[i + p * L] = t; }
+            int64_t o = orig[k]; orig[k] = orig[p]; orig[p] = o;
+        }
+        Dk[k] = d;
+        float r = sqrtf(fabsf(d)), sg = (d > 0.0f) ? 1.0f : -1.0f;
+        for (int64_t i = k + 1; i < L; ++i) {
+            float c = A[i + k * L];
+            s[i] = c / r;
+            A[i + k * L] = c / d;
+        }
+        _Pragma("omp parallel for schedule(dynamic, 16)")
+        for (int64_t j = k + 1; j < L; ++j) {
+            float nsj = -sg * s[j];
+            float *col = A + j * L;
+            for (int64_t i = j; i < L; ++i) col[i] = fmaf(nsj, s[i], col[i]);
+        }
+        first = 0;
+        ++k;
+    }
+    int64_t N = Ntau;
+    if (L - n_min < N) N = (L - n_min > 0) ? L - n_min : 0;
+    if (N < L) N = (N - n_extra > 0) ? N - n_extra : 0;
+    for (int64_t p = 0; p < N; ++p) perm[p] = orig[p];
+    {
+        char *used = (char *)calloc((size_t)(L > 0 ? L : 1), 1);
+        if (!used) { free(A); free(s); free(orig); return -1; }
+        for (int64_t p = 0; p < N; ++p) used[orig[p]] = 1;
+        int64_t w = N;
+        for (int64_t i = 0; i < L; ++i) if (!used[i]) perm[w++] = i;
+        free(used);
+    }
+    for (int64_t j = 0; j < L; ++j)
+        for (int64_t i = 0; i < L; ++i) {
+            float v = 0.0f;
+            if (j < N && i < N) v = (i == j) ? 1.0f : ((i > j) ? A[i + j * L] : 0.0f);
+            Lfac[i + j * L] = v;
+        }
+    out[0] = N; out[1] = Ntau;
+    free(A); free(s); free(orig);
+    return 0;
+}

@@ -149,3 +149,63 @@ def left_looking_ldu(K: np.ndarray, tau: float):
         Urows.append(ur)
         done.add(best)
     return piv, D, Lcols, Urows
+
+
+def left_looking_ldlt_blocks(K: np.ndarray, tau: float, blk, nblk: int):
+    """NEXT-4 pin: the multi-block rule by left-looking exact replay: candidates of
+    the current block only (ties -> smallest original index), ratio test between
+    successive pivots of the same block / pass, a block's first pivot tested against
+    0 only, then a final pass over everything left.  Returns (pivots, D, Lcols, Ntau)."""
+    L = K.shape[0]
+    v0 = {}
+    for i in range(L):
+        for j in range(i + 1):
+            v0[(i, j)] = f32(float(np.float32(K[i, j])))
+
+    def key(i, j):
+        return (i, j) if i >= j else (j, i)
+
+    piv, D, S, sig, Lcols = [], [], [], [], []
+    done = set()
+
+    def entry(i, j, k):
+        v = v0[key(i, j)]
+        for t in range(k):
+            v = fmaf_exact(-sig[t] * S[t][i], S[t][j], v)
+        return v
+
+    cur, first, k = 0, True, 0
+    Ntau = L
+    while k < L:
+        cands = [i for i in range(L) if i not in done and (cur >= nblk or blk[i] == cur)]
+        best, bd = None, None
+        for i in cands:
+            d = entry(i, i, k)
+            if best is None or abs(d) > abs(bd):
+                best, bd = i, d
+        fail = best is None or (bd == 0.0 if first else abs(float(bd)) < tau * abs(float(D[-1])))
+        if fail:
+            if cur < nblk:
+                cur, first = cur + 1, True
+                continue
+            Ntau = k
+            break
+        d = bd
+        r = f32(math.sqrt(abs(d)))
+        sg = 1.0 if d > 0 else -1.0
+        s, lc = {}, {}
+        for i in range(L):
+            if i in done or i == best:
+                continue
+            c = entry(i, best, k)
+            s[i] = f32(c / r)
+            lc[i] = f32(c / d)
+        piv.append(best)
+        D.append(d)
+        S.append(s)
+        sig.append(sg)
+        Lcols.append(lc)
+        done.add(best)
+        first = False
+        k += 1
+    return piv, D, Lcols, Ntau
