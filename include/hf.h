@@ -148,6 +148,27 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
 hf_status hf_lowfactor_export64(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm_host,
                                 double *D_host, double *Lfac, int64_t ldl);
 hf_status hf_lowfactor_destroy(hf_lowfactor *lf);
+/* ----------- NEXT-4: multi-block threshold postponing, sec. 2.2 */
+/* Nested-dissection blocks of the symmetric sparsity pattern of K (DEVICE,
+ * column-major, only K_ij != 0 is used): an m-level bisection tree (P:70,
+ * 2^m - 1 blocks when every level splits), recursive level-structure
+ * bisection (rule in nd.cu), blocks in post-order (children before their
+ * separator).  blk_host[L] = block of every index, *nblk_host = count.
+ * Synchronises. */
+hf_status hf_nd_blocks(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, int32_t levels, int32_t min_size,
+                       int32_t *blk_host, int32_t *nblk_host);
+/* Stage 1 with multi-block postponing: blocks 0..nblk-1 in order, the pivots of
+ * block j chosen among its remaining indices (rule [R3]), the ratio test [R4]
+ * against the previously accepted pivot (across blocks, [R21]; the very first
+ * pivot only against 0), the rest of a stopped block postponed to Lambda_0; then a final
+ * pass over every remaining index with the same rules, whose stop is
+ * N_tau; floor and enlargement (opts n_min, n_extra; "usually n = 4") as
+ * hf_factor_lowprec.  nblk = 0: exactly hf_factor_lowprec.  FP32 symmetric,
+ * one GPU.  blk_host: HOST int32[L], values in [0, nblk). */
+hf_status hf_factor_lowprec_blocks(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts *opts,
+                                   const int32_t *blk_host, int32_t nblk, hf_lowfactor **out, int64_t *N_host,
+                                   int64_t *n2_host, int64_t *n2_tau_only_host);
+
 /* NEXT-3: the unit upper factor U of a nonsymmetric LDU as Ufac = U^T (N x N,
  * DEVICE, ldu >= N, pivot order): Ufac[i + k ldu] = U_ki.  HF_ERR_STATE on a
  * symmetric factor. */

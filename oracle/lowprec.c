@@ -303,9 +303,11 @@ int oracle_ldu_f32(int64_t L, const double *K, int64_t ld, double tau, int64_t n
 /* matrix with index Lambda_j, if |K_{i+1,i+1}/K_ii| < tau, then the lower   */
 /* block of the matrix is not factorized": the pivots of block j are  */
 /* chosen among ITS remaining indices only (max |diag|, ties -> smallest     */
-/* original index [R3]), the ratio test compares successive pivots of the    */
-/* same block, a block's first pivot is only tested against 0; the rest of a */
-/* stopped block is postponed to Lambda_0.  "At the end of all threshold     */
+/* original index [R3]), the ratio test [R4] compares each candidate with the */
+/* previously ACCEPTED pivot of the elimination sequence (across blocks:     */
+/* reading [R21]; only the very first pivot is tested against 0 alone); the  */
+/* rest of a stopped block is postponed to Lambda_0.  "At the end of all     */
+/* threshold                                                                 */
 /* factorization following the elimination tree, we will again apply the     */
 /* LDU-factorization to the last Schur complement with indices Lambda_0"     */
 /* (P:80): a final pass over every remaining index with the same rules; its  */
@@ -328,7 +330,7 @@ int oracle_factor_blocks_f32(int64_t L, const double *K, int64_t ld, double tau,
     for (int64_t p = 0; p < L; ++p) orig[p] = p;
     int64_t Ntau = L;
     int32_t cur = 0;          /* current block; cur == nblk: the final pass over Lambda_0 */
-    int first = 1;            /* next pivot is the first of its block / pass */
+    int first = 1;            /* no pivot accepted yet */
     int64_t k = 0;
     while (k < L) {
         int64_t best = -1;
@@ -345,7 +347,7 @@ int oracle_factor_blocks_f32(int64_t L, const double *K, int64_t ld, double tau,
             fail = first ? (d == 0.0f) : (fabs((double)d) < tau * fabs((double)Dk[k - 1]));
         }
         if (fail) {
-            if (cur < nblk) { ++cur; first = 1; continue; }   /* the rest of the block -> Lambda_0 */
+            if (cur < nblk) { ++cur; continue; }   /* the rest of the block -> Lambda_0 */
             Ntau = k;                                         /* the final pass stops */
             break;
         }

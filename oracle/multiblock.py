@@ -7,7 +7,8 @@ nested-dissection elimination tree (sec. 2.2):
                   recursive level-structure bisection of the matrix graph,
                   blocks numbered in post-order (children before their
                   separator), 2^m - 1 blocks for m levels
-  factor_blocks   per-block FP32 factorization with the per-block tau-test,
+  factor_blocks   per-block FP32 factorization with the tau-test against the
+                  previously accepted pivot ([R21]),
                   the postponed entries collected in Lambda_0 and factored in a
                   final pass, floor and n-entry enlargement (oracle_factor_blocks_f32)
   hybrid_factor   Alg. 1 with that stage 1 (steps 2-5 as oracle.core)

@@ -222,6 +222,45 @@ hf_status hf_lowfactor_export(hf_ctx *ctx, const hf_lowfactor *lf, int64_t *perm
     });
 }
 
+hf_status hf_nd_blocks(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, int32_t levels, int32_t min_size,
+                       int32_t *blk_host, int32_t *nblk_host) {
+    if (!ctx || !blk_host || !nblk_host) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || K) && levels >= 1 && levels <= 30 && min_size >= 1,
+                   "hf_nd_blocks: bad arguments");
+        hf::nd_blocks(ctx, L, K, ld, levels, min_size, blk_host, nblk_host);
+    });
+}
+
+hf_status hf_factor_lowprec_blocks(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts *opts,
+                                   const int32_t *blk_host, int32_t nblk, hf_lowfactor **out, int64_t *N_host,
+                                   int64_t *n2_host, int64_t *n2_tau_only_host) {
+    if (!ctx || !out || (L > 0 && !blk_host)) return HF_ERR_INVALID_ARG;
+    *out = nullptr;
+    hf_lowprec_opts o{1e-2, 0, 0, 0, 32, 0};
+    if (opts) o = *opts;
+    if (o.prec == 0) o.prec = 32;
+    std::unique_ptr<hf_lowfactor> lf(new hf_lowfactor());
+    hf_status s = guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || K), "hf_factor_lowprec_blocks: bad arguments");
+        HF_REQUIRE(o.tau > 0.0 && o.tau < 1.0, "hf_factor_lowprec_blocks: tau must lie in (0,1)");
+        HF_REQUIRE(o.n_extra >= 0 && o.n_min >= 0, "hf_factor_lowprec_blocks: n_extra/n_min < 0");
+        HF_REQUIRE(o.nb >= 0 && o.nb <= 256 && o.nb % 8 == 0, "hf_factor_lowprec_blocks: nb in {0, 8..256, multiple of 8}");
+        HF_REQUIRE(o.prec == 32 && !o.nonsym, "hf_factor_lowprec_blocks: FP32 symmetric only");
+        HF_REQUIRE(ctx->nranks == 1 && ctx->s1parts == 0, "hf_factor_lowprec_blocks: single-GPU");
+        HF_REQUIRE(nblk >= 0, "hf_factor_lowprec_blocks: nblk < 0");
+        for (int64_t i = 0; i < L; ++i)
+            HF_REQUIRE(blk_host[i] >= 0 && blk_host[i] < std::max(nblk, 1), "hf_factor_lowprec_blocks: block id out of range");
+        hf::lowprec_factor(ctx, L, K, ld, o, lf.get(), blk_host, nblk);
+    });
+    if (s != HF_OK) return s;
+    if (N_host) *N_host = lf->N;
+    if (n2_host) *n2_host = lf->n2;
+    if (n2_tau_only_host) *n2_tau_only_host = lf->L - lf->Ntau;
+    *out = lf.release();
+    return HF_OK;
+}
+
 hf_status hf_lowfactor_export_u(hf_ctx *ctx, const hf_lowfactor *lf, float *Ufac, int64_t ldu) {
     if (!ctx || !lf) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {

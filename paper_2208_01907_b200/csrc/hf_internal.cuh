@@ -245,13 +245,16 @@ namespace hf {
 void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);
 void launch_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);   // NEXT-3
 void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
-                    hf_lowfactor *lf);
+                    hf_lowfactor *lf, const int32_t *blk_host = nullptr, int nblk = 0);
 void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                           hf_lowfactor *lf, int nparts);
 void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                       hf_lowfactor *lf);
 void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                        hf_lowfactor *lf);   // NEXT-3
+// NEXT-4: nested-dissection blocks of the symmetric pattern of K (nd.cu)
+void nd_blocks(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, int levels, int min_size, int32_t *blk_host,
+               int32_t *nblk_host);
 void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);
 void factor_hard(hf_ctx *ctx, hf_hybrid *hy, double eps_ker);
 void schur_gcr_dd(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *info);   // gcr_dd.cu

@@ -114,6 +114,13 @@ struct ChainArgs {
     int xmode;                   // 0: red.max + counter; 1: spread LL slots (HF_CHAIN_XCHG)
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
+    // NEXT-4, multi-block postponing: blk[original index] = block number in
+    // elimination-tree order, nblk blocks, then the final pass over Lambda_0; bstate =
+    // {current block, no pivot accepted yet, exchange attempt counter}
+    // carried across panels (null blk: the single-sequence rule)
+    const int32_t *blk;
+    int nblk;
+    int32_t *bstate;
     unsigned long long *dbg;   // optional per-phase time sums (CTA 0), HF_CHAIN_DEBUG
     // lookahead (the previous panel's trailing update runs concurrently): V is the
     // matrix at the START of the previous panel, in its position space; the
@@ -200,6 +207,11 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     __shared__ uint32_t redi[32];
     bool piv = !has;
     float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
+    const bool BLK = !PARTS && a.blk != nullptr;
+    int curblk = BLK ? a.bstate[0] : 0;
+    bool first = BLK ? (a.bstate[1] != 0) : (a.K0 == 0);
+    int64_t att = BLK ? (int64_t)a.bstate[2] : a.K0;   // exchange attempt: tags and buffer parity
+    const int32_t myblk = (BLK && has) ? a.blk[oi] : 0;
     // deferred stores of the previous step
     bool pend = false;
     float ps = 0.f, pn = 0.f, pl = 0.f;
@@ -208,11 +220,13 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
     unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = dbg ? gtimer() : 0;
 #define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
-    for (; t < nb; ++t) {
+    for (; t < nb;) {
         const int64_t k = a.K0 + t;
-        const uint64_t tag = step_tag(k);
-        // ---- A: [R3] local argmax of |diag| over own active rows
-        uint64_t key = piv ? 0ull : mkkey(dg, (uint32_t)i);
+        const uint64_t tag = step_tag(att);
+        const int par = (int)(att & 1);
+        // ---- A: [R3] local argmax of |diag| over own active rows (of the current block)
+        const bool cand = !piv && (!BLK || curblk >= a.nblk || myblk == curblk);
+        uint64_t key = cand ? mkkey(dg, (uint32_t)i) : 0ull;
         uint32_t kinfo = myinfo;
         if (PARTS) {
 #pragma unroll
@@ -250,7 +264,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             if (wid == 0) {
                 if (lane == 0) {
                     if (a.xmode == 1) {
-                        unsigned long long *slot = &a.slots[((size_t)(t & 1) * G + blockIdx.x) * SLOT_STRIDE];
+                        unsigned long long *slot = &a.slots[((size_t)par * G + blockIdx.x) * SLOT_STRIDE];
                         if (PARTS)   // the candidate's (partition, local column), next to its key
                             st_relaxed_u64(slot + 1, ((unsigned long long)(v ? vinfo : 0u) << 32) | tag);
                         st_relaxed_u64(slot, (v & ~TAGM) | tag);
@@ -260,7 +274,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
                     }
                 }
             } else if (v) {
-                unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + blockIdx.x) * (nb + 1);
+                unsigned long long *mb = a.mbox + ((size_t)par * G + blockIdx.x) * (nb + 1);
                 const int lr = (int)((int64_t)(POS_MAX - (uint32_t)((v >> 15) & POS_MAX)) - r0);
                 for (int u = lane; u < t; u += 32)
                     st_relaxed_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + lr]) << 32) | tag);
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- D: wait for all CTAs, read the winning key
         if (a.xmode == 1) {
             if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
-                const unsigned long long *sl = a.slots + (size_t)(t & 1) * G * SLOT_STRIDE;
+                const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
                 uint64_t mx, mi = 0;
                 for (;;) {
                     bool ok = true;
@@ -325,9 +339,15 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         const float absd = __uint_as_float((uint32_t)(bk >> 32));
         const int64_t P = (int64_t)(POS_MAX - (uint32_t)((bk >> 15) & POS_MAX));
         const float d = ((bk >> 14) & 1) ? -absd : absd;
-        // ---- E: [R4] stop test, ratio evaluated in FP64, strict
-        const bool stop = (k == 0) ? (absd == 0.f)
-                                   : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev)));
+        // ---- E: [R4] stop test, ratio evaluated in FP64, strict, against the previously
+        //      accepted pivot (across blocks [R21]; the very first pivot only against 0)
+        const bool stop = (bk == 0) || (first ? (absd == 0.f)
+                                              : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev))));
+        if (stop && BLK && curblk < a.nblk) {   // the rest of this block -> Lambda_0; next block, same step
+            ++curblk;
+            ++att;
+            continue;
+        }
         if (stop) {
             if (blockIdx.x == 0 && tid == 0) {
                 a.status[0] = (int32_t)k;
@@ -350,7 +370,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         }
         {
             const int owner = (int)(P / a.R);
-            const unsigned long long *mb = a.mbox + ((size_t)(t & 1) * G + owner) * (nb + 1);
+            const unsigned long long *mb = a.mbox + ((size_t)par * G + owner) * (nb + 1);
             for (int u = tid; u < t; u += nthr) {
                 uint64_t w;
                 do {
@@ -411,6 +431,9 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             dg = __fmaf_rn(ns, sv, dg);                 // lazy diagonal, same fma as the update
         }
         dprev = d;
+        first = false;
+        ++att;
+        ++t;
         PH(3)
     }
     if (pend) {   // flush the last step's values
@@ -419,6 +442,11 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
     }
     if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
+    if (BLK && blockIdx.x == 0 && tid == 0) {
+        a.bstate[0] = curblk;
+        a.bstate[1] = first ? 1 : 0;
+        a.bstate[2] = (int32_t)att;
+    }
     if (a.SNout && has) {   // this panel's values and the lazy diagonal, for the next panel's lookahead
         for (int u = 0; u < t; ++u) a.SNout[i * a.nbmax + u] = sneg[(size_t)u * a.R + tid];
         a.DGout[i] = dg;
@@ -1050,9 +1078,10 @@ static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_
 }
 
 void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
-                    hf_lowfactor *lf) {
+                    hf_lowfactor *lf, const int32_t *blk_host, int nblk_in) {
     cudaStream_t st = ctx->stream;
     const int nsm = ctx->num_sms;
+    const int o_nblk = blk_host ? nblk_in : 0;   // NEXT-4: multi-block postponing
     lf->L = L;
     lf->stream = st;
     if (L == 0) {
@@ -1082,7 +1111,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     // columns itself (the same fmaf, so the bits do not change).  Measured at C2: 103 ms
     // (chain 5.5 us/pivot: the concurrent update's memory traffic slows every exchange and
     // column read) against 99 ms serial, so the serial schedule is the default.
-    const bool look = getenv("HF_LOOKAHEAD") && atoi(getenv("HF_LOOKAHEAD")) != 0;
+    const bool look = !blk_host && getenv("HF_LOOKAHEAD") && atoi(getenv("HF_LOOKAHEAD")) != 0;
     const int64_t per_row = look ? 2 * nb_def + 3 : nb_def + 2;   // floats of shared memory per row
     int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / per_row))));
     if (const char *e = getenv("HF_CHAIN_CTAS")) gmax = std::max(1, std::min(nsm, atoi(e)));
@@ -1134,6 +1163,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     slots.zero(st);
     int xmode = 1;
     if (const char *e = getenv("HF_CHAIN_XCHG")) xmode = (strcmp(e, "counter") == 0) ? 0 : 1;
+    if (blk_host) xmode = 1;   // block transitions repeat a step: tagged slots only
     HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
 
     {
@@ -1157,6 +1187,15 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    DBuf<int32_t> blkd, bstate;   // NEXT-4: block of every original index; {block, first, attempt}
+    if (blk_host) {
+        blkd.alloc(std::max<int64_t>(L, 1), st);
+        HF_CUDA(cudaMemcpyAsync(blkd.p, blk_host, L * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        bstate.alloc(3, st);
+        const int32_t b0[3] = {0, 1, 0};
+        HF_CUDA(cudaMemcpyAsync(bstate.p, b0, sizeof(b0), cudaMemcpyHostToDevice, st));
+        HF_CUDA(cudaStreamSynchronize(st));   // the host arrays may die after the call
+    }
     DBuf<unsigned long long> dbg;
     const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
     if (want_dbg) {
@@ -1184,6 +1223,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
         ca.slots = slots.p; ca.xmode = xmode;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
+        ca.blk = blkd.p; ca.nblk = o_nblk; ca.bstate = bstate.p;
         ca.nbmax = nb;
         if (look && pidx > 0) {
             ca.mapprev = map[qb].p; ca.SNprev = SNrow[qb].p; ca.sigprev = sigma[qb].p; ca.DGprev = DG[qb].p;
@@ -1423,6 +1463,7 @@ void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, c
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = nullptr; ca.cnt = nullptr; ca.mbox = mbox.p; ca.slots = slots.p; ca.xmode = 1;
         ca.status = status.p; ca.dbg = nullptr;
+        ca.blk = nullptr; ca.nblk = 0; ca.bstate = nullptr;
         ca.mapprev = nullptr; ca.SNprev = nullptr; ca.sigprev = nullptr; ca.DGprev = nullptr;
         ca.nbprev = 0; ca.nbmax = nb; ca.SNout = nullptr; ca.DGout = nullptr;
         ca.parts = dtab.p + (size_t)cur * nparts; ca.nparts = nparts; ca.cb = CB; ca.colpos = colpos[cur].p;

@@ -31,6 +31,7 @@ EXPORTED = [
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
     "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64", "hf_schur_gcr_dd",
     "hf_hybrid_export_dd", "hf_lowfactor_export_u", "hf_scale_full", "hf_solve_dd",
+    "hf_nd_blocks", "hf_factor_lowprec_blocks",
 ]
 
 
@@ -90,6 +91,9 @@ def load() -> ctypes.CDLL:
                             ctypes.POINTER(gcr_info)],
         "hf_hybrid_export_dd": [vp, vp, vp, vp, i64, vp, vp, i64],
         "hf_solve_dd": [vp, vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
+        "hf_nd_blocks": [vp, i64, vp, i64, i32, i32, vp, ctypes.POINTER(i32)],
+        "hf_factor_lowprec_blocks": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), vp, i32, ctypes.POINTER(vp),
+                                     pi64, pi64, pi64],
         "hf_factor_hard": [vp, vp, dbl, pi64],
         "hf_hard_export": [vp, vp, vp, vp, pi64],
         "hf_solve": [vp, vp, vp, vp, ctypes.POINTER(gcr_info)],
@@ -461,3 +465,27 @@ def hf_solve_dd(ctx: Context, hy: Hybrid, b: torch.Tensor):
     info = gcr_info()
     ctx.check(ctx.lib.hf_solve_dd(ctx.h, hy.h, _ptr(b), _ptr(xh), _ptr(xl), ctypes.byref(info)))
     return xh, xl, GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true)
+
+
+def hf_nd_blocks(ctx: Context, K: torch.Tensor, levels: int, min_size: int = 8):
+    """NEXT-4: nested-dissection blocks of K's pattern.  Returns (blk np.int32[L], nblk)."""
+    _dev(K, torch.float64)
+    L = K.shape[0]
+    blk = np.empty(max(L, 1), dtype=np.int32)
+    n = ctypes.c_int32()
+    ctx.check(ctx.lib.hf_nd_blocks(ctx.h, L, _ptr(K), L, int(levels), int(min_size), _ptr(blk), ctypes.byref(n)))
+    return blk[:L], n.value
+
+
+def hf_factor_lowprec_blocks(ctx: Context, K: torch.Tensor, blk: np.ndarray, nblk: int, tau: float = 1e-2,
+                             n_extra: int = 0, n_min: int = 0, nb: int = 0) -> LowFactor:
+    """NEXT-4: stage 1 with multi-block postponing (blk: host int32[L], block ids in tree order)."""
+    _dev(K, torch.float64)
+    L = K.shape[0]
+    b = np.ascontiguousarray(blk, dtype=np.int32)
+    o = lowprec_opts(float(tau), int(n_extra), int(n_min), int(nb), 32, 0)
+    h = ctypes.c_void_p()
+    N, n2, n2t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.hf_factor_lowprec_blocks(ctx.h, L, _ptr(K), L, ctypes.byref(o), _ptr(b), int(nblk),
+                                               ctypes.byref(h), ctypes.byref(N), ctypes.byref(n2), ctypes.byref(n2t)))
+    return LowFactor(ctx, h, L, N.value, n2.value, n2t.value)

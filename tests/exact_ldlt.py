@@ -153,9 +153,9 @@ def left_looking_ldu(K: np.ndarray, tau: float):
 
 def left_looking_ldlt_blocks(K: np.ndarray, tau: float, blk, nblk: int):
     """NEXT-4 pin: the multi-block rule by left-looking exact replay: candidates of
-    the current block only (ties -> smallest original index), ratio test between
-    successive pivots of the same block / pass, a block's first pivot tested against
-    0 only, then a final pass over everything left.  Returns (pivots, D, Lcols, Ntau)."""
+    the current block only (ties -> smallest original index), ratio test against the
+    previously accepted pivot [R21] (the very first pivot against 0 only), then a final
+    pass over everything left.  Returns (pivots, D, Lcols, Ntau)."""
     L = K.shape[0]
     v0 = {}
     for i in range(L):
@@ -186,7 +186,7 @@ def left_looking_ldlt_blocks(K: np.ndarray, tau: float, blk, nblk: int):
         fail = best is None or (bd == 0.0 if first else abs(float(bd)) < tau * abs(float(D[-1])))
         if fail:
             if cur < nblk:
-                cur, first = cur + 1, True
+                cur += 1
                 continue
             Ntau = k
             break
