@@ -13,6 +13,7 @@
 // cp.async pipeline; shared layouts [k][m+4] / [k][n+4] make the DMMA
 // fragment loads bank-conflict free (8-byte words, 16 pairs per half warp).
 #include <algorithm>
+#include <cmath>
 
 #include "hf_internal.cuh"
 #include "k_dgemm.cuh"
@@ -163,11 +164,30 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
     if (M <= 0 || N <= 0) return;
     cudaStream_t st = ctx->stream;
     const int64_t mt = cdiv(M, BM), nt = cdiv(N, BN);
+    const size_t shm0 = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+    static int per_sm = 0;
+    if (!per_sm) {
+        HF_CUDA(cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm0));
+        HF_CUDA(cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm0));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dgemm<false>, 128, shm0));
+        per_sm = std::max(1, per_sm);
+    }
     if (splits <= 0) {
-        // enough CTAs for ~4 waves of 148 SMs, each split >= 256 deep
-        const int64_t want = cdiv(4 * (int64_t)ctx->num_sms, mt * nt);
-        splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 256));
-        splits = std::min(splits, 256);
+        // wave-aware split-K: among splits whose depth is >= 256, take the one whose CTA count
+        // fills the last wave best (the plain 1024-tile mat-vec fills 1.73 waves of 592 CTA
+        // slots -> 87 %; 4 splits give 6.92 waves -> 99 %); ties -> fewer splits
+        const int64_t slots = (int64_t)per_sm * ctx->num_sms;
+        const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(16, K / 256));
+        double best = -1.0;
+        splits = 1;
+        for (int64_t sp = 1; sp <= smax; ++sp) {
+            const double w = (double)(mt * nt * sp) / (double)slots;
+            const double eff = w / std::ceil(w);
+            if (eff > best + 0.02) {
+                best = eff;
+                splits = (int)sp;
+            }
+        }
     }
     if (K == 0) splits = 1;
     DgemmArgs g{M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, rowmask, nullptr};
@@ -175,13 +195,7 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
         work->alloc((size_t)splits * M * N, st);
         g.W = work->p;
     }
-    const size_t shm = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
-    static bool attr_done = false;
-    if (!attr_done) {
-        HF_CUDA(cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        HF_CUDA(cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        attr_done = true;
-    }
+    const size_t shm = shm0;
     ClassTimer tm(ctx, "dgemm");
     dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
     if (transA) k_dgemm<true><<<grid, 128, shm, st>>>(g);
