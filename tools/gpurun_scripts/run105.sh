@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_precond.py -x -q > gpurun_out/t105.log 2>&1; echo t=$?
+HF_TRSM_DEBUG=1 timeout 300 python tools/prof_trsm.py C2 256 3 > gpurun_out/p105.log 2>&1; echo p=$?
