@@ -1103,9 +1103,11 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     maxsmem -= (int)fa.sharedSizeBytes;
     // Chain geometry (measured on B200 at C2, chain + trailing ms: 148 CTAs / nb 256: 106.3,
     // 148 / 128: 103.3, 74 / 128: 100.6, 64 / 128: 95.0, 64 / 192: 95.8, 32 / 96: 98.8):
-    // fewer CTAs make the per-pivot exchange cheaper until the rows per CTA no longer fit a
-    // 128-wide panel in shared memory, so G = max(64, L / 443) and nb = 128 by default.
-    const int nb_def = 128;
+    // fewer CTAs make the per-pivot exchange cheaper until the rows per CTA no longer fit the
+    // panel in shared memory, so G = max(64, L / rows-that-fit) CTAs.
+    // nb = 160 (measured at C2 with the streaming trailing kernel, chain + trailing + other ms:
+    // nb 128: 88.4, 160: 87.9, 192: 87.9; the trailing update alone 32.2 / 30.9 / 29.6)
+    const int nb_def = 160;
     // Lookahead (HF_LOOKAHEAD=1, off by default): the chain of panel p+1 runs while panel
     // p's trailing update runs on a second stream, applying panel p's updates to its pivot
     // columns itself (the same fmaf, so the bits do not change).  Measured at C2: 103 ms
@@ -1121,6 +1123,8 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     int nb = o.nb > 0 ? o.nb : nb_def;
     // with lookahead the chain holds both panels' values of its rows in shared memory
     const int nbf = (look ? 2 : 1);
+    // the widest multiple of 16 (the trailing kernel's k chunk) that fits, e.g. 112 at C4
+    while (nb > 16 && (int64_t)(nbf * nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb -= 16;
     while (nb > 8 && (int64_t)(nbf * nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
     HF_REQUIRE(nb >= 8 && nb <= 1024, "panel width out of range");
 
