@@ -140,3 +140,29 @@ def test_dd_solve_exact_residual(ctx, name, seed):
     hy64.close()
     hy.close()
     lf.close()
+
+
+def test_dd_degenerate(ctx):
+    """n2 = 0 (nothing postponed: empty S22, hard factor a no-op, the solve is the block GCR
+    alone) and a 1 x 1 system through the double-double path."""
+    from paper_2208_01907_b200 import hf
+    K = torch.diag(torch.tensor([4.0, 2.0, 1.0, 0.5], dtype=torch.float64)).cuda()
+    hf.hf_scale(ctx, K)
+    lf = hf.hf_factor_lowprec(ctx, K, tau=1e-2, prec=64)
+    assert lf.n2 == 0
+    hy, info, _ = hf.hf_schur_gcr_dd(ctx, K, lf)
+    assert hf.hf_factor_hard(ctx, hy, eps_ker=1e-20) == 0
+    b = torch.tensor([1.0, -2.0, 3.0, 0.25], dtype=torch.float64, device="cuda")
+    xh, xl, _ = hf.hf_solve_dd(ctx, hy, b)
+    assert torch.equal(xh, b) and float(xl.abs().max()) == 0.0     # K = diag(+-1) after scaling
+    hy.close()
+    lf.close()
+    one = torch.tensor([[-5.0]], dtype=torch.float64, device="cuda")
+    hf.hf_scale(ctx, one)
+    lf = hf.hf_factor_lowprec(ctx, one, tau=1e-2, n_min=1, prec=64)
+    assert lf.n2 == 1
+    hy, info, S = hf.hf_schur_gcr_dd(ctx, one, lf, want_S22_host=True)
+    assert S[0][0, 0] == -1.0 and S[1][0, 0] == 0.0
+    assert hf.hf_factor_hard(ctx, hy, eps_ker=1e-20) == 0
+    hy.close()
+    lf.close()

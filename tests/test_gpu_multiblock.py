@@ -90,3 +90,33 @@ def test_multiblock_hybrid_vs_oracle(ctx, name, levels):
     assert float((K @ x - b).abs().max() / b.abs().max()) <= 1e-12
     hy.close()
     lf.close()
+
+
+def test_multiblock_edge_cases(ctx):
+    """One block per index (every block a single candidate), all indices in one block, a
+    block id out of range refused, L = 1, and a zero matrix (every block's first candidate
+    is 0: all postponed)."""
+    from paper_2208_01907_b200 import hf
+    Kb = hi.make_kbar("N16", 0)
+    K = Kb.cuda()
+    hf.hf_scale(ctx, K)
+    Ko, _ = oracle.scale(Kb.numpy())
+    L = Ko.shape[0]
+    for blk, nblk in ((np.arange(L, dtype=np.int32), L), (np.zeros(L, np.int32), 1),
+                      ((np.arange(L) % 5).astype(np.int32), 5)):
+        F = mb.factor_blocks(Ko, 1e-2, blk, nblk, n_min=1)
+        lf = hf.hf_factor_lowprec_blocks(ctx, K, blk, nblk, tau=1e-2, n_min=1)
+        perm, D, Lf = lf.export()
+        assert lf.N == F.N and np.array_equal(perm, F.perm) and np.array_equal(D, F.D)
+        assert np.array_equal(Lf.cpu().numpy(), F.Lfac)
+        lf.close()
+    with pytest.raises(hf.HFError):
+        hf.hf_factor_lowprec_blocks(ctx, K, np.full(L, 7, np.int32), 3)
+    one = torch.tensor([[2.0]], dtype=torch.float64, device="cuda")
+    lf = hf.hf_factor_lowprec_blocks(ctx, one, np.zeros(1, np.int32), 1)
+    assert lf.N == 1
+    lf.close()
+    z = torch.zeros(6, 6, dtype=torch.float64, device="cuda")
+    lf = hf.hf_factor_lowprec_blocks(ctx, z, np.array([0, 0, 1, 1, 2, 2], np.int32), 3)
+    assert lf.N == 0 and lf.n2 == 6
+    lf.close()

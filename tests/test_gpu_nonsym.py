@@ -124,3 +124,39 @@ def test_precond_nonsym_vs_oracle(ctx):
     e_g = np.abs(Wg[F.lam1] - exact).max()
     assert e_g <= max(10 * e_o, 100 * eps32 * np.abs(exact).max())
     lf.close()
+
+
+def test_nonsym_edge_cases(ctx):
+    """Degenerate inputs of the nonsymmetric path against the oracle: 1 x 1, a zero first
+    pivot (everything postponed), a strictly triangular-dominant matrix with no postponement
+    (n2 = 0: hf_schur_gcr returns an empty S22 and hf_factor_hard is a no-op), ragged sizes
+    around the 128-row tile, NaN refused."""
+    from paper_2208_01907_b200 import hf
+    cases = [np.array([[-3.0]]), np.array([[0.0, 2.0], [-1.0, 0.0]]),
+             np.eye(5) * 4 + np.triu(np.ones((5, 5)), 1)]
+    rng = np.random.default_rng(9)
+    for L in (127, 128, 129, 257):
+        A = rng.standard_normal((L, L))
+        A[np.arange(L), np.arange(L)] = rng.uniform(0.5, 2.0, L) * rng.choice([1, -1], L)
+        cases.append(A)
+    for Kbar in cases:
+        Ko, _ = nonsym.scale_full(Kbar)
+        F = nonsym.factor_ldu(Ko, 1e-2)
+        Kd = hi.colmajor(torch.from_numpy(Kbar.copy())).cuda()
+        hf.hf_scale_full(ctx, Kd)
+        lf = hf.hf_factor_lowprec(ctx, Kd, tau=1e-2, nonsym=True)
+        perm, D, Lf = lf.export()
+        assert lf.N == F.N and np.array_equal(perm, F.perm) and np.array_equal(D, F.D)
+        if F.N:
+            assert np.array_equal(Lf.cpu().numpy(), F.Lfac)
+            assert np.array_equal(lf.export_u().cpu().numpy(), F.Ufac)
+        hy, info, S22 = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
+        kd = hf.hf_factor_hard(ctx, hy)
+        if lf.n2 == 0:
+            assert kd == 0
+        hy.close()
+        lf.close()
+    bad = torch.eye(4, dtype=torch.float64, device="cuda")
+    bad[2, 1] = float("nan")
+    with pytest.raises(hf.HFError):
+        hf.hf_scale_full(ctx, bad)
