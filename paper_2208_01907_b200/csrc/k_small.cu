@@ -456,6 +456,32 @@ __device__ __forceinline__ void warp_best(Best &b) {
     }
 }
 
+// both bests of the CTA at once: warp shuffles, then one pass over the per-warp winners
+// (two barriers instead of the nine of two block_best trees)
+__device__ __forceinline__ void block_best2(Best &bd, Best &bo, Best *sh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    warp_best(bd);
+    warp_best(bo);
+    if (lane == 0) {
+        sh[wid] = bd;
+        sh[32 + wid] = bo;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        Best d = lane < nw ? sh[lane] : Best{-1.0, 0, 0, -1, -1};
+        Best o = lane < nw ? sh[32 + lane] : Best{-1.0, 0, 0, -1, -1};
+        warp_best(d);
+        warp_best(o);
+        if (lane == 0) {
+            sh[64] = d;
+            sh[65] = o;
+        }
+    }
+    __syncthreads();
+    bd = sh[64];
+    bo = sh[65];
+}
+
 __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *__restrict__ S, double thr,
                                                        double *__restrict__ A, double *__restrict__ Lcol,
                                                        int32_t *__restrict__ act, int32_t *__restrict__ posof,
@@ -490,8 +516,7 @@ __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *
             blocks[i] = 0;
         }
     int par = 0;
-    bd = block_best(bd, sh);
-    bo = block_best(bo, sh);
+    block_best2(bd, bo, sh);
     if (tid == 0) {
         gbest[(size_t)par * 2 * G + 2 * c] = bd;
         gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
@@ -552,8 +577,7 @@ __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *
                     posof[p] = (int32_t)k;
                 }
             }
-            bd = block_best(bd, sh);
-            bo = block_best(bo, sh);
+            block_best2(bd, bo, sh);
             if (tid == 0) {
                 gbest[(size_t)par * 2 * G + 2 * c] = bd;
                 gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
@@ -609,8 +633,7 @@ __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *
                     posof[q] = (int32_t)(k + 1);
                 }
             }
-            bd = block_best(bd, sh);
-            bo = block_best(bo, sh);
+            block_best2(bd, bo, sh);
             if (tid == 0) {
                 gbest[(size_t)par * 2 * G + 2 * c] = bd;
                 gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
