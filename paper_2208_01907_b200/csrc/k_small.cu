@@ -202,6 +202,70 @@ __global__ void k_maxres(int64_t n, const double *__restrict__ rn2, const double
 // (written by their owners at the end of step k-1) and updates its columns;
 // one grid barrier per step.
 //   p = a_kk;  a_ij -= a_ik a_kj / p;  a_kj /= p;  a_ik = -a_ik / p;  a_kk = 1/p
+// The same Gauss-Jordan inverse on one thread-block CLUSTER of 16 CTAs with the matrix in
+// distributed shared memory (n <= ~640): CTA r holds the columns j = r + 16 c; after a
+// step's update the owner of the next pivot column stores it into every CTA's shared buffer
+// (double buffered by step parity), so one cluster barrier per step replaces the grid
+// barrier and all reads are local.  Same arithmetic per entry as k_spd_inv.
+constexpr int SPD_CL = 16;
+__global__ void __launch_bounds__(512) k_spd_inv_cl(int n, const double *__restrict__ M, int64_t ldm,
+                                                    double *__restrict__ Minv, int *status) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double smd[];
+    const int r = (int)cl.block_rank(), tid = threadIdx.x, nt = blockDim.x;
+    const int ncl = (n - r + SPD_CL - 1) / SPD_CL;                 // local columns
+    const int ncmax = (n + SPD_CL - 1) / SPD_CL;
+    double *A = smd;                                              // [ncmax][n], local column c = global r + 16 c
+    double *cb = smd + (size_t)ncmax * n;                         // [2][n] pivot column buffers, then [ncmax]
+    for (int e = tid; e < ncl * n; e += nt) {
+        const int c = e / n, i = e % n;
+        A[e] = M[i + (int64_t)(r + SPD_CL * c) * ldm];
+    }
+    if (r == 0)   // column 0 is the first pivot column: every CTA's buffer 0
+        for (int e = tid; e < SPD_CL * n; e += nt) {
+            const int dst = e / n, i = e % n;
+            double *rb = cl.map_shared_rank(cb, dst);
+            rb[i] = M[i];
+        }
+    cl.sync();
+    int bad = 0;
+    for (int k = 0; k < n; ++k) {
+        const double *ck = cb + (k & 1) * n;
+        double p = ck[k];
+        if (!(p > 0.0)) {
+            bad = 1;
+            p = 1.0;
+        }
+        const double ip = 1.0 / p;
+        // the row-k multipliers of the local columns first (row k is overwritten below)
+        double *rrow = cb + 2 * (size_t)n;   // [ncmax]
+        for (int c = tid; c < ncl; c += nt) rrow[c] = A[(size_t)c * n + k] / p;
+        __syncthreads();
+        for (int e = tid; e < ncl * n; e += nt) {
+            const int c = e / n, i = e % n;
+            const int j = r + SPD_CL * c;
+            double *aj = A + (size_t)c * n;
+            if (j == k) aj[i] = (i == k) ? ip : -ck[i] / p;
+            else aj[i] = (i == k) ? rrow[c] : fma(-ck[i], rrow[c], aj[i]);
+        }
+        __syncthreads();
+        if (k + 1 < n && (k + 1) % SPD_CL == r) {   // broadcast the next pivot column
+            const double *src = A + (size_t)((k + 1) / SPD_CL) * n;
+            for (int e = tid; e < SPD_CL * n; e += nt) {
+                const int dst = e / n, i = e % n;
+                double *rb = cl.map_shared_rank(cb + ((k + 1) & 1) * n, dst);
+                rb[i] = src[i];
+            }
+        }
+        cl.sync();
+    }
+    for (int e = tid; e < ncl * n; e += nt) {
+        const int c = e / n, i = e % n;
+        Minv[i + (int64_t)(r + SPD_CL * c) * n] = A[e];
+    }
+    if (r == 0 && tid == 0 && bad) atomicOr(status, 1);
+}
+
 __global__ void __launch_bounds__(256) k_spd_inv(int64_t n, const double *__restrict__ M, int64_t ldm,
                                                  double *__restrict__ A, double *__restrict__ cbuf,
                                                  double *__restrict__ rbuf, int *status) {
@@ -815,6 +879,33 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
     ClassTimer tm_(ctx, "gram");
     wk.alloc((size_t)4 * n, ctx->stream);
     double *cb = wk.p, *rb = wk.p + 2 * n;
+    const size_t shm_cl = ((size_t)cdiv(n, SPD_CL) * n + 2 * (size_t)n + (size_t)cdiv(n, SPD_CL)) * sizeof(double);
+    static int cl_ok = -1;   // the 16-CTA cluster path: non-portable cluster size, checked once
+    if (cl_ok < 0) {
+        cl_ok = getenv("HF_SPD_NOCLUSTER") ? 0 : 1;
+        if (cl_ok && (cudaFuncSetAttribute(k_spd_inv_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                      cudaFuncSetAttribute(k_spd_inv_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess))
+            cl_ok = 0;
+        cudaGetLastError();
+    }
+    if (cl_ok && n >= 1 && shm_cl <= (size_t)227 * 1024) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(SPD_CL);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = shm_cl;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = SPD_CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const int ni = (int)n;
+        HF_CUDA(cudaLaunchKernelEx(&cfg, k_spd_inv_cl, ni, M, ldm, Minv, status));
+        HF_CHECK_LAUNCH(ctx);
+        return;
+    }
     int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(n, 4)), ctx->num_sms);
     void *args[] = {&n, &M, &ldm, &Minv, &cb, &rb, &status};
     HF_CUDA(cudaLaunchCooperativeKernel((void *)k_spd_inv, dim3(G), dim3(256), args, 0, ctx->stream));
