@@ -62,6 +62,7 @@ struct TrsmArgs {
     const int4 *pinfo;   // [nblk] block j: (first slot, #bulk slots, #near slots, tail q_lo); base slot last
     int npw;             // P-worker CTAs per chunk (block j -> worker j % npw)
     int nitems;
+    int h48;             // helper PARTIAL items in the 4 x 8 k-split form (FP32)
     T *part;         // partial sums [slot][chunk][64 x CW] (row-major)
     T *P;            // P_j, row-major Np x ncolp (by physical row)
     int *pflags;         // [2][nslots*nch]
@@ -158,6 +159,27 @@ __device__ __forceinline__ void tile_fms(T (&acc)[4][4], const T *As, const T *B
     tile_prod<true>(acc, As, Bs, tr, tc, k0, k1);
 }
 
+// Helper PARTIAL items (FP32): a 4 x 8 output block per thread over HALF the k range of
+// each tile (two k groups of 128 threads, reduced once per item), so a k step costs three
+// shared loads for 16 FFMA2 instead of two for 8.  A warp covers 8 row groups x 4 column
+// groups: one 128-B wavefront per operand load.
+__device__ __forceinline__ void tile_prod48(float2 (&c2)[4][4], const float *As, const float *Bs, int r4, int c8,
+                                            int k0) {
+#pragma unroll 8
+    for (int k = k0; k < k0 + TBS / 2; ++k) {
+        const float4 a = *reinterpret_cast<const float4 *>(&As[k * TBS + r4]);
+        const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[k * CW + c8]);
+        const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[k * CW + c8 + 4]);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float2 y[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                             make_float2(b1.z, b1.w)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) c2[i][jp] = __ffma2_rn(make_float2(av[i], av[i]), y[jp], c2[i][jp]);
+    }
+}
+
 // ------------------------------------------------------------------ setup: G = Dinv Op
 // In place, one 64x64 tile per CTA: Op(b-block, q-block) <- Dinv_b Op(b, q) for
 // every dependency block q of b (forward: q < b on Lp; backward: q > b on Up).
@@ -213,7 +235,9 @@ template <bool BWD>
 __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
     extern __shared__ __align__(16) T sm[];
     __shared__ int item_s;
-    const int tid = threadIdx.x, tr = tid & 15, tc = (tid >> 4) & 15;
+    // thread -> 4x4 output block: a warp covers 8 row groups x 4 column groups, so each
+    // k step's operand loads are one 128-B A wavefront and one 64-B B wavefront
+    const int tid = threadIdx.x, tr = (tid & 7) | (((tid >> 5) & 1) << 3), tc = ((tid >> 3) & 3) | (((tid >> 6) & 3) << 2);
     int *flags = a.flags + (BWD ? a.nblk * a.nch : 0);
     int *pflags = a.pflags + (BWD ? a.nslots * a.nch : 0);
     int *aflags = a.aflags + (BWD ? a.nblk * a.nch : 0);
@@ -351,26 +375,31 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
     // cp.async in flight.  Released flags are checked eight at a time (independent loads,
     // one round trip), so old dependencies cost no poll each.
     __shared__ int rdy_s;
-    auto accumulate = [&](T (&t)[4][4], int64_t r0, int c0, int cc, int q_lo, int q_hi) {
+    // h2 != null (helpers, FP32): the 4 x 8 k-split form of tile_prod48 into h2 instead of t
+    const int kg = tid >> 7, t7 = tid & 127;
+    const int r4h = ((t7 & 7) | (((t7 >> 5) & 1) << 3)) * 4, c8h = (((t7 >> 3) & 3) | ((t7 >> 6) << 2)) * 8;
+    auto accumulate = [&](T (&t)[4][4], int64_t r0, int c0, int cc, int q_lo, int q_hi, float2 (*h2)[4] = nullptr) {
         const int ndep = q_hi - q_lo;
         if (ndep <= 0) return;
         int ready = 0;   // blocks [q_lo, q_lo + ready) known released (uniform)
         auto ensure = [&](int dq) {
             if (dq < ready) return;
-            if (tid == 0) {
+            if (tid < 32) {   // warp 0: up to 32 flags in one round trip, ready prefix by ballot
                 const int *f = flags + (size_t)(q_lo + dq) * a.nch + cc;
-                const int nchk = min(8, ndep - dq);
-                int v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = u < nchk ? ld_relaxed32(f + (size_t)u * a.nch) : 0;
-                int n = 0;
-                while (n < nchk && v[n] == a.epoch) ++n;
+                const int nchk = min(32, ndep - dq);
+                const bool ok = tid < nchk && ld_relaxed32(f + (size_t)tid * a.nch) == a.epoch;
+                const unsigned bad = ~__ballot_sync(0xffffffffu, ok);
+                int n = __ffs(bad) - 1;   // bad != 0: lane nchk.. are never ok
+                if (n > nchk) n = nchk;
                 if (n == 0) {
-                    while (ld_relaxed32(f) != a.epoch) __nanosleep(20);
+                    if (tid == 0)
+                        while (ld_relaxed32(f) != a.epoch) __nanosleep(20);
                     n = 1;
                 }
-                fence_acquire();
-                rdy_s = dq + n;
+                if (tid == 0) {
+                    fence_acquire();
+                    rdy_s = dq + n;
+                }
             }
             bar_sync(5, NCOMP);
             ready = rdy_s;
@@ -396,7 +425,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             }
             bar_sync(5, NCOMP);
             const T *As = sm + (dq % 3) * 2 * TILE;
-            tile_fma(t, As, As + TILE, tr, tc);
+            if constexpr (sizeof(T) == 4) {
+                if (h2) tile_prod48(*reinterpret_cast<float2 (*)[4][4]>(h2), reinterpret_cast<const float *>(As),
+                                    reinterpret_cast<const float *>(As + TILE), r4h, c8h, kg * (TBS / 2));
+                else tile_fma(t, As, As + TILE, tr, tc);
+            } else {
+                tile_fma(t, As, As + TILE, tr, tc);
+            }
             bar_sync(5, NCOMP);
         }
     };
@@ -546,8 +581,49 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
         T t[4][4] = {};
         if (slot >= 0) {
             // PARTIAL: t = sum over the segment [q_lo, q_hi) of Op_bq Y_q -> slot
-            accumulate(t, r0, c0, cc, it.z & 0xFFFF, it.z >> 16);
-            store_slot(t, cc, slot);
+            if constexpr (sizeof(T) == 4) {
+                if (!a.h48) {
+                    accumulate(t, r0, c0, cc, it.z & 0xFFFF, it.z >> 16);
+                    store_slot(t, cc, slot);
+                    continue;
+                }
+                float2 h2[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp) h2[i][jp] = make_float2(0.f, 0.f);
+                accumulate(t, r0, c0, cc, it.z & 0xFFFF, it.z >> 16, h2);
+                // k group 1 -> shared (stage buffers are free after the last barrier), group 0 adds
+                // and stores the slot in its [64][CW] layout
+                T *red = sm;
+                if (kg == 1) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        st4(&red[(r4h + i) * CW + c8h], T(h2[i][0].x), T(h2[i][0].y), T(h2[i][1].x), T(h2[i][1].y));
+                        st4(&red[(r4h + i) * CW + c8h + 4], T(h2[i][2].x), T(h2[i][2].y), T(h2[i][3].x), T(h2[i][3].y));
+                    }
+                }
+                bar_sync(5, NCOMP);
+                if (kg == 0) {
+                    T *pp = a.part + ((size_t)slot * a.nch + cc) * (TBS * CW);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const V4<T> u0 = ld4(&red[(r4h + i) * CW + c8h]), u1 = ld4(&red[(r4h + i) * CW + c8h + 4]);
+                        st4(&pp[(r4h + i) * CW + c8h], T(h2[i][0].x) + u0.x, T(h2[i][0].y) + u0.y,
+                            T(h2[i][1].x) + u0.z, T(h2[i][1].y) + u0.w);
+                        st4(&pp[(r4h + i) * CW + c8h + 4], T(h2[i][2].x) + u1.x, T(h2[i][2].y) + u1.y,
+                            T(h2[i][3].x) + u1.z, T(h2[i][3].y) + u1.w);
+                    }
+                }
+                bar_sync(5, NCOMP);
+                if (tid == 0) {
+                    __threadfence();
+                    st_release32(&pflags[slot * a.nch + cc], a.epoch);
+                }
+            } else {
+                accumulate(t, r0, c0, cc, it.z & 0xFFFF, it.z >> 16);
+                store_slot(t, cc, slot);
+            }
         } else {
             // EARLY: base_j = Dinv_j RHS_j - (bulk slots, in order) -> the base slot
             const int4 pi = a.pinfo[j];
@@ -728,6 +804,7 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         p.flags.zero(st);
         p.epoch = 0;
     }
+    const int h48 = !(getenv("HF_TRSM_H48") && atoi(getenv("HF_TRSM_H48")) == 0);
     int npw = 2;   // HF_TRSM_PW: P-worker CTAs per chunk
     if (const char *e = getenv("HF_TRSM_PW")) npw = std::max(1, atoi(e));
     const int nroles = nch * (1 + npw);
@@ -738,7 +815,7 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
     p.epoch += 1;
     TrsmArgs a;
     a.N = p.N; a.Np = p.Np; a.ncol = (int)ncol; a.ncolp = ncolp; a.nch = nch; a.nblk = nblk; a.seg = seg;
-    a.items = p.items; a.pinfo = p.pinfo; a.npw = npw; a.nitems = p.nitems; a.part = p.part.p; a.P = p.P.p;
+    a.items = p.items; a.pinfo = p.pinfo; a.npw = npw; a.nitems = p.nitems; a.h48 = h48; a.part = p.part.p; a.P = p.P.p;
     a.pflags = p.pflags.p; a.aflags = p.flags.p + 2 * nblk * nch; a.nslots = p.nslots; a.Lp = p.Lp.p; a.Up = p.Up.p;
     a.LinvF = p.LinvF.p; a.LinvB = p.LinvB.p; a.D = p.D; a.perm = p.perm; a.R = R; a.ldr = ldr; a.Y = p.Y.p;
     a.Xb = p.Xb.p; a.flags = p.flags.p; a.counter = p.counter.p;
