@@ -184,6 +184,15 @@ hf_status hf_lowfactor_export_u(hf_ctx *ctx, const hf_lowfactor *lf, float *Ufac
 hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, const double *R,
                            int64_t ldr, double *W, int64_t ldw);
 
+/* Minv = M^{-1} for the SPD Gram matrix M_n = q_n^T q_n of Algorithm 5 (P:322-330:
+ * alpha_n = M_n^{-1} q_n^T r_n, beta_{n,m} = -M_m^{-1} q_m^T z), the step hf_schur_gcr runs
+ * once per iteration.  M: DEVICE n x n column-major FP64 (ldm >= n, only read); Minv:
+ * DEVICE n x n (ld n).  Gauss-Jordan without pivoting (16-CTA cluster, blocked by 16 for
+ * n <= 448); *breakdown_host = 1 when a pivot is not positive (M not numerically SPD,
+ * [R11]; Minv is then not meaningful), else 0.  Synchronises. */
+hf_status hf_gram_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *Minv,
+                          int32_t *breakdown_host);
+
 /* ------------- NEXT-2: IR / GCR / block GCR comparison (Fig. 2) */
 /* K11 X = B with the FP32 preconditioner of lf: method 0 = Algorithm 3 (mixed-
  * precision iterative refinement), 1 = Algorithm 4 (GCR, P:277-295,

@@ -8,6 +8,7 @@
 
 #include "hf_internal.cuh"
 #include "k_dgemm.cuh"
+#include "k_small.cuh"
 
 namespace {
 
@@ -310,6 +311,25 @@ hf_status hf_precond_apply(hf_ctx *ctx, const hf_lowfactor *lf, int64_t ncol, co
         hf::precond_setup(ctx, pc, lf);
         hf::precond_apply(ctx, pc, ncol, R, ldr, W, ldw);
         HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+hf_status hf_gram_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *Minv,
+                          int32_t *breakdown_host) {
+    if (!ctx || !breakdown_host) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(n >= 0 && ldm >= std::max<int64_t>(n, 1) && (n == 0 || (M && Minv)), "hf_gram_inverse: bad arguments");
+        *breakdown_host = 0;
+        if (n == 0) return;
+        hf::DBuf<double> wk, dg;
+        hf::DBuf<int> st;
+        st.alloc(1, ctx->stream);
+        st.zero(ctx->stream);
+        hf::spd_inverse(ctx, n, M, ldm, Minv, wk, dg, st.p);
+        int h = 0;
+        HF_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        *breakdown_host = h ? 1 : 0;
     });
 }
 

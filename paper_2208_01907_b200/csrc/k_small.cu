@@ -266,6 +266,116 @@ __global__ void __launch_bounds__(512) k_spd_inv_cl(int n, const double *__restr
     if (r == 0 && tid == 0 && bad) atomicOr(status, 1);
 }
 
+// BLOCKED Gauss-Jordan on the same 16-CTA cluster (n <= ~450): the pivot block P = 16
+// consecutive indices is one column per CTA, so per block step every owner broadcasts its
+// column into every CTA's panel buffer (double buffered by step parity), one cluster barrier,
+// then each CTA inverts A_PP (16 x 16, scalar Gauss-Jordan: its pivots are those of the
+// scalar elimination, so the breakdown test [R11] is unchanged) and applies the block pivot
+//   A_PP <- D = A_PP^{-1},  A_Pj <- D A_Pj,  A_iP <- -A_iP D,  A_ij <- A_ij - A_iP D A_Pj
+// to its own columns: n / 16 barriers instead of n.
+constexpr int SPD_BS = 16;
+__global__ void __launch_bounds__(512) k_spd_inv_blk(int n, const double *__restrict__ M, int64_t ldm,
+                                                     double *__restrict__ Minv, int *status) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double smd[];
+    const int r = (int)cl.block_rank(), tid = threadIdx.x, nt = blockDim.x;
+    const int ncl = (n - r + SPD_CL - 1) / SPD_CL;                // local columns (global r + 16 c)
+    const int ncmax = (n + SPD_CL - 1) / SPD_CL;
+    double *A = smd;                                             // [ncmax][n]
+    double *PB = A + (size_t)ncmax * n;                          // [2][SPD_BS][n] panel: column k of block
+    double *Rs = PB + 2 * (size_t)SPD_BS * n;                    // [ncmax][SPD_BS]  D A_Pj of own columns
+    __shared__ double Ds[SPD_BS][SPD_BS + 1];
+    __shared__ double dcol[SPD_BS], drow[SPD_BS];
+    for (int e = tid; e < ncl * n; e += nt) {
+        const int c = e / n, i = e % n;
+        A[e] = M[i + (int64_t)(r + SPD_CL * c) * ldm];
+    }
+    __syncthreads();
+    auto bcast = [&](int m) {   // own column of block m -> panel slot r of every CTA
+        if (SPD_BS * m + r >= n) return;
+        const double *src = A + (size_t)m * n;
+        double *dstb = PB + (size_t)(m & 1) * SPD_BS * n + (size_t)r * n;
+        for (int e = tid; e < SPD_CL * n; e += nt) {
+            const int dst = e / n, i = e % n;
+            cl.map_shared_rank(dstb, dst)[i] = src[i];
+        }
+    };
+    bcast(0);
+    cl.sync();
+    int bad = 0;
+    const int nblk = (n + SPD_BS - 1) / SPD_BS;
+    for (int m = 0; m < nblk; ++m) {
+        const int p0 = SPD_BS * m, bs = min(SPD_BS, n - p0);
+        const double *P = PB + (size_t)(m & 1) * SPD_BS * n;    // P[k * n + i] = A(i, p0 + k)
+        // D = A_PP^{-1} by scalar Gauss-Jordan (threads 0..bs*bs-1 own one entry each)
+        const int di = tid / SPD_BS, dj = tid % SPD_BS;
+        const bool dact = tid < SPD_BS * SPD_BS && di < bs && dj < bs;
+        if (dact) Ds[di][dj] = P[(size_t)dj * n + p0 + di];
+        __syncthreads();
+        for (int k = 0; k < bs; ++k) {
+            double pk = Ds[k][k];
+            if (!(pk > 0.0)) {
+                bad = 1;
+                pk = 1.0;
+            }
+            if (tid < bs) {
+                dcol[tid] = Ds[tid][k];
+                drow[tid] = Ds[k][tid] / pk;
+            }
+            __syncthreads();
+            if (dact) {
+                double v;
+                if (di == k && dj == k) v = 1.0 / pk;
+                else if (di == k) v = drow[dj];
+                else if (dj == k) v = -dcol[di] / pk;
+                else v = fma(-dcol[di], drow[dj], Ds[di][dj]);
+                Ds[di][dj] = v;
+            }
+            __syncthreads();
+        }
+        // Rs[c][k] = (D A_Pj)_k for own columns j = r + 16 c outside P (rows P read before the update)
+        for (int e = tid; e < ncl * SPD_BS; e += nt) {
+            const int c = e / SPD_BS, k = e % SPD_BS;
+            if (c == m || k >= bs) continue;
+            const double *aj = A + (size_t)c * n + p0;
+            double sacc = 0.0;
+            for (int l = 0; l < bs; ++l) sacc = fma(Ds[k][l], aj[l], sacc);
+            Rs[c * SPD_BS + k] = sacc;
+        }
+        __syncthreads();
+        for (int e = tid; e < ncl * n; e += nt) {
+            const int c = e / n, i = e % n;
+            double *aj = A + (size_t)c * n;
+            const bool inP = i >= p0 && i < p0 + bs;
+            if (c != m) {
+                if (inP) {
+                    aj[i] = Rs[c * SPD_BS + (i - p0)];
+                } else {
+                    double v = aj[i];
+                    for (int k = 0; k < bs; ++k) v = fma(-P[(size_t)k * n + i], Rs[c * SPD_BS + k], v);
+                    aj[i] = v;
+                }
+            } else {   // own column p0 + r of the pivot block
+                if (inP) {
+                    aj[i] = Ds[i - p0][r];
+                } else {
+                    double v = 0.0;
+                    for (int k = 0; k < bs; ++k) v = fma(-P[(size_t)k * n + i], Ds[k][r], v);
+                    aj[i] = v;
+                }
+            }
+        }
+        __syncthreads();
+        if (m + 1 < nblk) bcast(m + 1);
+        cl.sync();
+    }
+    for (int e = tid; e < ncl * n; e += nt) {
+        const int c = e / n, i = e % n;
+        Minv[i + (int64_t)(r + SPD_CL * c) * n] = A[e];
+    }
+    if (r == 0 && tid == 0 && bad) atomicOr(status, 1);
+}
+
 __global__ void __launch_bounds__(256) k_spd_inv(int64_t n, const double *__restrict__ M, int64_t ldm,
                                                  double *__restrict__ A, double *__restrict__ cbuf,
                                                  double *__restrict__ rbuf, int *status) {
@@ -888,11 +998,22 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
             cl_ok = 0;
         cudaGetLastError();
     }
-    if (cl_ok && n >= 1 && shm_cl <= (size_t)227 * 1024) {
+    const size_t shm_blk = ((size_t)cdiv(n, SPD_CL) * n + 2 * (size_t)SPD_BS * n + (size_t)cdiv(n, SPD_CL) * SPD_BS) *
+                           sizeof(double);
+    static int blk_ok = -1;
+    if (blk_ok < 0) {
+        blk_ok = (cl_ok && !getenv("HF_SPD_SCALAR")) ? 1 : 0;
+        if (blk_ok && (cudaFuncSetAttribute(k_spd_inv_blk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                       cudaFuncSetAttribute(k_spd_inv_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 223 * 1024) != cudaSuccess))
+            blk_ok = 0;   // 223 KB: its static shared arrays count against the 227 KB
+        cudaGetLastError();
+    }
+    if (cl_ok && n >= 1 && (shm_cl <= (size_t)227 * 1024 || (blk_ok && shm_blk <= (size_t)223 * 1024))) {
+        const bool blk = blk_ok && shm_blk <= (size_t)223 * 1024;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(SPD_CL);
         cfg.blockDim = dim3(512);
-        cfg.dynamicSmemBytes = shm_cl;
+        cfg.dynamicSmemBytes = blk ? shm_blk : shm_cl;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -902,7 +1023,8 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
         cfg.attrs = at;
         cfg.numAttrs = 1;
         const int ni = (int)n;
-        HF_CUDA(cudaLaunchKernelEx(&cfg, k_spd_inv_cl, ni, M, ldm, Minv, status));
+        if (blk) HF_CUDA(cudaLaunchKernelEx(&cfg, k_spd_inv_blk, ni, M, ldm, Minv, status));
+        else HF_CUDA(cudaLaunchKernelEx(&cfg, k_spd_inv_cl, ni, M, ldm, Minv, status));
         HF_CHECK_LAUNCH(ctx);
         return;
     }

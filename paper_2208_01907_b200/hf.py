@@ -31,7 +31,7 @@ EXPORTED = [
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
     "hf_stage1_partition", "hf_krylov_solve", "hf_lowfactor_export64", "hf_schur_gcr_dd",
     "hf_hybrid_export_dd", "hf_lowfactor_export_u", "hf_scale_full", "hf_solve_dd",
-    "hf_nd_blocks", "hf_factor_lowprec_blocks",
+    "hf_nd_blocks", "hf_factor_lowprec_blocks", "hf_gram_inverse",
 ]
 
 
@@ -100,6 +100,7 @@ def load() -> ctypes.CDLL:
         "hf_hybrid_destroy": [vp],
         "hf_trim_cache": [ctypes.c_int],
         "hf_precond_apply": [vp, vp, i64, vp, i64, vp, i64],
+        "hf_gram_inverse": [vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_int32)],
         "hf_shard_cols": [i64, ctypes.c_int, ctypes.c_int, pi64, pi64],
         "hf_set_virtual_rank": [vp, ctypes.c_int, ctypes.c_int],
         "hf_set_stage1_partitions": [vp, ctypes.c_int],
@@ -382,6 +383,20 @@ def hf_precond_apply(ctx: Context, lf: LowFactor, R: torch.Tensor, W: torch.Tens
         W = torch.empty(ncol, lf.L, dtype=torch.float64, device=R.device).T
     ctx.check(ctx.lib.hf_precond_apply(ctx.h, lf.h, ncol, _ptr(R), lf.L, _ptr(W), lf.L))
     return W
+
+
+def hf_gram_inverse(ctx: Context, M: torch.Tensor) -> tuple[torch.Tensor, bool]:
+    """(M^{-1}, breakdown) for the SPD Gram matrix of Alg. 5.  M: CUDA float64
+    (n, n), column-major or symmetric.  Returns Minv column-major (n, n) and the breakdown flag."""
+    if not (isinstance(M, torch.Tensor) and M.is_cuda and M.dtype == torch.float64 and M.dim() == 2
+            and M.shape[0] == M.shape[1]):
+        raise TypeError("M must be a square CUDA float64 tensor")
+    n = M.shape[0]
+    Mc = M if (n <= 1 or M.stride() == (1, n)) else M.T.contiguous().T
+    Minv = torch.empty(n, n, dtype=torch.float64, device=M.device).T
+    bd = ctypes.c_int32(0)
+    ctx.check(ctx.lib.hf_gram_inverse(ctx.h, n, _ptr(Mc), max(n, 1), _ptr(Minv), ctypes.byref(bd)))
+    return Minv, bool(bd.value)
 
 
 KRYLOV = {"ir": 0, "gcr": 1, "bgcr": 2}
