@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(512) k_spd_inv_cl(int n, const double *__restr
 // scalar elimination, so the breakdown test [R11] is unchanged) and applies the block pivot
 //   A_PP <- D = A_PP^{-1},  A_Pj <- D A_Pj,  A_iP <- -A_iP D,  A_ij <- A_ij - A_iP D A_Pj
 // to its own columns: n / 16 barriers instead of n.
-constexpr int SPD_BS = 16;
+constexpr int SPD_BS = SPD_CL;   // one column of every pivot block per CTA (the layout requires it)
 __global__ void __launch_bounds__(512) k_spd_inv_blk(int n, const double *__restrict__ M, int64_t ldm,
                                                      double *__restrict__ Minv, int *status) {
     cg::cluster_group cl = cg::this_cluster();
