@@ -819,6 +819,172 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
 #undef CC
 }
 
+// Persistent form of k_trailing_c (symmetric): two CTAs per SM walk the lower-triangle
+// tiles t = blockIdx.x, + gridDim.x, ...  While a tile is computed, each thread gathers the
+// 64 start values (seeds) IT will need for its next tile into shared memory with 4-byte
+// cp.async (zero-filled outside the triangle), so the scattered gather through the
+// compaction map -- most of a tile's non-FMA time in k_trailing_c -- overlaps the FMA
+// loop.  Each thread reads back only what it gathered itself: no barrier on the seed
+// buffer.  Same single fmaf chain per entry in pivot order (bit-identical).
+constexpr size_t TRAIL_P_SMEM = TRAIL_C_SMEM + (size_t)TB * TB * sizeof(float);   // + seeds
+__device__ __forceinline__ void cp_async4_z(void *sdst, const void *gsrc, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gsrc), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void tile_of(int64_t t, int64_t &bi, int64_t &bj) {
+    bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    bj = t - bi * (bi + 1) / 2;
+}
+__global__ void __launch_bounds__(256, 2) k_trailing_p(TrailArgs a, int64_t ntiles) {
+    if (a.status[2]) return;
+    extern __shared__ __align__(16) float dsm_t[];
+    float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t);
+    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t + TNS * TK * TB);
+    float *Sd = dsm_t + 2 * TNS * TK * TB;   // [TB cols][TB rows] seeds of the current tile
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int nchunk = (a.nbp + TK - 1) / TK;
+#define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
+#define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+    // this thread's 64 seeds of tile t -> Sd (its own entries only), one commit group
+    auto gather = [&](int64_t t) {
+        if (t < ntiles) {
+            int64_t bi, bj;
+            tile_of(t, bi, bj);
+            const int64_t row0 = bi * TB, col0 = bj * TB;
+            int32_t rm[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) rm[q] = (row0 + RR(q) < a.mp) ? a.map[row0 + RR(q)] : -1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int cl = CC(c);
+                const int32_t cm = (col0 + cl < a.mp) ? a.map[col0 + cl] : -1;
+                const float *colp = a.Vold + (int64_t)(cm >= 0 ? cm : 0) * a.ldv;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const bool ok = cm >= 0 && rm[q] >= cm;
+                    cp_async4_z(&Sd[cl * TB + RR(q)], ok ? colp + rm[q] : a.Vold, ok);
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    gather(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t bi, bj;
+        tile_of(t, bi, bj);
+        const int64_t row0 = bi * TB, col0 = bj * TB;
+        const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
+        auto issue = [&](int c) {
+            if (c < nchunk) {
+                const int st = c % TNS;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int e = tid + u * 256;
+                    const int k = e >> 5, r4 = (e & 31) * 4;
+                    const int64_t off = (int64_t)(c * TK + k) * a.ldc;
+                    cp_async16_g(&As[st][k][r4], a.Snc + off + row0 + r4);
+                    cp_async16_g(&Bs[st][k][r4], a.Sc + off + col0 + r4);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        // the previous tile's readers of the operand stages are done (barrier at its loop end)
+        issue(0);
+        issue(1);
+        // groups now: [seeds(t)], chunk0, chunk1 -> seeds(t) complete
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
+        float2 acc[8][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float *sc = Sd + CC(2 * j + h) * TB;
+                const float4 lo = *reinterpret_cast<const float4 *>(sc + tx * 4);
+                const float4 hi = *reinterpret_cast<const float4 *>(sc + 64 + tx * 4);
+                const float v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (h) acc[q][j].y = v[q];
+                    else acc[q][j].x = v[q];
+                }
+            }
+        }
+        for (int c = 0; c < nchunk; ++c) {
+            // commit order: chunk0, chunk1, [wait c=0] chunk2, seeds(next), [c=1] chunk3, [c=2]
+            // chunk4, ... -> chunk c is complete when at most 1 (c = 0), 2 (c = 1, 2) or
+            // 1 (c >= 3) newer groups are pending
+            if (c == 1 || c == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            issue(c + 2);
+            const int st = c % TNS;
+            const int kmax = min(TK, a.nbp - c * TK);
+            if (kmax == TK) {
+#pragma unroll
+                for (int kk = 0; kk < TK; ++kk) {
+                    const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                    const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                    const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                          make_float2(b1.z, b1.w)};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+                }
+            } else {
+                for (int kk = 0; kk < kmax; ++kk) {
+                    const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                    const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                    const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                          make_float2(b1.z, b1.w)};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+                }
+            }
+            // the next tile's seeds into this thread's own Sd entries: issued after the first
+            // chunk's FMAs consumed the values read from them
+            if (c == 0) gather(t + gridDim.x);
+        }
+        __syncthreads();   // every thread is done with the operand stages before the next tile's issue
+        const bool full = row0 > col0 && mpr == TB && mpc == TB && (a.ldv & 3) == 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cl = CC(2 * j + h);
+                float *colp = a.Vnew + (col0 + cl) * a.ldv + row0;
+                if (full) {
+                    *reinterpret_cast<float4 *>(colp + tx * 4) =
+                        h ? make_float4(acc[0][j].y, acc[1][j].y, acc[2][j].y, acc[3][j].y)
+                          : make_float4(acc[0][j].x, acc[1][j].x, acc[2][j].x, acc[3][j].x);
+                    *reinterpret_cast<float4 *>(colp + 64 + tx * 4) =
+                        h ? make_float4(acc[4][j].y, acc[5][j].y, acc[6][j].y, acc[7][j].y)
+                          : make_float4(acc[4][j].x, acc[5][j].x, acc[6][j].x, acc[7][j].x);
+                } else if (cl < mpc) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int rl = RR(q);
+                        if (rl < mpr && row0 + rl >= col0 + cl) colp[rl] = h ? acc[q][j].y : acc[q][j].x;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#undef RR
+#undef CC
+}
+
 // ------------------------------------------------------------------ partitioned trailing update
 // Column partition g (multi-GPU stage 1 / its emulation): FULL columns, every
 // active row.  Tile grid = row tiles x local column tiles (no triangle); entry
@@ -1191,6 +1357,19 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    // persistent trailing kernel (seed prefetch), two CTAs per SM -- OFF by default: measured
+    // 38.3 vs 31.0 ms per C2 step (FMA pipe 64.8 vs 71.5 % active; the 4-byte cp.async seed
+    // gather adds 155 MB of DRAM reads per large launch and leaves fewer warps resident).
+    // HF_TRAIL_PERSIST=1: for launches of more than two tiles per CTA, =2: at any size (tests)
+    const int pmode = getenv("HF_TRAIL_PERSIST") ? atoi(getenv("HF_TRAIL_PERSIST")) : 0;
+    const bool persist = pmode != 0;
+    int pgrid = 0;
+    if (persist) {
+        HF_CUDA(cudaFuncSetAttribute(k_trailing_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_P_SMEM));
+        int occ = 0;
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trailing_p, 256, TRAIL_P_SMEM));
+        pgrid = std::max(1, occ) * nsm;
+    }
     DBuf<int32_t> blkd, bstate;   // NEXT-4: block of every original index; {block, first, attempt}
     if (blk_host) {
         blkd.alloc(std::max<int64_t>(L, 1), st);
@@ -1272,8 +1451,13 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                     HF_CHECK_LAUNCH(ctx);
                 }
                 ClassTimer tm(ctx, "trailing");
-                if (Sc.p) k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
-                else k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
+                if (Sc.p && persist && (ntiles > 2 * pgrid || pmode == 2)) {
+                    k_trailing_p<<<(unsigned)pgrid, 256, TRAIL_P_SMEM, st>>>(ta, ntiles);
+                } else if (Sc.p) {
+                    k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
+                } else {
+                    k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
+                }
                 HF_CHECK_LAUNCH(ctx);
                 vb ^= 1;
             } else {

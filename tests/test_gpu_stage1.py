@@ -123,3 +123,21 @@ def test_stage1_lookahead_schedule_bitwise():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name,seed,nb", [("P512", 2, 0), ("P1024", 1, 0), ("P2048", 0, 64), ("S24", 0, 16),
+                                         ("C0", 3, 8)])
+def test_stage1_persistent_trailing_bitwise(ctx, name, seed, nb, monkeypatch):
+    """The persistent trailing kernel (k_trailing_p: seeds of the next tile gathered by
+    cp.async during the current one) forced at every size (HF_TRAIL_PERSIST=2; by default
+    it runs only for launches of more than two tiles per CTA, C2-sized panels): same bits
+    as the oracle, including ragged last chunks (nb = 8, 64) and tiny trailing matrices."""
+    monkeypatch.setenv("HF_TRAIL_PERSIST", "2")
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    _, _, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min, nb=nb)
+    assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+    if Fo.N:
+        assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
