@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     bool stopped = false;
     const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
     unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = dbg ? gtimer() : 0;
+    uint32_t spec2 = 0xFFFFFFFFu, spec3 = 0xFFFFFFFFu;   // HF_CHAIN_DEBUG speculation statistics
 #define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
     for (; t < nb;) {
         const int64_t k = a.K0 + t;
@@ -324,6 +325,26 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
                 if (lane == 0) {
                     bkey = mx;
                     pcol = (uint32_t)(mi >> 32);
+                }
+                if (a.dbg && blockIdx.x == 0 && !PARTS) {
+                    // speculation statistics: is this step's pivot the runner-up (or third) of
+                    // the previous step's per-CTA candidates? (positions; HF_CHAIN_DEBUG only)
+                    const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
+                    uint64_t v0 = lane < G ? (ld_relaxed_u64(&sl[(size_t)lane * SLOT_STRIDE]) & ~TAGM) : 0;
+                    uint64_t v1 = lane + 32 < G ? (ld_relaxed_u64(&sl[(size_t)(lane + 32) * SLOT_STRIDE]) & ~TAGM) : 0;
+                    const uint64_t k1 = warp_max64(umax64(v0, v1));
+                    const uint64_t k2 = warp_max64(umax64(v0 < k1 ? v0 : 0, v1 < k1 ? v1 : 0));
+                    const uint64_t k3 = warp_max64(umax64(v0 < k2 ? v0 : 0, v1 < k2 ? v1 : 0));
+                    const uint32_t p1 = (uint32_t)((k1 >> 15) & POS_MAX);
+                    if (lane == 0) {
+                        if (t > 0) {
+                            a.dbg[7] += 1;
+                            if (p1 == spec2) a.dbg[5] += 1;
+                            if (p1 == spec2 || p1 == spec3) a.dbg[6] += 1;
+                        }
+                        spec2 = k2 ? (uint32_t)((k2 >> 15) & POS_MAX) : 0xFFFFFFFFu;
+                        spec3 = k3 ? (uint32_t)((k3 >> 15) & POS_MAX) : 0xFFFFFFFFu;
+                    }
                 }
             }
         } else if (tid == 0) {
@@ -1201,6 +1222,9 @@ static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_
         const double np = hd[4] ? (double)hd[4] : 1.0;
         fprintf(stderr, "[hf chain] steps %llu  us/step: publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
                 hd[4], hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
+        if (hd[7])
+            fprintf(stderr, "[hf chain] pivot = previous step's runner-up candidate: %.1f %%, runner-up or third: %.1f %%\n",
+                    100.0 * hd[5] / hd[7], 100.0 * hd[6] / hd[7]);
     }
     // [R5] floor and [R9] enlargement: the last accepted pivots move to Lambda_2
     int64_t N = Ntau;
