@@ -755,9 +755,12 @@ __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *
             if (tid == 0) {
                 gbest[(size_t)par * 2 * G + 2 * c] = bd;
                 gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
+                // p leaves the active set BEFORE the barrier (this step skips p explicitly, so
+                // no reader of this step depends on act[p]); the barrier publishes it to the
+                // next step's readers
+                act[p] = 0;
             }
-            grid.sync();   // everyone has used act[] and column p of this step
-            if (c == 0 && tid == 0) act[p] = 0;
+            grid.sync();
             ++nblk;
             k += 1;
         } else {
@@ -811,14 +814,182 @@ __global__ void __launch_bounds__(256) k_hard_factor_f(int64_t n, const double *
             if (tid == 0) {
                 gbest[(size_t)par * 2 * G + 2 * c] = bd;
                 gbest[(size_t)par * 2 * G + 2 * c + 1] = bo;
+                act[p] = act[q] = 0;   // before the barrier, as for the 1x1 pivot
             }
             grid.sync();
-            if (c == 0 && tid == 0) act[p] = act[q] = 0;
             ++nblk;
             k += 2;
         }
     }
     if (c == 0 && tid == 0) *rank_out = k;
+}
+
+// The fused factorization on one 16-CTA CLUSTER (n <= 600): CTA r holds the columns
+// j = r + 16 c of the symmetrized S22 in shared memory; the pivot column(s) are read from
+// their owner's shared memory (never modified after the decision), the per-CTA bests go into
+// every CTA's shared slot array (double buffered by step parity), and one cluster barrier
+// per pivot replaces the grid barrier.  Per-entry arithmetic, tie rules and outputs are
+// those of k_hard_factor_f (bit-identical results).
+constexpr int HC = 16;
+__global__ void __launch_bounds__(512) k_hard_factor_cl(int n, const double *__restrict__ S, double thr,
+                                                        double *__restrict__ Lcol, int32_t *__restrict__ posof,
+                                                        double *__restrict__ Dh, int32_t *__restrict__ blocks,
+                                                        int32_t *__restrict__ pivots, int64_t *rank_out) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double smh[];
+    __shared__ Best sh[72];
+    __shared__ Best BB[2][HC][2];
+    __shared__ Best sdg, soff;
+    const int r = (int)cl.block_rank(), tid = threadIdx.x, nt = blockDim.x;
+    const int ncl = (n - r + HC - 1) / HC;
+    const int ncmax = (n + HC - 1) / HC;
+    double *A = smh;                                  // [ncmax][n], local column c = global r + 16 c
+    double *PC = A + (size_t)ncmax * n;               // [2][n] pivot column(s) of this step
+    int32_t *act = reinterpret_cast<int32_t *>(PC + 2 * (size_t)n);   // [n]
+    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+    Best bo{-1.0, 0, 0, -1, -1}, bd{-1.0, 0, 0, -1, -1};
+    for (int e = tid; e < ncl * n; e += nt) {
+        const int c = e / n, i = e % n;
+        const int64_t j = r + HC * c;
+        const double v = 0.5 * (S[i + j * n] + S[j + (int64_t)i * n]);
+        A[e] = v;
+        Dh[i + j * n] = 0.0;
+        if (i == j) {
+            Best cd{fabs(v), i, 0, i, i};
+            if (better(cd, bd)) bd = cd;
+        } else {
+            Best cd{fabs(v), min((int64_t)i, j), max((int64_t)i, j), i, j};
+            if (better(cd, bo)) bo = cd;
+        }
+    }
+    for (int i = tid; i < n; i += nt) {
+        act[i] = 1;
+        if (r == 0) {
+            posof[i] = -1;
+            blocks[i] = 0;
+        }
+    }
+    int par = 0;
+    auto publish = [&]() {   // this CTA's bests -> slot r of every CTA (parity par)
+        block_best2(bd, bo, sh);
+        if (tid < HC) {
+            Best *dst = cl.map_shared_rank(&BB[par][r][0], tid);
+            dst[0] = bd;
+            dst[1] = bo;
+        }
+    };
+    publish();
+    cl.sync();
+    int k = 0, nblk = 0;
+    while (k < n) {
+        if (tid < 32) {
+            Best d0 = tid < HC ? BB[par][tid][0] : Best{-1.0, 0, 0, -1, -1};
+            Best o0 = tid < HC ? BB[par][tid][1] : Best{-1.0, 0, 0, -1, -1};
+            warp_best(d0);
+            warp_best(o0);
+            if (tid == 0) {
+                sdg = d0;
+                soff = o0;
+            }
+        }
+        __syncthreads();
+        const Best d0 = sdg, o0 = soff;
+        const double mu1 = d0.v, mu0 = fmax(d0.v, o0.v);
+        if (mu0 <= thr) break;   // uniform across the cluster
+        par ^= 1;
+        bo = Best{-1.0, 0, 0, -1, -1};
+        bd = Best{-1.0, 0, 0, -1, -1};
+        const bool one = mu1 >= alpha * mu0;
+        const int p = one ? (int)d0.i : (int)min(o0.i, o0.j), q = one ? -1 : (int)max(o0.i, o0.j);
+        {   // pivot column(s) from their owners' shared memory (not modified in this step)
+            const double *sp = cl.map_shared_rank(A, p % HC) + (size_t)(p / HC) * n;
+            for (int i = tid; i < n; i += nt) PC[i] = sp[i];
+            if (!one) {
+                const double *sq = cl.map_shared_rank(A, q % HC) + (size_t)(q / HC) * n;
+                for (int i = tid; i < n; i += nt) PC[n + i] = sq[i];
+            }
+        }
+        __syncthreads();
+        const double *ap = PC, *aq = PC + n;
+        if (one) {
+            const double d = ap[p];
+            for (int e = tid; e < ncl * n; e += nt) {
+                const int c = e / n, i = e % n;
+                const int j = r + HC * c;
+                if (!act[j] || j == p || !act[i] || i == p) continue;
+                const double v = A[e] - (ap[i] * ap[j]) / d;
+                A[e] = v;
+                if (i == j) {
+                    Best cd{fabs(v), i, 0, i, i};
+                    if (better(cd, bd)) bd = cd;
+                } else {
+                    Best cd{fabs(v), min(i, j), max(i, j), i, j};
+                    if (better(cd, bo)) bo = cd;
+                }
+            }
+            if (r == 0) {
+                for (int i = tid; i < n; i += nt) Lcol[i + (int64_t)k * n] = (act[i] && i != p) ? ap[i] / d : 0.0;
+                if (tid == 0) {
+                    Dh[k + (int64_t)k * n] = d;
+                    blocks[nblk] = 1;
+                    pivots[k] = p;
+                    posof[p] = k;
+                }
+            }
+        } else {
+            const double a_ = ap[p], b_ = ap[q], c_ = aq[q];
+            const double det = a_ * c_ - b_ * b_;
+            const double E0 = c_ / det, E1 = -b_ / det, E2 = -b_ / det, E3 = a_ / det;
+            for (int e = tid; e < ncl * n; e += nt) {
+                const int c = e / n, i = e % n;
+                const int j = r + HC * c;
+                if (!act[j] || j == p || j == q || !act[i] || i == p || i == q) continue;
+                const double cc0 = ap[j], cc1 = aq[j];
+                const double lc0 = cc0 * E0 + cc1 * E1, lc1 = cc0 * E2 + cc1 * E3;
+                const double cr0 = ap[i], cr1 = aq[i];
+                const double lr0 = cr0 * E0 + cr1 * E1, lr1 = cr0 * E2 + cr1 * E3;
+                const double t1 = lr0 * cc0 + lr1 * cc1, t2 = lc0 * cr0 + lc1 * cr1;
+                const double v = A[e] - 0.5 * (t1 + t2);
+                A[e] = v;
+                if (i == j) {
+                    Best cd{fabs(v), i, 0, i, i};
+                    if (better(cd, bd)) bd = cd;
+                } else {
+                    Best cd{fabs(v), min(i, j), max(i, j), i, j};
+                    if (better(cd, bo)) bo = cd;
+                }
+            }
+            if (r == 0) {
+                for (int i = tid; i < n; i += nt) {
+                    const bool ok = act[i] && i != p && i != q;
+                    const double cr0 = ap[i], cr1 = aq[i];
+                    Lcol[i + (int64_t)k * n] = ok ? cr0 * E0 + cr1 * E1 : 0.0;
+                    Lcol[i + (int64_t)(k + 1) * n] = ok ? cr0 * E2 + cr1 * E3 : 0.0;
+                }
+                if (tid == 0) {
+                    Dh[k + (int64_t)k * n] = a_;
+                    Dh[k + 1 + (int64_t)k * n] = b_;
+                    Dh[k + (int64_t)(k + 1) * n] = b_;
+                    Dh[k + 1 + (int64_t)(k + 1) * n] = c_;
+                    blocks[nblk] = 2;
+                    pivots[k] = p;
+                    pivots[k + 1] = q;
+                    posof[p] = k;
+                    posof[q] = k + 1;
+                }
+            }
+        }
+        __syncthreads();   // every reader of act[] in this CTA is done
+        if (tid == 0) {
+            act[p] = 0;
+            if (!one) act[q] = 0;
+        }
+        publish();          // (block_best2's barriers order the act[] writes for this CTA)
+        cl.sync();
+        ++nblk;
+        k += one ? 1 : 2;
+    }
+    if (r == 0 && tid == 0) *rank_out = k;
 }
 
 // lab[pos] = Lambda_2 position at pivoted position pos (pivots first, then the
@@ -1052,8 +1223,35 @@ void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A,
     gb.alloc((size_t)4 * G, st);   // [2 step parities][2 G]
     void *args[] = {&n, &S, &thr, &A, &Lcol.p, &act, &posof, &gb.p, &Dh, &blocks, &piv, &rank_dev};
     static const bool unfused = getenv("HF_HARD_UNFUSED") != nullptr;   // the 3-barrier reference variant
-    HF_CUDA(cudaLaunchCooperativeKernel(unfused ? (void *)k_hard_factor_mc : (void *)k_hard_factor_f, dim3(G),
-                                        dim3(256), args, 0, st));
+    // the 16-CTA cluster kernel for n <= 600 (HF_HARD_NOCLUSTER: the cooperative one)
+    const size_t shm_cl = ((size_t)cdiv(n, HC) * n + 2 * (size_t)n) * sizeof(double) + (size_t)n * sizeof(int32_t);
+    static int hcl_ok = -1;
+    if (hcl_ok < 0) {
+        hcl_ok = getenv("HF_HARD_NOCLUSTER") ? 0 : 1;
+        if (hcl_ok && (cudaFuncSetAttribute(k_hard_factor_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                       cudaFuncSetAttribute(k_hard_factor_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess))
+            hcl_ok = 0;
+        cudaGetLastError();
+    }
+    if (hcl_ok && !unfused && n >= 1 && n <= 600 && shm_cl <= (size_t)200 * 1024) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(HC);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = shm_cl;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = HC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const int ni = (int)n;
+        HF_CUDA(cudaLaunchKernelEx(&cfg, k_hard_factor_cl, ni, S, thr, Lcol.p, posof, Dh, blocks, piv, rank_dev));
+    } else {
+        HF_CUDA(cudaLaunchCooperativeKernel(unfused ? (void *)k_hard_factor_mc : (void *)k_hard_factor_f, dim3(G),
+                                            dim3(256), args, 0, st));
+    }
     HF_CHECK_LAUNCH(ctx);
     k_hard_assemble<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 4096), 256, 0, st>>>(n, rank_dev, Lcol.p, posof,
                                                                                         piv, lab, Lh);
