@@ -34,7 +34,7 @@ struct GcrWork {
     DBuf<double> Minv;       // cap * n * n
     DBuf<double> R, H, G, Mn, An, C;
     DBuf<double> bn2, rn2, res;
-    DBuf<double> dgw, chw, chdg;
+    DBuf<double> dgw, dgw2, chw, chdg;
     DBuf<int> status;
     std::vector<double> *hist = nullptr;   // optional: max relative residual after every iteration
 };
@@ -107,12 +107,12 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
             const double *Pn = w.P.p + (size_t)it * n * L;
             const double *Qn = w.Q.p + (size_t)it * n * L;
             double *Minv = w.Minv.p + (size_t)it * n * n;
-            dgemm(ctx, true, n, n, L, 1.0, Qn, L, Qn, L, 0.0, w.Mn.p, n, nullptr, &w.dgw);   // M_n
-            dgemm(ctx, true, n, n, L, 1.0, Qn, L, R, L, 0.0, w.An.p, n, nullptr, &w.dgw);    // A_n
+            dgemm2(ctx, true, n, n, L, 1.0, Qn, L, Qn, L, 0.0, w.Mn.p, n,                    // M_n
+                   1.0, Qn, L, R, L, 0.0, w.An.p, n, &w.dgw, &w.dgw2);                      // A_n
             spd_inverse(ctx, n, w.Mn.p, n, Minv, w.chw, w.chdg, w.status.p);
             dgemm(ctx, false, n, n, n, 1.0, Minv, n, w.An.p, n, 0.0, w.C.p, n, nullptr, &w.dgw, 1);
-            dgemm(ctx, false, L, n, n, 1.0, Pn, L, w.C.p, n, 1.0, X, L, nullptr, &w.dgw, 1);   // x += p C
-            dgemm(ctx, false, L, n, n, -1.0, Qn, L, w.C.p, n, 1.0, R, L, nullptr, &w.dgw, 1);  // r -= q C
+            dgemm2(ctx, false, L, n, n, 1.0, Pn, L, w.C.p, n, 1.0, X, L,                      // x += p C
+                   -1.0, Qn, L, w.C.p, n, 1.0, R, L, &w.dgw, &w.dgw2, 1);                     // r -= q C
             colnorm2(ctx, L, n, R, L, w.rn2.p);
             maxres(ctx, n, w.rn2.p, w.bn2.p, w.res.p);
             res = read_res(ctx, w, &bad);
@@ -141,8 +141,8 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
             for (int m = 0; m <= it; ++m)                                   // G_m = -M_m^{-1} Q_m^T z
                 dgemm(ctx, false, n, n, n, -1.0, w.Minv.p + (size_t)m * n * n, n, w.H.p + (size_t)m * n, nb, 0.0,
                       w.G.p + (size_t)m * n, nb, nullptr, &w.dgw, 1);
-            dgemm(ctx, false, L, n, nb, 1.0, w.P.p, L, w.G.p, nb, 1.0, Pn1, L, nullptr, &w.dgw);  // p_{n+1}
-            dgemm(ctx, false, L, n, nb, 1.0, w.Q.p, L, w.G.p, nb, 1.0, Qn1, L, nullptr, &w.dgw);  // q_{n+1}
+            dgemm2(ctx, false, L, n, nb, 1.0, w.P.p, L, w.G.p, nb, 1.0, Pn1, L,               // p_{n+1}
+                   1.0, w.Q.p, L, w.G.p, nb, 1.0, Qn1, L, &w.dgw, &w.dgw2);                   // q_{n+1}
         }
     }
     info->iters = iters;

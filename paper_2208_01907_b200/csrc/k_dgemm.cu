@@ -40,15 +40,23 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// up to two problems of the same shape in one launch (blockIdx.z = problem * splits + split)
+struct DgemmBatch {
+    DgemmArgs g[2];
+    int splits;
+};
+
 template <bool TRANS_A>
-__global__ void __launch_bounds__(128) k_dgemm(DgemmArgs g) {
+__global__ void __launch_bounds__(128) k_dgemm(DgemmBatch gb) {
     extern __shared__ __align__(16) double sm[];
+    const int zs = (int)blockIdx.z % gb.splits, nsplit = gb.splits;
+    const DgemmArgs g = ((int)blockIdx.z >= gb.splits) ? gb.g[1] : gb.g[0];   // no dynamic param indexing
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
     const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
     // K range of this split
-    const int64_t kper = ((g.K + gridDim.z - 1) / gridDim.z + BK - 1) / BK * BK;
-    const int64_t kbeg = (int64_t)blockIdx.z * kper;
+    const int64_t kper = ((g.K + nsplit - 1) / nsplit + BK - 1) / BK * BK;
+    const int64_t kbeg = (int64_t)zs * kper;
     const int64_t kend = min(g.K, kbeg + kper);
     const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(128) k_dgemm(DgemmArgs g) {
     cp_wait<0>();
 
     // epilogue: fragment (row = lane/4, cols 2*(lane%4) + {0,1})
-    const bool partial = gridDim.z > 1;
+    const bool partial = nsplit > 1;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int64_t gm = m0 + wm * 32 + i * 8 + (lane >> 2);
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(128) k_dgemm(DgemmArgs g) {
                 const int64_t gn = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
                 if (gn >= g.N) continue;
                 if (partial) {
-                    g.W[(size_t)blockIdx.z * g.M * g.N + gm + gn * g.M] = acc[i][j][h];
+                    g.W[(size_t)zs * g.M * g.N + gm + gn * g.M] = acc[i][j][h];
                 } else {
                     double *c = g.C + gm + gn * g.ldc;
                     const double ab = keep ? __dmul_rn(g.alpha, acc[i][j][h]) : 0.0;
@@ -158,9 +166,9 @@ __global__ void k_reduce(DgemmArgs g, int splits) {
 
 }  // namespace
 
-void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
-           int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
-           const uint8_t *rowmask, DBuf<double> *work, int splits) {
+static void dgemm_launch(hf_ctx *ctx, bool transA, int nprob, const DgemmArgs *gs, DBuf<double> *const *work,
+                         int splits) {
+    const int64_t M = gs[0].M, N = gs[0].N, K = gs[0].K;
     if (M <= 0 || N <= 0) return;
     cudaStream_t st = ctx->stream;
     const int64_t mt = cdiv(M, BM), nt = cdiv(N, BN);
@@ -181,7 +189,7 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
         double best = -1.0;
         splits = 1;
         for (int64_t sp = 1; sp <= smax; ++sp) {
-            const double w = (double)(mt * nt * sp) / (double)slots;
+            const double w = (double)(mt * nt * sp * nprob) / (double)slots;
             const double eff = w / std::ceil(w);
             if (eff > best + 0.02) {
                 best = eff;
@@ -190,22 +198,47 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
         }
     }
     if (K == 0) splits = 1;
-    DgemmArgs g{M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, rowmask, nullptr};
-    if (splits > 1) {
-        work->alloc((size_t)splits * M * N, st);
-        g.W = work->p;
+    DgemmBatch gb;
+    gb.splits = splits;
+    for (int b = 0; b < nprob; ++b) {
+        gb.g[b] = gs[b];
+        if (splits > 1) {
+            work[b]->alloc((size_t)splits * M * N, st);
+            gb.g[b].W = work[b]->p;
+        }
     }
+    if (nprob == 1) gb.g[1] = gb.g[0];
     const size_t shm = shm0;
     ClassTimer tm(ctx, "dgemm");
-    dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
-    if (transA) k_dgemm<true><<<grid, 128, shm, st>>>(g);
-    else k_dgemm<false><<<grid, 128, shm, st>>>(g);
+    dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(splits * nprob));
+    if (transA) k_dgemm<true><<<grid, 128, shm, st>>>(gb);
+    else k_dgemm<false><<<grid, 128, shm, st>>>(gb);
     HF_CHECK_LAUNCH(ctx);
     if (splits > 1) {
         const int64_t total = M * N;
-        k_reduce<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 4096), 256, 0, st>>>(g, splits);
-        HF_CHECK_LAUNCH(ctx);
+        for (int b = 0; b < nprob; ++b) {
+            k_reduce<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 4096), 256, 0, st>>>(gb.g[b], splits);
+            HF_CHECK_LAUNCH(ctx);
+        }
     }
+}
+
+void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+           int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+           const uint8_t *rowmask, DBuf<double> *work, int splits) {
+    const DgemmArgs g{M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, rowmask, nullptr};
+    DBuf<double> *w[1] = {work};
+    dgemm_launch(ctx, transA, 1, &g, w, splits);
+}
+
+void dgemm2(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha0, const double *A0,
+            int64_t lda0, const double *B0, int64_t ldb0, double beta0, double *C0, int64_t ldc0, double alpha1,
+            const double *A1, int64_t lda1, const double *B1, int64_t ldb1, double beta1, double *C1, int64_t ldc1,
+            DBuf<double> *work0, DBuf<double> *work1, int splits) {
+    const DgemmArgs g[2] = {{M, N, K, alpha0, A0, lda0, B0, ldb0, beta0, C0, ldc0, nullptr, nullptr},
+                            {M, N, K, alpha1, A1, lda1, B1, ldb1, beta1, C1, ldc1, nullptr, nullptr}};
+    DBuf<double> *w[2] = {work0, work1};
+    dgemm_launch(ctx, transA, 2, g, w, splits);
 }
 
 }  // namespace hf

@@ -18,6 +18,13 @@ struct DgemmArgs {
     double *W;               // split-K partials
 };
 
+// Two problems of the same shape (no row mask) in one launch: C_b = beta_b C_b + alpha_b op(A_b) B_b
+// (better wave fill for the small block updates of Alg. 5); separate split-K work buffers.
+void dgemm2(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha0, const double *A0,
+            int64_t lda0, const double *B0, int64_t ldb0, double beta0, double *C0, int64_t ldc0, double alpha1,
+            const double *A1, int64_t lda1, const double *B1, int64_t ldb1, double beta1, double *C1, int64_t ldc1,
+            DBuf<double> *work0, DBuf<double> *work1, int splits = 0);
+
 // C = beta*C + alpha * rowmask o (op(A) B); splits <= 0 = automatic.
 void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
            int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
