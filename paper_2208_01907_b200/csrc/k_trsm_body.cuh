@@ -412,18 +412,17 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             load_dep(1, r0, (int64_t)phys(q_lo + 1) * TBS, c0);
             cp_commit();
         }
+        // one barrier per tile: it publishes stage dq and frees stage (dq + 2) % 3 (read in
+        // the previous iteration), which is refilled right after it
         for (int dq = 0; dq < ndep; ++dq) {
+            if (dq + 1 < ndep) cp_wait_1();
+            else cp_wait_all();
+            bar_sync(5, NCOMP);
             if (dq + 2 < ndep) {
                 ensure(dq + 2);
                 load_dep((dq + 2) % 3, r0, (int64_t)phys(q_lo + dq + 2) * TBS, c0);
                 cp_commit();
-                cp_wait_2();
-            } else if (dq + 1 < ndep) {
-                cp_wait_1();
-            } else {
-                cp_wait_all();
             }
-            bar_sync(5, NCOMP);
             const T *As = sm + (dq % 3) * 2 * TILE;
             if constexpr (sizeof(T) == 4) {
                 if (h2) tile_prod48(*reinterpret_cast<float2 (*)[4][4]>(h2), reinterpret_cast<const float *>(As),
@@ -432,8 +431,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_trsm(TrsmArgs a) {
             } else {
                 tile_fma(t, As, As + TILE, tr, tc);
             }
-            bar_sync(5, NCOMP);
         }
+        bar_sync(5, NCOMP);   // the stage buffers are free for the caller
     };
     // out = Dinv_j RHS_j (no dependency): forward truncates R (FP64, original order)
     // to FP32, backward starts from z = D^{-1} y
