@@ -7,10 +7,13 @@ constexpr int EPC = 16 / (int)sizeof(T);   // elements per 16-byte cp.async chun
 // ------------------------------------------------------------------ setup kernels
 // Lp (Np x Np, ld Np) = Lfac (N x N, ld N) padded with the identity; Up = Lp^T.
 // 32x32 tiles through shared memory so both the read and the transposed write
-// are coalesced.
+// are coalesced.  Only the lower tiles of Lp (and so the upper tiles of Up) are
+// written: nothing reads the other triangle (the diagonal-block inverses use the
+// strictly lower entries, the solves the off-diagonal blocks below / above).
 __global__ void __launch_bounds__(256) k_pad_transpose(int64_t N, int64_t Np, const T *__restrict__ Lf,
                                                        T *__restrict__ Lp, T *__restrict__ Up) {
     __shared__ T t[32][33];
+    if (blockIdx.x < blockIdx.y) return;   // a tile strictly above the diagonal
     const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
     for (int q = ty; q < 32; q += 8) {
