@@ -184,6 +184,18 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(x: float) -> float:
+    """Sum of a per-rank scalar over the default process group (identity without one)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -333,7 +345,8 @@ def main():
     ms_step = elapsed / args.steps
     # replicas: every rank factorises its own matrix (weak scaling); shard: one
     # factorization per step with stage 2 split over the ranks (strong scaling)
-    total_flops = fm["total"] * (world if args.mode == "replicas" else 1)
+    # (replicas: each rank's own matrix and iteration count, summed over the ranks)
+    total_flops = sum_over_ranks(fm["total"]) if args.mode == "replicas" else fm["total"]
     value = total_flops / (ms_step * 1e-3) / 1e12
 
     # ---- roofline of the dominant compute kernel (the FP32 trailing update)

@@ -37,6 +37,7 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(allp, mine)
             out[n2] = allp
         out["max"] = bench.max_over_ranks(float(10 * rank + 1))
+        out["sum"] = bench.sum_over_ranks(float(10 * rank + 1))   # replicas: whole-job flops
         for L in (1, 300, 16384, 23040):
             cols = hf.hf_stage1_partition(L, world, rank)
             allc = [None] * world
@@ -70,6 +71,7 @@ def test_shard_plan_and_rank_max_gloo():
         p.join(timeout=60)
     for r in range(world):
         assert res[r]["max"] == 11.0
+        assert res[r]["sum"] == 12.0
         for n2 in (0, 1, 3, 64, 256, 1344, 1345):
             sl = res[r][n2]
             assert sl == res[0][n2]                       # every rank sees the same plan
