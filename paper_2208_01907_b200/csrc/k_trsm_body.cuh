@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(256) k_scale_op(int nblk, int64_t Np, T *__res
     __syncthreads();
     T acc[4][4] = {};
     tile_fma(acc, As, Bs, tr, tc);                     // Dinv_b Op_bq
+    // column jj of the thread's 4x4 block: 4 consecutive rows -> one 16-byte (FP32) store
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) Op[(r0 + tr * 4 + i) + (q0 + tc * 4 + jj) * Np] = acc[i][jj];
+    for (int jj = 0; jj < 4; ++jj)
+        st4(&Op[(r0 + tr * 4) + (q0 + tc * 4 + jj) * Np], acc[0][jj], acc[1][jj], acc[2][jj], acc[3][jj]);
 }
 
 // W (original row order, ldw) = lift(Xb) on Lambda_1 rows, 0 on Lambda_2 rows
