@@ -35,20 +35,30 @@ sys.path.insert(0, ROOT)
 
 FFMA_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12     # TFLOP/s, B200 FP32 non-tensor
 DMMA_PEAK_MEASURED = 37.15                              # tools/peaks.py, profiles/peaks_r01.json
-KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "gram", "hard", "other")
+KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "trsm_setup", "gram", "hard", "other")
 
 
 def flop_model(L, N, Ntau, n2, iters):
-    """Algorithmic flops of one hybrid factorization."""
+    """Algorithmic flops of one hybrid factorization, counted
+    as block_gcr (gcr.cu) runs Alg. 5: K11-products for r_0, q_0, each z_{n+1} of a
+    non-final iteration and the reported true residual (iters + 2); preconditioner
+    applications for x_0, w_0 and each w_{n+1} of a non-final iteration (iters + 1);
+    per iteration M_n, A_n, the X and R updates (4 N x n2 x n2 products) and, on a
+    non-final iteration n, Q_m^T z and the P, Q updates over the n + 1 blocks
+    (3 (n + 1) products) plus the n2 x n2 products C = M^-1 A and G_m."""
     m = np.arange(L, L - Ntau, -1, dtype=np.float64)          # active size before each pivot
     f1 = float(np.sum((m - 1.0) * m))                          # rank-1 updates of the lower triangle
     mv = 2.0 * N * N * n2                                      # K11 W
     pc = 2.0 * N * N * n2                                      # FP32 fwd + bwd triangular solves
-    gram = sum(2.0 * N * n2 * n2 * (4 + 3 * (n + 1)) for n in range(iters))
-    f2 = (iters + 2) * mv + (iters + 1) * pc + gram
+    nn = 2.0 * N * n2 * n2
+    gram = sum(nn * 4 for n in range(iters)) + sum(nn * 3 * (n + 1) for n in range(iters - 1))
+    small = 2.0 * n2 ** 3 * (iters + sum(n + 1 for n in range(iters - 1)))
+    f2 = (iters + 2) * mv + (iters + 1) * pc + gram + small
     f3 = 2.0 * N * n2 * n2
     f4 = n2 ** 3 / 3.0
-    return {"stage1": f1, "gcr": f2, "schur": f3, "hard": f4, "total": f1 + f2 + f3 + f4}
+    dmma = (iters + 2) * mv + gram + small + f3                # the FP64 DMMA GEMM class
+    return {"stage1": f1, "gcr": f2, "schur": f3, "hard": f4, "total": f1 + f2 + f3 + f4,
+            "dmma": dmma, "trsm": (iters + 1) * pc}
 
 
 class Clocks:
@@ -171,6 +181,22 @@ def oracle_sample(Kb_np, spec, pivots=1024):
     return f_st1 + f_it, secs, desc
 
 
+def oracle_full(Kb_np, spec):
+    """The WHOLE oracle (Alg. 1 steps 1-5: scale, stage 1, block GCR, Schur, hard
+    factorization) on the config's matrix, as it stands.  Returns (flops, seconds,
+    description) with the same flop model as the GPU line."""
+    import oracle
+    L = Kb_np.shape[0]
+    t0 = time.perf_counter()
+    K, _ = oracle.scale(Kb_np)
+    HF = oracle.hybrid_factor(K, tau=spec.tau, n_min=spec.n_min)
+    secs = time.perf_counter() - t0
+    fm = flop_model(L, HF.F.N, HF.F.Ntau, HF.F.n2, HF.gcr.iters)
+    desc = (f"the whole oracle on {spec.name} (L={L}): scale + FP32 stage 1 + block GCR "
+            f"({HF.gcr.iters} iterations, n2={HF.F.n2}) + Schur + hard factorization")
+    return fm["total"], secs, desc
+
+
 def max_over_ranks(x: float) -> float:
     """Max of a per-rank scalar over the default process group (NCCL: device
     tensor, gloo: host tensor); identity without a group."""
@@ -215,6 +241,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pivots-sample", type=int, default=1024)
+    ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "full", "sample", "none"],
+                    help="auto: the whole oracle when L <= 16384 (C2: ~2 min on 16 host cores), else the "
+                         "bounded sample")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
                     help="N>1: replicas = one matrix per rank, no data-path collective (weak scaling); "
                          "shard = one matrix, block-GCR right-hand sides split over the ranks with the "
@@ -306,6 +335,7 @@ def main():
     for c in KCLASSES:
         ctx.kernel_stats(c)            # drain the warm-up records
     base = {c: ctx.kernel_stats(c) for c in KCLASSES}
+    wbase = {c: ctx.kernel_work(c) for c in KCLASSES}
     launches0 = ctx.launch_count()
     stage_ms = np.zeros(4)
     step_ms = []
@@ -337,6 +367,7 @@ def main():
     kstats = {c: ctx.kernel_stats(c) for c in base}
     kms = {c: (kstats[c][0] - base[c][0]) / args.steps for c in base}
     klaunch = {c: (kstats[c][1] - base[c][1]) / args.steps for c in base}
+    kwork = {c: tuple((a - b) / args.steps for a, b in zip(ctx.kernel_work(c), wbase[c])) for c in base}
 
     N, Ntau, n2, iters, kd, tres = results[-1]
     L = spec.L
@@ -349,9 +380,12 @@ def main():
     total_flops = sum_over_ranks(fm["total"]) if args.mode == "replicas" else fm["total"]
     value = total_flops / (ms_step * 1e-3) / 1e12
 
-    # ---- roofline of the dominant compute kernel (the FP32 trailing update)
+    # ---- roofline of the dominant compute kernel (the FP32 trailing update): its OWN
+    # algorithmic flops (one FMA per lower-triangle entry per pivot of each launch, as
+    # libhf reports them per launch; the in-panel part of F1 is the chain's)
     tr_ms = kms["trailing"]
-    achieved = fm["stage1"] / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else None
+    tr_fl = kwork["trailing"][0]
+    achieved = tr_fl / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else None
     traffic = load_traffic()
     roof = {"kernel": "k_trailing_c (FP32 FFMA2 symmetric rank-nb update, bitwise canonical order)",
             "bound": "alu", "achieved": achieved, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
@@ -360,8 +394,30 @@ def main():
                            "microbenchmark 72.6 FFMA / 74.3 FFMA2 TF/s (profiles/peaks_r01.json)",
             "traffic": traffic.get("bytes_per_launch") if traffic else None,
             "traffic_note": traffic.get("note") if traffic else "no ncu capture committed yet",
-            "ms_per_step": tr_ms, "launches_per_step": klaunch["trailing"]}
-    dg_ms = kms["dgemm"]
+            "flops_per_step": tr_fl, "ms_per_step": tr_ms, "launches_per_step": klaunch["trailing"]}
+    # ---- the other kernels' own rooflines
+    dg_ms, ts_ms, ch_ms = kms["dgemm"], kms["trsm"], kms["chain"]
+    dmma_ach = fm["dmma"] / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
+    trsm_ach = kwork["trsm"][0] / (ts_ms * 1e-3) / 1e12 if ts_ms > 0 else None
+    rooflines = {
+        "dgemm": {"kernel": "k_dgemm (FP64 DMMA mma.sync m8n8k4: K11 W mat-vecs, Gram / update products, Schur)",
+                  "bound": "fp64_tensor", "achieved": dmma_ach, "peak": DMMA_PEAK_MEASURED, "unit": "TFLOP/s",
+                  "frac": dmma_ach / DMMA_PEAK_MEASURED if dmma_ach else None,
+                  "flops_per_step": fm["dmma"], "flops_note": "algorithmic DMMA work only (mat-vecs on N = "
+                  "|Lambda_1| rows, Gram / update / n2 x n2 products, S22); the FP32 preconditioner is not in it",
+                  "executed_flops_per_step": kwork["dgemm"][0], "ms_per_step": dg_ms,
+                  "peak_source": "measured DMMA microbenchmark (tools/peaks.py, profiles/peaks_r01.json)"},
+        "trsm": {"kernel": "k_trsm<fwd/bwd> (FP32 FFMA2 dataflow triangular solves, n2 right-hand sides)",
+                 "bound": "alu", "achieved": trsm_ach, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
+                 "frac": trsm_ach / FFMA_PEAK_DERIVED if trsm_ach else None,
+                 "flops_per_step": kwork["trsm"][0], "ms_per_step": ts_ms,
+                 "hbm_gbs": kwork["trsm"][1] / (ts_ms * 1e-3) / 1e9 if ts_ms > 0 else None,
+                 "setup_ms_per_step": kms["trsm_setup"]},
+        "chain": {"kernel": "k_chain (cooperative persistent pivot chain, one launch per panel)",
+                  "bound": "latency", "us_per_pivot": ch_ms * 1e3 / max(Ntau, 1), "ms_per_step": ch_ms,
+                  "hbm_gbs": kwork["chain"][1] / (ch_ms * 1e-3) / 1e9 if ch_ms > 0 else None,
+                  "bytes_per_step": kwork["chain"][1]},
+    }
     shares = {c: round(kms[c] / ms_step, 4) for c in kms}
 
     line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -381,13 +437,13 @@ def main():
             "flops_per_step": fm, "per_step_stage_ms": step_ms,
             "kernel_ms_per_step": kms, "kernel_share": shares,
             "chain_us_per_pivot": kms["chain"] * 1e3 / max(Ntau, 1),
-            "dgemm_tflops": (fm["gcr"] + fm["schur"]) / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None,
-            "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary()}
+            "dgemm_tflops": dmma_ach,
+            "roofline": roof, "rooflines": rooflines, "gpu_launches": int(launches), "clocks": clk.summary()}
 
     # ---- end to end through the public API with host buffers
     if not args.no_e2e:
         Kh = Kb.cpu().pin_memory()
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, args.steps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -415,9 +471,16 @@ def main():
                        "ms_per_step": e_ms}
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    cb_mode = args.cpu_baseline
+    if cb_mode == "auto":
+        cb_mode = "full" if spec.L <= 16384 else "sample"
+    if rank == 0 and world == 1 and cb_mode != "none" and not args.no_cpu_baseline:
         try:
-            f, s_, desc = oracle_sample(Kb.cpu().numpy(), spec, pivots=args.pivots_sample)
+            Kh_np = Kb.cpu().numpy()
+            if cb_mode == "full":
+                f, s_, desc = oracle_full(Kh_np, spec)
+            else:
+                f, s_, desc = oracle_sample(Kh_np, spec, pivots=args.pivots_sample)
             line["cpu_baseline"] = {"value": f / s_ / 1e12, "unit": "TFLOP/s", "cores": host_cores(),
                                     "kind": "oracle", "sample": desc, "seconds": s_}
         except Exception as e:   # the oracle is a reported baseline, never the product

@@ -91,11 +91,19 @@ const char *hf_last_error(const hf_ctx *ctx);
 /* Instrumentation: number of kernels this context launched so far, and the
  * summed device time of one kernel class measured with CUDA events on the
  * context stream while profiling is enabled.  class: "trailing", "chain",
- * "dgemm", "trsm", "gram", "scale", "hard", "other". */
+ * "dgemm", "trsm" (the triangular-solve applications), "trsm_setup" (their
+ * operator setup), "gram", "scale", "hard", "other".  Every entry point runs on
+ * the context's device and restores the caller's current device. */
 hf_status hf_set_profiling(hf_ctx *ctx, int enable);
 hf_status hf_kernel_stats(hf_ctx *ctx, const char *kernel_class, double *ms_host,
                           int64_t *launches_host);
 hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host);
+/* The ALGORITHMIC work of one kernel class summed over the launches made while
+ * profiling was enabled (what the method must compute: e.g. one FMA
+ * per lower-triangle entry per pivot for "trailing", 2 N^2 n per application for
+ * "trsm", 2 M N K per product for "dgemm"); 0 for classes that do not report it.
+ * Cumulative like hf_kernel_stats. */
+hf_status hf_kernel_work(hf_ctx *ctx, const char *kernel_class, double *flops_host, double *bytes_host);
 /* Device workspaces and handle buffers come from a per-(device, stream) cache
  * that reuses freed blocks in stream order (no memory is re-mapped by a
  * repeated factorization); this synchronises the device and returns every

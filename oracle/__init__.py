@@ -20,6 +20,11 @@ Parts and what pins them (tests/test_oracle_*.py):
                          diagonal/special cases, ratio guarantee,
                          reconstruction, FP64 Schur argmax, planted count
                          (pinned)
+  factor_lowprec_prefix -- the same body stopped after k pivots (output
+                         interface only); pinned by equality with the first
+                         k columns of the full run (test_oracle_lowprec.py)
+  iterative_refinement -- exact factor converges in one step; the residual
+                         ratio equals rho(I - A Q^{-1}) (pinned)
   precond_apply       -- exact factors of diagonal / triangular cases,
                          residual bound (pinned)
   block_gcr, gcr      -- constructed solutions, orthogonality, M=1 == GCR,
@@ -36,7 +41,7 @@ not bitwise, because S22 carries FP64 cancellation noise).
 """
 from .core import (  # noqa: F401
     LowFactor, HardFactor, Hybrid, GcrInfo, OracleBreakdown, OracleNotConverged,
-    lib, scale, factor_lowprec, precond_apply, block_gcr, gcr,
+    lib, scale, factor_lowprec, factor_lowprec_prefix, FactorPrefix, precond_apply, block_gcr, gcr,
     iterative_refinement, extract_blocks, schur, factor_hard, hard_solve,
     hybrid_factor, hybrid_solve, kernel_dimension,
 )

@@ -46,8 +46,8 @@ def lib():
             i64, dp, fp, lp = (ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64))
             L.oracle_scale.argtypes = [i64, dp, i64, dp, dp]
-            L.oracle_factor_f32.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, fp, fp, lp]
-            L.oracle_factor_f64.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, dp, dp, lp]
+            L.oracle_factor_f32.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, fp, fp, lp, i64, lp]
+            L.oracle_factor_f64.argtypes = [i64, dp, i64, ctypes.c_double, i64, i64, i64, lp, dp, dp, lp, i64, lp]
             _lib = L
     return _lib
 
@@ -122,12 +122,49 @@ def factor_lowprec(K: np.ndarray, tau: float, n_min: int = 0, n_extra: int = 0,
     out = np.zeros(2, dtype=np.int64)
     fn = lib().oracle_factor_f32 if prec == "f32" else lib().oracle_factor_f64
     rc = fn(L, _ptr(K, ctypes.c_double), max(L, 1), float(tau), int(n_min), int(n_extra), int(max_steps),
-            _ptr(perm, ctypes.c_int64), _ptr(Dk, ct), _ptr(Lf, ct), _ptr(out, ctypes.c_int64))
+            _ptr(perm, ctypes.c_int64), _ptr(Dk, ct), _ptr(Lf, ct), _ptr(out, ctypes.c_int64), -1, None)
     if rc != 0:
         raise ValueError("oracle_factor: invalid arguments (tau must be in (0,1))")
     N, Ntau = int(out[0]), int(out[1])
     return LowFactor(L=L, N=N, Ntau=Ntau, perm=perm, D=Dk[:N].copy(),
                      Lfac=np.asfortranarray(Lf[:N, :N]), dtype=dt)
+
+
+@dataclass
+class FactorPrefix:
+    """The first `steps` pivots of stage 1 (a bounded run of the same algorithm)."""
+    pivots: np.ndarray    # int64[steps] original index of pivot k
+    D: np.ndarray         # [steps] d_k
+    Lcols: np.ndarray     # L x steps: L_{i,k} = c_i / d_k for every row, rows in pos_orig order
+    pos_orig: np.ndarray  # int64[L] original index at each position after the run
+
+
+def factor_lowprec_prefix(K: np.ndarray, tau: float, steps: int, n_min: int = 0,
+                          prec: str = "f32") -> FactorPrefix:
+    """Stage 1 stopped after `steps` pivots (the same oracle_factor body
+    as factor_lowprec): returns only the first `steps` factor columns, with every
+    row, so an L = 65536 run fits in host memory (L x steps instead of L x L).
+    An output-interface variant for the C4 prefix parity test, no arithmetic
+    change.  Raises if the tau-rule stops before `steps` pivots."""
+    K = np.asfortranarray(K, dtype=np.float64)
+    L = K.shape[0]
+    steps = int(min(steps, L))
+    dt = np.float32 if prec == "f32" else np.float64
+    ct = ctypes.c_float if prec == "f32" else ctypes.c_double
+    perm = np.empty(L, dtype=np.int64)
+    Dk = np.zeros(max(L, 1), dtype=dt)
+    Lf = np.empty((max(L, 1), max(steps, 1)), dtype=dt, order="F")
+    pos = np.empty(max(L, 1), dtype=np.int64)
+    out = np.zeros(2, dtype=np.int64)
+    fn = lib().oracle_factor_f32 if prec == "f32" else lib().oracle_factor_f64
+    rc = fn(L, _ptr(K, ctypes.c_double), max(L, 1), float(tau), int(n_min), 0, steps,
+            _ptr(perm, ctypes.c_int64), _ptr(Dk, ct), _ptr(Lf, ct), _ptr(out, ctypes.c_int64), steps,
+            _ptr(pos, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_factor: invalid arguments (tau must be in (0,1))")
+    if int(out[1]) < steps:
+        raise ValueError(f"the tau rule stopped after {int(out[1])} < {steps} pivots")
+    return FactorPrefix(pivots=pos[:steps].copy(), D=Dk[:steps].copy(), Lcols=Lf, pos_orig=pos[:L])
 
 
 def precond_apply(F: LowFactor, R: np.ndarray) -> np.ndarray:

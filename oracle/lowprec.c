@@ -22,7 +22,12 @@
  *                         pair of sec. 4.3).
  *
  * max_steps > 0 stops after that many pivots (a bounded sample for bench.py's
- * CPU baseline; results of such a run are not a factorization).
+ * CPU baseline, and the bitwise PREFIX comparison at C4 in the tests; results
+ * of such a run are not a factorization).  Output-only options (round 2,
+ * no arithmetic change): ncol >= 0 writes only the first ncol columns of Lfac
+ * (an L x ncol array; -1: all L), and a bounded run writes every row of them
+ * in its own position order, which pos_orig (nullable, [L]) receives as the
+ * original index of each position.
  *
  * Arithmetic is IEEE round-to-nearest, no contraction (compiled with
  * -ffp-contract=off); every FMA is an explicit fmaf/fma call.
@@ -160,26 +165,33 @@ int oracle_scale(int64_t L, const double *Kbar, int64_t ld, double *K, double *q
         for (int64_t i = 0; i < L; ++i) if (!used[i]) perm[w++] = i;          \
         free(used);                                                           \
     }                                                                         \
-    for (int64_t j = 0; j < L; ++j)                                           \
+    /* a bounded run (kmax < L) keeps EVERY row of its kmax columns, in its   \
+       own position order (pos_orig below): output only, no arithmetic change */ \
+    const int64_t nrow = (kmax < L) ? L : N;                                  \
+    const int64_t nc = (ncol >= 0 && ncol < L) ? ncol : L;                    \
+    for (int64_t j = 0; j < nc; ++j)                                          \
         for (int64_t i = 0; i < L; ++i) {                                     \
             T v = (T)0;                                                       \
-            if (j < N && i < N) v = (i == j) ? (T)1 : ((i > j) ? A[i + j * L] : (T)0); \
+            if (j < N && i < nrow) v = (i == j) ? (T)1 : ((i > j) ? A[i + j * L] : (T)0); \
             Lfac[i + j * L] = v;                                              \
         }                                                                     \
+    if (pos_orig) for (int64_t p = 0; p < L; ++p) pos_orig[p] = orig[p];      \
     out[0] = N; out[1] = Ntau;                                                \
     free(A); free(s); free(orig);                                             \
     return 0;
 
 int oracle_factor_f32(int64_t L, const double *K, int64_t ld, double tau,
                       int64_t n_min, int64_t n_extra, int64_t max_steps,
-                      int64_t *perm, float *Dk, float *Lfac, int64_t *out)
+                      int64_t *perm, float *Dk, float *Lfac, int64_t *out,
+                      int64_t ncol, int64_t *pos_orig)
 {
     ORACLE_FACTOR_BODY(float, fmaf, sqrtf, fabsf)
 }
 
 int oracle_factor_f64(int64_t L, const double *K, int64_t ld, double tau,
                       int64_t n_min, int64_t n_extra, int64_t max_steps,
-                      int64_t *perm, double *Dk, double *Lfac, int64_t *out)
+                      int64_t *perm, double *Dk, double *Lfac, int64_t *out,
+                      int64_t ncol, int64_t *pos_orig)
 {
     ORACLE_FACTOR_BODY(double, fma, sqrt, fabs)
 }

@@ -3,6 +3,7 @@
 // the kernels of k_*.cu.
 #include <math.h>
 
+#include <atomic>
 #include <cstring>
 #include <memory>
 
@@ -13,9 +14,30 @@
 namespace {
 
 thread_local std::string g_noctx_error;
+std::atomic<uint64_t> g_ctx_serial{0};
+
+// switches to the context's device for the duration of a call and restores the
+// caller's current device (every launch and kernel attribute of a call then
+// targets ctx->device whatever device the caller has current)
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const hf_ctx *ctx) {
+        if (!ctx) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            return;
+        }
+        if (prev != ctx->device) cudaSetDevice(ctx->device);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 template <typename F>
 hf_status guarded(hf_ctx *ctx, F &&f) {
+    DeviceGuard dg(ctx);
     try {
         f();
         if (ctx) ctx->last_error.clear();
@@ -67,12 +89,9 @@ hf_status hf_create(int device, void *cuda_stream, hf_ctx **out) {
         c->device = device;
         c->num_sms = p.multiProcessorCount;
         c->stream = (cudaStream_t)cuda_stream;
-        // keep freed workspace reserved in the stream-ordered pool: re-mapping GBs of
-        // physical memory on every factorization costs more than the factorization
-        cudaMemPool_t pool;
-        HF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t thr = UINT64_MAX;
-        HF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        c->serial = ++g_ctx_serial;
+        // (libhf's workspaces come from its own cache, alloc.cu; the device's default
+        // stream-ordered pool, which other libraries in the process use, is left alone)
     });
     if (s != HF_OK) return s;
     *out = c.release();
@@ -81,6 +100,7 @@ hf_status hf_create(int device, void *cuda_stream, hf_ctx **out) {
 
 hf_status hf_destroy(hf_ctx *ctx) {
     if (!ctx) return HF_OK;
+    DeviceGuard dg(ctx);
     cudaStreamSynchronize(ctx->stream);
     for (auto &kv : ctx->pending)
         for (auto &pr : kv.second) {
@@ -132,6 +152,15 @@ hf_status hf_kernel_stats(hf_ctx *ctx, const char *cls, double *ms_host, int64_t
         }
         if (ms_host) *ms_host = ms;
         if (launches_host) *launches_host = n;
+    });
+}
+
+hf_status hf_kernel_work(hf_ctx *ctx, const char *cls, double *flops_host, double *bytes_host) {
+    if (!ctx || !cls) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        auto it = ctx->work.find(cls);
+        if (flops_host) *flops_host = it != ctx->work.end() ? it->second.flops : 0.0;
+        if (bytes_host) *bytes_host = it != ctx->work.end() ? it->second.bytes : 0.0;
     });
 }
 

@@ -94,6 +94,22 @@ struct KStat {
     double ms = 0.0;
     int64_t launches = 0;
 };
+// algorithmic work of one kernel class (flops, bytes), summed while profiling
+struct KWork {
+    double flops = 0.0, bytes = 0.0;
+};
+
+// one-time per-device state (kernel attributes such as the dynamic shared-memory
+// limit apply per device context, so a process with contexts on several devices
+// sets them once per device)
+constexpr int HF_MAX_DEV = 64;
+struct DevState {
+    int v[HF_MAX_DEV];
+    explicit DevState(int init) {
+        for (int &x : v) x = init;
+    }
+    int &operator[](int dev) { return v[((dev % HF_MAX_DEV) + HF_MAX_DEV) % HF_MAX_DEV]; }
+};
 
 }  // namespace hf
 
@@ -107,6 +123,7 @@ struct TrsmTable {
 }  // namespace hf
 
 struct hf_ctx {
+    uint64_t serial = 0;               // unique per context (never reused): owner tag of cached tables
     int device = 0;
     cudaStream_t stream = 0;
     int num_sms = 148;
@@ -122,6 +139,7 @@ struct hf_ctx {
     // pending (start, stop) event pairs per class; resolved lazily
     std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::map<std::string, hf::KStat> stats;
+    std::map<std::string, hf::KWork> work;   // algorithmic flops / bytes per class (hf_kernel_work)
     std::vector<cudaEvent_t> event_pool;
     std::map<std::pair<int, int>, hf::TrsmTable> trsm_tables;   // (nblk, nch) -> table
     cudaStream_t side = nullptr;       // second stream (stage-1 lookahead: trailing updates), lazily created
@@ -131,12 +149,17 @@ struct hf_ctx {
 namespace hf {
 
 // RAII timer around launches of one kernel class (only when profiling).
+// flops / bytes: the ALGORITHMIC work of the launches it brackets (what the method
+// must compute, e.g. only the lower-triangle entries of a trailing update), summed
+// per class for hf_kernel_work while profiling; 0 where nobody reports it.
 struct ClassTimer {
     hf_ctx *ctx;
     const char *cls;
     cudaStream_t s;
     cudaEvent_t a = nullptr, b = nullptr;
-    ClassTimer(hf_ctx *c, const char *k, cudaStream_t on = nullptr) : ctx(c), cls(k), s(on ? on : c->stream) {
+    double fl = 0.0, by = 0.0;
+    ClassTimer(hf_ctx *c, const char *k, cudaStream_t on = nullptr, double flops = 0.0, double bytes = 0.0)
+        : ctx(c), cls(k), s(on ? on : c->stream), fl(flops), by(bytes) {
         if (!ctx->profiling) return;
         a = take(); b = take();
         cudaEventRecord(a, s);
@@ -145,6 +168,9 @@ struct ClassTimer {
         if (!ctx->profiling || !a) return;
         cudaEventRecord(b, s);
         ctx->pending[cls].push_back({a, b});
+        auto &w = ctx->work[cls];
+        w.flops += fl;
+        w.bytes += by;
     }
     cudaEvent_t take() {
         if (!ctx->event_pool.empty()) {
@@ -182,7 +208,8 @@ struct PrecondT {
     DBuf<int> counter;
     int epoch = 0;
     // dataflow workspaces (k_trsm.cu), re-sized when the block/chunk counts change
-    int tab_nblk = -1, tab_nch = -1, nitems = 0, nslots = 0;
+    int tab_nblk = -1, tab_nch = -1, tab_seg = -1, nitems = 0, nslots = 0;
+    uint64_t tab_ctx = 0;          // serial of the context whose table cache owns items / pinfo
     const int4 *items = nullptr;   // owned by the context's table cache
     const int4 *pinfo = nullptr;
     DBuf<T> part;

@@ -173,7 +173,8 @@ static void dgemm_launch(hf_ctx *ctx, bool transA, int nprob, const DgemmArgs *g
     cudaStream_t st = ctx->stream;
     const int64_t mt = cdiv(M, BM), nt = cdiv(N, BN);
     const size_t shm0 = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
-    static int per_sm = 0;
+    static DevState per_sm_dev(0);   // per device: kernel attributes apply per device context
+    int &per_sm = per_sm_dev[ctx->device];
     if (!per_sm) {
         HF_CUDA(cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm0));
         HF_CUDA(cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm0));
@@ -209,7 +210,8 @@ static void dgemm_launch(hf_ctx *ctx, bool transA, int nprob, const DgemmArgs *g
     }
     if (nprob == 1) gb.g[1] = gb.g[0];
     const size_t shm = shm0;
-    ClassTimer tm(ctx, "dgemm");
+    ClassTimer tm(ctx, "dgemm", st, 2.0 * (double)M * (double)N * (double)K * nprob,
+                  8.0 * nprob * ((double)M * K + (double)K * N + 2.0 * (double)M * N));
     dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(splits * nprob));
     if (transA) k_dgemm<true><<<grid, 128, shm, st>>>(gb);
     else k_dgemm<false><<<grid, 128, shm, st>>>(gb);

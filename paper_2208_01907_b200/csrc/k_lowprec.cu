@@ -1208,6 +1208,21 @@ __global__ void k_gather_L(int64_t N, const int32_t *__restrict__ pivorig, const
 }  // namespace
 
 // ------------------------------------------------------------------ host driver
+// algorithmic work per launch, reported through hf_kernel_work:
+//  trailing update of a panel of nbp pivots leaving mp active indices: one FMA per
+//    lower-triangle entry (diagonal included) per pivot; bytes = the triangle read
+//    and written once plus the two panel operands;
+//  chain: per pivot t of the panel, the column c_I of every active row brought up to
+//    date over the t earlier in-panel pivots (one FMA each), and 16 bytes per row
+//    (the panel-start column read, s, -sigma s, L written).
+static double trail_flops(int64_t mp, int nbp) { return (double)mp * (double)(mp + 1) * nbp; }
+static double trail_bytes(int64_t mp, int nbp) { return (double)mp * (mp + 1) * 4.0 + 8.0 * mp * nbp; }
+static double chain_flops(int64_t m, int nbp) {
+    double f = 0.0;
+    for (int t = 0; t < nbp; ++t) f += 2.0 * (double)(m - t) * t;
+    return f;
+}
+static double chain_bytes(int64_t m, int nbp) { return 16.0 * ((double)m * nbp - 0.5 * (double)nbp * (nbp - 1)); }
 // the part of stage 1 after the panels: N, Pi, D and the factor in pivot order
 static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, DBuf<int32_t> &status,
                            DBuf<int32_t> &pivorig, DBuf<float> &Dk, DBuf<float> &Lorig, DBuf<unsigned long long> *dbg) {
@@ -1442,7 +1457,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ca.DGout = look ? DG[pb].p : nullptr;
         ca.parts = nullptr; ca.nparts = 1; ca.cb = 1; ca.colpos = nullptr; ca.ldp = 0;
         {
-            ClassTimer tm(ctx, "chain");
+            ClassTimer tm(ctx, "chain", st, chain_flops(m, nbp), chain_bytes(m, nbp));
             void *args[] = {&ca};
             HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain<false>, dim3((unsigned)G), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
@@ -1474,7 +1489,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                         mp, nbp, map[pb].p, S[pb].p, Sn[pb].p, L, Sc.p, Snc.p, ldc, status.p);
                     HF_CHECK_LAUNCH(ctx);
                 }
-                ClassTimer tm(ctx, "trailing");
+                ClassTimer tm(ctx, "trailing", st, trail_flops(mp, nbp), trail_bytes(mp, nbp));
                 if (Sc.p && persist && (ntiles > 2 * pgrid || pmode == 2)) {
                     k_trailing_p<<<(unsigned)pgrid, 256, TRAIL_P_SMEM, st>>>(ta, ntiles);
                 } else if (Sc.p) {
@@ -1497,7 +1512,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                     HF_CHECK_LAUNCH(ctx);
                 }
                 {
-                    ClassTimer tm(ctx, "trailing", st2);
+                    ClassTimer tm(ctx, "trailing", st2, trail_flops(mp, nbp), trail_bytes(mp, nbp));
                     k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st2>>>(ta);
                     HF_CHECK_LAUNCH(ctx);
                 }

@@ -1161,7 +1161,8 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
     wk.alloc((size_t)4 * n, ctx->stream);
     double *cb = wk.p, *rb = wk.p + 2 * n;
     const size_t shm_cl = ((size_t)cdiv(n, SPD_CL) * n + 2 * (size_t)n + (size_t)cdiv(n, SPD_CL)) * sizeof(double);
-    static int cl_ok = -1;   // the 16-CTA cluster path: non-portable cluster size, checked once
+    static DevState cl_ok_dev(-1);   // the 16-CTA cluster path: non-portable cluster size, checked once per device
+    int &cl_ok = cl_ok_dev[ctx->device];
     if (cl_ok < 0) {
         cl_ok = getenv("HF_SPD_NOCLUSTER") ? 0 : 1;
         if (cl_ok && (cudaFuncSetAttribute(k_spd_inv_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
@@ -1171,7 +1172,8 @@ void spd_inverse(hf_ctx *ctx, int64_t n, const double *M, int64_t ldm, double *M
     }
     const size_t shm_blk = ((size_t)cdiv(n, SPD_CL) * n + 2 * (size_t)SPD_BS * n + (size_t)cdiv(n, SPD_CL) * SPD_BS) *
                            sizeof(double);
-    static int blk_ok = -1;
+    static DevState blk_ok_dev(-1);
+    int &blk_ok = blk_ok_dev[ctx->device];
     if (blk_ok < 0) {
         blk_ok = (cl_ok && !getenv("HF_SPD_SCALAR")) ? 1 : 0;
         if (blk_ok && (cudaFuncSetAttribute(k_spd_inv_blk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
@@ -1213,7 +1215,8 @@ void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A,
     DBuf<int32_t> flags;
     flags.alloc((size_t)3 * n, st);   // act | posof | pivots
     int32_t *act = flags.p, *posof = flags.p + n, *piv = flags.p + 2 * n;
-    static int per_sm = 0;
+    static DevState per_sm_dev(0);
+    int &per_sm = per_sm_dev[ctx->device];
     if (!per_sm) {
         HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hard_factor_mc, 256, 0));
         per_sm = std::max(1, per_sm);
@@ -1225,7 +1228,8 @@ void hard_factor(hf_ctx *ctx, int64_t n, const double *S, double thr, double *A,
     static const bool unfused = getenv("HF_HARD_UNFUSED") != nullptr;   // the 3-barrier reference variant
     // the 16-CTA cluster kernel for n <= 600 (HF_HARD_NOCLUSTER: the cooperative one)
     const size_t shm_cl = ((size_t)cdiv(n, HC) * n + 2 * (size_t)n) * sizeof(double) + (size_t)n * sizeof(int32_t);
-    static int hcl_ok = -1;
+    static DevState hcl_ok_dev(-1);
+    int &hcl_ok = hcl_ok_dev[ctx->device];
     if (hcl_ok < 0) {
         hcl_ok = getenv("HF_HARD_NOCLUSTER") ? 0 : 1;
         if (hcl_ok && (cudaFuncSetAttribute(k_hard_factor_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||

@@ -660,7 +660,7 @@ void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T 
     p.Up.alloc((size_t)p.Np * p.Np, st);
     p.LinvF.alloc((size_t)nblk * TILE, st);
     p.LinvB.alloc((size_t)nblk * TILE, st);
-    ClassTimer tm(ctx, "trsm");
+    ClassTimer tm(ctx, "trsm_setup");
     dim3 g((unsigned)(p.Np / 32), (unsigned)(p.Np / 32));
     DBuf<T> Ulp, Ltr, scr;   // nonsymmetric only: Ufac padded, a discarded transpose / inverse
     if (!Ufac) {
@@ -677,12 +677,13 @@ void precond_setup_t(hf_ctx *ctx, PrecondT<T> &p, int64_t N, int64_t L, const T 
     }
     const size_t sm_inv = (size_t)2 * TBS * (TBS + 1) * sizeof(T);
     const size_t sm_sc = ((size_t)TBS * (TBS + 1) + 4 + TILE) * sizeof(T);
-    static bool attr_setup = false;
+    static DevState attr_setup_dev(0);
+    int &attr_setup = attr_setup_dev[ctx->device];
     if (!attr_setup) {
         HF_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_inv));
         HF_CUDA(cudaFuncSetAttribute(k_scale_op<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
         HF_CUDA(cudaFuncSetAttribute(k_scale_op<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-        attr_setup = true;
+        attr_setup = 1;
     }
     if (!Ufac) {
         k_diag_inv<<<(unsigned)nblk, TBS, sm_inv, st>>>(p.Np, p.Lp.p, p.LinvF.p, p.LinvB.p);
@@ -777,7 +778,9 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
     p.Y.alloc((size_t)p.Np * ncolp, st);
     p.Xb.alloc((size_t)p.Np * ncolp, st);
     p.P.alloc((size_t)p.Np * ncolp, st);
-    if (p.tab_nblk != nblk || p.tab_nch != nch) {
+    // the item table lives in the context's cache: look it up again whenever the shape,
+    // the segment or the context differs (a hybrid may be solved through another context)
+    if (p.tab_nblk != nblk || p.tab_nch != nch || p.tab_seg != seg || p.tab_ctx != ctx->serial) {
         auto key = std::make_pair(nblk, nch * 1000 + seg);
         auto it = ctx->trsm_tables.find(key);
         if (it == ctx->trsm_tables.end()) {
@@ -799,6 +802,8 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         p.nslots = it->second.nslots;
         p.tab_nblk = nblk;
         p.tab_nch = nch;
+        p.tab_seg = seg;
+        p.tab_ctx = ctx->serial;
         p.part.alloc((size_t)std::max(p.nslots, 1) * nch * TBS * CW, st);
         p.pflags.alloc((size_t)2 * std::max(p.nslots, 1) * nch, st);
         p.pflags.zero(st);
@@ -829,7 +834,8 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
         a.dbg = p.dbg.p;
     }
     const size_t shm = (size_t)SMEM_ELEMS * sizeof(T);
-    static int per_sm = 0;
+    static DevState per_sm_dev(0);
+    int &per_sm = per_sm_dev[ctx->device];
     if (!per_sm) {
         HF_CUDA(cudaFuncSetAttribute(k_trsm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         HF_CUDA(cudaFuncSetAttribute(k_trsm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -842,7 +848,11 @@ void precond_apply_t(hf_ctx *ctx, PrecondT<T> &p, int64_t ncol, const double *R,
     // role leave, so launch enough that helpers remain
     const int grid = std::min(std::max(nroles * per_sm + 1, nroles + p.nitems + per_sm), ctx->num_sms * per_sm);
     HF_REQUIRE(grid >= nroles * per_sm + 1, "preconditioner: too many RHS chunks for one launch");
-    ClassTimer tm(ctx, "trsm");
+    // algorithmic work of one application (forward + backward): N^2 ncol FMAs, the two
+    // triangles of the factor (sizeof(T) N^2 / 2 each) and the right-hand sides in/out
+    const double nn = (double)p.N * (double)p.N;
+    ClassTimer tm(ctx, "trsm", st, 2.0 * nn * (double)ncol,
+                  (double)sizeof(T) * nn + 16.0 * (double)p.N * (double)ncol);
     void *args[] = {&a};
     HF_CUDA(cudaLaunchCooperativeKernel((void *)k_trsm<false>, dim3(grid), dim3(NTHR), args, shm, st));
     HF_CHECK_LAUNCH(ctx);

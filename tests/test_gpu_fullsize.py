@@ -3,17 +3,20 @@ times (default options, one context, the config's tau / n_min):
 
   C2 (L = 16384): the whole oracle (stage 1 bitwise on Pi, Lambda_2, D and the
       factor; block GCR + Schur + hard factor) against the CUDA path.
-  C3 (L = 23040): stage 1 bitwise on the first 512 pivots (the oracle's
-      bounded run), S22 against the dense FP64 Schur complement of Eq. 2
-      (LAPACK solve with K11), kernel dimension 2 (the two translations,
-      SURVEY 8(c) item 13), manufactured residual.
-  C4 (L = 65536, 34 GB in FP64): properties that hold at any size, computed on
-      the GPU in FP64 from the exported factor: the strict ratio test on every
-      accepted pivot [R4], the reconstruction bound on sampled entries,
-      the pivot rule at sampled steps [R3] (up to FP32 rounding), block-GCR
-      true residual, manufactured residual.
-
-Set HF_FULLSIZE_ORACLE=1 to also run the whole oracle at C3 (minutes)."""
+  C3 (L = 23040): the whole oracle (stage 1 bitwise on Pi, Lambda_2, D and the
+      factor; S22 e_S, kernel dimension) plus S22 against the dense FP64 Schur
+      complement of Eq. 2 (LAPACK solve with K11), kernel dimension 2 (the two
+      translations), manufactured residual.  (~4 min)
+  C4 (L = 65536, 34 GB in FP64): scaling bitwise on a sampled principal
+      sub-block (K_ij depends only on Kbar_ij, Kbar_ii, Kbar_jj [R1]); stage 1
+      BITWISE against the oracle's bounded run of its first 1024 pivots (Pi
+      prefix, D, and the first 1024 factor columns on every Lambda_1 row);
+      then properties that hold at any size, computed on the GPU in FP64 from
+      the exported factor: the strict ratio test on every accepted pivot [R4],
+      the reconstruction bound on sampled entries, the pivot rule at
+      sampled steps [R3] (up to FP32 rounding), block-GCR true residual,
+      manufactured residual.  (~4 min, ~60 GB of host memory)
+"""
 import os
 
 import numpy as np
@@ -83,22 +86,22 @@ def test_c3_full(ctx):
     Kb = hi.make_kbar("C3", 0)
     Ko, _ = oracle.scale(Kb.numpy())
     Kd, lf, hy, info, S22, kd = _gpu_path(ctx, spec, Kb)
+    assert np.array_equal(Kd.cpu().numpy(), Ko)
     perm, D, Lf = lf.export()
-    if os.environ.get("HF_FULLSIZE_ORACLE"):
-        HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
-        assert np.array_equal(perm, HF.F.perm) and np.array_equal(D, HF.F.D)
-        K11, K12, K21, K22 = oracle.extract_blocks(HF.K, HF.F)
-        den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
-        assert np.linalg.norm(S22 - HF.S22) / den <= 1e-10
+    # the whole oracle (Alg. 1 steps 1-5) on the same scaled matrix
+    HF = oracle.hybrid_factor(Ko, tau=spec.tau, n_min=spec.n_min)
+    assert lf.N == HF.F.N and lf.L - lf.n2_tau_only == HF.F.Ntau
+    assert np.array_equal(perm, HF.F.perm)                  # Pi and Lambda_2, bitwise
+    assert np.array_equal(D, HF.F.D)
+    assert torch.equal(Lf.cpu(), torch.from_numpy(HF.F.Lfac))
+    K11, K12, K21, K22 = oracle.extract_blocks(HF.K, HF.F)
+    den = np.linalg.norm(K22) + np.linalg.norm(K21) * np.linalg.norm(HF.X)
+    assert np.linalg.norm(S22 - HF.S22) / den <= 1e-10      # [R17] e_S
+    thr = HF.H.thr
+    margin = min(abs(np.array(HF.H.mu_hist) - thr))
+    if margin > 10 * np.linalg.norm(S22 - HF.S22):
         assert kd == HF.kernel_dim
-    # stage 1: the first 512 pivots, D and factor columns bitwise
-    F = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min, max_steps=512)
-    assert np.array_equal(perm[:512], F.perm[:512])
-    assert np.array_equal(D[:512], F.D[:512])
-    Lg = Lf[:, :512].cpu().numpy()
-    # oracle columns of the bounded run: rows are in ITS position order, which
-    # coincides with the final pivot order on the first 512 rows only
-    assert np.array_equal(Lg[:512], F.Lfac[:512, :512])
+    del HF, K11, K21
     # S22 against the dense FP64 Schur complement of Eq. (2) (LAPACK solve with K11)
     l1, l2 = perm[: lf.N], perm[lf.N:]
     K11, K12, K22 = Ko[np.ix_(l1, l1)], Ko[np.ix_(l1, l2)], Ko[np.ix_(l2, l2)]
@@ -111,15 +114,38 @@ def test_c3_full(ctx):
     assert _rho_manufactured(ctx, hy, Kd) <= 1e-12
 
 
-def test_c4_full_properties(ctx):
+C4_PREFIX = 1024
+
+
+def test_c4_full(ctx):
     spec = hi.CONFIGS["C4"]
     Kb = hi.make_kbar("C4", 0, device="cuda")
+    # [R1] scaling: a principal sub-block of Kbar scales to the same bits as in K
+    sub = torch.from_numpy(np.sort(np.random.default_rng(4).choice(spec.L, 384, replace=False))).cuda()
+    Kb_sub = Kb[sub][:, sub].cpu().numpy()
     Kd, lf, hy, info, S22, kd = _gpu_path(ctx, spec, Kb)
     del Kb
     torch.cuda.empty_cache()
+    Ko_sub, _ = oracle.scale(Kb_sub)
+    assert np.array_equal(Kd[sub][:, sub].cpu().numpy(), Ko_sub)
     perm, D, Lf = lf.export()
     N = lf.N
     assert N == spec.L - spec.n_min
+    # stage 1, bitwise: the oracle's bounded run of the first C4_PREFIX pivots on the
+    # same scaled K (the symmetric row-major tensor read as its column-major transpose)
+    Kh = Kd.cpu().numpy().T
+    pre = oracle.factor_lowprec_prefix(Kh, spec.tau, C4_PREFIX, n_min=spec.n_min)
+    del Kh
+    k = C4_PREFIX
+    assert np.array_equal(perm[:k], pre.pivots)             # Pi prefix
+    assert np.array_equal(D[:k], pre.D)
+    rank = np.full(spec.L, -1, dtype=np.int64)
+    rank[perm[:N]] = np.arange(N)
+    rows = rank[pre.pos_orig]
+    ok = rows >= 0                                          # every Lambda_1 row
+    Lg = Lf[torch.from_numpy(rows[ok]).cuda(), :k].cpu().numpy()
+    assert np.array_equal(Lg, pre.Lcols[ok])
+    del pre, Lg
     # [R4] strict ratio test held at every accepted pivot
     Dd = np.abs(D.astype(np.float64))
     assert np.all(Dd[1:] >= spec.tau * Dd[:-1])

@@ -107,3 +107,54 @@ def test_iteration_ordering_bgcr_gcr_ir():
     its_g = max(oracle.gcr(A, F, B[:, j])[1].iters for j in range(4))
     its_ir = max(oracle.iterative_refinement(A, F, B[:, j], max_iter=200)[1].iters for j in range(4))
     assert ib.iters <= its_g <= its_ir
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 3 pins.  A broken refinement (wrong sign of the
+# correction, x replaced instead of updated, residual not recomputed from b)
+# fails at least one of these; `its_g <= its_ir` above does not pin it alone.
+# ---------------------------------------------------------------------------
+def test_ir_exact_factor_converges_in_one_step():
+    """A = diag(2^k): the FP32 factor is exact, so Q^{-1} = A^{-1} on FP32 data.
+    b has bits below FP32 precision, so x_0 = Q^{-1} RN32(b) misses them and
+    r_0 = b - RN32(b) != 0 exactly; r_0 is FP32-representable, hence step 4 (the
+    correction e = Q^{-1} r_0, x_1 = x_0 + e) is exact: r_1 = 0."""
+    n = 16
+    d = 2.0 ** np.arange(-4, 12)[:n]
+    A = np.diag(d * np.where(np.arange(n) % 3 == 0, -1.0, 1.0))
+    F = oracle.factor_lowprec(A, 1e-6)
+    assert F.N == n
+    A11 = A[np.ix_(F.lam1, F.lam1)]
+    b = (1.0 + 2.0 ** -40) * np.arange(1, n + 1, dtype=np.float64)
+    x, info = oracle.iterative_refinement(A11, F, b)
+    assert info.history[0][0] > 0                       # x_0 is not exact ...
+    assert info.iters == 1 and info.converged           # ... x_1 is
+    assert np.array_equal(A11 @ x, b)
+
+
+def test_ir_rate_is_spectral_radius_of_iteration_matrix():
+    """Krylov reading of Alg. 3: r_{n+1} = (I - A Q^{-1}) r_n, so
+    ||r_{n+1}|| / ||r_n|| -> rho(I - A Q^{-1}) (power method).  Q is the FP32
+    factor of A' = V diag(a / (1 - mu)) V^T while the iteration runs on
+    A = V diag(a) V^T, so I - A A'^{-1} = V diag(mu) V^T: rho = 0.5 exactly in
+    exact arithmetic, the next |mu| = 0.2, FP32 noise ~1e-6."""
+    n = 24
+    rng = np.random.default_rng(11)
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = np.linspace(1.0, 2.0, n)
+    mu = np.concatenate([[0.5, -0.2], np.linspace(-0.15, 0.15, n - 2)])
+    A = (V * a) @ V.T
+    A = 0.5 * (A + A.T)
+    Ap = (V * (a / (1.0 - mu))) @ V.T
+    Ap = 0.5 * (Ap + Ap.T)
+    F = oracle.factor_lowprec(Ap, 1e-6)
+    assert F.N == n
+    A11 = A[np.ix_(F.lam1, F.lam1)]
+    b = rng.standard_normal(n)
+    _, info = oracle.iterative_refinement(A11, F, b, tol=1e-300, max_iter=30)
+    h = np.array([float(v[0]) for v in info.history])
+    assert info.iters == 30
+    ratios = h[21:] / h[20:-1]
+    assert np.all(np.abs(ratios - 0.5) < 1e-4), ratios
+    # the opposite sign of the correction would iterate with I + A Q^{-1}: rho = 1.5
+    # (diverges); with mu -> -mu the rate is the same 0.5 in norm

@@ -174,3 +174,22 @@ def test_determinism():
     b = oracle.factor_lowprec(K, 1e-2)
     assert np.array_equal(a.perm, b.perm) and np.array_equal(a.D, b.D)
     assert np.array_equal(a.Lfac, b.Lfac)
+
+
+def test_prefix_run_equals_full_run_columns():
+    """factor_lowprec_prefix (the bounded run used for the C4 prefix parity test)
+    returns the same pivots, D and factor columns as the full run, for every
+    row: map the prefix run's positions to the full run's pivot order."""
+    Kb = hi.make_kbar("C0", 3)
+    K, _ = oracle.scale(Kb.numpy())
+    full = oracle.factor_lowprec(K, 1e-2, n_min=4)
+    k = 40
+    pre = oracle.factor_lowprec_prefix(K, 1e-2, k, n_min=4)
+    assert np.array_equal(pre.pivots, full.perm[:k])
+    assert np.array_equal(pre.D, full.D[:k])
+    rank = np.full(K.shape[0], -1)
+    rank[full.perm[:full.N]] = np.arange(full.N)
+    rows = rank[pre.pos_orig]
+    ok = rows >= 0
+    assert np.array_equal(pre.Lcols[ok], full.Lfac[rows[ok], :k])
+    assert sorted(pre.pos_orig.tolist()) == list(range(K.shape[0]))
