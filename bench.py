@@ -229,13 +229,28 @@ def host_cores():
         return os.cpu_count()
 
 
+def spawn_ranks(n: int) -> None:
+    """bench.py --gpus N without WORLD_SIZE: run N ranks under torch.distributed.run
+    on 127.0.0.1 (the contract's launch) and pass their output through."""
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    if r.returncode != 0:
+        raise SystemExit(r.returncode)
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=None)
     ap.add_argument("--impl", default="hf", choices=["hf", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -244,11 +259,24 @@ def main():
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "full", "sample", "none"],
                     help="auto: the whole oracle when L <= 16384 (C2: ~2 min on 16 host cores), else the "
                          "bounded sample")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
-                    help="N>1: replicas = one matrix per rank, no data-path collective (weak scaling); "
-                         "shard = one matrix, block-GCR right-hand sides split over the ranks with the "
-                         "S22 / X12 slices broadcast over NCCL inside libhf (strong scaling of stage 2)")
+    ap.add_argument("--mode", default=None, choices=["replicas", "shard"],
+                    help="N>1 (default shard): shard = ONE matrix factored by all ranks -- stage 1 "
+                         "distributed (lower-triangle 1D block-cyclic, per-pivot key exchange over NVLink), "
+                         "block-GCR right-hand sides split over the ranks with the S22 / X12 slices broadcast "
+                         "(strong scaling); replicas = one matrix per rank, no data-path collective (weak)")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None and args.impl == "hf":
+        # launch our own ranks (one process per GPU) and relay rank 0's line
+        return spawn_ranks(args.gpus)
+    if world_env is not None and args.impl == "hf" and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+    if args.mode is None:
+        args.mode = "shard" if args.gpus > 1 else "replicas"
+    if args.config is None:
+        # N = 1: the configuration the single-GPU targets are quoted on (C2); N > 1: the
+        # scale-out configuration (C4, L = 65536) factored across the ranks
+        args.config = "C4" if (args.gpus > 1 and args.mode == "shard") else "C2"
 
     import torch
     import torch.distributed as dist
@@ -264,6 +292,10 @@ def main():
         if rank != 0:
             return
         Kb = hi.make_kbar(spec, args.seed, device="cuda" if (torch.cuda.is_available() and spec.L > 4096) else "cpu")
+        if spec.L > 16384:
+            # a bounded sample of the scale-out workload: its leading 16384 x 16384 principal
+            # block (the same planted construction), so every step stays within seconds
+            Kb = Kb[:16384, :16384].contiguous()
         Kb = Kb.cpu().numpy()
         for _ in range(args.warmup):
             oracle_sample(Kb, spec, pivots=max(16, args.pivots_sample // 16))

@@ -226,8 +226,8 @@ hf_status hf_factor_lowprec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld,
         } else if (o.prec == 64) {
             HF_REQUIRE(ctx->nranks == 1 && ctx->s1parts == 0, "hf_factor_lowprec: prec 64 is single-GPU");
             hf::lowprec_factor64(ctx, L, K, ld, o, lf.get());
-        } else if (ctx->nranks > 1) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->nranks);
-        else if (ctx->s1parts > 0) hf::lowprec_factor_parts(ctx, L, K, ld, o, lf.get(), ctx->s1parts);
+        } else if (ctx->nranks > 1) hf::lowprec_factor_dist(ctx, L, K, ld, o, lf.get(), ctx->nranks);
+        else if (ctx->s1parts > 0) hf::lowprec_factor_dist(ctx, L, K, ld, o, lf.get(), ctx->s1parts);
         else hf::lowprec_factor(ctx, L, K, ld, o, lf.get());
     });
     if (s != HF_OK) return s;

@@ -275,6 +275,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                     hf_lowfactor *lf, const int32_t *blk_host = nullptr, int nblk = 0);
 void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                           hf_lowfactor *lf, int nparts);
+void lowprec_outputs(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, const int32_t *status,
+                     const int32_t *pivorig, const float *Dk);
+void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                         hf_lowfactor *lf, int nranks_emulated);
 void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                       hf_lowfactor *lf);
 void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,

@@ -1,0 +1,971 @@
+// k_dist.cu -- stage 1 (steps a2/a3: FP32 LDL^T with symmetric max-|diag| pivoting
+// and threshold postponing, rules [R2]-[R10]) DISTRIBUTED over G
+// ranks (BASELINE north_star: "1D block-column-cyclic layout ...
+// allreduce(max) picks the pivot ... broadcast distributes each factored panel").
+//
+// Layout: original index j is OWNED by rank (j / 128) % G.
+// Rank g stores, for every active index J it owns ("local column" c, kept in
+// position order), the LOWER-triangle entries v_IJ of all active I with
+// pos(I) >= pos(J), rows by global position (compacted stably after each panel,
+// as on one GPU).  Every unordered pair {I, J} is stored once, so the total
+// trailing-update work over the ranks equals one GPU's (no full columns).
+//
+// Pivot chain (k_chain_d, one cooperative launch per panel per rank): the chain
+// ROWS of rank g are the indices it owns.  Per pivot:
+//   A  local argmax over own rows -> (|d|, position, sign) key + (rank, local col)
+//   B  every CTA stores its key into the slot array of EVERY rank (one hop over
+//      NVLink, tag-validated "LL" words, no fences) and its candidate row's panel
+//      values into its own rank's mailbox
+//   C  each CTA polls its own rank's slots: the max key is the pivot P ([R3]),
+//      identical on every rank (it is the allreduce(max) of the north_star)
+//   D  column entries for own rows I: pos(I) < pos(P): row P of own column I
+//      (local); pos(I) > pos(P): column P on its owner (a peer read); the pivot
+//      row's panel values from the winner's mailbox (a peer read)
+//   E  c_I, s_I = c_I / sqrt|d|, L = c_I / d, lazy diagonal -- the same fmaf
+//      sequence as the one-GPU chain [R8], so the bits do not depend on G.
+// After the chain each rank gathers the panel S of ALL rows from the owners
+// (k_dgather: the panel broadcast), compacts its local columns and updates its
+// own lower-triangle columns (k_trailing_d, the FFMA2 tile of k_trailing_c over a
+// device-built tile list).  The factor rows are gathered from their owners at the
+// end.
+//
+// One code path for real ranks and their one-GPU emulation: every peer buffer is
+// reached through a per-rank pointer table (CUDA-IPC mappings on a multi-GPU
+// context; plain buffers of this GPU when G ranks are emulated, where ONE
+// cooperative launch runs all ranks' chain CTAs -- the profiling guide forbids
+// separate launches that wait on one another on one GPU).  Cross-rank spins carry
+// a timeout (status[3] = 1, HF_ERR) so a lost peer cannot hang the GPU.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hf_internal.cuh"
+
+namespace hf {
+namespace {
+
+constexpr uint32_t DPOS_MAX = 0x1FFFF;   // 17-bit position field -> L <= 131071
+constexpr int DCB = 128;                 // ownership block: owner(j) = (j / DCB) % G
+constexpr int DTB = 128;                 // trailing tile
+constexpr int DTK = 16;                  // trailing k chunk
+constexpr int DTNS = 3;                  // cp.async stages
+constexpr size_t DTRAIL_SMEM = (size_t)2 * DTNS * DTK * DTB * sizeof(float);
+constexpr int DSLOT = 32;                // 256 B between slots
+constexpr uint64_t DTAGM = 0x3FFF;
+
+__device__ __forceinline__ int owner_of(int64_t j, int G) { return (int)((j / DCB) % G); }
+__host__ __device__ __forceinline__ int64_t col_orig(int64_t c, int h, int G) {
+    return (c / DCB) * ((int64_t)DCB * G) + (int64_t)h * DCB + (c % DCB);
+}
+__device__ __forceinline__ uint64_t dkey(float d, uint32_t pos) {
+    const uint64_t ab = __float_as_uint(fabsf(d));
+    return (ab << 32) | ((uint64_t)(DPOS_MAX - pos) << 15) | ((uint64_t)(d < 0.f) << 14) | 1ull;
+}
+__device__ __forceinline__ uint64_t dtag(int64_t k) { return (uint64_t)(k % 16383) + 1; }
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// system scope: the words cross NVLink on a multi-GPU context
+__device__ __forceinline__ void st_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_sys_f32(const float *p) {
+    float v;
+    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace
+
+// per-rank buffers, reached through a device table (peer mappings on a real run)
+struct DRank {
+    float *V[2];             // L x ncols, rows = global position, ld = ldp (ping-pong)
+    int32_t *lpos[2];        // local column -> global position (this / next panel)
+    int32_t *lorig[2];       // local column -> original index
+    int32_t *nloc;           // [2] active local columns (this / next panel)
+    int32_t *cmapL;          // new local column -> old local column
+    float *S;                // own rows' s_i^t at panel-start positions, ld = lds
+    float *Lorig;            // L_{orig, k} (may alias across emulated ranks)
+    unsigned long long *slots;   // [2][G * Cmax][DSLOT]
+    unsigned long long *mbox;    // [2][Cmax][nbmax + 1]
+    float *Dk;               // [L] pivots d_k
+    int32_t *pivorig;        // [L] original index of pivot k
+    int32_t *pivpos;         // [nbmax] pivot positions of the panel
+    float *sigma;            // [nbmax] sign of d_t
+    int32_t *status;         // [4]: N_tau if stopped, pivots in last panel, stopped, peer timeout
+    int32_t *orig[2];        // global position -> original index (identical on every rank)
+    int32_t *map;            // new position -> old position
+    int32_t *tiles;          // [CTmax + 1] tile prefix | [CTmax] first row tile
+    float *Sc, *Snc;         // the panel in the NEW position space (all rows), ld = ldc
+    float *Scol;             // s of own local columns (new local order), ld = ldcol
+    unsigned int *bar;       // cross-rank barrier counter
+};
+
+namespace {
+
+struct DChainArgs {
+    const DRank *rp;
+    int G, rank0, Cper, R, cur, nbp, nbmax;
+    int64_t m, K0, ldp, lds, ldl;
+    double tau;
+    unsigned long long timeout_ns;
+};
+
+// One cooperative launch: CTA b belongs to rank rank0 + b / Cper (its local
+// index lb = b % Cper) and owns local columns [lb R, lb R + R) of that rank.
+__global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
+    extern __shared__ __align__(16) float smem[];
+    __shared__ unsigned long long red[32];
+    __shared__ uint32_t redi[32];
+    __shared__ unsigned long long bkey;
+    __shared__ uint32_t binfo;
+    __shared__ int bail;
+    const int grp = blockIdx.x / a.Cper, lb = blockIdx.x % a.Cper;
+    const int h = a.rank0 + grp;
+    const DRank &me = a.rp[h];
+    if (*(volatile int32_t *)&me.status[2] || *(volatile int32_t *)&me.status[3]) return;   // uniform per rank
+    const int GT = a.G * a.Cper;
+    const int gid = h * a.Cper + lb;
+    const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
+    const int cur = a.cur;
+    const int64_t nl = me.nloc[cur];
+    const int64_t c0 = (int64_t)lb * a.R;
+    const int64_t nown = max((int64_t)0, min((int64_t)a.R, nl - c0));
+    const int nb = a.nbp;
+    float *sneg = smem;                                          // [nbp][R] -sigma_u s_i^u, own rows
+    float *sp = smem + (((size_t)nb * a.R + 3) & ~(size_t)3);    // [nbp] s_P^u of the pivot row
+    float *sgm = sp + nb;                                        // [nbp] sigma_u
+    const bool has = tid < nown;
+    const int64_t c = c0 + tid;                                  // own local column = own row
+    const int64_t i = has ? (int64_t)me.lpos[cur][c] : 0;        // its global position
+    const int32_t oi = has ? me.lorig[cur][c] : 0;
+    const float *Vme = me.V[cur];
+    float dg = has ? Vme[i + c * a.ldp] : 0.f;                   // lazy diagonal
+    const uint32_t myinfo = has ? (((uint32_t)h << 20) | (uint32_t)c) : 0u;
+    bool piv = !has;
+    float dprev = a.K0 > 0 ? me.Dk[a.K0 - 1] : 0.f;
+    bool pend = false;
+    float ps = 0.f, pl = 0.f;
+    int t = 0;
+    bool stopped = false;
+    if (tid == 0) bail = 0;
+    const unsigned long long deadline = gtime() + a.timeout_ns;
+    unsigned long long *myslots = me.slots;
+    for (; t < nb;) {
+        const int64_t k = a.K0 + t;
+        const uint64_t tag = dtag(k);
+        const int par = (int)(k & 1);
+        // ---- A: [R3] local argmax over own active rows, carrying (rank, local column)
+        uint64_t key = !piv ? dkey(dg, (uint32_t)i) : 0ull;
+        uint32_t kinfo = myinfo;
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) {
+            const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, key, o2);
+            const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, kinfo, o2);
+            if (ok2 > key) {
+                key = ok2;
+                kinfo = oi2;
+            }
+        }
+        if (lane == 0) {
+            red[wid] = key;
+            redi[wid] = kinfo;
+        }
+        __syncthreads();
+        // ---- B: publish the CTA's key to every rank; its candidate's panel values to its mailbox
+        if (wid < 2) {
+            uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
+            uint32_t vinfo = (lane < nwarp) ? redi[lane] : 0u;
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) {
+                const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, v, o2);
+                const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, vinfo, o2);
+                if (ok2 > v) {
+                    v = ok2;
+                    vinfo = oi2;
+                }
+            }
+            if (wid == 0) {
+                for (int q = lane; q < a.G; q += 32) {   // one slot per CTA in every rank's array
+                    unsigned long long *slot = a.rp[q].slots + ((size_t)par * GT + gid) * DSLOT;
+                    st_sys_u64(slot + 1, ((unsigned long long)(v ? vinfo : 0u) << 32) | tag);
+                    st_sys_u64(slot, (v & ~DTAGM) | tag);
+                }
+            } else if (v) {
+                unsigned long long *mb = me.mbox + ((size_t)par * a.Cper + lb) * (a.nbmax + 1);
+                const int lr = (int)((int64_t)(vinfo & 0xFFFFF) - c0);
+                for (int u = lane; u < t; u += 32)
+                    st_sys_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + lr]) << 32) | tag);
+            }
+        }
+        // ---- deferred global stores of step t-1 (own rows)
+        if (pend) {
+            me.S[i + (int64_t)(t - 1) * a.lds] = ps;
+            me.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            pend = false;
+        }
+        // ---- C: every slot of this step (tags); the max key is the pivot
+        if (wid == 0) {
+            const unsigned long long *sl = myslots + (size_t)par * GT * DSLOT;
+            uint64_t mx, mi = 0;
+            unsigned spins = 0;
+            for (;;) {
+                bool ok = true;
+                mx = 0;
+                for (int g = lane; g < GT; g += 32) {
+                    const uint64_t sv = ld_sys_u64(&sl[(size_t)g * DSLOT]);
+                    const uint64_t si = ld_sys_u64(&sl[(size_t)g * DSLOT + 1]);
+                    ok &= ((sv & DTAGM) == tag) && ((si & DTAGM) == tag);
+                    if (sv > mx) {
+                        mx = sv;
+                        mi = si;
+                    }
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+                if ((++spins & 1023u) == 0 && gtime() > deadline) {
+                    if (lane == 0) {
+                        bail = 1;
+                        me.status[3] = 1;
+                    }
+                    break;
+                }
+            }
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) {
+                const uint64_t ox = __shfl_xor_sync(0xffffffffu, mx, o2);
+                const uint64_t oi2 = __shfl_xor_sync(0xffffffffu, mi, o2);
+                if (ox > mx) {
+                    mx = ox;
+                    mi = oi2;
+                }
+            }
+            if (lane == 0) {
+                bkey = mx;
+                binfo = (uint32_t)(mi >> 32);
+            }
+        }
+        __syncthreads();
+        if (bail) return;
+        const uint64_t bk = bkey;
+        const float absd = __uint_as_float((uint32_t)(bk >> 32));
+        const int64_t P = (int64_t)(DPOS_MAX - (uint32_t)((bk >> 15) & DPOS_MAX));
+        const float d = ((bk >> 14) & 1) ? -absd : absd;
+        // ---- [R4] stop test, in FP64, strict, against the previous accepted pivot
+        const bool stop = (bk == 0) || (a.K0 + t == 0 ? (absd == 0.f)
+                                                       : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev))));
+        if (stop) {
+            if (lb == 0 && tid == 0) {
+                me.status[0] = (int32_t)k;
+                me.status[1] = t;
+                me.status[2] = 1;
+            }
+            stopped = true;
+            break;
+        }
+        const float sg = d > 0.f ? 1.f : -1.f;
+        const uint32_t w = binfo;
+        const int hP = (int)(w >> 20);
+        const int64_t cP = (int64_t)(w & 0xFFFFF);
+        // ---- D: own rows' panel-start column entries (peer read for rows below P), then
+        //      the pivot row's panel values from the winner's mailbox
+        float v = 0.f;
+        if (!piv && i != P) {
+            if (i > P) v = ld_sys_f32(a.rp[hP].V[cur] + i + cP * a.ldp);   // column P on its owner
+            else v = Vme[P + c * a.ldp];                                  // row P of own column
+        }
+        {
+            const unsigned long long *mb = a.rp[hP].mbox + ((size_t)par * a.Cper + cP / a.R) * (a.nbmax + 1);
+            for (int u = tid; u < t; u += nthr) {
+                uint64_t ww;
+                unsigned spins = 0;
+                do {
+                    ww = ld_sys_u64(&mb[u]);
+                    if ((++spins & 1023u) == 0 && gtime() > deadline) {
+                        bail = 1;
+                        me.status[3] = 1;
+                        break;
+                    }
+                } while ((ww & DTAGM) != tag);
+                sp[u] = -sgm[u] * __uint_as_float((uint32_t)(ww >> 32));   // s_P^u (exact sign flip)
+            }
+            if (tid == 0) sgm[t] = sg;
+        }
+        __syncthreads();
+        if (bail) return;
+        // ---- E: column, scaled column, lazy diagonal [R6]-[R8], [R10]
+        const float r = __fsqrt_rn(absd);
+        if (lb == 0 && tid == 0) {   // every rank records the pivot (identical everywhere)
+            me.Dk[k] = d;
+            me.pivorig[k] = me.orig[cur][P];
+            me.pivpos[t] = (int32_t)P;
+            me.sigma[t] = sg;
+        }
+        if (has && i == P) {
+            piv = true;
+        } else if (!piv) {
+            float cc = v;
+            const float *sn = sneg + tid;
+            int u = 0;
+            for (; u + 8 <= t; u += 8) {   // [R8] one fmaf per earlier in-panel pivot, in order
+                float x[8], y[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    x[q] = sn[(size_t)(u + q) * a.R];
+                    y[q] = sp[u + q];
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) cc = __fmaf_rn(x[q], y[q], cc);
+            }
+            for (; u < t; ++u) cc = __fmaf_rn(sn[(size_t)u * a.R], sp[u], cc);
+            const float sv = __fdiv_rn(cc, r);
+            const float ns = -sg * sv;
+            sneg[(size_t)t * a.R + tid] = ns;
+            ps = sv;
+            pl = __fdiv_rn(cc, d);
+            pend = true;
+            dg = __fmaf_rn(ns, sv, dg);
+        }
+        dprev = d;
+        ++t;
+    }
+    if (pend) {
+        me.S[i + (int64_t)(t - 1) * a.lds] = ps;
+        me.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+    }
+    if (!stopped && lb == 0 && tid == 0) me.status[1] = t;
+}
+
+// --------------------------------------------------------------- per-rank setup
+// V_h[i + c ldp] = RN32(K(i, j)) for own column c (original j) and rows i >= j
+// (lower triangle of K [R1], [R2]); lpos = lorig = j; orig = iota
+__global__ void k_dcast(int64_t L, const double *__restrict__ K, int64_t ld, int h, int G, float *__restrict__ V,
+                        int64_t ldp, int64_t ncols, int32_t *lpos, int32_t *lorig) {
+    for (int64_t c = blockIdx.x; c < ncols; c += gridDim.x) {
+        const int64_t j = col_orig(c, h, G);
+        if (threadIdx.x == 0) {
+            lpos[c] = (int32_t)j;
+            lorig[c] = (int32_t)j;
+        }
+        const double *kc = K + j * ld;
+        float *vc = V + c * ldp;
+        for (int64_t i = j + threadIdx.x; i < L; i += blockDim.x) vc[i] = __double2float_rn(kc[i]);
+    }
+}
+
+__global__ void k_diota(int64_t n, int32_t *a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+
+// global stable compaction (identical on every rank): map[new] = old, orig_new
+__global__ void k_dcompact(int64_t m, int nbp, const int32_t *__restrict__ pivpos, const int32_t *__restrict__ orig,
+                           int32_t *__restrict__ map, int32_t *__restrict__ norig, const int32_t *status) {
+    __shared__ int32_t srt[1024];
+    if (status[2] || status[3]) return;
+    for (int q = threadIdx.x; q < nbp; q += blockDim.x) {
+        const int32_t v = pivpos[q];
+        int rk = 0;
+        for (int w = 0; w < nbp; ++w) rk += (pivpos[w] < v);
+        srt[rk] = v;
+    }
+    __syncthreads();
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nbp;
+        while (lo < hi) {
+            const int md = (lo + hi) >> 1;
+            if (srt[md] < p) lo = md + 1;
+            else hi = md;
+        }
+        if (!(lo < nbp && srt[lo] == p)) {
+            map[p - lo] = (int32_t)p;
+            norig[p - lo] = orig[p];
+        }
+    }
+}
+
+// local compaction of rank h: old local column c (position pos) -> c - #own pivots
+// below pos, at position pos - #pivots below pos; cmapL[new] = old
+__global__ void k_dlocal(int h, int G, int nbp, const int32_t *__restrict__ pivpos, const int32_t *__restrict__ orig,
+                         const int32_t *__restrict__ lpos, const int32_t *__restrict__ lorig, int32_t *__restrict__ nlpos,
+                         int32_t *__restrict__ nlorig, int32_t *__restrict__ cmapL, int32_t *nloc, int cur,
+                         const int32_t *status) {
+    __shared__ int32_t srt[1024], ownp[1025];
+    if (status[2] || status[3]) return;
+    for (int q = threadIdx.x; q < nbp; q += blockDim.x) {
+        const int32_t v = pivpos[q];
+        int rk = 0;
+        for (int w = 0; w < nbp; ++w) rk += (pivpos[w] < v);
+        srt[rk] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {   // prefix count of own pivots in sorted order
+        int cnt = 0;
+        ownp[0] = 0;
+        for (int q = 0; q < nbp; ++q) {
+            cnt += owner_of(orig[srt[q]], G) == h;
+            ownp[q + 1] = cnt;
+        }
+        if (blockIdx.x == 0) nloc[cur ^ 1] = nloc[cur] - cnt;
+    }
+    __syncthreads();
+    const int64_t nl = nloc[cur];
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nl; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = lpos[c];
+        int lo = 0, hi = nbp;
+        while (lo < hi) {
+            const int md = (lo + hi) >> 1;
+            if (srt[md] < p) lo = md + 1;
+            else hi = md;
+        }
+        if (lo < nbp && srt[lo] == p) continue;   // pivoted
+        const int64_t cn = c - ownp[lo];
+        nlpos[cn] = p - lo;
+        nlorig[cn] = lorig[c];
+        cmapL[cn] = (int32_t)c;
+    }
+}
+
+// the panel broadcast: Sc[t ldc + p'] = s of the row at new position p', read from
+// the rank owning it (a peer read on a real run), Snc = -sigma_t s
+struct DGatherArgs {
+    const DRank *rp;
+    int h, G, nbp, cur;
+    int64_t mp, lds, ldc;
+};
+__global__ void k_dgather(DGatherArgs a) {
+    const DRank &me = a.rp[a.h];
+    if (me.status[2] || me.status[3]) return;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.mp) return;
+    const int64_t o = me.map[p];                          // panel-start position of the row
+    const float *src = a.rp[owner_of(me.orig[a.cur][o], a.G)].S;
+    const int t0 = blockIdx.y * 16, t1 = min(a.nbp, t0 + 16);
+    for (int t = t0; t < t1; ++t) {
+        const float sv = src[o + (int64_t)t * a.lds];
+        me.Sc[(int64_t)t * a.ldc + p] = sv;
+        me.Snc[(int64_t)t * a.ldc + p] = -me.sigma[t] * sv;
+    }
+}
+
+// s of own local columns in their new order: Scol[t ldcol + c'] = Sc[t ldc + lpos'[c']];
+// the tile list of the trailing update: column tile ct starts at row tile lpos'[128 ct] / 128
+__global__ void k_dcols(int nbp, int64_t mp, const float *__restrict__ Sc, int64_t ldc, const int32_t *__restrict__ nlpos,
+                        const int32_t *nloc, int nxt, float *__restrict__ Scol, int64_t ldcol, int32_t *tiles, int ctmax,
+                        const int32_t *status) {
+    if (status[2] || status[3]) return;
+    const int64_t nl = nloc[nxt];
+    if (blockIdx.x == 0) {   // tile prefix (one CTA)
+        __shared__ int32_t cnt[1024];
+        const int RT = (int)((mp + DTB - 1) / DTB);
+        const int CT = (int)((nl + DTB - 1) / DTB);
+        for (int ct = threadIdx.x; ct < ctmax; ct += blockDim.x) {
+            int rt0 = 0, n = 0;
+            if (ct < CT) {
+                rt0 = nlpos[(int64_t)ct * DTB] / DTB;
+                n = RT - rt0;
+            }
+            cnt[ct] = n;
+            tiles[ctmax + 1 + ct] = rt0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int ct = 0; ct < ctmax; ++ct) {
+                tiles[ct] = s;
+                s += cnt[ct];
+            }
+            tiles[ctmax] = s;
+        }
+        return;
+    }
+    const int64_t cn = (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
+    if (cn >= ldcol) return;
+    const int64_t pp = cn < nl ? (int64_t)nlpos[cn] : -1;
+    for (int t = 0; t < nbp; ++t) Scol[(int64_t)t * ldcol + cn] = pp >= 0 ? Sc[(int64_t)t * ldc + pp] : 0.f;
+}
+
+__device__ __forceinline__ void cp_async16_d(void *sdst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+// Trailing update of rank h's own lower-triangle columns (persistent over the tile
+// list): entry (row p', local column c') starts from Vold[map[p'] + cmapL[c'] ldp]
+// and receives one fmaf(-sigma_t s_I^t, s_J^t, v) per pivot t in order [R8] -- the
+// inner loop of k_trailing_c; rows above the column's position are not stored.
+struct DTrailArgs {
+    int64_t mp;
+    int nbp, ctmax;
+    const float *Vold;
+    float *Vnew;
+    int64_t ldp;
+    const int32_t *map;     // new position -> old position (rows)
+    const int32_t *cmapL;   // new local column -> old local column
+    const int32_t *nlpos;   // new local column -> new position
+    const int32_t *nloc;    // [2]
+    int nxt;
+    const int32_t *tiles;
+    const float *Snc, *Scol;
+    int64_t ldc, ldcol;
+    const int32_t *status;
+};
+__global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
+    if (a.status[2] || a.status[3]) return;
+    extern __shared__ __align__(16) float dsm[];
+    float (*As)[DTK][DTB] = reinterpret_cast<float (*)[DTK][DTB]>(dsm);
+    float (*Bs)[DTK][DTB] = reinterpret_cast<float (*)[DTK][DTB]>(dsm + DTNS * DTK * DTB);
+    __shared__ int32_t rmap[DTB], cmap[DTB], cpos[DTB];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int nchunk = (a.nbp + DTK - 1) / DTK;
+    const int64_t ntiles = a.tiles[a.ctmax];
+    const int64_t nl = a.nloc[a.nxt];
+#define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
+#define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+        int lo = 0, hi = a.ctmax - 1;   // column tile: last ct with tiles[ct] <= tt
+        while (lo < hi) {
+            const int md = (lo + hi + 1) >> 1;
+            if (a.tiles[md] <= tt) lo = md;
+            else hi = md - 1;
+        }
+        const int ct = lo;
+        const int64_t rt = a.tiles[a.ctmax + 1 + ct] + (tt - a.tiles[ct]);
+        const int64_t row0 = rt * DTB, col0 = (int64_t)ct * DTB;
+        const int mpr = (int)min((int64_t)DTB, a.mp - row0), mpc = (int)min((int64_t)DTB, nl - col0);
+        auto issue = [&](int cq) {
+            if (cq < nchunk) {
+                const int st = cq % DTNS;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int e = tid + u * 256;
+                    const int k = e >> 5, r4 = (e & 31) * 4;
+                    cp_async16_d(&As[st][k][r4], a.Snc + (int64_t)(cq * DTK + k) * a.ldc + row0 + r4);
+                    cp_async16_d(&Bs[st][k][r4], a.Scol + (int64_t)(cq * DTK + k) * a.ldcol + col0 + r4);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        __syncthreads();   // the previous tile's readers of As / Bs / maps are done
+        issue(0);
+        issue(1);
+        if (tid < DTB) {
+            rmap[tid] = (tid < mpr) ? a.map[row0 + tid] : -1;
+        } else {
+            const int q = tid - DTB;
+            cmap[q] = (q < mpc) ? a.cmapL[col0 + q] : -1;
+            cpos[q] = (q < mpc) ? a.nlpos[col0 + q] : 0x7FFFFFFF;
+        }
+        __syncthreads();
+        float2 acc[8][4];
+        {
+            int32_t rm[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int cl = CC(2 * j + hh);
+                    const int32_t cm = cmap[cl];
+                    const int32_t cp = cpos[cl];
+                    const float *colp = a.Vold + (int64_t)(cm >= 0 ? cm : 0) * a.ldp;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool ok = cm >= 0 && rm[q] >= 0 && row0 + RR(q) >= cp;
+                        const float v = ok ? __ldg(colp + rm[q]) : 0.f;
+                        if (hh) acc[q][j].y = v;
+                        else acc[q][j].x = v;
+                    }
+                }
+            }
+        }
+        for (int cq = 0; cq < nchunk; ++cq) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            issue(cq + 2);
+            const int st = cq % DTNS;
+            const int kmax = min(DTK, a.nbp - cq * DTK);
+            if (kmax == DTK) {
+#pragma unroll
+                for (int kk = 0; kk < DTK; ++kk) {
+                    const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                    const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                    const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                          make_float2(b1.z, b1.w)};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+                }
+            } else {
+                for (int kk = 0; kk < kmax; ++kk) {   // ragged last chunk: exactly nbp updates
+                    const float4 a0 = *reinterpret_cast<const float4 *>(&As[st][kk][tx * 4]);
+                    const float4 a1 = *reinterpret_cast<const float4 *>(&As[st][kk][64 + tx * 4]);
+                    const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[st][kk][ty * 4]);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[st][kk][64 + ty * 4]);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                          make_float2(b1.z, b1.w)};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
+                }
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        // fully below the diagonal band (every row at or below every column's position)
+        const bool full = mpr == DTB && mpc == DTB && row0 >= cpos[DTB - 1] && (a.ldp & 3) == 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int cl = CC(2 * j + hh);
+                float *colp = a.Vnew + (col0 + cl) * a.ldp + row0;
+                if (full) {
+                    *reinterpret_cast<float4 *>(colp + tx * 4) =
+                        hh ? make_float4(acc[0][j].y, acc[1][j].y, acc[2][j].y, acc[3][j].y)
+                           : make_float4(acc[0][j].x, acc[1][j].x, acc[2][j].x, acc[3][j].x);
+                    *reinterpret_cast<float4 *>(colp + 64 + tx * 4) =
+                        hh ? make_float4(acc[4][j].y, acc[5][j].y, acc[6][j].y, acc[7][j].y)
+                           : make_float4(acc[4][j].x, acc[5][j].x, acc[6][j].x, acc[7][j].x);
+                } else if (cl < mpc) {
+                    const int32_t cp = cpos[cl];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int rl = RR(q);
+                        if (rl < mpr && row0 + rl >= cp) colp[rl] = hh ? acc[q][j].y : acc[q][j].x;
+                    }
+                }
+            }
+        }
+    }
+#undef RR
+#undef CC
+}
+
+// Lfac[a + k ldf] = L_{pivorig[a], k} from the rank owning row pivorig[a]
+__global__ void k_dgather_L(int64_t N, int G, const DRank *rp, int h, int64_t ldl, float *__restrict__ Lfac,
+                            int64_t ldf) {
+    const int32_t *pivorig = rp[h].pivorig;
+    for (int64_t k = blockIdx.x; k < N; k += gridDim.x) {
+        float *dst = Lfac + k * ldf;
+        for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
+            float v = 0.f;
+            if (r == k) v = 1.f;
+            else if (r > k) {
+                const int32_t o = pivorig[r];
+                v = rp[owner_of(o, G)].Lorig[o + k * ldl];
+            }
+            dst[r] = v;
+        }
+    }
+}
+
+// cross-rank barrier (real ranks): every rank adds 1 to every rank's counter
+// (release, system scope), then waits until its own counter reaches G * epoch
+__global__ void k_xbar(const DRank *rp, int G, int h, unsigned int epoch, unsigned long long timeout_ns) {
+    if (threadIdx.x != 0) return;
+    for (int q = 0; q < G; ++q) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(rp[q].bar) : "memory");
+    const unsigned long long deadline = gtime() + timeout_ns;
+    const unsigned int want = (unsigned int)G * epoch;
+    unsigned int v;
+    unsigned spins = 0;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(rp[h].bar) : "memory");
+        if (v >= want) break;
+        if ((++spins & 1023u) == 0 && gtime() > deadline) {
+            rp[h].status[3] = 1;
+            break;
+        }
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host driver
+struct DistBufs {
+    DBuf<float> V[2], S, Sc, Snc, Scol, Dk, sigma;
+    DBuf<int32_t> lpos[2], lorig[2], nloc, cmapL, pivorig, pivpos, status, orig[2], map, tiles;
+    DBuf<unsigned long long> slots, mbox;
+    DBuf<unsigned int> bar;
+};
+
+// trailing: one FMA per lower-triangle entry per pivot (the same algorithmic count as
+// one GPU: every pair is stored on exactly one rank); chain as in k_lowprec.cu
+static double dtrail_flops_total(int64_t mp, int nbp) { return (double)mp * (double)(mp + 1) * nbp; }
+// "<cls>@<rank>": per-rank kernel classes of the emulation (tools/dist_model.py)
+static const char *rank_class(const char *cls, int h) {
+    static std::vector<std::string> names[2];
+    const int w = cls[0] == 't' ? 0 : 1;
+    auto &v = names[w];
+    if (v.capacity() < 64) v.reserve(64);   // c_str() pointers stay valid (G <= 64)
+    while ((int)v.size() <= h) v.push_back(std::string(cls) + "@" + std::to_string(v.size()));
+    return v[h].c_str();
+}
+
+void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
+                         hf_lowfactor *lf, int nparts) {
+    cudaStream_t st = ctx->stream;
+    const int nsm = ctx->num_sms;
+    lf->L = L;
+    lf->stream = st;
+    if (L == 0) {
+        lf->N = lf->Ntau = lf->n2 = 0;
+        return;
+    }
+    const bool real = ctx->nranks > 1;
+    const int G = real ? ctx->nranks : nparts;
+    HF_REQUIRE(L <= (int64_t)DPOS_MAX - 1, "L too large for the 17-bit position key");
+    HF_REQUIRE(G >= 1 && G <= 64, "stage-1 ranks out of range (1..64)");
+    HF_REQUIRE(L <= ((int64_t)1 << 20), "L too large for the 20-bit local column field");
+    const int lo = real ? ctx->rank : 0, hi = real ? ctx->rank + 1 : G;
+    std::vector<int64_t> ncols(G, 0);
+    for (int64_t j = 0; j < L; ++j) ncols[(j / DCB) % G]++;
+    int64_t ncmax = 1;
+    for (auto c : ncols) ncmax = std::max(ncmax, c);
+
+    // chain geometry: Cper CTAs per rank, R rows each, the panel's values of own rows in
+    // shared memory (R x nb floats); emulated ranks share this GPU's SMs (one CTA per SM)
+    int maxsmem = 0;
+    HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    cudaFuncAttributes fa;
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_d));
+    maxsmem -= (int)fa.sharedSizeBytes + 64;
+    const int cmax_sm = real ? nsm : std::max(1, nsm / G);
+    int cper_def = (int)std::min<int64_t>(cmax_sm, std::max<int64_t>(1, cdiv(ncmax, 128)));
+    if (const char *e = getenv("HF_DIST_CTAS")) cper_def = std::max(1, std::min(cmax_sm, atoi(e)));
+    int Cmax = std::max(cper_def, (int)std::min<int64_t>(cmax_sm, cdiv(ncmax, 1024)));
+    int64_t R0 = cdiv(ncmax, Cmax);
+    int nb = o.nb > 0 ? o.nb : 128;
+    while (nb > 16 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem) nb -= 16;
+    while (nb > 8 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem) nb /= 2;
+    // more CTAs if the panel does not fit even at nb = 8
+    while ((int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem && Cmax < cmax_sm) {
+        ++Cmax;
+        R0 = cdiv(ncmax, Cmax);
+    }
+    HF_REQUIRE(R0 <= 1024 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 <= (int64_t)maxsmem,
+               "stage 1 (distributed): a rank's rows do not fit its chain CTAs");
+    const int64_t ldp = L, lds = L, ldl = L;
+    const int64_t ldc = cdiv(L, DTB) * DTB;
+    const int64_t ldcol = cdiv(ncmax, DTB) * DTB;
+    const int ctmax = (int)cdiv(ncmax, DTB);
+    HF_REQUIRE(ctmax <= 1024, "stage 1 (distributed): too many column tiles per rank");
+    const int nbpad = (int)cdiv(nb, DTK) * DTK;
+
+    std::vector<DistBufs> B(G);
+    DBuf<float> Lorig_shared;
+    std::vector<DRank> tab(G);
+    std::memset(tab.data(), 0, sizeof(DRank) * G);
+    for (int h = lo; h < hi; ++h) {
+        DistBufs &b = B[h];
+        const int64_t nc = std::max<int64_t>(ncols[h], 1);
+        for (int q = 0; q < 2; ++q) {
+            b.V[q].alloc((size_t)L * nc, st);
+            b.lpos[q].alloc(nc, st);
+            b.lorig[q].alloc(nc, st);
+            b.orig[q].alloc(L, st);
+        }
+        b.S.alloc((size_t)L * nb, st);
+        b.Sc.alloc((size_t)ldc * nbpad, st);
+        b.Snc.alloc((size_t)ldc * nbpad, st);
+        b.Scol.alloc((size_t)ldcol * nbpad, st);
+        b.Dk.alloc(L, st);
+        b.sigma.alloc(nb, st);
+        b.nloc.alloc(2, st);
+        b.cmapL.alloc(nc, st);
+        b.pivorig.alloc(L, st);
+        b.pivpos.alloc(nb, st);
+        b.status.alloc(4, st);
+        b.status.zero(st);
+        b.map.alloc(L, st);
+        b.tiles.alloc((size_t)2 * ctmax + 1, st);
+        b.slots.alloc((size_t)2 * G * Cmax * DSLOT, st);
+        b.slots.zero(st);
+        b.mbox.alloc((size_t)2 * Cmax * (nb + 1), st);
+        b.mbox.zero(st);
+        b.bar.alloc(1, st);
+        b.bar.zero(st);
+        DRank &r = tab[h];
+        for (int q = 0; q < 2; ++q) {
+            r.V[q] = b.V[q].p;
+            r.lpos[q] = b.lpos[q].p;
+            r.lorig[q] = b.lorig[q].p;
+            r.orig[q] = b.orig[q].p;
+        }
+        r.nloc = b.nloc.p; r.cmapL = b.cmapL.p; r.S = b.S.p; r.slots = b.slots.p; r.mbox = b.mbox.p;
+        r.Dk = b.Dk.p; r.pivorig = b.pivorig.p; r.pivpos = b.pivpos.p; r.sigma = b.sigma.p; r.status = b.status.p;
+        r.map = b.map.p; r.tiles = b.tiles.p; r.Sc = b.Sc.p; r.Snc = b.Snc.p; r.Scol = b.Scol.p; r.bar = b.bar.p;
+    }
+    // the factor rows by original index: one per rank on a real run, shared when emulated
+    DBuf<float> Lorig_mine;
+    if (real) {
+        Lorig_mine.alloc((size_t)L * L, st);
+        tab[ctx->rank].Lorig = Lorig_mine.p;
+    } else {
+        Lorig_shared.alloc((size_t)L * L, st);
+        for (int h = 0; h < G; ++h) tab[h].Lorig = Lorig_shared.p;
+    }
+    std::vector<void *> opened;
+#ifdef HF_WITH_NCCL
+    if (real) {
+        // peers' V (both buffers), S, slots, mbox, Lorig, barrier counter: CUDA-IPC handles
+        // all-gathered over NCCL, opened with peer access (NVLink)
+        constexpr int NH = 7;
+        void *mine[NH] = {tab[ctx->rank].V[0], tab[ctx->rank].V[1], tab[ctx->rank].S, tab[ctx->rank].slots,
+                          tab[ctx->rank].mbox, tab[ctx->rank].Lorig, tab[ctx->rank].bar};
+        std::vector<cudaIpcMemHandle_t> hm(NH);
+        for (int q = 0; q < NH; ++q) HF_CUDA(cudaIpcGetMemHandle(&hm[q], mine[q]));
+        const size_t hb = NH * sizeof(cudaIpcMemHandle_t);
+        DBuf<char> dh;
+        dh.alloc(hb * (G + 1), st);
+        HF_CUDA(cudaMemcpyAsync(dh.p, hm.data(), hb, cudaMemcpyHostToDevice, st));
+        collective_allgather_bytes(ctx, dh.p, dh.p + hb, hb);
+        std::vector<cudaIpcMemHandle_t> all((size_t)NH * G);
+        HF_CUDA(cudaMemcpyAsync(all.data(), dh.p + hb, hb * G, cudaMemcpyDeviceToHost, st));
+        HF_CUDA(cudaStreamSynchronize(st));
+        for (int g = 0; g < G; ++g) {
+            if (g == ctx->rank) continue;
+            void *pp[NH];
+            for (int q = 0; q < NH; ++q) {
+                HF_CUDA(cudaIpcOpenMemHandle(&pp[q], all[(size_t)g * NH + q], cudaIpcMemLazyEnablePeerAccess));
+                opened.push_back(pp[q]);
+            }
+            tab[g].V[0] = (float *)pp[0]; tab[g].V[1] = (float *)pp[1]; tab[g].S = (float *)pp[2];
+            tab[g].slots = (unsigned long long *)pp[3]; tab[g].mbox = (unsigned long long *)pp[4];
+            tab[g].Lorig = (float *)pp[5]; tab[g].bar = (unsigned int *)pp[6];
+        }
+    }
+#else
+    HF_REQUIRE(!real, "multi-GPU stage 1 needs NCCL");
+#endif
+    DBuf<DRank> dtab;
+    dtab.alloc(G, st);
+    HF_CUDA(cudaMemcpyAsync(dtab.p, tab.data(), sizeof(DRank) * G, cudaMemcpyHostToDevice, st));
+    const unsigned long long timeout_ns = 60ull * 1000000000ull;
+    unsigned int bar_epoch = 0;
+    auto xbar = [&]() {   // real ranks only: stream-ordered device barrier over NVLink
+        if (!real) return;
+        ++bar_epoch;
+        k_xbar<<<1, 32, 0, st>>>(dtab.p, G, ctx->rank, bar_epoch, timeout_ns);
+        HF_CHECK_LAUNCH(ctx);
+    };
+
+    {
+        ClassTimer tm(ctx, "other");
+        for (int h = lo; h < hi; ++h) {
+            DistBufs &b = B[h];
+            k_dcast<<<(unsigned)std::min<int64_t>(std::max<int64_t>(ncols[h], 1), 65535), 256, 0, st>>>(
+                L, K, ld, h, G, b.V[0].p, ldp, ncols[h], b.lpos[0].p, b.lorig[0].p);
+            HF_CHECK_LAUNCH(ctx);
+            k_diota<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, b.orig[0].p);
+            HF_CHECK_LAUNCH(ctx);
+            const int32_t nl0[2] = {(int32_t)ncols[h], 0};
+            HF_CUDA(cudaMemcpyAsync(b.nloc.p, nl0, sizeof(nl0), cudaMemcpyHostToDevice, st));
+        }
+        HF_CUDA(cudaStreamSynchronize(st));   // nl0 dies here
+    }
+    xbar();   // every rank's columns are cast before anyone reads them
+    HF_CUDA(cudaFuncSetAttribute(k_chain_d, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DTRAIL_SMEM));
+    int tocc = 0;
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, k_trailing_d, 256, DTRAIL_SMEM));
+    const int tgrid = std::max(1, tocc) * nsm;
+
+    int cur = 0;
+    int64_t m = L, K0 = 0;
+    while (m > 0) {
+        const int nbp = (int)std::min<int64_t>(nb, m);
+        // rows per rank are at most min(ncols, m): fewer chain CTAs as the matrix shrinks
+        const int64_t rows_hi = std::min<int64_t>(ncmax, m);
+        const int Cper = (int)std::max<int64_t>(1, std::min<int64_t>(Cmax, cdiv(rows_hi, R0)));
+        const int nthr = (int)std::max<int64_t>(64, cdiv(R0, 32) * 32);
+        const size_t shm = ((size_t)nbp * R0 + 3 * nbp + 8) * sizeof(float);
+        DChainArgs ca;
+        ca.rp = dtab.p; ca.G = G; ca.rank0 = lo; ca.Cper = Cper; ca.R = (int)R0; ca.cur = cur; ca.nbp = nbp;
+        ca.nbmax = nb; ca.m = m; ca.K0 = K0; ca.ldp = ldp; ca.lds = lds; ca.ldl = ldl; ca.tau = o.tau;
+        ca.timeout_ns = timeout_ns;
+        {
+            double cf = 0.0;
+            for (int t = 0; t < nbp; ++t) cf += 2.0 * (double)(m - t) * t;
+            ClassTimer tm(ctx, "chain", st, cf, 16.0 * ((double)m * nbp - 0.5 * (double)nbp * (nbp - 1)));
+            void *args[] = {&ca};
+            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain_d, dim3((unsigned)((hi - lo) * Cper)), dim3(nthr), args,
+                                                shm, st));
+            HF_CHECK_LAUNCH(ctx);
+        }
+        xbar();   // every rank's S of this panel is written before it is gathered
+        const int64_t mp = m - nbp;
+        if (mp > 0) {
+            for (int h = lo; h < hi; ++h) {
+                DistBufs &b = B[h];
+                {
+                    ClassTimer tm(ctx, "other");
+                    ClassTimer tr(ctx, rank_class("gather", h), st);
+                    k_dcompact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
+                        m, nbp, b.pivpos.p, b.orig[cur].p, b.map.p, b.orig[cur ^ 1].p, b.status.p);
+                    HF_CHECK_LAUNCH(ctx);
+                    k_dlocal<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ncols[h], 256), 1024)), 256, 0, st>>>(
+                        h, G, nbp, b.pivpos.p, b.orig[cur].p, b.lpos[cur].p, b.lorig[cur].p, b.lpos[cur ^ 1].p,
+                        b.lorig[cur ^ 1].p, b.cmapL.p, b.nloc.p, cur, b.status.p);
+                    HF_CHECK_LAUNCH(ctx);
+                    DGatherArgs ga;
+                    ga.rp = dtab.p; ga.h = h; ga.G = G; ga.nbp = nbp; ga.cur = cur; ga.mp = mp; ga.lds = lds; ga.ldc = ldc;
+                    k_dgather<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st>>>(ga);
+                    HF_CHECK_LAUNCH(ctx);
+                    k_dcols<<<(unsigned)(1 + cdiv(ldcol, 256)), 256, 0, st>>>(nbp, mp, b.Sc.p, ldc, b.lpos[cur ^ 1].p,
+                                                                            b.nloc.p, cur ^ 1, b.Scol.p, ldcol,
+                                                                            b.tiles.p, ctmax, b.status.p);
+                    HF_CHECK_LAUNCH(ctx);
+                }
+                DTrailArgs ta;
+                ta.mp = mp; ta.nbp = nbp; ta.ctmax = ctmax; ta.Vold = b.V[cur].p; ta.Vnew = b.V[cur ^ 1].p;
+                ta.ldp = ldp; ta.map = b.map.p; ta.cmapL = b.cmapL.p; ta.nlpos = b.lpos[cur ^ 1].p; ta.nloc = b.nloc.p;
+                ta.nxt = cur ^ 1; ta.tiles = b.tiles.p; ta.Snc = b.Snc.p; ta.Scol = b.Scol.p; ta.ldc = ldc;
+                ta.ldcol = ldcol; ta.status = b.status.p;
+                // this rank's share of the algorithmic update (exact per rank is device-side;
+                // the total over the ranks equals one GPU's)
+                ClassTimer tm(ctx, "trailing", st, dtrail_flops_total(mp, nbp) / G, 0.0);
+                ClassTimer tr(ctx, rank_class("trailing", h), st);   // per rank (the time model)
+                k_trailing_d<<<(unsigned)tgrid, 256, DTRAIL_SMEM, st>>>(ta);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            xbar();   // every rank's columns of the next panel are updated before the next chain
+            cur ^= 1;
+        }
+        K0 += nbp;
+        m = mp;
+    }
+    // outputs: every rank holds the pivots, D and the status; the factor rows come
+    // from their owners
+    const int me = lo;
+    lowprec_outputs(ctx, L, o, lf, B[me].status.p, B[me].pivorig.p, B[me].Dk.p);
+    if (lf->N > 0) {
+        ClassTimer tm(ctx, "other");
+        k_dgather_L<<<(unsigned)std::min<int64_t>(lf->N, 65535), 256, 0, st>>>(lf->N, G, dtab.p, me, ldl, lf->Lfac.p,
+                                                                              lf->N);
+        HF_CHECK_LAUNCH(ctx);
+    }
+    xbar();   // nobody reads a peer's buffers any more
+    HF_CUDA(cudaStreamSynchronize(st));
+    int32_t hs[4];
+    HF_CUDA(cudaMemcpy(hs, B[me].status.p, sizeof(hs), cudaMemcpyDeviceToHost));
+    for (void *p : opened) cudaIpcCloseMemHandle(p);
+    HF_REQUIRE(hs[3] == 0, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)");
+}
+
+}  // namespace hf

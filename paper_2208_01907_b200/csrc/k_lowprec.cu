@@ -1223,24 +1223,16 @@ static double chain_flops(int64_t m, int nbp) {
     return f;
 }
 static double chain_bytes(int64_t m, int nbp) { return 16.0 * ((double)m * nbp - 0.5 * (double)nbp * (nbp - 1)); }
-// the part of stage 1 after the panels: N, Pi, D and the factor in pivot order
-static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, DBuf<int32_t> &status,
-                           DBuf<int32_t> &pivorig, DBuf<float> &Dk, DBuf<float> &Lorig, DBuf<unsigned long long> *dbg) {
+// N, Pi, D (host and device) and the factor buffer of lf from the chain's outputs
+// (status = {N_tau if stopped, -, stopped}, pivorig, Dk); the caller gathers the factor
+void lowprec_outputs(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, const int32_t *status,
+                     const int32_t *pivorig, const float *Dk) {
     cudaStream_t st = ctx->stream;
     int32_t hs[4];
-    HF_CUDA(cudaMemcpyAsync(hs, status.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HF_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
     HF_CUDA(cudaStreamSynchronize(st));
+    HF_REQUIRE(hs[3] == 0, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)");
     const int64_t Ntau = hs[2] ? hs[0] : L;
-    if (dbg) {
-        unsigned long long hd[8];
-        HF_CUDA(cudaMemcpy(hd, dbg->p, sizeof(hd), cudaMemcpyDeviceToHost));
-        const double np = hd[4] ? (double)hd[4] : 1.0;
-        fprintf(stderr, "[hf chain] steps %llu  us/step: publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
-                hd[4], hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
-        if (hd[7])
-            fprintf(stderr, "[hf chain] pivot = previous step's runner-up candidate: %.1f %%, runner-up or third: %.1f %%\n",
-                    100.0 * hd[5] / hd[7], 100.0 * hd[6] / hd[7]);
-    }
     // [R5] floor and [R9] enlargement: the last accepted pivots move to Lambda_2
     int64_t N = Ntau;
     if (L - o.n_min < N) N = std::max<int64_t>(0, L - o.n_min);
@@ -1251,9 +1243,9 @@ static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_
 
     // [R10] Pi = [pivots, Lambda_2 ascending]
     std::vector<int32_t> po(std::max<int64_t>(N, 1));
-    if (N > 0) HF_CUDA(cudaMemcpyAsync(po.data(), pivorig.p, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(po.data(), pivorig, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     lf->h_D.assign(std::max<int64_t>(N, 1), 0.f);
-    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->h_D.data(), Dk.p, N * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->h_D.data(), Dk, N * sizeof(float), cudaMemcpyDeviceToHost, st));
     HF_CUDA(cudaStreamSynchronize(st));
     lf->h_D.resize(N);
     std::vector<int32_t> rank(L, -1);
@@ -1265,20 +1257,36 @@ static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_
     int64_t w = N;
     for (int64_t i = 0; i < L; ++i)
         if (rank[i] < 0) lf->h_perm[w++] = i;
-
     lf->perm.alloc(L, st);
     lf->pos1.alloc(L, st);
     HF_CUDA(cudaMemcpyAsync(lf->perm.p, lf->h_perm.data(), L * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     HF_CUDA(cudaMemcpyAsync(lf->pos1.p, rank.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     lf->D.alloc(std::max<int64_t>(N, 1), st);
-    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->D.p, Dk.p, N * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    if (N > 0) HF_CUDA(cudaMemcpyAsync(lf->D.p, Dk, N * sizeof(float), cudaMemcpyDeviceToDevice, st));
     lf->Lfac.alloc((size_t)std::max<int64_t>(N, 1) * std::max<int64_t>(N, 1), st);
+    HF_CUDA(cudaStreamSynchronize(st));   // host vectors used by the copies above must outlive them
+}
+
+static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, DBuf<int32_t> &status,
+                           DBuf<int32_t> &pivorig, DBuf<float> &Dk, DBuf<float> &Lorig, DBuf<unsigned long long> *dbg) {
+    cudaStream_t st = ctx->stream;
+    if (dbg) {
+        unsigned long long hd[8];
+        HF_CUDA(cudaMemcpy(hd, dbg->p, sizeof(hd), cudaMemcpyDeviceToHost));
+        const double np = hd[4] ? (double)hd[4] : 1.0;
+        fprintf(stderr, "[hf chain] steps %llu  us/step: publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
+                hd[4], hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
+        if (hd[7])
+            fprintf(stderr, "[hf chain] pivot = previous step's runner-up candidate: %.1f %%, runner-up or third: %.1f %%\n",
+                    100.0 * hd[5] / hd[7], 100.0 * hd[6] / hd[7]);
+    }
+    lowprec_outputs(ctx, L, o, lf, status.p, pivorig.p, Dk.p);
+    const int64_t N = lf->N;
     if (N > 0) {
         ClassTimer tm(ctx, "other");
         k_gather_L<<<(unsigned)std::min<int64_t>(N, 65535), 256, 0, st>>>(N, pivorig.p, Lorig.p, L, lf->Lfac.p, N);
         HF_CHECK_LAUNCH(ctx);
     }
-    // host vectors used by the copies above must outlive them
     HF_CUDA(cudaStreamSynchronize(st));
 }
 

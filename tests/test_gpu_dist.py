@@ -84,12 +84,15 @@ def test_nccl_path_one_rank():
 
 
 @pytest.mark.parametrize("name,seed,G,nb", [("P512", 0, 1, 0), ("P512", 2, 3, 0), ("P2048", 0, 2, 0),
-                                            ("P2048", 1, 5, 64), ("N32", 0, 4, 0), ("S24", 0, 3, 128),
-                                            ("C1", 0, 8, 0)])
-def test_stage1_partitions_bitwise(ctx, name, seed, G, nb):
-    """The column-partitioned stage 1 of the multi-GPU path (every partition's FULL
-    columns, replicated pivot chain reading the pivot column from its owner), all G
-    partitions emulated on this GPU: Pi, D and L bit-identical to the oracle [R8]."""
+                                            ("P2048", 1, 5, 64), ("P2048", 2, 8, 0), ("N32", 0, 4, 0),
+                                            ("S24", 0, 3, 128), ("S24", 1, 6, 32), ("C1", 0, 8, 0),
+                                            ("C1", 0, 7, 96), ("P1024", 0, 4, 16), ("C0", 1, 2, 8)])
+def test_stage1_distributed_bitwise(ctx, name, seed, G, nb):
+    """The distributed stage 1 of the multi-GPU path (k_dist.cu: lower-triangle
+    1D block-cyclic ownership, chain rows split over the ranks, per-pivot key
+    exchange over every rank's slots, panel gathered from the owners), all G
+    ranks emulated on this GPU in one cooperative chain launch: Pi, Lambda_2, D
+    and L bit-identical to the oracle [R8] for G = 1..8 and several panel widths."""
     from paper_2208_01907_b200 import hf
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
@@ -106,3 +109,25 @@ def test_stage1_partitions_bitwise(ctx, name, seed, G, nb):
     assert lf.N == Fo.N and lf.L - lf.n2_tau_only == Fo.Ntau
     assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
     assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("G", [2, 8])
+def test_stage1_distributed_c2_equals_one_gpu(ctx, G):
+    """C2 at full size (L = 16384, n_min 256): the G-rank emulation of the
+    distributed stage 1 is bit-identical to the one-GPU path (which
+    test_gpu_fullsize.py pins to the whole oracle)."""
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS["C2"]
+    Kb = hi.make_kbar("C2", 0, device="cuda")
+    hf.hf_scale(ctx, Kb)
+    lf1 = hf.hf_factor_lowprec(ctx, Kb, tau=spec.tau, n_min=spec.n_min)
+    p1, D1, L1 = lf1.export()
+    try:
+        hf.hf_set_stage1_partitions(ctx, G)
+        lfG = hf.hf_factor_lowprec(ctx, Kb, tau=spec.tau, n_min=spec.n_min)
+    finally:
+        hf.hf_set_stage1_partitions(ctx, 0)
+    pG, DG, LG = lfG.export()
+    assert np.array_equal(p1, pG) and np.array_equal(D1, DG)
+    assert torch.equal(L1, LG)
