@@ -70,45 +70,32 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// system scope: the words cross NVLink on a multi-GPU context
-__device__ __forceinline__ void st_sys_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ float ld_sys_f32(const float *p) {
-    float v;
-    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-    return v;
-}
-
 }  // namespace
 
-// per-rank buffers, reached through a device table (peer mappings on a real run)
+// per-rank buffers, reached through a device table (peer mappings on a real run).
+// [2] arrays are indexed by the parity `cur` of the panel that wrote / reads them.
 struct DRank {
     float *V[2];             // L x ncols, rows = global position, ld = ldp (ping-pong)
-    int32_t *lpos[2];        // local column -> global position (this / next panel)
+    int32_t *lpos[2];        // local column -> global position (by panel parity)
     int32_t *lorig[2];       // local column -> original index
-    int32_t *nloc;           // [2] active local columns (this / next panel)
-    int32_t *cmapL;          // new local column -> old local column
-    float *S;                // own rows' s_i^t at panel-start positions, ld = lds
+    int32_t *nloc;           // [2] active local columns
+    int32_t *cmapL;          // new local column -> old local column (last compaction)
+    float *S[2];             // own rows' s_i^t at the panel's positions, ld = lds
+    float *DG[2];            // own rows' lazy diagonal at the end of the panel (lookahead)
     float *Lorig;            // L_{orig, k} (may alias across emulated ranks)
-    unsigned long long *slots;   // [2][G * Cmax][DSLOT]
+    unsigned long long *slots;   // [2][G * Cmax][DSLOT]  {key, info} pairs
     unsigned long long *mbox;    // [2][Cmax][nbmax + 1]
     float *Dk;               // [L] pivots d_k
     int32_t *pivorig;        // [L] original index of pivot k
-    int32_t *pivpos;         // [nbmax] pivot positions of the panel
-    float *sigma;            // [nbmax] sign of d_t
+    int32_t *pivpos[2];      // [nbmax] pivot positions of the panel
+    float *sigma[2];         // [nbmax] sign of d_t
     int32_t *status;         // [4]: N_tau if stopped, pivots in last panel, stopped, peer timeout
     int32_t *orig[2];        // global position -> original index (identical on every rank)
-    int32_t *map;            // new position -> old position
-    int32_t *tiles;          // [CTmax + 1] tile prefix | [CTmax] first row tile
+    int32_t *map;            // new position -> old position (last compaction)
+    int32_t *tiles;          // [CTmax + 1] tile prefix | [CTmax] first row tile | [1] tile counter
     float *Sc, *Snc;         // the panel in the NEW position space (all rows), ld = ldc
     float *Scol;             // s of own local columns (new local order), ld = ldcol
-    unsigned int *bar;       // cross-rank barrier counter
+    unsigned int *bar;       // [2] cross-rank barrier counters (chain stream, trailing stream)
 };
 
 namespace {
@@ -116,19 +103,52 @@ namespace {
 struct DChainArgs {
     const DRank *rp;
     int G, rank0, Cper, R, cur, nbp, nbmax;
+    int nbq;                 // lookahead: pivots of the previous panel applied here (0: serial)
     int64_t m, K0, ldp, lds, ldl;
     double tau;
     unsigned long long timeout_ns;
+    unsigned long long *dbg;   // optional per-phase time sums of CTA 0 (HF_CHAIN_DEBUG)
 };
+
+template <bool SYS>
+__device__ __forceinline__ void st_x_v2(unsigned long long *p, unsigned long long a, unsigned long long b) {
+    if (SYS) asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    else asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void ld_x_v2(const unsigned long long *p, unsigned long long &a, unsigned long long &b) {
+    if (SYS) asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void st_x(unsigned long long *p, unsigned long long v) {
+    if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ unsigned long long ld_x(const unsigned long long *p) {
+    unsigned long long v;
+    if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // One cooperative launch: CTA b belongs to rank rank0 + b / Cper (its local
 // index lb = b % Cper) and owns local columns [lb R, lb R + R) of that rank.
+// SYS: the exchange words cross NVLink (real ranks, system scope); else the
+// ranks are emulated on this GPU (gpu scope).
+// Lookahead (nbq > 0): the previous panel's trailing update is still running, so
+// the matrix read here is the one at the START of the previous panel (V[cur ^ 1],
+// index spaces of that panel) and its nbq updates of the pivot column are applied
+// here first, one fmaf per pivot in order -- the same operands the trailing update
+// uses (role-symmetric [R8]), so the bits equal the serial schedule's.
+template <bool SYS>
 __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
     extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
-    __shared__ uint32_t redi[32];
+    __shared__ uint32_t redi[32], redl[32];
     __shared__ unsigned long long bkey;
-    __shared__ uint32_t binfo;
+    __shared__ uint32_t binfo, blb;
     __shared__ int bail;
     const int grp = blockIdx.x / a.Cper, lb = blockIdx.x % a.Cper;
     const int h = a.rank0 + grp;
@@ -137,83 +157,125 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
     const int GT = a.G * a.Cper;
     const int gid = h * a.Cper + lb;
     const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
-    const int cur = a.cur;
+    const int cur = a.cur, prv = cur ^ 1;
+    const bool look = a.nbq > 0;
+    const int nbq = a.nbq;
     const int64_t nl = me.nloc[cur];
     const int64_t c0 = (int64_t)lb * a.R;
     const int64_t nown = max((int64_t)0, min((int64_t)a.R, nl - c0));
     const int nb = a.nbp;
     float *sneg = smem;                                          // [nbp][R] -sigma_u s_i^u, own rows
-    float *sp = smem + (((size_t)nb * a.R + 3) & ~(size_t)3);    // [nbp] s_P^u of the pivot row
-    float *sgm = sp + nb;                                        // [nbp] sigma_u
+    float *snp = sneg + (size_t)nb * a.R;                        // [nbq][R] the same, previous panel
+    float *sp = smem + (((size_t)(nb + nbq) * a.R + 3) & ~(size_t)3);   // [nbp] s_P^u of the pivot row
+    float *spp = sp + nb;                                        // [nbq] s_P^u, previous panel
+    float *sgm = spp + nbq;                                      // [nbp] sigma_u
+    __shared__ int32_t pvs[256];                                 // [nbp] pivot positions (nb <= 256)
     const bool has = tid < nown;
     const int64_t c = c0 + tid;                                  // own local column = own row
-    const int64_t i = has ? (int64_t)me.lpos[cur][c] : 0;        // its global position
+    const int64_t i = has ? (int64_t)me.lpos[cur][c] : 0;        // its position (this panel)
     const int32_t oi = has ? me.lorig[cur][c] : 0;
-    const float *Vme = me.V[cur];
-    float dg = has ? Vme[i + c * a.ldp] : 0.f;                   // lazy diagonal
-    const uint32_t myinfo = has ? (((uint32_t)h << 20) | (uint32_t)c) : 0u;
+    const int64_t cr = (has && look) ? (int64_t)me.cmapL[c] : c;            // its column in the V read
+    const int64_t io = (has && look) ? (int64_t)me.lpos[prv][cr] : i;       // its row in the V read
+    const float *Vme = me.V[look ? prv : cur];
+    float dg = 0.f;                                              // lazy diagonal
+    if (has) dg = look ? me.DG[prv][cr] : Vme[io + cr * a.ldp];
+    if (has && look) {
+        const float *Sq = me.S[prv] + io;
+        const float *sq = me.sigma[prv];
+        for (int u = 0; u < nbq; ++u) snp[(size_t)u * a.R + tid] = -sq[u] * Sq[(int64_t)u * a.lds];
+    }
+    const uint32_t myinfo = has ? (((uint32_t)h << 20) | (uint32_t)cr) : 0u;
+    // every pointer the step loop uses, in registers / shared memory (the exchange asm's
+    // memory clobbers would otherwise reload them from the table on the critical path)
+    __shared__ const float *sV[64], *sSp[64];
+    __shared__ const unsigned long long *sMb[64];
+    __shared__ unsigned long long *sSl[64];
+    for (int q = tid; q < a.G; q += nthr) {
+        sV[q] = a.rp[q].V[look ? prv : cur];
+        sSp[q] = a.rp[q].S[prv];
+        sMb[q] = a.rp[q].mbox;
+        sSl[q] = a.rp[q].slots;
+    }
+    float *const Sme = me.S[cur];
+    float *const Lor = me.Lorig;
+    float *const Dk = me.Dk;
+    int32_t *const pvme = me.pivpos[cur];
+    float *const sgme = me.sigma[cur];
+    int32_t *const stat = me.status;
+    const int32_t *const mapme = me.map;
+    unsigned long long *const mbme = me.mbox;
     bool piv = !has;
-    float dprev = a.K0 > 0 ? me.Dk[a.K0 - 1] : 0.f;
+    float dprev = a.K0 > 0 ? Dk[a.K0 - 1] : 0.f;
     bool pend = false;
     float ps = 0.f, pl = 0.f;
     int t = 0;
     bool stopped = false;
     if (tid == 0) bail = 0;
     const unsigned long long deadline = gtime() + a.timeout_ns;
-    unsigned long long *myslots = me.slots;
+    const unsigned long long *myslots = me.slots;
+    const bool dbgon = a.dbg && blockIdx.x == 0 && tid == 0;
+    unsigned long long ph[6] = {0, 0, 0, 0, 0, 0}, tp = dbgon ? gtime() : 0;
+#define PH(q) if (dbgon) { const unsigned long long n_ = gtime(); ph[q] += n_ - tp; tp = n_; }
     for (; t < nb;) {
         const int64_t k = a.K0 + t;
         const uint64_t tag = dtag(k);
         const int par = (int)(k & 1);
-        // ---- A: [R3] local argmax over own active rows, carrying (rank, local column)
+        PH(4)
+        // ---- A: [R3] local argmax over own active rows, carrying (rank, column in the V read)
         uint64_t key = !piv ? dkey(dg, (uint32_t)i) : 0ull;
-        uint32_t kinfo = myinfo;
+        uint32_t kinfo = myinfo, klr = (uint32_t)tid;
 #pragma unroll
         for (int o2 = 16; o2 > 0; o2 >>= 1) {
             const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, key, o2);
             const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, kinfo, o2);
+            const uint32_t ol2 = __shfl_xor_sync(0xffffffffu, klr, o2);
             if (ok2 > key) {
                 key = ok2;
                 kinfo = oi2;
+                klr = ol2;
             }
         }
         if (lane == 0) {
             red[wid] = key;
             redi[wid] = kinfo;
+            redl[wid] = klr;
         }
         __syncthreads();
-        // ---- B: publish the CTA's key to every rank; its candidate's panel values to its mailbox
+        PH(0)
+        // ---- B: publish {key, info | lb} to every rank; the candidate's panel values to the mailbox
         if (wid < 2) {
             uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
             uint32_t vinfo = (lane < nwarp) ? redi[lane] : 0u;
+            uint32_t vlr = (lane < nwarp) ? redl[lane] : 0u;
 #pragma unroll
             for (int o2 = 16; o2 > 0; o2 >>= 1) {
                 const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, v, o2);
                 const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, vinfo, o2);
+                const uint32_t ol2 = __shfl_xor_sync(0xffffffffu, vlr, o2);
                 if (ok2 > v) {
                     v = ok2;
                     vinfo = oi2;
+                    vlr = ol2;
                 }
             }
             if (wid == 0) {
-                for (int q = lane; q < a.G; q += 32) {   // one slot per CTA in every rank's array
-                    unsigned long long *slot = a.rp[q].slots + ((size_t)par * GT + gid) * DSLOT;
-                    st_sys_u64(slot + 1, ((unsigned long long)(v ? vinfo : 0u) << 32) | tag);
-                    st_sys_u64(slot, (v & ~DTAGM) | tag);
-                }
+                const unsigned long long w1 =
+                    ((unsigned long long)(v ? vinfo : 0u) << 32) | ((unsigned long long)lb << 14) | tag;
+                for (int q = lane; q < a.G; q += 32)   // one slot per CTA in every rank's array
+                    st_x_v2<SYS>(sSl[q] + ((size_t)par * GT + gid) * DSLOT, (v & ~DTAGM) | tag, w1);
             } else if (v) {
-                unsigned long long *mb = me.mbox + ((size_t)par * a.Cper + lb) * (a.nbmax + 1);
-                const int lr = (int)((int64_t)(vinfo & 0xFFFFF) - c0);
+                unsigned long long *mb = mbme + ((size_t)par * a.Cper + lb) * (a.nbmax + 1);
                 for (int u = lane; u < t; u += 32)
-                    st_sys_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + lr]) << 32) | tag);
+                    st_x<SYS>(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + vlr]) << 32) | tag);
             }
         }
         // ---- deferred global stores of step t-1 (own rows)
         if (pend) {
-            me.S[i + (int64_t)(t - 1) * a.lds] = ps;
-            me.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            Sme[i + (int64_t)(t - 1) * a.lds] = ps;
+            Lor[(int64_t)oi + (k - 1) * a.ldl] = pl;
             pend = false;
         }
+        PH(1)
         // ---- C: every slot of this step (tags); the max key is the pivot
         if (wid == 0) {
             const unsigned long long *sl = myslots + (size_t)par * GT * DSLOT;
@@ -223,8 +285,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
                 bool ok = true;
                 mx = 0;
                 for (int g = lane; g < GT; g += 32) {
-                    const uint64_t sv = ld_sys_u64(&sl[(size_t)g * DSLOT]);
-                    const uint64_t si = ld_sys_u64(&sl[(size_t)g * DSLOT + 1]);
+                    unsigned long long sv, si;
+                    ld_x_v2<SYS>(&sl[(size_t)g * DSLOT], sv, si);
                     ok &= ((sv & DTAGM) == tag) && ((si & DTAGM) == tag);
                     if (sv > mx) {
                         mx = sv;
@@ -235,7 +297,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
                 if ((++spins & 1023u) == 0 && gtime() > deadline) {
                     if (lane == 0) {
                         bail = 1;
-                        me.status[3] = 1;
+                        stat[3] = 1;
                     }
                     break;
                 }
@@ -252,6 +314,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
             if (lane == 0) {
                 bkey = mx;
                 binfo = (uint32_t)(mi >> 32);
+                blb = (uint32_t)((mi >> 14) & 0x3FFFF);
             }
         }
         __syncthreads();
@@ -265,9 +328,9 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
                                                        : ((double)absd < __dmul_rn(a.tau, fabs((double)dprev))));
         if (stop) {
             if (lb == 0 && tid == 0) {
-                me.status[0] = (int32_t)k;
-                me.status[1] = t;
-                me.status[2] = 1;
+                stat[0] = (int32_t)k;
+                stat[1] = t;
+                stat[2] = 1;
             }
             stopped = true;
             break;
@@ -276,44 +339,69 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
         const uint32_t w = binfo;
         const int hP = (int)(w >> 20);
         const int64_t cP = (int64_t)(w & 0xFFFFF);
-        // ---- D: own rows' panel-start column entries (peer read for rows below P), then
-        //      the pivot row's panel values from the winner's mailbox
+        const int64_t Po = look ? (int64_t)mapme[P] : P;            // the pivot's row in the V read
+        PH(2)
+        // ---- D: own rows' column entries from the matrix read (peer for rows below P), then
+        //      the pivot row's panel values from the winner's mailbox (+ previous panel's)
         float v = 0.f;
         if (!piv && i != P) {
-            if (i > P) v = ld_sys_f32(a.rp[hP].V[cur] + i + cP * a.ldp);   // column P on its owner
-            else v = Vme[P + c * a.ldp];                                  // row P of own column
+            if (io > Po) v = sV[hP][io + cP * a.ldp];                         // column P on its owner
+            else v = Vme[Po + cr * a.ldp];                                    // row P of own column
         }
         {
-            const unsigned long long *mb = a.rp[hP].mbox + ((size_t)par * a.Cper + cP / a.R) * (a.nbmax + 1);
+            const unsigned long long *mb = sMb[hP] + ((size_t)par * a.Cper + blb) * (a.nbmax + 1);
             for (int u = tid; u < t; u += nthr) {
                 uint64_t ww;
                 unsigned spins = 0;
-                do {
-                    ww = ld_sys_u64(&mb[u]);
+                for (;;) {
+                    ww = ld_x<SYS>(&mb[u]);
+                    if ((ww & DTAGM) == tag) break;
                     if ((++spins & 1023u) == 0 && gtime() > deadline) {
                         bail = 1;
-                        me.status[3] = 1;
+                        stat[3] = 1;
                         break;
                     }
-                } while ((ww & DTAGM) != tag);
+                }
                 sp[u] = -sgm[u] * __uint_as_float((uint32_t)(ww >> 32));   // s_P^u (exact sign flip)
             }
-            if (tid == 0) sgm[t] = sg;
+            if (look) {
+                const float *Sp = sSp[hP] + Po;
+                for (int u = tid; u < nbq; u += nthr) spp[u] = Sp[(int64_t)u * a.lds];
+            }
+            if (tid == 0) {
+                sgm[t] = sg;
+                pvs[t] = (int32_t)P;
+            }
         }
         __syncthreads();
         if (bail) return;
+        PH(3)
         // ---- E: column, scaled column, lazy diagonal [R6]-[R8], [R10]
         const float r = __fsqrt_rn(absd);
         if (lb == 0 && tid == 0) {   // every rank records the pivot (identical everywhere)
-            me.Dk[k] = d;
-            me.pivorig[k] = me.orig[cur][P];
-            me.pivpos[t] = (int32_t)P;
-            me.sigma[t] = sg;
+            Dk[k] = d;
+            pvme[t] = (int32_t)P;
+            sgme[t] = sg;
         }
         if (has && i == P) {
             piv = true;
         } else if (!piv) {
             float cc = v;
+            {   // [R8] the previous panel's pivots first (what its trailing update applies), in order
+                const float *sq = snp + tid;
+                int u = 0;
+                for (; u + 8 <= nbq; u += 8) {
+                    float x[8], y[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        x[q] = sq[(size_t)(u + q) * a.R];
+                        y[q] = spp[u + q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) cc = __fmaf_rn(x[q], y[q], cc);
+                }
+                for (; u < nbq; ++u) cc = __fmaf_rn(sq[(size_t)u * a.R], spp[u], cc);
+            }
             const float *sn = sneg + tid;
             int u = 0;
             for (; u + 8 <= t; u += 8) {   // [R8] one fmaf per earlier in-panel pivot, in order
@@ -339,10 +427,19 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
         ++t;
     }
     if (pend) {
-        me.S[i + (int64_t)(t - 1) * a.lds] = ps;
-        me.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+        Sme[i + (int64_t)(t - 1) * a.lds] = ps;
+        Lor[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
     }
-    if (!stopped && lb == 0 && tid == 0) me.status[1] = t;
+    if (dbgon) {
+        for (int q = 0; q < 5; ++q) a.dbg[q] += ph[q];
+        a.dbg[5] += t;
+    }
+#undef PH
+    if (has && !piv) me.DG[cur][c] = dg;   // for the next panel's lookahead
+    if (lb == 0) {   // off the critical path: the pivots' original indices
+        for (int u = tid; u < t; u += nthr) me.pivorig[a.K0 + u] = me.orig[cur][pvs[u]];
+        if (!stopped && tid == 0) me.status[1] = t;
+    }
 }
 
 // --------------------------------------------------------------- per-rank setup
@@ -448,12 +545,13 @@ __global__ void k_dgather(DGatherArgs a) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= a.mp) return;
     const int64_t o = me.map[p];                          // panel-start position of the row
-    const float *src = a.rp[owner_of(me.orig[a.cur][o], a.G)].S;
+    const float *src = a.rp[owner_of(me.orig[a.cur][o], a.G)].S[a.cur];
+    const float *sg = me.sigma[a.cur];
     const int t0 = blockIdx.y * 16, t1 = min(a.nbp, t0 + 16);
     for (int t = t0; t < t1; ++t) {
         const float sv = src[o + (int64_t)t * a.lds];
         me.Sc[(int64_t)t * a.ldc + p] = sv;
-        me.Snc[(int64_t)t * a.ldc + p] = -me.sigma[t] * sv;
+        me.Snc[(int64_t)t * a.ldc + p] = -sg[t] * sv;
     }
 }
 
@@ -485,6 +583,7 @@ __global__ void k_dcols(int nbp, int64_t mp, const float *__restrict__ Sc, int64
                 s += cnt[ct];
             }
             tiles[ctmax] = s;
+            tiles[2 * ctmax + 1] = 0;   // the trailing kernel's tile counter
         }
         return;
     }
@@ -505,7 +604,7 @@ __device__ __forceinline__ void cp_async16_d(void *sdst, const void *gsrc) {
 // inner loop of k_trailing_c; rows above the column's position are not stored.
 struct DTrailArgs {
     int64_t mp;
-    int nbp, ctmax;
+    int nbp, ctmax, reserve;
     const float *Vold;
     float *Vnew;
     int64_t ldp;
@@ -527,11 +626,23 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
     __shared__ int32_t rmap[DTB], cmap[DTB], cpos[DTB];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int nchunk = (a.nbp + DTK - 1) / DTK;
+    if (a.reserve > 0) {   // lookahead: the first `reserve` SMs stay free for the next chain
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if ((int)smid < a.reserve) return;
+    }
+    __shared__ int64_t next;
     const int64_t ntiles = a.tiles[a.ctmax];
     const int64_t nl = a.nloc[a.nxt];
+    int *ctr = const_cast<int *>(a.tiles) + 2 * a.ctmax + 1;
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
-    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    for (;;) {
+        __syncthreads();   // the previous tile's readers of As / Bs / maps / next are done
+        if (tid == 0) next = atomicAdd(ctr, 1);
+        __syncthreads();
+        const int64_t tt = next;
+        if (tt >= ntiles) break;
         int lo = 0, hi = a.ctmax - 1;   // column tile: last ct with tiles[ct] <= tt
         while (lo < hi) {
             const int md = (lo + hi + 1) >> 1;
@@ -555,7 +666,6 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        __syncthreads();   // the previous tile's readers of As / Bs / maps are done
         issue(0);
         issue(1);
         if (tid < DTB) {
@@ -677,15 +787,15 @@ __global__ void k_dgather_L(int64_t N, int G, const DRank *rp, int h, int64_t ld
 
 // cross-rank barrier (real ranks): every rank adds 1 to every rank's counter
 // (release, system scope), then waits until its own counter reaches G * epoch
-__global__ void k_xbar(const DRank *rp, int G, int h, unsigned int epoch, unsigned long long timeout_ns) {
+__global__ void k_xbar(const DRank *rp, int G, int h, int which, unsigned int epoch, unsigned long long timeout_ns) {
     if (threadIdx.x != 0) return;
-    for (int q = 0; q < G; ++q) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(rp[q].bar) : "memory");
+    for (int q = 0; q < G; ++q) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(rp[q].bar + which) : "memory");
     const unsigned long long deadline = gtime() + timeout_ns;
     const unsigned int want = (unsigned int)G * epoch;
     unsigned int v;
     unsigned spins = 0;
     for (;;) {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(rp[h].bar) : "memory");
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(rp[h].bar + which) : "memory");
         if (v >= want) break;
         if ((++spins & 1023u) == 0 && gtime() > deadline) {
             rp[h].status[3] = 1;
@@ -698,14 +808,14 @@ __global__ void k_xbar(const DRank *rp, int G, int h, unsigned int epoch, unsign
 
 // ------------------------------------------------------------------ host driver
 struct DistBufs {
-    DBuf<float> V[2], S, Sc, Snc, Scol, Dk, sigma;
-    DBuf<int32_t> lpos[2], lorig[2], nloc, cmapL, pivorig, pivpos, status, orig[2], map, tiles;
+    DBuf<float> V[2], S[2], DG[2], sigma[2], Sc, Snc, Scol, Dk;
+    DBuf<int32_t> lpos[2], lorig[2], pivpos[2], orig[2], nloc, cmapL, pivorig, status, map, tiles;
     DBuf<unsigned long long> slots, mbox;
     DBuf<unsigned int> bar;
 };
 
 // trailing: one FMA per lower-triangle entry per pivot (the same algorithmic count as
-// one GPU: every pair is stored on exactly one rank); chain as in k_lowprec.cu
+// one GPU: every pair is stored on exactly one rank)
 static double dtrail_flops_total(int64_t mp, int nbp) { return (double)mp * (double)(mp + 1) * nbp; }
 // "<cls>@<rank>": per-rank kernel classes of the emulation (tools/dist_model.py)
 static const char *rank_class(const char *cls, int h) {
@@ -737,29 +847,37 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     for (int64_t j = 0; j < L; ++j) ncols[(j / DCB) % G]++;
     int64_t ncmax = 1;
     for (auto c : ncols) ncmax = std::max(ncmax, c);
+    // lookahead (the chain of panel p+1 runs while panel p's trailing update runs on a
+    // second stream, on the SMs the chain leaves free): default on real ranks; the
+    // emulation runs it for the bitwise tests (HF_DIST_LOOKAHEAD=0/1 overrides)
+    bool look = real;
+    if (const char *e = getenv("HF_DIST_LOOKAHEAD")) look = atoi(e) != 0;
 
     // chain geometry: Cper CTAs per rank, R rows each, the panel's values of own rows in
-    // shared memory (R x nb floats); emulated ranks share this GPU's SMs (one CTA per SM)
+    // shared memory (R x nb floats, twice with lookahead); about one GPU's worth of slots
+    // in total (G x Cper ~ #SMs) -- the same per-rank geometry for real and emulated ranks,
+    // so the emulation measures the real per-rank chain up to the NVLink latency
     int maxsmem = 0;
     HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_d));
-    maxsmem -= (int)fa.sharedSizeBytes + 64;
+    cudaFuncAttributes fa, fb;
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_d<false>));
+    HF_CUDA(cudaFuncGetAttributes(&fb, k_chain_d<true>));
+    maxsmem -= (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes) + 64;
     const int cmax_sm = real ? nsm : std::max(1, nsm / G);
-    int cper_def = (int)std::min<int64_t>(cmax_sm, std::max<int64_t>(1, cdiv(ncmax, 128)));
+    int cper_def = (int)std::min<int64_t>(std::max(1, nsm / G), std::max<int64_t>(1, cdiv(ncmax, 128)));
     if (const char *e = getenv("HF_DIST_CTAS")) cper_def = std::max(1, std::min(cmax_sm, atoi(e)));
     int Cmax = std::max(cper_def, (int)std::min<int64_t>(cmax_sm, cdiv(ncmax, 1024)));
     int64_t R0 = cdiv(ncmax, Cmax);
+    const int nf = look ? 2 : 1;
+    auto fits = [&](int nbx, int64_t R) { return (int64_t)(nf * nbx * R + 4 * nbx + 16) * 4 <= (int64_t)maxsmem; };
     int nb = o.nb > 0 ? o.nb : 128;
-    while (nb > 16 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem) nb -= 16;
-    while (nb > 8 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem) nb /= 2;
-    // more CTAs if the panel does not fit even at nb = 8
-    while ((int64_t)(nb * R0 + 3 * nb + 8) * 4 > (int64_t)maxsmem && Cmax < cmax_sm) {
+    while (nb > 16 && !fits(nb, R0)) nb -= 16;
+    while (nb > 8 && !fits(nb, R0)) nb /= 2;
+    while (!fits(nb, R0) && Cmax < cmax_sm) {   // more CTAs if the panel does not fit even at nb = 8
         ++Cmax;
         R0 = cdiv(ncmax, Cmax);
     }
-    HF_REQUIRE(R0 <= 1024 && (int64_t)(nb * R0 + 3 * nb + 8) * 4 <= (int64_t)maxsmem,
-               "stage 1 (distributed): a rank's rows do not fit its chain CTAs");
+    HF_REQUIRE(R0 <= 1024 && fits(nb, R0), "stage 1 (distributed): a rank's rows do not fit its chain CTAs");
     const int64_t ldp = L, lds = L, ldl = L;
     const int64_t ldc = cdiv(L, DTB) * DTB;
     const int64_t ldcol = cdiv(ncmax, DTB) * DTB;
@@ -768,66 +886,57 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     const int nbpad = (int)cdiv(nb, DTK) * DTK;
 
     std::vector<DistBufs> B(G);
-    DBuf<float> Lorig_shared;
+    DBuf<float> Lorig_all;
     std::vector<DRank> tab(G);
     std::memset(tab.data(), 0, sizeof(DRank) * G);
     for (int h = lo; h < hi; ++h) {
         DistBufs &b = B[h];
         const int64_t nc = std::max<int64_t>(ncols[h], 1);
+        DRank &r = tab[h];
         for (int q = 0; q < 2; ++q) {
             b.V[q].alloc((size_t)L * nc, st);
             b.lpos[q].alloc(nc, st);
             b.lorig[q].alloc(nc, st);
             b.orig[q].alloc(L, st);
+            b.S[q].alloc((size_t)L * nb, st);
+            b.DG[q].alloc(nc, st);
+            b.sigma[q].alloc(nb, st);
+            b.pivpos[q].alloc(nb, st);
+            r.V[q] = b.V[q].p; r.lpos[q] = b.lpos[q].p; r.lorig[q] = b.lorig[q].p; r.orig[q] = b.orig[q].p;
+            r.S[q] = b.S[q].p; r.DG[q] = b.DG[q].p; r.sigma[q] = b.sigma[q].p; r.pivpos[q] = b.pivpos[q].p;
         }
-        b.S.alloc((size_t)L * nb, st);
         b.Sc.alloc((size_t)ldc * nbpad, st);
         b.Snc.alloc((size_t)ldc * nbpad, st);
         b.Scol.alloc((size_t)ldcol * nbpad, st);
         b.Dk.alloc(L, st);
-        b.sigma.alloc(nb, st);
         b.nloc.alloc(2, st);
         b.cmapL.alloc(nc, st);
         b.pivorig.alloc(L, st);
-        b.pivpos.alloc(nb, st);
         b.status.alloc(4, st);
         b.status.zero(st);
         b.map.alloc(L, st);
-        b.tiles.alloc((size_t)2 * ctmax + 1, st);
+        b.tiles.alloc((size_t)2 * ctmax + 2, st);
         b.slots.alloc((size_t)2 * G * Cmax * DSLOT, st);
         b.slots.zero(st);
         b.mbox.alloc((size_t)2 * Cmax * (nb + 1), st);
         b.mbox.zero(st);
-        b.bar.alloc(1, st);
+        b.bar.alloc(2, st);
         b.bar.zero(st);
-        DRank &r = tab[h];
-        for (int q = 0; q < 2; ++q) {
-            r.V[q] = b.V[q].p;
-            r.lpos[q] = b.lpos[q].p;
-            r.lorig[q] = b.lorig[q].p;
-            r.orig[q] = b.orig[q].p;
-        }
-        r.nloc = b.nloc.p; r.cmapL = b.cmapL.p; r.S = b.S.p; r.slots = b.slots.p; r.mbox = b.mbox.p;
-        r.Dk = b.Dk.p; r.pivorig = b.pivorig.p; r.pivpos = b.pivpos.p; r.sigma = b.sigma.p; r.status = b.status.p;
+        r.nloc = b.nloc.p; r.cmapL = b.cmapL.p; r.slots = b.slots.p; r.mbox = b.mbox.p;
+        r.Dk = b.Dk.p; r.pivorig = b.pivorig.p; r.status = b.status.p;
         r.map = b.map.p; r.tiles = b.tiles.p; r.Sc = b.Sc.p; r.Snc = b.Snc.p; r.Scol = b.Scol.p; r.bar = b.bar.p;
     }
     // the factor rows by original index: one per rank on a real run, shared when emulated
-    DBuf<float> Lorig_mine;
-    if (real) {
-        Lorig_mine.alloc((size_t)L * L, st);
-        tab[ctx->rank].Lorig = Lorig_mine.p;
-    } else {
-        Lorig_shared.alloc((size_t)L * L, st);
-        for (int h = 0; h < G; ++h) tab[h].Lorig = Lorig_shared.p;
-    }
+    Lorig_all.alloc((size_t)L * L, st);
+    for (int h = lo; h < hi; ++h) tab[h].Lorig = Lorig_all.p;
     std::vector<void *> opened;
 #ifdef HF_WITH_NCCL
     if (real) {
-        // peers' V (both buffers), S, slots, mbox, Lorig, barrier counter: CUDA-IPC handles
-        // all-gathered over NCCL, opened with peer access (NVLink)
-        constexpr int NH = 7;
-        void *mine[NH] = {tab[ctx->rank].V[0], tab[ctx->rank].V[1], tab[ctx->rank].S, tab[ctx->rank].slots,
-                          tab[ctx->rank].mbox, tab[ctx->rank].Lorig, tab[ctx->rank].bar};
+        // peers' V and S (both buffers), slots, mbox, Lorig, barrier counters: CUDA-IPC
+        // handles all-gathered over NCCL, opened with peer access (NVLink)
+        constexpr int NH = 8;
+        const DRank &m0 = tab[ctx->rank];
+        void *mine[NH] = {m0.V[0], m0.V[1], m0.S[0], m0.S[1], m0.slots, m0.mbox, m0.Lorig, m0.bar};
         std::vector<cudaIpcMemHandle_t> hm(NH);
         for (int q = 0; q < NH; ++q) HF_CUDA(cudaIpcGetMemHandle(&hm[q], mine[q]));
         const size_t hb = NH * sizeof(cudaIpcMemHandle_t);
@@ -845,9 +954,10 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
                 HF_CUDA(cudaIpcOpenMemHandle(&pp[q], all[(size_t)g * NH + q], cudaIpcMemLazyEnablePeerAccess));
                 opened.push_back(pp[q]);
             }
-            tab[g].V[0] = (float *)pp[0]; tab[g].V[1] = (float *)pp[1]; tab[g].S = (float *)pp[2];
-            tab[g].slots = (unsigned long long *)pp[3]; tab[g].mbox = (unsigned long long *)pp[4];
-            tab[g].Lorig = (float *)pp[5]; tab[g].bar = (unsigned int *)pp[6];
+            tab[g].V[0] = (float *)pp[0]; tab[g].V[1] = (float *)pp[1];
+            tab[g].S[0] = (float *)pp[2]; tab[g].S[1] = (float *)pp[3];
+            tab[g].slots = (unsigned long long *)pp[4]; tab[g].mbox = (unsigned long long *)pp[5];
+            tab[g].Lorig = (float *)pp[6]; tab[g].bar = (unsigned int *)pp[7];
         }
     }
 #else
@@ -857,12 +967,31 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     dtab.alloc(G, st);
     HF_CUDA(cudaMemcpyAsync(dtab.p, tab.data(), sizeof(DRank) * G, cudaMemcpyHostToDevice, st));
     const unsigned long long timeout_ns = 60ull * 1000000000ull;
-    unsigned int bar_epoch = 0;
-    auto xbar = [&]() {   // real ranks only: stream-ordered device barrier over NVLink
+    cudaStream_t st2 = st;
+    if (look) {
+        if (!ctx->side) {
+            HF_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            for (auto &e : ctx->ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        st2 = ctx->side;
+    }
+    unsigned int bar_epoch[2] = {0, 0};
+    auto xbar = [&](cudaStream_t s, int which) {   // real ranks only: stream-ordered device barrier
         if (!real) return;
-        ++bar_epoch;
-        k_xbar<<<1, 32, 0, st>>>(dtab.p, G, ctx->rank, bar_epoch, timeout_ns);
+        ++bar_epoch[which];
+        k_xbar<<<1, 32, 0, s>>>(dtab.p, G, ctx->rank, which, bar_epoch[which], timeout_ns);
         HF_CHECK_LAUNCH(ctx);
+    };
+    // per-panel device times of the emulation (HF_DIST_PANEL_TIMES: tools/dist_model.py)
+    const bool ptimes = !real && getenv("HF_DIST_PANEL_TIMES") != nullptr;
+    std::vector<cudaEvent_t> pev;
+    std::vector<int> pkind;   // 0: a chain (2 events), 1: one rank's gather + trailing (3 events)
+    auto pevent = [&](cudaStream_t s) {
+        if (!ptimes) return;
+        cudaEvent_t e;
+        HF_CUDA(cudaEventCreate(&e));
+        HF_CUDA(cudaEventRecord(e, s));
+        pev.push_back(e);
     };
 
     {
@@ -879,76 +1008,149 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         }
         HF_CUDA(cudaStreamSynchronize(st));   // nl0 dies here
     }
-    xbar();   // every rank's columns are cast before anyone reads them
-    HF_CUDA(cudaFuncSetAttribute(k_chain_d, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    xbar(st, 0);   // every rank's columns are cast before anyone reads them
+    for (void *kf : {(void *)k_chain_d<false>, (void *)k_chain_d<true>})
+        HF_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DTRAIL_SMEM));
     int tocc = 0;
     HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, k_trailing_d, 256, DTRAIL_SMEM));
     const int tgrid = std::max(1, tocc) * nsm;
+    if (look) {
+        HF_CUDA(cudaEventRecord(ctx->ev[0], st));   // the side stream starts after the setup
+        HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[0], 0));
+    }
 
-    int cur = 0;
+    const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
+    DBuf<unsigned long long> dbgbuf;
+    if (want_dbg) {
+        dbgbuf.alloc(8, st);
+        dbgbuf.zero(st);
+    }
+    int cur = 0, nbprev = 0;
     int64_t m = L, K0 = 0;
+    bool loc_pending = false;   // lookahead: a compaction on st2 the next chain must wait for
     while (m > 0) {
         const int nbp = (int)std::min<int64_t>(nb, m);
+        const int nbq = (look && K0 > 0) ? nbprev : 0;
         // rows per rank are at most min(ncols, m): fewer chain CTAs as the matrix shrinks
         const int64_t rows_hi = std::min<int64_t>(ncmax, m);
         const int Cper = (int)std::max<int64_t>(1, std::min<int64_t>(Cmax, cdiv(rows_hi, R0)));
         const int nthr = (int)std::max<int64_t>(64, cdiv(R0, 32) * 32);
-        const size_t shm = ((size_t)nbp * R0 + 3 * nbp + 8) * sizeof(float);
+        const size_t shm = ((size_t)(nbp + nbq) * R0 + 4 + 3 * (size_t)nbp + nbq + 8) * sizeof(float);
         DChainArgs ca;
         ca.rp = dtab.p; ca.G = G; ca.rank0 = lo; ca.Cper = Cper; ca.R = (int)R0; ca.cur = cur; ca.nbp = nbp;
-        ca.nbmax = nb; ca.m = m; ca.K0 = K0; ca.ldp = ldp; ca.lds = lds; ca.ldl = ldl; ca.tau = o.tau;
+        ca.nbmax = nb; ca.nbq = nbq; ca.m = m; ca.K0 = K0; ca.ldp = ldp; ca.lds = lds; ca.ldl = ldl; ca.tau = o.tau;
         ca.timeout_ns = timeout_ns;
+        ca.dbg = want_dbg ? dbgbuf.p : nullptr;
+        if (loc_pending) {   // the previous panel's compaction (and the trailing update before it)
+            HF_CUDA(cudaStreamWaitEvent(st, ctx->ev[1], 0));
+            loc_pending = false;
+        }
+        if (ptimes) pkind.push_back(0);
+        pevent(st);
         {
             double cf = 0.0;
-            for (int t = 0; t < nbp; ++t) cf += 2.0 * (double)(m - t) * t;
+            for (int t = 0; t < nbp; ++t) cf += 2.0 * (double)(m - t) * (t + nbq);
             ClassTimer tm(ctx, "chain", st, cf, 16.0 * ((double)m * nbp - 0.5 * (double)nbp * (nbp - 1)));
             void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain_d, dim3((unsigned)((hi - lo) * Cper)), dim3(nthr), args,
-                                                shm, st));
+            void *kf = real ? (void *)k_chain_d<true> : (void *)k_chain_d<false>;
+            HF_CUDA(cudaLaunchCooperativeKernel(kf, dim3((unsigned)((hi - lo) * Cper)), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }
-        xbar();   // every rank's S of this panel is written before it is gathered
+        pevent(st);
+        xbar(st, 0);   // every rank's S of this panel is written before it is gathered
         const int64_t mp = m - nbp;
         if (mp > 0) {
+            if (look) {   // the side stream waits for this chain
+                HF_CUDA(cudaEventRecord(ctx->ev[2], st));
+                HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[2], 0));
+            }
+            for (int h = lo; h < hi; ++h) {   // compaction of this panel (global and own columns)
+                DistBufs &b = B[h];
+                ClassTimer tm(ctx, "other", st2);
+                ClassTimer tr(ctx, rank_class("gather", h), st2);
+                k_dcompact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st2>>>(
+                    m, nbp, b.pivpos[cur].p, b.orig[cur].p, b.map.p, b.orig[cur ^ 1].p, b.status.p);
+                HF_CHECK_LAUNCH(ctx);
+                k_dlocal<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ncols[h], 256), 1024)), 256, 0, st2>>>(
+                    h, G, nbp, b.pivpos[cur].p, b.orig[cur].p, b.lpos[cur].p, b.lorig[cur].p, b.lpos[cur ^ 1].p,
+                    b.lorig[cur ^ 1].p, b.cmapL.p, b.nloc.p, cur, b.status.p);
+                HF_CHECK_LAUNCH(ctx);
+            }
+            if (look) {   // the next chain waits for this compaction (and what precedes it on st2)
+                HF_CUDA(cudaEventRecord(ctx->ev[1], st2));
+                loc_pending = true;
+            }
             for (int h = lo; h < hi; ++h) {
                 DistBufs &b = B[h];
+                if (ptimes) pkind.push_back(1);
+                pevent(st2);
                 {
-                    ClassTimer tm(ctx, "other");
-                    ClassTimer tr(ctx, rank_class("gather", h), st);
-                    k_dcompact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
-                        m, nbp, b.pivpos.p, b.orig[cur].p, b.map.p, b.orig[cur ^ 1].p, b.status.p);
-                    HF_CHECK_LAUNCH(ctx);
-                    k_dlocal<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ncols[h], 256), 1024)), 256, 0, st>>>(
-                        h, G, nbp, b.pivpos.p, b.orig[cur].p, b.lpos[cur].p, b.lorig[cur].p, b.lpos[cur ^ 1].p,
-                        b.lorig[cur ^ 1].p, b.cmapL.p, b.nloc.p, cur, b.status.p);
-                    HF_CHECK_LAUNCH(ctx);
+                    ClassTimer tm(ctx, "other", st2);
+                    ClassTimer tr(ctx, rank_class("gather", h), st2);
                     DGatherArgs ga;
                     ga.rp = dtab.p; ga.h = h; ga.G = G; ga.nbp = nbp; ga.cur = cur; ga.mp = mp; ga.lds = lds; ga.ldc = ldc;
-                    k_dgather<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st>>>(ga);
+                    k_dgather<<<dim3((unsigned)cdiv(mp, 256), (unsigned)cdiv(nbp, 16)), 256, 0, st2>>>(ga);
                     HF_CHECK_LAUNCH(ctx);
-                    k_dcols<<<(unsigned)(1 + cdiv(ldcol, 256)), 256, 0, st>>>(nbp, mp, b.Sc.p, ldc, b.lpos[cur ^ 1].p,
-                                                                            b.nloc.p, cur ^ 1, b.Scol.p, ldcol,
-                                                                            b.tiles.p, ctmax, b.status.p);
+                    k_dcols<<<(unsigned)(1 + cdiv(ldcol, 256)), 256, 0, st2>>>(nbp, mp, b.Sc.p, ldc, b.lpos[cur ^ 1].p,
+                                                                             b.nloc.p, cur ^ 1, b.Scol.p, ldcol,
+                                                                             b.tiles.p, ctmax, b.status.p);
                     HF_CHECK_LAUNCH(ctx);
                 }
+                pevent(st2);
                 DTrailArgs ta;
                 ta.mp = mp; ta.nbp = nbp; ta.ctmax = ctmax; ta.Vold = b.V[cur].p; ta.Vnew = b.V[cur ^ 1].p;
                 ta.ldp = ldp; ta.map = b.map.p; ta.cmapL = b.cmapL.p; ta.nlpos = b.lpos[cur ^ 1].p; ta.nloc = b.nloc.p;
                 ta.nxt = cur ^ 1; ta.tiles = b.tiles.p; ta.Snc = b.Snc.p; ta.Scol = b.Scol.p; ta.ldc = ldc;
                 ta.ldcol = ldcol; ta.status = b.status.p;
-                // this rank's share of the algorithmic update (exact per rank is device-side;
-                // the total over the ranks equals one GPU's)
-                ClassTimer tm(ctx, "trailing", st, dtrail_flops_total(mp, nbp) / G, 0.0);
-                ClassTimer tr(ctx, rank_class("trailing", h), st);   // per rank (the time model)
-                k_trailing_d<<<(unsigned)tgrid, 256, DTRAIL_SMEM, st>>>(ta);
+                // real ranks with lookahead: leave the chain's SMs free (the next chain
+                // launches while this update runs); the emulation's chain spans every SM
+                ta.reserve = (look && real) ? Cmax : 0;
+                ClassTimer tm(ctx, "trailing", st2, dtrail_flops_total(mp, nbp) / G, 0.0);
+                ClassTimer tr(ctx, rank_class("trailing", h), st2);   // per rank (the time model)
+                k_trailing_d<<<(unsigned)tgrid, 256, DTRAIL_SMEM, st2>>>(ta);
                 HF_CHECK_LAUNCH(ctx);
+                pevent(st2);
             }
-            xbar();   // every rank's columns of the next panel are updated before the next chain
+            xbar(st2, 1);   // every rank's columns of the next-but-one chain's matrix are updated
             cur ^= 1;
         }
+        nbprev = nbp;
         K0 += nbp;
         m = mp;
+    }
+    if (look) {   // join the side stream
+        HF_CUDA(cudaEventRecord(ctx->ev[3], st2));
+        HF_CUDA(cudaStreamWaitEvent(st, ctx->ev[3], 0));
+    }
+    if (ptimes) {   // per panel: chain ms; per rank: gather ms and trailing ms
+        HF_CUDA(cudaStreamSynchronize(st));
+        std::string line = "[";
+        size_t q = 0;
+        for (size_t pi = 0; pi < pkind.size(); ++pi) {
+            if (pkind[pi] == 0) {   // chain start / end
+                float ch = 0.f;
+                cudaEventElapsedTime(&ch, pev[q], pev[q + 1]);
+                line += std::string(pi ? "]},{" : "{") + "\"chain\":" + std::to_string(ch) + ",\"ranks\":[";
+                q += 2;
+            } else {                // gather start / trailing start / trailing end of one rank
+                float g = 0.f, t = 0.f;
+                cudaEventElapsedTime(&g, pev[q], pev[q + 1]);
+                cudaEventElapsedTime(&t, pev[q + 1], pev[q + 2]);
+                line += std::string(pkind[pi - 1] == 0 ? "" : ",") + "[" + std::to_string(g) + "," + std::to_string(t) + "]";
+                q += 3;
+            }
+        }
+        line += pkind.empty() ? "]" : "]}]";
+        fprintf(stderr, "[hf dist panels] %s\n", line.c_str());
+        for (auto e : pev) cudaEventDestroy(e);
+    }
+    if (want_dbg) {
+        unsigned long long hd[8];
+        HF_CUDA(cudaMemcpy(hd, dbgbuf.p, sizeof(hd), cudaMemcpyDeviceToHost));
+        const double np = hd[5] ? (double)hd[5] : 1.0;
+        fprintf(stderr, "[hf dchain] steps %llu  us/step: argmax %.3f  publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
+                hd[5], hd[4] / np * 1e-3, hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
     }
     // outputs: every rank holds the pivots, D and the status; the factor rows come
     // from their owners
@@ -960,7 +1162,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
                                                                               lf->N);
         HF_CHECK_LAUNCH(ctx);
     }
-    xbar();   // nobody reads a peer's buffers any more
+    xbar(st, 0);   // nobody reads a peer's buffers any more
     HF_CUDA(cudaStreamSynchronize(st));
     int32_t hs[4];
     HF_CUDA(cudaMemcpy(hs, B[me].status.p, sizeof(hs), cudaMemcpyDeviceToHost));

@@ -87,13 +87,18 @@ def test_nccl_path_one_rank():
                                             ("P2048", 1, 5, 64), ("P2048", 2, 8, 0), ("N32", 0, 4, 0),
                                             ("S24", 0, 3, 128), ("S24", 1, 6, 32), ("C1", 0, 8, 0),
                                             ("C1", 0, 7, 96), ("P1024", 0, 4, 16), ("C0", 1, 2, 8)])
-def test_stage1_distributed_bitwise(ctx, name, seed, G, nb):
+@pytest.mark.parametrize("look", [0, 1])
+def test_stage1_distributed_bitwise(ctx, name, seed, G, nb, look, monkeypatch):
     """The distributed stage 1 of the multi-GPU path (k_dist.cu: lower-triangle
     1D block-cyclic ownership, chain rows split over the ranks, per-pivot key
     exchange over every rank's slots, panel gathered from the owners), all G
     ranks emulated on this GPU in one cooperative chain launch: Pi, Lambda_2, D
-    and L bit-identical to the oracle [R8] for G = 1..8 and several panel widths."""
+    and L bit-identical to the oracle [R8] for G = 1..8 and several panel widths,
+    with the serial schedule and with the lookahead one (the chain of panel p+1
+    reads the matrix at the start of panel p and applies panel p's updates itself
+    while panel p's trailing update runs on a second stream)."""
     from paper_2208_01907_b200 import hf
+    monkeypatch.setenv("HF_DIST_LOOKAHEAD", str(look))
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
     Ko, _ = oracle.scale(Kb.numpy())
@@ -112,12 +117,13 @@ def test_stage1_distributed_bitwise(ctx, name, seed, G, nb):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("G", [2, 8])
-def test_stage1_distributed_c2_equals_one_gpu(ctx, G):
+@pytest.mark.parametrize("G,look", [(2, 0), (8, 0), (8, 1)])
+def test_stage1_distributed_c2_equals_one_gpu(ctx, G, look, monkeypatch):
     """C2 at full size (L = 16384, n_min 256): the G-rank emulation of the
     distributed stage 1 is bit-identical to the one-GPU path (which
     test_gpu_fullsize.py pins to the whole oracle)."""
     from paper_2208_01907_b200 import hf
+    monkeypatch.setenv("HF_DIST_LOOKAHEAD", str(look))
     spec = hi.CONFIGS["C2"]
     Kb = hi.make_kbar("C2", 0, device="cuda")
     hf.hf_scale(ctx, Kb)
