@@ -343,11 +343,12 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
         PH(2)
         // ---- D: own rows' column entries from the matrix read (peer for rows below P), then
         //      the pivot row's panel values from the winner's mailbox (+ previous panel's)
-        float v = 0.f;
-        if (!piv && i != P) {
-            if (io > Po) v = sV[hP][io + cP * a.ldp];                         // column P on its owner
-            else v = Vme[Po + cr * a.ldp];                                    // row P of own column
-        }
+        // one unconditional global load (the address selected first), issued before the
+        // mailbox poll so the two latencies overlap (threads without an entry read Vme[0])
+        const float *vp = (io > Po) ? (sV[hP] + io + cP * a.ldp)    // column P on its owner
+                                    : (Vme + Po + cr * a.ldp);     // row P of own column
+        const bool want = !piv && i != P;
+        const float v = __ldcg(want ? vp : Vme);   // consumed only after the barrier (phase E)
         {
             const unsigned long long *mb = sMb[hP] + ((size_t)par * a.Cper + blb) * (a.nbmax + 1);
             for (int u = tid; u < t; u += nthr) {
@@ -850,8 +851,12 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     // lookahead (the chain of panel p+1 runs while panel p's trailing update runs on a
     // second stream, on the SMs the chain leaves free): default on real ranks; the
     // emulation runs it for the bitwise tests (HF_DIST_LOOKAHEAD=0/1 overrides)
+    // (=2: the lookahead chain with everything on one stream -- the time model's
+    // measurement of the lookahead chain's own cost, no concurrency)
     bool look = real;
-    if (const char *e = getenv("HF_DIST_LOOKAHEAD")) look = atoi(e) != 0;
+    int look_mode = real ? 1 : 0;
+    if (const char *e = getenv("HF_DIST_LOOKAHEAD")) look_mode = atoi(e);
+    look = look_mode != 0;
 
     // chain geometry: Cper CTAs per rank, R rows each, the panel's values of own rows in
     // shared memory (R x nb floats, twice with lookahead); about one GPU's worth of slots
@@ -968,7 +973,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     HF_CUDA(cudaMemcpyAsync(dtab.p, tab.data(), sizeof(DRank) * G, cudaMemcpyHostToDevice, st));
     const unsigned long long timeout_ns = 60ull * 1000000000ull;
     cudaStream_t st2 = st;
-    if (look) {
+    if (look && look_mode != 2) {
         if (!ctx->side) {
             HF_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
             for (auto &e : ctx->ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1015,7 +1020,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     int tocc = 0;
     HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, k_trailing_d, 256, DTRAIL_SMEM));
     const int tgrid = std::max(1, tocc) * nsm;
-    if (look) {
+    if (st2 != st) {
         HF_CUDA(cudaEventRecord(ctx->ev[0], st));   // the side stream starts after the setup
         HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[0], 0));
     }
@@ -1061,7 +1066,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         xbar(st, 0);   // every rank's S of this panel is written before it is gathered
         const int64_t mp = m - nbp;
         if (mp > 0) {
-            if (look) {   // the side stream waits for this chain
+            if (st2 != st) {   // the side stream waits for this chain
                 HF_CUDA(cudaEventRecord(ctx->ev[2], st));
                 HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[2], 0));
             }
@@ -1077,7 +1082,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
                     b.lorig[cur ^ 1].p, b.cmapL.p, b.nloc.p, cur, b.status.p);
                 HF_CHECK_LAUNCH(ctx);
             }
-            if (look) {   // the next chain waits for this compaction (and what precedes it on st2)
+            if (st2 != st) {   // the next chain waits for this compaction (and what precedes it on st2)
                 HF_CUDA(cudaEventRecord(ctx->ev[1], st2));
                 loc_pending = true;
             }
@@ -1119,7 +1124,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         K0 += nbp;
         m = mp;
     }
-    if (look) {   // join the side stream
+    if (st2 != st) {   // join the side stream
         HF_CUDA(cudaEventRecord(ctx->ev[3], st2));
         HF_CUDA(cudaStreamWaitEvent(st, ctx->ev[3], 0));
     }

@@ -382,12 +382,15 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- F: [R6] pivot row from the winner's mailbox, stale column for own rows
         const int64_t Po = a.mapprev ? (int64_t)a.mapprev[P] : P;   // pivot in V's position space
         // the column load is issued first so its latency overlaps the mailbox poll below
-        float v = 0.f;
+        // (one unconditional load from a selected address, its value used only after the
+        // barrier below: a conditional load merged into a register stalls the thread here)
+        float v;
         if (PARTS) {
             const uint32_t w = pcol;   // read after the barrier that published bkey
-            if (!piv && i != P) v = a.parts[w >> 20][i + (int64_t)(w & 0xFFFFF) * a.ldp];
-        } else if (!piv && i != P) {
-            v = (io >= Po) ? a.V[io + Po * a.ldv] : a.V[Po + io * a.ldv];
+            v = (!piv && i != P) ? a.parts[w >> 20][i + (int64_t)(w & 0xFFFFF) * a.ldp] : 0.f;
+        } else {
+            const float *vp = (io >= Po) ? (a.V + io + Po * a.ldv) : (a.V + Po + io * a.ldv);
+            v = __ldcg((!piv && i != P) ? vp : a.V);
         }
         {
             const int owner = (int)(P / a.R);
