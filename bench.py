@@ -337,11 +337,16 @@ def main():
     gen_dev = "cuda" if spec.L > 4096 else "cpu"
     seed = args.seed + (rank if args.mode == "replicas" else 0)
     Kb = hi.make_kbar(spec, seed, device=gen_dev).to(dev).contiguous()
-    K = torch.empty_like(Kb)
+    # L > 32768 (C4, 34 GB in FP64): no pristine device copy -- every step scales K in
+    # place; after the first, hf_scale sees an already-scaled matrix (Q = I, the same
+    # bits) and does the same reads, multiplications and writes
+    restore = spec.L <= 32768
+    K = torch.empty_like(Kb) if restore else Kb
     torch.cuda.synchronize()
 
     def step(profile=False):
-        K.copy_(Kb)
+        if restore:
+            K.copy_(Kb)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
         hf.hf_scale(ctx, K)
@@ -460,9 +465,11 @@ def main():
                        "tau": spec.tau, "n_min": spec.n_min, "seed": args.seed, "gcr_iters": iters,
                        "kernel_dim": kd, "gcr_true_rel_res": tres,
                        "parallelism": ("single" if world == 1 else
-                                       ("replicas" if args.mode == "replicas" else f"stage2-rhs-shard{world}")),
-                       "l2": "inputs larger than L2 (K fp64 %.2f GB); restore copy of Kbar inside each step" %
-                             (8 * L * L / 1e9)},
+                                       ("replicas" if args.mode == "replicas" else
+                                        f"stage1-dist{world} (lower-triangle 1D block-cyclic) + stage2-rhs-shard{world}")),
+                       "l2": "inputs larger than L2 (K fp64 %.2f GB); %s" %
+                             (8 * L * L / 1e9, "restore copy of Kbar inside each step" if restore else
+                              "K scaled in place every step (idempotent after the first)")},
             "seconds_per_factorization": ms_step / 1e3,
             "stage_ms": {"scale": stage_ms[0] / args.steps, "lowprec": stage_ms[1] / args.steps,
                          "schur_gcr": stage_ms[2] / args.steps, "hard": stage_ms[3] / args.steps},
@@ -474,33 +481,40 @@ def main():
 
     # ---- end to end through the public API with host buffers
     if not args.no_e2e:
-        Kh = Kb.cpu().pin_memory()
-        e2e_steps = max(1, args.steps)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        d2h = 0
-        for _ in range(e2e_steps):
-            K.copy_(Kh, non_blocking=True)
-            hf.hf_scale(ctx, K)
-            lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)
-            hy, info, S22 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True)
-            kd = hf.hf_factor_hard(ctx, hy)
-            perm, D, _ = lf.export(with_L=False)
-            d2h = S22.nbytes if S22 is not None else 0
-            d2h += perm.nbytes + D.nbytes + 8
-            hy.close()
-            lf.close()
-        t1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = t0.elapsed_time(t1) / e2e_steps
-        e_ms = max_over_ranks(e_ms)
-        line["e2e"] = {"value": total_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                       "h2d_bytes_per_step": int(Kh.numel() * 8), "d2h_bytes_per_step": int(d2h),
-                       "ms_per_step": e_ms}
+        try:
+            Kh = (Kb if restore else hi.make_kbar(spec, seed, device=gen_dev)).cpu().pin_memory()
+            e2e_steps = max(1, args.steps) if restore else 1   # C4: 34 GB per rank crosses the host link once
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            d2h = 0
+            for _ in range(e2e_steps):
+                K.copy_(Kh, non_blocking=True)
+                hf.hf_scale(ctx, K)
+                lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)
+                hy, info, S22 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True)
+                kd = hf.hf_factor_hard(ctx, hy)
+                perm, D, _ = lf.export(with_L=False)
+                d2h = S22.nbytes if S22 is not None else 0
+                d2h += perm.nbytes + D.nbytes + 8
+                hy.close()
+                lf.close()
+            t1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = t0.elapsed_time(t1) / e2e_steps
+            e2e_err = None
+        except Exception as e:   # a failed end-to-end leg must not lose the device-timed line
+            e_ms, e2e_err = -1.0, repr(e)[:300]
+        e_ms = max_over_ranks(e_ms)   # every rank takes part, failed or not
+        if e2e_err is None and e_ms > 0:
+            line["e2e"] = {"value": total_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                           "h2d_bytes_per_step": int(Kh.numel() * 8), "d2h_bytes_per_step": int(d2h),
+                           "ms_per_step": e_ms}
+        else:
+            line["e2e"] = {"value": None, "unit": "TFLOP/s", "unavailable": e2e_err or "failed on another rank"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cb_mode = args.cpu_baseline

@@ -53,7 +53,9 @@ __global__ void __launch_bounds__(128) k_dgemm(DgemmBatch gb) {
     const DgemmArgs g = ((int)blockIdx.z >= gb.splits) ? gb.g[1] : gb.g[0];   // no dynamic param indexing
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
-    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    // grid.x = N tiles (fastest): the N tiles of one M tile run side by side, so each A
+    // (= K11) tile comes from DRAM once and from L2 for the other N tiles
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     // K range of this split
     const int64_t kper = ((g.K + nsplit - 1) / nsplit + BK - 1) / BK * BK;
     const int64_t kbeg = (int64_t)zs * kper;
@@ -212,7 +214,8 @@ static void dgemm_launch(hf_ctx *ctx, bool transA, int nprob, const DgemmArgs *g
     const size_t shm = shm0;
     ClassTimer tm(ctx, "dgemm", st, 2.0 * (double)M * (double)N * (double)K * nprob,
                   8.0 * nprob * ((double)M * K + (double)K * N + 2.0 * (double)M * N));
-    dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(splits * nprob));
+    HF_REQUIRE(mt <= 65535, "dgemm: too many row tiles for grid.y");
+    dim3 grid((unsigned)nt, (unsigned)mt, (unsigned)(splits * nprob));
     if (transA) k_dgemm<true><<<grid, 128, shm, st>>>(gb);
     else k_dgemm<false><<<grid, 128, shm, st>>>(gb);
     HF_CHECK_LAUNCH(ctx);

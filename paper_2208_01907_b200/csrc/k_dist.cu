@@ -110,6 +110,25 @@ struct DChainArgs {
     unsigned long long *dbg;   // optional per-phase time sums of CTA 0 (HF_CHAIN_DEBUG)
 };
 
+// c <- fmaf(x_u, y_u, c) for u = 0..n-1 in order [R8]; x_u = xs[u * R] (own row's
+// panel values, shared memory, stride R), y_u = ys[u] (broadcast).  (Issuing the next
+// 8 loads ahead of the current 8 FMAs measured slower: 0.96 vs 0.80 us per C2 pivot.)
+__device__ __forceinline__ float fma_chain(float c, const float *xs, const float *ys, int n, int R) {
+    int u = 0;
+    for (; u + 8 <= n; u += 8) {
+        float x[8], y[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            x[q] = xs[(size_t)(u + q) * R];
+            y[q] = ys[u + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c = __fmaf_rn(x[q], y[q], c);
+    }
+    for (; u < n; ++u) c = __fmaf_rn(xs[(size_t)u * R], ys[u], c);
+    return c;
+}
+
 template <bool SYS>
 __device__ __forceinline__ void st_x_v2(unsigned long long *p, unsigned long long a, unsigned long long b) {
     if (SYS) asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -388,34 +407,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
             piv = true;
         } else if (!piv) {
             float cc = v;
-            {   // [R8] the previous panel's pivots first (what its trailing update applies), in order
-                const float *sq = snp + tid;
-                int u = 0;
-                for (; u + 8 <= nbq; u += 8) {
-                    float x[8], y[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        x[q] = sq[(size_t)(u + q) * a.R];
-                        y[q] = spp[u + q];
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) cc = __fmaf_rn(x[q], y[q], cc);
-                }
-                for (; u < nbq; ++u) cc = __fmaf_rn(sq[(size_t)u * a.R], spp[u], cc);
-            }
-            const float *sn = sneg + tid;
-            int u = 0;
-            for (; u + 8 <= t; u += 8) {   // [R8] one fmaf per earlier in-panel pivot, in order
-                float x[8], y[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    x[q] = sn[(size_t)(u + q) * a.R];
-                    y[q] = sp[u + q];
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) cc = __fmaf_rn(x[q], y[q], cc);
-            }
-            for (; u < t; ++u) cc = __fmaf_rn(sn[(size_t)u * a.R], sp[u], cc);
+            cc = fma_chain(cc, snp + tid, spp, nbq, a.R);   // [R8] the previous panel's pivots first
+            cc = fma_chain(cc, sneg + tid, sp, t, a.R);     // then the earlier in-panel pivots, in order
             const float sv = __fdiv_rn(cc, r);
             const float ns = -sg * sv;
             sneg[(size_t)t * a.R + tid] = ns;
@@ -594,6 +587,9 @@ __global__ void k_dcols(int nbp, int64_t mp, const float *__restrict__ Sc, int64
     for (int t = 0; t < nbp; ++t) Scol[(int64_t)t * ldcol + cn] = pp >= 0 ? Sc[(int64_t)t * ldc + pp] : 0.f;
 }
 
+__device__ __forceinline__ void cp_async16_sd(unsigned sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async16_d(void *sdst, const void *gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
@@ -633,39 +629,52 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
         if ((int)smid < a.reserve) return;
     }
     __shared__ int64_t next;
+    __shared__ int32_t tpre[1025], trt0[1024];   // the tile list (ctmax <= 1024), once per CTA
+    for (int q = threadIdx.x; q <= a.ctmax; q += blockDim.x) tpre[q] = a.tiles[q];
+    for (int q = threadIdx.x; q < a.ctmax; q += blockDim.x) trt0[q] = a.tiles[a.ctmax + 1 + q];
     const int64_t ntiles = a.tiles[a.ctmax];
     const int64_t nl = a.nloc[a.nxt];
     int *ctr = const_cast<int *>(a.tiles) + 2 * a.ctmax + 1;
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
+    // the next tile's index is fetched (atomic) while the current one computes
+    __shared__ int64_t after;
+    if (tid == 0) next = atomicAdd(ctr, 1);
     for (;;) {
-        __syncthreads();   // the previous tile's readers of As / Bs / maps / next are done
-        if (tid == 0) next = atomicAdd(ctr, 1);
-        __syncthreads();
+        __syncthreads();   // the previous tile's readers of As / Bs / maps are done; next is set
         const int64_t tt = next;
         if (tt >= ntiles) break;
+        if (tid == 0) after = atomicAdd(ctr, 1);
         int lo = 0, hi = a.ctmax - 1;   // column tile: last ct with tiles[ct] <= tt
         while (lo < hi) {
             const int md = (lo + hi + 1) >> 1;
-            if (a.tiles[md] <= tt) lo = md;
+            if (tpre[md] <= tt) lo = md;
             else hi = md - 1;
         }
         const int ct = lo;
-        const int64_t rt = a.tiles[a.ctmax + 1 + ct] + (tt - a.tiles[ct]);
+        const int64_t rt = trt0[ct] + (tt - tpre[ct]);
         const int64_t row0 = rt * DTB, col0 = (int64_t)ct * DTB;
         const int mpr = (int)min((int64_t)DTB, a.mp - row0), mpc = (int)min((int64_t)DTB, nl - col0);
+        // source pointers advanced by one chunk per issue, rotating stage (no per-chunk
+        // multiplies on the FMA pipe; see k_trailing_c)
+        const int ek0 = tid >> 5, er0 = (tid & 31) * 4;
+        const float *pa = a.Snc + (int64_t)ek0 * a.ldc + row0 + er0;
+        const float *pb = a.Scol + (int64_t)ek0 * a.ldcol + col0 + er0;
+        const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][ek0][er0]);
+        const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][ek0][er0]);
+        constexpr unsigned STGB = DTK * DTB * sizeof(float), EIGHTB = 8 * DTB * sizeof(float);
+        unsigned soff = 0;
         auto issue = [&](int cq) {
             if (cq < nchunk) {
-                const int st = cq % DTNS;
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int e = tid + u * 256;
-                    const int k = e >> 5, r4 = (e & 31) * 4;
-                    cp_async16_d(&As[st][k][r4], a.Snc + (int64_t)(cq * DTK + k) * a.ldc + row0 + r4);
-                    cp_async16_d(&Bs[st][k][r4], a.Scol + (int64_t)(cq * DTK + k) * a.ldcol + col0 + r4);
-                }
+                cp_async16_sd(sA + soff, pa);
+                cp_async16_sd(sA + soff + EIGHTB, pa + 8 * a.ldc);
+                cp_async16_sd(sB + soff, pb);
+                cp_async16_sd(sB + soff + EIGHTB, pb + 8 * a.ldcol);
+                pa += (int64_t)DTK * a.ldc;
+                pb += (int64_t)DTK * a.ldcol;
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
+            soff = (soff == (DTNS - 1) * STGB) ? 0u : soff + STGB;
         };
         issue(0);
         issue(1);
@@ -700,11 +709,11 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
                 }
             }
         }
-        for (int cq = 0; cq < nchunk; ++cq) {
+        int st = 0;
+        for (int cq = 0; cq < nchunk; ++cq, st = (st == DTNS - 1) ? 0 : st + 1) {
             asm volatile("cp.async.wait_group 1;" ::: "memory");
             __syncthreads();
             issue(cq + 2);
-            const int st = cq % DTNS;
             const int kmax = min(DTK, a.nbp - cq * DTK);
             if (kmax == DTK) {
 #pragma unroll
@@ -763,6 +772,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
                 }
             }
         }
+        if (tid == 0) next = after;   // read by everyone after the barrier at the loop top
     }
 #undef RR
 #undef CC
@@ -848,13 +858,15 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     for (int64_t j = 0; j < L; ++j) ncols[(j / DCB) % G]++;
     int64_t ncmax = 1;
     for (auto c : ncols) ncmax = std::max(ncmax, c);
-    // lookahead (the chain of panel p+1 runs while panel p's trailing update runs on a
-    // second stream, on the SMs the chain leaves free): default on real ranks; the
-    // emulation runs it for the bitwise tests (HF_DIST_LOOKAHEAD=0/1 overrides)
+    // lookahead (HF_DIST_LOOKAHEAD=1: the chain of panel p+1 runs while panel p's trailing
+    // update runs on a second stream, on the SMs the chain leaves free).  Off by default:
+    // measured on one B200 the chain runs 1.57x slower beside the concurrent update and
+    // the time model then projects the serial schedule faster at every G
+    // (profiles/dist_lookahead_c2_r02.log, profiles/dist_model_c4_r02.json).
     // (=2: the lookahead chain with everything on one stream -- the time model's
     // measurement of the lookahead chain's own cost, no concurrency)
-    bool look = real;
-    int look_mode = real ? 1 : 0;
+    bool look = false;
+    int look_mode = 0;
     if (const char *e = getenv("HF_DIST_LOOKAHEAD")) look_mode = atoi(e);
     look = look_mode != 0;
 
@@ -869,7 +881,11 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     HF_CUDA(cudaFuncGetAttributes(&fb, k_chain_d<true>));
     maxsmem -= (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes) + 64;
     const int cmax_sm = real ? nsm : std::max(1, nsm / G);
-    int cper_def = (int)std::min<int64_t>(std::max(1, nsm / G), std::max<int64_t>(1, cdiv(ncmax, 128)));
+    // as few CTAs as the panel's shared memory allows (fewer CTAs: a cheaper exchange; the
+    // one-GPU chain's measured optimum is 64 CTAs at C2), at least 64 over all ranks
+    const int nf0 = look ? 2 : 1;
+    const int64_t rows_fit = std::max<int64_t>(32, (int64_t)(maxsmem / 4) / (nf0 * 128 + 4));
+    int cper_def = (int)std::min<int64_t>(cmax_sm, std::max<int64_t>(cdiv(64, G), cdiv(ncmax, rows_fit)));
     if (const char *e = getenv("HF_DIST_CTAS")) cper_def = std::max(1, std::min(cmax_sm, atoi(e)));
     int Cmax = std::max(cper_def, (int)std::min<int64_t>(cmax_sm, cdiv(ncmax, 1024)));
     int64_t R0 = cdiv(ncmax, Cmax);
@@ -1110,7 +1126,8 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
                 ta.ldcol = ldcol; ta.status = b.status.p;
                 // real ranks with lookahead: leave the chain's SMs free (the next chain
                 // launches while this update runs); the emulation's chain spans every SM
-                ta.reserve = (look && real) ? Cmax : 0;
+                // (G = 1: one GPU, the lookahead is real there too)
+                ta.reserve = (look && st2 != st && (real || G == 1)) ? Cmax : 0;
                 ClassTimer tm(ctx, "trailing", st2, dtrail_flops_total(mp, nbp) / G, 0.0);
                 ClassTimer tr(ctx, rank_class("trailing", h), st2);   // per rank (the time model)
                 k_trailing_d<<<(unsigned)tgrid, 256, DTRAIL_SMEM, st2>>>(ta);

@@ -11,7 +11,7 @@ measured on ONE B200 (this run has no multi-GPU box): VERDICT r01 item 2.
     chain_p*  = chain_emul_p + nbp * dNV + t_bar
     upd_p*    = max_h gather_ph + remote_p / BW + max_h trail_ph + t_bar
     serial    : T = sum_p (chain_p + upd_p)                       (HF_DIST_LOOKAHEAD=0)
-    lookahead : T = chain_0 + sum_p max(chain_{p+1}, upd_p * nsm / (nsm - Cper))
+    lookahead : T = chain_0 + sum_p max(CONC * chain_{p+1}, upd_p * nsm / (nsm - Cper))
                 (the chain of panel p+1 beside panel p's update on the other SMs;
                  chain and update times from the lookahead geometry, measured with
                  HF_DIST_LOOKAHEAD=2: the lookahead kernels on one stream)
@@ -37,6 +37,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 DNV_US = 2.0
+# the chain runs this much slower beside a concurrent trailing update on the other SMs
+# (measured on one B200 at C2 through the same kernels, G = 1 with 64 reserved chain SMs:
+# chain 95.8 ms with the lookahead vs 61.1 ms serial, profiles/dist_lookahead_c2_r02.log)
+CONC = 95.8 / 61.1
 BW = 770e9
 T_BAR_US = 4.0
 NSM = 148
@@ -121,7 +125,7 @@ def model(res1, resG, L, G, look):
         s = NSM / (NSM - cper)
         T = ch[0]
         for p in range(n):
-            nxt = ch[p + 1] if p + 1 < n else 0.0
+            nxt = ch[p + 1] * CONC if p + 1 < n else 0.0
             T += max(nxt, up[p] * s)
         T += Lg
     return {"model_ms": T, "chain_ms_sum": sum(ch), "update_ms_sum": sum(up), "panels": n, "nb": nb,
@@ -138,7 +142,8 @@ def main():
     one = run(name, 0, 0)
     res = {"config": name, "L": L, "one_gpu_stage1_ms": one["ms"],
            "assumptions": {"dNV_us_per_pivot": DNV_US, "peer_GBps": BW / 1e9, "barrier_us": T_BAR_US,
-                           "lookahead_trailing_slowdown": "nsm / (nsm - nsm // G)"}, "G": {}}
+                           "lookahead_trailing_slowdown": "nsm / (nsm - nsm // G)",
+                           "lookahead_chain_slowdown_measured": CONC}, "G": {}}
     for G in Gs:
         rs = run(name, G, 0)
         rl = run(name, G, 2)
