@@ -64,19 +64,27 @@ hf_status hf_nccl_unique_id(void *id128_host);
  * hard factorization and hf_solve are replicated (deterministic kernels:
  * identical on every rank).  Pure host function, needs no device. */
 hf_status hf_shard_cols(int64_t n2, int nranks, int rank, int64_t *c0_host, int64_t *c1_host);
-/* Multi-GPU stage 1: on a context of nranks > 1,
- * hf_factor_lowprec splits the FP32 trailing matrix by columns: rank r holds
- * FULL columns (all active rows) of the original indices j with
- * (j / 128) % nranks == r and updates only those; every rank runs the pivot
- * chain itself (same inputs, same pivots, no pivot exchange) and reads each
- * pivot column from its owner's memory through a CUDA-IPC peer mapping over
- * NVLink; one NCCL barrier per panel.  Results are bitwise those of one GPU.
- * hf_set_stage1_partitions(ctx, G > 0) runs the same partitioned algorithm
- * with all G partitions on this GPU (single-process emulation, tests); 0 = the
- * single-GPU lower-triangle path. */
+/* Multi-GPU stage 1 (P:64-67, P:72-75 distributed): on a context of
+ * nranks > 1, hf_factor_lowprec distributes the FP32 factorization in a 1D
+ * block-cyclic layout of the LOWER triangle: rank r owns the original indices
+ * j with (j / 128) % nranks == r and stores, for each, the entries v_IJ of the
+ * active I at or below it (every pair on exactly one rank: the trailing-update
+ * work over the ranks equals one GPU's).  The pivot chain's rows are split the
+ * same way; per pivot every chain CTA stores its tagged (|d|, position) key into
+ * every rank's slot array over NVLink (the max-reduction that picks the pivot),
+ * the pivot column's entries below the pivot are read from its owner and the
+ * pivot row's in-panel values from the winner's mailbox; after each panel every
+ * rank gathers the panel from the owners and updates its own columns.  Peer
+ * buffers are CUDA-IPC mappings (handles all-gathered over NCCL), barriers are
+ * device-side; a peer that stops answering for 60 s makes the call fail with
+ * HF_ERR_NCCL ("peer did not answer") instead of hanging.  Pi, D and L
+ * are bitwise those of one GPU on every rank.
+ * hf_set_stage1_partitions(ctx, G > 0) runs the same distributed algorithm with
+ * all G ranks on this GPU (one cooperative chain launch over every rank's CTAs:
+ * single-process emulation, tests and the time model); 0 = the single-GPU path. */
 hf_status hf_set_stage1_partitions(hf_ctx *ctx, int nparts);
-/* The columns (original indices, increasing) partition `part` of `nparts` owns
- * in that factorization: j with (j / 128) % nparts == part.  Host only; the
+/* The indices (original, increasing) rank `part` of `nparts` owns in that
+ * factorization: j with (j / 128) % nparts == part.  Host only; the
  * list is written if cols_host is not NULL (room for L entries). */
 hf_status hf_stage1_partition(int64_t L, int nparts, int part, int64_t *ncols_host, int64_t *cols_host);
 /* Single-GPU emulation of one rank of that sharding (tests): with nranks > 0,

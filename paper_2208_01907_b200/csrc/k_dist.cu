@@ -1189,7 +1189,7 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
     int32_t hs[4];
     HF_CUDA(cudaMemcpy(hs, B[me].status.p, sizeof(hs), cudaMemcpyDeviceToHost));
     for (void *p : opened) cudaIpcCloseMemHandle(p);
-    HF_REQUIRE(hs[3] == 0, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)");
+    if (hs[3] != 0) throw Error{HF_ERR_NCCL, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)"};
 }
 
 }  // namespace hf

@@ -151,17 +151,7 @@ struct ChainArgs {
     int nbprev, nbmax;
     float *SNout;             // [pos][nbmax] this panel's values (for the next panel)
     float *DGout;             // [pos] lazy diagonal at the end of this panel
-    // column-partitioned trailing matrix (multi-GPU stage 1 and its single-GPU emulation):
-    // partition g holds FULL columns (all active rows, by position) of the original indices
-    // j with (j / cb) % nparts == g, at local column colpos[j]; parts[g] is its buffer
-    // (a peer pointer on a multi-GPU run).  Null parts: the lower-triangle V above.
-    const float *const *parts;
-    int nparts, cb;
-    const int32_t *colpos;    // [L] original index -> local column in its partition (-1: pivoted)
-    int64_t ldp;              // leading dimension of the partition buffers
 };
-
-__device__ __forceinline__ int part_of(int64_t j, int cb, int nparts) { return (int)((j / cb) % nparts); }
 
 constexpr int SLOT_STRIDE = 32;     // 256 B between slots: no two CTAs' slots share an L2 line
 constexpr uint64_t TAGM = 0x3FFF;   // 14-bit step tag in the low bits of every exchanged word
@@ -191,12 +181,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //     (tag-checked) and the panel-start column V[:, P] for own rows;
 //  G  c_i = chain of fmaf over the earlier in-panel pivots in order [R8],
 //     s = c/r, L = c/d, diagonal.
-template <bool PARTS>
 __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
     __shared__ unsigned long long bkey;
-    __shared__ uint32_t pcol;   // (partition << 20 | local column) of the pivot (parts mode)
     if (*(volatile int32_t *)&a.status[2]) return;   // uniform: set by an earlier launch
     const int G = gridDim.x;
     const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
@@ -215,18 +203,12 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const int64_t io = (has && a.mapprev) ? (int64_t)a.mapprev[i] : i;   // own row in V's position space
     const int32_t oi = has ? a.orig[i] : 0;
     float dg = 0.f;   // lazy diagonal of own row
-    if (has) {
-        if (PARTS) dg = a.parts[part_of(oi, a.cb, a.nparts)][i + (int64_t)a.colpos[oi] * a.ldp];
-        else dg = a.DGprev ? a.DGprev[io] : a.V[i + i * a.ldv];
-    }
+    if (has) dg = a.DGprev ? a.DGprev[io] : a.V[i + i * a.ldv];
     if (has)
         for (int u = 0; u < nbq; ++u) snp[(size_t)u * a.R + tid] = a.SNprev[io * a.nbmax + u];
-    // PARTS: where the own row's column lives (partition << 20 | local column), fixed in a panel
-    const uint32_t myinfo = (PARTS && has) ? ((uint32_t)a.colpos[oi] | ((uint32_t)part_of(oi, a.cb, a.nparts) << 20)) : 0u;
-    __shared__ uint32_t redi[32];
     bool piv = !has;
     float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
-    const bool BLK = !PARTS && a.blk != nullptr;
+    const bool BLK = a.blk != nullptr;
     int curblk = BLK ? a.bstate[0] : 0;
     bool first = BLK ? (a.bstate[1] != 0) : (a.K0 == 0);
     int64_t att = BLK ? (int64_t)a.bstate[2] : a.K0;   // exchange attempt: tags and buffer parity
@@ -247,46 +229,17 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- A: [R3] local argmax of |diag| over own active rows (of the current block)
         const bool cand = !piv && (!BLK || curblk >= a.nblk || myblk == curblk);
         uint64_t key = cand ? mkkey(dg, (uint32_t)i) : 0ull;
-        uint32_t kinfo = myinfo;
-        if (PARTS) {
-#pragma unroll
-            for (int o2 = 16; o2 > 0; o2 >>= 1) {   // max key, carrying its row's column info
-                const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, key, o2);
-                const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, kinfo, o2);
-                if (ok2 > key) {
-                    key = ok2;
-                    kinfo = oi2;
-                }
-            }
-            if (lane == 0) redi[wid] = kinfo;
-        } else {
-            key = warp_max64(key);
-        }
+        key = warp_max64(key);
         if (lane == 0) red[wid] = key;
         __syncthreads();
         // ---- B: publish
         if (wid < 2) {
             uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
-            uint32_t vinfo = (PARTS && lane < nwarp) ? redi[lane] : 0u;
-            if (PARTS) {
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) {
-                    const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, v, o2);
-                    const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, vinfo, o2);
-                    if (ok2 > v) {
-                        v = ok2;
-                        vinfo = oi2;
-                    }
-                }
-            } else {
-                v = warp_max64(v);
-            }
+            v = warp_max64(v);
             if (wid == 0) {
                 if (lane == 0) {
                     if (a.xmode == 1) {
                         unsigned long long *slot = &a.slots[((size_t)par * G + blockIdx.x) * SLOT_STRIDE];
-                        if (PARTS)   // the candidate's (partition, local column), next to its key
-                            st_relaxed_u64(slot + 1, ((unsigned long long)(v ? vinfo : 0u) << 32) | tag);
                         st_relaxed_u64(slot, (v & ~TAGM) | tag);
                     } else {
                         if (v) red_max_u64(&a.keys[t], v);
@@ -312,40 +265,20 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         if (a.xmode == 1) {
             if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
                 const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
-                uint64_t mx, mi = 0;
+                uint64_t mx;
                 for (;;) {
                     bool ok = true;
                     mx = 0;
                     for (int g = lane; g < G; g += 32) {
                         const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * SLOT_STRIDE]);
                         ok &= (sv & TAGM) == tag;
-                        if (PARTS) {
-                            const uint64_t si = ld_relaxed_u64(&sl[(size_t)g * SLOT_STRIDE + 1]);
-                            ok &= (si & TAGM) == tag;
-                            if (sv > mx) mi = si;
-                        }
                         mx = umax64(mx, sv);
                     }
                     if (__all_sync(0xffffffffu, ok)) break;
                 }
-                if (PARTS) {
-#pragma unroll
-                    for (int o2 = 16; o2 > 0; o2 >>= 1) {   // max key, carrying its info word
-                        const uint64_t ox = __shfl_xor_sync(0xffffffffu, mx, o2);
-                        const uint64_t oi2 = __shfl_xor_sync(0xffffffffu, mi, o2);
-                        if (ox > mx) {
-                            mx = ox;
-                            mi = oi2;
-                        }
-                    }
-                } else {
-                    mx = warp_max64(mx);
-                }
-                if (lane == 0) {
-                    bkey = mx;
-                    pcol = (uint32_t)(mi >> 32);
-                }
-                if (a.dbg && blockIdx.x == 0 && !PARTS) {
+                mx = warp_max64(mx);
+                if (lane == 0) bkey = mx;
+                if (a.dbg && blockIdx.x == 0) {
                     // speculation statistics: is this step's pivot the runner-up (or third) of
                     // the previous step's per-CTA candidates? (positions; HF_CHAIN_DEBUG only)
                     const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
@@ -403,14 +336,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // the column load is issued first so its latency overlaps the mailbox poll below
         // (one unconditional load from a selected address, its value used only after the
         // barrier below: a conditional load merged into a register stalls the thread here)
-        float v;
-        if (PARTS) {
-            const uint32_t w = pcol;   // read after the barrier that published bkey
-            v = (!piv && i != P) ? a.parts[w >> 20][i + (int64_t)(w & 0xFFFFF) * a.ldp] : 0.f;
-        } else {
-            const float *vp = (io >= Po) ? (a.V + io + Po * a.ldv) : (a.V + Po + io * a.ldv);
-            v = __ldcg((!piv && i != P) ? vp : a.V);
-        }
+        const float *vp = (io >= Po) ? (a.V + io + Po * a.ldv) : (a.V + Po + io * a.ldv);
+        const float v = __ldcg((!piv && i != P) ? vp : a.V);
         {
             const int owner = (int)(P / a.R);
             const unsigned long long *mb = a.mbox + ((size_t)par * G + owner) * (nb + 1);
@@ -1017,188 +944,6 @@ __global__ void __launch_bounds__(256, 2) k_trailing_p(TrailArgs a, int64_t ntil
 }
 
 // ------------------------------------------------------------------ partitioned trailing update
-// Column partition g (multi-GPU stage 1 / its emulation): FULL columns, every
-// active row.  Tile grid = row tiles x local column tiles (no triangle); entry
-// (r, c) starts from the previous panel's value (rows compacted by map, columns
-// by cmap) and receives one fmaf per pivot in order -- for r < c that is the
-// role-swapped product of the lower-triangle entry, bit-identical by [R8].
-struct RectArgs {
-    int64_t mp;                  // active rows after the panel
-    const int32_t *mcount;       // [1] active local columns after the panel (device)
-    int nbp;
-    const float *Vold;
-    float *Vnew;
-    int64_t ldp;
-    const int32_t *map;          // new row position -> old row position
-    const int32_t *cmap;         // new local column -> old local column
-    const int32_t *colold;       // new local column -> old ROW position of that index (S lookup)
-    const float *S, *Sn;
-    int64_t lds;
-    const int32_t *status;
-};
-
-__global__ void __launch_bounds__(256, 2) k_trailing_rect(RectArgs a) {
-    if (a.status[2]) return;
-    const int64_t mc = *a.mcount;
-    const int64_t row0 = (int64_t)blockIdx.x * TB, col0 = (int64_t)blockIdx.y * TB;
-    if (col0 >= mc || row0 >= a.mp) return;
-    __shared__ __align__(16) float As[2][TK][TB];
-    __shared__ __align__(16) float Bs[2][TK][TB];
-    __shared__ int32_t rmap[TB], cmap[TB], cpos[TB];
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    if (tid < TB) {
-        rmap[tid] = (row0 + tid < a.mp) ? a.map[row0 + tid] : -1;
-        cmap[tid] = (col0 + tid < mc) ? a.cmap[col0 + tid] : -1;
-        cpos[tid] = (col0 + tid < mc) ? a.colold[col0 + tid] : -1;
-    }
-    __syncthreads();
-#define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
-#define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
-    float2 acc[8][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int32_t cm0 = cmap[CC(2 * j)], cm1 = cmap[CC(2 * j + 1)];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int32_t rm = rmap[RR(q)];
-            acc[q][j].x = (cm0 >= 0 && rm >= 0) ? a.Vold[(int64_t)rm + (int64_t)cm0 * a.ldp] : 0.f;
-            acc[q][j].y = (cm1 >= 0 && rm >= 0) ? a.Vold[(int64_t)rm + (int64_t)cm1 * a.ldp] : 0.f;
-        }
-    }
-    const int lr = tid & 127, lk = tid >> 7;
-    const int32_t arow = rmap[lr], bcol = cpos[lr];
-    const float *Ap = a.Sn + (arow >= 0 ? arow : 0);
-    const float *Bp = a.S + (bcol >= 0 ? bcol : 0);
-    float ra[TK / 2], rb[TK / 2];
-    auto gload = [&](int t0) {
-#pragma unroll
-        for (int q = 0; q < TK / 2; ++q) {
-            const int tt = t0 + lk + 2 * q;
-            const bool ok = tt < a.nbp;
-            ra[q] = (ok && arow >= 0) ? Ap[(int64_t)tt * a.lds] : 0.f;
-            rb[q] = (ok && bcol >= 0) ? Bp[(int64_t)tt * a.lds] : 0.f;
-        }
-    };
-    auto sstore = [&](int buf) {
-#pragma unroll
-        for (int q = 0; q < TK / 2; ++q) {
-            As[buf][lk + 2 * q][lr] = ra[q];
-            Bs[buf][lk + 2 * q][lr] = rb[q];
-        }
-    };
-    gload(0);
-    sstore(0);
-    __syncthreads();
-    int buf = 0;
-    for (int t0 = 0; t0 < a.nbp; t0 += TK) {
-        const bool more = t0 + TK < a.nbp;
-        if (more) gload(t0 + TK);
-        const int kmax = min(TK, a.nbp - t0);
-        for (int kk = 0; kk < kmax; ++kk) {   // exactly nbp updates, in order
-            const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][tx * 4]);
-            const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + tx * 4]);
-            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4]);
-            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + ty * 4]);
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                                  make_float2(b1.z, b1.w)};
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[q][j] = __ffma2_rn(make_float2(av[q], av[q]), bv[j], acc[q][j]);
-        }
-        if (more) {
-            sstore(buf ^ 1);
-            __syncthreads();
-            buf ^= 1;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t c = col0 + CC(2 * j + h);
-            if (c >= mc) continue;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int64_t r = row0 + RR(q);
-                if (r < a.mp) a.Vnew[r + c * a.ldp] = h ? acc[q][j].y : acc[q][j].x;
-            }
-        }
-#undef RR
-#undef CC
-}
-
-// full-column FP32 copy of partition g: Vg[i + lc * ldp] = RN32(K(i, j)) for the
-// original indices j of g in increasing order (lower triangle of K read [R1])
-__global__ void k_cast_part(int64_t L, const double *__restrict__ K, int64_t ld, int g, int nparts, int cb,
-                            float *__restrict__ Vg, int64_t ldp, int64_t ncols) {
-    for (int64_t lc = blockIdx.x; lc < ncols; lc += gridDim.x) {
-        const int64_t j = (lc / cb) * ((int64_t)cb * nparts) + (int64_t)g * cb + (lc % cb);
-        float *vc = Vg + lc * ldp;
-        for (int64_t i = threadIdx.x; i < L; i += blockDim.x)
-            vc[i] = __double2float_rn(i >= j ? K[i + j * ld] : K[j + i * ld]);
-    }
-}
-
-__global__ void k_colpos_init(int64_t L, int nparts, int cb, int32_t *colpos) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < L) colpos[j] = (int32_t)((j / ((int64_t)cb * nparts)) * cb + (j % cb));
-}
-
-// posold[orig[p]] = p (old positions of the active indices)
-__global__ void k_posinv(int64_t m, const int32_t *__restrict__ orig, int32_t *__restrict__ posold,
-                         const int32_t *status) {
-    if (status[2]) return;
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < m) posold[orig[p]] = (int32_t)p;
-}
-
-// after a panel: colnew[j] = colold[j] - #(pivots of the panel in j's partition with a
-// smaller local column), -1 for the pivots themselves; for every partition g the maps
-// cmap_g[new] = old local column, cpos_g[new] = old row position, and the count.
-__global__ void k_colpos_update(int64_t L, int nparts, int cb, int nbp, const int32_t *__restrict__ piv,
-                                const int32_t *__restrict__ colold, int32_t *__restrict__ colnew,
-                                const int32_t *__restrict__ posold, int32_t *__restrict__ cmap,
-                                int32_t *__restrict__ cpos, int64_t ldmap, int32_t *__restrict__ mcount,
-                                const int32_t *status) {
-    if (status[2]) return;
-    __shared__ int32_t pv[1024], pc[1024], cnt[1024];
-    for (int q = threadIdx.x; q < nbp; q += blockDim.x) {
-        pv[q] = piv[q];
-        pc[q] = colold[piv[q]];
-    }
-    for (int q = threadIdx.x; q < nparts; q += blockDim.x) cnt[q] = 0;
-    __syncthreads();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = colold[j];
-        if (c < 0) {
-            colnew[j] = -1;
-            continue;
-        }
-        const int g = part_of(j, cb, nparts);
-        int dec = 0;
-        bool isp = false;
-        for (int q = 0; q < nbp; ++q) {
-            if (part_of(pv[q], cb, nparts) != g) continue;
-            if (pv[q] == j) isp = true;
-            dec += (pc[q] < c);
-        }
-        if (isp) {
-            colnew[j] = -1;
-            continue;
-        }
-        const int32_t cn = c - dec;
-        colnew[j] = cn;
-        cmap[(int64_t)g * ldmap + cn] = c;
-        cpos[(int64_t)g * ldmap + cn] = posold[j];
-        atomicAdd(&cnt[g], 1);
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < nparts; q += blockDim.x)
-        if (cnt[q]) atomicAdd(&mcount[q], cnt[q]);
-}
-
 // ------------------------------------------------------------------ factor gather
 // Lfac[a + k*N] = Lorig[pivorig[a] + k*ldl] (a > k), 1 (a == k), 0 (a < k)
 __global__ void k_gather_L(int64_t N, const int32_t *__restrict__ pivorig, const float *__restrict__ Lorig,
@@ -1241,7 +986,7 @@ void lowprec_outputs(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfac
     int32_t hs[4];
     HF_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
     HF_CUDA(cudaStreamSynchronize(st));
-    HF_REQUIRE(hs[3] == 0, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)");
+    if (hs[3] != 0) throw Error{HF_ERR_NCCL, "stage 1: a peer did not answer within the exchange timeout (multi-GPU chain)"};
     const int64_t Ntau = hs[2] ? hs[0] : L;
     // [R5] floor and [R9] enlargement: the last accepted pivots move to Lambda_2
     int64_t N = Ntau;
@@ -1317,12 +1062,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     int maxsmem = 0;
     HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain<false>));
-    {
-        cudaFuncAttributes fb;
-        HF_CUDA(cudaFuncGetAttributes(&fb, k_chain<true>));
-        fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
-    }
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain));
     maxsmem -= (int)fa.sharedSizeBytes;
     // Chain geometry (measured on B200 at C2, chain + trailing ms: 148 CTAs / nb 256: 106.3,
     // 148 / 128: 103.3, 74 / 128: 100.6, 64 / 128: 95.0, 64 / 192: 95.8, 32 / 96: 98.8):
@@ -1411,8 +1151,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[0], 0));
     }
 
-    HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
-    HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     // persistent trailing kernel (seed prefetch), two CTAs per SM -- OFF by default: measured
     // 38.3 vs 31.0 ms per C2 step (FMA pipe 64.8 vs 71.5 % active; the 4-byte cp.async seed
@@ -1473,11 +1212,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         }
         ca.SNout = look ? SNrow[pb].p : nullptr;
         ca.DGout = look ? DG[pb].p : nullptr;
-        ca.parts = nullptr; ca.nparts = 1; ca.cb = 1; ca.colpos = nullptr; ca.ldp = 0;
         {
             ClassTimer tm(ctx, "chain", st, chain_flops(m, nbp), chain_bytes(m, nbp));
             void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain<false>, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain, dim3((unsigned)G), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }
         const int64_t mp = m - nbp;
@@ -1556,214 +1294,6 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     V[0].release();   // the trailing buffers are done: keep the peak at K + Lorig + Lfac
     V[1].release();
     lowprec_finish(ctx, L, o, lf, status, pivorig, Dk, Lorig, want_dbg ? &dbg : nullptr);
-}
-
-// ------------------------------------------------------------------ partitioned driver
-// Stage 1 with the trailing matrix split by columns: partition g
-// holds FULL columns of the original indices j with (j / CB) % G == g.  Every
-// rank runs the pivot chain itself (identical inputs -> identical pivots, no
-// pivot exchange); the chain reads each pivot column from its owner's
-// partition (a CUDA-IPC peer pointer over NVLink on a multi-GPU run) and each
-// rank applies the trailing update to its own columns only (2x the flops of
-// the triangle, split G ways).  Bitwise equal to the single-GPU path [R8].
-// nparts > 1 with ctx->nranks == 1: all partitions live on this GPU (the
-// single-process emulation used by the tests).
-void lowprec_factor_parts(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
-                          hf_lowfactor *lf, int nparts) {
-    cudaStream_t st = ctx->stream;
-    const int nsm = ctx->num_sms;
-    lf->L = L;
-    lf->stream = st;
-    if (L == 0) {
-        lf->N = lf->Ntau = lf->n2 = 0;
-        return;
-    }
-    HF_REQUIRE(L <= (int64_t)POS_MAX - 1, "L too large for the 17-bit position key");
-    HF_REQUIRE(nparts >= 1 && nparts <= 1024, "stage-1 partitions out of range");
-    const bool real = ctx->nranks > 1;            // one partition per rank, peers over IPC
-    HF_REQUIRE(!real || nparts == ctx->nranks, "partitions must equal ranks on a multi-GPU context");
-    const int CB = 128;
-    int maxsmem = 0;
-    HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain<false>));
-    {
-        cudaFuncAttributes fb;
-        HF_CUDA(cudaFuncGetAttributes(&fb, k_chain<true>));
-        fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
-    }
-    maxsmem -= (int)fa.sharedSizeBytes;
-    const int nb_def = 128;
-    int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / (nb_def + 2)))));
-    const int64_t G0 = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(L, 32)));
-    const int64_t R0 = cdiv(L, G0);
-    HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
-    int nb = o.nb > 0 ? o.nb : nb_def;
-    while (nb > 8 && (int64_t)(nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
-
-    // partition sizes and buffers (2 ping-pong buffers of L x ncols_g)
-    std::vector<int64_t> ncols(nparts, 0);
-    for (int64_t j = 0; j < L; ++j) ncols[(j / CB) % nparts]++;
-    int64_t ldmap = 1;
-    for (auto c : ncols) ldmap = std::max(ldmap, c);
-    const int lo = real ? ctx->rank : 0, hi = real ? ctx->rank + 1 : nparts;   // partitions held here
-    std::vector<DBuf<float>> VP((size_t)2 * nparts);
-    for (int g = lo; g < hi; ++g)
-        for (int b = 0; b < 2; ++b) VP[(size_t)b * nparts + g].alloc((size_t)L * std::max<int64_t>(ncols[g], 1), st);
-    std::vector<float *> tab((size_t)2 * nparts, nullptr);
-    for (int g = lo; g < hi; ++g)
-        for (int b = 0; b < 2; ++b) tab[(size_t)b * nparts + g] = VP[(size_t)b * nparts + g].p;
-    std::vector<void *> opened;
-#ifdef HF_WITH_NCCL
-    if (real) {
-        // exchange CUDA-IPC handles of every rank's two buffers (NCCL all-gather of the bytes)
-        std::vector<cudaIpcMemHandle_t> mine(2);
-        for (int b = 0; b < 2; ++b) HF_CUDA(cudaIpcGetMemHandle(&mine[b], tab[(size_t)b * nparts + ctx->rank]));
-        DBuf<char> hb;
-        hb.alloc((size_t)2 * sizeof(cudaIpcMemHandle_t) * (nparts + 1), st);
-        HF_CUDA(cudaMemcpyAsync(hb.p, mine.data(), 2 * sizeof(cudaIpcMemHandle_t), cudaMemcpyHostToDevice, st));
-        collective_allgather_bytes(ctx, hb.p, hb.p + 2 * sizeof(cudaIpcMemHandle_t), 2 * sizeof(cudaIpcMemHandle_t));
-        std::vector<cudaIpcMemHandle_t> all((size_t)2 * nparts);
-        HF_CUDA(cudaMemcpyAsync(all.data(), hb.p + 2 * sizeof(cudaIpcMemHandle_t),
-                                (size_t)2 * nparts * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost, st));
-        HF_CUDA(cudaStreamSynchronize(st));
-        for (int g = 0; g < nparts; ++g) {
-            if (g == ctx->rank) continue;
-            for (int b = 0; b < 2; ++b) {
-                void *ptr = nullptr;
-                HF_CUDA(cudaIpcOpenMemHandle(&ptr, all[(size_t)g * 2 + b], cudaIpcMemLazyEnablePeerAccess));
-                tab[(size_t)b * nparts + g] = static_cast<float *>(ptr);
-                opened.push_back(ptr);
-            }
-        }
-    }
-#else
-    HF_REQUIRE(!real, "multi-GPU stage 1 needs NCCL");
-#endif
-    DBuf<float *> dtab;
-    dtab.alloc((size_t)2 * nparts, st);
-    HF_CUDA(cudaMemcpyAsync(dtab.p, tab.data(), tab.size() * sizeof(float *), cudaMemcpyHostToDevice, st));
-
-    DBuf<int32_t> orig[2], map, colpos[2], posold, cmap, cpos, mcount;
-    orig[0].alloc(L, st);
-    orig[1].alloc(L, st);
-    map.alloc(L, st);
-    colpos[0].alloc(L, st);
-    colpos[1].alloc(L, st);
-    posold.alloc(L, st);
-    cmap.alloc((size_t)nparts * ldmap, st);
-    cpos.alloc((size_t)nparts * ldmap, st);
-    mcount.alloc(nparts, st);
-    DBuf<float> S, Sn, sigma, Lorig, Dk;
-    S.alloc((size_t)L * nb, st);
-    Sn.alloc((size_t)L * nb, st);
-    sigma.alloc(nb, st);
-    Lorig.alloc((size_t)L * L, st);
-    Dk.alloc(L, st);
-    DBuf<int32_t> pivpos, pivorig, status;
-    pivpos.alloc(nb, st);
-    pivorig.alloc(L, st);
-    status.alloc(4, st);
-    DBuf<unsigned long long> mbox, slots;
-    mbox.alloc((size_t)2 * nsm * (nb + 1), st);
-    mbox.zero(st);
-    slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
-    slots.zero(st);
-    HF_CUDA(cudaMemsetAsync(status.p, 0, 4 * sizeof(int32_t), st));
-    {
-        ClassTimer tm(ctx, "other");
-        for (int g = lo; g < hi; ++g) {
-            k_cast_part<<<(unsigned)std::min<int64_t>(std::max<int64_t>(ncols[g], 1), 65535), 256, 0, st>>>(
-                L, K, ld, g, nparts, CB, tab[g], L, ncols[g]);
-            HF_CHECK_LAUNCH(ctx);
-        }
-        k_iota32<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
-        HF_CHECK_LAUNCH(ctx);
-        k_colpos_init<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, nparts, CB, colpos[0].p);
-        HF_CHECK_LAUNCH(ctx);
-    }
-#ifdef HF_WITH_NCCL
-    DBuf<int> bar;
-    if (real) {
-        bar.alloc(1, st);
-        bar.zero(st);
-        collective_barrier(ctx, bar.p);   // every rank's partitions are cast before anyone reads them
-    }
-#endif
-    HF_CUDA(cudaFuncSetAttribute(k_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
-    HF_CUDA(cudaFuncSetAttribute(k_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
-    std::vector<int64_t> bound(ncols);
-    int cur = 0;
-    int64_t m = L, K0 = 0;
-    while (m > 0) {
-        const int nbp = (int)std::min<int64_t>(nb, m);
-        const int64_t G = std::min<int64_t>(gmax, std::max<int64_t>(1, cdiv(m, 32)));
-        const int64_t R = cdiv(m, G);
-        const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
-        const size_t shm = ((size_t)nbp * R + 3 * nbp + 4) * sizeof(float);
-        ChainArgs ca;
-        ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;
-        ca.V = nullptr; ca.ldv = L; ca.orig = orig[cur].p;
-        ca.S = S.p; ca.Sn = Sn.p; ca.lds = L; ca.sigma = sigma.p; ca.pivpos = pivpos.p;
-        ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
-        ca.keys = nullptr; ca.cnt = nullptr; ca.mbox = mbox.p; ca.slots = slots.p; ca.xmode = 1;
-        ca.status = status.p; ca.dbg = nullptr;
-        ca.blk = nullptr; ca.nblk = 0; ca.bstate = nullptr;
-        ca.mapprev = nullptr; ca.SNprev = nullptr; ca.sigprev = nullptr; ca.DGprev = nullptr;
-        ca.nbprev = 0; ca.nbmax = nb; ca.SNout = nullptr; ca.DGout = nullptr;
-        ca.parts = dtab.p + (size_t)cur * nparts; ca.nparts = nparts; ca.cb = CB; ca.colpos = colpos[cur].p;
-        ca.ldp = L;
-        {
-            ClassTimer tm(ctx, "chain");
-            void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain<true>, dim3((unsigned)G), dim3(nthr), args, shm, st));
-            HF_CHECK_LAUNCH(ctx);
-        }
-        const int64_t mp = m - nbp;
-        if (mp > 0) {
-            {
-                ClassTimer tm(ctx, "other");
-                k_compact<<<(unsigned)std::min<int64_t>(cdiv(m, 256), 4096), 256, 0, st>>>(
-                    m, nbp, pivpos.p, orig[cur].p, map.p, orig[cur ^ 1].p, status.p);
-                HF_CHECK_LAUNCH(ctx);
-                k_posinv<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(m, orig[cur].p, posold.p, status.p);
-                HF_CHECK_LAUNCH(ctx);
-                HF_CUDA(cudaMemsetAsync(mcount.p, 0, nparts * sizeof(int32_t), st));
-                k_colpos_update<<<(unsigned)std::min<int64_t>(cdiv(L, 256), 4096), 256, 0, st>>>(
-                    L, nparts, CB, nbp, pivorig.p + K0, colpos[cur].p, colpos[cur ^ 1].p, posold.p, cmap.p,
-                    cpos.p, ldmap, mcount.p, status.p);
-                HF_CHECK_LAUNCH(ctx);
-            }
-            for (int g = lo; g < hi; ++g) {
-                bound[g] = std::min<int64_t>(bound[g], mp);
-                if (bound[g] <= 0) continue;
-                RectArgs ra;
-                ra.mp = mp; ra.mcount = mcount.p + g; ra.nbp = nbp;
-                ra.Vold = tab[(size_t)cur * nparts + g]; ra.Vnew = tab[(size_t)(cur ^ 1) * nparts + g]; ra.ldp = L;
-                ra.map = map.p; ra.cmap = cmap.p + (size_t)g * ldmap; ra.colold = cpos.p + (size_t)g * ldmap;
-                ra.S = S.p; ra.Sn = Sn.p; ra.lds = L; ra.status = status.p;
-                dim3 grid((unsigned)cdiv(mp, TB), (unsigned)cdiv(bound[g], TB));
-                ClassTimer tm(ctx, "trailing");
-                k_trailing_rect<<<grid, 256, 0, st>>>(ra);
-                HF_CHECK_LAUNCH(ctx);
-            }
-#ifdef HF_WITH_NCCL
-            if (real) collective_barrier(ctx, bar.p);   // peers' columns of the next panel are written
-#endif
-            cur ^= 1;
-        }
-        K0 += nbp;
-        m = mp;
-    }
-#ifdef HF_WITH_NCCL
-    if (real) {
-        collective_barrier(ctx, bar.p);               // nobody reads a peer's buffers any more
-        HF_CUDA(cudaStreamSynchronize(st));
-        for (void *ptr : opened) cudaIpcCloseMemHandle(ptr);
-    }
-#endif
-    for (auto &b : VP) b.release();
-    lowprec_finish(ctx, L, o, lf, status, pivorig, Dk, Lorig, nullptr);
 }
 
 // ========================================================================= NEXT-3
