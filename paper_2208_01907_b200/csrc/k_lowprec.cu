@@ -129,7 +129,8 @@ struct ChainArgs {
     int32_t *pivorig;   // [L] original index of pivot k
     unsigned long long *keys;    // [nbp] per-step max key (zeroed before the launch)    (xmode 0)
     unsigned int *cnt;           // arrival counter (zeroed before the launch)          (xmode 0)
-    unsigned long long *slots;   // [2][G][SLOT_STRIDE] per-CTA key | step tag, one line each (xmode 1)
+    unsigned long long *slots;   // [2][G][sstride] per-CTA key | step tag (xmode 1)
+    int sstride;                 // words between two CTAs' slots (HF_SLOT_STRIDE; 32 = one L2 line each)
     int xmode;                   // 0: red.max + counter; 1: spread LL slots (HF_CHAIN_XCHG)
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
@@ -219,9 +220,10 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     int t = 0;
     bool stopped = false;
     const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
-    unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = dbg ? gtimer() : 0;
+    const bool dbga = a.dbg && tid == 0;   // per-CTA phase sums (HF_CHAIN_DEBUG=2: the skew)
+    unsigned long long ph[5] = {0, 0, 0, 0, 0}, tp = dbga ? gtimer() : 0;
     uint32_t spec2 = 0xFFFFFFFFu, spec3 = 0xFFFFFFFFu;   // HF_CHAIN_DEBUG speculation statistics
-#define PH(q) if (dbg) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
+#define PH(q) if (dbga) { unsigned long long n_ = gtimer(); ph[q] += n_ - tp; tp = n_; }
     for (; t < nb;) {
         const int64_t k = a.K0 + t;
         const uint64_t tag = step_tag(att);
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             if (wid == 0) {
                 if (lane == 0) {
                     if (a.xmode == 1) {
-                        unsigned long long *slot = &a.slots[((size_t)par * G + blockIdx.x) * SLOT_STRIDE];
+                        unsigned long long *slot = &a.slots[((size_t)par * G + blockIdx.x) * a.sstride];
                         st_relaxed_u64(slot, (v & ~TAGM) | tag);
                     } else {
                         if (v) red_max_u64(&a.keys[t], v);
@@ -264,13 +266,13 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         // ---- D: wait for all CTAs, read the winning key
         if (a.xmode == 1) {
             if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
-                const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
+                const unsigned long long *sl = a.slots + (size_t)par * G * a.sstride;
                 uint64_t mx;
                 for (;;) {
                     bool ok = true;
                     mx = 0;
                     for (int g = lane; g < G; g += 32) {
-                        const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * SLOT_STRIDE]);
+                        const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * a.sstride]);
                         ok &= (sv & TAGM) == tag;
                         mx = umax64(mx, sv);
                     }
@@ -281,9 +283,9 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
                 if (a.dbg && blockIdx.x == 0) {
                     // speculation statistics: is this step's pivot the runner-up (or third) of
                     // the previous step's per-CTA candidates? (positions; HF_CHAIN_DEBUG only)
-                    const unsigned long long *sl = a.slots + (size_t)par * G * SLOT_STRIDE;
-                    uint64_t v0 = lane < G ? (ld_relaxed_u64(&sl[(size_t)lane * SLOT_STRIDE]) & ~TAGM) : 0;
-                    uint64_t v1 = lane + 32 < G ? (ld_relaxed_u64(&sl[(size_t)(lane + 32) * SLOT_STRIDE]) & ~TAGM) : 0;
+                    const unsigned long long *sl = a.slots + (size_t)par * G * a.sstride;
+                    uint64_t v0 = lane < G ? (ld_relaxed_u64(&sl[(size_t)lane * a.sstride]) & ~TAGM) : 0;
+                    uint64_t v1 = lane + 32 < G ? (ld_relaxed_u64(&sl[(size_t)(lane + 32) * a.sstride]) & ~TAGM) : 0;
                     const uint64_t k1 = warp_max64(umax64(v0, v1));
                     const uint64_t k2 = warp_max64(umax64(v0 < k1 ? v0 : 0, v1 < k1 ? v1 : 0));
                     const uint64_t k3 = warp_max64(umax64(v0 < k2 ? v0 : 0, v1 < k2 ? v1 : 0));
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         for (int q = 0; q < 4; ++q) a.dbg[q] += ph[q];
         a.dbg[4] += t;
     }
+    if (dbga)
+        for (int q = 0; q < 4; ++q) a.dbg[8 + 4 * blockIdx.x + q] += ph[q];
 #undef PH
 }
 
@@ -1029,6 +1033,23 @@ static void lowprec_finish(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_
         unsigned long long hd[8];
         HF_CUDA(cudaMemcpy(hd, dbg->p, sizeof(hd), cudaMemcpyDeviceToHost));
         const double np = hd[4] ? (double)hd[4] : 1.0;
+        {   // per-CTA sums: min / mean / max over the chain CTAs of every phase
+            std::vector<unsigned long long> pc((size_t)4 * ctx->num_sms);
+            HF_CUDA(cudaMemcpy(pc.data(), dbg->p + 8, pc.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            int nact = 0;
+            for (int b = 0; b < ctx->num_sms; ++b) nact += pc[(size_t)4 * b] > 0;
+            for (int q = 0; q < 4; ++q) {
+                double mn = 1e30, mx = 0.0, sm = 0.0;
+                for (int b = 0; b < nact; ++b) {
+                    const double v = pc[(size_t)4 * b + q] / np * 1e-3;
+                    mn = std::min(mn, v);
+                    mx = std::max(mx, v);
+                    sm += v;
+                }
+                fprintf(stderr, "[hf chain] phase %d over %d CTAs: min %.3f mean %.3f max %.3f us/step\n", q, nact, mn,
+                        sm / std::max(nact, 1), mx);
+            }
+        }
         fprintf(stderr, "[hf chain] steps %llu  us/step: publish %.3f  exchange %.3f  fetch %.3f  compute %.3f\n",
                 hd[4], hd[0] / np * 1e-3, hd[1] / np * 1e-3, hd[2] / np * 1e-3, hd[3] / np * 1e-3);
         if (hd[7])
@@ -1126,6 +1147,8 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     xchg.alloc((size_t)nb + 2, st);
     mbox.alloc((size_t)2 * nsm * (nb + 1), st);
     mbox.zero(st);
+    int sstride = SLOT_STRIDE;
+    if (const char *e = getenv("HF_SLOT_STRIDE")) sstride = std::max(1, std::min(64, atoi(e)));
     slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
     slots.zero(st);
     int xmode = 1;
@@ -1178,7 +1201,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     DBuf<unsigned long long> dbg;
     const bool want_dbg = getenv("HF_CHAIN_DEBUG") != nullptr;
     if (want_dbg) {
-        dbg.alloc(8, st);
+        dbg.alloc(8 + 4 * 1024, st);
         dbg.zero(st);
     }
     // buffers of panel p: V[vb] is the matrix at the START of panel p (its position space),
@@ -1200,7 +1223,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ca.S = S[pb].p; ca.Sn = Sn[pb].p; ca.lds = L; ca.sigma = sigma[pb].p; ca.pivpos = pivpos.p;
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
-        ca.slots = slots.p; ca.xmode = xmode;
+        ca.slots = slots.p; ca.xmode = xmode; ca.sstride = sstride;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
         ca.blk = blkd.p; ca.nblk = o_nblk; ca.bstate = bstate.p;
         ca.nbmax = nb;
