@@ -129,6 +129,19 @@ __device__ __forceinline__ float fma_chain(float c, const float *xs, const float
     return c;
 }
 
+// warp max of a 64-bit key (redux.sync on the high then the low word) and the payload
+// of the lane holding it (keys are distinct when non-zero: they carry the position)
+__device__ __forceinline__ void warp_argmax(uint64_t &key, uint32_t &p1, uint32_t &p2) {
+    const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const unsigned win = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
+    const int src = __ffs(win) - 1;
+    p1 = __shfl_sync(0xffffffffu, p1, src);
+    p2 = __shfl_sync(0xffffffffu, p2, src);
+    key = ((uint64_t)mh << 32) | ml;
+}
+
 template <bool SYS>
 __device__ __forceinline__ void st_x_v2(unsigned long long *p, unsigned long long a, unsigned long long b) {
     if (SYS) asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
     bool piv = !has;
     float dprev = a.K0 > 0 ? Dk[a.K0 - 1] : 0.f;
     bool pend = false;
-    float ps = 0.f, pl = 0.f;
+    float ps = 0.f, pc = 0.f, pd = 1.f;   // (L = c / d is formed at the deferred store)
     int t = 0;
     bool stopped = false;
     if (tid == 0) bail = 0;
@@ -243,17 +256,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
         // ---- A: [R3] local argmax over own active rows, carrying (rank, column in the V read)
         uint64_t key = !piv ? dkey(dg, (uint32_t)i) : 0ull;
         uint32_t kinfo = myinfo, klr = (uint32_t)tid;
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) {
-            const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, key, o2);
-            const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, kinfo, o2);
-            const uint32_t ol2 = __shfl_xor_sync(0xffffffffu, klr, o2);
-            if (ok2 > key) {
-                key = ok2;
-                kinfo = oi2;
-                klr = ol2;
-            }
-        }
+        warp_argmax(key, kinfo, klr);
         if (lane == 0) {
             red[wid] = key;
             redi[wid] = kinfo;
@@ -266,17 +269,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
             uint64_t v = (lane < nwarp) ? red[lane] : 0ull;
             uint32_t vinfo = (lane < nwarp) ? redi[lane] : 0u;
             uint32_t vlr = (lane < nwarp) ? redl[lane] : 0u;
-#pragma unroll
-            for (int o2 = 16; o2 > 0; o2 >>= 1) {
-                const uint64_t ok2 = __shfl_xor_sync(0xffffffffu, v, o2);
-                const uint32_t oi2 = __shfl_xor_sync(0xffffffffu, vinfo, o2);
-                const uint32_t ol2 = __shfl_xor_sync(0xffffffffu, vlr, o2);
-                if (ok2 > v) {
-                    v = ok2;
-                    vinfo = oi2;
-                    vlr = ol2;
-                }
-            }
+            warp_argmax(v, vinfo, vlr);
             if (wid == 0) {
                 const unsigned long long w1 =
                     ((unsigned long long)(v ? vinfo : 0u) << 32) | ((unsigned long long)lb << 14) | tag;
@@ -291,7 +284,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
         // ---- deferred global stores of step t-1 (own rows)
         if (pend) {
             Sme[i + (int64_t)(t - 1) * a.lds] = ps;
-            Lor[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            Lor[(int64_t)oi + (k - 1) * a.ldl] = __fdiv_rn(pc, pd);   // [R10], off the critical path
             pend = false;
         }
         PH(1)
@@ -413,7 +406,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
             const float ns = -sg * sv;
             sneg[(size_t)t * a.R + tid] = ns;
             ps = sv;
-            pl = __fdiv_rn(cc, d);
+            pc = cc;
+            pd = d;
             pend = true;
             dg = __fmaf_rn(ns, sv, dg);
         }
@@ -422,7 +416,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
     }
     if (pend) {
         Sme[i + (int64_t)(t - 1) * a.lds] = ps;
-        Lor[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+        Lor[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = __fdiv_rn(pc, pd);
     }
     if (dbgon) {
         for (int q = 0; q < 5; ++q) a.dbg[q] += ph[q];

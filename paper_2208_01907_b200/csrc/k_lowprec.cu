@@ -48,10 +48,13 @@ __device__ __forceinline__ uint64_t mkkey(float d, uint32_t pos) {
 
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
+// unsigned max of a 64-bit key over the warp: two single-instruction reductions
+// (redux.sync) on the high word, then on the low word among the lanes holding it
 __device__ __forceinline__ uint64_t warp_max64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+    const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((uint64_t)mh << 32) | ml;
 }
 
 __device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v) {
@@ -76,7 +79,8 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 
 // c <- fmaf(x_u, y_u, c) for u = 0..n-1 in order [R8]; x_u = xs[u * R] (own row's
 // panel values, shared memory, stride R), y_u = ys[u] (broadcast).  (Issuing the next
-// 8 loads ahead of the current 8 FMAs measured slower: 0.96 vs 0.80 us per C2 pivot.)
+// 8 loads ahead of the current 8 FMAs measured slower, 0.96 and 1.63 vs 0.76 us per
+// C2 pivot: register pressure under the 64-register bound of the 1024-thread launch.)
 __device__ __forceinline__ float fma_chain(float c, const float *xs, const float *ys, int n, int R) {
     int u = 0;
     for (; u + 8 <= n; u += 8) {
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const int32_t myblk = (BLK && has) ? a.blk[oi] : 0;
     // deferred stores of the previous step
     bool pend = false;
-    float ps = 0.f, pn = 0.f, pl = 0.f;
+    float ps = 0.f, pn = 0.f, pc = 0.f, pd = 1.f;   // (L = c / d is formed at the deferred store)
     int t = 0;
     bool stopped = false;
     const bool dbg = a.dbg && blockIdx.x == 0 && tid == 0;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         if (pend) {
             a.S[i + (int64_t)(t - 1) * a.lds] = ps;
             a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
-            a.Lorig[(int64_t)oi + (k - 1) * a.ldl] = pl;
+            a.Lorig[(int64_t)oi + (k - 1) * a.ldl] = __fdiv_rn(pc, pd);   // [R10] L = c / d, off the critical path
             pend = false;
         }
         PH(0)
@@ -372,7 +376,8 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             sneg[(size_t)t * a.R + tid] = ns;
             ps = sv;
             pn = ns;
-            pl = __fdiv_rn(c, d);                       // [R10] L = c / d
+            pc = c;
+            pd = d;
             pend = true;
             dg = __fmaf_rn(ns, sv, dg);                 // lazy diagonal, same fma as the update
         }
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     if (pend) {   // flush the last step's values
         a.S[i + (int64_t)(t - 1) * a.lds] = ps;
         a.Sn[i + (int64_t)(t - 1) * a.lds] = pn;
-        a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = pl;
+        a.Lorig[(int64_t)oi + (a.K0 + t - 1) * a.ldl] = __fdiv_rn(pc, pd);
     }
     if (!stopped && blockIdx.x == 0 && tid == 0) a.status[1] = t;
     if (BLK && blockIdx.x == 0 && tid == 0) {
@@ -695,7 +700,27 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
     float2 acc[8][4];
-    {
+    // an interior tile (strictly below the diagonal, no ragged edge; every tile but the edges
+    // for NS): all 64 seeds exist, so no masks; the column bases are computed once and kept
+    // as 64-bit pointers for the row offsets (fewer FMA-pipe IMADs and parameter reloads)
+    const bool interior = (NS || row0 > col0) && mpr == TB && mpc == TB;
+    if (interior) {
+        int32_t rm[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
+        const float *vold = a.Vold;
+        const int64_t ldv = a.ldv;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float *c0p = vold + (int64_t)cmap[CC(2 * j)] * ldv;
+            const float *c1p = vold + (int64_t)cmap[CC(2 * j + 1)] * ldv;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                acc[q][j].x = __ldg(c0p + rm[q]);
+                acc[q][j].y = __ldg(c1p + rm[q]);
+            }
+        }
+    } else {
         int32_t rm[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
