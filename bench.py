@@ -432,6 +432,16 @@ def main():
             "traffic": traffic.get("bytes_per_launch") if traffic else None,
             "traffic_note": traffic.get("note") if traffic else "no ncu capture committed yet",
             "flops_per_step": tr_fl, "ms_per_step": tr_ms, "launches_per_step": klaunch["trailing"]}
+    # ---- the chain's floor: its grid-wide exchange alone, in the geometry libhf picks
+    # (k_lowprec.cu: max(64, L / rows-that-fit) CTAs, at most one per SM; one thread per row)
+    xfloor = None
+    if world == 1 or args.mode == "replicas":
+        try:
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            g_ct = min(nsm, max(64, -(-L // 358)), max(1, -(-L // 32)))
+            xfloor = ctx.chain_exchange_floor(g_ct, -(-(-(-L // g_ct)) // 32) * 32, 8192)
+        except Exception:
+            xfloor = None
     # ---- the other kernels' own rooflines
     dg_ms, ts_ms, ch_ms = kms["dgemm"], kms["trsm"], kms["chain"]
     dmma_ach = fm["dmma"] / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
@@ -452,6 +462,11 @@ def main():
                  "setup_ms_per_step": kms["trsm_setup"]},
         "chain": {"kernel": "k_chain (cooperative persistent pivot chain, one launch per panel)",
                   "bound": "latency", "us_per_pivot": ch_ms * 1e3 / max(Ntau, 1), "ms_per_step": ch_ms,
+                  "exchange_floor_us": xfloor, "frac_of_floor": (xfloor / (ch_ms * 1e3 / max(Ntau, 1)))
+                  if (xfloor and ch_ms > 0) else None,
+                  "floor_note": "the chain's grid-wide exchange alone (hf_chain_exchange_floor: block key "
+                                "reduction + tagged slot store + poll of every slot, same CTA geometry, no column "
+                                "fetch, no arithmetic), measured live after the timed region",
                   "hbm_gbs": kwork["chain"][1] / (ch_ms * 1e-3) / 1e9 if ch_ms > 0 else None,
                   "bytes_per_step": kwork["chain"][1]},
     }

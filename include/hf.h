@@ -112,6 +112,12 @@ hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host);
  * "trsm", 2 M N K per product for "dgemm"); 0 for classes that do not report it.
  * Cumulative like hf_kernel_stats. */
 hf_status hf_kernel_work(hf_ctx *ctx, const char *kernel_class, double *flops_host, double *bytes_host);
+/* Instrumentation (the pivot chain's roofline): microseconds per step of the chain's
+ * grid-wide exchange ALONE -- nctas cooperative CTAs of nthreads threads, per step a
+ * block max-reduction of a key, one tag-validated slot store per CTA and a poll of every
+ * slot -- with no column fetch and no arithmetic.  The floor under the chain's per-pivot
+ * time for that geometry. */
+hf_status hf_chain_exchange_floor(hf_ctx *ctx, int nctas, int nthreads, int steps, double *us_per_step_host);
 /* Device workspaces and handle buffers come from a per-(device, stream) cache
  * that reuses freed blocks in stream order (no memory is re-mapped by a
  * repeated factorization); this synchronises the device and returns every

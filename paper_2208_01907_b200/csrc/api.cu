@@ -164,6 +164,11 @@ hf_status hf_kernel_work(hf_ctx *ctx, const char *cls, double *flops_host, doubl
     });
 }
 
+hf_status hf_chain_exchange_floor(hf_ctx *ctx, int nctas, int nthreads, int steps, double *us_per_step_host) {
+    if (!ctx || !us_per_step_host || nctas < 1 || steps < 1) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] { *us_per_step_host = hf::chain_exchange_floor(ctx, nctas, nthreads, steps); });
+}
+
 hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host) {
     if (!ctx || !launches_host) return HF_ERR_INVALID_ARG;
     *launches_host = ctx->launches;

@@ -273,6 +273,7 @@ void launch_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int 
 void launch_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, int *bad_flag);   // NEXT-3
 void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,
                     hf_lowfactor *lf, const int32_t *blk_host = nullptr, int nblk = 0);
+double chain_exchange_floor(hf_ctx *ctx, int nctas, int nthreads, int steps);
 void lowprec_outputs(hf_ctx *ctx, int64_t L, const hf_lowprec_opts &o, hf_lowfactor *lf, const int32_t *status,
                      const int32_t *pivorig, const float *Dk);
 void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const hf_lowprec_opts &o,

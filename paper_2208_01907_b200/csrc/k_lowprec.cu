@@ -411,6 +411,52 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
 #undef PH
 }
 
+// ------------------------------------------------------------------ exchange floor
+// The chain's grid-wide step with nothing else in it (instrumentation, the chain's
+// roofline): per step every CTA reduces a key over its threads (warp redux + shared
+// memory, as phase A), one thread stores it into its spread slot (phase B) and warp 0
+// polls every slot until all carry the step's tag (phase D), then a block barrier.
+__global__ void __launch_bounds__(1024, 1) k_xchg_floor(unsigned long long *slots, int sstride, int steps,
+                                                       unsigned long long *out) {
+    __shared__ unsigned long long red[32], bkey;
+    const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+    unsigned long long acc = 0;
+    const unsigned long long t0 = gtimer();
+    for (int t = 0; t < steps; ++t) {
+        const uint64_t tag = step_tag(t);
+        const int par = t & 1;
+        uint64_t key = mkkey((float)((tid * 7 + t * 13 + blockIdx.x) & 1023), (uint32_t)(blockIdx.x * 1024 + tid));
+        key = warp_max64(key);
+        if (lane == 0) red[wid] = key;
+        __syncthreads();
+        if (wid == 0) {
+            uint64_t v = lane < nwarp ? red[lane] : 0ull;
+            v = warp_max64(v);
+            if (lane == 0) st_relaxed_u64(&slots[((size_t)par * G + blockIdx.x) * sstride], (v & ~TAGM) | tag);
+            const unsigned long long *sl = slots + (size_t)par * G * sstride;
+            uint64_t mx;
+            for (;;) {
+                bool ok = true;
+                mx = 0;
+                for (int g = lane; g < G; g += 32) {
+                    const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * sstride]);
+                    ok &= (sv & TAGM) == tag;
+                    mx = umax64(mx, sv);
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+            }
+            mx = warp_max64(mx);
+            if (lane == 0) bkey = mx;
+        }
+        __syncthreads();
+        acc += bkey & 1;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        out[0] = gtimer() - t0;
+        out[1] = acc;
+    }
+}
+
 // ------------------------------------------------------------------ compaction
 // map[j'] = old position of the j'-th surviving index (stable), norig likewise.
 __global__ void k_compact(int64_t m, int nbp, const int32_t *__restrict__ pivpos,
@@ -451,6 +497,7 @@ struct TrailArgs {
     const float *Sn;       // Sn[old + t*lds]   = -sigma_t s_i^t
     int64_t lds;
     const int32_t *status;
+    int64_t ntiles;        // k_trailing_c: tiles of the launch (persistent CTAs)
     const float *Sc;       // Sc[t*ldc + new]  = s^t of the row at NEW position (compacted panel)
     const float *Snc;      // Snc[t*ldc + new] = -sigma_t s^t
     int64_t ldc;           // multiple of 4; >= the padded tile extent
@@ -646,21 +693,39 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t);
     float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t + TNS * TK * TB);
     __shared__ int32_t rmap[TB], cmap[TB];
-
-    const int64_t t = blockIdx.x;
-    int64_t bi, bj;
-    if (NS) {
-        const int64_t T = (a.mp + TB - 1) / TB;
-        bi = t % T;
-        bj = t / T;
-    } else {
-        bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-        while (bi * (bi + 1) / 2 > t) --bi;
-        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-        bj = t - bi * (bi + 1) / 2;
-    }
-    const int64_t row0 = bi * TB, col0 = bj * TB;
+    // persistent: CTA b takes tiles b, b + grid, ... (the order of the one-tile-per-CTA
+    // launch); the next tile's compaction-map entry is loaded into a register while the
+    // current tile computes, so a tile's seed gather waits for one memory latency, not two
+    auto tile_of = [&](int64_t t, int64_t &bi, int64_t &bj) {
+        if (NS) {
+            const int64_t T = (a.mp + TB - 1) / TB;
+            bi = t % T;
+            bj = t / T;
+        } else {
+            bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while (bi * (bi + 1) / 2 > t) --bi;
+            while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+            bj = t - bi * (bi + 1) / 2;
+        }
+    };
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    auto map_entry = [&](int64_t t) -> int32_t {   // this thread's rmap / cmap entry of tile t
+        int64_t bi, bj;
+        tile_of(t, bi, bj);
+        const int64_t base = (tid < TB ? bi : bj) * TB + (tid & (TB - 1));
+        return base < a.mp ? a.map[base] : -1;
+    };
+    int64_t t = blockIdx.x;
+    if (t >= a.ntiles) return;
+    {
+        const int32_t m0 = map_entry(t);
+        if (tid < TB) rmap[tid] = m0;
+        else cmap[tid - TB] = m0;
+    }
+    for (;;) {
+    int64_t bi, bj;
+    tile_of(t, bi, bj);
+    const int64_t row0 = bi * TB, col0 = bj * TB;
     const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
     const int nchunk = (a.nbp + TK - 1) / TK;
 
@@ -692,10 +757,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     };
     issue(0);
     issue(1);
-
-    if (tid < TB) rmap[tid] = (tid < mpr) ? a.map[row0 + tid] : -1;
-    else cmap[tid - TB] = (tid - TB < mpc) ? a.map[col0 + tid - TB] : -1;
-    __syncthreads();
+    __syncthreads();   // this tile's maps (stored before the loop or at the end of the previous tile)
 
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
 #define CC(q) (((q) < 4) ? ty * 4 + (q) : 64 + ty * 4 + ((q)-4))
@@ -741,6 +803,8 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
         }
     }
 
+    const int64_t tn = t + gridDim.x;
+    const int32_t mnext = tn < a.ntiles ? map_entry(tn) : -1;   // consumed after the main loop
     int st = 0;   // stage of chunk c
     for (int c = 0; c < nchunk; ++c, st = (st == TNS - 1) ? 0 : st + 1) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -801,6 +865,12 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
                 }
             }
         }
+    }
+    __syncthreads();   // every thread is done with this tile's maps and operand stages
+    if (tn >= a.ntiles) break;
+    if (tid < TB) rmap[tid] = mnext;
+    else cmap[tid - TB] = mnext;
+    t = tn;
     }
 #undef RR
 #undef CC
@@ -1201,6 +1271,14 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
 
     HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    // k_trailing_c: one tile per CTA (default) or persistent CTAs, occupancy x SMs, each
+    // prefetching its next tile's compaction map while the current one computes
+    // (HF_TRAIL_PCTA=1; measured slower: C2 32.0 vs 29.7 ms, C4 1926 vs 1780 ms per
+    // factorization -- the hardware's CTA launch overlaps the next tile's prologue better)
+    int cocc = 0;
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cocc, k_trailing_c<false>, 256, TRAIL_C_SMEM));
+    const bool trail_pcta = getenv("HF_TRAIL_PCTA") && atoi(getenv("HF_TRAIL_PCTA")) != 0;
+    const int64_t cgrid = trail_pcta ? (int64_t)std::max(1, cocc) * nsm : INT64_MAX;
     // persistent trailing kernel (seed prefetch), two CTAs per SM -- OFF by default: measured
     // 38.3 vs 31.0 ms per C2 step (FMA pipe 64.8 vs 71.5 % active; the 4-byte cp.async seed
     // gather adds 155 MB of DRAM reads per large launch and leaves fewer warps resident).
@@ -1280,11 +1358,12 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
             // writes the start of panel p into the other buffer, and this one then turns it
             // into the start of panel p+1 in V[vb], which the next chain no longer needs.
             TrailArgs ta;
-            ta.mp = mp; ta.nbp = nbp; ta.ldv = L;
+            ta.mp = mp; ta.nbp = nbp; ta.ldv = L; ta.ntiles = 0;
             ta.map = map[pb].p; ta.S = S[pb].p; ta.Sn = Sn[pb].p; ta.lds = L; ta.status = status.p;
             ta.Sc = Sc.p; ta.Snc = Snc.p; ta.ldc = ldc;
             const int64_t T = cdiv(mp, TB);
             const int64_t ntiles = T * (T + 1) / 2;
+            ta.ntiles = ntiles;
             if (!look) {
                 ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
                 if (Sc.p) {
@@ -1297,7 +1376,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 if (Sc.p && persist && (ntiles > 2 * pgrid || pmode == 2)) {
                     k_trailing_p<<<(unsigned)pgrid, 256, TRAIL_P_SMEM, st>>>(ta, ntiles);
                 } else if (Sc.p) {
-                    k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st>>>(ta);
+                    k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
                 } else {
                     k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 }
@@ -1317,7 +1396,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 }
                 {
                     ClassTimer tm(ctx, "trailing", st2, trail_flops(mp, nbp), trail_bytes(mp, nbp));
-                    k_trailing_c<false><<<(unsigned)ntiles, 256, TRAIL_C_SMEM, st2>>>(ta);
+                    k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st2>>>(ta);
                     HF_CHECK_LAUNCH(ctx);
                 }
                 // the next chain reads the start of panel p (vsrc); before it runs, the trailing
@@ -1619,7 +1698,7 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
                 HF_CHECK_LAUNCH(ctx);
             }
             TrailArgs ta;
-            ta.mp = mp; ta.nbp = nbp; ta.ldv = L; ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L;
+            ta.mp = mp; ta.nbp = nbp; ta.ldv = L; ta.ntiles = cdiv(mp, TB) * cdiv(mp, TB); ta.map = map.p; ta.S = S.p; ta.Sn = Sn.p; ta.lds = L;
             ta.status = status.p; ta.Sc = Sc.p; ta.Snc = Snc.p; ta.ldc = ldc;
             ta.Vold = V[cur].p; ta.Vnew = V[cur ^ 1].p;
             const int64_t T = cdiv(mp, TB);
@@ -1646,4 +1725,25 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
     HF_CUDA(cudaStreamSynchronize(st));
 }
 
+}  // namespace hf
+
+namespace hf {
+// microseconds per exchange step of the chain's grid-wide exchange alone
+double chain_exchange_floor(hf_ctx *ctx, int nctas, int nthreads, int steps) {
+    cudaStream_t st = ctx->stream;
+    nctas = std::max(1, std::min(nctas, ctx->num_sms));
+    nthreads = std::max(32, std::min(1024, (nthreads + 31) / 32 * 32));
+    DBuf<unsigned long long> slots, out;
+    slots.alloc((size_t)2 * nctas * SLOT_STRIDE, st);
+    slots.zero(st);
+    out.alloc(2, st);
+    int ss = SLOT_STRIDE;
+    void *args[] = {&slots.p, &ss, &steps, &out.p};
+    HF_CUDA(cudaLaunchCooperativeKernel((void *)k_xchg_floor, dim3((unsigned)nctas), dim3(nthreads), args, 0, st));
+    HF_CHECK_LAUNCH(ctx);
+    unsigned long long h[2];
+    HF_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    HF_CUDA(cudaStreamSynchronize(st));
+    return (double)h[0] * 1e-3 / std::max(steps, 1);
+}
 }  // namespace hf

@@ -25,7 +25,7 @@ _NAMES = {0: "HF_OK", 1: "HF_ERR_INVALID_ARG", 2: "HF_ERR_CUDA", 3: "HF_ERR_NCCL
 
 EXPORTED = [
     "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
-    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
+    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
         "hf_set_profiling": [vp, ctypes.c_int],
         "hf_kernel_stats": [vp, ctypes.c_char_p, pdbl, pi64],
         "hf_kernel_work": [vp, ctypes.c_char_p, pdbl, pdbl],
+        "hf_chain_exchange_floor": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, pdbl],
         "hf_launch_count": [vp, pi64],
         "hf_scale": [vp, i64, vp, i64, vp],
         "hf_scale_full": [vp, i64, vp, i64, vp],
@@ -198,6 +199,12 @@ class Context:
         fl, by = ctypes.c_double(), ctypes.c_double()
         self.check(self.lib.hf_kernel_work(self.h, cls.encode(), ctypes.byref(fl), ctypes.byref(by)))
         return fl.value, by.value
+
+    def chain_exchange_floor(self, nctas: int, nthreads: int, steps: int = 4096) -> float:
+        """us per step of the chain's grid-wide exchange alone (instrumentation)."""
+        us = ctypes.c_double()
+        self.check(self.lib.hf_chain_exchange_floor(self.h, int(nctas), int(nthreads), int(steps), ctypes.byref(us)))
+        return us.value
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()
