@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
             if (wid == 0) {
                 const unsigned long long w1 =
                     ((unsigned long long)(v ? vinfo : 0u) << 32) | ((unsigned long long)lb << 14) | tag;
-                for (int q = lane; q < a.G; q += 32)   // one slot per CTA in every rank's array
+                // one slot per CTA in every rank's array (emulated ranks share one array: one
+                // store, as each real rank's poll of its own array sees one store per CTA)
+                for (int q = lane; q < (SYS ? a.G : 1); q += 32)
                     st_x_v2<SYS>(sSl[q] + ((size_t)par * GT + gid) * DSLOT, (v & ~DTAGM) | tag, w1);
             } else if (v) {
                 unsigned long long *mb = mbme + ((size_t)par * a.Cper + lb) * (a.nbmax + 1);
@@ -681,7 +683,25 @@ __global__ void __launch_bounds__(256, 2) k_trailing_d(DTrailArgs a) {
         }
         __syncthreads();
         float2 acc[8][4];
-        {
+        // an interior tile (full, every row at or below every column's position): all 64
+        // seeds exist, unmasked gathers (as in k_trailing_c)
+        if (mpr == DTB && mpc == DTB && row0 >= cpos[DTB - 1]) {
+            int32_t rm[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
+            const float *vold = a.Vold;
+            const int64_t ldp = a.ldp;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float *c0p = vold + (int64_t)cmap[CC(2 * j)] * ldp;
+                const float *c1p = vold + (int64_t)cmap[CC(2 * j + 1)] * ldp;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    acc[q][j].x = __ldg(c0p + rm[q]);
+                    acc[q][j].y = __ldg(c1p + rm[q]);
+                }
+            }
+        } else {
             int32_t rm[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) rm[q] = rmap[RR(q)];
@@ -941,6 +961,8 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         r.Dk = b.Dk.p; r.pivorig = b.pivorig.p; r.status = b.status.p;
         r.map = b.map.p; r.tiles = b.tiles.p; r.Sc = b.Sc.p; r.Snc = b.Snc.p; r.Scol = b.Scol.p; r.bar = b.bar.p;
     }
+    if (!real)   // emulated ranks share one slot array (see k_chain_d's publish)
+        for (int h = lo; h < hi; ++h) tab[h].slots = B[lo].slots.p;
     // the factor rows by original index: one per rank on a real run, shared when emulated
     Lorig_all.alloc((size_t)L * L, st);
     for (int h = lo; h < hi; ++h) tab[h].Lorig = Lorig_all.p;
