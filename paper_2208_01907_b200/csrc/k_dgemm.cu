@@ -157,8 +157,18 @@ __global__ void k_reduce(DgemmArgs g, int splits) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t gm = e % g.M, gn = e / g.M;
+        // the partials are summed in split order (deterministic); their loads are issued
+        // eight at a time ahead of the adds so their latencies overlap
         double s = 0.0;
-        for (int z = 0; z < splits; ++z) s += g.W[(size_t)z * total + e];
+        int z = 0;
+        for (; z + 8 <= splits; z += 8) {
+            double w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u] = __ldcs(&g.W[(size_t)(z + u) * total + e]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += w[u];
+        }
+        for (; z < splits; ++z) s += __ldcs(&g.W[(size_t)z * total + e]);
         const bool keep = !g.rowmask || g.rowmask[gm];
         double *c = g.C + gm + gn * g.ldc;
         const double ab = keep ? __dmul_rn(g.alpha, s) : 0.0;
