@@ -24,6 +24,11 @@ measured on ONE B200 (this run has no multi-GPU box): VERDICT r01 item 2.
     device-side NVLink barrier (one remote atomic + poll); remote_p = m_p nbp 4 B
     (G-1)/G (the panel broadcast).
 
+  full hybrid (Alg. 1 steps 1-5): scale + stage 1 (model above) + stage 2 sharded over the
+    right-hand sides (each rank's block GCR + S22 slice timed ALONE on this GPU through
+    hf_set_virtual_rank: what it runs on its own GPU) + the S22 / X12 slice broadcast at BW +
+    the replicated hard factorization.
+
     python tools/dist_model.py [config=C4] [G list=2,4,8] > profiles/dist_model_r02.json
 """
 import hashlib
@@ -82,6 +87,47 @@ def worker(name, G, mode):
     print(json.dumps(out), flush=True)
 
 
+def worker_stage2(name, Gs):
+    """Stage 2 (block GCR + S22 slice) of the RHS-sharded multi-GPU path: each rank's own
+    slice measured alone on this GPU (hf_set_virtual_rank), ranks 0 and G-1; G = 1 is the
+    one-GPU stage 2.  Also the one-GPU scale and hard-factor times."""
+    import torch
+    import hf_inputs as hi
+    from paper_2208_01907_b200 import hf
+    spec = hi.CONFIGS[name]
+    K = hi.make_kbar(name, 0, device="cuda")
+    ctx = hf.Context(0)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    hf.hf_scale(ctx, K)
+    e[1].record()
+    torch.cuda.synchronize()
+    scale_ms = e[0].elapsed_time(e[1])
+    lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=spec.n_min)
+    out = {"scale_ms": scale_ms, "n2": lf.n2, "stage2": {}}
+    for G in Gs:
+        per = []
+        for r in ([0, G - 1] if G > 1 else [0]):
+            hf.hf_set_virtual_rank(ctx, r, G) if G > 1 else hf.hf_set_virtual_rank(ctx, 0, 0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            hy, info, _ = hf.hf_schur_gcr(ctx, K, lf, accept_failure=True)
+            e1.record()
+            torch.cuda.synchronize()
+            per.append({"rank": r, "iters": info.iters, "true_res": info.max_rel_res_true,
+                        "ms": e0.elapsed_time(e1)})
+            if G == 1:
+                e0.record()
+                hf.hf_factor_hard(ctx, hy)
+                e1.record()
+                torch.cuda.synchronize()
+                out["hard_ms"] = e0.elapsed_time(e1)
+            hy.close()
+        out["stage2"][G] = per
+    hf.hf_set_virtual_rank(ctx, 0, 0)
+    print(json.dumps(out), flush=True)
+
+
 def run(name, G, mode):
     env = dict(os.environ, HF_DIST_LOOKAHEAD=str(mode), HF_DIST_PANEL_TIMES="1")
     r = subprocess.run([sys.executable, os.path.abspath(__file__), "--worker", name, str(G), str(mode)],
@@ -135,6 +181,8 @@ def model(res1, resG, L, G, look):
 def main():
     if sys.argv[1:2] == ["--worker"]:
         return worker(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
+    if sys.argv[1:2] == ["--stage2"]:
+        return worker_stage2(sys.argv[2], [int(x) for x in sys.argv[3].split(",")])
     name = sys.argv[1] if len(sys.argv) > 1 else "C4"
     Gs = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,4,8").split(",")]
     import hf_inputs as hi
@@ -154,6 +202,25 @@ def main():
                        "serial": dict(ms_, speedup=one["ms"] / ms_["model_ms"], emul_total_ms=rs["ms"]),
                        "lookahead": dict(ml_, speedup=one["ms"] / ml_["model_ms"], emul_total_ms=rl["ms"])}
         print(json.dumps({G: res["G"][G]}), file=sys.stderr, flush=True)
+    # the whole hybrid factorization (Alg. 1 steps 1-5): stage 2 sharded over the right-hand
+    # sides (each rank's slice timed alone on this GPU, the slower of ranks 0 and G-1), the
+    # S22 / X12 slices broadcast at 770 GB/s, scale and hard factor replicated
+    r2 = subprocess.run([sys.executable, os.path.abspath(__file__), "--stage2", name,
+                         ",".join(str(g) for g in [1] + Gs)], capture_output=True, text=True, timeout=1800)
+    if r2.returncode == 0:
+        s2 = json.loads(r2.stdout.strip().splitlines()[-1])
+        n2 = s2["n2"]
+        t1_full = s2["scale_ms"] + one["ms"] + s2["stage2"]["1"][0]["ms"] + s2.get("hard_ms", 0.0)
+        res["full_hybrid"] = {"one_gpu_ms": t1_full, "scale_ms": s2["scale_ms"], "hard_ms": s2.get("hard_ms"),
+                              "stage2_one_gpu": s2["stage2"]["1"], "G": {}}
+        for G in Gs:
+            st2 = max(p["ms"] for p in s2["stage2"][str(G)])
+            slices = (n2 * n2 + float(hi.CONFIGS[name].L - n2) * n2) * 8.0 * (G - 1) / G   # S22 + X12 slices
+            tG = s2["scale_ms"] + res["G"][G]["serial"]["model_ms"] + st2 + slices / BW * 1e3 + s2.get("hard_ms", 0.0)
+            res["full_hybrid"]["G"][G] = {"stage2_per_rank": s2["stage2"][str(G)], "stage2_ms": st2,
+                                          "slice_exchange_ms": slices / BW * 1e3, "model_ms": tG,
+                                          "speedup": t1_full / tG}
+        print(json.dumps({"full_hybrid": res["full_hybrid"]}), file=sys.stderr, flush=True)
     print(json.dumps(res), flush=True)
 
 
