@@ -135,6 +135,7 @@ struct ChainArgs {
     unsigned int *cnt;           // arrival counter (zeroed before the launch)          (xmode 0)
     unsigned long long *slots;   // [2][G][sstride] per-CTA key | step tag (xmode 1)
     int sstride;                 // words between two CTAs' slots (HF_SLOT_STRIDE; 32 = one L2 line each)
+    int spec;                    // prefetch the runner-up candidates' columns (HF_CHAIN_SPEC, xmode 1, no blocks)
     int xmode;                   // 0: red.max + counter; 1: spread LL slots (HF_CHAIN_XCHG)
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
     __shared__ unsigned long long bkey;
+    __shared__ int32_t spec_p[2];   // speculative next-pivot positions (a.spec)
     if (*(volatile int32_t *)&a.status[2]) return;   // uniform: set by an earlier launch
     const int G = gridDim.x;
     const int tid = threadIdx.x, nthr = blockDim.x, nwarp = nthr >> 5, lane = tid & 31, wid = tid >> 5;
@@ -269,6 +271,28 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         PH(0)
         // ---- D: wait for all CTAs, read the winning key
         if (a.xmode == 1) {
+            if (wid == 1 && a.spec) {
+                // speculation: the runner-up and third of this step's per-CTA candidates are
+                // the likeliest next pivots (C2: 22 / 33 %); their column entries of this
+                // CTA's rows are prefetched into L2 after the barrier (warp 1 polls the same
+                // slots as warp 0 and ranks them, off warp 0's path)
+                const unsigned long long *sl = a.slots + (size_t)par * G * a.sstride;
+                uint64_t v0, v1;
+                for (;;) {
+                    v0 = lane < G ? ld_relaxed_u64(&sl[(size_t)lane * a.sstride]) : tag;
+                    v1 = lane + 32 < G ? ld_relaxed_u64(&sl[(size_t)(lane + 32) * a.sstride]) : tag;
+                    if (__all_sync(0xffffffffu, ((v0 & TAGM) == tag) && ((v1 & TAGM) == tag))) break;
+                }
+                v0 = lane < G ? (v0 & ~TAGM) : 0;
+                v1 = lane + 32 < G ? (v1 & ~TAGM) : 0;
+                const uint64_t k1 = warp_max64(umax64(v0, v1));
+                const uint64_t k2 = warp_max64(umax64(v0 < k1 ? v0 : 0, v1 < k1 ? v1 : 0));
+                const uint64_t k3 = warp_max64(umax64(v0 < k2 ? v0 : 0, v1 < k2 ? v1 : 0));
+                if (lane == 0) {
+                    spec_p[0] = k2 ? (int32_t)(POS_MAX - (uint32_t)((k2 >> 15) & POS_MAX)) : -1;
+                    spec_p[1] = k3 ? (int32_t)(POS_MAX - (uint32_t)((k3 >> 15) & POS_MAX)) : -1;
+                }
+            }
             if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
                 const unsigned long long *sl = a.slots + (size_t)par * G * a.sstride;
                 uint64_t mx;
@@ -358,6 +382,17 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             if (tid == 0) sgm[t] = sg;
         }
         __syncthreads();
+        if (a.spec && !piv) {   // L2 prefetch of this row's entries of the speculative next pivots
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int32_t ps_ = spec_p[q];
+                if (ps_ >= 0 && ps_ != (int32_t)P && ps_ < a.m) {
+                    const int64_t pso = a.mapprev ? (int64_t)a.mapprev[ps_] : ps_;
+                    const float *pp = (io >= pso) ? (a.V + io + pso * a.ldv) : (a.V + pso + io * a.ldv);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pp));
+                }
+            }
+        }
         PH(2)
         // ---- G: column, scaled column, lazy diagonal
         const float r = __fsqrt_rn(absd);               // [R7]
@@ -1243,6 +1278,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     mbox.alloc((size_t)2 * nsm * (nb + 1), st);
     mbox.zero(st);
     int sstride = SLOT_STRIDE;
+    // HF_CHAIN_SPEC=1: L2 prefetch of the runner-up candidates' columns (measured slower at C2:
+    // chain 53.3 vs 51.5 ms -- a 22-33 % hit rate does not pay for the extra poll and traffic)
+    int chain_spec = 0;
+    if (const char *e = getenv("HF_CHAIN_SPEC")) chain_spec = atoi(e);
     if (const char *e = getenv("HF_SLOT_STRIDE")) sstride = std::max(1, std::min(64, atoi(e)));
     slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
     slots.zero(st);
@@ -1327,6 +1366,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ca.Lorig = Lorig.p; ca.ldl = L; ca.Dk = Dk.p; ca.pivorig = pivorig.p;
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
         ca.slots = slots.p; ca.xmode = xmode; ca.sstride = sstride;
+        ca.spec = (xmode == 1 && !blk_host && G <= 64) ? chain_spec : 0;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
         ca.blk = blkd.p; ca.nblk = o_nblk; ca.bstate = bstate.p;
         ca.nbmax = nb;
