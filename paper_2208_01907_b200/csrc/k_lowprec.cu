@@ -136,6 +136,7 @@ struct ChainArgs {
     unsigned long long *slots;   // [2][G][sstride] per-CTA key | step tag (xmode 1)
     int sstride;                 // words between two CTAs' slots (HF_SLOT_STRIDE; 32 = one L2 line each)
     int spec;                    // prefetch the runner-up candidates' columns (HF_CHAIN_SPEC, xmode 1, no blocks)
+    int dpoll;                   // two poll rounds in flight (HF_CHAIN_DPOLL)
     int xmode;                   // 0: red.max + counter; 1: spread LL slots (HF_CHAIN_XCHG)
     unsigned long long *mbox;    // [2][G][nb] candidate-row values: float bits << 32 | step tag
     int32_t *status;    // [0] Ntau if stopped, [1] pivots done in last panel, [2] stopped
@@ -296,15 +297,39 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             if (wid == 0) {   // every slot of this step (tags), max = the pivot key; no fence needed
                 const unsigned long long *sl = a.slots + (size_t)par * G * a.sstride;
                 uint64_t mx;
-                for (;;) {
-                    bool ok = true;
-                    mx = 0;
-                    for (int g = lane; g < G; g += 32) {
-                        const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * a.sstride]);
-                        ok &= (sv & TAGM) == tag;
-                        mx = umax64(mx, sv);
+                if (G <= 64 && a.dpoll) {
+                    // two poll rounds in flight (the second issued half a round trip after the
+                    // first), so the last slot's arrival is seen sooner; G <= 64: two slots per lane
+                    const unsigned long long *s0 = &sl[(size_t)lane * a.sstride];
+                    const unsigned long long *s1 = &sl[(size_t)(lane + 32) * a.sstride];
+                    const bool h0 = lane < G, h1 = lane + 32 < G;
+                    uint64_t a0 = h0 ? ld_relaxed_u64(s0) : tag, a1 = h1 ? ld_relaxed_u64(s1) : tag;
+                    uint64_t b0 = h0 ? ld_relaxed_u64(s0) : tag, b1 = h1 ? ld_relaxed_u64(s1) : tag;
+                    for (;;) {
+                        if (__all_sync(0xffffffffu, ((a0 & TAGM) == tag) && ((a1 & TAGM) == tag))) {
+                            mx = umax64(h0 ? a0 : 0, h1 ? a1 : 0);
+                            break;
+                        }
+                        a0 = h0 ? ld_relaxed_u64(s0) : tag;
+                        a1 = h1 ? ld_relaxed_u64(s1) : tag;
+                        if (__all_sync(0xffffffffu, ((b0 & TAGM) == tag) && ((b1 & TAGM) == tag))) {
+                            mx = umax64(h0 ? b0 : 0, h1 ? b1 : 0);
+                            break;
+                        }
+                        b0 = h0 ? ld_relaxed_u64(s0) : tag;
+                        b1 = h1 ? ld_relaxed_u64(s1) : tag;
                     }
-                    if (__all_sync(0xffffffffu, ok)) break;
+                } else {
+                    for (;;) {
+                        bool ok = true;
+                        mx = 0;
+                        for (int g = lane; g < G; g += 32) {
+                            const uint64_t sv = ld_relaxed_u64(&sl[(size_t)g * a.sstride]);
+                            ok &= (sv & TAGM) == tag;
+                            mx = umax64(mx, sv);
+                        }
+                        if (__all_sync(0xffffffffu, ok)) break;
+                    }
                 }
                 mx = warp_max64(mx);
                 if (lane == 0) bkey = mx;
@@ -1282,6 +1307,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     // chain 53.3 vs 51.5 ms -- a 22-33 % hit rate does not pay for the extra poll and traffic)
     int chain_spec = 0;
     if (const char *e = getenv("HF_CHAIN_SPEC")) chain_spec = atoi(e);
+    // HF_CHAIN_DPOLL=1: two poll rounds in flight (measured 52.5 vs 52.1 ms chain at C2: off)
+    int chain_dpoll = 0;
+    if (const char *e = getenv("HF_CHAIN_DPOLL")) chain_dpoll = atoi(e);
     if (const char *e = getenv("HF_SLOT_STRIDE")) sstride = std::max(1, std::min(64, atoi(e)));
     slots.alloc((size_t)2 * nsm * SLOT_STRIDE, st);
     slots.zero(st);
@@ -1367,6 +1395,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         ca.keys = xchg.p; ca.cnt = reinterpret_cast<unsigned int *>(xchg.p + nb); ca.mbox = mbox.p;
         ca.slots = slots.p; ca.xmode = xmode; ca.sstride = sstride;
         ca.spec = (xmode == 1 && !blk_host && G <= 64) ? chain_spec : 0;
+        ca.dpoll = chain_dpoll;
         ca.status = status.p; ca.dbg = want_dbg ? dbg.p : nullptr;
         ca.blk = blkd.p; ca.nblk = o_nblk; ca.bstate = bstate.p;
         ca.nbmax = nb;
