@@ -862,7 +862,13 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         lf->N = lf->Ntau = lf->n2 = 0;
         return;
     }
-    const bool real = ctx->nranks > 1;
+    // real ranks: a multi-GPU context, or a one-rank NCCL context asked for one partition
+    // (the real-rank code path -- IPC handles over NCCL, device barrier, system-scope
+    // exchange -- on a single GPU, for the tests; there are no peers to map)
+    bool real = ctx->nranks > 1;
+#ifdef HF_WITH_NCCL
+    if (ctx->comm && ctx->nranks == 1 && nparts == 1) real = true;
+#endif
     const int G = real ? ctx->nranks : nparts;
     HF_REQUIRE(L <= (int64_t)DPOS_MAX - 1, "L too large for the 17-bit position key");
     HF_REQUIRE(G >= 1 && G <= 64, "stage-1 ranks out of range (1..64)");

@@ -137,3 +137,32 @@ def test_stage1_distributed_c2_equals_one_gpu(ctx, G, look, monkeypatch):
     pG, DG, LG = lfG.export()
     assert np.array_equal(p1, pG) and np.array_equal(D1, DG)
     assert torch.equal(L1, LG)
+
+
+@pytest.mark.parametrize("look", [0, 1])
+def test_stage1_real_rank_path_one_gpu(look, monkeypatch):
+    """The REAL-rank code path of the distributed stage 1 on one GPU: a one-rank NCCL
+    context asked for one partition runs it exactly as a rank of a multi-GPU job does
+    (CUDA-IPC handles all-gathered over NCCL, device-side NVLink barrier kernels,
+    system-scope exchange words, the serial and the lookahead schedules with the chain's
+    SMs reserved) -- only the peer mappings are absent.  Bitwise against the oracle."""
+    from paper_2208_01907_b200 import hf
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    monkeypatch.setenv("HF_DIST_LOOKAHEAD", str(look))
+    spec = hi.CONFIGS["P2048"]
+    Kb = hi.make_kbar("P2048", 1)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    c = hf.Context(0, nccl_id=hf.nccl_unique_id(), rank=0, nranks=1)
+    try:
+        Kd = Kb.cuda()
+        hf.hf_scale(c, Kd)
+        hf.hf_set_stage1_partitions(c, 1)
+        lf = hf.hf_factor_lowprec(c, Kd, tau=spec.tau, n_min=spec.n_min)
+        perm, D, Lf = lf.export()
+        assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+        assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+        lf.close()
+    finally:
+        c.close()
