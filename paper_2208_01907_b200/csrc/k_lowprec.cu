@@ -746,13 +746,17 @@ constexpr int TNS = 3;   // cp.async stages
 constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float);
 // NS (NEXT-3, nonsymmetric LDU): the FULL square trailing matrix (T x T tiles),
 // A operand -l_I, B operand r_J, v_IJ <- fmaf(-l_I, r_J, v_IJ) [R19].
-template <bool NS>
+// TMA (BULK): the panel operands staged by the bulk-copy engine (cp.async.bulk, one 512-byte
+// row per instruction, issued by 32 threads per chunk, completion counted in bytes on a
+// per-stage mbarrier) instead of 16-byte cp.async from every thread.
+template <bool NS, bool BULK = false>
 __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     if (a.status[2]) return;
     extern __shared__ __align__(16) float dsm_t[];   // [TNS][TK][TB] x 2 (48 KB: dynamic)
     float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t);
     float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t + TNS * TK * TB);
     __shared__ int32_t rmap[TB], cmap[TB];
+    __shared__ __align__(8) unsigned long long mbar[TNS];   // BULK: one per operand stage
     // persistent: CTA b takes tiles b, b + grid, ... (the order of the one-tile-per-CTA
     // launch); the next tile's compaction-map entry is loaded into a register while the
     // current tile computes, so a tile's seed gather waits for one memory latency, not two
@@ -803,18 +807,48 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][ek0][er0]);
     constexpr unsigned STGB = TK * TB * sizeof(float), EIGHTB = 8 * TB * sizeof(float);
     unsigned soff = 0;   // stage of the next issue, in bytes
+    int sidx = 0;        // its index
+    const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
     auto issue = [&](int c) {
-        if (c < nchunk) {
-            cp_async16_s(sA + soff, pa);
-            cp_async16_s(sA + soff + EIGHTB, pa + eight);
-            cp_async16_s(sB + soff, pb);
-            cp_async16_s(sB + soff + EIGHTB, pb + eight);
-            pa += cstride;
-            pb += cstride;
+        if (BULK) {
+            if (c < nchunk && tid < 2 * TK) {
+                // thread k < 16: row k of the A operand; 16 <= k < 32: row k - 16 of B
+                const int k = tid & (TK - 1);
+                const bool isb = tid >= TK;
+                const unsigned dst = (isb ? (unsigned)__cvta_generic_to_shared(&Bs[0][0][0])
+                                          : (unsigned)__cvta_generic_to_shared(&As[0][0][0])) +
+                                     soff + (unsigned)(k * TB * sizeof(float));
+                const float *src = (isb ? a.Sc + col0 : a.Snc + row0) + (int64_t)(c * TK + k) * a.ldc;
+                const unsigned mb = mb0 + 8u * (unsigned)sidx;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the generic reads
+                if (tid == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                                 "r"((unsigned)(2 * TK * TB * sizeof(float))) : "memory");
+                __syncwarp();
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(dst), "l"(src), "r"((unsigned)(TB * sizeof(float))), "r"(mb) : "memory");
+            }
+        } else {
+            if (c < nchunk) {
+                cp_async16_s(sA + soff, pa);
+                cp_async16_s(sA + soff + EIGHTB, pa + eight);
+                cp_async16_s(sB + soff, pb);
+                cp_async16_s(sB + soff + EIGHTB, pb + eight);
+                pa += cstride;
+                pb += cstride;
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
         soff = (soff == (TNS - 1) * STGB) ? 0u : soff + STGB;
+        sidx = (sidx == TNS - 1) ? 0 : sidx + 1;
     };
+    if (BULK && tid == 0) {   // the stage mbarriers: one arrival (the expect_tx) per use
+        for (int q = 0; q < TNS; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u * q) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (BULK) __syncthreads();
+    unsigned phase_bits = 0;   // BULK: parity of each stage's next completion
     issue(0);
     issue(1);
     __syncthreads();   // this tile's maps (stored before the loop or at the end of the previous tile)
@@ -867,8 +901,19 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     const int32_t mnext = tn < a.ntiles ? map_entry(tn) : -1;   // consumed after the main loop
     int st = 0;   // stage of chunk c
     for (int c = 0; c < nchunk; ++c, st = (st == TNS - 1) ? 0 : st + 1) {
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();                    // chunk c landed for all threads; stage (c+2)%3 is free
+        if (BULK) {
+            const unsigned mb = mb0 + 8u * (unsigned)st;
+            const unsigned ph = (phase_bits >> st) & 1u;
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(mb), "r"(ph) : "memory");
+            phase_bits ^= 1u << st;
+            __syncthreads();                // every thread is done with stage (c+2)%3 (read in c-1)
+        } else {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();                // chunk c landed for all threads; stage (c+2)%3 is free
+        }
         issue(c + 2);
         const int kmax = min(TK, a.nbp - c * TK);
         if (kmax == TK) {
@@ -1338,6 +1383,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
 
     HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    // HF_TRAIL_BULK=1: the panel operands staged by the bulk-copy (TMA) engine
+    const bool trail_bulk = getenv("HF_TRAIL_BULK") && atoi(getenv("HF_TRAIL_BULK")) != 0;
     // k_trailing_c: one tile per CTA (default) or persistent CTAs, occupancy x SMs, each
     // prefetching its next tile's compaction map while the current one computes
     // (HF_TRAIL_PCTA=1; measured slower: C2 32.0 vs 29.7 ms, C4 1926 vs 1780 ms per
@@ -1445,7 +1493,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 if (Sc.p && persist && (ntiles > 2 * pgrid || pmode == 2)) {
                     k_trailing_p<<<(unsigned)pgrid, 256, TRAIL_P_SMEM, st>>>(ta, ntiles);
                 } else if (Sc.p) {
-                    k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
+                    if (trail_bulk)
+                        k_trailing_c<false, true><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
+                    else
+                        k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
                 } else {
                     k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 }

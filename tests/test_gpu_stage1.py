@@ -141,3 +141,21 @@ def test_stage1_persistent_trailing_bitwise(ctx, name, seed, nb, monkeypatch):
     assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
     if Fo.N:
         assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+
+
+@pytest.mark.parametrize("env", ["HF_TRAIL_BULK", "HF_TRAIL_PCTA"])
+@pytest.mark.parametrize("name,seed,nb", [("P1024", 1, 0), ("P2048", 0, 64), ("S24", 0, 16), ("C0", 3, 8)])
+def test_stage1_trailing_variants_bitwise(ctx, name, seed, nb, env, monkeypatch):
+    """The trailing update's opt-in variants, same bits as the oracle: the panel operands
+    staged by the bulk-copy (TMA) engine with per-stage mbarriers (HF_TRAIL_BULK), and
+    persistent CTAs prefetching the next tile's compaction map (HF_TRAIL_PCTA) -- both
+    measured slower than the default on C2."""
+    monkeypatch.setenv(env, "1")
+    spec = hi.CONFIGS[name]
+    Kb = hi.make_kbar(name, seed)
+    Ko, _ = oracle.scale(Kb.numpy())
+    Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+    _, _, lf, perm, D, Lf = _run(ctx, Kb, spec.tau, n_min=spec.n_min, nb=nb)
+    assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+    if Fo.N:
+        assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
