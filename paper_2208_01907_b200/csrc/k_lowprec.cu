@@ -27,6 +27,8 @@
 // bit because the product is exact inside the FMA, so the row/column roles of
 // the oracle (right-looking) and of these kernels need not match.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
@@ -749,12 +751,19 @@ constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float);
 // TMA (BULK): the panel operands staged by the bulk-copy engine (cp.async.bulk, one 512-byte
 // row per instruction, issued by 32 threads per chunk, completion counted in bytes on a
 // per-stage mbarrier) instead of 16-byte cp.async from every thread.
-template <bool NS, bool BULK = false>
-__global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
+// BULK = 2: one 2D tensor copy (cp.async.bulk.tensor, a 16 x 128 box) per operand per chunk
+// through the tensor maps tmA (Snc) / tmB (Sc).
+template <bool NS, int BULK = 0>
+__global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmB) {
     if (a.status[2]) return;
     extern __shared__ __align__(16) float dsm_t[];   // [TNS][TK][TB] x 2 (48 KB: dynamic)
-    float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t);
-    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm_t + TNS * TK * TB);
+    // the tensor copies need 128 B aligned destinations; the dynamic window starts 32 B past
+    // one (measured), so BULK = 2 launches with 128 B more and rounds up
+    float *dsm = BULK == 2 ? reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(dsm_t) + 127) & ~uintptr_t(127))
+                           : dsm_t;
+    float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm);
+    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm + TNS * TK * TB);
     __shared__ int32_t rmap[TB], cmap[TB];
     __shared__ __align__(8) unsigned long long mbar[TNS];   // BULK: one per operand stage
     // persistent: CTA b takes tiles b, b + grid, ... (the order of the one-tile-per-CTA
@@ -810,7 +819,22 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a) {
     int sidx = 0;        // its index
     const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
     auto issue = [&](int c) {
-        if (BULK) {
+        if (BULK == 2) {
+            if (c < nchunk && tid == 0) {
+                const unsigned mb = mb0 + 8u * (unsigned)sidx;
+                const unsigned dA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]) + soff;
+                const unsigned dB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]) + soff;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                             "r"((unsigned)(2 * TK * TB * sizeof(float))) : "memory");
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                             " [%0], [%1, {%2, %3}], [%4];"
+                             ::"r"(dA), "l"(&tmA), "r"((int)row0), "r"(c * TK), "r"(mb) : "memory");
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                             " [%0], [%1, {%2, %3}], [%4];"
+                             ::"r"(dB), "l"(&tmB), "r"((int)col0), "r"(c * TK), "r"(mb) : "memory");
+            }
+        } else if (BULK) {
             if (c < nchunk && tid < 2 * TK) {
                 // thread k < 16: row k of the A operand; 16 <= k < 32: row k - 16 of B
                 const int k = tid & (TK - 1);
@@ -1167,6 +1191,27 @@ __global__ void k_gather_L(int64_t N, const int32_t *__restrict__ pivorig, const
 }  // namespace
 
 // ------------------------------------------------------------------ host driver
+// tensor map of a compacted panel buffer (ldc positions x nrows pivots, FP32, row = one
+// pivot's values): the 2D TMA box of the trailing update is 128 positions x 16 pivots
+static void make_panel_tmap(CUtensorMap *m, const float *base, int64_t ldc, int64_t nrows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        HF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        HF_REQUIRE(fn && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)ldc, (cuuint64_t)nrows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldc * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)TB, (cuuint32_t)TK};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{HF_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+}
+
 // algorithmic work per launch, reported through hf_kernel_work:
 //  trailing update of a panel of nbp pivots leaving mp active indices: one FMA per
 //    lower-triangle entry (diagonal included) per pivot; bytes = the triangle read
@@ -1383,9 +1428,18 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
 
     HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
-    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
-    // HF_TRAIL_BULK=1: the panel operands staged by the bulk-copy (TMA) engine
-    const bool trail_bulk = getenv("HF_TRAIL_BULK") && atoi(getenv("HF_TRAIL_BULK")) != 0;
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
+    HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM + 128));
+    // HF_TRAIL_BULK=1: the panel operands staged by the bulk-copy (TMA) engine row by row;
+    // =2: by 2D tensor copies (a 16 x 128 box per operand per chunk)
+    const int trail_bulk = getenv("HF_TRAIL_BULK") ? atoi(getenv("HF_TRAIL_BULK")) : 0;
+    CUtensorMap tmA, tmB;
+    std::memset(&tmA, 0, sizeof(tmA));
+    std::memset(&tmB, 0, sizeof(tmB));
+    if (trail_bulk == 2) {
+        make_panel_tmap(&tmA, Snc.p, ldc, cdiv(nb, TK) * TK);
+        make_panel_tmap(&tmB, Sc.p, ldc, cdiv(nb, TK) * TK);
+    }
     // k_trailing_c: one tile per CTA (default) or persistent CTAs, occupancy x SMs, each
     // prefetching its next tile's compaction map while the current one computes
     // (HF_TRAIL_PCTA=1; measured slower: C2 32.0 vs 29.7 ms, C4 1926 vs 1780 ms per
@@ -1493,10 +1547,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 if (Sc.p && persist && (ntiles > 2 * pgrid || pmode == 2)) {
                     k_trailing_p<<<(unsigned)pgrid, 256, TRAIL_P_SMEM, st>>>(ta, ntiles);
                 } else if (Sc.p) {
-                    if (trail_bulk)
-                        k_trailing_c<false, true><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
-                    else
-                        k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st>>>(ta);
+                    const unsigned tg = (unsigned)std::min<int64_t>(ntiles, cgrid);
+                    if (trail_bulk == 2) k_trailing_c<false, 2><<<tg, 256, TRAIL_C_SMEM + 128, st>>>(ta, tmA, tmB);
+                    else if (trail_bulk) k_trailing_c<false, 1><<<tg, 256, TRAIL_C_SMEM, st>>>(ta, tmA, tmB);
+                    else k_trailing_c<false><<<tg, 256, TRAIL_C_SMEM, st>>>(ta, tmA, tmB);
                 } else {
                     k_trailing<<<(unsigned)ntiles, 256, 0, st>>>(ta);
                 }
@@ -1516,7 +1570,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
                 }
                 {
                     ClassTimer tm(ctx, "trailing", st2, trail_flops(mp, nbp), trail_bytes(mp, nbp));
-                    k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st2>>>(ta);
+                    k_trailing_c<false><<<(unsigned)std::min<int64_t>(ntiles, cgrid), 256, TRAIL_C_SMEM, st2>>>(ta, tmA, tmB);
                     HF_CHECK_LAUNCH(ctx);
                 }
                 // the next chain reads the start of panel p (vsrc); before it runs, the trailing
@@ -1824,7 +1878,9 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
             const int64_t T = cdiv(mp, TB);
             {
                 ClassTimer tm(ctx, "trailing");
-                k_trailing_c<true><<<(unsigned)(T * T), 256, TRAIL_C_SMEM, st>>>(ta);
+                CUtensorMap tz;
+                std::memset(&tz, 0, sizeof(tz));
+                k_trailing_c<true><<<(unsigned)(T * T), 256, TRAIL_C_SMEM, st>>>(ta, tz, tz);
                 HF_CHECK_LAUNCH(ctx);
             }
             cur ^= 1;

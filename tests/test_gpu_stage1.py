@@ -143,14 +143,15 @@ def test_stage1_persistent_trailing_bitwise(ctx, name, seed, nb, monkeypatch):
         assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
 
 
-@pytest.mark.parametrize("env", ["HF_TRAIL_BULK", "HF_TRAIL_PCTA"])
+@pytest.mark.parametrize("env,val", [("HF_TRAIL_BULK", "1"), ("HF_TRAIL_BULK", "2"), ("HF_TRAIL_PCTA", "1")])
 @pytest.mark.parametrize("name,seed,nb", [("P1024", 1, 0), ("P2048", 0, 64), ("S24", 0, 16), ("C0", 3, 8)])
-def test_stage1_trailing_variants_bitwise(ctx, name, seed, nb, env, monkeypatch):
+def test_stage1_trailing_variants_bitwise(ctx, name, seed, nb, env, val, monkeypatch):
     """The trailing update's opt-in variants, same bits as the oracle: the panel operands
-    staged by the bulk-copy (TMA) engine with per-stage mbarriers (HF_TRAIL_BULK), and
+    staged by the bulk-copy (TMA) engine with per-stage mbarriers, row by row
+    (HF_TRAIL_BULK=1) or as 2D tensor-map boxes (HF_TRAIL_BULK=2), and
     persistent CTAs prefetching the next tile's compaction map (HF_TRAIL_PCTA) -- both
     measured slower than the default on C2."""
-    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv(env, val)
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
     Ko, _ = oracle.scale(Kb.numpy())
