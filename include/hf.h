@@ -131,6 +131,15 @@ hf_status hf_trim_cache(int device);
  * q: FP64[L].  Returns HF_ERR_INVALID_ARG if K holds NaN/Inf on or below the
  * diagonal. */
 hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);
+/* The same scaling from a HOST matrix: the lower triangle (i >= j, the only part
+ * hf_scale reads) of Kbar_host (L x L, column-major, ldh >= L; pinned memory makes
+ * the copy asynchronous, pageable memory works) is copied into the device K (ld)
+ * in column panels of 256 on the context stream, then scaled in place as above
+ * (the upper triangle of K is written from the lower one; that of Kbar_host is
+ * never read).  *h2d_bytes_host (if not NULL) = bytes moved host -> device.
+ * Synchronises the stream.  Same errors as hf_scale. */
+hf_status hf_scale_host(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
+                        double *q, int64_t *h2d_bytes_host);
 /* NEXT-3: the same scaling for a GENERAL matrix (every entry read and written:
  * K_ij = (q_i Kbar_ij) q_j, K_ii = sign Kbar_ii).  Same errors as hf_scale. */
 hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);

@@ -192,6 +192,37 @@ hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
     });
 }
 
+// The lower triangle of a host Kbar moves in column panels of 256: one 2D copy per panel
+// (rows j0..L-1 of columns j0..j0+255), so the bytes on the host link are L^2/2 x 8 plus the
+// panels' diagonal blocks; the upper triangle, which hf_scale never reads, stays on the host.
+hf_status hf_scale_host(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
+                        double *q, int64_t *h2d_bytes_host) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ldh >= L && ld >= L && (L == 0 || (Kbar_host && K && q)), "hf_scale_host: bad arguments");
+        if (h2d_bytes_host) *h2d_bytes_host = 0;
+        if (L == 0) return;
+        constexpr int64_t W = 256;
+        int64_t bytes = 0;
+        for (int64_t j0 = 0; j0 < L; j0 += W) {
+            const int64_t w = std::min<int64_t>(W, L - j0);
+            HF_CUDA(cudaMemcpy2DAsync(K + j0 + j0 * ld, (size_t)ld * sizeof(double), Kbar_host + j0 + j0 * ldh,
+                                      (size_t)ldh * sizeof(double), (size_t)(L - j0) * sizeof(double), (size_t)w,
+                                      cudaMemcpyHostToDevice, ctx->stream));
+            bytes += (L - j0) * w * (int64_t)sizeof(double);
+        }
+        hf::DBuf<int> bad;
+        bad.alloc(1, ctx->stream);
+        bad.zero(ctx->stream);
+        hf::launch_scale(ctx, L, K, ld, q, bad.p);
+        int hb = 0;
+        HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+        HF_REQUIRE(!hb, "hf_scale_host: K holds NaN or Inf");
+        if (h2d_bytes_host) *h2d_bytes_host = bytes;
+    });
+}
+
 hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
     if (!ctx) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {

@@ -79,25 +79,43 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     return v;
 }
 
-// c <- fmaf(x_u, y_u, c) for u = 0..n-1 in order [R8]; x_u = xs[u * R] (own row's
-// panel values, shared memory, stride R), y_u = ys[u] (broadcast).  (Issuing the next
-// 8 loads ahead of the current 8 FMAs measured slower, 0.96 and 1.63 vs 0.76 us per
-// C2 pivot: register pressure under the 64-register bound of the 1024-thread launch.)
-__device__ __forceinline__ float fma_chain(float c, const float *xs, const float *ys, int n, int R) {
+// c <- fmaf(x_u, y_u, c) for u = 0..n-1 in order [R8].  x_u: the own row's panel values in
+// shared memory, interleaved by four (x_u at xs[(u >> 2) * R4 + (u & 3)], R4 = 4 x rows per
+// CTA: one 16-byte load per thread per four pivots, four wavefronts per warp); y_u = ys[u]
+// (broadcast, 16-byte aligned: one 16-byte load per four pivots, one wavefront).  The scalar
+// form (one 4-byte load of each operand and an address IMAD per fmaf) was bound by the
+// shared-memory wavefronts of the broadcast loads.
+__device__ __forceinline__ float fma_chain(float c, const float *xs, const float *ys, int n, int R4) {
     int u = 0;
     for (; u + 8 <= n; u += 8) {
-        float x[8], y[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            x[q] = xs[(size_t)(u + q) * R];
-            y[q] = ys[u + q];
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) c = __fmaf_rn(x[q], y[q], c);
+        const float4 x0 = *reinterpret_cast<const float4 *>(xs);
+        const float4 x1 = *reinterpret_cast<const float4 *>(xs + R4);
+        const float4 y0 = *reinterpret_cast<const float4 *>(ys + u);
+        const float4 y1 = *reinterpret_cast<const float4 *>(ys + u + 4);
+        xs += 2 * R4;
+        c = __fmaf_rn(x0.x, y0.x, c);
+        c = __fmaf_rn(x0.y, y0.y, c);
+        c = __fmaf_rn(x0.z, y0.z, c);
+        c = __fmaf_rn(x0.w, y0.w, c);
+        c = __fmaf_rn(x1.x, y1.x, c);
+        c = __fmaf_rn(x1.y, y1.y, c);
+        c = __fmaf_rn(x1.z, y1.z, c);
+        c = __fmaf_rn(x1.w, y1.w, c);
     }
-    for (; u < n; ++u) c = __fmaf_rn(xs[(size_t)u * R], ys[u], c);
+    if (u + 4 <= n) {
+        const float4 x0 = *reinterpret_cast<const float4 *>(xs);
+        const float4 y0 = *reinterpret_cast<const float4 *>(ys + u);
+        xs += R4;
+        u += 4;
+        c = __fmaf_rn(x0.x, y0.x, c);
+        c = __fmaf_rn(x0.y, y0.y, c);
+        c = __fmaf_rn(x0.z, y0.z, c);
+        c = __fmaf_rn(x0.w, y0.w, c);
+    }
+    for (int q = 0; u < n; ++u, ++q) c = __fmaf_rn(xs[q], ys[u], c);
     return c;
 }
+__host__ __device__ __forceinline__ int64_t ceil4(int64_t n) { return (n + 3) & ~(int64_t)3; }
 
 // ------------------------------------------------------------------ cast [R2]
 __global__ void k_cast_lower(int64_t L, const double *__restrict__ K, int64_t ldk, float *__restrict__ V,
@@ -202,11 +220,15 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     const int64_t nown = max((int64_t)0, min((int64_t)a.R, a.m - r0));
     const int nb = a.nbp;
     const int nbq = a.nbprev;                 // previous panel's pivots (lookahead) or 0
-    float *sneg = smem;                       // [nbp][R]  -sigma_u s_i^u for own rows
-    float *snp = sneg + (size_t)nb * a.R;     // [nbq][R]  the same for the previous panel
-    float *sp = smem + (((size_t)(nb + nbq) * a.R + 3) & ~(size_t)3);   // [nbp] s_P^u of the current pivot row (16-B aligned)
-    float *spp = sp + nb;                     // [nbq]     s_P^u of the previous panel
-    float *sgm = spp + nbq;                   // [nbp]     sigma_u
+    // panel values interleaved by four (fma_chain): value u of own row r at
+    // [(u >> 2) * 4R + 4r + (u & 3)]; every array starts 16-byte aligned
+    const int R4 = 4 * a.R;
+    auto sx = [&](int u, int r) -> size_t { return (size_t)(u >> 2) * R4 + 4 * r + (u & 3); };
+    float *sneg = smem;                            // [nbp][R]  -sigma_u s_i^u for own rows
+    float *snp = sneg + (size_t)ceil4(nb) * a.R;   // [nbq][R]  the same for the previous panel
+    float *sp = snp + (size_t)ceil4(nbq) * a.R;    // [nbp] s_P^u of the current pivot row
+    float *spp = sp + ceil4(nb);                   // [nbq]     s_P^u of the previous panel
+    float *sgm = spp + ceil4(nbq);                 // [nbp]     sigma_u
 
     const bool has = tid < nown;
     const int64_t i = r0 + tid;
@@ -215,7 +237,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
     float dg = 0.f;   // lazy diagonal of own row
     if (has) dg = a.DGprev ? a.DGprev[io] : a.V[i + i * a.ldv];
     if (has)
-        for (int u = 0; u < nbq; ++u) snp[(size_t)u * a.R + tid] = a.SNprev[io * a.nbmax + u];
+        for (int u = 0; u < nbq; ++u) snp[sx(u, tid)] = a.SNprev[io * a.nbmax + u];
     bool piv = !has;
     float dprev = a.K0 > 0 ? a.Dk[a.K0 - 1] : 0.f;
     const bool BLK = a.blk != nullptr;
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
                 unsigned long long *mb = a.mbox + ((size_t)par * G + blockIdx.x) * (nb + 1);
                 const int lr = (int)((int64_t)(POS_MAX - (uint32_t)((v >> 15) & POS_MAX)) - r0);
                 for (int u = lane; u < t; u += 32)
-                    st_relaxed_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[(size_t)u * a.R + lr]) << 32) | tag);
+                    st_relaxed_u64(&mb[u], ((unsigned long long)__float_as_uint(sneg[sx(u, lr)]) << 32) | tag);
             }
         }
         // ---- C: deferred global stores of step t-1
@@ -431,11 +453,11 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
             a.sigma[t] = sg;
         } else if (!piv) {
             float c = v;
-            c = fma_chain(c, snp + tid, spp, nbq, a.R);   // [R8] the previous panel's pivots first
-            c = fma_chain(c, sneg + tid, sp, t, a.R);   // [R8] one fmaf per earlier pivot, in order
+            c = fma_chain(c, snp + 4 * tid, spp, nbq, R4);   // [R8] the previous panel's pivots first
+            c = fma_chain(c, sneg + 4 * tid, sp, t, R4);   // [R8] one fmaf per earlier pivot, in order
             const float sv = __fdiv_rn(c, r);
             const float ns = -sg * sv;                  // exact
-            sneg[(size_t)t * a.R + tid] = ns;
+            sneg[sx(t, tid)] = ns;
             ps = sv;
             pn = ns;
             pc = c;
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
         a.bstate[2] = (int32_t)att;
     }
     if (a.SNout && has) {   // this panel's values and the lazy diagonal, for the next panel's lookahead
-        for (int u = 0; u < t; ++u) a.SNout[i * a.nbmax + u] = sneg[(size_t)u * a.R + tid];
+        for (int u = 0; u < t; ++u) a.SNout[i * a.nbmax + u] = sneg[sx(u, tid)];
         a.DGout[i] = dg;
     }
     if (dbg) {
@@ -1353,8 +1375,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     // with lookahead the chain holds both panels' values of its rows in shared memory
     const int nbf = (look ? 2 : 1);
     // the widest multiple of 16 (the trailing kernel's k chunk) that fits, e.g. 112 at C4
-    while (nb > 16 && (int64_t)(nbf * nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb -= 16;
-    while (nb > 8 && (int64_t)(nbf * nb * R0 + 3 * nb) * 4 > (int64_t)maxsmem) nb /= 2;
+    auto chain_fits = [&](int w) { return (int64_t)(nbf * ceil4(w) * R0 + 3 * ceil4(w) + 4) * 4 <= (int64_t)maxsmem; };
+    while (nb > 16 && !chain_fits(nb)) nb -= 16;
+    while (nb > 8 && !chain_fits(nb)) nb /= 2;
     HF_REQUIRE(nb >= 8 && nb <= 1024, "panel width out of range");
 
     DBuf<float> V[2];
@@ -1487,7 +1510,8 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         const int64_t R = cdiv(m, G);
         const int nthr = (int)std::max<int64_t>(64, cdiv(R, 32) * 32);
         const int pb = look ? (pidx & 1) : 0, qb = pb ^ 1;
-        const size_t shm = ((size_t)(nbp + (look ? nbprev : 0)) * R + 3 * nbp + (look ? nbprev : 0) + 4) * sizeof(float);
+        const int64_t nbq_ = look ? nbprev : 0;
+        const size_t shm = ((size_t)(ceil4(nbp) + ceil4(nbq_)) * R + 2 * ceil4(nbp) + ceil4(nbq_) + 4) * sizeof(float);
         if (xmode == 0) HF_CUDA(cudaMemsetAsync(xchg.p, 0, xchg.n * sizeof(unsigned long long), st));
         ChainArgs ca;
         ca.m = m; ca.K0 = K0; ca.nbp = nbp; ca.R = (int)R; ca.tau = o.tau;

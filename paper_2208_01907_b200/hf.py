@@ -25,7 +25,7 @@ _NAMES = {0: "HF_OK", 1: "HF_ERR_INVALID_ARG", 2: "HF_ERR_CUDA", 3: "HF_ERR_NCCL
 
 EXPORTED = [
     "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
-    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_factor_lowprec",
+    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_scale_host", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
         "hf_chain_exchange_floor": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, pdbl],
         "hf_launch_count": [vp, pi64],
         "hf_scale": [vp, i64, vp, i64, vp],
+        "hf_scale_host": [vp, i64, vp, i64, vp, i64, vp, vp],
         "hf_scale_full": [vp, i64, vp, i64, vp],
         "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
         "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
@@ -257,6 +258,24 @@ def hf_scale(ctx: Context, K: torch.Tensor) -> torch.Tensor:
     q = torch.empty(L, dtype=torch.float64, device=K.device)
     ctx.check(ctx.lib.hf_scale(ctx.h, L, _ptr(K), L, _ptr(q)))
     return q
+
+
+def hf_scale_host(ctx: Context, Kbar_host: torch.Tensor, K: torch.Tensor):
+    """P:40 scaling from a host matrix: the lower triangle of Kbar_host (CPU FP64 L x L,
+    column-major memory = a transposed-contiguous or symmetric tensor; pin it for an
+    asynchronous copy) is copied into the device K and scaled there.  Returns
+    (q device FP64[L], bytes copied host -> device)."""
+    _dev(K, torch.float64)
+    if Kbar_host.device.type != "cpu" or Kbar_host.dtype != torch.float64 or not Kbar_host.is_contiguous():
+        raise ValueError("Kbar_host must be a contiguous CPU float64 tensor")
+    L = K.shape[0]
+    if tuple(Kbar_host.shape) != (L, L):
+        raise ValueError("Kbar_host and K differ in shape")
+    q = torch.empty(L, dtype=torch.float64, device=K.device)
+    nb = ctypes.c_int64(0)
+    ctx.check(ctx.lib.hf_scale_host(ctx.h, L, _ptr(Kbar_host), L, _ptr(K), L, _ptr(q),
+                                    ctypes.byref(nb)))
+    return q, int(nb.value)
 
 
 def hf_scale_full(ctx: Context, K: torch.Tensor) -> torch.Tensor:

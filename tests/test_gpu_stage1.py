@@ -49,6 +49,30 @@ def test_stage1_bitwise(ctx, name, seed):
         assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
 
 
+@pytest.mark.parametrize("name,seed,pinned", [("C0", 0, True), ("P1024", 1, False), ("P512", 2, True)])
+def test_scale_from_host_lower_triangle(ctx, name, seed, pinned):
+    """hf_scale_host (the end-to-end entry: Kbar on the host) = the oracle's scaling, bitwise,
+    reading only the lower triangle: the host matrix's upper triangle is overwritten with NaN
+    and the result must not change; the bytes moved are the lower-triangle column panels."""
+    from paper_2208_01907_b200 import hf
+    Kb = hi.make_kbar(name, seed)
+    Ko, qo = oracle.scale(Kb.numpy())
+    L = Kb.shape[0]
+    Kh = Kb.clone()
+    # memory is column-major: element (i, j) of the matrix is Kh[j, i]; poison i < j
+    iu = torch.triu_indices(L, L, offset=1)
+    Kh[iu[1], iu[0]] = float("nan")
+    if pinned:
+        Kh = Kh.pin_memory()
+    Kd = torch.empty(L, L, dtype=torch.float64, device="cuda")
+    q, nbytes = hf.hf_scale_host(ctx, Kh, Kd)
+    assert np.array_equal(q.cpu().numpy(), qo)
+    assert np.array_equal(Kd.cpu().numpy(), Ko)
+    W = 256
+    assert nbytes == sum((L - j0) * min(W, L - j0) * 8 for j0 in range(0, L, W))
+    assert nbytes <= (L * L + L * W) // 2 * 8             # the lower half + the diagonal blocks
+
+
 @pytest.mark.parametrize("nb", [8, 16, 64, 128])
 def test_stage1_panel_width_invariance(ctx, nb):
     """Panel width changes the blocking, never the bits (canonical order [R8])."""
