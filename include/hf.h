@@ -140,6 +140,18 @@ hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);
  * Synchronises the stream.  Same errors as hf_scale. */
 hf_status hf_scale_host(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
                         double *q, int64_t *h2d_bytes_host);
+/* Asynchronous form of hf_scale_host's copy, for pipelining the next matrix's
+ * transfer behind the current factorization: the same lower-triangle panels of
+ * Kbar_host into K, issued on the context's own upload stream (created on first
+ * use) and returning at once (pinned Kbar_host: the host must keep it unchanged
+ * until the copy is done; pageable memory makes the call synchronous).  The copy
+ * is NOT ordered after work already queued on the context stream: the caller
+ * must not upload into a K that queued work still reads.  The next hf_scale /
+ * hf_scale_host on this context orders the context stream after every upload
+ * issued before it.  *h2d_bytes_host (if not NULL) = bytes the copy moves.  The
+ * paper's scaling step then runs by hf_scale(K). */
+hf_status hf_upload_lower(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
+                          int64_t *h2d_bytes_host);
 /* NEXT-3: the same scaling for a GENERAL matrix (every entry read and written:
  * K_ij = (q_i Kbar_ij) q_j, K_ii = sign Kbar_ii).  Same errors as hf_scale. */
 hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q);

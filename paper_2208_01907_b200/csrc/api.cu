@@ -114,6 +114,11 @@ hf_status hf_destroy(hf_ctx *ctx) {
     }
     for (auto e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->up) {
+        cudaStreamSynchronize(ctx->up);
+        cudaStreamDestroy(ctx->up);
+    }
+    if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
 #ifdef HF_WITH_NCCL
     if (ctx->comm) ncclCommDestroy(ctx->comm);
 #endif
@@ -176,25 +181,50 @@ hf_status hf_launch_count(const hf_ctx *ctx, int64_t *launches_host) {
 }
 
 // ------------------------------------------------------------------ a1
+// The lower triangle of a host Kbar moves in column panels of 256: one 2D copy per panel
+// (rows j0..L-1 of columns j0..j0+255), so the bytes on the host link are L^2/2 x 8 plus the
+// panels' diagonal blocks; the upper triangle, which hf_scale never reads, stays on the host.
+static int64_t copy_lower_panels(cudaStream_t st, int64_t L, const double *Kh, int64_t ldh, double *K, int64_t ld) {
+    constexpr int64_t W = 256;
+    int64_t bytes = 0;
+    for (int64_t j0 = 0; j0 < L; j0 += W) {
+        const int64_t w = std::min<int64_t>(W, L - j0);
+        HF_CUDA(cudaMemcpy2DAsync(K + j0 + j0 * ld, (size_t)ld * sizeof(double), Kh + j0 + j0 * ldh,
+                                  (size_t)ldh * sizeof(double), (size_t)(L - j0) * sizeof(double), (size_t)w,
+                                  cudaMemcpyHostToDevice, st));
+        bytes += (L - j0) * w * (int64_t)sizeof(double);
+    }
+    return bytes;
+}
+
+// the context stream waits for the uploads issued so far (hf_upload_lower)
+static void order_after_uploads(hf_ctx *ctx) {
+    if (!ctx->up_pending) return;
+    HF_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->up_ev, 0));
+    ctx->up_pending = false;
+}
+
+static void scale_checked(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q, const char *who) {
+    hf::DBuf<int> bad;
+    bad.alloc(1, ctx->stream);
+    bad.zero(ctx->stream);
+    hf::launch_scale(ctx, L, K, ld, q, bad.p);
+    int hb = 0;
+    HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    HF_REQUIRE(!hb, std::string(who) + ": K holds NaN or Inf");
+}
+
 hf_status hf_scale(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
     if (!ctx) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {
         HF_REQUIRE(L >= 0 && ld >= L && (L == 0 || (K && q)), "hf_scale: bad arguments");
         if (L == 0) return;
-        hf::DBuf<int> bad;
-        bad.alloc(1, ctx->stream);
-        bad.zero(ctx->stream);
-        hf::launch_scale(ctx, L, K, ld, q, bad.p);
-        int hb = 0;
-        HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        HF_CUDA(cudaStreamSynchronize(ctx->stream));
-        HF_REQUIRE(!hb, "hf_scale: K holds NaN or Inf");
+        order_after_uploads(ctx);
+        scale_checked(ctx, L, K, ld, q, "hf_scale");
     });
 }
 
-// The lower triangle of a host Kbar moves in column panels of 256: one 2D copy per panel
-// (rows j0..L-1 of columns j0..j0+255), so the bytes on the host link are L^2/2 x 8 plus the
-// panels' diagonal blocks; the upper triangle, which hf_scale never reads, stays on the host.
 hf_status hf_scale_host(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
                         double *q, int64_t *h2d_bytes_host) {
     if (!ctx) return HF_ERR_INVALID_ARG;
@@ -202,23 +232,27 @@ hf_status hf_scale_host(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t
         HF_REQUIRE(L >= 0 && ldh >= L && ld >= L && (L == 0 || (Kbar_host && K && q)), "hf_scale_host: bad arguments");
         if (h2d_bytes_host) *h2d_bytes_host = 0;
         if (L == 0) return;
-        constexpr int64_t W = 256;
-        int64_t bytes = 0;
-        for (int64_t j0 = 0; j0 < L; j0 += W) {
-            const int64_t w = std::min<int64_t>(W, L - j0);
-            HF_CUDA(cudaMemcpy2DAsync(K + j0 + j0 * ld, (size_t)ld * sizeof(double), Kbar_host + j0 + j0 * ldh,
-                                      (size_t)ldh * sizeof(double), (size_t)(L - j0) * sizeof(double), (size_t)w,
-                                      cudaMemcpyHostToDevice, ctx->stream));
-            bytes += (L - j0) * w * (int64_t)sizeof(double);
+        order_after_uploads(ctx);
+        const int64_t bytes = copy_lower_panels(ctx->stream, L, Kbar_host, ldh, K, ld);
+        scale_checked(ctx, L, K, ld, q, "hf_scale_host");
+        if (h2d_bytes_host) *h2d_bytes_host = bytes;
+    });
+}
+
+hf_status hf_upload_lower(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64_t ldh, double *K, int64_t ld,
+                          int64_t *h2d_bytes_host) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && ldh >= L && ld >= L && (L == 0 || (Kbar_host && K)), "hf_upload_lower: bad arguments");
+        if (h2d_bytes_host) *h2d_bytes_host = 0;
+        if (L == 0) return;
+        if (!ctx->up) {
+            HF_CUDA(cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
+            HF_CUDA(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
         }
-        hf::DBuf<int> bad;
-        bad.alloc(1, ctx->stream);
-        bad.zero(ctx->stream);
-        hf::launch_scale(ctx, L, K, ld, q, bad.p);
-        int hb = 0;
-        HF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        HF_CUDA(cudaStreamSynchronize(ctx->stream));
-        HF_REQUIRE(!hb, "hf_scale_host: K holds NaN or Inf");
+        const int64_t bytes = copy_lower_panels(ctx->up, L, Kbar_host, ldh, K, ld);
+        HF_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
+        ctx->up_pending = true;
         if (h2d_bytes_host) *h2d_bytes_host = bytes;
     });
 }

@@ -144,6 +144,11 @@ struct hf_ctx {
     std::map<std::pair<int, int>, hf::TrsmTable> trsm_tables;   // (nblk, nch) -> table
     cudaStream_t side = nullptr;       // second stream (stage-1 lookahead: trailing updates), lazily created
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // hf_upload_lower: host -> device copies on their own stream (lazily created); the
+    // event marks the last one, and hf_scale / hf_scale_host order the context stream after it
+    cudaStream_t up = nullptr;
+    cudaEvent_t up_ev = nullptr;
+    bool up_pending = false;
 };
 
 namespace hf {

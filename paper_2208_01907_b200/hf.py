@@ -25,7 +25,7 @@ _NAMES = {0: "HF_OK", 1: "HF_ERR_INVALID_ARG", 2: "HF_ERR_CUDA", 3: "HF_ERR_NCCL
 
 EXPORTED = [
     "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
-    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_scale_host", "hf_factor_lowprec",
+    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_scale_host", "hf_upload_lower", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
@@ -81,6 +81,7 @@ def load() -> ctypes.CDLL:
         "hf_launch_count": [vp, pi64],
         "hf_scale": [vp, i64, vp, i64, vp],
         "hf_scale_host": [vp, i64, vp, i64, vp, i64, vp, vp],
+        "hf_upload_lower": [vp, i64, vp, i64, vp, i64, vp],
         "hf_scale_full": [vp, i64, vp, i64, vp],
         "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
         "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
@@ -276,6 +277,21 @@ def hf_scale_host(ctx: Context, Kbar_host: torch.Tensor, K: torch.Tensor):
     ctx.check(ctx.lib.hf_scale_host(ctx.h, L, _ptr(Kbar_host), L, _ptr(K), L, _ptr(q),
                                     ctypes.byref(nb)))
     return q, int(nb.value)
+
+
+def hf_upload_lower(ctx: Context, Kbar_host: torch.Tensor, K: torch.Tensor) -> int:
+    """Asynchronous copy of the lower triangle of Kbar_host (CPU FP64 L x L, pinned for
+    asynchrony) into the device K on the context's upload stream; the next hf_scale on
+    this context waits for it.  K must not be in use by queued work.  Returns the bytes."""
+    _dev(K, torch.float64)
+    if Kbar_host.device.type != "cpu" or Kbar_host.dtype != torch.float64 or not Kbar_host.is_contiguous():
+        raise ValueError("Kbar_host must be a contiguous CPU float64 tensor")
+    L = K.shape[0]
+    if tuple(Kbar_host.shape) != (L, L):
+        raise ValueError("Kbar_host and K differ in shape")
+    nb = ctypes.c_int64(0)
+    ctx.check(ctx.lib.hf_upload_lower(ctx.h, L, _ptr(Kbar_host), L, _ptr(K), L, ctypes.byref(nb)))
+    return int(nb.value)
 
 
 def hf_scale_full(ctx: Context, K: torch.Tensor) -> torch.Tensor:

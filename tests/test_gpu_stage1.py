@@ -73,6 +73,31 @@ def test_scale_from_host_lower_triangle(ctx, name, seed, pinned):
     assert nbytes <= (L * L + L * W) // 2 * 8             # the lower half + the diagonal blocks
 
 
+def test_upload_pipelined_with_factorization(ctx):
+    """hf_upload_lower (asynchronous, the library's upload stream) of matrix B while matrix A
+    factors on the context stream, then hf_scale(B) (ordered after the upload) and B's
+    factorization: both results bitwise equal to the oracle's."""
+    from paper_2208_01907_b200 import hf
+    specA, specB = hi.CONFIGS["P1024"], hi.CONFIGS["P512"]
+    KbA, KbB = hi.make_kbar("P1024", 3), hi.make_kbar("P512", 4)
+    KA = KbA.to("cuda").contiguous()
+    KB = torch.empty(KbB.shape, dtype=torch.float64, device="cuda")
+    hB = KbB.clone().pin_memory()
+    hf.hf_scale(ctx, KA)
+    lfA = hf.hf_factor_lowprec(ctx, KA, tau=specA.tau, n_min=specA.n_min)   # queued on the context stream
+    hf.hf_upload_lower(ctx, hB, KB)                                        # concurrent copy
+    hf.hf_scale(ctx, KB)
+    lfB = hf.hf_factor_lowprec(ctx, KB, tau=specB.tau, n_min=specB.n_min)
+    for Kb, spec, lf in ((KbA, specA, lfA), (KbB, specB, lfB)):
+        Ko, _ = oracle.scale(Kb.numpy())
+        Fo = oracle.factor_lowprec(Ko, spec.tau, n_min=spec.n_min)
+        perm, D, Lf = lf.export()
+        assert np.array_equal(perm, Fo.perm) and np.array_equal(D, Fo.D)
+        if Fo.N:
+            assert np.array_equal(Lf.cpu().numpy(), Fo.Lfac)
+        lf.close()
+
+
 @pytest.mark.parametrize("nb", [8, 16, 64, 128])
 def test_stage1_panel_width_invariance(ctx, nb):
     """Panel width changes the blocking, never the bits (canonical order [R8])."""
