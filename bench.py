@@ -35,10 +35,23 @@ sys.path.insert(0, ROOT)
 
 FFMA_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12     # TFLOP/s, B200 FP32 non-tensor
 DMMA_PEAK_MEASURED = 37.15                              # tools/peaks.py, profiles/peaks_r01.json
-KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "trsm_setup", "gram", "hard", "other")
+KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "trsm_setup", "gram", "hard", "other",
+            "ozaki_split", "ozaki_imma", "ozaki_combine")
+OZAKI_SLICES = 8                                        # ozaki.cu default (hf_gcr_opts.slices = 0)
 
 
-def flop_model(L, N, Ntau, n2, iters):
+def int8_peak():
+    """Dense int8 tensor peak: the driver-measured bf16 dense peak (MEASURED_PEAKS.json,
+    burst) x the nominal int8 / bf16 ratio (4.5 / 2.25 POPS, B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        return 2.0 * bf16, "MEASURED_PEAKS.json bf16_tflops (burst) x 2 (nominal int8 / bf16 ratio)"
+    except Exception:
+        return 4500.0, "nominal B200 dense int8 (no MEASURED_PEAKS.json)"
+
+
+def flop_model(L, N, Ntau, n2, iters, ozaki=False):
     """Algorithmic flops of one hybrid factorization, counted
     as block_gcr (gcr.cu) runs Alg. 5: K11-products for r_0, q_0, each z_{n+1} of a
     non-final iteration and the reported true residual (iters + 2); preconditioner
@@ -56,9 +69,10 @@ def flop_model(L, N, Ntau, n2, iters):
     f2 = (iters + 2) * mv + (iters + 1) * pc + gram + small
     f3 = 2.0 * N * n2 * n2
     f4 = n2 ** 3 / 3.0
-    dmma = (iters + 2) * mv + gram + small + f3                # the FP64 DMMA GEMM class
+    matvec = (iters + 2) * mv
+    dmma = (0.0 if ozaki else matvec) + gram + small + f3      # the FP64 DMMA GEMM class
     return {"stage1": f1, "gcr": f2, "schur": f3, "hard": f4, "total": f1 + f2 + f3 + f4,
-            "dmma": dmma, "trsm": (iters + 1) * pc}
+            "dmma": dmma, "matvec": matvec, "trsm": (iters + 1) * pc}
 
 
 class Clocks:
@@ -408,7 +422,8 @@ def main():
 
     N, Ntau, n2, iters, kd, tres = results[-1]
     L = spec.L
-    fm = flop_model(L, N, Ntau, n2, iters)
+    ozaki = kms.get("ozaki_imma", 0.0) > 0.0
+    fm = flop_model(L, N, Ntau, n2, iters, ozaki=ozaki)
     elapsed = max_over_ranks(elapsed)
     ms_step = elapsed / args.steps
     # replicas: every rank factorises its own matrix (weak scaling); shard: one
@@ -447,11 +462,14 @@ def main():
     dmma_ach = fm["dmma"] / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
     trsm_ach = kwork["trsm"][0] / (ts_ms * 1e-3) / 1e12 if ts_ms > 0 else None
     rooflines = {
-        "dgemm": {"kernel": "k_dgemm (FP64 DMMA mma.sync m8n8k4: K11 W mat-vecs, Gram / update products, Schur)",
+        "dgemm": {"kernel": ("k_dgemm (FP64 DMMA mma.sync m8n8k4: Gram / update products, Schur; the K11 W "
+                             "mat-vecs run on the int8 tensor cores, rooflines.matvec)") if ozaki else
+                            "k_dgemm (FP64 DMMA mma.sync m8n8k4: K11 W mat-vecs, Gram / update products, Schur)",
                   "bound": "fp64_tensor", "achieved": dmma_ach, "peak": DMMA_PEAK_MEASURED, "unit": "TFLOP/s",
                   "frac": dmma_ach / DMMA_PEAK_MEASURED if dmma_ach else None,
-                  "flops_per_step": fm["dmma"], "flops_note": "algorithmic DMMA work only (mat-vecs on N = "
-                  "|Lambda_1| rows, Gram / update / n2 x n2 products, S22); the FP32 preconditioner is not in it",
+                  "flops_per_step": fm["dmma"], "flops_note": "algorithmic DMMA work only (%sGram / update / "
+                  "n2 x n2 products, S22); the FP32 preconditioner is not in it" %
+                  ("" if ozaki else "mat-vecs on N = |Lambda_1| rows, "),
                   "executed_flops_per_step": kwork["dgemm"][0], "ms_per_step": dg_ms,
                   "peak_source": "measured DMMA microbenchmark (tools/peaks.py, profiles/peaks_r01.json)"},
         "trsm": {"kernel": "k_trsm<fwd/bwd> (FP32 FFMA2 dataflow triangular solves, n2 right-hand sides)",
@@ -470,12 +488,32 @@ def main():
                   "hbm_gbs": kwork["chain"][1] / (ch_ms * 1e-3) / 1e9 if ch_ms > 0 else None,
                   "bytes_per_step": kwork["chain"][1]},
     }
+    if ozaki:
+        # the FP64 mat-vec emulated on the int8 tensor cores (ozaki.cu): s(s+1)/2 exact slice
+        # products per mat-vec, each 2 N^2 n2 int8 ops of algorithmic work; the int8 GEMMs are
+        # cuBLASLt's (a plain library GEMM), the splitting and the combination libhf's
+        mv_ms = kms["ozaki_split"] + kms["ozaki_imma"] + kms["ozaki_combine"]
+        nprod = OZAKI_SLICES * (OZAKI_SLICES + 1) // 2
+        i8_ops = nprod * fm["matvec"]
+        i8_peak, i8_src = int8_peak()
+        i8_ach = i8_ops / (kms["ozaki_imma"] * 1e-3) / 1e12
+        rooflines["matvec"] = {
+            "kernel": "K11 W as FP64 emulated on the int8 tensor cores (Ozaki scheme, %d slices: k_oz_split, "
+                      "%d int8 GEMMs per mat-vec on cuBLASLt IMMA, k_oz_combine<%d>)" % (OZAKI_SLICES, OZAKI_SLICES,
+                                                                                         OZAKI_SLICES),
+            "bound": "int8_tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s", "frac": i8_ach / i8_peak,
+            "peak_source": i8_src, "int8_ops_per_step": i8_ops, "products_per_matvec": nprod,
+            "fp64_equivalent_tflops": fm["matvec"] / (mv_ms * 1e-3) / 1e12,
+            "fp64_equivalent_vs_dmma_peak": fm["matvec"] / (mv_ms * 1e-3) / 1e12 / DMMA_PEAK_MEASURED,
+            "ms_per_step": mv_ms, "imma_ms_per_step": kms["ozaki_imma"], "split_ms_per_step": kms["ozaki_split"],
+            "combine_ms_per_step": kms["ozaki_combine"],
+            "library_launches_per_step": (iters + 2) * OZAKI_SLICES}
     shares = {c: round(kms[c] / ms_step, 4) for c in kms}
 
     line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if args.mode == "replicas" else "strong", "vs_baseline": None,
-            "dtype": "fp32+fp64", "data": "synthetic",
+            "dtype": "fp32+fp64+i8" if ozaki else "fp32+fp64", "data": "synthetic",
             "config": {"workload": spec.name, "L": L, "N": N, "n2": n2, "n2_tau_only": L - Ntau,
                        "tau": spec.tau, "n_min": spec.n_min, "seed": args.seed, "gcr_iters": iters,
                        "kernel_dim": kd, "gcr_true_rel_res": tres,

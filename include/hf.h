@@ -249,10 +249,31 @@ hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
                           int64_t ncol, const double *B, double *X, double tol, int32_t max_iter,
                           int32_t *iters_host, double *hist_host, int32_t hist_len);
 
+/* The block mat-vec of Alg. 5 alone (P:507's "SpMM in higher
+ * precision"): Z = K W for a SYMMETRIC K (L x L, ld; the Ozaki path reads row m
+ * as column m), W: L x n (ldw), Z: L x n (ldz), all DEVICE FP64.  matvec 1 = FP64
+ * DMMA, 2 = FP64 emulated on the int8 tensor cores with `slices` slices (0 = 8;
+ * see hf_gcr_opts).  Synchronises. */
+hf_status hf_matvec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const double *W, int64_t ldw, int64_t n,
+                    double *Z, int64_t ldz, int32_t matvec, int32_t slices);
+
 /* ------------------------ a4-a6: block GCR + Schur */
 typedef struct {
     double tol;        /* per-column recursive ||r||_2/||b||_2 target [R13] (1e-14) */
     int32_t max_iter;  /* iteration cap (100)                                       */
+    /* the FP64 block mat-vec K11 W (P:507's "SpMM in higher precision"):
+     *   1: FP64 DMMA tensor-core GEMM;
+     *   2: FP64 emulated on the int8 tensor cores (Ozaki scheme, ozaki.cu): K's
+     *      rows and W's columns split into `slices` exact 7-bit fixed-point
+     *      slices under a power-of-two scale, every slice product an exact
+     *      int8 GEMM, the products with p + q <= slices + 1 summed exactly per
+     *      group and the groups in FP64 -- error below
+     *      ~2^(-7 slices) Lk max|K_m.| max|W_.c| per entry (8 slices: 2^-56,
+     *      against FP64's Lk 2^-53 |K||W|);
+     *   0: automatic = 2 when the block has >= 32 columns, else 1.
+     * The environment variable HF_MATVEC=dmma|ozaki overrides 0.             */
+    int32_t matvec;
+    int32_t slices;    /* matvec 2: slices per operand, 2..9 (0 = 8)               */
 } hf_gcr_opts;
 typedef struct {
     int32_t iters;                 /* completed block-GCR iterations          */

@@ -76,8 +76,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             os.remove(o)
     if force or jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         _, libdir = _nccl_dirs()
+        cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, f"-L{libdir}", "-l:libnccl.so.2",
-               "-Xlinker", f"-rpath={libdir}", "-lcudart"]
+               "-Xlinker", f"-rpath={libdir}", f"-L{cudalib}", "-l:libcublasLt.so.12", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

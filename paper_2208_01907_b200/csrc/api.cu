@@ -10,30 +10,14 @@
 #include "hf_internal.cuh"
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
+#include "ozaki.cuh"
 
 namespace {
 
 thread_local std::string g_noctx_error;
 std::atomic<uint64_t> g_ctx_serial{0};
 
-// switches to the context's device for the duration of a call and restores the
-// caller's current device (every launch and kernel attribute of a call then
-// targets ctx->device whatever device the caller has current)
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(const hf_ctx *ctx) {
-        if (!ctx) return;
-        if (cudaGetDevice(&prev) != cudaSuccess) {
-            prev = -1;
-            return;
-        }
-        if (prev != ctx->device) cudaSetDevice(ctx->device);
-        else prev = -1;
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
+using hf::DeviceGuard;
 
 template <typename F>
 hf_status guarded(hf_ctx *ctx, F &&f) {
@@ -257,6 +241,26 @@ hf_status hf_upload_lower(hf_ctx *ctx, int64_t L, const double *Kbar_host, int64
     });
 }
 
+hf_status hf_matvec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const double *W, int64_t ldw, int64_t n,
+                    double *Z, int64_t ldz, int32_t matvec, int32_t slices) {
+    if (!ctx) return HF_ERR_INVALID_ARG;
+    return guarded(ctx, [&] {
+        HF_REQUIRE(L >= 0 && n >= 0 && ld >= L && ldw >= L && ldz >= L && (matvec == 1 || matvec == 2) &&
+                       (slices == 0 || (slices >= 2 && slices <= 9)) && (L == 0 || n == 0 || (K && W && Z)),
+                   "hf_matvec: bad arguments");
+        if (L == 0 || n == 0) return;
+        if (matvec == 1) {
+            hf::DBuf<double> work;
+            hf::dgemm(ctx, false, L, n, L, 1.0, K, ld, W, ldw, 0.0, Z, ldz, nullptr, &work);
+        } else {
+            hf::Ozaki oz;
+            hf::ozaki_prepare(ctx, oz, K, ld, L, nullptr, slices > 0 ? slices : hf::ozaki_slices(), n);
+            hf::ozaki_matvec(ctx, oz, W, ldw, n, Z, ldz, 0.0, 1.0);
+        }
+        HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 hf_status hf_scale_full(hf_ctx *ctx, int64_t L, double *K, int64_t ld, double *q) {
     if (!ctx) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {
@@ -438,7 +442,7 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
                        hf_gcr_info *info_host) {
     if (!ctx || !lf || !out) return HF_ERR_INVALID_ARG;
     *out = nullptr;
-    hf_gcr_opts o{1e-14, 100};
+    hf_gcr_opts o{1e-14, 100, 0, 0};
     if (opts) o = *opts;
     hf_gcr_info info{0, 0.0, 0.0};
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
@@ -446,6 +450,8 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
         HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr: bad arguments");
 
         HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr: tol > 0, max_iter >= 1");
+        HF_REQUIRE(o.matvec >= 0 && o.matvec <= 2 && (o.slices == 0 || (o.slices >= 2 && o.slices <= 9)),
+                   "hf_schur_gcr: matvec in 0..2, slices 0 or 2..9");
         hy->K = K;
         hy->ld = ld;
         hy->L = lf->L;
@@ -474,7 +480,7 @@ hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
                           double *S22lo_host_or_null, hf_gcr_info *info_host) {
     if (!ctx || !lf || !out) return HF_ERR_INVALID_ARG;
     *out = nullptr;
-    hf_gcr_opts o{1e-28, 100};
+    hf_gcr_opts o{1e-28, 100, 0, 0};
     if (opts) o = *opts;
     hf_gcr_info info{0, 0.0, 0.0};
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
@@ -511,7 +517,7 @@ hf_status hf_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double 
     hf_status s = guarded(ctx, [&] {
         if (!hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: not a double-double hybrid"};
         if (!hy->hard_done && hy->n2 > 0) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: call hf_factor_hard first"};
-        hf_gcr_opts o{1e-28, 100};
+        hf_gcr_opts o{1e-28, 100, 0, 0};
         hf::hybrid_solve_dd(ctx, hy, b, xhi, xlo, o, &info);
     });
     if (info_host) *info_host = info;
@@ -570,7 +576,7 @@ hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x,
         if (!hy->hard_done && hy->n2 > 0)
             throw hf::Error{HF_ERR_STATE, "hf_solve: call hf_factor_hard first"};
         if (hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve: a double-double hybrid is solved by hf_solve_dd"};
-        hf_gcr_opts o{1e-14, 100};
+        hf_gcr_opts o{1e-14, 100, 0, 0};
         hf::hybrid_solve(ctx, hy, b, x, o, &info);
     });
     if (info_host) *info_host = info;

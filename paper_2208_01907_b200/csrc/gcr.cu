@@ -18,9 +18,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
+#include "ozaki.cuh"
 
 #include <string>
 #include <vector>
@@ -37,7 +39,36 @@ struct GcrWork {
     DBuf<double> dgw, dgw2, chw, chdg;
     DBuf<int> status;
     std::vector<double> *hist = nullptr;   // optional: max relative residual after every iteration
+    Ozaki *oz = nullptr;                   // the mat-vec on the int8 tensor cores (ozaki.cu), else DMMA
+    std::unique_ptr<Ozaki> ozown;
 };
+
+// hf_gcr_opts.matvec: 2 = the Ozaki-scheme mat-vec, 1 = DMMA, 0 = automatic (Ozaki for
+// blocks of >= 32 columns; HF_MATVEC=dmma|ozaki overrides the automatic choice)
+void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, int64_t n,
+                  const hf_gcr_opts &o, GcrWork &w) {
+    if (w.oz) return;
+    int mode = o.matvec;
+    if (mode == 0) {
+        mode = n >= 32 ? 2 : 1;
+        if (const char *e = getenv("HF_MATVEC")) {
+            if (std::string(e) == "dmma") mode = 1;
+            else if (std::string(e) == "ozaki") mode = 2;
+        }
+    }
+    if (mode != 2 || L == 0) return;
+    w.ozown.reset(new Ozaki());
+    try {
+        ozaki_prepare(ctx, *w.ozown, K, ld, L, mask, o.slices > 0 ? o.slices : ozaki_slices(), n);
+    } catch (const Error &e) {
+        // the slices take as much memory as K itself; the automatic choice falls back to
+        // the DMMA product when they do not fit (e.g. C4 beside the FP32 preconditioner)
+        if (e.st != HF_ERR_OOM || o.matvec == 2) throw;
+        w.ozown.reset();
+        return;
+    }
+    w.oz = w.ozown.get();
+}
 
 void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {
     if (need <= w.cap) return;
@@ -60,6 +91,10 @@ void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {
 // Z = mask o (K W)   (K11 W in original row order)
 inline void matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, const double *W,
                    int64_t n, double *Z, double beta, double alpha, GcrWork &w) {
+    if (w.oz) {
+        ozaki_matvec(ctx, *w.oz, W, L, n, Z, L, beta, alpha);
+        return;
+    }
     dgemm(ctx, false, L, n, L, alpha, K, ld, W, L, beta, Z, L, mask, &w.dgw);
 }
 
@@ -77,6 +112,7 @@ double read_res(hf_ctx *ctx, GcrWork &w, int *bad) {
 void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, Precond &pc,
                const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info, GcrWork &w) {
     cudaStream_t st = ctx->stream;
+    setup_matvec(ctx, K, ld, L, mask, n, o, w);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
     w.rn2.alloc(n, st);
@@ -167,6 +203,7 @@ void iterative_refinement(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, c
                           const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info,
                           GcrWork &w) {
     cudaStream_t st = ctx->stream;
+    setup_matvec(ctx, K, ld, L, mask, n, o, w);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
     w.rn2.alloc(n, st);
@@ -417,6 +454,7 @@ extern "C" hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, c
                                      int64_t ncol, const double *B, double *X, double tol, int32_t max_iter,
                                      int32_t *iters_host, double *hist_host, int32_t hist_len) {
     if (!ctx || !lf) return HF_ERR_INVALID_ARG;
+    hf::DeviceGuard dg(ctx);
     try {
         const int64_t L = lf->L;
         if (!(method >= 0 && method <= 2) || ncol < 0 || ld < L || tol <= 0.0 || max_iter < 1 ||
@@ -433,7 +471,7 @@ extern "C" hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, c
         hf::DBuf<double> Bm;
         Bm.alloc((size_t)L * ncol, st);
         for (int64_t c = 0; c < ncol; ++c) hf::mask_vec(ctx, L, mask.p, B + c * L, Bm.p + c * L);
-        hf_gcr_opts o{tol, max_iter};
+        hf_gcr_opts o{tol, max_iter, 0, 0};
         hf_gcr_info info{0, 0.0, 0.0};
         std::vector<double> hist;
         int32_t iters = 0;

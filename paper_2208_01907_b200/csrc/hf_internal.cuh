@@ -153,6 +153,25 @@ struct hf_ctx {
 
 namespace hf {
 
+// switches to the context's device for the duration of a call and restores the
+// caller's current device (every launch and kernel attribute of a call then
+// targets ctx->device whatever device the caller has current)
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const hf_ctx *ctx) {
+        if (!ctx) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            return;
+        }
+        if (prev != ctx->device) cudaSetDevice(ctx->device);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // RAII timer around launches of one kernel class (only when profiling).
 // flops / bytes: the ALGORITHMIC work of the launches it brackets (what the method
 // must compute, e.g. only the lower-triangle entries of a trailing update), summed

@@ -25,7 +25,7 @@ _NAMES = {0: "HF_OK", 1: "HF_ERR_INVALID_ARG", 2: "HF_ERR_CUDA", 3: "HF_ERR_NCCL
 
 EXPORTED = [
     "hf_create", "hf_create_dist", "hf_nccl_unique_id", "hf_destroy", "hf_last_error",
-    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_scale_host", "hf_upload_lower", "hf_factor_lowprec",
+    "hf_set_profiling", "hf_kernel_stats", "hf_kernel_work", "hf_chain_exchange_floor", "hf_launch_count", "hf_scale", "hf_scale_host", "hf_upload_lower", "hf_matvec", "hf_factor_lowprec",
     "hf_lowfactor_export", "hf_lowfactor_destroy", "hf_schur_gcr", "hf_hybrid_export",
     "hf_factor_hard", "hf_hard_export", "hf_solve", "hf_hybrid_destroy", "hf_trim_cache",
     "hf_precond_apply", "hf_shard_cols", "hf_set_virtual_rank", "hf_set_stage1_partitions",
@@ -47,7 +47,11 @@ class lowprec_opts(ctypes.Structure):
 
 
 class gcr_opts(ctypes.Structure):
-    _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32)]
+    _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("matvec", ctypes.c_int32),
+                ("slices", ctypes.c_int32)]
+
+
+MATVEC = {"auto": 0, "dmma": 1, "ozaki": 2}
 
 
 class gcr_info(ctypes.Structure):
@@ -82,6 +86,7 @@ def load() -> ctypes.CDLL:
         "hf_scale": [vp, i64, vp, i64, vp],
         "hf_scale_host": [vp, i64, vp, i64, vp, i64, vp, vp],
         "hf_upload_lower": [vp, i64, vp, i64, vp, i64, vp],
+        "hf_matvec": [vp, i64, vp, i64, vp, i64, i64, vp, i64, i32, i32],
         "hf_scale_full": [vp, i64, vp, i64, vp],
         "hf_factor_lowprec": [vp, i64, vp, i64, ctypes.POINTER(lowprec_opts), ctypes.POINTER(vp), pi64, pi64, pi64],
         "hf_lowfactor_export": [vp, vp, vp, vp, vp, i64],
@@ -294,6 +299,21 @@ def hf_upload_lower(ctx: Context, Kbar_host: torch.Tensor, K: torch.Tensor) -> i
     return int(nb.value)
 
 
+def hf_matvec(ctx: Context, K: torch.Tensor, W: torch.Tensor, matvec: str = "ozaki", slices: int = 0) -> torch.Tensor:
+    """Z = K W for a symmetric device FP64 K (L x L) and W (L x n as a column-major
+    matrix: a (n, L) contiguous tensor, i.e. W.T of a row-major L x n); returns Z in the
+    same (n, L) layout.  matvec "dmma" or "ozaki"."""
+    _dev(K, torch.float64)
+    _dev(W, torch.float64)
+    L = K.shape[0]
+    n = W.shape[0]
+    if W.shape[1] != L or not W.is_contiguous():
+        raise ValueError("W must be a contiguous (n, L) tensor")
+    Z = torch.empty_like(W)
+    ctx.check(ctx.lib.hf_matvec(ctx.h, L, _ptr(K), L, _ptr(W), L, n, _ptr(Z), L, MATVEC[matvec], int(slices)))
+    return Z
+
+
 def hf_scale_full(ctx: Context, K: torch.Tensor) -> torch.Tensor:
     """NEXT-3: in-place scaling of a general matrix (memory = column-major K); returns q."""
     _dev(K, torch.float64)
@@ -470,10 +490,12 @@ def hf_krylov_solve(ctx: Context, K: torch.Tensor, lf: LowFactor, B: torch.Tenso
 
 
 def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-14, max_iter: int = 100,
-                 want_S22_host: bool = False, accept_failure: bool = False):
-    """Returns (Hybrid, GcrInfo, S22 host np.ndarray or None)."""
+                 want_S22_host: bool = False, accept_failure: bool = False, matvec: str = "auto",
+                 slices: int = 0):
+    """Returns (Hybrid, GcrInfo, S22 host np.ndarray or None).  matvec: "auto" | "dmma" |
+    "ozaki" (hf_gcr_opts.matvec), slices: the Ozaki slices (0 = default)."""
     _dev(K, torch.float64)
-    o = gcr_opts(float(tol), int(max_iter))
+    o = gcr_opts(float(tol), int(max_iter), MATVEC[matvec], int(slices))
     info = gcr_info()
     h = ctypes.c_void_p()
     S = np.empty((lf.n2, lf.n2), dtype=np.float64, order="F") if (want_S22_host and lf.n2) else None
@@ -490,7 +512,7 @@ def hf_schur_gcr_dd(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1
     """NEXT-1: block GCR + Schur complement in double-double with the FP64 factor lf
     (prec = 64) as preconditioner.  Returns (Hybrid, GcrInfo, (S22hi, S22lo) host or None)."""
     _dev(K, torch.float64)
-    o = gcr_opts(float(tol), int(max_iter))
+    o = gcr_opts(float(tol), int(max_iter), 0, 0)
     info = gcr_info()
     h = ctypes.c_void_p()
     want = want_S22_host and lf.n2

@@ -47,6 +47,7 @@ def _gpu_path(ctx, spec, Kb):
     lf = hf.hf_factor_lowprec(ctx, Kd, tau=spec.tau, n_min=spec.n_min)
     hy, info, S22 = hf.hf_schur_gcr(ctx, Kd, lf, want_S22_host=True)
     kd = hf.hf_factor_hard(ctx, hy)
+    hf.hf_trim_cache(0)   # the library's cached workspaces (the mat-vec slices: as large as K) go back
     return Kd, lf, hy, info, S22, kd
 
 
