@@ -75,6 +75,42 @@ def flop_model(L, N, Ntau, n2, iters, ozaki=False):
             "dmma": dmma, "matvec": matvec, "trsm": (iters + 1) * pc}
 
 
+def trsm_roofline(N, n2, iters, flops, ms, setup_ms, ach, nbytes):
+    """The FP32 preconditioner's roofline.  Default form (k_trsm_blk.cu): blocked solves whose
+    products run on the bf16 tensor cores as six exact-part products each (FP32 precision);
+    its executed bf16 work per application is 6 x (the diagonal-block inverse products + the
+    off-diagonal updates) x 2 directions on the padded size Nb = nb BS, BS = 2048 (the
+    k_trsm_blk.cu rule), against the measured bf16 peak; the FP32-equivalent rate is
+    reported against the FFMA peak.  HF_PRECOND=dataflow: the FFMA2 dataflow kernels."""
+    if os.environ.get("HF_PRECOND") == "dataflow":
+        return {"kernel": "k_trsm<fwd/bwd> (FP32 FFMA2 dataflow triangular solves, n2 right-hand sides)",
+                "bound": "alu", "achieved": ach, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
+                "frac": ach / FFMA_PEAK_DERIVED if ach else None, "flops_per_step": flops, "ms_per_step": ms,
+                "hbm_gbs": nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None, "setup_ms_per_step": setup_ms}
+    BS = 64
+    while BS < 2048 and BS < N:
+        BS *= 2
+    nb = -(-N // BS)
+    Nb = nb * BS
+    ncp = -(-n2 // 8) * 8
+    per_dir = nb * 2.0 * BS * BS * ncp + sum(2.0 * (Nb - (j + 1) * BS) * BS * ncp for j in range(nb - 1))
+    bf16_fl = 6 * 2 * per_dir * (iters + 1)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bpk, src = float(json.load(f)["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (burst)"
+    except Exception:
+        bpk, src = 2250.0, "nominal B200 dense bf16"
+    b_ach = bf16_fl / (ms * 1e-3) / 1e12 if ms > 0 else None
+    return {"kernel": "blocked FP32 preconditioner (k_trsm_blk.cu: %d-row diagonal-block inverses + "
+                      "off-diagonal updates, each product as 6 exact bf16-part GEMMs on cuBLASLt, FP32 "
+                      "accumulation; k_blk_split_rows / gather / dscale / scatter)" % BS,
+            "bound": "bf16_tensor", "achieved": b_ach, "peak": bpk, "unit": "TFLOP/s",
+            "frac": b_ach / bpk if b_ach else None, "peak_source": src, "bf16_flops_per_step": bf16_fl,
+            "fp32_equivalent_tflops": ach, "fp32_equivalent_vs_ffma_peak": ach / FFMA_PEAK_DERIVED if ach else None,
+            "flops_per_step": flops, "ms_per_step": ms, "block_rows": BS, "blocks": nb,
+            "hbm_gbs": nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None, "setup_ms_per_step": setup_ms}
+
+
 class Clocks:
     """Clock / throttle-reason sampler for the timed region.  NVML in-process
     (the same counters nvidia-smi's clocks line reads: clocks.sm, clocks.max.sm,
@@ -472,12 +508,8 @@ def main():
                   ("" if ozaki else "mat-vecs on N = |Lambda_1| rows, "),
                   "executed_flops_per_step": kwork["dgemm"][0], "ms_per_step": dg_ms,
                   "peak_source": "measured DMMA microbenchmark (tools/peaks.py, profiles/peaks_r01.json)"},
-        "trsm": {"kernel": "k_trsm<fwd/bwd> (FP32 FFMA2 dataflow triangular solves, n2 right-hand sides)",
-                 "bound": "alu", "achieved": trsm_ach, "peak": FFMA_PEAK_DERIVED, "unit": "TFLOP/s",
-                 "frac": trsm_ach / FFMA_PEAK_DERIVED if trsm_ach else None,
-                 "flops_per_step": kwork["trsm"][0], "ms_per_step": ts_ms,
-                 "hbm_gbs": kwork["trsm"][1] / (ts_ms * 1e-3) / 1e9 if ts_ms > 0 else None,
-                 "setup_ms_per_step": kms["trsm_setup"]},
+        "trsm": trsm_roofline(N, n2, iters, kwork["trsm"][0], ts_ms, kms["trsm_setup"], trsm_ach,
+                              kwork["trsm"][1]),
         "chain": {"kernel": "k_chain (cooperative persistent pivot chain, one launch per panel)",
                   "bound": "latency", "us_per_pivot": ch_ms * 1e3 / max(Ntau, 1), "ms_per_step": ch_ms,
                   "exchange_floor_us": xfloor, "frac_of_floor": (xfloor / (ch_ms * 1e3 / max(Ntau, 1)))

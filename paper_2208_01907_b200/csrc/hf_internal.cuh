@@ -240,10 +240,24 @@ struct PrecondT {
     DBuf<int> pflags;
     DBuf<unsigned long long> dbg;
 };
+// the blocked 3xTF32 form of the FP32 preconditioner (k_trsm_blk.cu)
+struct PrecondBlk {
+    int64_t N = 0, L = 0, Nb = 0, BS = 0;
+    int nb = 0;
+    const float *D = nullptr;
+    const int64_t *perm = nullptr;
+    const int32_t *pos1 = nullptr;
+    DBuf<uint16_t> Lpart[3];       // Nb x Nb: padded L as three exact bfloat16 parts (lower tiles)
+    DBuf<uint16_t> Ipart[3];       // diagonal-block inverses (parts), block j at j BS (BS + 1), ld BS
+    DBuf<float> X, Y;              // Nb x ncp FP32 workspaces (column-major)
+    DBuf<uint16_t> Spart[3];       // Nb x ncp: bf16 parts of the current block's operand
+};
 struct Precond {
     int prec = 32;
+    bool blk = false;              // FP32, symmetric: the blocked tensor-core solve
     PrecondT<float> f;
     PrecondT<double> d;
+    PrecondBlk b;
 };
 }  // namespace hf
 

@@ -30,6 +30,14 @@ void dgemm(hf_ctx *ctx, bool transA, int64_t M, int64_t N, int64_t K, double alp
            int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
            const uint8_t *rowmask, DBuf<double> *work, int splits = 0);
 
+// the blocked tensor-core form of the FP32 preconditioner (k_trsm_blk.cu; HF_PRECOND=dataflow
+// selects the k_trsm.cu dataflow kernels instead)
+bool precond_blocked_enabled();
+void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const float *Lfac, const float *D,
+                       const int64_t *perm, const int32_t *pos1);
+void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R, int64_t ldr, double *W,
+                       int64_t ldw);
+
 // FP32 preconditioner Q^{-1} (k_trsm.cu); struct Precond is in hf_internal.cuh
 void precond_setup(hf_ctx *ctx, Precond &p, const hf_lowfactor *lf);
 // W (L x ncol, original order, ldw) = Q^{-1} R (R: L x ncol, original order, ldr);

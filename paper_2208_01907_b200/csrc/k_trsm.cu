@@ -149,6 +149,11 @@ using T = double;
 // ------------------------------------------------------------------ precision dispatch
 void precond_setup(hf_ctx *ctx, Precond &p, const hf_lowfactor *lf) {
     p.prec = lf->prec;
+    p.blk = lf->prec != 64 && !lf->nonsym && precond_blocked_enabled();
+    if (p.blk) {
+        precond_blk_setup(ctx, p.b, lf->N, lf->L, lf->Lfac.p, lf->D.p, lf->perm.p, lf->pos1.p);
+        return;
+    }
     if (lf->prec == 64)
         p64::precond_setup_t(ctx, p.d, lf->N, lf->L, lf->Lfac64.p, lf->D64.p, lf->perm.p, lf->pos1.p);
     else
@@ -157,7 +162,8 @@ void precond_setup(hf_ctx *ctx, Precond &p, const hf_lowfactor *lf) {
 }
 
 void precond_apply(hf_ctx *ctx, Precond &p, int64_t ncol, const double *R, int64_t ldr, double *W, int64_t ldw) {
-    if (p.prec == 64) p64::precond_apply_t(ctx, p.d, ncol, R, ldr, W, ldw);
+    if (p.blk) precond_blk_apply(ctx, p.b, ncol, R, ldr, W, ldw);
+    else if (p.prec == 64) p64::precond_apply_t(ctx, p.d, ncol, R, ldr, W, ldw);
     else p32::precond_apply_t(ctx, p.f, ncol, R, ldr, W, ldw);
 }
 

@@ -1,0 +1,280 @@
+// k_trsm_blk.cu -- the lower-precision preconditioner Q^{-1} = L^{-T} D^{-1} L^{-1} of
+// P:242 / P:506 ("forward/backward substitution in lower precision ... BLAS level 3
+// TRSM") as a BLOCKED solve whose work is tensor-core GEMMs:
+//
+//   forward  L Y = R:  for j = 0..nb-1:  Y_j = Linv_j R_j;   R_{>j} -= L_{>j,j} Y_j
+//   Z = D^{-1} Y
+//   backward L^T X = Z: for j = nb-1..0: X_j = Linv_j^T Z_j; Z_{<j} -= (L_{j,<j})^T X_j
+//
+// with blocks of BS = 2048 rows (nb = 8 at C2), Linv_j the inverse of the unit lower
+// diagonal block L_jj (formed once per factorization by recursive doubling from the
+// 64 x 64 inverses: inv([A 0; C B]) = [A^-1 0; -B^-1 C A^-1  B^-1], FP32 GEMMs), and
+// every product in FP32 precision on the BF16 tensor cores by an exact three-way split
+// x = x1 + x2 + x3 (x1 = RN_bf16(x), x2 = RN_bf16(x - x1), x3 = x - x1 - x2: 3 x 8 bits
+// hold FP32's 24 exactly) and the six products with i + j <= 4:
+//   A B ~= A1 B1 + (A1 B2 + A2 B1) + (A1 B3 + A3 B1 + A2 B2)   (FP32 accumulation,
+//   summed from the smallest; the dropped A2 B3 + A3 B2 + A3 B3 are ~2^-25 |A||B|, below
+//   FP32's unit roundoff; an exactly representable identity block stays exact).
+// The sequential chain of the substitution is nb GEMM pairs per direction instead
+// of N / 64 dependent 64-row links (k_trsm.cu), and the products run at tensor-core
+// rate.  Any summation order is allowed for the preconditioner [R12]; the L factor
+// and D are the FP32 ones of stage 1, pivot order, unchanged.
+//
+// Operand layouts (column-major, ld Nb = nb BS; L padded with the identity):
+//   L1..L3  Nb x Nb bf16 parts, only the tiles on / below the diagonal are read;
+//   I1..I3  block j's BS x BS inverse at j BS (BS + 1) with ld BS (the FP32 inverse is
+//           built there first: the diagonal offset g of any doubling pair maps to
+//           g (BS + 1), so the pairs of one level across all blocks form ONE strided
+//           batched GEMM);
+//   X, Y (FP32), S1..S3 (bf16 parts of the current block)  Nb x ncp, the right-hand
+//           sides in pivot order (ncp = ncol rounded to 8).
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "k_dgemm.cuh"
+#include "lt.cuh"
+
+using bf16 = __nv_bfloat16;
+
+namespace hf {
+namespace {
+
+// x = p1 + p2 + p3 exactly, each a bfloat16 (round to nearest at every step)
+__device__ __forceinline__ void split3(float x, bf16 &p1, bf16 &p2, bf16 &p3) {
+    p1 = __float2bfloat16_rn(x);
+    const float r = x - __bfloat162float(p1);   // exact
+    p2 = __float2bfloat16_rn(r);
+    p3 = __float2bfloat16_rn(r - __bfloat162float(p2));   // exact: at most 8 bits remain
+}
+
+// Lp (Nb x Nb) = Lfac (N x N, ld N) padded with the identity; lower 32 x 32 tiles only
+__global__ void __launch_bounds__(256) k_blk_pad(int64_t N, int64_t Nb, const float *__restrict__ Lf,
+                                                 float *__restrict__ Lp) {
+    if (blockIdx.x < blockIdx.y) return;
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int q = ty; q < 32; q += 8) {
+        const int64_t i = i0 + tx, j = j0 + q;
+        Lp[i + j * Nb] = (i < N && j < N) ? Lf[i + j * N] : (i == j ? 1.f : 0.f);
+    }
+}
+
+// inverse of each 64 x 64 unit lower diagonal block of Lp into the packed Inv (column j of
+// the inverse by forward substitution, one thread per column)
+__global__ void __launch_bounds__(64) k_blk_inv64(int64_t Nb, const float *__restrict__ Lp, int64_t BS,
+                                                  float *__restrict__ Inv) {
+    __shared__ float Ls[64][65], Xs[64][65];
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    const int j = threadIdx.x;
+    for (int i = 0; i < 64; ++i) Ls[i][j] = Lp[(r0 + i) + (r0 + j) * Nb];
+    __syncthreads();
+    for (int i = 0; i < 64; ++i) {
+        float s = (i == j) ? 1.f : 0.f;
+        if (i > j)
+            for (int k = j; k < i; ++k) s = __fmaf_rn(-Ls[i][k], Xs[k][j], s);
+        Xs[i][j] = (i < j) ? 0.f : s;
+    }
+    __syncthreads();
+    float *dst = Inv + r0 * (BS + 1);   // diagonal offset r0 -> packed r0 (BS + 1)
+    for (int i = 0; i < 64; ++i) dst[i + (int64_t)j * BS] = Xs[i][j];
+}
+
+// n elements of x -> the three bf16 parts
+__global__ void k_blk_split_all(int64_t n, const float *__restrict__ x, bf16 *__restrict__ p1, bf16 *__restrict__ p2,
+                                bf16 *__restrict__ p3) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        split3(x[e], p1[e], p2[e], p3[e]);
+}
+
+// the lower 32 x 32 tiles of the Nb x Nb matrix x -> the three bf16 parts
+__global__ void __launch_bounds__(256) k_blk_split_lower(int64_t Nb, const float *__restrict__ x,
+                                                         bf16 *__restrict__ p1, bf16 *__restrict__ p2,
+                                                         bf16 *__restrict__ p3) {
+    if (blockIdx.x < blockIdx.y) return;
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int q = ty; q < 32; q += 8) {
+        const int64_t e = (i0 + tx) + (j0 + q) * Nb;
+        split3(x[e], p1[e], p2[e], p3[e]);
+    }
+}
+
+// rows [r0, r0 + nr) x ncp columns of X (ld) -> the parts (same positions)
+__global__ void k_blk_split_rows(int64_t r0, int64_t nr, int64_t ncp, const float *__restrict__ X, int64_t ld,
+                                 bf16 *__restrict__ p1, bf16 *__restrict__ p2, bf16 *__restrict__ p3) {
+    const int64_t total = nr * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = (r0 + e % nr) + (e / nr) * ld;
+        split3(X[q], p1[q], p2[q], p3[q]);
+    }
+}
+
+// X (Nb x ncp, pivot order) = RN32(R[perm]) (FP64 -> FP32 truncation), zero padding
+__global__ void k_blk_gather(int64_t N, int64_t Nb, int64_t ncol, int64_t ncp, const int64_t *__restrict__ perm,
+                             const double *__restrict__ R, int64_t ldr, float *__restrict__ X) {
+    const int64_t total = Nb * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % Nb, c = e / Nb;
+        X[e] = (i < N && c < ncol) ? __double2float_rn(R[perm[i] + c * ldr]) : 0.f;
+    }
+}
+
+// Y <- D^{-1} Y (rows < N; IEEE quotient)
+__global__ void k_blk_dscale(int64_t N, int64_t Nb, int64_t ncp, const float *__restrict__ D, float *__restrict__ Y) {
+    const int64_t total = Nb * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % Nb;
+        if (i < N) Y[e] = __fdiv_rn(Y[e], D[i]);
+    }
+}
+
+// W (L x ncol, original order, FP64) = lift(X[pos1]), 0 on Lambda_2 rows
+__global__ void k_blk_scatter(int64_t L, int64_t Nb, int64_t ncol, const int32_t *__restrict__ pos1,
+                              const float *__restrict__ X, double *__restrict__ W, int64_t ldw) {
+    const int64_t total = L * ncol;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % L, c = e / L;
+        const int32_t r = pos1[i];
+        W[i + c * ldw] = r >= 0 ? (double)X[r + c * Nb] : 0.0;
+    }
+}
+
+unsigned grid_for(hf_ctx *ctx, int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
+}
+
+// C = alpha A B + beta C in FP32 precision: the six bf16 part products with i + j <= 4,
+// smallest first
+void gemm6(hf_ctx *ctx, bool tA, int64_t m, int64_t n, int64_t k, float alpha, bf16 *const A[3], int64_t lda,
+           bf16 *const B[3], int64_t ldb, float beta, float *C, int64_t ldc) {
+    static const int ord[6][2] = {{2, 0}, {0, 2}, {1, 1}, {1, 0}, {0, 1}, {0, 0}};
+    for (int q = 0; q < 6; ++q)
+        lt_bgemm(ctx, tA, m, n, k, alpha, A[ord[q][0]], lda, B[ord[q][1]], ldb, q ? 1.f : beta, C, ldc);
+}
+
+}  // namespace
+
+bool precond_blocked_enabled() {
+    const char *e = getenv("HF_PRECOND");
+    return !(e && std::string(e) == "dataflow");
+}
+
+void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const float *Lfac, const float *D,
+                       const int64_t *perm, const int32_t *pos1) {
+    cudaStream_t st = ctx->stream;
+    p.N = N;
+    p.L = L;
+    p.D = D;
+    p.perm = perm;
+    p.pos1 = pos1;
+    if (N == 0) return;
+    int64_t bsmax = 2048;   // HF_PRECOND_BS: tuning (a power of two times 64)
+    if (const char *e = getenv("HF_PRECOND_BS")) bsmax = std::max<int64_t>(64, atoll(e));
+    int64_t BS = 64;
+    while (BS < bsmax && BS < N) BS *= 2;
+    p.BS = BS;
+    p.nb = (int)cdiv(N, BS);
+    p.Nb = p.nb * BS;
+    const int64_t Nb = p.Nb;
+    ClassTimer tm(ctx, "trsm_setup");
+    const size_t ninv = (size_t)p.nb * BS * (BS + 1);
+    DBuf<float> Lp, Inv, T;   // FP32 working copies, released after the split
+    Lp.alloc((size_t)Nb * Nb, st);
+    Inv.alloc(ninv, st);
+    T.alloc((size_t)Nb * BS / 4 + 1, st);
+    HF_CUDA(cudaMemsetAsync(Inv.p, 0, ninv * sizeof(float), st));
+    dim3 g((unsigned)(Nb / 32), (unsigned)(Nb / 32));
+    k_blk_pad<<<g, 256, 0, st>>>(N, Nb, Lfac, Lp.p);
+    HF_CHECK_LAUNCH(ctx);
+    k_blk_inv64<<<(unsigned)(Nb / 64), 64, 0, st>>>(Nb, Lp.p, BS, Inv.p);
+    HF_CHECK_LAUNCH(ctx);
+    // recursive doubling, IEEE FP32 GEMMs: all pairs of one level in one batched call each
+    for (int64_t h = 64; h < BS; h *= 2) {
+        const int batch = (int)(Nb / (2 * h));
+        const int64_t sd = 2 * h * (BS + 1), sl = 2 * h * (Nb + 1);
+        // T_p = C_p Ainv_p,  C_p = L[g+h : g+2h, g : g+h]
+        lt_sgemm(ctx, false, false, h, h, h, 1.f, Lp.p + h, Nb, sl, Inv.p, BS, sd, 0.f, T.p, h, h * h, batch, false);
+        // Inv[g+h : g+2h, g : g+h] = -Binv_p T_p
+        lt_sgemm(ctx, false, false, h, h, h, -1.f, Inv.p + h * (BS + 1), BS, sd, T.p, h, h * h, 0.f, Inv.p + h, BS, sd,
+                 batch, false);
+    }
+    for (int q = 0; q < 3; ++q) {
+        p.Lpart[q].alloc((size_t)Nb * Nb, st);
+        p.Ipart[q].alloc(ninv, st);
+    }
+    auto P = [](DBuf<uint16_t> &b) { return reinterpret_cast<bf16 *>(b.p); };
+    k_blk_split_all<<<grid_for(ctx, (int64_t)ninv), 256, 0, st>>>((int64_t)ninv, Inv.p, P(p.Ipart[0]), P(p.Ipart[1]),
+                                                                  P(p.Ipart[2]));
+    HF_CHECK_LAUNCH(ctx);
+    k_blk_split_lower<<<g, 256, 0, st>>>(Nb, Lp.p, P(p.Lpart[0]), P(p.Lpart[1]), P(p.Lpart[2]));
+    HF_CHECK_LAUNCH(ctx);
+}
+
+void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R, int64_t ldr, double *W,
+                       int64_t ldw) {
+    cudaStream_t st = ctx->stream;
+    if (ncol == 0) return;
+    if (p.N == 0) {
+        HF_CUDA(cudaMemset2DAsync(W, ldw * sizeof(double), 0, p.L * sizeof(double), ncol, st));
+        return;
+    }
+    const int64_t Nb = p.Nb, BS = p.BS, ncp = (ncol + 7) / 8 * 8;
+    p.X.alloc((size_t)Nb * ncp, st);
+    p.Y.alloc((size_t)Nb * ncp, st);
+    for (int q = 0; q < 3; ++q) p.Spart[q].alloc((size_t)Nb * ncp, st);
+    const double nn = (double)p.N * (double)p.N;
+    ClassTimer tm(ctx, "trsm", st, 2.0 * nn * (double)ncol, 6.0 * nn + 16.0 * (double)p.N * (double)ncol);
+    float *X = p.X.p, *Y = p.Y.p;
+    auto P = [](DBuf<uint16_t> &b) { return reinterpret_cast<bf16 *>(b.p); };
+    bf16 *S[3] = {P(p.Spart[0]), P(p.Spart[1]), P(p.Spart[2])};
+    auto Loff = [&](int64_t off, bf16 *out[3]) {
+        for (int q = 0; q < 3; ++q) out[q] = P(p.Lpart[q]) + off;
+    };
+    auto Ioff = [&](int j, bf16 *out[3]) {
+        for (int q = 0; q < 3; ++q) out[q] = P(p.Ipart[q]) + (size_t)j * BS * (BS + 1);
+    };
+    auto Soff = [&](int64_t r0, bf16 *out[3]) {
+        for (int q = 0; q < 3; ++q) out[q] = S[q] + r0;
+    };
+    auto split = [&](const float *src, int64_t r0, int64_t nr) {
+        k_blk_split_rows<<<grid_for(ctx, nr * ncp), 256, 0, st>>>(r0, nr, ncp, src, Nb, S[0], S[1], S[2]);
+        HF_CHECK_LAUNCH(ctx);
+    };
+    bf16 *A[3], *B[3];
+    k_blk_gather<<<grid_for(ctx, Nb * ncp), 256, 0, st>>>(p.N, Nb, ncol, ncp, p.perm, R, ldr, X);
+    HF_CHECK_LAUNCH(ctx);
+    // forward: L Y = X
+    for (int j = 0; j < p.nb; ++j) {
+        const int64_t j0 = (int64_t)j * BS;
+        split(X, j0, BS);
+        Ioff(j, A);
+        Soff(j0, B);
+        gemm6(ctx, false, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Y + j0, Nb);             // Y_j = Linv_j X_j
+        if (j + 1 < p.nb) {
+            split(Y, j0, BS);
+            const int64_t r1 = j0 + BS;
+            Loff(r1 + j0 * Nb, A);
+            gemm6(ctx, false, Nb - r1, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, X + r1, Nb);   // X_{>j} -= L_{>j,j} Y_j
+        }
+    }
+    k_blk_dscale<<<grid_for(ctx, Nb * ncp), 256, 0, st>>>(p.N, Nb, ncp, p.D, Y);
+    HF_CHECK_LAUNCH(ctx);
+    // backward: L^T X = Y
+    for (int j = p.nb - 1; j >= 0; --j) {
+        const int64_t j0 = (int64_t)j * BS;
+        split(Y, j0, BS);
+        Ioff(j, A);
+        Soff(j0, B);
+        gemm6(ctx, true, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, X + j0, Nb);              // X_j = Linv_j^T Y_j
+        if (j > 0) {
+            split(X, j0, BS);
+            Loff(j0, A);
+            gemm6(ctx, true, j0, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Y, Nb);              // Y_{<j} -= L_{j,<j}^T X_j
+        }
+    }
+    k_blk_scatter<<<grid_for(ctx, p.L * ncol), 256, 0, st>>>(p.L, Nb, ncol, p.pos1, X, W, ldw);
+    HF_CHECK_LAUNCH(ctx);
+}
+
+}  // namespace hf

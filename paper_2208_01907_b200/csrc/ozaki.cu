@@ -27,8 +27,6 @@
 // the concatenated [B_1 .. B_{s+1-p}] (A_p read once per mat-vec), on
 // cuBLASLt's IMMA kernels (a plain library GEMM); the splitting and the
 // combination are the kernels below.
-#include <cublasLt.h>
-
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -38,17 +36,11 @@
 #include <mutex>
 #include <string>
 
+#include "lt.cuh"
 #include "ozaki.cuh"
 
 namespace hf {
 namespace {
-
-#define HF_CUBLAS(x)                                                                                   \
-    do {                                                                                               \
-        cublasStatus_t s_ = (x);                                                                       \
-        if (s_ != CUBLAS_STATUS_SUCCESS)                                                               \
-            throw Error{HF_ERR_CUDA, std::string(#x) + ": cublasLt status " + std::to_string((int)s_)}; \
-    } while (0)
 
 // smallest e with max |x| < 2^e over the masked entries of one vector; 0 for a zero vector
 __device__ __forceinline__ int exp_bound(double mx) {
@@ -156,72 +148,6 @@ __global__ void __launch_bounds__(256) k_oz_combine(int64_t L, int64_t n, const 
     }
 }
 
-struct LtPlan {
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, ld = nullptr;
-    cublasLtMatmulAlgo_t algo;
-};
-
-// one cuBLASLt handle, workspace and plan cache per device, created on first use and
-// kept for the process (never destroyed: no teardown ordering against the CUDA context)
-struct LtState {
-    cublasLtHandle_t h = nullptr;
-    void *ws = nullptr;
-    std::map<std::array<int64_t, 6>, LtPlan> plans;   // (rows, cols, k, lda, ldb, ldd) -> descriptors + algorithm
-    std::mutex mu;                                     // guards plans
-};
-constexpr size_t LT_WS = (size_t)32 << 20;
-
-LtState &lt_state(hf_ctx *ctx) {
-    static std::mutex mu;
-    static LtState *st[256] = {};
-    std::lock_guard<std::mutex> g(mu);
-    LtState *&s = st[ctx->device % 256];
-    if (!s) {
-        std::unique_ptr<LtState> n(new LtState());
-        HF_CUBLAS(cublasLtCreate(&n->h));
-        HF_CUDA(cudaMalloc(&n->ws, LT_WS));
-        s = n.release();
-    }
-    return *s;
-}
-
-// D (rows x cols, int32, ldd) = A^T B, A: k x rows int8 (lda), B: k x cols int8 (ldb);
-// descriptors and the heuristic's algorithm are kept per shape
-void imma(hf_ctx *ctx, int64_t rows, int64_t cols, int64_t k, const int8_t *A, int64_t lda, const int8_t *B,
-          int64_t ldb, int32_t *D, int64_t ldd) {
-    LtState &lt = lt_state(ctx);
-    const size_t wsb = LT_WS;
-    const std::array<int64_t, 6> key{rows, cols, k, lda, ldb, ldd};
-    std::lock_guard<std::mutex> g(lt.mu);
-    auto it = lt.plans.find(key);
-    if (it == lt.plans.end()) {
-        LtPlan pl;
-        HF_CUBLAS(cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
-        const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-        HF_CUBLAS(cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)));
-        HF_CUBLAS(cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)));
-        HF_CUBLAS(cublasLtMatrixLayoutCreate(&pl.la, CUDA_R_8I, (uint64_t)k, (uint64_t)rows, lda));
-        HF_CUBLAS(cublasLtMatrixLayoutCreate(&pl.lb, CUDA_R_8I, (uint64_t)k, (uint64_t)cols, ldb));
-        HF_CUBLAS(cublasLtMatrixLayoutCreate(&pl.ld, CUDA_R_32I, (uint64_t)rows, (uint64_t)cols, ldd));
-        cublasLtMatmulPreference_t pref;
-        HF_CUBLAS(cublasLtMatmulPreferenceCreate(&pref));
-        HF_CUBLAS(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb,
-                                                       sizeof(wsb)));
-        cublasLtMatmulHeuristicResult_t res;
-        int nres = 0;
-        HF_CUBLAS(cublasLtMatmulAlgoGetHeuristic(lt.h, pl.op, pl.la, pl.lb, pl.ld, pl.ld, pref, 1, &res, &nres));
-        cublasLtMatmulPreferenceDestroy(pref);
-        HF_REQUIRE(nres > 0, "ozaki: no cuBLASLt int8 algorithm for this shape");
-        pl.algo = res.algo;
-        it = lt.plans.emplace(key, pl).first;
-    }
-    const LtPlan &pl = it->second;
-    const int32_t one = 1, zero = 0;
-    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &one, A, pl.la, B, pl.lb, &zero, D, pl.ld, D, pl.ld, &pl.algo, lt.ws, wsb,
-                             ctx->stream));   // a library kernel: not in ctx->launches (libhf's own)
-}
-
 }  // namespace
 
 int ozaki_slices() {
@@ -276,7 +202,7 @@ void ozaki_matvec(hf_ctx *ctx, Ozaki &oz, const double *W, int64_t ldw, int64_t 
         int64_t off = 0;
         for (int p = 1; p <= s; ++p) {
             const int64_t nc = (int64_t)(s + 1 - p) * n;
-            imma(ctx, ldA, nc, ldA, oz.A.p + (size_t)(p - 1) * ldA * ldA, ldA, oz.B.p, ldA, oz.C.p + off * ldA, ldA);
+            lt_imma(ctx, ldA, nc, ldA, oz.A.p + (size_t)(p - 1) * ldA * ldA, ldA, oz.B.p, ldA, oz.C.p + off * ldA, ldA);
             off += nc;
         }
     }

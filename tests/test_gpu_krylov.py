@@ -4,7 +4,8 @@ time) and Algorithm 5 (block GCR) with the same FP32 preconditioner and FP64
 mat-vec kernels (hf_krylov_solve), against the oracle's Alg. 3/4/5:
   * the qualitative ordering of Fig. 2: block GCR <= GCR <= IR iterations;
   * iteration counts within one of the oracle's (FP64 rounding of the
-    recurrences differs), solutions normwise within 1e-8 of the oracle's."""
+    recurrences differs) with the dataflow preconditioner, at most one more with
+    the blocked one; solutions normwise within 1e-8 of the oracle's."""
 import numpy as np
 import pytest
 import torch
@@ -25,9 +26,16 @@ def ctx():
     c.close()
 
 
+@pytest.mark.parametrize("precond", ["dataflow", "blocked"])
 @pytest.mark.parametrize("name,seed,ncol", [("P1024", 0, 16), ("N32", 0, 4), ("S24", 0, 8)])
-def test_fig2_ordering_and_oracle(ctx, name, seed, ncol):
+def test_fig2_ordering_and_oracle(ctx, name, seed, ncol, precond, monkeypatch):
+    """precond: the FP32 preconditioner's form.  The dataflow substitution (k_trsm.cu)
+    follows the oracle's iteration counts within one; the blocked tensor-core solve
+    (k_trsm_blk.cu, explicit diagonal-block inverses) applies the same M^-1 with a
+    different FP32 error (DESIGN.md [R12]) and may converge in FEWER iterations (P1024:
+    block GCR 4 vs 6), so for it the bar is at most one MORE than the oracle."""
     from paper_2208_01907_b200 import hf
+    monkeypatch.setenv("HF_PRECOND", precond)
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
     Ko, _ = oracle.scale(Kb.numpy())
@@ -55,10 +63,15 @@ def test_fig2_ordering_and_oracle(ctx, name, seed, ncol):
     Xb, ib = oracle.block_gcr(K11, F, Bp)
     ig = max(oracle.gcr(K11, F, Bp[:, j])[1].iters for j in range(ncol))
     iro = [oracle.iterative_refinement(K11, F, Bp[:, j], max_iter=300)[1] for j in range(ncol)]
-    assert abs(its["bgcr"] - ib.iters) <= 1 and abs(its["gcr"] - ig) <= 1, (its, ib.iters, ig)
-    assert conv["ir"] == all(r.converged for r in iro)
-    if conv["ir"]:
-        assert abs(its["ir"] - max(r.iters for r in iro)) <= 1
+    if precond == "dataflow":
+        assert abs(its["bgcr"] - ib.iters) <= 1 and abs(its["gcr"] - ig) <= 1, (its, ib.iters, ig)
+        assert conv["ir"] == all(r.converged for r in iro)
+        if conv["ir"]:
+            assert abs(its["ir"] - max(r.iters for r in iro)) <= 1
+    else:
+        assert its["bgcr"] <= ib.iters + 1 and its["gcr"] <= ig + 1, (its, ib.iters, ig)
+        if all(r.converged for r in iro):
+            assert conv["ir"] and its["ir"] <= max(r.iters for r in iro) + 1
     for m in ("ir", "gcr", "bgcr"):
         if conv[m]:
             assert np.linalg.norm(xs[m] - Xb) <= 1e-8 * np.linalg.norm(Xb), m

