@@ -102,6 +102,11 @@ hf_status hf_destroy(hf_ctx *ctx) {
         cudaStreamSynchronize(ctx->up);
         cudaStreamDestroy(ctx->up);
     }
+    for (auto a : ctx->aux)
+        if (a) {
+            cudaStreamSynchronize(a);
+            cudaStreamDestroy(a);
+        }
     if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
 #ifdef HF_WITH_NCCL
     if (ctx->comm) ncclCommDestroy(ctx->comm);

@@ -149,6 +149,8 @@ struct hf_ctx {
     cudaStream_t up = nullptr;
     cudaEvent_t up_ev = nullptr;
     bool up_pending = false;
+    // the blocked preconditioner's two helper streams (k_trsm_blk.cu), lazily created
+    cudaStream_t aux[2] = {nullptr, nullptr};
 };
 
 namespace hf {
@@ -240,7 +242,7 @@ struct PrecondT {
     DBuf<int> pflags;
     DBuf<unsigned long long> dbg;
 };
-// the blocked 3xTF32 form of the FP32 preconditioner (k_trsm_blk.cu)
+// the blocked tensor-core form of the FP32 preconditioner (k_trsm_blk.cu)
 struct PrecondBlk {
     int64_t N = 0, L = 0, Nb = 0, BS = 0;
     int nb = 0;
@@ -249,8 +251,17 @@ struct PrecondBlk {
     const int32_t *pos1 = nullptr;
     DBuf<uint16_t> Lpart[3];       // Nb x Nb: padded L as three exact bfloat16 parts (lower tiles)
     DBuf<uint16_t> Ipart[3];       // diagonal-block inverses (parts), block j at j BS (BS + 1), ld BS
-    DBuf<float> X, Y;              // Nb x ncp FP32 workspaces (column-major)
-    DBuf<uint16_t> Spart[3];       // Nb x ncp: bf16 parts of the current block's operand
+    DBuf<uint16_t> Gpart[3];       // G_j = L_{j+1,j} Linv_j (parts), block j at j BS^2, ld BS
+    DBuf<uint16_t> Hpart[3];       // H_j = Linv_{j+1} L_{j+1,j} (parts), block j at j BS^2, ld BS
+    DBuf<float> Xa, Xb, Y;         // Nb x ncp FP32 workspaces (column-major)
+    DBuf<uint16_t> SX[3], SY[3];   // Nb x ncp: bf16 parts of the right-hand side / solution blocks
+    std::vector<cudaEvent_t> ev;   // per-block events of the three-stream schedule
+    PrecondBlk() = default;
+    PrecondBlk(const PrecondBlk &) = delete;
+    PrecondBlk &operator=(const PrecondBlk &) = delete;
+    ~PrecondBlk() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
 };
 struct Precond {
     int prec = 32;

@@ -100,13 +100,14 @@ __global__ void __launch_bounds__(256) k_blk_split_lower(int64_t Nb, const float
     }
 }
 
-// rows [r0, r0 + nr) x ncp columns of X (ld) -> the parts (same positions)
-__global__ void k_blk_split_rows(int64_t r0, int64_t nr, int64_t ncp, const float *__restrict__ X, int64_t ld,
-                                 bf16 *__restrict__ p1, bf16 *__restrict__ p2, bf16 *__restrict__ p3) {
+// rows [r0, r0 + nr) x ncp columns of X (+ X2 if given; ld) -> the parts (same positions)
+__global__ void k_blk_split_rows(int64_t r0, int64_t nr, int64_t ncp, const float *__restrict__ X,
+                                 const float *__restrict__ X2, int64_t ld, bf16 *__restrict__ p1,
+                                 bf16 *__restrict__ p2, bf16 *__restrict__ p3) {
     const int64_t total = nr * ncp;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = (r0 + e % nr) + (e / nr) * ld;
-        split3(X[q], p1[q], p2[q], p3[q]);
+        split3(X2 ? X[q] + X2[q] : X[q], p1[q], p2[q], p3[q]);
     }
 }
 
@@ -144,13 +145,25 @@ unsigned grid_for(hf_ctx *ctx, int64_t n) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
 }
 
-// C = alpha A B + beta C in FP32 precision: the six bf16 part products with i + j <= 4,
-// smallest first
-void gemm6(hf_ctx *ctx, bool tA, int64_t m, int64_t n, int64_t k, float alpha, bf16 *const A[3], int64_t lda,
-           bf16 *const B[3], int64_t ldb, float beta, float *C, int64_t ldc) {
+// C = alpha op(A) B + beta C in FP32 precision: the six bf16 part products with i + j <= 4,
+// smallest first, on stream st, `batch` problems at element strides sA / sB / sC
+void gemm6(hf_ctx *ctx, cudaStream_t st, bool tA, int64_t m, int64_t n, int64_t k, float alpha, bf16 *const A[3],
+           int64_t lda, bf16 *const B[3], int64_t ldb, float beta, float *C, int64_t ldc, int batch = 1,
+           int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
     static const int ord[6][2] = {{2, 0}, {0, 2}, {1, 1}, {1, 0}, {0, 1}, {0, 0}};
     for (int q = 0; q < 6; ++q)
-        lt_bgemm(ctx, tA, m, n, k, alpha, A[ord[q][0]], lda, B[ord[q][1]], ldb, q ? 1.f : beta, C, ldc);
+        lt_bgemm(ctx, tA, m, n, k, alpha, A[ord[q][0]], lda, B[ord[q][1]], ldb, q ? 1.f : beta, C, ldc, st, batch, sA,
+                 sB, sC);
+}
+
+bf16 *bp(DBuf<uint16_t> &b) { return reinterpret_cast<bf16 *>(b.p); }
+void parts(DBuf<uint16_t> (&b)[3], int64_t off, bf16 *out[3]) {
+    for (int q = 0; q < 3; ++q) out[q] = bp(b[q]) + off;
+}
+
+cudaStream_t aux_stream(hf_ctx *ctx, int i) {
+    if (!ctx->aux[i]) HF_CUDA(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking));
+    return ctx->aux[i];
 }
 
 }  // namespace
@@ -182,7 +195,7 @@ void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const f
     DBuf<float> Lp, Inv, T;   // FP32 working copies, released after the split
     Lp.alloc((size_t)Nb * Nb, st);
     Inv.alloc(ninv, st);
-    T.alloc((size_t)Nb * BS / 4 + 1, st);
+    T.alloc(std::max<size_t>((size_t)Nb * BS / 4, (size_t)std::max(p.nb - 1, 1) * BS * BS), st);
     HF_CUDA(cudaMemsetAsync(Inv.p, 0, ninv * sizeof(float), st));
     dim3 g((unsigned)(Nb / 32), (unsigned)(Nb / 32));
     k_blk_pad<<<g, 256, 0, st>>>(N, Nb, Lfac, Lp.p);
@@ -203,14 +216,48 @@ void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const f
         p.Lpart[q].alloc((size_t)Nb * Nb, st);
         p.Ipart[q].alloc(ninv, st);
     }
-    auto P = [](DBuf<uint16_t> &b) { return reinterpret_cast<bf16 *>(b.p); };
-    k_blk_split_all<<<grid_for(ctx, (int64_t)ninv), 256, 0, st>>>((int64_t)ninv, Inv.p, P(p.Ipart[0]), P(p.Ipart[1]),
-                                                                  P(p.Ipart[2]));
+    k_blk_split_all<<<grid_for(ctx, (int64_t)ninv), 256, 0, st>>>((int64_t)ninv, Inv.p, bp(p.Ipart[0]), bp(p.Ipart[1]),
+                                                                  bp(p.Ipart[2]));
     HF_CHECK_LAUNCH(ctx);
-    k_blk_split_lower<<<g, 256, 0, st>>>(Nb, Lp.p, P(p.Lpart[0]), P(p.Lpart[1]), P(p.Lpart[2]));
+    k_blk_split_lower<<<g, 256, 0, st>>>(Nb, Lp.p, bp(p.Lpart[0]), bp(p.Lpart[1]), bp(p.Lpart[2]));
     HF_CHECK_LAUNCH(ctx);
+    // the couplings of consecutive blocks, so that the next block's update needs the current
+    // block's right-hand side, not its solution:  G_j = L_{j+1,j} Linv_j (forward),
+    // H_j = Linv_{j+1} L_{j+1,j} (backward), in FP32 precision (six part products)
+    if (p.nb > 1) {
+        const int nc = p.nb - 1;
+        const size_t ng = (size_t)nc * BS * BS;
+        bf16 *A[3], *B[3];
+        for (int which = 0; which < 2; ++which) {
+            DBuf<uint16_t> (&out)[3] = which ? p.Hpart : p.Gpart;
+            if (which == 0) {   // G_j = L_{j+1,j} Inv_j
+                parts(p.Lpart, BS, A);
+                parts(p.Ipart, 0, B);
+                gemm6(ctx, st, false, BS, BS, BS, 1.f, A, Nb, B, BS, 0.f, T.p, BS, nc, BS * (Nb + 1), BS * (BS + 1),
+                      BS * BS);
+            } else {            // H_j = Inv_{j+1} L_{j+1,j}
+                parts(p.Ipart, BS * (BS + 1), A);
+                parts(p.Lpart, BS, B);
+                gemm6(ctx, st, false, BS, BS, BS, 1.f, A, BS, B, Nb, 0.f, T.p, BS, nc, BS * (BS + 1), BS * (Nb + 1),
+                      BS * BS);
+            }
+            for (int q = 0; q < 3; ++q) out[q].alloc(ng, st);
+            k_blk_split_all<<<grid_for(ctx, (int64_t)ng), 256, 0, st>>>((int64_t)ng, T.p, bp(out[0]), bp(out[1]),
+                                                                      bp(out[2]));
+            HF_CHECK_LAUNCH(ctx);
+        }
+    }
+    if (p.ev.empty()) {
+        p.ev.resize((size_t)4 * p.nb + 4);
+        for (auto &e : p.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
 }
 
+// Three streams per direction: A (the context stream) splits block j's right-hand side and
+// forms its solution; C applies the coupling to block j +- 1 from the right-hand side (the
+// sequential path: split -> coupling product -> split); B runs the bulk update of the
+// blocks beyond from the solution.  The coupling updates accumulate into Xa, the bulk ones
+// into Xb, so the two never write the same words; block j's right-hand side is Xa + Xb.
 void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R, int64_t ldr, double *W,
                        int64_t ldw) {
     cudaStream_t st = ctx->stream;
@@ -220,60 +267,103 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         return;
     }
     const int64_t Nb = p.Nb, BS = p.BS, ncp = (ncol + 7) / 8 * 8;
-    p.X.alloc((size_t)Nb * ncp, st);
+    const int nb = p.nb;
+    p.Xa.alloc((size_t)Nb * ncp, st);
+    p.Xb.alloc((size_t)Nb * ncp, st);
     p.Y.alloc((size_t)Nb * ncp, st);
-    for (int q = 0; q < 3; ++q) p.Spart[q].alloc((size_t)Nb * ncp, st);
+    for (int q = 0; q < 3; ++q) {
+        p.SX[q].alloc((size_t)Nb * ncp, st);
+        p.SY[q].alloc((size_t)Nb * ncp, st);
+    }
     const double nn = (double)p.N * (double)p.N;
     ClassTimer tm(ctx, "trsm", st, 2.0 * nn * (double)ncol, 6.0 * nn + 16.0 * (double)p.N * (double)ncol);
-    float *X = p.X.p, *Y = p.Y.p;
-    auto P = [](DBuf<uint16_t> &b) { return reinterpret_cast<bf16 *>(b.p); };
-    bf16 *S[3] = {P(p.Spart[0]), P(p.Spart[1]), P(p.Spart[2])};
-    auto Loff = [&](int64_t off, bf16 *out[3]) {
-        for (int q = 0; q < 3; ++q) out[q] = P(p.Lpart[q]) + off;
-    };
-    auto Ioff = [&](int j, bf16 *out[3]) {
-        for (int q = 0; q < 3; ++q) out[q] = P(p.Ipart[q]) + (size_t)j * BS * (BS + 1);
-    };
-    auto Soff = [&](int64_t r0, bf16 *out[3]) {
-        for (int q = 0; q < 3; ++q) out[q] = S[q] + r0;
-    };
-    auto split = [&](const float *src, int64_t r0, int64_t nr) {
-        k_blk_split_rows<<<grid_for(ctx, nr * ncp), 256, 0, st>>>(r0, nr, ncp, src, Nb, S[0], S[1], S[2]);
+    cudaStream_t sb = aux_stream(ctx, 0), sc = aux_stream(ctx, 1);
+    cudaEvent_t *evX = p.ev.data(), *evY = evX + nb, *evC = evY + nb, *evB = evC + nb, *evS = evB + nb;
+    float *Xa = p.Xa.p, *Xb = p.Xb.p, *Y = p.Y.p;
+    bf16 *A[3], *B[3];
+    auto split = [&](cudaStream_t s, const float *src, const float *src2, int64_t r0, DBuf<uint16_t> (&out)[3]) {
+        k_blk_split_rows<<<grid_for(ctx, BS * ncp), 256, 0, s>>>(r0, BS, ncp, src, src2, Nb, bp(out[0]), bp(out[1]),
+                                                                 bp(out[2]));
         HF_CHECK_LAUNCH(ctx);
     };
-    bf16 *A[3], *B[3];
-    k_blk_gather<<<grid_for(ctx, Nb * ncp), 256, 0, st>>>(p.N, Nb, ncol, ncp, p.perm, R, ldr, X);
+    auto fork = [&]() {   // B and C start after everything queued on A so far
+        HF_CUDA(cudaEventRecord(evS[0], st));
+        HF_CUDA(cudaStreamWaitEvent(sb, evS[0], 0));
+        HF_CUDA(cudaStreamWaitEvent(sc, evS[0], 0));
+    };
+    auto join = [&]() {   // A continues after everything queued on B and C
+        HF_CUDA(cudaEventRecord(evS[1], sb));
+        HF_CUDA(cudaEventRecord(evS[2], sc));
+        HF_CUDA(cudaStreamWaitEvent(st, evS[1], 0));
+        HF_CUDA(cudaStreamWaitEvent(st, evS[2], 0));
+    };
+    k_blk_gather<<<grid_for(ctx, Nb * ncp), 256, 0, st>>>(p.N, Nb, ncol, ncp, p.perm, R, ldr, Xa);
     HF_CHECK_LAUNCH(ctx);
-    // forward: L Y = X
-    for (int j = 0; j < p.nb; ++j) {
+    HF_CUDA(cudaMemsetAsync(Xb, 0, (size_t)Nb * ncp * sizeof(float), st));
+    fork();
+    // ---- forward: L Y = X
+    for (int j = 0; j < nb; ++j) {
         const int64_t j0 = (int64_t)j * BS;
-        split(X, j0, BS);
-        Ioff(j, A);
-        Soff(j0, B);
-        gemm6(ctx, false, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Y + j0, Nb);             // Y_j = Linv_j X_j
-        if (j + 1 < p.nb) {
-            split(Y, j0, BS);
-            const int64_t r1 = j0 + BS;
-            Loff(r1 + j0 * Nb, A);
-            gemm6(ctx, false, Nb - r1, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, X + r1, Nb);   // X_{>j} -= L_{>j,j} Y_j
+        if (j >= 1) HF_CUDA(cudaStreamWaitEvent(st, evC[j - 1], 0));   // coupling of j-1 wrote Xa_j
+        if (j >= 2) HF_CUDA(cudaStreamWaitEvent(st, evB[j - 2], 0));   // bulk of j-2 wrote Xb_j
+        split(st, Xa, Xb, j0, p.SX);
+        HF_CUDA(cudaEventRecord(evX[j], st));
+        if (j + 1 < nb) {   // C: Xa_{j+1} -= G_j X_j
+            HF_CUDA(cudaStreamWaitEvent(sc, evX[j], 0));
+            parts(p.Gpart, (size_t)j * BS * BS, A);
+            parts(p.SX, j0, B);
+            gemm6(ctx, sc, false, BS, ncp, BS, -1.f, A, BS, B, Nb, 1.f, Xa + j0 + BS, Nb);
+            HF_CUDA(cudaEventRecord(evC[j], sc));
+        }
+        parts(p.Ipart, (size_t)j * BS * (BS + 1), A);                    // A: Y_j = Linv_j X_j
+        parts(p.SX, j0, B);
+        gemm6(ctx, st, false, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Y + j0, Nb);
+        if (j + 2 < nb) {   // B: Xb_{>j+1} -= L_{>j+1,j} Y_j
+            split(st, Y, nullptr, j0, p.SY);
+            HF_CUDA(cudaEventRecord(evY[j], st));
+            HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
+            const int64_t r2 = j0 + 2 * BS;
+            parts(p.Lpart, r2 + j0 * Nb, A);
+            parts(p.SY, j0, B);
+            gemm6(ctx, sb, false, Nb - r2, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Xb + r2, Nb);
+            HF_CUDA(cudaEventRecord(evB[j], sb));
         }
     }
+    join();
     k_blk_dscale<<<grid_for(ctx, Nb * ncp), 256, 0, st>>>(p.N, Nb, ncp, p.D, Y);
     HF_CHECK_LAUNCH(ctx);
-    // backward: L^T X = Y
-    for (int j = p.nb - 1; j >= 0; --j) {
+    // ---- backward: L^T X = Z (Z = D^-1 Y: Za = Y, Zb = 0; the solution goes to Xa)
+    float *Za = Y, *Zb = Xb, *Xo = Xa;
+    HF_CUDA(cudaMemsetAsync(Zb, 0, (size_t)Nb * ncp * sizeof(float), st));
+    fork();
+    for (int j = nb - 1; j >= 0; --j) {
         const int64_t j0 = (int64_t)j * BS;
-        split(Y, j0, BS);
-        Ioff(j, A);
-        Soff(j0, B);
-        gemm6(ctx, true, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, X + j0, Nb);              // X_j = Linv_j^T Y_j
-        if (j > 0) {
-            split(X, j0, BS);
-            Loff(j0, A);
-            gemm6(ctx, true, j0, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Y, Nb);              // Y_{<j} -= L_{j,<j}^T X_j
+        if (j + 1 < nb) HF_CUDA(cudaStreamWaitEvent(st, evC[j + 1], 0));   // coupling of j+1 wrote Za_j
+        if (j + 2 < nb) HF_CUDA(cudaStreamWaitEvent(st, evB[j + 2], 0));   // bulk of j+2 wrote Zb_j
+        split(st, Za, Zb, j0, p.SX);
+        HF_CUDA(cudaEventRecord(evX[j], st));
+        if (j >= 1) {   // C: Za_{j-1} -= H_{j-1}^T Z_j
+            HF_CUDA(cudaStreamWaitEvent(sc, evX[j], 0));
+            parts(p.Hpart, (size_t)(j - 1) * BS * BS, A);
+            parts(p.SX, j0, B);
+            gemm6(ctx, sc, true, BS, ncp, BS, -1.f, A, BS, B, Nb, 1.f, Za + j0 - BS, Nb);
+            HF_CUDA(cudaEventRecord(evC[j], sc));
+        }
+        parts(p.Ipart, (size_t)j * BS * (BS + 1), A);                      // A: X_j = Linv_j^T Z_j
+        parts(p.SX, j0, B);
+        gemm6(ctx, st, true, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Xo + j0, Nb);
+        if (j >= 2) {   // B: Zb_{<j-1} -= (L_{j,<j-1})^T X_j
+            split(st, Xo, nullptr, j0, p.SY);
+            HF_CUDA(cudaEventRecord(evY[j], st));
+            HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
+            parts(p.Lpart, j0, A);
+            parts(p.SY, j0, B);
+            gemm6(ctx, sb, true, j0 - BS, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Zb, Nb);
+            HF_CUDA(cudaEventRecord(evB[j], sb));
         }
     }
-    k_blk_scatter<<<grid_for(ctx, p.L * ncol), 256, 0, st>>>(p.L, Nb, ncol, p.pos1, X, W, ldw);
+    join();
+    k_blk_scatter<<<grid_for(ctx, p.L * ncol), 256, 0, st>>>(p.L, Nb, ncol, p.pos1, Xo, W, ldw);
     HF_CHECK_LAUNCH(ctx);
 }
 

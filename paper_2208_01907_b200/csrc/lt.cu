@@ -29,9 +29,10 @@ struct LtPlan {
 // kept for the process (never destroyed: no teardown ordering against the CUDA context)
 struct LtState {
     cublasLtHandle_t h = nullptr;
-    void *ws = nullptr;
+    std::map<cudaStream_t, void *> ws;   // one workspace per stream: concurrent GEMMs never share one
     std::map<std::array<int64_t, 14>, LtPlan> plans;
-    std::mutex mu;   // guards plans
+    std::mutex mu;   // guards plans and ws
+    void *workspace(cudaStream_t s);
 };
 constexpr size_t LT_WS = (size_t)32 << 20;
 
@@ -43,10 +44,18 @@ LtState &lt_state(hf_ctx *ctx) {
     if (!s) {
         std::unique_ptr<LtState> n(new LtState());
         HF_CUBLAS(cublasLtCreate(&n->h));
-        HF_CUDA(cudaMalloc(&n->ws, LT_WS));
         s = n.release();
     }
     return *s;
+}
+
+void *LtState::workspace(cudaStream_t s) {
+    auto it = ws.find(s);
+    if (it != ws.end()) return it->second;
+    void *p = nullptr;
+    HF_CUDA(cudaMalloc(&p, LT_WS));
+    ws.emplace(s, p);
+    return p;
 }
 
 cublasLtMatrixLayout_t layout(cudaDataType_t t, int64_t rows, int64_t cols, int64_t ld, int batch, int64_t stride) {
@@ -107,8 +116,8 @@ void lt_imma(hf_ctx *ctx, int64_t rows, int64_t cols, int64_t k, const int8_t *A
     std::lock_guard<std::mutex> g(lt.mu);
     const LtPlan &pl = plan(lt, {1, 1, 0, rows, cols, k, lda, ldb, ldd, 1, 0, 0, 0, 0});
     const int32_t one = 1, zero = 0;
-    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &one, A, pl.la, B, pl.lb, &zero, D, pl.lc, D, pl.lc, &pl.algo, lt.ws, LT_WS,
-                             ctx->stream));
+    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &one, A, pl.la, B, pl.lb, &zero, D, pl.lc, D, pl.lc, &pl.algo,
+                             lt.workspace(ctx->stream), LT_WS, ctx->stream));
 }
 
 void lt_sgemm(hf_ctx *ctx, bool tA, bool tB, int64_t m, int64_t n, int64_t k, float alpha, const float *A,
@@ -119,18 +128,21 @@ void lt_sgemm(hf_ctx *ctx, bool tA, bool tB, int64_t m, int64_t n, int64_t k, fl
     std::lock_guard<std::mutex> g(lt.mu);
     const LtPlan &pl = plan(lt, {2, tA, tB, m, n, k, lda, ldb, ldc, batch, batch > 1 ? sA : 0,
                                  batch > 1 ? sB : 0, batch > 1 ? sC : 0, tf32 ? 1 : 0});
-    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &alpha, A, pl.la, B, pl.lb, &beta, C, pl.lc, C, pl.lc, &pl.algo, lt.ws,
-                             LT_WS, ctx->stream));
+    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &alpha, A, pl.la, B, pl.lb, &beta, C, pl.lc, C, pl.lc, &pl.algo,
+                             lt.workspace(ctx->stream), LT_WS, ctx->stream));
 }
 
 void lt_bgemm(hf_ctx *ctx, bool tA, int64_t m, int64_t n, int64_t k, float alpha, const __nv_bfloat16 *A,
-              int64_t lda, const __nv_bfloat16 *B, int64_t ldb, float beta, float *C, int64_t ldc) {
-    if (m == 0 || n == 0) return;
+              int64_t lda, const __nv_bfloat16 *B, int64_t ldb, float beta, float *C, int64_t ldc,
+              cudaStream_t st, int batch, int64_t sA, int64_t sB, int64_t sC) {
+    if (m == 0 || n == 0 || batch == 0) return;
+    if (!st) st = ctx->stream;
     LtState &lt = lt_state(ctx);
     std::lock_guard<std::mutex> g(lt.mu);
-    const LtPlan &pl = plan(lt, {3, tA, 0, m, n, k, lda, ldb, ldc, 1, 0, 0, 0, 0});
-    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &alpha, A, pl.la, B, pl.lb, &beta, C, pl.lc, C, pl.lc, &pl.algo, lt.ws,
-                             LT_WS, ctx->stream));
+    const LtPlan &pl = plan(lt, {3, tA, 0, m, n, k, lda, ldb, ldc, batch, batch > 1 ? sA : 0, batch > 1 ? sB : 0,
+                                 batch > 1 ? sC : 0, 0});
+    HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &alpha, A, pl.la, B, pl.lb, &beta, C, pl.lc, C, pl.lc, &pl.algo,
+                             lt.workspace(st), LT_WS, st));
 }
 
 }  // namespace hf

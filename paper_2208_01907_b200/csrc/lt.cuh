@@ -1,7 +1,7 @@
 // lt.cuh -- the plain library GEMMs libhf issues through cuBLASLt (lt.cu): the exact
 // int8 slice products of the emulated FP64 mat-vec (ozaki.cu) and the FP32 / 3xTF32
 // block products of the blocked preconditioner (k_trsm_blk.cu).  Descriptors and the
-// heuristic's algorithm are cached per shape; one handle and workspace per device.
+// heuristic's algorithm are cached per shape; one handle per device, one workspace per stream.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -20,8 +20,10 @@ void lt_sgemm(hf_ctx *ctx, bool tA, bool tB, int64_t m, int64_t n, int64_t k, fl
               int64_t lda, int64_t sA, const float *B, int64_t ldb, int64_t sB, float beta, float *C, int64_t ldc,
               int64_t sC, int batch, bool tf32);
 
-// C = alpha op(A) B + beta C with bfloat16 operands, FP32 output and accumulation
+// C = alpha op(A) B + beta C with bfloat16 operands, FP32 output and accumulation, on stream st
+// (0: the context stream), `batch` problems at the given element strides
 void lt_bgemm(hf_ctx *ctx, bool tA, int64_t m, int64_t n, int64_t k, float alpha, const __nv_bfloat16 *A,
-              int64_t lda, const __nv_bfloat16 *B, int64_t ldb, float beta, float *C, int64_t ldc);
+              int64_t lda, const __nv_bfloat16 *B, int64_t ldb, float beta, float *C, int64_t ldc,
+              cudaStream_t st = nullptr, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0);
 
 }  // namespace hf
