@@ -112,3 +112,31 @@ def test_schur_gcr_ozaki_matches_dmma(ctx, name, seed):
     hy1.close()
     hy2.close()
     lf.close()
+
+
+def test_edge_cases_extreme_scales_and_zeros(ctx):
+    """Rows of K spread over 2^-600..2^600 (the row exponents must not overflow or lose the
+    scale), an all-zero row / column of K, an all-zero column of W, a W column of subnormal
+    magnitude, L not a multiple of 16 (the zero-padded slices): entrywise within the bound of
+    test_error_bound_vs_extended_precision, zeros exactly zero."""
+    from paper_2208_01907_b200 import hf
+    rng = np.random.default_rng(11)
+    L, n, s = 333, 36, 8
+    d = 2.0 ** rng.integers(-300, 300, size=L).astype(np.float64)
+    K = _sym(rng.standard_normal((L, L))) * d[:, None] * d[None, :]
+    K[17, :] = 0.0
+    K[:, 17] = 0.0
+    W = rng.standard_normal((n, L))
+    W[3] = 0.0
+    W[5] *= 2.0 ** -1060                      # subnormal column
+    W[:, 17] = 1.0
+    ref = W.astype(np.longdouble) @ K.astype(np.longdouble)
+    Z = hf.hf_matvec(ctx, torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda(), "ozaki").cpu().numpy()
+    assert np.all(Z[3] == 0.0) and np.all(Z[:, 17] == 0.0)
+    em = np.array([_exp_bound(K[:, m]) for m in range(L)])
+    fc = np.array([_exp_bound(W[c]) for c in range(n)])
+    bound = (s + 2) * np.ldexp(np.ldexp(1.0, -7 * s) * L, em[None, :] + fc[:, None])
+    bound = bound + 8 * 2.0 ** -53 * np.abs(ref).astype(np.float64) + 1e-320
+    err = np.abs((Z.astype(np.longdouble) - ref).astype(np.float64))
+    assert np.all(np.isfinite(Z))
+    assert (err <= bound).all(), float((err / bound).max())
