@@ -10,6 +10,7 @@
 #include "hf_internal.cuh"
 #include "k_dgemm.cuh"
 #include "k_small.cuh"
+#include "lt.cuh"
 #include "ozaki.cuh"
 
 namespace {
@@ -105,6 +106,10 @@ hf_status hf_destroy(hf_ctx *ctx) {
     for (auto a : ctx->aux)
         if (a) {
             cudaStreamSynchronize(a);
+            try {
+                hf::lt_release_stream(ctx, a);
+            } catch (...) {
+            }
             cudaStreamDestroy(a);
         }
     if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);

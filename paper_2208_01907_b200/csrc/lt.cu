@@ -109,6 +109,17 @@ const LtPlan &plan(LtState &lt, const std::array<int64_t, 14> &key) {
 
 }  // namespace
 
+// the workspace of a stream that is about to be destroyed (hf_destroy: the context's helper
+// streams, after they are synchronised); a later stream with the same handle gets a new one
+void lt_release_stream(hf_ctx *ctx, cudaStream_t s) {
+    LtState &lt = lt_state(ctx);
+    std::lock_guard<std::mutex> g(lt.mu);
+    auto it = lt.ws.find(s);
+    if (it == lt.ws.end()) return;
+    cudaFree(it->second);
+    lt.ws.erase(it);
+}
+
 // library kernels: not counted in ctx->launches (libhf's own launches)
 void lt_imma(hf_ctx *ctx, int64_t rows, int64_t cols, int64_t k, const int8_t *A, int64_t lda, const int8_t *B,
              int64_t ldb, int32_t *D, int64_t ldd) {

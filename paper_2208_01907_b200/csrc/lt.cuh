@@ -26,4 +26,7 @@ void lt_bgemm(hf_ctx *ctx, bool tA, int64_t m, int64_t n, int64_t k, float alpha
               int64_t lda, const __nv_bfloat16 *B, int64_t ldb, float beta, float *C, int64_t ldc,
               cudaStream_t st = nullptr, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0);
 
+// frees the workspace kept for stream s (call before destroying s, after synchronising it)
+void lt_release_stream(hf_ctx *ctx, cudaStream_t s);
+
 }  // namespace hf
