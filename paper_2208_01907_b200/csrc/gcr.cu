@@ -64,10 +64,12 @@ void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uin
         // the slices take as much memory as K itself; the automatic choice falls back to
         // the DMMA product when they do not fit (e.g. C4 beside the FP32 preconditioner)
         if (e.st != HF_ERR_OOM || o.matvec == 2) throw;
+        if (getenv("HF_MATVEC_DEBUG")) fprintf(stderr, "[hf matvec] int8 slices do not fit (%s): DMMA\n", e.msg.c_str());
         w.ozown.reset();
         return;
     }
     w.oz = w.ozown.get();
+    if (getenv("HF_MATVEC_DEBUG")) fprintf(stderr, "[hf matvec] int8 slices, n = %lld\n", (long long)n);
 }
 
 void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {

@@ -109,6 +109,10 @@ def worker_stage2(name, Gs):
         per = []
         for r in ([0, G - 1] if G > 1 else [0]):
             hf.hf_set_virtual_rank(ctx, r, G) if G > 1 else hf.hf_set_virtual_rank(ctx, 0, 0)
+            # warm-up run first: the library GEMMs' plans (cuBLASLt heuristics, once per shape
+            # and process) and the device cache's first mappings are not per-factorization costs
+            hy, info, _ = hf.hf_schur_gcr(ctx, K, lf, accept_failure=True)
+            hy.close()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             hy, info, _ = hf.hf_schur_gcr(ctx, K, lf, accept_failure=True)
