@@ -249,12 +249,13 @@ struct PrecondBlk {
     const float *D = nullptr;
     const int64_t *perm = nullptr;
     const int32_t *pos1 = nullptr;
-    DBuf<uint16_t> Lpart[3];       // Nb x Nb: padded L as three exact bfloat16 parts (lower tiles)
-    DBuf<uint16_t> Ipart[3];       // diagonal-block inverses (parts), block j at j BS (BS + 1), ld BS
-    DBuf<uint16_t> Gpart[3];       // G_j = L_{j+1,j} Linv_j (parts), block j at j BS^2, ld BS
-    DBuf<uint16_t> Hpart[3];       // H_j = Linv_{j+1} L_{j+1,j} (parts), block j at j BS^2, ld BS
+    DBuf<uint16_t> Lc, Lr;         // the strictly lower blocks of L as three exact bfloat16 parts,
+                                   // packed by block column (parts side by side) / block row
+                                   // (parts stacked): k_trsm_blk.cu lc_off / lr_off
+    DBuf<uint16_t> Ic, It;         // Linv_j, six-part concatenations (BS x 6BS / 6BS x BS) per block
+    DBuf<uint16_t> Gc, Ht;         // G_j = L_{j+1,j} Linv_j (BS x 6BS), H_j = Linv_{j+1} L_{j+1,j} (6BS x BS)
     DBuf<float> Xa, Xb, Y;         // Nb x ncp FP32 workspaces (column-major)
-    DBuf<uint16_t> SX[3], SY[3];   // Nb x ncp: bf16 parts of the right-hand side / solution blocks
+    DBuf<uint16_t> S6, SB;         // per block: 6BS x ncp part stacks of its right-hand side / solution
     std::vector<cudaEvent_t> ev;   // per-block events of the three-stream schedule
     PrecondBlk() = default;
     PrecondBlk(const PrecondBlk &) = delete;

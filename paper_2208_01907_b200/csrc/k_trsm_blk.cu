@@ -111,6 +111,103 @@ __global__ void k_blk_split_rows(int64_t r0, int64_t nr, int64_t ncp, const floa
     }
 }
 
+// Part orders of the K-concatenated products.  The six part products with i + j <= 4 as ONE
+// GEMM over K' = 6 BS:  [A3 A1 A2 A2 A1 A1] . [B1; B3; B2; B1; B2; B1]  (SMALL order, for the
+// latency-critical diagonal-inverse and coupling products, whose A operands are stored with
+// their parts duplicated), or as three GEMMs over the three-part L layout:
+// [L1 L2 L3] . [B1; B1; B1],  [L1 L2] . [B2; B2],  L1 . B3  (BULK order of the B stack).
+__constant__ int kOrdSmall[6] = {2, 0, 1, 1, 0, 0};   // A part per K block (B: kOrdSmallB)
+__constant__ int kOrdSmallB[6] = {0, 2, 1, 0, 1, 0};
+__constant__ int kOrdBulkB[6] = {0, 0, 0, 1, 1, 2};
+
+__device__ __forceinline__ bf16 part_of(const bf16 (&pp)[3], int q) { return q == 0 ? pp[0] : (q == 1 ? pp[1] : pp[2]); }
+
+// BS x BS FP32 blocks (ld lds, block stride sstride) -> the six-part concatenation with
+// duplicated A parts: cols != 0: BS x 6BS, part kOrdSmall[q] in columns [q BS, (q+1) BS)
+// (A operand, op N); cols == 0: 6BS x BS, part kOrdSmall[q] in rows [q BS, (q+1) BS) (op T).
+// Two consecutive rows per thread: 4-byte stores of bf16 pairs.
+__global__ void k_blk_cat6(int nblk, int64_t BS, const float *__restrict__ src, int64_t lds, int64_t sstride,
+                           bf16 *__restrict__ dst, int cols) {
+    const int64_t per = BS * BS, hper = per / 2, total = (int64_t)nblk * hper;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / hper, w = e % hper, r = 2 * (w % (BS / 2)), c = w / (BS / 2);
+        const float *sp = src + b * sstride + r + c * lds;
+        bf16 pa[3], pb[3];
+        split3(sp[0], pa[0], pa[1], pa[2]);
+        split3(sp[1], pb[0], pb[1], pb[2]);
+        bf16 *d = dst + b * 6 * per;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const int pq = kOrdSmall[q];
+            const __nv_bfloat162 v = __halves2bfloat162(part_of(pa, pq), part_of(pb, pq));
+            bf16 *t = cols ? d + r + (q * BS + c) * BS : d + (q * BS + r) + c * 6 * BS;
+            *reinterpret_cast<__nv_bfloat162 *>(t) = v;
+        }
+    }
+}
+
+// rows [r0, r0 + BS) x ncp columns of X (+ X2; ld) -> a 6BS x ncp stack (ld 6BS) of their
+// parts in the SMALL (bulk == 0) or BULK B order; two consecutive rows per thread
+__global__ void k_blk_split6(int64_t r0, int64_t BS, int64_t ncp, const float *__restrict__ X,
+                             const float *__restrict__ X2, int64_t ld, bf16 *__restrict__ dst, int bulk) {
+    const int64_t hb = BS / 2, total = hb * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = 2 * (e % hb), c = e / hb, q0 = (r0 + r) + c * ld;
+        float2 v = *reinterpret_cast<const float2 *>(X + q0);
+        if (X2) {
+            const float2 v2 = *reinterpret_cast<const float2 *>(X2 + q0);
+            v.x += v2.x;
+            v.y += v2.y;
+        }
+        bf16 pa[3], pb[3];
+        split3(v.x, pa[0], pa[1], pa[2]);
+        split3(v.y, pb[0], pb[1], pb[2]);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const int pq = bulk ? kOrdBulkB[q] : kOrdSmallB[q];
+            *reinterpret_cast<__nv_bfloat162 *>(dst + (q * BS + r) + c * 6 * BS) =
+                __halves2bfloat162(part_of(pa, pq), part_of(pb, pq));
+        }
+    }
+}
+
+// offsets of the packed L layouts (nb blocks of BS):
+//   Lc: block column j (j < nb - 1) = rows (j+1)BS .. Nb-1 (height h_j = (nb-1-j) BS) x the
+//       three parts side by side (3BS columns), ld h_j, at 3 BS^2 (j (nb-1) - j (j-1) / 2)
+//   Lr: block row i (i >= 1) = the three parts stacked (3BS rows) x columns 0 .. iBS-1,
+//       ld 3BS, at 3 BS^2 (i-1) i / 2
+__host__ __device__ __forceinline__ int64_t lc_off(int64_t j, int64_t nb, int64_t BS) {
+    return 3 * BS * BS * (j * (nb - 1) - j * (j - 1) / 2);
+}
+__host__ __device__ __forceinline__ int64_t lr_off(int64_t i, int64_t BS) { return 3 * BS * BS * ((i - 1) * i / 2); }
+
+// the strictly-below-block-diagonal entries of Lp (Nb x Nb FP32) -> their parts in Lc and Lr;
+// 64 x 32 tiles, two consecutive rows per thread (4-byte stores of bf16 pairs)
+__global__ void __launch_bounds__(256) k_blk_pack_L(int64_t Nb, int64_t BS, const float *__restrict__ Lp,
+                                                    bf16 *__restrict__ Lc, bf16 *__restrict__ Lr) {
+    const int64_t i0 = (int64_t)blockIdx.x * 64, j0 = (int64_t)blockIdx.y * 32;
+    if (i0 / BS <= j0 / BS) return;   // tiles never straddle a BS block (BS >= 64)
+    const int64_t nb = Nb / BS;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t r = i0 + 2 * tx, bi = r / BS;
+    for (int q = ty; q < 32; q += 8) {
+        const int64_t c = j0 + q, bj = c / BS;
+        const float2 v = *reinterpret_cast<const float2 *>(Lp + r + c * Nb);
+        bf16 pa[3], pb[3];
+        split3(v.x, pa[0], pa[1], pa[2]);
+        split3(v.y, pb[0], pb[1], pb[2]);
+        const int64_t h = (nb - 1 - bj) * BS;
+        bf16 *dc = Lc + lc_off(bj, nb, BS) + (r - (bj + 1) * BS);
+        bf16 *dr = Lr + lr_off(bi, BS) + (r - bi * BS) + c * 3 * BS;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const __nv_bfloat162 w = __halves2bfloat162(pa[p], pb[p]);
+            *reinterpret_cast<__nv_bfloat162 *>(dc + (p * BS + (c - bj * BS)) * h) = w;
+            *reinterpret_cast<__nv_bfloat162 *>(dr + p * BS) = w;
+        }
+    }
+}
+
 // X (Nb x ncp, pivot order) = RN32(R[perm]) (FP64 -> FP32 truncation), zero padding
 __global__ void k_blk_gather(int64_t N, int64_t Nb, int64_t ncol, int64_t ncp, const int64_t *__restrict__ perm,
                              const double *__restrict__ R, int64_t ldr, float *__restrict__ X) {
@@ -189,13 +286,13 @@ void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const f
     p.BS = BS;
     p.nb = (int)cdiv(N, BS);
     p.Nb = p.nb * BS;
-    const int64_t Nb = p.Nb;
+    const int64_t Nb = p.Nb, nb = p.nb;
     ClassTimer tm(ctx, "trsm_setup");
-    const size_t ninv = (size_t)p.nb * BS * (BS + 1);
-    DBuf<float> Lp, Inv, T;   // FP32 working copies, released after the split
+    const size_t ninv = (size_t)nb * BS * (BS + 1), per6 = (size_t)6 * BS * BS;
+    DBuf<float> Lp, Inv, T;   // FP32 working copies, released at the end
     Lp.alloc((size_t)Nb * Nb, st);
     Inv.alloc(ninv, st);
-    T.alloc(std::max<size_t>((size_t)Nb * BS / 4, (size_t)std::max(p.nb - 1, 1) * BS * BS), st);
+    T.alloc(std::max<size_t>((size_t)Nb * BS / 4, (size_t)std::max<int64_t>(nb - 1, 1) * BS * BS), st);
     HF_CUDA(cudaMemsetAsync(Inv.p, 0, ninv * sizeof(float), st));
     dim3 g((unsigned)(Nb / 32), (unsigned)(Nb / 32));
     k_blk_pad<<<g, 256, 0, st>>>(N, Nb, Lfac, Lp.p);
@@ -212,52 +309,70 @@ void precond_blk_setup(hf_ctx *ctx, PrecondBlk &p, int64_t N, int64_t L, const f
         lt_sgemm(ctx, false, false, h, h, h, -1.f, Inv.p + h * (BS + 1), BS, sd, T.p, h, h * h, 0.f, Inv.p + h, BS, sd,
                  batch, false);
     }
-    for (int q = 0; q < 3; ++q) {
-        p.Lpart[q].alloc((size_t)Nb * Nb, st);
-        p.Ipart[q].alloc(ninv, st);
+    // the operands of the solves
+    const size_t nlc = (size_t)lc_off(nb - 1, nb, BS), nlr = (size_t)lr_off(nb, BS);
+    p.Lc.alloc(std::max<size_t>(nlc, 1), st);
+    p.Lr.alloc(std::max<size_t>(nlr, 1), st);
+    if (nb > 1) {
+        k_blk_pack_L<<<dim3((unsigned)(Nb / 64), (unsigned)(Nb / 32)), 256, 0, st>>>(Nb, BS, Lp.p, bp(p.Lc), bp(p.Lr));
+        HF_CHECK_LAUNCH(ctx);
     }
-    k_blk_split_all<<<grid_for(ctx, (int64_t)ninv), 256, 0, st>>>((int64_t)ninv, Inv.p, bp(p.Ipart[0]), bp(p.Ipart[1]),
-                                                                  bp(p.Ipart[2]));
+    p.Ic.alloc(nb * per6, st);
+    p.It.alloc(nb * per6, st);
+    k_blk_cat6<<<grid_for(ctx, nb * BS * BS / 2), 256, 0, st>>>(nb, BS, Inv.p, BS, BS * (BS + 1), bp(p.Ic), 1);
     HF_CHECK_LAUNCH(ctx);
-    k_blk_split_lower<<<g, 256, 0, st>>>(Nb, Lp.p, bp(p.Lpart[0]), bp(p.Lpart[1]), bp(p.Lpart[2]));
+    k_blk_cat6<<<grid_for(ctx, nb * BS * BS / 2), 256, 0, st>>>(nb, BS, Inv.p, BS, BS * (BS + 1), bp(p.It), 0);
     HF_CHECK_LAUNCH(ctx);
     // the couplings of consecutive blocks, so that the next block's update needs the current
     // block's right-hand side, not its solution:  G_j = L_{j+1,j} Linv_j (forward),
-    // H_j = Linv_{j+1} L_{j+1,j} (backward), in FP32 precision (six part products)
-    if (p.nb > 1) {
-        const int nc = p.nb - 1;
-        const size_t ng = (size_t)nc * BS * BS;
-        bf16 *A[3], *B[3];
-        for (int which = 0; which < 2; ++which) {
-            DBuf<uint16_t> (&out)[3] = which ? p.Hpart : p.Gpart;
-            if (which == 0) {   // G_j = L_{j+1,j} Inv_j
-                parts(p.Lpart, BS, A);
-                parts(p.Ipart, 0, B);
-                gemm6(ctx, st, false, BS, BS, BS, 1.f, A, Nb, B, BS, 0.f, T.p, BS, nc, BS * (Nb + 1), BS * (BS + 1),
-                      BS * BS);
-            } else {            // H_j = Inv_{j+1} L_{j+1,j}
-                parts(p.Ipart, BS * (BS + 1), A);
-                parts(p.Lpart, BS, B);
-                gemm6(ctx, st, false, BS, BS, BS, 1.f, A, BS, B, Nb, 0.f, T.p, BS, nc, BS * (BS + 1), BS * (Nb + 1),
-                      BS * BS);
-            }
-            for (int q = 0; q < 3; ++q) out[q].alloc(ng, st);
-            k_blk_split_all<<<grid_for(ctx, (int64_t)ng), 256, 0, st>>>((int64_t)ng, T.p, bp(out[0]), bp(out[1]),
-                                                                      bp(out[2]));
-            HF_CHECK_LAUNCH(ctx);
+    // H_j = Linv_{j+1} L_{j+1,j} (backward), FP32 precision (the six part products, batched)
+    if (nb > 1) {
+        const int nc = (int)nb - 1;
+        DBuf<uint16_t> Ls[3], Is[3];   // parts of the sub-diagonal blocks and of the inverses
+        for (int q = 0; q < 3; ++q) {
+            Ls[q].alloc((size_t)nc * BS * BS, st);
+            Is[q].alloc(ninv, st);
         }
+        k_blk_split_all<<<grid_for(ctx, (int64_t)ninv), 256, 0, st>>>((int64_t)ninv, Inv.p, bp(Is[0]), bp(Is[1]),
+                                                                      bp(Is[2]));
+        HF_CHECK_LAUNCH(ctx);
+        // the sub-diagonal blocks L_{j+1,j} into a packed FP32 copy (T), then parts
+        HF_CUDA(cudaMemcpy2DAsync(T.p, BS * sizeof(float), Lp.p + BS, Nb * sizeof(float), BS * sizeof(float), BS, 
+                                  cudaMemcpyDeviceToDevice, st));   // block 0 (the batched form follows)
+        for (int j = 1; j < nc; ++j)
+            HF_CUDA(cudaMemcpy2DAsync(T.p + (size_t)j * BS * BS, BS * sizeof(float), Lp.p + (j + 1) * BS + j * BS * Nb,
+                                      Nb * sizeof(float), BS * sizeof(float), BS, cudaMemcpyDeviceToDevice, st));
+        k_blk_split_all<<<grid_for(ctx, (int64_t)nc * BS * BS), 256, 0, st>>>((int64_t)nc * BS * BS, T.p, bp(Ls[0]),
+                                                                              bp(Ls[1]), bp(Ls[2]));
+        HF_CHECK_LAUNCH(ctx);
+        bf16 *A[3], *B[3];
+        p.Gc.alloc((size_t)nc * per6, st);
+        p.Ht.alloc((size_t)nc * per6, st);
+        // G_j = L_{j+1,j} Inv_j -> T -> Gc
+        parts(Ls, 0, A);
+        parts(Is, 0, B);
+        gemm6(ctx, st, false, BS, BS, BS, 1.f, A, BS, B, BS, 0.f, T.p, BS, nc, BS * BS, BS * (BS + 1), BS * BS);
+        k_blk_cat6<<<grid_for(ctx, nc * BS * BS / 2), 256, 0, st>>>(nc, BS, T.p, BS, BS * BS, bp(p.Gc), 1);
+        HF_CHECK_LAUNCH(ctx);
+        // H_j = Inv_{j+1} L_{j+1,j} -> T -> Ht
+        parts(Is, BS * (BS + 1), A);
+        parts(Ls, 0, B);
+        gemm6(ctx, st, false, BS, BS, BS, 1.f, A, BS, B, BS, 0.f, T.p, BS, nc, BS * (BS + 1), BS * BS, BS * BS);
+        k_blk_cat6<<<grid_for(ctx, nc * BS * BS / 2), 256, 0, st>>>(nc, BS, T.p, BS, BS * BS, bp(p.Ht), 0);
+        HF_CHECK_LAUNCH(ctx);
     }
     if (p.ev.empty()) {
-        p.ev.resize((size_t)4 * p.nb + 4);
+        p.ev.resize((size_t)4 * nb + 4);
         for (auto &e : p.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
 
-// Three streams per direction: A (the context stream) splits block j's right-hand side and
+// Three streams per direction: A (the context stream) stacks block j's right-hand side and
 // forms its solution; C applies the coupling to block j +- 1 from the right-hand side (the
-// sequential path: split -> coupling product -> split); B runs the bulk update of the
-// blocks beyond from the solution.  The coupling updates accumulate into Xa, the bulk ones
-// into Xb, so the two never write the same words; block j's right-hand side is Xa + Xb.
+// sequential path: stack -> one coupling GEMM -> stack); B runs the bulk update of the
+// blocks beyond from the solution (three GEMMs over the packed three-part L).  The coupling
+// updates accumulate into Xa, the bulk ones into Xb, so the two never write the same words;
+// block j's right-hand side is Xa + Xb.
 void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R, int64_t ldr, double *W,
                        int64_t ldw) {
     cudaStream_t st = ctx->stream;
@@ -266,25 +381,33 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         HF_CUDA(cudaMemset2DAsync(W, ldw * sizeof(double), 0, p.L * sizeof(double), ncol, st));
         return;
     }
-    const int64_t Nb = p.Nb, BS = p.BS, ncp = (ncol + 7) / 8 * 8;
-    const int nb = p.nb;
+    const int64_t Nb = p.Nb, BS = p.BS, ncp = (ncol + 7) / 8 * 8, nb = p.nb;
+    const size_t per6 = (size_t)6 * BS * BS, stk = (size_t)6 * BS * ncp;
     p.Xa.alloc((size_t)Nb * ncp, st);
     p.Xb.alloc((size_t)Nb * ncp, st);
     p.Y.alloc((size_t)Nb * ncp, st);
-    for (int q = 0; q < 3; ++q) {
-        p.SX[q].alloc((size_t)Nb * ncp, st);
-        p.SY[q].alloc((size_t)Nb * ncp, st);
-    }
+    p.S6.alloc(nb * stk, st);
+    p.SB.alloc(nb * stk, st);
     const double nn = (double)p.N * (double)p.N;
-    ClassTimer tm(ctx, "trsm", st, 2.0 * nn * (double)ncol, 6.0 * nn + 16.0 * (double)p.N * (double)ncol);
+    ClassTimer tm(ctx, "trsm", st, 2.0 * nn * (double)ncol, 3.0 * nn + 16.0 * (double)p.N * (double)ncol);
     cudaStream_t sb = aux_stream(ctx, 0), sc = aux_stream(ctx, 1);
     cudaEvent_t *evX = p.ev.data(), *evY = evX + nb, *evC = evY + nb, *evB = evC + nb, *evS = evB + nb;
     float *Xa = p.Xa.p, *Xb = p.Xb.p, *Y = p.Y.p;
-    bf16 *A[3], *B[3];
-    auto split = [&](cudaStream_t s, const float *src, const float *src2, int64_t r0, DBuf<uint16_t> (&out)[3]) {
-        k_blk_split_rows<<<grid_for(ctx, BS * ncp), 256, 0, s>>>(r0, BS, ncp, src, src2, Nb, bp(out[0]), bp(out[1]),
-                                                                 bp(out[2]));
+    bf16 *S6 = bp(p.S6), *SB = bp(p.SB), *Lc = bp(p.Lc), *Lr = bp(p.Lr);
+    auto stack = [&](cudaStream_t s, const float *src, const float *src2, int64_t j, bf16 *dst, int bulk) {
+        k_blk_split6<<<grid_for(ctx, BS * ncp / 2), 256, 0, s>>>(j * BS, BS, ncp, src, src2, Nb, dst + j * stk, bulk);
         HF_CHECK_LAUNCH(ctx);
+    };
+    // one GEMM over K' = 6BS (the duplicated-part A operands)
+    auto gemm_small = [&](cudaStream_t s, bool tA, const bf16 *A, int64_t j, float alpha, float beta, float *C) {
+        lt_bgemm(ctx, tA, BS, ncp, 6 * BS, alpha, A, tA ? 6 * BS : BS, S6 + j * stk, 6 * BS, beta, C, Nb, s);
+    };
+    // the bulk product from the three-part L: K' = 3BS, 2BS, BS over the stack's BULK blocks
+    auto gemm_bulk = [&](cudaStream_t s, bool tA, int64_t m, const bf16 *A, int64_t lda, int64_t j, float *C) {
+        const bf16 *Bj = SB + j * stk;
+        lt_bgemm(ctx, tA, m, ncp, 3 * BS, -1.f, A, lda, Bj, 6 * BS, 1.f, C, Nb, s);
+        lt_bgemm(ctx, tA, m, ncp, 2 * BS, -1.f, A, lda, Bj + 3 * BS, 6 * BS, 1.f, C, Nb, s);
+        lt_bgemm(ctx, tA, m, ncp, BS, -1.f, A, lda, Bj + 5 * BS, 6 * BS, 1.f, C, Nb, s);
     };
     auto fork = [&]() {   // B and C start after everything queued on A so far
         HF_CUDA(cudaEventRecord(evS[0], st));
@@ -302,30 +425,24 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
     HF_CUDA(cudaMemsetAsync(Xb, 0, (size_t)Nb * ncp * sizeof(float), st));
     fork();
     // ---- forward: L Y = X
-    for (int j = 0; j < nb; ++j) {
-        const int64_t j0 = (int64_t)j * BS;
+    for (int64_t j = 0; j < nb; ++j) {
+        const int64_t j0 = j * BS;
         if (j >= 1) HF_CUDA(cudaStreamWaitEvent(st, evC[j - 1], 0));   // coupling of j-1 wrote Xa_j
         if (j >= 2) HF_CUDA(cudaStreamWaitEvent(st, evB[j - 2], 0));   // bulk of j-2 wrote Xb_j
-        split(st, Xa, Xb, j0, p.SX);
+        stack(st, Xa, Xb, j, S6, 0);
         HF_CUDA(cudaEventRecord(evX[j], st));
         if (j + 1 < nb) {   // C: Xa_{j+1} -= G_j X_j
             HF_CUDA(cudaStreamWaitEvent(sc, evX[j], 0));
-            parts(p.Gpart, (size_t)j * BS * BS, A);
-            parts(p.SX, j0, B);
-            gemm6(ctx, sc, false, BS, ncp, BS, -1.f, A, BS, B, Nb, 1.f, Xa + j0 + BS, Nb);
+            gemm_small(sc, false, bp(p.Gc) + j * per6, j, -1.f, 1.f, Xa + j0 + BS);
             HF_CUDA(cudaEventRecord(evC[j], sc));
         }
-        parts(p.Ipart, (size_t)j * BS * (BS + 1), A);                    // A: Y_j = Linv_j X_j
-        parts(p.SX, j0, B);
-        gemm6(ctx, st, false, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Y + j0, Nb);
+        gemm_small(st, false, bp(p.Ic) + j * per6, j, 1.f, 0.f, Y + j0);   // A: Y_j = Linv_j X_j
         if (j + 2 < nb) {   // B: Xb_{>j+1} -= L_{>j+1,j} Y_j
-            split(st, Y, nullptr, j0, p.SY);
+            stack(st, Y, nullptr, j, SB, 1);
             HF_CUDA(cudaEventRecord(evY[j], st));
             HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
-            const int64_t r2 = j0 + 2 * BS;
-            parts(p.Lpart, r2 + j0 * Nb, A);
-            parts(p.SY, j0, B);
-            gemm6(ctx, sb, false, Nb - r2, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Xb + r2, Nb);
+            const int64_t h = (nb - 1 - j) * BS;
+            gemm_bulk(sb, false, h - BS, Lc + lc_off(j, nb, BS) + BS, h, j, Xb + j0 + 2 * BS);
             HF_CUDA(cudaEventRecord(evB[j], sb));
         }
     }
@@ -336,29 +453,23 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
     float *Za = Y, *Zb = Xb, *Xo = Xa;
     HF_CUDA(cudaMemsetAsync(Zb, 0, (size_t)Nb * ncp * sizeof(float), st));
     fork();
-    for (int j = nb - 1; j >= 0; --j) {
-        const int64_t j0 = (int64_t)j * BS;
+    for (int64_t j = nb - 1; j >= 0; --j) {
+        const int64_t j0 = j * BS;
         if (j + 1 < nb) HF_CUDA(cudaStreamWaitEvent(st, evC[j + 1], 0));   // coupling of j+1 wrote Za_j
         if (j + 2 < nb) HF_CUDA(cudaStreamWaitEvent(st, evB[j + 2], 0));   // bulk of j+2 wrote Zb_j
-        split(st, Za, Zb, j0, p.SX);
+        stack(st, Za, Zb, j, S6, 0);
         HF_CUDA(cudaEventRecord(evX[j], st));
         if (j >= 1) {   // C: Za_{j-1} -= H_{j-1}^T Z_j
             HF_CUDA(cudaStreamWaitEvent(sc, evX[j], 0));
-            parts(p.Hpart, (size_t)(j - 1) * BS * BS, A);
-            parts(p.SX, j0, B);
-            gemm6(ctx, sc, true, BS, ncp, BS, -1.f, A, BS, B, Nb, 1.f, Za + j0 - BS, Nb);
+            gemm_small(sc, true, bp(p.Ht) + (j - 1) * per6, j, -1.f, 1.f, Za + j0 - BS);
             HF_CUDA(cudaEventRecord(evC[j], sc));
         }
-        parts(p.Ipart, (size_t)j * BS * (BS + 1), A);                      // A: X_j = Linv_j^T Z_j
-        parts(p.SX, j0, B);
-        gemm6(ctx, st, true, BS, ncp, BS, 1.f, A, BS, B, Nb, 0.f, Xo + j0, Nb);
+        gemm_small(st, true, bp(p.It) + j * per6, j, 1.f, 0.f, Xo + j0);   // A: X_j = Linv_j^T Z_j
         if (j >= 2) {   // B: Zb_{<j-1} -= (L_{j,<j-1})^T X_j
-            split(st, Xo, nullptr, j0, p.SY);
+            stack(st, Xo, nullptr, j, SB, 1);
             HF_CUDA(cudaEventRecord(evY[j], st));
             HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
-            parts(p.Lpart, j0, A);
-            parts(p.SY, j0, B);
-            gemm6(ctx, sb, true, j0 - BS, ncp, BS, -1.f, A, Nb, B, Nb, 1.f, Zb, Nb);
+            gemm_bulk(sb, true, j0 - BS, Lr + lr_off(j, BS), 3 * BS, j, Zb);
             HF_CUDA(cudaEventRecord(evB[j], sb));
         }
     }
