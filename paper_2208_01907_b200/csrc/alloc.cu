@@ -143,6 +143,17 @@ void dev_free(void *p, cudaStream_t s) {
     c.cached_bytes += l.bytes;
 }
 
+// bytes the cache holds free (reusable, or returned to the driver on an OOM retry) on a device
+size_t cached_free_bytes(int dev) {
+    Cache &c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    size_t b = 0;
+    for (auto &kv : c.free_)
+        if (kv.first.first == dev)
+            for (auto &e : kv.second) b += e.first;
+    return b;
+}
+
 }  // namespace hf
 
 extern "C" hf_status hf_trim_cache(int device) {

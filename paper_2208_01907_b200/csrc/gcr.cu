@@ -68,6 +68,20 @@ void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uin
         w.ozown.reset();
         return;
     }
+    if (o.matvec == 0) {
+        // the automatic choice also leaves room for the block GCR's own growth: P and Q for 16
+        // blocks while the 8-block ones are still alive (grow() doubles them), plus 1 GB
+        size_t fr = 0, tot = 0;
+        HF_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t need = (size_t)3 * 8 * (size_t)L * (size_t)n * 8 + ((size_t)1 << 30);
+        if (fr + cached_free_bytes(ctx->device) < need) {
+            if (getenv("HF_MATVEC_DEBUG"))
+                fprintf(stderr, "[hf matvec] int8 slices leave %zu of %zu bytes needed: DMMA\n",
+                        fr + cached_free_bytes(ctx->device), need);
+            w.ozown.reset();
+            return;
+        }
+    }
     w.oz = w.ozown.get();
     if (getenv("HF_MATVEC_DEBUG")) fprintf(stderr, "[hf matvec] int8 slices, n = %lld\n", (long long)n);
 }

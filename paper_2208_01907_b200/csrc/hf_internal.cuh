@@ -52,6 +52,7 @@ struct Error {
 // device-memory cache (alloc.cu): stream-ordered reuse of freed blocks
 void *dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void *p, cudaStream_t s);
+size_t cached_free_bytes(int dev);
 
 template <typename T>
 struct DBuf {

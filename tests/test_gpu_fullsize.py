@@ -119,7 +119,12 @@ C4_PREFIX = 1024
 
 
 def test_c4_full(ctx):
+    from paper_2208_01907_b200 import hf
     spec = hi.CONFIGS["C4"]
+    # C4 uses most of the device: release what the earlier full-size tests left cached in
+    # torch's allocator and in the library's
+    torch.cuda.empty_cache()
+    hf.hf_trim_cache(0)
     Kb = hi.make_kbar("C4", 0, device="cuda")
     # [R1] scaling: a principal sub-block of Kbar scales to the same bits as in K
     sub = torch.from_numpy(np.sort(np.random.default_rng(4).choice(spec.L, 384, replace=False))).cuda()
