@@ -108,6 +108,11 @@ def trsm_roofline(N, n2, iters, flops, ms, setup_ms, ach, nbytes):
             "frac": b_ach / bpk if b_ach else None, "peak_source": src, "bf16_flops_per_step": bf16_fl,
             "fp32_equivalent_tflops": ach, "fp32_equivalent_vs_ffma_peak": ach / FFMA_PEAK_DERIVED if ach else None,
             "flops_per_step": flops, "ms_per_step": ms, "block_rows": BS, "blocks": nb,
+            # per application and direction: nb inverse products, nb - 1 couplings (one GEMM each
+            # over K' = 6 BS) and three bulk GEMMs for each of nb - 2 blocks; the setup's doubling
+            # levels (2 each) and the 12 batched coupling part products
+            "library_launches_per_step": (iters + 1) * 2 * (nb + (nb - 1) + 3 * max(nb - 2, 0))
+                                         + 2 * max(0, int(np.log2(BS // 64))) + (12 if nb > 1 else 0),
             "hbm_gbs": nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None, "setup_ms_per_step": setup_ms}
 
 
