@@ -73,8 +73,8 @@ def test_blocked_preconditioner_executed_bf16_work(N, n2, monkeypatch):
     r = bench.trsm_roofline(N, n2, iters, 2.0 * N * N * n2 * (iters + 1), 1.0, 0.5, 1.0, 1.0)
     assert r["bf16_flops_per_step"] == pytest.approx(6 * 2 * per_dir * (iters + 1), rel=1e-12)
     assert r["block_rows"] == BS and r["blocks"] == nb
-    if N == 16128:   # C2: 7 applications x 2 directions x (8 + 7 + 3 x 6) + 2 x 5 + 12
-        assert r["library_launches_per_step"] == 7 * 2 * 33 + 10 + 12
+    if N == 16128:   # C2, 6 applications: x 2 directions x (8 + 7 + 3 x 6) + 2 x 5 + 12
+        assert r["library_launches_per_step"] == (iters + 1) * 2 * 33 + 10 + 12
 
 
 def test_launch_summary_separates_library_kernels(tmp_path):
