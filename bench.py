@@ -38,6 +38,7 @@ DMMA_PEAK_MEASURED = 37.15                              # tools/peaks.py, profil
 KCLASSES = ("scale", "chain", "trailing", "dgemm", "trsm", "trsm_setup", "gram", "hard", "other",
             "ozaki_split", "ozaki_imma", "ozaki_combine")
 OZAKI_SLICES = 8                                        # ozaki.cu default (hf_gcr_opts.slices = 0)
+OZAKI_MODULI = 16                                       # ozaki2.cu (the residue form)
 
 
 def int8_peak():
@@ -412,7 +413,7 @@ def main():
         ev[3].record(stream)
         kd = hf.hf_factor_hard(ctx, hy)
         ev[4].record(stream)
-        res = (lf.N, lf.L - lf.n2_tau_only, lf.n2, info.iters, kd, info.max_rel_res_true)
+        res = (lf.N, lf.L - lf.n2_tau_only, lf.n2, info.iters, kd, info.max_rel_res_true, info.matvec)
         hy.close()               # one factorization's buffers live at a time: the library's
         lf.close()               # memory cache then serves every step from the same blocks
         return res, ev
@@ -461,7 +462,7 @@ def main():
     klaunch = {c: (kstats[c][1] - base[c][1]) / args.steps for c in base}
     kwork = {c: tuple((a - b) / args.steps for a, b in zip(ctx.kernel_work(c), wbase[c])) for c in base}
 
-    N, Ntau, n2, iters, kd, tres = results[-1]
+    N, Ntau, n2, iters, kd, tres, mv_form = results[-1]
     L = spec.L
     ozaki = kms.get("ozaki_imma", 0.0) > 0.0
     fm = flop_model(L, N, Ntau, n2, iters, ozaki=ozaki)
@@ -530,27 +531,32 @@ def main():
         # products per mat-vec, each 2 N^2 n2 int8 ops of algorithmic work; the int8 GEMMs are
         # cuBLASLt's (a plain library GEMM), the splitting and the combination libhf's
         mv_ms = kms["ozaki_split"] + kms["ozaki_imma"] + kms["ozaki_combine"]
-        nprod = OZAKI_SLICES * (OZAKI_SLICES + 1) // 2
+        crt = mv_form == 3
+        nprod = OZAKI_MODULI if crt else OZAKI_SLICES * (OZAKI_SLICES + 1) // 2
         i8_ops = nprod * fm["matvec"]
         i8_peak, i8_src = int8_peak()
         i8_ach = i8_ops / (kms["ozaki_imma"] * 1e-3) / 1e12
         rooflines["matvec"] = {
-            "kernel": "K11 W as FP64 emulated on the int8 tensor cores (Ozaki scheme, %d slices: k_oz_split, "
-                      "%d int8 GEMMs per mat-vec on cuBLASLt IMMA, k_oz_combine<%d>)" % (OZAKI_SLICES, OZAKI_SLICES,
-                                                                                         OZAKI_SLICES),
+            "kernel": ("K11 W as FP64 emulated on the int8 tensor cores, residue (CRT) form: 53-bit integer "
+                       "scalings, %d moduli <= 256 (k_oz2_residues, %d exact int8 GEMMs per mat-vec on cuBLASLt "
+                       "IMMA, k_oz2_combine: Garner mixed radix + FP64 Horner)" % (OZAKI_MODULI, OZAKI_MODULI)) if crt
+                      else ("K11 W as FP64 emulated on the int8 tensor cores (Ozaki scheme, %d slices: k_oz_split, "
+                            "%d int8 GEMMs per mat-vec on cuBLASLt IMMA, k_oz_combine<%d>)" %
+                            (OZAKI_SLICES, OZAKI_SLICES, OZAKI_SLICES)),
             "bound": "int8_tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s", "frac": i8_ach / i8_peak,
             "peak_source": i8_src, "int8_ops_per_step": i8_ops, "products_per_matvec": nprod,
             "fp64_equivalent_tflops": fm["matvec"] / (mv_ms * 1e-3) / 1e12,
             "fp64_equivalent_vs_dmma_peak": fm["matvec"] / (mv_ms * 1e-3) / 1e12 / DMMA_PEAK_MEASURED,
             "ms_per_step": mv_ms, "imma_ms_per_step": kms["ozaki_imma"], "split_ms_per_step": kms["ozaki_split"],
             "combine_ms_per_step": kms["ozaki_combine"],
-            "library_launches_per_step": (iters + 2) * OZAKI_SLICES}
+            "library_launches_per_step": (iters + 2) * (OZAKI_MODULI if crt else OZAKI_SLICES)}
     shares = {c: round(kms[c] / ms_step, 4) for c in kms}
 
     line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if args.mode == "replicas" else "strong", "vs_baseline": None,
             "dtype": "fp32+fp64+i8" if ozaki else "fp32+fp64", "data": "synthetic",
+            "matvec_form": {1: "fp64 DMMA", 2: "int8 slices (Ozaki)", 3: "int8 residues (CRT)"}.get(mv_form),
             "config": {"workload": spec.name, "L": L, "N": N, "n2": n2, "n2_tau_only": L - Ntau,
                        "tau": spec.tau, "n_min": spec.n_min, "seed": args.seed, "gcr_iters": iters,
                        "kernel_dim": kd, "gcr_true_rel_res": tres,

@@ -253,7 +253,7 @@ hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
  * precision"): Z = K W for a SYMMETRIC K (L x L, ld; the Ozaki path reads row m
  * as column m), W: L x n (ldw), Z: L x n (ldz), all DEVICE FP64.  matvec 1 = FP64
  * DMMA, 2 = FP64 emulated on the int8 tensor cores with `slices` slices (0 = 8;
- * see hf_gcr_opts).  Synchronises. */
+ * see hf_gcr_opts), 3 = the residue form.  Synchronises. */
 hf_status hf_matvec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const double *W, int64_t ldw, int64_t n,
                     double *Z, int64_t ldz, int32_t matvec, int32_t slices);
 
@@ -263,6 +263,12 @@ typedef struct {
     int32_t max_iter;  /* iteration cap (100)                                       */
     /* the FP64 block mat-vec K11 W (P:507's "SpMM in higher precision"):
      *   1: FP64 DMMA tensor-core GEMM;
+     *   3: FP64 emulated on the int8 tensor cores in residue (Chinese remainder)
+     *      form (ozaki2.cu): K and W scaled by powers of two to 53-bit integers,
+     *      16 pairwise coprime moduli <= 256, one exact int8 GEMM per modulus,
+     *      the exact integer product rebuilt by Garner's mixed radix and
+     *      rounded in FP64 -- error below Lk 2^(e_m + f_c - 52) + 16 ulps;
+     *      16 int8 copies of K of memory, Lk <= 130000;
      *   2: FP64 emulated on the int8 tensor cores (Ozaki scheme, ozaki.cu): K's
      *      rows and W's columns split into `slices` exact 7-bit fixed-point
      *      slices under a power-of-two scale, every slice product an exact
@@ -270,8 +276,9 @@ typedef struct {
      *      group and the groups in FP64 -- error below
      *      ~2^(-7 slices) Lk max|K_m.| max|W_.c| per entry (8 slices: 2^-56,
      *      against FP64's Lk 2^-53 |K||W|);
-     *   0: automatic = 2 when the block has >= 32 columns, else 1.
-     * The environment variable HF_MATVEC=dmma|ozaki overrides 0.             */
+     *   0: automatic: for blocks of >= 32 columns 3, else 2, else 1, as device
+     *      memory allows (the K copies and the block GCR's growth); else 1.
+     * The environment variable HF_MATVEC=dmma|ozaki|ozaki2 overrides 0.      */
     int32_t matvec;
     int32_t slices;    /* matvec 2: slices per operand, 2..9 (0 = 8)               */
 } hf_gcr_opts;
@@ -279,6 +286,7 @@ typedef struct {
     int32_t iters;                 /* completed block-GCR iterations          */
     double max_rel_res_recursive;  /* max over columns at exit (recursive r)  */
     double max_rel_res_true;       /* max over columns of ||K12 - K11 X||/||K12|| */
+    int32_t matvec;                /* the mat-vec form that ran (hf_gcr_opts.matvec 1..3) */
 } hf_gcr_info;
 
 /* Alg. 1 steps 2-4: K11 X12 = K12 by right-preconditioned block GCR in FP64

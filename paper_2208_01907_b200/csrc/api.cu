@@ -255,17 +255,21 @@ hf_status hf_matvec(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const d
                     double *Z, int64_t ldz, int32_t matvec, int32_t slices) {
     if (!ctx) return HF_ERR_INVALID_ARG;
     return guarded(ctx, [&] {
-        HF_REQUIRE(L >= 0 && n >= 0 && ld >= L && ldw >= L && ldz >= L && (matvec == 1 || matvec == 2) &&
+        HF_REQUIRE(L >= 0 && n >= 0 && ld >= L && ldw >= L && ldz >= L && matvec >= 1 && matvec <= 3 &&
                        (slices == 0 || (slices >= 2 && slices <= 9)) && (L == 0 || n == 0 || (K && W && Z)),
                    "hf_matvec: bad arguments");
         if (L == 0 || n == 0) return;
         if (matvec == 1) {
             hf::DBuf<double> work;
             hf::dgemm(ctx, false, L, n, L, 1.0, K, ld, W, ldw, 0.0, Z, ldz, nullptr, &work);
-        } else {
+        } else if (matvec == 2) {
             hf::Ozaki oz;
             hf::ozaki_prepare(ctx, oz, K, ld, L, nullptr, slices > 0 ? slices : hf::ozaki_slices(), n);
             hf::ozaki_matvec(ctx, oz, W, ldw, n, Z, ldz, 0.0, 1.0);
+        } else {
+            hf::Ozaki2 oz;
+            hf::ozaki2_prepare(ctx, oz, K, ld, L, nullptr, n);
+            hf::ozaki2_matvec(ctx, oz, W, ldw, n, Z, ldz, 0.0, 1.0);
         }
         HF_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -454,14 +458,14 @@ hf_status hf_schur_gcr(hf_ctx *ctx, const double *K, int64_t ld, const hf_lowfac
     *out = nullptr;
     hf_gcr_opts o{1e-14, 100, 0, 0};
     if (opts) o = *opts;
-    hf_gcr_info info{0, 0.0, 0.0};
+    hf_gcr_info info{0, 0.0, 0.0, 0};
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
     hf_status s = guarded(ctx, [&] {
         HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr: bad arguments");
 
         HF_REQUIRE(o.tol > 0.0 && o.max_iter >= 1, "hf_schur_gcr: tol > 0, max_iter >= 1");
-        HF_REQUIRE(o.matvec >= 0 && o.matvec <= 2 && (o.slices == 0 || (o.slices >= 2 && o.slices <= 9)),
-                   "hf_schur_gcr: matvec in 0..2, slices 0 or 2..9");
+        HF_REQUIRE(o.matvec >= 0 && o.matvec <= 3 && (o.slices == 0 || (o.slices >= 2 && o.slices <= 9)),
+                   "hf_schur_gcr: matvec in 0..3, slices 0 or 2..9");
         hy->K = K;
         hy->ld = ld;
         hy->L = lf->L;
@@ -492,7 +496,7 @@ hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
     *out = nullptr;
     hf_gcr_opts o{1e-28, 100, 0, 0};
     if (opts) o = *opts;
-    hf_gcr_info info{0, 0.0, 0.0};
+    hf_gcr_info info{0, 0.0, 0.0, 0};
     std::unique_ptr<hf_hybrid> hy(new hf_hybrid());
     hf_status s = guarded(ctx, [&] {
         HF_REQUIRE(ld >= lf->L && (lf->L == 0 || K), "hf_schur_gcr_dd: bad arguments");
@@ -523,7 +527,7 @@ hf_status hf_schur_gcr_dd(hf_ctx *ctx, const double *K, int64_t ld, const hf_low
 hf_status hf_solve_dd(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *xhi, double *xlo,
                       hf_gcr_info *info_host) {
     if (!ctx || !hy || !b || !xhi || !xlo) return HF_ERR_INVALID_ARG;
-    hf_gcr_info info{0, 0.0, 0.0};
+    hf_gcr_info info{0, 0.0, 0.0, 0};
     hf_status s = guarded(ctx, [&] {
         if (!hy->dd) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: not a double-double hybrid"};
         if (!hy->hard_done && hy->n2 > 0) throw hf::Error{HF_ERR_STATE, "hf_solve_dd: call hf_factor_hard first"};
@@ -581,7 +585,7 @@ hf_status hf_hard_export(hf_ctx *ctx, const hf_hybrid *hy, int64_t *perm2_host, 
 
 hf_status hf_solve(hf_ctx *ctx, const hf_hybrid *hy, const double *b, double *x, hf_gcr_info *info_host) {
     if (!ctx || !hy || !b || !x) return HF_ERR_INVALID_ARG;
-    hf_gcr_info info{0, 0.0, 0.0};
+    hf_gcr_info info{0, 0.0, 0.0, 0};
     hf_status s = guarded(ctx, [&] {
         if (!hy->hard_done && hy->n2 > 0)
             throw hf::Error{HF_ERR_STATE, "hf_solve: call hf_factor_hard first"};

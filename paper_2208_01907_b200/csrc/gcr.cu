@@ -41,49 +41,72 @@ struct GcrWork {
     std::vector<double> *hist = nullptr;   // optional: max relative residual after every iteration
     Ozaki *oz = nullptr;                   // the mat-vec on the int8 tensor cores (ozaki.cu), else DMMA
     std::unique_ptr<Ozaki> ozown;
+    std::unique_ptr<Ozaki2> oz2;           // the residue form (ozaki2.cu, matvec 3)
 };
 
-// hf_gcr_opts.matvec: 2 = the Ozaki-scheme mat-vec, 1 = DMMA, 0 = automatic (Ozaki for
-// blocks of >= 32 columns; HF_MATVEC=dmma|ozaki overrides the automatic choice)
+// hf_gcr_opts.matvec: 3 = the residue (CRT) form of the int8 emulation (ozaki2.cu), 2 = the
+// slice form (ozaki.cu), 1 = DMMA, 0 = automatic: for blocks of >= 32 columns the residue
+// form, else the slice form, else DMMA, as device memory allows; HF_MATVEC=dmma|ozaki|ozaki2
+// overrides the automatic choice
 void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, int64_t n,
                   const hf_gcr_opts &o, GcrWork &w) {
-    if (w.oz) return;
+    if (w.oz || w.oz2) return;
+    const bool dbg = getenv("HF_MATVEC_DEBUG") != nullptr;
     int mode = o.matvec;
-    if (mode == 0) {
-        mode = n >= 32 ? 2 : 1;
+    const bool autom = mode == 0;
+    if (autom) {
+        mode = n >= 32 ? 3 : 1;
         if (const char *e = getenv("HF_MATVEC")) {
             if (std::string(e) == "dmma") mode = 1;
             else if (std::string(e) == "ozaki") mode = 2;
+            else if (std::string(e) == "ozaki2") mode = 3;
         }
     }
-    if (mode != 2 || L == 0) return;
+    if (L == 0 || mode == 1) return;
+    // the automatic choice also leaves room for the block GCR's own growth: P and Q for 16
+    // blocks while the 8-block ones are still alive (grow() doubles them), plus 1 GB
+    auto room = [&]() {
+        size_t fr = 0, tot = 0;
+        HF_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t need = (size_t)3 * 8 * (size_t)L * (size_t)n * 8 + ((size_t)1 << 30);
+        const size_t have = fr + cached_free_bytes(ctx->device);
+        if (have < need && dbg) fprintf(stderr, "[hf matvec] %zu of %zu bytes left\n", have, need);
+        return have >= need;
+    };
+    if (mode == 3) {   // the residue form (16 int8 residue copies of K)
+        w.oz2.reset(new Ozaki2());
+        try {
+            ozaki2_prepare(ctx, *w.oz2, K, ld, L, mask, n);
+        } catch (const Error &e) {
+            if (e.st != HF_ERR_OOM || !autom) throw;
+            if (dbg) fprintf(stderr, "[hf matvec] int8 residues do not fit (%s)\n", e.msg.c_str());
+            w.oz2.reset();
+        }
+        if (w.oz2 && (!autom || room())) {
+            if (dbg) fprintf(stderr, "[hf matvec] int8 residues (CRT), n = %lld\n", (long long)n);
+            return;
+        }
+        w.oz2.reset();
+        mode = 2;   // the automatic choice tries the slice form (8 copies' worth) next
+    }
     w.ozown.reset(new Ozaki());
     try {
         ozaki_prepare(ctx, *w.ozown, K, ld, L, mask, o.slices > 0 ? o.slices : ozaki_slices(), n);
     } catch (const Error &e) {
         // the slices take as much memory as K itself; the automatic choice falls back to
         // the DMMA product when they do not fit (e.g. C4 beside the FP32 preconditioner)
-        if (e.st != HF_ERR_OOM || o.matvec == 2) throw;
-        if (getenv("HF_MATVEC_DEBUG")) fprintf(stderr, "[hf matvec] int8 slices do not fit (%s): DMMA\n", e.msg.c_str());
+        if (e.st != HF_ERR_OOM || !autom) throw;
+        if (dbg) fprintf(stderr, "[hf matvec] int8 slices do not fit (%s): DMMA\n", e.msg.c_str());
         w.ozown.reset();
         return;
     }
-    if (o.matvec == 0) {
-        // the automatic choice also leaves room for the block GCR's own growth: P and Q for 16
-        // blocks while the 8-block ones are still alive (grow() doubles them), plus 1 GB
-        size_t fr = 0, tot = 0;
-        HF_CUDA(cudaMemGetInfo(&fr, &tot));
-        const size_t need = (size_t)3 * 8 * (size_t)L * (size_t)n * 8 + ((size_t)1 << 30);
-        if (fr + cached_free_bytes(ctx->device) < need) {
-            if (getenv("HF_MATVEC_DEBUG"))
-                fprintf(stderr, "[hf matvec] int8 slices leave %zu of %zu bytes needed: DMMA\n",
-                        fr + cached_free_bytes(ctx->device), need);
-            w.ozown.reset();
-            return;
-        }
+    if (autom && !room()) {
+        if (dbg) fprintf(stderr, "[hf matvec] int8 slices: DMMA\n");
+        w.ozown.reset();
+        return;
     }
     w.oz = w.ozown.get();
-    if (getenv("HF_MATVEC_DEBUG")) fprintf(stderr, "[hf matvec] int8 slices, n = %lld\n", (long long)n);
+    if (dbg) fprintf(stderr, "[hf matvec] int8 slices, n = %lld\n", (long long)n);
 }
 
 void grow(hf_ctx *ctx, GcrWork &w, int64_t L, int64_t n, int64_t need) {
@@ -111,6 +134,10 @@ inline void matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const ui
         ozaki_matvec(ctx, *w.oz, W, L, n, Z, L, beta, alpha);
         return;
     }
+    if (w.oz2) {
+        ozaki2_matvec(ctx, *w.oz2, W, L, n, Z, L, beta, alpha);
+        return;
+    }
     dgemm(ctx, false, L, n, L, alpha, K, ld, W, L, beta, Z, L, mask, &w.dgw);
 }
 
@@ -129,6 +156,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
                const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info, GcrWork &w) {
     cudaStream_t st = ctx->stream;
     setup_matvec(ctx, K, ld, L, mask, n, o, w);
+    info->matvec = w.oz2 ? 3 : (w.oz ? 2 : 1);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
     w.rn2.alloc(n, st);
@@ -220,6 +248,7 @@ void iterative_refinement(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, c
                           GcrWork &w) {
     cudaStream_t st = ctx->stream;
     setup_matvec(ctx, K, ld, L, mask, n, o, w);
+    info->matvec = w.oz2 ? 3 : (w.oz ? 2 : 1);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
     w.rn2.alloc(n, st);
@@ -488,7 +517,7 @@ extern "C" hf_status hf_krylov_solve(hf_ctx *ctx, const double *K, int64_t ld, c
         Bm.alloc((size_t)L * ncol, st);
         for (int64_t c = 0; c < ncol; ++c) hf::mask_vec(ctx, L, mask.p, B + c * L, Bm.p + c * L);
         hf_gcr_opts o{tol, max_iter, 0, 0};
-        hf_gcr_info info{0, 0.0, 0.0};
+        hf_gcr_info info{0, 0.0, 0.0, 0};
         std::vector<double> hist;
         int32_t iters = 0;
         hf_status fail = HF_OK;

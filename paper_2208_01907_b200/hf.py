@@ -51,12 +51,12 @@ class gcr_opts(ctypes.Structure):
                 ("slices", ctypes.c_int32)]
 
 
-MATVEC = {"auto": 0, "dmma": 1, "ozaki": 2}
+MATVEC = {"auto": 0, "dmma": 1, "ozaki": 2, "ozaki2": 3}
 
 
 class gcr_info(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("max_rel_res_recursive", ctypes.c_double),
-                ("max_rel_res_true", ctypes.c_double)]
+                ("max_rel_res_true", ctypes.c_double), ("matvec", ctypes.c_int32)]
 
 
 _lib = None
@@ -389,6 +389,7 @@ class GcrInfo:
     max_rel_res_recursive: float
     max_rel_res_true: float
     status: int = HF_OK
+    matvec: int = 0        # the mat-vec form that ran: 1 DMMA, 2 int8 slices, 3 int8 residues
 
 
 class Hybrid:
@@ -503,7 +504,7 @@ def hf_schur_gcr(ctx: Context, K: torch.Tensor, lf: LowFactor, tol: float = 1e-1
                               _ptr(S), ctypes.byref(info))
     ok = (HF_ERR_NOT_CONVERGED, HF_ERR_BREAKDOWN) if accept_failure else ()
     ctx.check(st, ok)
-    gi = GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true, st)
+    gi = GcrInfo(info.iters, info.max_rel_res_recursive, info.max_rel_res_true, st, info.matvec)
     return Hybrid(ctx, h, lf, K), gi, S
 
 

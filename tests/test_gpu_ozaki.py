@@ -44,6 +44,10 @@ def test_integer_operands_exact(ctx, L, n, bits):
     assert np.array_equal(Z, exact)
     Zd = hf.hf_matvec(ctx, Kd, Wd, "dmma").cpu().numpy()
     assert np.array_equal(Zd, exact)
+    # the residue form reconstructs the exact integer product and rounds it by a Horner
+    # evaluation in FP64: within 16 ulps of the exact product
+    Z2 = hf.hf_matvec(ctx, Kd, Wd, "ozaki2").cpu().numpy()
+    assert np.all(np.abs(Z2 - exact) <= 16 * 2.0 ** -53 * np.abs(exact))
 
 
 def _exp_bound(v):
@@ -86,8 +90,34 @@ def test_error_bound_vs_extended_precision(ctx, s):
         assert e_oz <= max(10 * e_dm, 1e-15), (e_oz, e_dm)
 
 
+def test_residue_form_error_bound_vs_extended_precision(ctx):
+    """ozaki2.cu: |Z - KW| <= Lk 2^(e_m + f_c - 52) (the 53-bit truncations of both operands)
+    + 2^-48 |KW| (the FP64 Horner evaluation) entrywise, rows / columns spread over 2^+-12;
+    at the FP64 DMMA product's level normwise."""
+    from paper_2208_01907_b200 import hf
+    rng = np.random.default_rng(21)
+    L, n = 768, 40
+    d = 2.0 ** rng.uniform(-12, 12, size=L)
+    K = _sym(rng.standard_normal((L, L))) * d[:, None] * d[None, :]
+    W = rng.standard_normal((n, L)) * (2.0 ** rng.uniform(-8, 8, size=n))[:, None]
+    ref = W.astype(np.longdouble) @ K.astype(np.longdouble)
+    Kd, Wd = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    Z = hf.hf_matvec(ctx, Kd, Wd, "ozaki2").cpu().numpy()
+    em = np.array([_exp_bound(K[:, m]) for m in range(L)])
+    fc = np.array([_exp_bound(W[c]) for c in range(n)])
+    bound = L * np.ldexp(1.0, em[None, :] + fc[:, None] - 52) + 2.0 ** -48 * np.abs(ref).astype(np.float64)
+    err = np.abs((Z.astype(np.longdouble) - ref).astype(np.float64))
+    assert (err <= bound).all(), float((err / bound).max())
+    Zd = hf.hf_matvec(ctx, Kd, Wd, "dmma").cpu().numpy()
+    nref = np.linalg.norm(ref.astype(np.float64))
+    e2 = np.linalg.norm((Z - ref).astype(np.float64)) / nref
+    ed = np.linalg.norm((Zd - ref).astype(np.float64)) / nref
+    assert e2 <= max(10 * ed, 1e-15), (e2, ed)
+
+
+@pytest.mark.parametrize("mv", ["ozaki", "ozaki2"])
 @pytest.mark.parametrize("name,seed", [("P2048", 0), ("S24", 0), ("P4096", 1)])
-def test_schur_gcr_ozaki_matches_dmma(ctx, name, seed):
+def test_schur_gcr_ozaki_matches_dmma(ctx, name, seed, mv):
     """The block GCR + Schur complement with the emulated mat-vec: same iteration count
     (+-1) and S22 within 1e-9 of the FP64 DMMA run, true residuals <= 1e-12, and the
     oracle's S22 within the stage-2 parity tolerance."""
@@ -98,7 +128,7 @@ def test_schur_gcr_ozaki_matches_dmma(ctx, name, seed):
     hf.hf_scale(ctx, K)
     lf = hf.hf_factor_lowprec(ctx, K, tau=spec.tau, n_min=max(spec.n_min, 32))
     hy1, i1, S1 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True, matvec="dmma")
-    hy2, i2, S2 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True, matvec="ozaki")
+    hy2, i2, S2 = hf.hf_schur_gcr(ctx, K, lf, want_S22_host=True, matvec=mv)
     assert abs(i1.iters - i2.iters) <= 1
     assert i2.max_rel_res_true <= 1e-12 and i1.max_rel_res_true <= 1e-12
     Ko, _ = oracle.scale(Kb.numpy())
