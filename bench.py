@@ -539,7 +539,7 @@ def main():
         rooflines["matvec"] = {
             "kernel": ("K11 W as FP64 emulated on the int8 tensor cores, residue (CRT) form: 53-bit integer "
                        "scalings, %d moduli <= 256 (k_oz2_residues, %d exact int8 GEMMs per mat-vec on cuBLASLt "
-                       "IMMA, k_oz2_combine: Garner mixed radix + FP64 Horner)" % (OZAKI_MODULI, OZAKI_MODULI)) if crt
+                       "IMMA as one strided batch, k_oz2_combine: Garner mixed radix + FP64 Horner)" % (OZAKI_MODULI, OZAKI_MODULI)) if crt
                       else ("K11 W as FP64 emulated on the int8 tensor cores (Ozaki scheme, %d slices: k_oz_split, "
                             "%d int8 GEMMs per mat-vec on cuBLASLt IMMA, k_oz_combine<%d>)" %
                             (OZAKI_SLICES, OZAKI_SLICES, OZAKI_SLICES)),
@@ -549,7 +549,7 @@ def main():
             "fp64_equivalent_vs_dmma_peak": fm["matvec"] / (mv_ms * 1e-3) / 1e12 / DMMA_PEAK_MEASURED,
             "ms_per_step": mv_ms, "imma_ms_per_step": kms["ozaki_imma"], "split_ms_per_step": kms["ozaki_split"],
             "combine_ms_per_step": kms["ozaki_combine"],
-            "library_launches_per_step": (iters + 2) * (OZAKI_MODULI if crt else OZAKI_SLICES)}
+            "library_launches_per_step": (iters + 2) * (1 if crt else OZAKI_SLICES)}
     shares = {c: round(kms[c] / ms_step, 4) for c in kms}
 
     line = {"metric": "hybrid_factor_schur_tflops", "value": value, "unit": "TFLOP/s", "n_gpus": world,

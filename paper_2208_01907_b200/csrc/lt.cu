@@ -122,10 +122,12 @@ void lt_release_stream(hf_ctx *ctx, cudaStream_t s) {
 
 // library kernels: not counted in ctx->launches (libhf's own launches)
 void lt_imma(hf_ctx *ctx, int64_t rows, int64_t cols, int64_t k, const int8_t *A, int64_t lda, const int8_t *B,
-             int64_t ldb, int32_t *D, int64_t ldd) {
+             int64_t ldb, int32_t *D, int64_t ldd, int batch, int64_t sA, int64_t sB, int64_t sD) {
+    if (rows == 0 || cols == 0 || batch == 0) return;
     LtState &lt = lt_state(ctx);
     std::lock_guard<std::mutex> g(lt.mu);
-    const LtPlan &pl = plan(lt, {1, 1, 0, rows, cols, k, lda, ldb, ldd, 1, 0, 0, 0, 0});
+    const LtPlan &pl = plan(lt, {1, 1, 0, rows, cols, k, lda, ldb, ldd, batch, batch > 1 ? sA : 0,
+                                 batch > 1 ? sB : 0, batch > 1 ? sD : 0, 0});
     const int32_t one = 1, zero = 0;
     HF_CUBLAS(cublasLtMatmul(lt.h, pl.op, &one, A, pl.la, B, pl.lb, &zero, D, pl.lc, D, pl.lc, &pl.algo,
                              lt.workspace(ctx->stream), LT_WS, ctx->stream));

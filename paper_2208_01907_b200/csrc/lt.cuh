@@ -9,9 +9,10 @@
 
 namespace hf {
 
-// D (rows x cols, int32, ldd) = A^T B;  A: k x rows int8 (lda), B: k x cols int8 (ldb)
+// D (rows x cols, int32, ldd) = A^T B;  A: k x rows int8 (lda), B: k x cols int8 (ldb);
+// `batch` problems at the given element strides
 void lt_imma(hf_ctx *ctx, int64_t rows, int64_t cols, int64_t k, const int8_t *A, int64_t lda, const int8_t *B,
-             int64_t ldb, int32_t *D, int64_t ldd);
+             int64_t ldb, int32_t *D, int64_t ldd, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sD = 0);
 
 // C = alpha op(A) op(B) + beta C, FP32 column-major, `batch` problems at the given element
 // strides; tf32: the tensor-core TF32 path (inputs rounded to TF32 by the hardware, FP32

@@ -49,26 +49,6 @@ int inv_mod(int a, int m) {   // a^{-1} mod m (gcd 1)
     return 1;
 }
 
-void upload_constants() {
-    static std::once_flag once[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::call_once(once[dev % 64], [] {
-        int pm[NMOD][NMOD] = {}, pinv[NMOD] = {};
-        for (int l = 0; l < NMOD; ++l) {
-            const int m = kModH[l];
-            long long P = 1 % m;   // P_j mod m_l
-            for (int j = 0; j < l; ++j) {
-                pm[l][j] = (int)P;
-                P = (P * kModH[j]) % m;
-            }
-            pinv[l] = inv_mod((int)P, m);   // P_l^{-1} mod m_l
-        }
-        cudaMemcpyToSymbol(kPm, pm, sizeof(pm));
-        cudaMemcpyToSymbol(kPinv, pinv, sizeof(pinv));
-    });
-    HF_CUDA(cudaGetLastError());
-}
 
 __device__ __forceinline__ int exp_bound2(double mx) {
     if (!(mx > 0.0)) return 0;
@@ -94,64 +74,114 @@ __device__ __forceinline__ double block_max2(double v) {
 }
 
 // one block per vector (a column of K = row of the symmetric K, or a column of W): the
-// exponent of its masked maximum, then its 16 residue vectors.  The 53-bit integer
-// x' = trunc(x 2^{53-e}) (signed, two's complement) is cut into c2 2^36 + c1 2^18 + c0 with
-// 0 <= c0, c1 < 2^18 and |c2| < 2^17: x' mod m = (c0 + c1 (2^18 mod m) + c2 (2^36 mod m) + O_m)
-// mod m, the offset O_m (a multiple of m above 2^25) making the sum non-negative and below
-// 2^27; then the symmetric range [-m/2, m/2).
-__host__ __device__ constexpr unsigned pow18(int l) { return (1u << 18) % (unsigned)modulus(l); }
-__host__ __device__ constexpr unsigned pow36(int l) { return pow18(l) * pow18(l) % (unsigned)modulus(l); }
-__host__ __device__ constexpr int offset(int l) { return ((1 << 25) + modulus(l) - 1) / modulus(l) * modulus(l); }
-
-__device__ __forceinline__ void chunks(double w, int &c0, int &c1, int &c2) {
-    const long long s = (long long)w;   // exact: |w| < 2^53
-    c0 = (int)(s & 0x3FFFF);
-    c1 = (int)((s >> 18) & 0x3FFFF);
-    c2 = (int)(s >> 36);
+// exponent e of its masked maximum, then its 16 residue vectors.  The 53-bit integer
+// x' = trunc(x 2^{53-e}) (two's complement) is cut into five 13-bit chunks,
+// x' = c0 + c1 2^13 + c2 2^26 + c3 2^39 + c4 2^52 (0 <= c0..c3 < 2^13, c4 in [-2, 1]), and per
+// modulus, all in exact FP32 arithmetic (every value an integer below 2^24):
+//   y = sum_i c_i p_i,  p_i = 2^{13 i} mod m in [-m/2, m/2]     (|y| < 3.2e6 < 2^22)
+//   q = rint(y / m)  as  fma(y, fl(1/m), 1.5 2^23) - 1.5 2^23   (|y fl(1/m) - y/m| < 1e-3, while
+//                     y/m is >= 1/(2m) >= 2e-3 from a half-integer for odd m; exact for m = 256)
+//   r = y - q m, |r| <= m/2, taken as the low byte of the float r + 1.5 2^23
+// so r = x' (mod m) with |r| <= 128 (-128 for the one tie of m = 256): a residue the int8 GEMM
+// takes as is (the combine reduces its sums mod m again).
+__host__ __device__ constexpr int pchunk(int l, int i) {   // 2^{13 i} mod m, symmetric
+    int r = 1;
+    for (int k = 0; k < i; ++k) r = r * (1 << 13) % modulus(l);
+    return 2 * r > modulus(l) ? r - modulus(l) : r;
 }
+constexpr float kMagic = 12582912.0f;   // 1.5 2^23: adding it rounds to an integer, keeps two's complement bits
+
+// two entries at once (FFMA2 / FADD2: two independent IEEE operations per instruction); the
+// per-modulus constants as float2 pairs in constant memory so FFMA2 reads them as operands
+__constant__ float2 kRc[NMOD][6];   // p_1..p_4, 1/m, -m (each duplicated)
 
 template <int L0>
-__device__ __forceinline__ unsigned residue_byte(int c0, int c1, int c2) {
-    constexpr unsigned M = (unsigned)modulus(L0);
-    const unsigned y = (unsigned)(c0 + c1 * (int)pow18(L0) + c2 * (int)pow36(L0) + offset(L0));
-    const unsigned r = y % M;                                           // [0, M)
-    return (2 * r >= M ? r - M : r) & 0xFFu;                            // the symmetric residue's byte
+__device__ __forceinline__ float2 residue_pair(const float2 (&c)[5]) {
+    const float2 mg = make_float2(kMagic, kMagic);
+    float2 y = __ffma2_rn(c[1], kRc[L0][0], c[0]);
+    y = __ffma2_rn(c[2], kRc[L0][1], y);
+    y = __ffma2_rn(c[3], kRc[L0][2], y);
+    y = __ffma2_rn(c[4], kRc[L0][3], y);
+    const float2 q = __fadd2_rn(__ffma2_rn(y, kRc[L0][4], mg), make_float2(-kMagic, -kMagic));
+    return __ffma2_rn(q, kRc[L0][5], __fadd2_rn(y, mg));   // r + 1.5 2^23: r in byte 0
 }
 
-// four consecutive entries per thread: per modulus one 32-bit store of their four residues
+// four consecutive entries per thread (two pairs): per modulus one 32-bit store of their four
+// residues
 template <int L0>
-__device__ __forceinline__ void store_residues(const int (&c)[4][3], int8_t *o, int64_t res_stride) {
+__device__ __forceinline__ void store_residues(const float2 (&c01)[5], const float2 (&c23)[5], int8_t *o,
+                                               int64_t res_stride) {
     if constexpr (L0 < NMOD) {
-        unsigned packed = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) packed |= residue_byte<L0>(c[i][0], c[i][1], c[i][2]) << (8 * i);
-        *reinterpret_cast<unsigned *>(o + (int64_t)L0 * res_stride) = packed;
-        store_residues<L0 + 1>(c, o, res_stride);
+        const float2 r01 = residue_pair<L0>(c01), r23 = residue_pair<L0>(c23);
+        const unsigned lo = __byte_perm(__float_as_uint(r01.x), __float_as_uint(r01.y), 0x0040);
+        const unsigned hi = __byte_perm(__float_as_uint(r23.x), __float_as_uint(r23.y), 0x0040);
+        *reinterpret_cast<unsigned *>(o + (int64_t)L0 * res_stride) = __byte_perm(lo, hi, 0x5410);
+        store_residues<L0 + 1>(c01, c23, o, res_stride);
     }
 }
 
+__device__ __forceinline__ float chunk_f(unsigned bits) {   // 0 <= bits < 2^13, exactly
+    return __int_as_float((int)(bits | 0x4B000000u)) - 8388608.0f;
+}
+
 // ldA and res_stride are multiples of 16, so every 4-entry group is 4-byte aligned
-__global__ void __launch_bounds__(256) k_oz2_residues(int64_t len, int64_t ldA, const double *__restrict__ X,
-                                                      int64_t ldx, const uint8_t *__restrict__ mask,
-                                                      int64_t res_stride, int8_t *__restrict__ out,
-                                                      int32_t *__restrict__ ex) {
-    const int64_t v = blockIdx.x;
-    const double *x = X + v * ldx;
+// the exponent of a vector's masked maximum (one block per vector)
+__device__ __forceinline__ int vector_exponent(const double *x, int64_t len, const uint8_t *mask) {
     double mx = 0.0;
     for (int64_t k = threadIdx.x; k < len; k += blockDim.x)
         if (!mask || mask[k]) mx = fmax(mx, fabs(x[k]));
-    const int e = exp_bound2(block_max2(mx));
-    if (threadIdx.x == 0) ex[v] = e;
+    return exp_bound2(block_max2(mx));
+}
+
+__global__ void __launch_bounds__(256) k_oz2_exponents(int64_t len, const double *__restrict__ X, int64_t ldx,
+                                                       const uint8_t *__restrict__ mask, int32_t *__restrict__ ex) {
+    const int e = vector_exponent(X + (int64_t)blockIdx.x * ldx, len, mask);
+    if (threadIdx.x == 0) ex[blockIdx.x] = e;
+}
+
+// given = 0: one block per vector finds the exponent itself (K: L blocks fill the GPU);
+// given = 1: the exponents are in ex already (k_oz2_exponents) and blockIdx.y cuts each vector
+// into gridDim.y pieces (W: n vectors alone would leave most SMs idle)
+__global__ void __launch_bounds__(256) k_oz2_residues(int64_t len, int64_t ldA, const double *__restrict__ X,
+                                                      int64_t ldx, const uint8_t *__restrict__ mask,
+                                                      int64_t res_stride, int8_t *__restrict__ out,
+                                                      int32_t *__restrict__ ex, int given) {
+    const int64_t v = blockIdx.x;
+    const double *x = X + v * ldx;
+    int e;
+    if (given) {
+        e = ex[v];
+    } else {
+        e = vector_exponent(x, len, mask);
+        if (threadIdx.x == 0) ex[v] = e;
+    }
+    // x 2^{53-e} as (x 2^a) 2^b with both factors normal doubles (e can be as low as -1073)
+    const int a = min(53 - e, 1000);
+    const double sa = ldexp(1.0, a), sb = ldexp(1.0, 53 - e - a);
+    const int64_t piece = (ldA / 4 + gridDim.y - 1) / gridDim.y * 4;   // entries per piece, a multiple of 4
+    const int64_t kbeg = (int64_t)blockIdx.y * piece, kend = min(ldA, kbeg + piece);
     int8_t *o = out + v * ldA;
-    for (int64_t k0 = 4 * (int64_t)threadIdx.x; k0 < ldA; k0 += 4 * (int64_t)blockDim.x) {
-        int c[4][3];
+    for (int64_t k0 = kbeg + 4 * (int64_t)threadIdx.x; k0 < kend; k0 += 4 * (int64_t)blockDim.x) {
+        float2 c01[5], c23[5];   // the chunks of entries (k0, k0+1) and (k0+2, k0+3) as FFMA2 pairs
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int64_t k = k0 + i;
-            const double w = (k < len && (!mask || mask[k])) ? trunc(scalbn(x[k], 53 - e)) : 0.0;   // |w| < 2^53
-            chunks(w, c[i][0], c[i][1], c[i][2]);
+            // branch-free: loads at a clamped index (len >= 1), then the selection
+            const int64_t k = k0 + i, kc = min(k, len - 1);
+            const double xl = __ldg(x + kc);
+            const bool keep = k < len && (!mask || __ldg(mask + kc));
+            const double xv = keep ? xl : 0.0;
+            const long long s = __double2ll_rz((xv * sa) * sb);   // |s| < 2^53, exact scaling
+            const unsigned lo = (unsigned)s, hi = (unsigned)((unsigned long long)s >> 32);
+            float2 *c = i < 2 ? c01 : c23;
+            float *cc[5] = {i & 1 ? &c[0].y : &c[0].x, i & 1 ? &c[1].y : &c[1].x, i & 1 ? &c[2].y : &c[2].x,
+                            i & 1 ? &c[3].y : &c[3].x, i & 1 ? &c[4].y : &c[4].x};
+            *cc[0] = chunk_f(lo & 0x1FFFu);
+            *cc[1] = chunk_f((lo >> 13) & 0x1FFFu);
+            *cc[2] = chunk_f(__funnelshift_r(lo, hi, 26) & 0x1FFFu);
+            *cc[3] = chunk_f((hi >> 7) & 0x1FFFu);
+            *cc[4] = (float)((int)hi >> 20);                    // s >> 52 in [-2, 1]
         }
-        store_residues<0>(c, o + k0, res_stride);
+        store_residues<0>(c01, c23, o + k0, res_stride);
     }
 }
 
@@ -198,6 +228,34 @@ __global__ void __launch_bounds__(256) k_oz2_combine(int64_t L, int64_t n, const
     }
 }
 
+void upload_constants() {
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(once[dev % 64], [] {
+        int pm[NMOD][NMOD] = {}, pinv[NMOD] = {};
+        for (int l = 0; l < NMOD; ++l) {
+            const int m = kModH[l];
+            long long P = 1 % m;   // P_j mod m_l
+            for (int j = 0; j < l; ++j) {
+                pm[l][j] = (int)P;
+                P = (P * kModH[j]) % m;
+            }
+            pinv[l] = inv_mod((int)P, m);   // P_l^{-1} mod m_l
+        }
+        float2 rc[NMOD][6];
+        for (int l = 0; l < NMOD; ++l) {
+            for (int i = 1; i <= 4; ++i) rc[l][i - 1] = make_float2((float)pchunk(l, i), (float)pchunk(l, i));
+            rc[l][4] = make_float2(1.0f / (float)kModH[l], 1.0f / (float)kModH[l]);
+            rc[l][5] = make_float2(-(float)kModH[l], -(float)kModH[l]);
+        }
+        cudaMemcpyToSymbol(kRc, rc, sizeof(rc));
+        cudaMemcpyToSymbol(kPm, pm, sizeof(pm));
+        cudaMemcpyToSymbol(kPinv, pinv, sizeof(pinv));
+    });
+    HF_CUDA(cudaGetLastError());
+}
+
 unsigned grid2(hf_ctx *ctx, int64_t n) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16));
 }
@@ -220,7 +278,7 @@ void ozaki2_prepare(hf_ctx *ctx, Ozaki2 &oz, const double *K, int64_t ld, int64_
     oz.f.alloc((size_t)std::max<int64_t>(n, 1), st);
     oz.C.alloc((size_t)NMOD * std::max<int64_t>(n, 1) * ldA, st);
     ClassTimer tm(ctx, "ozaki_split", st, 0.0, 8.0 * (double)L * L + (double)NMOD * L * ldA);
-    k_oz2_residues<<<(unsigned)L, 256, 0, st>>>(L, ldA, K, ld, mask, ldA * ldA, oz.A.p, oz.e.p);
+    k_oz2_residues<<<(unsigned)L, 256, 0, st>>>(L, ldA, K, ld, mask, ldA * ldA, oz.A.p, oz.e.p, 0);
     HF_CHECK_LAUNCH(ctx);
 }
 
@@ -233,14 +291,25 @@ void ozaki2_matvec(hf_ctx *ctx, Ozaki2 &oz, const double *W, int64_t ldw, int64_
     oz.C.alloc((size_t)NMOD * n * ldA, st);
     {
         ClassTimer tm(ctx, "ozaki_split", st, 0.0, 8.0 * (double)L * n + (double)NMOD * n * ldA);
-        k_oz2_residues<<<(unsigned)n, 256, 0, st>>>(L, ldA, W, ldw, oz.mask, n * ldA, oz.B.p, oz.f.p);
+        k_oz2_exponents<<<(unsigned)n, 256, 0, st>>>(L, W, ldw, oz.mask, oz.f.p);
+        HF_CHECK_LAUNCH(ctx);
+        // pieces of >= 4096 entries, about eight blocks per SM over all columns
+        const int64_t want = std::max<int64_t>(1, (int64_t)ctx->num_sms * 8 / std::max<int64_t>(n, 1));
+        const unsigned pieces = (unsigned)std::min<int64_t>(want, std::max<int64_t>(1, ldA / 4096));
+        k_oz2_residues<<<dim3((unsigned)n, pieces), 256, 0, st>>>(L, ldA, W, ldw, oz.mask, n * ldA, oz.B.p,
+                                                                  oz.f.p, 1);
         HF_CHECK_LAUNCH(ctx);
     }
     {
         ClassTimer tm(ctx, "ozaki_imma", st, 2.0 * (double)L * L * n, (double)NMOD * L * ldA);
-        for (int l = 0; l < NMOD; ++l)
-            lt_imma(ctx, ldA, n, ldA, oz.A.p + (size_t)l * ldA * ldA, ldA, oz.B.p + (size_t)l * n * ldA, ldA,
-                    oz.C.p + (size_t)l * n * ldA, ldA);
+        // the 16 products as one strided batch (16 x the tiles of one product: no partial last wave)
+        static const bool batched = !(getenv("HF_OZ2_BATCH") && atoi(getenv("HF_OZ2_BATCH")) == 0);
+        if (batched)
+            lt_imma(ctx, ldA, n, ldA, oz.A.p, ldA, oz.B.p, ldA, oz.C.p, ldA, NMOD, ldA * ldA, n * ldA, n * ldA);
+        else
+            for (int l = 0; l < NMOD; ++l)
+                lt_imma(ctx, ldA, n, ldA, oz.A.p + (size_t)l * ldA * ldA, ldA, oz.B.p + (size_t)l * n * ldA, ldA,
+                        oz.C.p + (size_t)l * n * ldA, ldA);
     }
     ClassTimer tm(ctx, "ozaki_combine", st, 0.0, 4.0 * NMOD * (double)n * L + 16.0 * (double)L * n);
     k_oz2_combine<<<grid2(ctx, L * n), 256, 0, st>>>(L, n, oz.C.p, ldA, n * ldA, oz.e.p, oz.f.p, oz.mask, alpha,
