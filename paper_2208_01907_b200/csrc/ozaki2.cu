@@ -38,9 +38,7 @@ __host__ __device__ constexpr int modulus(int l) {
          : l == 13 ? 199 : l == 14 ? 197 : 193;
 }
 // Garner with partial products: v_l = ((r_l - sum_{j<l} v_j (P_j mod m_l)) mod m_l) Pinv_l mod m_l,
-// P_j = m_0 ... m_{j-1} (P_0 = 1), Pinv_l = P_l^{-1} mod m_l
-__constant__ int kPm[NMOD][NMOD];   // kPm[l][j] = P_j mod m_l (j < l)
-__constant__ int kPinv[NMOD];
+// P_j = m_0 ... m_{j-1} (P_0 = 1), Pinv_l = P_l^{-1} mod m_l (k_oz2_combine)
 
 int inv_mod(int a, int m) {   // a^{-1} mod m (gcd 1)
     a %= m;
@@ -185,46 +183,84 @@ __global__ void __launch_bounds__(256) k_oz2_residues(int64_t len, int64_t ldA, 
     }
 }
 
-// per entry: the 16 residues -> Garner's symmetric mixed-radix digits (partial products: one
-// reduction per digit) -> Horner in FP64 -> the scaling, the mask, alpha and beta
+
+// Garner in exact FP32 arithmetic, two entries at once (FFMA2).  Digit l of the symmetric
+// mixed radix, v_l = ((x_l - sum_{j<l} v_j P_j) Pinv_l) mod m_l in [-m_l/2, m_l/2]:
+//   s = x_lo + x_hi (2^16 mod m) - sum_j v_j (P_j mod m)   (x_l = x_hi 2^16 + x_lo, int32 sum of
+//       the GEMM; |s| < 2^22 + 2^16 + 15 2^14 < 4.6e6, an exact FP32 integer)
+//   r = s - m rint(s/m)       (rint by the 1.5 2^23 constant: |s fl(1/m) - s/m| < 1.4e-3 < 1/(2m)
+//                              for every odd m <= 255, exact for m = 256, so r is the symmetric
+//                              residue)
+//   v = w - m rint(w/m), w = r Pinv_l  (|w| <= 2^14: exact, symmetric again)
+// then Horner in FP64 (16 roundings) as before.
+__constant__ float2 kGc[NMOD][NMOD + 5];   // [l][j < l]: -(P_j mod m_l); [l][16..20]: 2^16 mod m_l, Pinv_l, 1/m_l, -m_l, 0
+
+__device__ __forceinline__ float2 round_mod(float2 s, const float2 &invm, const float2 &negm) {
+    const float2 mg = make_float2(kMagic, kMagic);
+    const float2 q = __fadd2_rn(__ffma2_rn(s, invm, mg), make_float2(-kMagic, -kMagic));
+    return __ffma2_rn(q, negm, s);
+}
+
 template <int L0>
-__device__ __forceinline__ void garner(const int32_t (&x)[NMOD], int (&v)[NMOD]) {
+__device__ __forceinline__ void garner2(const float2 (&xlo)[NMOD], const float2 (&xhi)[NMOD], float2 (&v)[NMOD]) {
     if constexpr (L0 < NMOD) {
-        constexpr int M = modulus(L0);
-        int s = x[L0] % M;   // |x| < 2^31 -> (-M, M)
+        float2 s = __ffma2_rn(xhi[L0], kGc[L0][16], xlo[L0]);
 #pragma unroll
-        for (int j = 0; j < L0; ++j) s -= v[j] * kPm[L0][j];   // |s| < 2^20
-        int t = s % M;
-        if (t < 0) t += M;
-        t = (t * kPinv[L0]) % M;
-        v[L0] = (2 * t >= M) ? t - M : t;                       // symmetric digit
-        garner<L0 + 1>(x, v);
+        for (int j = 0; j < L0; ++j) s = __ffma2_rn(v[j], kGc[L0][j], s);
+        const float2 r = round_mod(s, kGc[L0][18], kGc[L0][19]);
+        v[L0] = round_mod(__fmul2_rn(r, kGc[L0][17]), kGc[L0][18], kGc[L0][19]);
+        garner2<L0 + 1>(xlo, xhi, v);
     }
 }
 
-__global__ void __launch_bounds__(256) k_oz2_combine(int64_t L, int64_t n, const int32_t *__restrict__ C,
-                                                     int64_t ldc, int64_t cstride, const int32_t *__restrict__ em,
+__device__ __forceinline__ void split16(int32_t x, float &lo, float &hi) {   // exact: x = hi 2^16 + lo
+    lo = __int_as_float((int)(((unsigned)x & 0xFFFFu) | 0x4B000000u)) - 8388608.0f;
+    hi = __int_as_float((int)((((unsigned)x >> 16) ^ 0x8000u) | 0x4B000000u)) - 8421376.0f;   // 2^23 + 2^15
+}
+
+// two entries per thread, rows m and m + 1 of column c = blockIdx.y (one 8-byte load per
+// modulus: ldc and cstride are multiples of 16 and row ldA - 1 >= L - 1 exists): the 16 int32
+// sums -> digits -> Horner (digit pairs first, exactly in FP32: |v_{2k+1} m_{2k} + v_{2k}| < 2^16)
+// -> the scaling, the mask, alpha and beta
+__global__ void __launch_bounds__(256) k_oz2_combine(int64_t L, const int32_t *__restrict__ C, int64_t ldc,
+                                                     int64_t cstride, const int32_t *__restrict__ em,
                                                      const int32_t *__restrict__ fc, const uint8_t *__restrict__ mask,
                                                      double alpha, double beta, double *__restrict__ Z, int64_t ldz) {
-    const int64_t total = L * n;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t m = e % L, c = e / L;
-        const bool keep = !mask || mask[m];
-        double acc = 0.0;
-        if (keep) {
-            int32_t x[NMOD];
+    const int64_t c = blockIdx.y, m = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (m >= L) return;
+    const bool two = m + 1 < L;
+    const bool keep0 = !mask || mask[m], keep1 = two && (!mask || mask[m + 1]);
+    float2 xlo[NMOD], xhi[NMOD];
+    const int32_t *cp = C + m + c * ldc;
 #pragma unroll
-            for (int l = 0; l < NMOD; ++l) x[l] = __ldcs(&C[(int64_t)l * cstride + m + c * ldc]);
-            int v[NMOD];
-            garner<0>(x, v);
-            double X = (double)v[NMOD - 1];
+    for (int l = 0; l < NMOD; ++l) {
+        const int2 x = __ldcs(reinterpret_cast<const int2 *>(cp + (int64_t)l * cstride));
+        float lo0, hi0, lo1, hi1;
+        split16(x.x, lo0, hi0);
+        split16(x.y, lo1, hi1);
+        xlo[l] = make_float2(lo0, lo1);
+        xhi[l] = make_float2(hi0, hi1);
+    }
+    float2 v[NMOD];
+    garner2<0>(xlo, xhi, v);
+    double X0 = 0.0, X1 = 0.0;
 #pragma unroll
-            for (int l = NMOD - 2; l >= 0; --l) X = fma(X, (double)modulus(l), (double)v[l]);
-            acc = scalbn(X, em[m] + fc[c] - 106);
-        }
-        double *z = Z + m + c * ldz;
-        const double ab = keep ? __dmul_rn(alpha, acc) : 0.0;
-        *z = (beta == 0.0) ? ab : fma(beta, *z, ab);
+    for (int k = NMOD / 2 - 1; k >= 0; --k) {
+        const float mk = (float)modulus(2 * k);
+        const float2 u = __ffma2_rn(v[2 * k + 1], make_float2(mk, mk), v[2 * k]);
+        const double R = (double)modulus(2 * k) * (double)modulus(2 * k + 1);
+        X0 = fma(X0, R, (double)u.x);
+        X1 = fma(X1, R, (double)u.y);
+    }
+    const int32_t fcol = fc[c];
+    double *z = Z + m + c * ldz;
+    {
+        const double ab = keep0 ? __dmul_rn(alpha, scalbn(X0, em[m] + fcol - 106)) : 0.0;
+        z[0] = (beta == 0.0) ? ab : fma(beta, z[0], ab);
+    }
+    if (two) {
+        const double ab = keep1 ? __dmul_rn(alpha, scalbn(X1, em[m + 1] + fcol - 106)) : 0.0;
+        z[1] = (beta == 0.0) ? ab : fma(beta, z[1], ab);
     }
 }
 
@@ -250,8 +286,17 @@ void upload_constants() {
             rc[l][5] = make_float2(-(float)kModH[l], -(float)kModH[l]);
         }
         cudaMemcpyToSymbol(kRc, rc, sizeof(rc));
-        cudaMemcpyToSymbol(kPm, pm, sizeof(pm));
-        cudaMemcpyToSymbol(kPinv, pinv, sizeof(pinv));
+        float2 gc[NMOD][NMOD + 5] = {};
+        auto sym = [](long long r, int m) { r %= m; if (r < 0) r += m; return (float)(2 * r > m ? r - m : r); };
+        for (int l = 0; l < NMOD; ++l) {
+            const int m = kModH[l];
+            for (int j = 0; j < l; ++j) gc[l][j] = make_float2(-sym(pm[l][j], m), -sym(pm[l][j], m));
+            gc[l][16] = make_float2(sym(65536, m), sym(65536, m));
+            gc[l][17] = make_float2(sym(pinv[l], m), sym(pinv[l], m));
+            gc[l][18] = make_float2(1.0f / (float)m, 1.0f / (float)m);
+            gc[l][19] = make_float2(-(float)m, -(float)m);
+        }
+        cudaMemcpyToSymbol(kGc, gc, sizeof(gc));
     });
     HF_CUDA(cudaGetLastError());
 }
@@ -312,8 +357,8 @@ void ozaki2_matvec(hf_ctx *ctx, Ozaki2 &oz, const double *W, int64_t ldw, int64_
                         oz.C.p + (size_t)l * n * ldA, ldA);
     }
     ClassTimer tm(ctx, "ozaki_combine", st, 0.0, 4.0 * NMOD * (double)n * L + 16.0 * (double)L * n);
-    k_oz2_combine<<<grid2(ctx, L * n), 256, 0, st>>>(L, n, oz.C.p, ldA, n * ldA, oz.e.p, oz.f.p, oz.mask, alpha,
-                                                      beta, Z, ldz);
+    k_oz2_combine<<<dim3((unsigned)((L + 511) / 512), (unsigned)n), 256, 0, st>>>(L, oz.C.p, ldA, n * ldA, oz.e.p,
+                                                                                oz.f.p, oz.mask, alpha, beta, Z, ldz);
     HF_CHECK_LAUNCH(ctx);
 }
 
