@@ -10,6 +10,7 @@
 // once.  At most HF_CACHE_FRACTION (default 0.4) of the device is kept
 // cached, so the caller's own allocator (torch) keeps room; hf_trim_cache()
 // (include/hf.h) releases everything cached.
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -69,6 +70,16 @@ void trim_device(int dev) {
 
 }  // namespace
 
+void host_trace(const char *where) {
+    static const double thr = getenv("HF_TRACE_HOST") ? atof(getenv("HF_TRACE_HOST")) : -1.0;
+    if (thr < 0.0) return;
+    static auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - last).count();
+    if (ms > thr) fprintf(stderr, "[hf host] %.3f ms before %s\n", ms, where);
+    last = now;
+}
+
 void *dev_alloc(size_t bytes, cudaStream_t s) {
     int dev = 0;
     HF_CUDA(cudaGetDevice(&dev));
@@ -92,7 +103,9 @@ void *dev_alloc(size_t bytes, cudaStream_t s) {
     void *p = nullptr;
     static const bool dbg = getenv("HF_ALLOC_DEBUG") != nullptr;
     if (dbg) fprintf(stderr, "[hf alloc] cudaMalloc %zu bytes (cached %zu)\n", want, c.cached_bytes);
+    host_trace("cudaMalloc call");
     cudaError_t e = cudaMalloc(&p, want);
+    host_trace("cudaMalloc");
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
         trim_device(dev);
@@ -134,8 +147,10 @@ void dev_free(void *p, cudaStream_t s) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(l.dev);
+        host_trace("over-cap free");
         cudaStreamSynchronize(s);
         cudaFree(p);
+        host_trace("over-cap free done");
         cudaSetDevice(cur);
         return;
     }

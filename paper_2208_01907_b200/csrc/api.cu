@@ -24,7 +24,9 @@ template <typename F>
 hf_status guarded(hf_ctx *ctx, F &&f) {
     DeviceGuard dg(ctx);
     try {
+        hf::host_trace("api call");
         f();
+        hf::host_trace("api return");
         if (ctx) ctx->last_error.clear();
         return HF_OK;
     } catch (const hf::Error &e) {

@@ -66,23 +66,29 @@ void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uin
     // the automatic choice also leaves room for the block GCR's own growth: P and Q for 16
     // blocks while the 8-block ones are still alive (grow() doubles them), plus 1 GB
     auto room = [&]() {
+        auto it = ctx->matvec_room.find({L, n});
+        if (it != ctx->matvec_room.end()) return it->second;
         size_t fr = 0, tot = 0;
         HF_CUDA(cudaMemGetInfo(&fr, &tot));
         const size_t need = (size_t)3 * 8 * (size_t)L * (size_t)n * 8 + ((size_t)1 << 30);
         const size_t have = fr + cached_free_bytes(ctx->device);
         if (have < need && dbg) fprintf(stderr, "[hf matvec] %zu of %zu bytes left\n", have, need);
+        ctx->matvec_room[{L, n}] = have >= need;
         return have >= need;
     };
     if (mode == 3) {   // the residue form (16 int8 residue copies of K)
         w.oz2.reset(new Ozaki2());
         try {
             ozaki2_prepare(ctx, *w.oz2, K, ld, L, mask, n);
+            host_trace("ozaki2_prepare");
         } catch (const Error &e) {
             if (e.st != HF_ERR_OOM || !autom) throw;
             if (dbg) fprintf(stderr, "[hf matvec] int8 residues do not fit (%s)\n", e.msg.c_str());
             w.oz2.reset();
         }
-        if (w.oz2 && (!autom || room())) {
+        const bool fits = w.oz2 && (!autom || room());
+        host_trace("room");
+        if (fits) {
             if (dbg) fprintf(stderr, "[hf matvec] int8 residues (CRT), n = %lld\n", (long long)n);
             return;
         }
@@ -146,7 +152,9 @@ double read_res(hf_ctx *ctx, GcrWork &w, int *bad) {
     int st = 0;
     HF_CUDA(cudaMemcpyAsync(&r, w.res.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     HF_CUDA(cudaMemcpyAsync(&st, w.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    host_trace("residual sync");
     HF_CUDA(cudaStreamSynchronize(ctx->stream));
+    host_trace("residual sync done");
     *bad = st;
     return r;
 }
@@ -156,6 +164,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
                const double *B, int64_t n, double *X, const hf_gcr_opts &o, hf_gcr_info *info, GcrWork &w) {
     cudaStream_t st = ctx->stream;
     setup_matvec(ctx, K, ld, L, mask, n, o, w);
+    host_trace("setup_matvec");
     info->matvec = w.oz2 ? 3 : (w.oz ? 2 : 1);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
@@ -170,6 +179,7 @@ void block_gcr(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_
 
     colnorm2(ctx, L, n, B, L, w.bn2.p);
     precond_apply(ctx, pc, n, B, L, X, L);                       // find x_0: Q x_0 = b
+    host_trace("precond_apply x0");
     HF_CUDA(cudaMemcpyAsync(R, B, (size_t)L * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     matvec(ctx, K, ld, L, mask, X, n, R, 1.0, -1.0, w);          // r_0 = b - A x_0
     colnorm2(ctx, L, n, R, L, w.rn2.p);
@@ -248,6 +258,7 @@ void iterative_refinement(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, c
                           GcrWork &w) {
     cudaStream_t st = ctx->stream;
     setup_matvec(ctx, K, ld, L, mask, n, o, w);
+    host_trace("setup_matvec");
     info->matvec = w.oz2 ? 3 : (w.oz ? 2 : 1);
     w.R.alloc((size_t)L * n, st);
     w.bn2.alloc(n, st);
@@ -300,7 +311,9 @@ void schur_gcr(hf_ctx *ctx, hf_hybrid *hy, const hf_gcr_opts &o, hf_gcr_info *in
     hy->lam2.alloc(std::max<int64_t>(n2, 1), st);
     if (n2 > 0)
         HF_CUDA(cudaMemcpyAsync(hy->lam2.p, lf->perm.p + N, n2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    host_trace("schur_gcr start");
     precond_setup(ctx, hy->pc, lf);
+    host_trace("precond_setup");
     hy->X.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->B.alloc((size_t)std::max<int64_t>(L * n2, 1), st);
     hy->S22.alloc((size_t)std::max<int64_t>(n2 * n2, 1), st);

@@ -152,6 +152,9 @@ struct hf_ctx {
     bool up_pending = false;
     // the blocked preconditioner's two helper streams (k_trsm_blk.cu), lazily created
     cudaStream_t aux[2] = {nullptr, nullptr};
+    // the automatic mat-vec choice's memory check per (L, n) (gcr.cu): made once, since
+    // cudaMemGetInfo waits on the device and the choice then stays the same for every solve
+    std::map<std::pair<int64_t, int64_t>, bool> matvec_room;
 };
 
 namespace hf {
@@ -212,6 +215,10 @@ struct ClassTimer {
 };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// host-side pacing diagnostics (HF_TRACE_HOST=<ms>): prints the host time since the previous
+// trace point when it exceeds the threshold
+void host_trace(const char *where);
 
 }  // namespace hf
 
