@@ -174,8 +174,9 @@ __device__ __forceinline__ unsigned long long ld_x(const unsigned long long *p) 
 // index spaces of that panel) and its nbq updates of the pivot column are applied
 // here first, one fmaf per pivot in order -- the same operands the trailing update
 // uses (role-symmetric [R8]), so the bits equal the serial schedule's.
-template <bool SYS>
-__global__ void __launch_bounds__(1024, 1) k_chain_d(DChainArgs a) {
+// MAXT: the launch bound, as k_chain's (a 256 / 512 bound lifts the 64-register cap)
+template <bool SYS, int MAXT = 1024>
+__global__ void __launch_bounds__(MAXT, 1) k_chain_d(DChainArgs a) {
     extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
     __shared__ uint32_t redi[32], redl[32];
@@ -1052,7 +1053,8 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
         HF_CUDA(cudaStreamSynchronize(st));   // nl0 dies here
     }
     xbar(st, 0);   // every rank's columns are cast before anyone reads them
-    for (void *kf : {(void *)k_chain_d<false>, (void *)k_chain_d<true>})
+    for (void *kf : {(void *)k_chain_d<false>, (void *)k_chain_d<true>, (void *)k_chain_d<false, 256>,
+                     (void *)k_chain_d<true, 256>, (void *)k_chain_d<false, 512>, (void *)k_chain_d<true, 512>})
         HF_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DTRAIL_SMEM));
     int tocc = 0;
@@ -1096,7 +1098,11 @@ void lowprec_factor_dist(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, co
             for (int t = 0; t < nbp; ++t) cf += 2.0 * (double)(m - t) * (t + nbq);
             ClassTimer tm(ctx, "chain", st, cf, 16.0 * ((double)m * nbp - 0.5 * (double)nbp * (nbp - 1)));
             void *args[] = {&ca};
-            void *kf = real ? (void *)k_chain_d<true> : (void *)k_chain_d<false>;
+            const int lb = std::max(nthr, getenv("HF_CHAIN_LB") ? atoi(getenv("HF_CHAIN_LB")) : 0);
+            void *kf = real ? (lb <= 256 ? (void *)k_chain_d<true, 256> : lb <= 512 ? (void *)k_chain_d<true, 512>
+                                                                               : (void *)k_chain_d<true>)
+                            : (lb <= 256 ? (void *)k_chain_d<false, 256> : lb <= 512 ? (void *)k_chain_d<false, 512>
+                                                                                : (void *)k_chain_d<false>);
             HF_CUDA(cudaLaunchCooperativeKernel(kf, dim3((unsigned)((hi - lo) * Cper)), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }

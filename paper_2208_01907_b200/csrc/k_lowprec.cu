@@ -208,7 +208,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //     (tag-checked) and the panel-start column V[:, P] for own rows;
 //  G  c_i = chain of fmaf over the earlier in-panel pivots in order [R8],
 //     s = c/r, L = c/d, diagonal.
-__global__ void __launch_bounds__(1024, 1) k_chain(ChainArgs a) {
+// MAXT: the launch bound (threads = own rows rounded to a warp: 256 at C2, 448 at C4).  A
+// bound of 256 / 512 lifts the register cap from 64 to 255 / 128 (108 used at 256): C2 chain
+// 52.0 -> 49.5 ms per step, same box, alternating runs.  Software-pipelining the fmaf chain's
+// shared loads with those registers was slower (51.6 ms).  HF_CHAIN_LB=1024 forces the
+// 1024-thread build.
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_chain(ChainArgs a) {
     extern __shared__ __align__(16) float smem[];
     __shared__ unsigned long long red[32];
     __shared__ unsigned long long bkey;
@@ -1350,7 +1356,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     int maxsmem = 0;
     HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain));
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain<1024>));
     maxsmem -= (int)fa.sharedSizeBytes;
     // Chain geometry (measured on B200 at C2, chain + trailing ms: 148 CTAs / nb 256: 106.3,
     // 148 / 128: 103.3, 74 / 128: 100.6, 64 / 128: 95.0, 64 / 192: 95.8, 32 / 96: 98.8):
@@ -1449,7 +1455,10 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         HF_CUDA(cudaStreamWaitEvent(st2, ctx->ev[0], 0));
     }
 
-    HF_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    const int chain_lb = getenv("HF_CHAIN_LB") ? atoi(getenv("HF_CHAIN_LB")) : 0;
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM + 128));
@@ -1536,7 +1545,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
         {
             ClassTimer tm(ctx, "chain", st, chain_flops(m, nbp), chain_bytes(m, nbp));
             void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            const int lb = std::max(nthr, chain_lb);
+            void *kf = lb <= 256 ? (void *)k_chain<256> : lb <= 512 ? (void *)k_chain<512> : (void *)k_chain<1024>;
+            HF_CUDA(cudaLaunchCooperativeKernel(kf, dim3((unsigned)G), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }
         const int64_t mp = m - nbp;
