@@ -1676,7 +1676,9 @@ struct ChainNSArgs {
 //    row V[P, :] entries of own indices from the panel-start matrix
 //  G c_i = V_iP + sum_u fmaf(-l_i^u, r_P^u), r_i = V_Pi + sum_u fmaf(-l_P^u, r_i^u)
 //    (u ascending), l_i = c_i / d, lazy diagonal fmaf(-l_i, r_i, v_ii)
-__global__ void __launch_bounds__(1024, 1) k_chain_ns(ChainNSArgs a) {
+// MAXT: the launch bound, as k_chain's (a 256 / 512 bound lifts the 64-register cap)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_chain_ns(ChainNSArgs a) {
     extern __shared__ float smem[];
     __shared__ unsigned long long red[32];
     __shared__ unsigned long long bkey;
@@ -1830,7 +1832,7 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
     int maxsmem = 0;
     HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_ns));
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain_ns<1024>));
     maxsmem -= (int)fa.sharedSizeBytes;
     const int nb_def = 64;   // two panel values per own index
     int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 4 / (2 * nb_def + 2)))));
@@ -1873,7 +1875,9 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
         k_iota32<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
         HF_CHECK_LAUNCH(ctx);
     }
-    HF_CUDA(cudaFuncSetAttribute(k_chain_ns, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain_ns<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain_ns<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain_ns<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     HF_CUDA(cudaFuncSetAttribute(k_trailing_c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRAIL_C_SMEM));
     int cur = 0;
     int64_t m = L, K0 = 0;
@@ -1892,7 +1896,9 @@ void lowprec_factor_ns(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, cons
         {
             ClassTimer tm(ctx, "chain");
             void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain_ns, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            const int lb = std::max(nthr, getenv("HF_CHAIN_LB") ? atoi(getenv("HF_CHAIN_LB")) : 0);
+            void *kf = lb <= 256 ? (void *)k_chain_ns<256> : lb <= 512 ? (void *)k_chain_ns<512> : (void *)k_chain_ns<1024>;
+            HF_CUDA(cudaLaunchCooperativeKernel(kf, dim3((unsigned)G), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }
         const int64_t mp = m - nbp;

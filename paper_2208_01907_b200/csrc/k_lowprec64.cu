@@ -80,7 +80,9 @@ struct Chain64Args {
     int32_t *status;
 };
 
-__global__ void __launch_bounds__(1024, 1) k_chain64(Chain64Args a) {
+// MAXT: the launch bound, as k_chain's (a 256 / 512 bound lifts the 64-register cap)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_chain64(Chain64Args a) {
     extern __shared__ double smem64[];
     __shared__ unsigned long long rab[32];
     __shared__ uint32_t rpi[32];
@@ -358,7 +360,7 @@ void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const
     int maxsmem = 0;
     HF_CUDA(cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain64));
+    HF_CUDA(cudaFuncGetAttributes(&fa, k_chain64<1024>));
     maxsmem -= (int)fa.sharedSizeBytes;
     const int nb_def = 64;
     const int gmax = (int)std::min<int64_t>(nsm, std::max<int64_t>(64, cdiv(L, (int64_t)(maxsmem / 8 / (nb_def + 2)))));
@@ -395,7 +397,9 @@ void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const
         k_iota32_64<<<(unsigned)cdiv(L, 256), 256, 0, st>>>(L, orig[0].p);
         HF_CHECK_LAUNCH(ctx);
     }
-    HF_CUDA(cudaFuncSetAttribute(k_chain64, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain64<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain64<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
+    HF_CUDA(cudaFuncSetAttribute(k_chain64<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem));
     int cur = 0;
     int64_t m = L, K0 = 0;
     while (m > 0) {
@@ -409,7 +413,9 @@ void lowprec_factor64(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const
         {
             ClassTimer tm(ctx, "chain");
             void *args[] = {&ca};
-            HF_CUDA(cudaLaunchCooperativeKernel((void *)k_chain64, dim3((unsigned)G), dim3(nthr), args, shm, st));
+            const int lb = std::max(nthr, getenv("HF_CHAIN_LB") ? atoi(getenv("HF_CHAIN_LB")) : 0);
+            void *kf = lb <= 256 ? (void *)k_chain64<256> : lb <= 512 ? (void *)k_chain64<512> : (void *)k_chain64<1024>;
+            HF_CUDA(cudaLaunchCooperativeKernel(kf, dim3((unsigned)G), dim3(nthr), args, shm, st));
             HF_CHECK_LAUNCH(ctx);
         }
         const int64_t mp = m - nbp;
