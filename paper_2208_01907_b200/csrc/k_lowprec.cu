@@ -1378,6 +1378,7 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     const int64_t R0 = cdiv(L, G0);
     HF_REQUIRE(R0 <= 1024, "L too large for one chain CTA per SM (R > 1024)");
     int nb = o.nb > 0 ? o.nb : nb_def;
+    if (o.nb <= 0 && getenv("HF_NB")) nb = std::max(8, atoi(getenv("HF_NB")));   // sweeps
     // with lookahead the chain holds both panels' values of its rows in shared memory
     const int nbf = (look ? 2 : 1);
     // the widest multiple of 16 (the trailing kernel's k chunk) that fits, e.g. 112 at C4

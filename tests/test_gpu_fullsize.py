@@ -182,4 +182,8 @@ def test_c4_full(ctx):
         assert abs(float(sd[0])) >= float(sd.abs().max()) - tol
         assert abs(float(sd[0]) - float(D[k])) <= tol
     assert info.max_rel_res_true <= 1e-12
+    # [R12]: the blocked tensor-core preconditioner may not cost iterations against the FP32
+    # substitution (the dataflow form, HF_PRECOND=dataflow: 16 at C4); the blocked form takes
+    # 11, and 18 when its bulk update accumulated the small bf16 parts after the large one
+    assert info.iters <= 16
     assert _rho_manufactured(ctx, hy, Kd) <= 1e-12
