@@ -393,6 +393,10 @@ def main():
     gen_dev = "cuda" if spec.L > 4096 else "cpu"
     seed = args.seed + (rank if args.mode == "replicas" else 0)
     Kb = hi.make_kbar(spec, seed, device=gen_dev).to(dev).contiguous()
+    if dev.type == "cuda":
+        # the generator's temporaries stay in torch's cache (C4: 39 GB beside the 34 GB input),
+        # which the library's device memory (the int8 residues of K) then cannot use
+        torch.cuda.empty_cache()
     # L > 32768 (C4, 34 GB in FP64): no pristine device copy -- every step scales K in
     # place; after the first, hf_scale sees an already-scaled matrix (Q = I, the same
     # bits) and does the same reads, multiplications and writes

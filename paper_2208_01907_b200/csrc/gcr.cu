@@ -45,9 +45,9 @@ struct GcrWork {
 };
 
 // hf_gcr_opts.matvec: 3 = the residue (CRT) form of the int8 emulation (ozaki2.cu), 2 = the
-// slice form (ozaki.cu), 1 = DMMA, 0 = automatic: for blocks of >= 32 columns the residue
-// form, else the slice form, else DMMA, as device memory allows; HF_MATVEC=dmma|ozaki|ozaki2
-// overrides the automatic choice
+// slice form (ozaki.cu), 1 = DMMA, 0 = automatic: for blocks of >= 96 columns the residue
+// form, for >= 32 (or when the residues do not fit) the slice form, else DMMA, as device
+// memory allows; HF_MATVEC=dmma|ozaki|ozaki2 overrides the automatic choice
 void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uint8_t *mask, int64_t n,
                   const hf_gcr_opts &o, GcrWork &w) {
     if (w.oz || w.oz2) return;
@@ -55,7 +55,11 @@ void setup_matvec(hf_ctx *ctx, const double *K, int64_t ld, int64_t L, const uin
     int mode = o.matvec;
     const bool autom = mode == 0;
     if (autom) {
-        mode = n >= 32 ? 3 : 1;
+        // the residue form reads 16 int8 copies of K per mat-vec, the slice form 8 (one per A
+        // slice, the B slices side by side) but computes 36 products instead of 16: with few
+        // columns the mat-vec is bound by those reads (C4, n = 64: residues 11.3 ms, slices
+        // 8.3 ms per mat-vec; n = 512: residues 23 ms, slices 46 ms; C2 n = 256: residues)
+        mode = n >= 96 ? 3 : (n >= 32 ? 2 : 1);
         if (const char *e = getenv("HF_MATVEC")) {
             if (std::string(e) == "dmma") mode = 1;
             else if (std::string(e) == "ozaki") mode = 2;

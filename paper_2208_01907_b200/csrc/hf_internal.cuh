@@ -263,6 +263,7 @@ struct PrecondBlk {
     DBuf<uint16_t> Ic, It;         // Linv_j, six-part concatenations (BS x 6BS / 6BS x BS) per block
     DBuf<uint16_t> Gc, Ht;         // G_j = L_{j+1,j} Linv_j (BS x 6BS), H_j = Linv_{j+1} L_{j+1,j} (6BS x BS)
     DBuf<float> Xa, Xb, Y;         // Nb x ncp FP32 workspaces (column-major)
+    DBuf<float> P6a, P6c;          // 6 x BS x ncp part-product partials of the small products (streams A, C)
     DBuf<uint16_t> S6, SB;         // per block: 6BS x ncp part stacks of its right-hand side / solution
     std::vector<cudaEvent_t> ev;   // per-block events of the three-stream schedule
     PrecondBlk() = default;

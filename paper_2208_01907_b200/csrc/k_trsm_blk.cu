@@ -111,6 +111,20 @@ __global__ void k_blk_split_rows(int64_t r0, int64_t nr, int64_t ncp, const floa
     }
 }
 
+// C (BS x ncp, ld ldc) = alpha (P0 + P1 + ... + P5) + beta C, the six part products of a
+// small product in their SMALL order (smallest first), summed in IEEE FP32 in that order
+__global__ void __launch_bounds__(256) k_blk_sum6(int64_t BS, int64_t ncp, const float *__restrict__ P, float alpha,
+                                                  float beta, float *__restrict__ C, int64_t ldc) {
+    const int64_t per = BS * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+        float v = P[e];
+#pragma unroll
+        for (int q = 1; q < 6; ++q) v += P[e + q * per];
+        float *c = C + (e % BS) + (e / BS) * ldc;
+        *c = beta == 0.f ? alpha * v : fmaf(beta, *c, alpha * v);
+    }
+}
+
 // Part orders of the K-concatenated products.  The six part products with i + j <= 4 as ONE
 // GEMM over K' = 6 BS:  [A3 A1 A2 A2 A1 A1] . [B1; B3; B2; B1; B2; B1]  (SMALL order, for the
 // latency-critical diagonal-inverse and coupling products, whose A operands are stored with
@@ -180,6 +194,12 @@ __global__ void k_blk_split6(int64_t r0, int64_t BS, int64_t ncp, const float *_
 //       three parts side by side, L3 L2 L1 (3BS columns), ld h_j, at 3 BS^2 (j (nb-1) - j (j-1) / 2)
 //   Lr: block row i (i >= 1) = the three parts stacked, L3 L2 L1 (3BS rows) x columns 0 .. iBS-1,
 //       ld 3BS, at 3 BS^2 (i-1) i / 2
+// the small products as a batch of six part GEMMs (HF_PRECOND_SPLITK=0/1 forces; default:
+// fewer than 256 right-hand-side columns)
+static bool splitk_small(int64_t ncp) {
+    if (const char *e = getenv("HF_PRECOND_SPLITK")) return atoi(e) != 0;
+    return ncp < 256;
+}
 __host__ __device__ __forceinline__ int64_t lc_off(int64_t j, int64_t nb, int64_t BS) {
     return 3 * BS * BS * (j * (nb - 1) - j * (j - 1) / 2);
 }
@@ -403,8 +423,25 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         k_blk_split6<<<grid_for(ctx, BS * ncp / 2), 256, 0, s>>>(j * BS, BS, ncp, src, src2, Nb, dst + j * stk, bulk);
         HF_CHECK_LAUNCH(ctx);
     };
-    // one GEMM over K' = 6BS (the duplicated-part A operands)
+    // one GEMM over K' = 6BS (the duplicated-part A operands), or (split) the six part products
+    // as one strided batch of K = BS GEMMs into partials summed smallest first by k_blk_sum6:
+    // with few right-hand sides the single GEMM has BS ncp / 64^2 CTAs walking a 6BS-long K
+    // (C4 with 64 columns per rank: 32 CTAs; trsm 183 -> 169 ms per stage 2 there, neutral at
+    // C2's 256 columns, where the default keeps the single GEMM)
+    const bool split = splitk_small(ncp);
+    if (split) {
+        p.P6a.alloc((size_t)6 * BS * ncp, st);
+        p.P6c.alloc((size_t)6 * BS * ncp, st);
+    }
     auto gemm_small = [&](cudaStream_t s, bool tA, const bf16 *A, int64_t j, float alpha, float beta, float *C) {
+        if (split) {
+            float *P6 = (s == sc) ? p.P6c.p : p.P6a.p;
+            lt_bgemm(ctx, tA, BS, ncp, BS, 1.f, A, tA ? 6 * BS : BS, S6 + j * stk, 6 * BS, 0.f, P6, BS, s, 6,
+                     tA ? BS : BS * BS, BS, BS * ncp);
+            k_blk_sum6<<<grid_for(ctx, BS * ncp), 256, 0, s>>>(BS, ncp, P6, alpha, beta, C, Nb);
+            HF_CHECK_LAUNCH(ctx);
+            return;
+        }
         lt_bgemm(ctx, tA, BS, ncp, 6 * BS, alpha, A, tA ? 6 * BS : BS, S6 + j * stk, 6 * BS, beta, C, Nb, s);
     };
     // the bulk product from the three-part L: K' = 3BS, 2BS, BS over the stack's BULK blocks

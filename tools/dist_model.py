@@ -58,6 +58,7 @@ def worker(name, G, mode):
     from paper_2208_01907_b200 import hf
     spec = hi.CONFIGS[name]
     K = hi.make_kbar(name, 0, device="cuda")
+    torch.cuda.empty_cache()   # the generator's temporaries (C4: 39 GB) back to the device
     ctx = hf.Context(0)
     hf.hf_scale(ctx, K)
     if G:
@@ -96,6 +97,7 @@ def worker_stage2(name, Gs):
     from paper_2208_01907_b200 import hf
     spec = hi.CONFIGS[name]
     K = hi.make_kbar(name, 0, device="cuda")
+    torch.cuda.empty_cache()   # the generator's temporaries (C4: 39 GB) back to the device
     ctx = hf.Context(0)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e[0].record()
