@@ -265,6 +265,8 @@ struct PrecondBlk {
     DBuf<float> Xa, Xb, Y;         // Nb x ncp FP32 workspaces (column-major)
     DBuf<float> P6a, P6c;          // 6 x BS x ncp part-product partials of the small products (streams A, C)
     DBuf<uint16_t> S6, SB;         // per block: 6BS x ncp part stacks of its right-hand side / solution
+    DBuf<uint16_t> SC;             // few columns: per block the 3BS x 3ncp part matrix of the bulk update
+    DBuf<float> TB;                // few columns: Nb x 3ncp partials of the bulk update
     std::vector<cudaEvent_t> ev;   // per-block events of the three-stream schedule
     PrecondBlk() = default;
     PrecondBlk(const PrecondBlk &) = delete;

@@ -189,6 +189,41 @@ __global__ void k_blk_split6(int64_t r0, int64_t BS, int64_t ncp, const float *_
     }
 }
 
+// few columns: the bulk update's B operand as ONE 3BS x 3ncp matrix (ld 3BS) against the
+// packed [L3 L2 L1], so a single GEMM reads L once:  column block 0 = [B1; B1; B1],
+// 1 = [0; B2; B2], 2 = [0; 0; B3]  ->  T = [L3B1 + L2B1 + L1B1, L2B2 + L1B2, L1B3]
+__global__ void k_blk_split_cat(int64_t r0, int64_t BS, int64_t ncp, const float *__restrict__ X, int64_t ld,
+                                bf16 *__restrict__ dst) {
+    const int64_t hb = BS / 2, total = hb * ncp, ldd = 3 * BS;
+    const bf16 z = __float2bfloat16_rn(0.f);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = 2 * (e % hb), c = e / hb;
+        const float2 v = *reinterpret_cast<const float2 *>(X + (r0 + r) + c * ld);
+        bf16 pa[3], pb[3];
+        split3(v.x, pa[0], pa[1], pa[2]);
+        split3(v.y, pb[0], pb[1], pb[2]);
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb)
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {   // slot sl pairs with L part 3 - sl
+                const bool on = sl >= cb;
+                *reinterpret_cast<__nv_bfloat162 *>(dst + (sl * BS + r) + (cb * ncp + c) * ldd) =
+                    on ? __halves2bfloat162(part_of(pa, cb), part_of(pb, cb)) : __halves2bfloat162(z, z);
+            }
+    }
+}
+
+// C (m x ncp, ldc) -= (T2 + T1) + T0, the bulk update's three partials smallest first
+__global__ void k_blk_sub3(int64_t m, int64_t ncp, const float *__restrict__ T, int64_t ldt, float *__restrict__ C,
+                           int64_t ldc) {
+    const int64_t total = m * ncp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e % m, c = e / m;
+        const float s = (T[r + (2 * ncp + c) * ldt] + T[r + (ncp + c) * ldt]) + T[r + c * ldt];
+        C[r + c * ldc] -= s;
+    }
+}
+
 // offsets of the packed L layouts (nb blocks of BS):
 //   Lc: block column j (j < nb - 1) = rows (j+1)BS .. Nb-1 (height h_j = (nb-1-j) BS) x the
 //       three parts side by side, L3 L2 L1 (3BS columns), ld h_j, at 3 BS^2 (j (nb-1) - j (j-1) / 2)
@@ -198,6 +233,12 @@ __global__ void k_blk_split6(int64_t r0, int64_t BS, int64_t ncp, const float *_
 // fewer than 256 right-hand-side columns)
 static bool splitk_small(int64_t ncp) {
     if (const char *e = getenv("HF_PRECOND_SPLITK")) return atoi(e) != 0;
+    return ncp < 256;
+}
+// the bulk update as one GEMM against the 3BS x 3ncp part matrix (HF_PRECOND_BCAT=0/1 forces;
+// default: fewer than 256 columns, where the three-GEMM form is bound by its repeated L reads)
+static bool bcat_bulk(int64_t ncp) {
+    if (const char *e = getenv("HF_PRECOND_BCAT")) return atoi(e) != 0;
     return ncp < 256;
 }
 __host__ __device__ __forceinline__ int64_t lc_off(int64_t j, int64_t nb, int64_t BS) {
@@ -445,7 +486,20 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         lt_bgemm(ctx, tA, BS, ncp, 6 * BS, alpha, A, tA ? 6 * BS : BS, S6 + j * stk, 6 * BS, beta, C, Nb, s);
     };
     // the bulk product from the three-part L: K' = 3BS, 2BS, BS over the stack's BULK blocks
+    const bool bcat = bcat_bulk(ncp);
+    const size_t stc = (size_t)9 * BS * ncp;
+    if (bcat) {
+        p.SC.alloc(nb * stc, st);
+        p.TB.alloc((size_t)Nb * 3 * ncp, st);
+    }
     auto gemm_bulk = [&](cudaStream_t s, bool tA, int64_t m, const bf16 *A, int64_t lda, int64_t j, float *C) {
+        if (bcat) {   // one GEMM reads [L3 L2 L1] once; the partials are subtracted smallest first
+            if (m <= 0) return;
+            lt_bgemm(ctx, tA, m, 3 * ncp, 3 * BS, 1.f, A, lda, bp(p.SC) + j * stc, 3 * BS, 0.f, p.TB.p, m, s);
+            k_blk_sub3<<<grid_for(ctx, m * ncp), 256, 0, s>>>(m, ncp, p.TB.p, m, C, Nb);
+            HF_CHECK_LAUNCH(ctx);
+            return;
+        }
         const bf16 *Bj = SB + j * stk;
         // smallest first: L1 B3, [L2 L1] [B2; B2], [L3 L2 L1] [B1; B1; B1] (parts stored reversed)
         const int64_t po = tA ? BS : BS * lda;   // one part further along K in A
@@ -482,7 +536,13 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         }
         gemm_small(st, false, bp(p.Ic) + j * per6, j, 1.f, 0.f, Y + j0);   // A: Y_j = Linv_j X_j
         if (j + 2 < nb) {   // B: Xb_{>j+1} -= L_{>j+1,j} Y_j
-            stack(st, Y, nullptr, j, SB, 1);
+            if (bcat) {
+                k_blk_split_cat<<<grid_for(ctx, BS * ncp / 2), 256, 0, st>>>(j * BS, BS, ncp, Y, Nb,
+                                                                              bp(p.SC) + j * stc);
+                HF_CHECK_LAUNCH(ctx);
+            } else {
+                stack(st, Y, nullptr, j, SB, 1);
+            }
             HF_CUDA(cudaEventRecord(evY[j], st));
             HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
             const int64_t h = (nb - 1 - j) * BS;
@@ -510,7 +570,13 @@ void precond_blk_apply(hf_ctx *ctx, PrecondBlk &p, int64_t ncol, const double *R
         }
         gemm_small(st, true, bp(p.It) + j * per6, j, 1.f, 0.f, Xo + j0);   // A: X_j = Linv_j^T Z_j
         if (j >= 2) {   // B: Zb_{<j-1} -= (L_{j,<j-1})^T X_j
-            stack(st, Xo, nullptr, j, SB, 1);
+            if (bcat) {
+                k_blk_split_cat<<<grid_for(ctx, BS * ncp / 2), 256, 0, st>>>(j * BS, BS, ncp, Xo, Nb,
+                                                                              bp(p.SC) + j * stc);
+                HF_CHECK_LAUNCH(ctx);
+            } else {
+                stack(st, Xo, nullptr, j, SB, 1);
+            }
             HF_CUDA(cudaEventRecord(evY[j], st));
             HF_CUDA(cudaStreamWaitEvent(sb, evY[j], 0));
             gemm_bulk(sb, true, j0 - BS, Lr + lr_off(j, BS), 3 * BS, j, Zb);
