@@ -37,12 +37,21 @@ def _exact(F, Rp):
 CASES = [("P512", 0, 8), ("P1024", 1, 130), ("N32", 0, 1), ("S24", 0, 64), ("C1", 0, 4), ("P2048", 0, 200)]
 
 
-@pytest.mark.parametrize("mode", ["blocked", "dataflow"])
+# blocked: below 256 columns the small products run as a batch of six part GEMMs and the bulk
+# update as one GEMM against the 3BS x 3ncp part matrix; _wide forces the forms used from 256
+# columns on (one K' = 6BS GEMM per small product, three bulk GEMMs); _bs256: 256-row blocks
+# (HF_PRECOND_BS), so these sizes have several blocks and run the coupling and bulk updates
+@pytest.mark.parametrize("mode", ["blocked", "blocked_bs256", "blocked_wide_bs256", "dataflow"])
 @pytest.mark.parametrize("name,seed,ncol", CASES)
 def test_precond_apply_vs_oracle(ctx, name, seed, ncol, mode, monkeypatch):
     from paper_2208_01907_b200 import hf
     if mode == "dataflow":
         monkeypatch.setenv("HF_PRECOND", "dataflow")
+    if "wide" in mode:
+        monkeypatch.setenv("HF_PRECOND_SPLITK", "0")
+        monkeypatch.setenv("HF_PRECOND_BCAT", "0")
+    if "bs256" in mode:
+        monkeypatch.setenv("HF_PRECOND_BS", "256")
     spec = hi.CONFIGS[name]
     Kb = hi.make_kbar(name, seed)
     Ko, _ = oracle.scale(Kb.numpy())
