@@ -1427,7 +1427,9 @@ void lowprec_factor(hf_ctx *ctx, int64_t L, const double *K, int64_t ld, const h
     // chain 53.3 vs 51.5 ms -- a 22-33 % hit rate does not pay for the extra poll and traffic)
     int chain_spec = 0;
     if (const char *e = getenv("HF_CHAIN_SPEC")) chain_spec = atoi(e);
-    // HF_CHAIN_DPOLL=1: two poll rounds in flight (measured 52.5 vs 52.1 ms chain at C2: off)
+    // HF_CHAIN_DPOLL=1: two poll rounds in flight (measured 52.5 vs 52.1 ms chain at C2: off;
+    // with the launch bound matched to the block: 49.2 / 49.2 / 49.8 / 49.2 vs 49.5 / 49.7 /
+    // 49.4 / 49.4 ms over four alternating pairs -- within the run-to-run spread, still off)
     int chain_dpoll = 0;
     if (const char *e = getenv("HF_CHAIN_DPOLL")) chain_dpoll = atoi(e);
     if (const char *e = getenv("HF_SLOT_STRIDE")) sstride = std::max(1, std::min(64, atoi(e)));
