@@ -772,8 +772,15 @@ __device__ __forceinline__ void cp_async16_g(void *sdst, const void *gsrc) {
 // k_trailing with the panel operands streamed from the compacted panel by 16-byte
 // cp.async, three stages in flight (no register staging, no per-element address
 // arithmetic); the same single fmaf chain per entry in pivot order.
-constexpr int TNS = 3;   // cp.async stages
-constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float);
+constexpr int TNS = 3;   // cp.async stages (k_trailing_p)
+#ifndef HF_TNSC
+#define HF_TNSC 2
+#endif
+// k_trailing_c's operand stages (TNSC - 1 chunks in flight).  Two stages (32 KB per CTA) beat
+// three (48 KB) and four: C2 trailing 29.2 vs 29.8 / 29.8 ms per step (two alternating runs
+// each) -- the smaller shared carve-out leaves more L1 to the once-per-tile seed gathers
+constexpr int TNSC = HF_TNSC;
+constexpr size_t TRAIL_C_SMEM = (size_t)2 * TNSC * TK * TB * sizeof(float);
 // NS (NEXT-3, nonsymmetric LDU): the FULL square trailing matrix (T x T tiles),
 // A operand -l_I, B operand r_J, v_IJ <- fmaf(-l_I, r_J, v_IJ) [R19].
 // TMA (BULK): the panel operands staged by the bulk-copy engine (cp.async.bulk, one 512-byte
@@ -785,15 +792,15 @@ template <bool NS, int BULK = 0>
 __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB) {
     if (a.status[2]) return;
-    extern __shared__ __align__(16) float dsm_t[];   // [TNS][TK][TB] x 2 (48 KB: dynamic)
+    extern __shared__ __align__(16) float dsm_t[];   // [TNSC][TK][TB] x 2 (48 KB: dynamic)
     // the tensor copies need 128 B aligned destinations; the dynamic window starts 32 B past
     // one (measured), so BULK = 2 launches with 128 B more and rounds up
     float *dsm = BULK == 2 ? reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(dsm_t) + 127) & ~uintptr_t(127))
                            : dsm_t;
     float (*As)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm);
-    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm + TNS * TK * TB);
+    float (*Bs)[TK][TB] = reinterpret_cast<float (*)[TK][TB]>(dsm + TNSC * TK * TB);
     __shared__ int32_t rmap[TB], cmap[TB];
-    __shared__ __align__(8) unsigned long long mbar[TNS];   // BULK: one per operand stage
+    __shared__ __align__(8) unsigned long long mbar[TNSC];   // BULK: one per operand stage
     // persistent: CTA b takes tiles b, b + grid, ... (the order of the one-tile-per-CTA
     // launch); the next tile's compaction-map entry is loaded into a register while the
     // current tile computes, so a tile's seed gather waits for one memory latency, not two
@@ -830,7 +837,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid
     const int mpr = (int)min((int64_t)TB, a.mp - row0), mpc = (int)min((int64_t)TB, a.mp - col0);
     const int nchunk = (a.nbp + TK - 1) / TK;
 
-    // chunk c -> stage c % TNS: TK pivots x 128 positions of each operand, 2 x 16 B per
+    // chunk c -> stage c % TNSC: TK pivots x 128 positions of each operand, 2 x 16 B per
     // thread each.  The four source pointers advance by one chunk per issue (64-bit adds
     // on the ALU pipe) and the stage rotates: no per-chunk multiplies or modulo on the FMA
     // pipe, which the update saturates (IMAD runs on it, rt 2 like FFMA2).
@@ -891,18 +898,18 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        soff = (soff == (TNS - 1) * STGB) ? 0u : soff + STGB;
-        sidx = (sidx == TNS - 1) ? 0 : sidx + 1;
+        soff = (soff == (TNSC - 1) * STGB) ? 0u : soff + STGB;
+        sidx = (sidx == TNSC - 1) ? 0 : sidx + 1;
     };
     if (BULK && tid == 0) {   // the stage mbarriers: one arrival (the expect_tx) per use
-        for (int q = 0; q < TNS; ++q)
+        for (int q = 0; q < TNSC; ++q)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u * q) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (BULK) __syncthreads();
     unsigned phase_bits = 0;   // BULK: parity of each stage's next completion
-    issue(0);
-    issue(1);
+#pragma unroll
+    for (int q = 0; q < TNSC - 1; ++q) issue(q);
     __syncthreads();   // this tile's maps (stored before the loop or at the end of the previous tile)
 
 #define RR(q) (((q) < 4) ? tx * 4 + (q) : 64 + tx * 4 + ((q)-4))
@@ -952,7 +959,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid
     const int64_t tn = t + gridDim.x;
     const int32_t mnext = tn < a.ntiles ? map_entry(tn) : -1;   // consumed after the main loop
     int st = 0;   // stage of chunk c
-    for (int c = 0; c < nchunk; ++c, st = (st == TNS - 1) ? 0 : st + 1) {
+    for (int c = 0; c < nchunk; ++c, st = (st == TNSC - 1) ? 0 : st + 1) {
         if (BULK) {
             const unsigned mb = mb0 + 8u * (unsigned)st;
             const unsigned ph = (phase_bits >> st) & 1u;
@@ -963,10 +970,10 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid
             phase_bits ^= 1u << st;
             __syncthreads();                // every thread is done with stage (c+2)%3 (read in c-1)
         } else {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-            __syncthreads();                // chunk c landed for all threads; stage (c+2)%3 is free
+            asm volatile("cp.async.wait_group %0;" ::"n"(TNSC - 2) : "memory");
+            __syncthreads();                // chunk c landed for all threads; stage (c-1)%TNSC is free
         }
-        issue(c + 2);
+        issue(c + TNSC - 1);
         const int kmax = min(TK, a.nbp - c * TK);
         if (kmax == TK) {
 #pragma unroll
@@ -1040,7 +1047,7 @@ __global__ void __launch_bounds__(256, 2) k_trailing_c(TrailArgs a, const __grid
 // compaction map -- most of a tile's non-FMA time in k_trailing_c -- overlaps the FMA
 // loop.  Each thread reads back only what it gathered itself: no barrier on the seed
 // buffer.  Same single fmaf chain per entry in pivot order (bit-identical).
-constexpr size_t TRAIL_P_SMEM = TRAIL_C_SMEM + (size_t)TB * TB * sizeof(float);   // + seeds
+constexpr size_t TRAIL_P_SMEM = (size_t)2 * TNS * TK * TB * sizeof(float) + (size_t)TB * TB * sizeof(float);   // + seeds
 __device__ __forceinline__ void cp_async4_z(void *sdst, const void *gsrc, bool ok) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gsrc), "r"(ok ? 4 : 0) : "memory");
