@@ -843,6 +843,8 @@ __global__ void __launch_bounds__(512) k_hard_factor_cl(int n, const double *__r
     const int r = (int)cl.block_rank(), tid = threadIdx.x, nt = blockDim.x;
     const int ncl = (n - r + HC - 1) / HC;
     const int ncmax = (n + HC - 1) / HC;
+    // (c, i) of this thread's flat entries e = tid, tid + nt, ... advanced without a division
+    const int c0 = tid / n, i0 = tid % n, dc = nt / n, di = nt % n;
     double *A = smh;                                  // [ncmax][n], local column c = global r + 16 c
     double *PC = A + (size_t)ncmax * n;               // [2][n] pivot column(s) of this step
     int32_t *act = reinterpret_cast<int32_t *>(PC + 2 * (size_t)n);   // [n]
@@ -913,8 +915,7 @@ __global__ void __launch_bounds__(512) k_hard_factor_cl(int n, const double *__r
         const double *ap = PC, *aq = PC + n;
         if (one) {
             const double d = ap[p];
-            for (int e = tid; e < ncl * n; e += nt) {
-                const int c = e / n, i = e % n;
+            for (int e = tid, c = c0, i = i0; e < ncl * n; e += nt, c += dc, i += di, (i >= n ? (i -= n, ++c) : 0)) {
                 const int j = r + HC * c;
                 if (!act[j] || j == p || !act[i] || i == p) continue;
                 const double v = A[e] - (ap[i] * ap[j]) / d;
@@ -940,8 +941,7 @@ __global__ void __launch_bounds__(512) k_hard_factor_cl(int n, const double *__r
             const double a_ = ap[p], b_ = ap[q], c_ = aq[q];
             const double det = a_ * c_ - b_ * b_;
             const double E0 = c_ / det, E1 = -b_ / det, E2 = -b_ / det, E3 = a_ / det;
-            for (int e = tid; e < ncl * n; e += nt) {
-                const int c = e / n, i = e % n;
+            for (int e = tid, c = c0, i = i0; e < ncl * n; e += nt, c += dc, i += di, (i >= n ? (i -= n, ++c) : 0)) {
                 const int j = r + HC * c;
                 if (!act[j] || j == p || j == q || !act[i] || i == p || i == q) continue;
                 const double cc0 = ap[j], cc1 = aq[j];
